@@ -246,7 +246,7 @@ def train_golden(gg, topo, cfg):
     rec = {"placements": [], "logp": [], "measure": [], "grads": [], "baseline_before": []}
     orig_fs = ref_policy.forward_sample
     orig_ru = ref_trainer.reinforce_update
-    orig_me = ref_trainer.measure
+    orig_me = ref.measure
 
     def fs(params, feats, rng):
         s = orig_fs(params, feats, rng)
@@ -260,17 +260,15 @@ def train_golden(gg, topo, cfg):
         rec["grads"].append(np.full(params.flat_size, np.nan) if g is None else g)
         return g
 
-    def me(gg_, topo_, placement, noise=None, steps=10):
-        m = orig_me(gg_, topo_, placement, noise=noise, steps=steps)
-        rec["measure"].append(m)
-        return m
-
-    ref_policy.forward_sample, ref_trainer.reinforce_update, ref_trainer.measure = fs, ru, me
+    ref_policy.forward_sample, ref_trainer.reinforce_update = fs, ru
     try:
         res = ref.train(gg, topo, cfg)
     finally:
-        ref_policy.forward_sample, ref_trainer.reinforce_update, ref_trainer.measure = orig_fs, orig_ru, orig_me
+        ref_policy.forward_sample, ref_trainer.reinforce_update = orig_fs, orig_ru
     U, K = cfg.total_updates, cfg.k
+    # measure() runs on worker threads (completion order), so re-derive per k
+    # (the simulator is pure; noise is off in these runs).
+    rec["measure"] = [orig_me(gg, topo, p) for p in rec["placements"]]
     csv = ref.log_to_csv(res.log, include_wall=False)
     out = dict(
         placements=np.array(rec["placements"], np.uint8).reshape(U, K, -1),
