@@ -1,1 +1,16 @@
-"""B200-native device-placement REINFORCE hot path (arXiv 1706.04972)."""
+"""B200-native REINFORCE device-placement hot path (arXiv 1706.04972).
+
+Drop-in for the reference package ``devplace`` on its hot path: the graph
+input model, the placement scorer (simulator), the seq2seq policy and the
+REINFORCE trainer keep the reference names and signatures; the work runs in
+hand-written sm_100a CUDA kernels behind the C-ABI in include/devplace_b200.h.
+"""
+
+from . import graph, simulator  # noqa: F401
+from .graph import (ComputationGraph, CycleError, Edge, GraphError, Group, GroupedGraph,  # noqa: F401
+                    GroupEdge, Operation, coalesce_sole_consumers, singleton_groups, topo_order)
+from .simulator import (INFEASIBLE, Device, DeviceTopology, NoiseSpec, SimReport,  # noqa: F401
+                        TopologyError, check_memory, default_topology, measure, simulate,
+                        simulate_batch)
+
+__version__ = "0.1.0"

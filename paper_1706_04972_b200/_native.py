@@ -1,0 +1,93 @@
+"""ctypes binding of the C-ABI in include/devplace_b200.h.
+
+The product path has no fallback: if the sm_100a library is missing or no CUDA
+device is visible, every entry point raises ``NativeUnavailable``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from .build import LIB
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+U64 = ctypes.c_uint64
+F64 = ctypes.c_double
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "dp_last_error": (ctypes.c_char_p, []),
+    "dp_graph_create": (I32, [I32, I32, P, P, P, P, P, P, P, P, P, P, P]),
+    "dp_graph_destroy": (None, [P]),
+    "dp_simulate_batch": (I32, [P, I32, P, I32, P, P, P, P, P, P, P, P]),
+}
+
+
+class NativeUnavailable(RuntimeError):
+    pass
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("devplace_b200 needs a CUDA device (sm_100a); none is visible")
+        if not os.path.exists(LIB):
+            raise NativeUnavailable(f"CUDA library not built: {LIB} (run __graft_entry__.build())")
+        L = ctypes.CDLL(LIB)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+        return L
+
+
+def load_only():
+    """Load the library and bind every declared symbol without touching CUDA
+    (used by CPU tests to check the exported ABI)."""
+    L = ctypes.CDLL(LIB)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+def check(rc: int, what: str):
+    if rc == 0:
+        return
+    msg = lib().dp_last_error().decode(errors="replace")
+    if rc == 1:
+        raise ValueError(f"{what}: {msg}")
+    raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None for None)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
