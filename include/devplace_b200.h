@@ -80,6 +80,101 @@ int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *placement, in
                       double *makespan, double *busy, double *transfer, int64_t *peak,
                       uint8_t *feasible, int32_t *order, uint8_t *err, void *stream);
 
+/* ----------------------------------------------------------------- policy */
+
+/* Create the device policy engine for one grouped graph's features and the
+ * policy hyper-parameters (pkg/policy.py:45-114, 120-146).  Uploads the
+ * structural features once (GroupFeatures.from_grouped, pkg/policy.py:97-114):
+ *   h_type_off[T+1], h_type_idx[...]  type-vocab indices per decode step
+ *                                      (sorted type names, with multiplicity)
+ *   h_shape[T*shape_slots], h_adj[T*adj_slots]
+ * and allocates activations for up to k_max samples.  hidden must be 64,
+ * 1 <= n_dev <= 32, 1 <= dev_dim <= 32. */
+int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_t dev_dim, int32_t type_dim,
+                     int32_t shape_slots, int32_t adj_slots, int32_t vocab_rows, const int32_t *h_type_off,
+                     const int32_t *h_type_idx, const double *h_shape, const double *h_adj, int32_t k_max,
+                     dp_policy **out);
+void dp_policy_destroy(dp_policy *p);
+/* Length of the flat parameter vector (PolicyParams.flat_size, pkg/policy.py:164-166). */
+int64_t dp_policy_num_params(const dp_policy *p);
+
+/* Encoder for a parameter snapshot `params` (flat f64 [P], canonical _FIELDS
+ * order, pkg/policy.py:41-42): input assembly, LSTM encoder over the T
+ * groups in topo order and the decoder input table (pkg/policy.py:256-287).
+ * Runs once per snapshot; all decode calls reuse it. */
+int dp_policy_encode(dp_policy *p, const double *params, void *stream);
+
+/* Copy the assembled encoder inputs of the last encode (embed_groups(),
+ * pkg/policy.py:266-268) into out[T*input_dim] (device). */
+int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream);
+
+/* Decode K samples from the encoded snapshot — forward_sample() /
+ * log_prob_of() / step_distributions() (pkg/policy.py:288-340).
+ *   h_pcg[4]      numpy PCG64 state (state_hi, state_lo, inc_hi, inc_lo) of the
+ *                 caller's Generator; sample k, step t consumes draw
+ *                 draw_base + (draw_counter ? *draw_counter * draws_per_count : 0)
+ *                 + (k_offset + k)*T + t, i.e. exactly the draws K sequential
+ *                 forward_sample calls would consume.
+ *   forced[K*T]   optional (device): teacher-forced choices by rank instead of
+ *                 sampling (then h_pcg may be NULL)
+ *   choice_out[K*T] optional (device): sampled device per rank
+ *   logp[K]       (device) log-probability of each placement
+ *   probs_out[K*T*n_dev] optional (device): per-step distributions
+ * The activations of the last decode stay in the engine (the forward cache
+ * used by dp_policy_backward). */
+int dp_policy_decode(dp_policy *p, const double *params, int32_t K, int64_t k_offset, const uint64_t *h_pcg,
+                     uint64_t draw_base, const int64_t *draw_counter, int64_t draws_per_count,
+                     const uint8_t *forced, uint8_t *choice_out, double *logp, double *probs_out, void *stream);
+
+/* grad[P] = sum_k adv[k] * d log p(placement_k) / d params over the samples of
+ * the last decode call (K must match) — grad_log_prob() weighted and summed as
+ * in reinforce_update() (pkg/policy.py:351-409, pkg/trainer.py:147-151). */
+int dp_policy_backward(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
+                       void *stream);
+
+/* ---------------------------------------------------------------- trainer */
+
+/* Device-resident controller state (one per controller); zero-initialise,
+ * then set baseline = failing signal and best_r = +inf (pkg/trainer.py:263-267). */
+typedef struct {
+    double baseline;      /* BaselineState.value */
+    double baseline_prev; /* B used for this update's advantages */
+    double best_r;        /* best feasible reward so far (+inf if none) */
+    int64_t update;       /* controller-local update index */
+    int64_t adam_t;       /* ParameterStore._t */
+    int64_t version;      /* ParameterStore.version */
+    int64_t rejected;     /* ParameterStore.rejected */
+    int64_t n_used;
+    int64_t n_feasible;
+    int64_t best_update;
+    int64_t best_k;
+    int64_t error;        /* 1: a feasible measurement was not positive/finite */
+} dp_train_state;
+
+/* Rewards, best-so-far, success-only filter, baseline and advantages for one
+ * update (pkg/trainer.py:66-72, 83-84, 138-154, 281-304), on device:
+ *   makespan[K], feasible[K], choice[K*T]: all K samples of the update
+ *   adv[K_local] (out): (R_k - B) for used samples k_offset.. else 0
+ *   best_choice[T] (out): updated when the best reward improves
+ *   log_rows[log_cap*8] (out): row `update` = (update, controller, version,
+ *   mean_R, baseline, best_R, n_feasible, n_used); version is filled by
+ *   dp_adam_apply. */
+int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespan, const uint8_t *feasible,
+                          const uint8_t *choice, double failing, double decay, int64_t success_only_after,
+                          int64_t k_offset, int32_t K_local, dp_train_state *state, double *adv,
+                          uint8_t *best_choice, double *log_rows, int64_t log_cap, int32_t controller_id,
+                          void *stream);
+
+/* ParameterStore.apply (pkg/trainer.py:113-131): grad is the advantage-weighted
+ * SUM from dp_policy_backward; it is divided by n_used here.  Skips the step
+ * when n_used == 0 (reinforce_update returned None), rejects non-finite
+ * gradients (rejected++), else Adam with bias_corr[2*(t-1)+{0,1}] =
+ * 1-b1^t, 1-b2^t (host-computed Python floats) and version++.  Then advances
+ * state->update.  flag: device int32 scratch, zero-initialised. */
+int dp_adam_apply(int64_t P, double *params, double *m, double *v, const double *grad, const double *bias_corr,
+                  int64_t t_cap, double lr, double b1, double b2, double eps, dp_train_state *state,
+                  int32_t *flag, double *log_rows, int64_t log_cap, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

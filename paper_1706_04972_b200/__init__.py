@@ -13,4 +13,12 @@ from .simulator import (INFEASIBLE, Device, DeviceTopology, NoiseSpec, SimReport
                         TopologyError, check_memory, default_topology, measure, simulate,
                         simulate_batch)
 
+from . import policy, trainer  # noqa: F401,E402
+from .policy import (EmbeddingSpec, GroupFeatures, PolicyParams, SampledPlacement,  # noqa: F401,E402
+                     embed_groups, forward_sample, grad_log_prob, load_checkpoint, log_prob_of,
+                     sample_batch, save_checkpoint, step_distributions)
+from .trainer import (BaselineState, LogRow, ParameterStore, RewardSpec, TrainerConfig,  # noqa: F401,E402
+                      TrainResult, apply_adam, log_to_csv, reinforce_update, reward_of, run_controller,
+                      suggest_failing_signal, train)
+
 __version__ = "0.1.0"

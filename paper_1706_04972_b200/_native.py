@@ -26,7 +26,21 @@ SIGNATURES = {
     "dp_graph_create": (I32, [I32, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "dp_graph_destroy": (None, [P]),
     "dp_simulate_batch": (I32, [P, I32, P, I32, P, P, P, P, P, P, P, P]),
+    "dp_policy_create": (I32, [I32, I32, I32, I32, I32, I32, I32, I32, P, P, P, P, I32, P]),
+    "dp_policy_destroy": (None, [P]),
+    "dp_policy_num_params": (I64, [P]),
+    "dp_policy_encode": (I32, [P, P, P]),
+    "dp_policy_read_inputs": (I32, [P, P, P]),
+    "dp_policy_decode": (I32, [P, P, I32, I64, P, U64, P, I64, P, P, P, P, P]),
+    "dp_policy_backward": (I32, [P, P, I32, P, P, P]),
+    "dp_reinforce_epilogue": (I32, [I32, I32, P, P, P, F64, F64, I64, I64, I32, P, P, P, P, I64, I32, P]),
+    "dp_adam_apply": (I32, [I64, P, P, P, P, P, I64, F64, F64, F64, F64, P, P, P, I64, P]),
 }
+
+# struct dp_train_state (include/devplace_b200.h): 3 doubles then 9 int64
+TRAIN_STATE_FIELDS = ("baseline", "baseline_prev", "best_r", "update", "adam_t", "version", "rejected",
+                      "n_used", "n_feasible", "best_update", "best_k", "error")
+TRAIN_STATE_WORDS = len(TRAIN_STATE_FIELDS)
 
 
 class NativeUnavailable(RuntimeError):

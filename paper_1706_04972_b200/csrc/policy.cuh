@@ -1,0 +1,55 @@
+// Device-resident policy state shared by the forward/backward kernels.
+#pragma once
+#include "common.cuh"
+
+namespace dp {
+
+constexpr int kH = 64;        // LSTM width (reference default hidden=64, pkg/trainer.py:173)
+constexpr int kG = 4 * kH;    // gates per cell (i, f, o, g — pkg/policy.py:224-233)
+constexpr int kThreads = 256; // one thread per gate column in the recurrent kernels
+constexpr int kMaxDD = 32;    // device-embedding width limit
+constexpr int kMaxD = 32;     // device count limit (u8 choices)
+constexpr int kEncPad = kH + 1;  // padded row stride of enc_states in shared memory
+
+// Parameter offsets inside the flat vector, canonical _FIELDS order
+// (pkg/policy.py:41-42, 136-146, 168-169).
+struct ParamLayout {
+    int64_t type_table, dev_table, w_enc, b_enc, w_dec, b_dec, w_att, w_out, b_out, total;
+};
+
+struct PolicyDims {
+    int T, D, dd, td, ss, as, F, V1;
+    ParamLayout off;
+};
+
+}  // namespace dp
+
+struct dp_policy {
+    dp::PolicyDims dims;
+    int k_max;
+    // features (uploaded once)
+    int32_t *type_off, *type_idx;
+    int32_t *occ_off, *occ_t;  // per type row: decode steps using it (with multiplicity), t-ascending
+    double *zeros;             // [64] zero cell state (encoder step 0)
+    double *shape, *adj;
+    // encoder activations (one sequence, shared by all samples)
+    double *X;      // [T*F]   assembled inputs (pkg/policy.py:256-263)
+    double *XP;     // [T*G]   X @ w_enc[:F] + b_enc
+    double *enc_h;  // [T*H]   enc_states
+    double *enc_c;  // [T*H]
+    double *enc_g;  // [T*G]   gate activations i,f,o,g
+    double *edev;   // [(D+1)*G] dev_table @ w_dec[:dd] + b_dec (decoder input projection)
+    // decoder activations, [k][t][...] (the opaque forward cache)
+    double *act_h, *act_c, *act_g, *act_ctx, *act_u, *act_p, *act_stat;
+    uint8_t *act_choice;  // [k*T] by rank
+    double *act_logp;     // [k]
+    int last_K;
+    // backward scratch
+    double *row_q, *row_dctx, *row_w, *row_dq, *row_dhx;  // per (k,t)
+    double *dh0, *dc0;                                   // [k*H]
+    double *d_enc;                                       // [T*H]
+    double *da_enc;                                      // [T*G]
+    double *partial;                                     // per-CTA partial sums
+    size_t partial_elems;
+    double *gacc;                                        // [P] accumulator
+};

@@ -1,0 +1,755 @@
+// Policy forward on sm_100a: encoder (once per parameter snapshot) and the
+// attentional decoder that samples K placements at once.
+//
+// Reference: /root/reference/pkg/src/devplace/policy.py
+//   inputs      _assemble_inputs        policy.py:256-263
+//   LSTM cell   _lstm_step / _sigmoid   policy.py:220-233  (gate order i, f, o, g)
+//   encoder     _forward                policy.py:276-287
+//   decoder     _forward                policy.py:288-311
+//   sampling    forward_sample.choose   policy.py:317-326
+//
+// Everything is IEEE fp64 like the reference (numpy float64): sampled indices
+// must be bit-exact, and fp32/TF32 flip 0.006-1.2 draws per update
+// (SURVEY.md §0.5).  Design:
+//   * the encoder is identical for all K samples, so it runs ONCE per snapshot
+//     (the reference reruns it per sample): x@W_x+b for all t is one parallel
+//     GEMM, only h@W_h (64x256) stays sequential — one CTA, one thread per gate
+//     column with its 64 W_h weights in registers, 4 gates of a unit in 4
+//     adjacent lanes (shuffle exchange, one barrier per step);
+//   * the decoder input projection collapses to a (D+1)x256 table
+//     edev = dev_table @ W_dec[:dd] + b_dec, gathered by the previous choice;
+//   * attention uses s = enc @ (W_att^T h) (== (enc @ W_att^T) @ h, the
+//     reference's proj @ h) so only enc_states (T x 64) is needed; it is staged
+//     in shared memory with a padded stride (conflict-free for both the
+//     row-per-thread score pass and the column-per-lane context pass);
+//   * one CTA owns M samples for all T steps (samples are independent, no grid
+//     sync); the softmax / PCG64 draw / log-prob tail runs warp-per-sample.
+
+#include <math.h>
+
+#include <vector>
+
+#include "pcg64.cuh"
+#include "policy.cuh"
+
+namespace dp {
+
+__device__ __forceinline__ double sigmoid_ref(double x) { return 1.0 / (1.0 + exp(-x)); }
+
+// numpy pairwise_sum order for n <= 128 (np.add.reduce on a contiguous array):
+// n < 8 sequential; otherwise 8 interleaved accumulators, fixed tree, tail.
+__device__ __forceinline__ double np_sum_small(const double *a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; i++) r += a[i];
+        return r;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] += a[i + j];
+    }
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; i++) res += a[i];
+    return res;
+}
+
+// ---------------------------------------------------------------- prologue
+// X[t] = [mean(type_table[idx_t]) | shape_t | adj_t]   (policy.py:256-263)
+__global__ void enc_inputs_kernel(PolicyDims dm, const double *__restrict__ params,
+                                  const int32_t *__restrict__ type_off, const int32_t *__restrict__ type_idx,
+                                  const double *__restrict__ shape, const double *__restrict__ adj,
+                                  double *__restrict__ X) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= dm.T * dm.F) return;
+    const int t = idx / dm.F, f = idx % dm.F;
+    double v;
+    if (f < dm.td) {
+        // numpy mean(axis=0): first row, then sequential adds, then / count
+        const double *tab = params + dm.off.type_table;
+        const int a = type_off[t], b = type_off[t + 1];
+        double s = tab[(size_t)type_idx[a] * dm.td + f];
+        for (int i = a + 1; i < b; i++) s = s + tab[(size_t)type_idx[i] * dm.td + f];
+        v = s / (double)(b - a);
+    } else if (f < dm.td + dm.ss) {
+        v = shape[(size_t)t * dm.ss + (f - dm.td)];
+    } else {
+        v = adj[(size_t)t * dm.as + (f - dm.td - dm.ss)];
+    }
+    X[idx] = v;
+}
+
+// C[r, j] = sum_i A[r, i] * B[i, j] + bias[j]   (small dense projections)
+__global__ void gemm_bias_kernel(int R, int N, int Kd, const double *__restrict__ A, int lda,
+                                 const double *__restrict__ B, int ldb, const double *__restrict__ bias,
+                                 double *__restrict__ C, int ldc) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.y;
+    if (j >= N || r >= R) return;
+    const double *a = A + (size_t)r * lda;
+    double acc = 0.0;
+    for (int i = 0; i < Kd; i++) acc = fma(a[i], B[(size_t)i * ldb + j], acc);
+    C[(size_t)r * ldc + j] = acc + bias[j];
+}
+
+// 64-term dot of a shared-memory vector (broadcast) with a register column.
+__device__ __forceinline__ double dot64_sh_reg(const double *__restrict__ hs, const double (&w)[kH]) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int k = 0; k < kH; k += 4) {
+        const double2 h01 = *reinterpret_cast<const double2 *>(hs + k);
+        const double2 h23 = *reinterpret_cast<const double2 *>(hs + k + 2);
+        a0 = fma(h01.x, w[k], a0);
+        a1 = fma(h01.y, w[k + 1], a1);
+        a2 = fma(h23.x, w[k + 2], a2);
+        a3 = fma(h23.y, w[k + 3], a3);
+    }
+    return (a0 + a1) + (a2 + a3);
+}
+
+// ---------------------------------------------------------------- encoder
+// One CTA, 256 threads: thread (u, gate) = (tid>>2, tid&3) owns gate column
+// col = gate*64 + u of W_enc's h-rows in registers.  Per step: a = XP[t] + h.W_h,
+// activation, 4-lane shuffle to the unit's owner, c/h update, one barrier.
+__global__ void __launch_bounds__(kThreads, 1)
+    enc_rec_kernel(PolicyDims dm, const double *__restrict__ params, const double *__restrict__ XP,
+                   double *__restrict__ enc_h, double *__restrict__ enc_c, double *__restrict__ enc_g) {
+    __shared__ __align__(16) double hbuf[2][kH];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int u = tid >> 2, gate = tid & 3, col = gate * kH + u;
+    const double *Wh = params + dm.off.w_enc + (size_t)dm.F * kG;
+    double w[kH];
+#pragma unroll
+    for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
+    if (tid < kH) hbuf[0][tid] = 0.0;
+    double c = 0.0;
+    double xp = dm.T > 0 ? XP[col] : 0.0;
+    __syncthreads();
+    const int base = lane & ~3;
+    for (int t = 0; t < dm.T; t++) {
+        const double a = xp + dot64_sh_reg(hbuf[t & 1], w);
+        if (t + 1 < dm.T) xp = XP[(size_t)(t + 1) * kG + col];
+        const double act = gate == 3 ? tanh(a) : sigmoid_ref(a);
+        enc_g[(size_t)t * kG + col] = act;
+        const double iv = __shfl_sync(0xffffffffu, act, base + 0);
+        const double fv = __shfl_sync(0xffffffffu, act, base + 1);
+        const double ov = __shfl_sync(0xffffffffu, act, base + 2);
+        const double gv = __shfl_sync(0xffffffffu, act, base + 3);
+        if (gate == 0) {
+            c = fv * c + iv * gv;
+            const double h = ov * tanh(c);
+            hbuf[(t + 1) & 1][u] = h;
+            enc_h[(size_t)t * kH + u] = h;
+            enc_c[(size_t)t * kH + u] = c;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- decoder
+struct DecArgs {
+    PolicyDims dm;
+    const double *params;
+    int K;
+    long long k_offset;
+    uint64_t st_hi, st_lo, inc_hi, inc_lo;
+    unsigned long long draw_base;
+    const long long *draw_counter;
+    long long draws_per_count;
+    const uint8_t *forced;
+    const double *enc_h, *enc_c, *edev;
+    double *act_h, *act_c, *act_g, *act_ctx, *act_u, *act_p, *act_stat;
+    uint8_t *choice, *choice_out;
+    double *logp, *probs_out;
+    int M, enc_in_smem, Tpad;
+    // shared-memory offsets (doubles)
+    int o_enc, o_watt, o_wout, o_devt, o_bout, o_edev, o_h, o_q, o_ctx, o_c, o_u, o_p, o_alpha, o_red,
+        o_red2, o_pcg, o_misc;
+};
+
+template <int MT>
+__global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const PolicyDims &dm = a.dm;
+    const int T = dm.T, D = dm.D, dd = dm.dd, M = a.M;
+    const int k0 = blockIdx.x * M;
+    const int Mb = min(M, a.K - k0);
+    const double *P = a.params;
+
+    double *encS = a.enc_in_smem ? sm + a.o_enc : nullptr;
+    const int enc_ld = a.enc_in_smem ? kEncPad : kH;
+    const double *enc = a.enc_in_smem ? encS : a.enc_h;
+    double *watt = sm + a.o_watt;
+    double *wout = sm + a.o_wout;
+    double *devt = sm + a.o_devt;
+    double *bout = sm + a.o_bout;
+    double *edev = sm + a.o_edev;
+    double *hS = sm + a.o_h;      // [2][M][64]
+    double *qS = sm + a.o_q;      // [M][64]
+    double *ctxS = sm + a.o_ctx;  // [M][64]
+    double *cS = sm + a.o_c;      // [M][64]
+    double *uS = sm + a.o_u;      // [M][32]
+    double *pS = sm + a.o_p;      // [M][32]
+    double *alS = sm + a.o_alpha; // [M][Tpad]
+    double *red = sm + a.o_red;   // [8][M] x 2
+    double *red2 = sm + a.o_red2; // [4][M][64]
+    unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
+    int *prev = reinterpret_cast<int *>(sm + a.o_misc);                               // [M]
+    double *lp = sm + a.o_misc + 16;                                                   // [M]
+
+    // ---- stage weights ----
+    if (encS)
+        for (int i = tid; i < T * kH; i += kThreads) encS[(i >> 6) * kEncPad + (i & 63)] = a.enc_h[i];
+    for (int i = tid; i < kH * kH; i += kThreads) watt[i] = P[dm.off.w_att + i];
+    for (int i = tid; i < 2 * kH * dd; i += kThreads) wout[i] = P[dm.off.w_out + i];
+    for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
+    for (int i = tid; i < D; i += kThreads) bout[i] = P[dm.off.b_out + i];
+    for (int i = tid; i < (D + 1) * kG; i += kThreads) edev[i] = a.edev[i];
+    for (int i = tid; i < Mb * kH; i += kThreads) {
+        hS[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
+        cS[i] = a.enc_c[(size_t)(T - 1) * kH + (i & 63)];
+    }
+    if (tid < Mb) {
+        prev[tid] = D;
+        lp[tid] = 0.0;
+        if (!a.forced) {
+            const long long kg = a.k_offset + k0 + tid;
+            unsigned long long n0 = a.draw_base + (unsigned long long)kg * (unsigned long long)T;
+            if (a.draw_counter) n0 += (unsigned long long)(*a.draw_counter) * (unsigned long long)a.draws_per_count;
+            const u128 s = pcg_jump(u128{a.st_hi, a.st_lo}, u128{a.inc_hi, a.inc_lo}, n0);
+            pcg[2 * tid] = s.hi;
+            pcg[2 * tid + 1] = s.lo;
+        }
+    }
+    const int u = tid >> 2, gate = tid & 3, col = gate * kH + u;
+    double w[kH];
+    {
+        const double *Wh = P + dm.off.w_dec + (size_t)dd * kG;
+#pragma unroll
+        for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
+    }
+    __syncthreads();
+
+    const int base = lane & ~3;
+    const int Tq = (T + 3) / 4;
+    for (int t = 0; t < T; t++) {
+        const int cur = t & 1;
+        // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
+        for (int m = 0; m < Mb; m++) {
+            const double *hc = hS + (cur * M + m) * kH;
+            const double av = edev[prev[m] * kG + col] + dot64_sh_reg(hc, w);
+            const double act = gate == 3 ? tanh(av) : sigmoid_ref(av);
+            const size_t row = (size_t)(k0 + m) * T + t;
+            a.act_g[row * kG + col] = act;
+            const double iv = __shfl_sync(0xffffffffu, act, base + 0);
+            const double fv = __shfl_sync(0xffffffffu, act, base + 1);
+            const double ov = __shfl_sync(0xffffffffu, act, base + 2);
+            const double gv = __shfl_sync(0xffffffffu, act, base + 3);
+            if (gate == 0) {
+                const double cn = fv * cS[m * kH + u] + iv * gv;
+                const double hn = ov * tanh(cn);
+                cS[m * kH + u] = cn;
+                hS[((cur ^ 1) * M + m) * kH + u] = hn;
+                a.act_h[row * kH + u] = hn;
+                a.act_c[row * kH + u] = cn;
+            }
+        }
+        __syncthreads();
+        const double *hN = hS + (cur ^ 1) * M * kH;
+        // ---- B: q = W_att^T h ----
+        for (int idx = tid; idx < Mb * kH; idx += kThreads) {
+            const int m = idx >> 6, j = idx & 63;
+            const double *hv = hN + m * kH;
+            double q0 = 0.0, q1 = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < kH; l += 2) {
+                q0 = fma(watt[l * kH + j], hv[l], q0);
+                q1 = fma(watt[(l + 1) * kH + j], hv[l + 1], q1);
+            }
+            qS[idx] = q0 + q1;
+        }
+        __syncthreads();
+        // ---- C: scores s_i = enc_i . q, softmax over T (policy.py:296-299) ----
+        double mx[MT];
+#pragma unroll
+        for (int m = 0; m < MT; m++) mx[m] = -INFINITY;
+        for (int i = tid; i < T; i += kThreads) {
+            const double *er = enc + (size_t)i * enc_ld;
+            double s[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++) s[m] = 0.0;
+#pragma unroll 4
+            for (int j = 0; j < kH; j++) {
+                const double e = er[j];
+#pragma unroll
+                for (int m = 0; m < MT; m++) s[m] = fma(e, qS[m * kH + j], s[m]);
+            }
+#pragma unroll
+            for (int m = 0; m < MT; m++) {
+                if (m < Mb) {
+                    alS[m * a.Tpad + i] = s[m];
+                    mx[m] = fmax(mx[m], s[m]);
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < MT; m++) {
+            double v = mx[m];
+            for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+            if (lane == 0) red[warp * MT + m] = v;
+        }
+        __syncthreads();
+        double gmax[MT], sm_[MT];
+#pragma unroll
+        for (int m = 0; m < MT; m++) {
+            double v = red[m];
+            for (int ww = 1; ww < kThreads / 32; ww++) v = fmax(v, red[ww * MT + m]);
+            gmax[m] = v;
+            sm_[m] = 0.0;
+        }
+        for (int i = tid; i < T; i += kThreads) {
+#pragma unroll
+            for (int m = 0; m < MT; m++) {
+                if (m < Mb) {
+                    const double e = exp(alS[m * a.Tpad + i] - gmax[m]);
+                    alS[m * a.Tpad + i] = e;
+                    sm_[m] += e;
+                }
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < MT; m++) {
+            double v = sm_[m];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) red[8 * MT + warp * MT + m] = v;
+        }
+        __syncthreads();
+        double gsum[MT];
+#pragma unroll
+        for (int m = 0; m < MT; m++) {
+            double v = red[8 * MT + m];
+            for (int ww = 1; ww < kThreads / 32; ww++) v += red[8 * MT + ww * MT + m];
+            gsum[m] = v;
+        }
+        for (int i = tid; i < T; i += kThreads) {
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) alS[m * a.Tpad + i] = alS[m * a.Tpad + i] / gsum[m];
+        }
+        if (tid < Mb) {
+            const size_t row = (size_t)(k0 + tid) * T + t;
+            // stats for the backward's recompute of alpha
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m == tid) {
+                    a.act_stat[row * 2] = gmax[m];
+                    a.act_stat[row * 2 + 1] = gsum[m];
+                }
+        }
+        __syncthreads();
+        // ---- D: ctx = alpha @ enc (policy.py:300) ----
+        {
+            const int j = tid & 63, part = tid >> 6;
+            const int i0 = part * Tq, i1 = min(T, i0 + Tq);
+            double acc[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++) acc[m] = 0.0;
+            for (int i = i0; i < i1; i++) {
+                const double e = enc[(size_t)i * enc_ld + j];
+#pragma unroll
+                for (int m = 0; m < MT; m++) acc[m] = fma(alS[m * a.Tpad + i], e, acc[m]);
+            }
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) red2[(part * M + m) * kH + j] = acc[m];
+        }
+        __syncthreads();
+        for (int idx = tid; idx < Mb * kH; idx += kThreads) {
+            const int m = idx >> 6, j = idx & 63;
+            const double v = ((red2[(0 * M + m) * kH + j] + red2[(1 * M + m) * kH + j]) +
+                              red2[(2 * M + m) * kH + j]) + red2[(3 * M + m) * kH + j];
+            ctxS[idx] = v;
+            a.act_ctx[((size_t)(k0 + m) * T + t) * kH + j] = v;
+        }
+        __syncthreads();
+        // ---- E: output layer, log-softmax, draw (policy.py:301-308, 320-323) ----
+        for (int m = warp; m < Mb; m += kThreads / 32) {
+            const double *hv = hN + m * kH;
+            const double *cv = ctxS + m * kH;
+            const size_t row = (size_t)(k0 + m) * T + t;
+            double uo = 0.0;
+            if (dd <= 16) {
+                const int o = lane & 15, half = lane >> 4;
+                const double *src = half ? cv : hv;
+                double p0 = 0.0, p1 = 0.0;
+                if (o < dd) {
+                    for (int i = 0; i < kH; i += 2) {
+                        p0 = fma(src[i], wout[(half * kH + i) * dd + o], p0);
+                        p1 = fma(src[i + 1], wout[(half * kH + i + 1) * dd + o], p1);
+                    }
+                }
+                const double part = p0 + p1;
+                uo = part + __shfl_xor_sync(0xffffffffu, part, 16);
+                if (half) uo = 0.0;
+            } else {
+                const int o = lane;
+                if (o < dd) {
+                    double p0 = 0.0, p1 = 0.0;
+                    for (int i = 0; i < kH; i++) {
+                        p0 = fma(hv[i], wout[i * dd + o], p0);
+                        p1 = fma(cv[i], wout[(kH + i) * dd + o], p1);
+                    }
+                    uo = p0 + p1;
+                }
+            }
+            if (lane < dd) {
+                uS[m * 32 + lane] = uo;
+                a.act_u[row * dd + lane] = uo;
+            }
+            __syncwarp();
+            double z = -INFINITY;
+            if (lane < D) {
+                double zz = 0.0;
+                for (int o = 0; o < dd; o++) zz = fma(devt[lane * dd + o], uS[m * 32 + o], zz);
+                z = zz + bout[lane];
+            }
+            double zmax = z;
+            for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+            const double zs = z - zmax;
+            if (lane < D) pS[m * 32 + lane] = exp(zs);
+            __syncwarp();
+            double lse = 0.0;
+            if (lane == 0) lse = log(np_sum_small(pS + m * 32, D));
+            lse = __shfl_sync(0xffffffffu, lse, 0);
+            const double pr = exp(zs - lse);
+            __syncwarp();
+            if (lane < D) {
+                pS[m * 32 + lane] = pr;
+                a.act_p[row * D + lane] = pr;
+                if (a.probs_out) a.probs_out[row * D + lane] = pr;
+            }
+            __syncwarp();
+            int ch = 0;
+            if (lane == 0) {
+                if (a.forced) {
+                    ch = a.forced[row];
+                } else {
+                    u128 s{pcg[2 * m], pcg[2 * m + 1]};
+                    s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
+                    pcg[2 * m] = s.hi;
+                    pcg[2 * m + 1] = s.lo;
+                    const double r = pcg_double(s);
+                    double cdf = 0.0;
+                    int cnt = 0;
+                    for (int dv = 0; dv < D; dv++) {
+                        cdf += pS[m * 32 + dv];
+                        cnt += (cdf <= r) ? 1 : 0;
+                    }
+                    ch = cnt < D - 1 ? cnt : D - 1;
+                }
+            }
+            ch = __shfl_sync(0xffffffffu, ch, 0);
+            const double zc = __shfl_sync(0xffffffffu, zs, ch);
+            if (lane == 0) {
+                lp[m] += zc - lse;
+                prev[m] = ch;
+                a.choice[row] = (uint8_t)ch;
+                if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < Mb) a.logp[k0 + tid] = lp[tid];
+}
+
+}  // namespace dp
+
+using namespace dp;
+
+// ---------------------------------------------------------------- host API
+static ParamLayout layout_of(int V1, int D, int dd, int F, int td) {
+    ParamLayout o;
+    int64_t p = 0;
+    o.type_table = p;
+    p += (int64_t)V1 * td;
+    o.dev_table = p;
+    p += (int64_t)(D + 1) * dd;
+    o.w_enc = p;
+    p += (int64_t)(F + kH) * kG;
+    o.b_enc = p;
+    p += kG;
+    o.w_dec = p;
+    p += (int64_t)(dd + kH) * kG;
+    o.b_dec = p;
+    p += kG;
+    o.w_att = p;
+    p += (int64_t)kH * kH;
+    o.w_out = p;
+    p += (int64_t)2 * kH * dd;
+    o.b_out = p;
+    p += D;
+    o.total = p;
+    return o;
+}
+
+extern "C" void dp_policy_destroy(dp_policy *p) {
+    if (!p) return;
+    void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
+                    p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_ctx, p->act_u, p->act_p,
+                    p->act_stat, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
+                    p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+    delete p;
+}
+
+size_t dp_backward_partial_elems(const dp_policy *p);  // policy_bwd.cu
+
+extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_t dev_dim, int32_t type_dim,
+                                int32_t shape_slots, int32_t adj_slots, int32_t vocab_rows,
+                                const int32_t *h_type_off, const int32_t *h_type_idx, const double *h_shape,
+                                const double *h_adj, int32_t k_max, dp_policy **out) {
+    DP_REQUIRE(out != nullptr, "dp_policy_create: out is NULL");
+    DP_REQUIRE(T >= 1, "cannot place an empty group sequence");
+    DP_REQUIRE(hidden == kH, "dp_policy_create: this build supports hidden=64 (reference default)");
+    DP_REQUIRE(n_dev >= 1 && n_dev <= kMaxD, "dp_policy_create: need 1 <= num_devices <= 32");
+    DP_REQUIRE(dev_dim >= 1 && dev_dim <= kMaxDD, "dp_policy_create: need 1 <= dev_dim <= 32");
+    DP_REQUIRE(type_dim >= 1 && shape_slots >= 1 && adj_slots >= 1, "all embedding widths must be >= 1");
+    DP_REQUIRE(vocab_rows >= 1 && k_max >= 1, "dp_policy_create: bad vocab_rows / k_max");
+    dp_policy *p = new dp_policy();
+    PolicyDims &dm = p->dims;
+    dm.T = T;
+    dm.D = n_dev;
+    dm.dd = dev_dim;
+    dm.td = type_dim;
+    dm.ss = shape_slots;
+    dm.as = adj_slots;
+    dm.F = type_dim + shape_slots + adj_slots;
+    dm.V1 = vocab_rows;
+    dm.off = layout_of(vocab_rows, n_dev, dev_dim, dm.F, type_dim);
+    p->k_max = k_max;
+    const int n_idx = h_type_off[T];
+    for (int t = 0; t < T; t++)
+        if (h_type_off[t + 1] <= h_type_off[t]) {
+            dp_policy_destroy(p);
+            dp::set_error("dp_policy_create: every group needs >= 1 member type");
+            return DP_EINVAL;
+        }
+    const size_t rows = (size_t)k_max * T;
+    bool ok = true;
+    auto alloc = [&](void **dst, size_t bytes) {
+        if (!ok) return;
+        if (cudaMalloc(dst, bytes ? bytes : 8) != cudaSuccess) ok = false;
+    };
+    auto upload = [&](void **dst, const void *src, size_t bytes) {
+        alloc(dst, bytes);
+        if (ok && bytes && cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) ok = false;
+    };
+    upload((void **)&p->type_off, h_type_off, sizeof(int32_t) * (T + 1));
+    upload((void **)&p->type_idx, h_type_idx, sizeof(int32_t) * n_idx);
+    {
+        std::vector<int32_t> occ_off(vocab_rows + 1, 0), occ_t(n_idx);
+        for (int i = 0; i < n_idx; i++) {
+            if (h_type_idx[i] < 0 || h_type_idx[i] >= vocab_rows) {
+                dp_policy_destroy(p);
+                dp::set_error("dp_policy_create: type index out of range");
+                return DP_EINVAL;
+            }
+            occ_off[h_type_idx[i] + 1]++;
+        }
+        for (int v = 0; v < vocab_rows; v++) occ_off[v + 1] += occ_off[v];
+        std::vector<int32_t> fill(occ_off.begin(), occ_off.end() - 1);
+        for (int t = 0; t < T; t++)
+            for (int i = h_type_off[t]; i < h_type_off[t + 1]; i++) occ_t[fill[h_type_idx[i]]++] = t;
+        upload((void **)&p->occ_off, occ_off.data(), sizeof(int32_t) * (vocab_rows + 1));
+        upload((void **)&p->occ_t, occ_t.data(), sizeof(int32_t) * n_idx);
+        std::vector<double> z(kH, 0.0);
+        upload((void **)&p->zeros, z.data(), sizeof(double) * kH);
+    }
+    upload((void **)&p->shape, h_shape, sizeof(double) * T * shape_slots);
+    upload((void **)&p->adj, h_adj, sizeof(double) * T * adj_slots);
+    alloc((void **)&p->X, sizeof(double) * T * dm.F);
+    alloc((void **)&p->XP, sizeof(double) * T * kG);
+    alloc((void **)&p->enc_h, sizeof(double) * T * kH);
+    alloc((void **)&p->enc_c, sizeof(double) * T * kH);
+    alloc((void **)&p->enc_g, sizeof(double) * T * kG);
+    alloc((void **)&p->edev, sizeof(double) * (n_dev + 1) * kG);
+    alloc((void **)&p->act_h, sizeof(double) * rows * kH);
+    alloc((void **)&p->act_c, sizeof(double) * rows * kH);
+    alloc((void **)&p->act_g, sizeof(double) * rows * kG);
+    alloc((void **)&p->act_ctx, sizeof(double) * rows * kH);
+    alloc((void **)&p->act_u, sizeof(double) * rows * dev_dim);
+    alloc((void **)&p->act_p, sizeof(double) * rows * n_dev);
+    alloc((void **)&p->act_stat, sizeof(double) * rows * 2);
+    alloc((void **)&p->act_choice, rows);
+    alloc((void **)&p->act_logp, sizeof(double) * k_max);
+    alloc((void **)&p->row_q, sizeof(double) * rows * kH);
+    alloc((void **)&p->row_dctx, sizeof(double) * rows * kH);
+    alloc((void **)&p->row_w, sizeof(double) * rows);
+    alloc((void **)&p->row_dq, sizeof(double) * rows * kH);
+    alloc((void **)&p->row_dhx, sizeof(double) * rows * kH);
+    alloc((void **)&p->dh0, sizeof(double) * k_max * kH);
+    alloc((void **)&p->dc0, sizeof(double) * k_max * kH);
+    alloc((void **)&p->d_enc, sizeof(double) * T * kH);
+    alloc((void **)&p->da_enc, sizeof(double) * T * kG);
+    p->partial_elems = dp_backward_partial_elems(p);
+    alloc((void **)&p->partial, sizeof(double) * p->partial_elems);
+    alloc((void **)&p->gacc, sizeof(double) * dm.off.total);
+    if (!ok) {
+        dp::set_error(std::string("dp_policy_create: allocation/upload failed: ") +
+                      cudaGetErrorString(cudaGetLastError()));
+        dp_policy_destroy(p);
+        return DP_ECUDA;
+    }
+    p->last_K = 0;
+    *out = p;
+    return DP_OK;
+}
+
+extern "C" int64_t dp_policy_num_params(const dp_policy *p) { return p ? p->dims.off.total : -1; }
+
+extern "C" int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream) {
+    DP_REQUIRE(p && out, "dp_policy_read_inputs: NULL argument");
+    DP_CUDA_TRY(cudaMemcpyAsync(out, p->X, sizeof(double) * p->dims.T * p->dims.F, cudaMemcpyDeviceToDevice,
+                                (cudaStream_t)stream));
+    return DP_OK;
+}
+
+extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream) {
+    DP_REQUIRE(p && params, "dp_policy_encode: NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const PolicyDims &dm = p->dims;
+    const int nx = dm.T * dm.F;
+    enc_inputs_kernel<<<ceil_div(nx, 256), 256, 0, st>>>(dm, params, p->type_off, p->type_idx, p->shape, p->adj,
+                                                          p->X);
+    DP_LAUNCH_CHECK();
+    gemm_bias_kernel<<<dim3(1, dm.T), kG, 0, st>>>(dm.T, kG, dm.F, p->X, dm.F, params + dm.off.w_enc, kG,
+                                                   params + dm.off.b_enc, p->XP, kG);
+    DP_LAUNCH_CHECK();
+    gemm_bias_kernel<<<dim3(1, dm.D + 1), kG, 0, st>>>(dm.D + 1, kG, dm.dd, params + dm.off.dev_table, dm.dd,
+                                                       params + dm.off.w_dec, kG, params + dm.off.b_dec, p->edev,
+                                                       kG);
+    DP_LAUNCH_CHECK();
+    enc_rec_kernel<<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+namespace {
+struct DecPlan {
+    int M, MT, enc_in_smem, Tpad;
+    size_t smem;
+    DecArgs proto;
+};
+
+bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
+    const int T = dm.T;
+    const size_t budget = 225 * 1024;
+    int M = ceil_div(K, kNumSMs);
+    if (M < 1) M = 1;
+    if (M > 16) M = 16;
+    for (; M >= 1; M = (M > 1 ? M - 1 : 0)) {
+        for (int enc_smem = 1; enc_smem >= 0; enc_smem--) {
+            DecArgs &a = pl.proto;
+            const int Tpad = (T + 1) & ~1;
+            int o = 0;
+            auto take = [&](int n) {
+                const int r = o;
+                o += (n + 1) & ~1;
+                return r;
+            };
+            a.o_enc = enc_smem ? take(T * kEncPad) : 0;
+            a.o_watt = take(kH * kH);
+            a.o_wout = take(2 * kH * dm.dd);
+            a.o_devt = take(dm.D * dm.dd);
+            a.o_bout = take(dm.D);
+            a.o_edev = take((dm.D + 1) * kG);
+            a.o_h = take(2 * M * kH);
+            a.o_q = take(M * kH);
+            a.o_ctx = take(M * kH);
+            a.o_c = take(M * kH);
+            a.o_u = take(M * 32);
+            a.o_p = take(M * 32);
+            a.o_alpha = take(M * Tpad);
+            const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : 16;
+            a.o_red = take(2 * 8 * MT);
+            a.o_red2 = take(4 * M * kH);
+            a.o_pcg = take(2 * M);
+            a.o_misc = take(16 + M);
+            const size_t bytes = (size_t)o * sizeof(double);
+            if (bytes <= budget) {
+                pl.M = M;
+                pl.MT = MT;
+                pl.enc_in_smem = enc_smem;
+                pl.Tpad = Tpad;
+                pl.smem = bytes;
+                return true;
+            }
+        }
+        if (M == 1) break;
+    }
+    return false;
+}
+}  // namespace
+
+extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, int64_t k_offset,
+                                const uint64_t *h_pcg, uint64_t draw_base, const int64_t *draw_counter,
+                                int64_t draws_per_count, const uint8_t *forced, uint8_t *choice_out,
+                                double *logp, double *probs_out, void *stream) {
+    DP_REQUIRE(p && params && logp, "dp_policy_decode: NULL argument");
+    DP_REQUIRE(K >= 1 && K <= p->k_max, "dp_policy_decode: K out of range (1..k_max)");
+    DP_REQUIRE(forced || h_pcg, "dp_policy_decode: need a PCG64 state or a forced placement");
+    const PolicyDims &dm = p->dims;
+    DecPlan pl;
+    DP_REQUIRE(plan_decoder(dm, K, pl), "dp_policy_decode: shared-memory plan failed");
+    DecArgs a = pl.proto;
+    a.dm = dm;
+    a.params = params;
+    a.K = K;
+    a.k_offset = k_offset;
+    if (h_pcg) {
+        a.st_hi = h_pcg[0];
+        a.st_lo = h_pcg[1];
+        a.inc_hi = h_pcg[2];
+        a.inc_lo = h_pcg[3];
+    } else {
+        a.st_hi = a.st_lo = a.inc_hi = a.inc_lo = 0;
+    }
+    a.draw_base = draw_base;
+    a.draw_counter = (const long long *)draw_counter;
+    a.draws_per_count = draws_per_count;
+    a.forced = forced;
+    a.enc_h = p->enc_h;
+    a.enc_c = p->enc_c;
+    a.edev = p->edev;
+    a.act_h = p->act_h;
+    a.act_c = p->act_c;
+    a.act_g = p->act_g;
+    a.act_ctx = p->act_ctx;
+    a.act_u = p->act_u;
+    a.act_p = p->act_p;
+    a.act_stat = p->act_stat;
+    a.choice = p->act_choice;
+    a.choice_out = choice_out;
+    a.logp = logp;
+    a.probs_out = probs_out;
+    a.M = pl.M;
+    a.enc_in_smem = pl.enc_in_smem;
+    a.Tpad = pl.Tpad;
+    const int grid = ceil_div(K, pl.M);
+    cudaStream_t st = (cudaStream_t)stream;
+    const void *fn = pl.MT == 1 ? (const void *)dec_kernel<1>
+                     : pl.MT == 2 ? (const void *)dec_kernel<2>
+                     : pl.MT == 4 ? (const void *)dec_kernel<4>
+                     : pl.MT == 8 ? (const void *)dec_kernel<8>
+                                  : (const void *)dec_kernel<16>;
+    DP_CUDA_TRY(allow_big_smem(fn, 227 * 1024));
+    void *args[] = {&a};
+    DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));
+    p->last_K = K;
+    return DP_OK;
+}

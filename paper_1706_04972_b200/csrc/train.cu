@@ -1,0 +1,208 @@
+// REINFORCE epilogue and Adam on sm_100a: everything after scoring, on device,
+// so one training update is a fixed launch sequence (CUDA-graph capturable).
+//
+// Reference (/root/reference/pkg/src/devplace/trainer.py):
+//   reward_of            66-72     R = sqrt(m) | failing signal
+//   best-so-far          284-287   strict <, feasible only, k order
+//   success-only filter  289-292
+//   reinforce_update     138-154   adv = R - B over used samples; /= n_used
+//   BaselineState.update 83-84     B <- decay*B + (1-decay)*mean(used R)
+//   LogRow               298-308   mean_R = np.mean(all K rewards)
+//   ParameterStore.apply 113-131   finite check, Adam, version++
+// Scalar statistics replicate numpy's pairwise summation exactly and the
+// Adam element recurrences use unfused mul/add in numpy's order (compiled
+// with --fmad=false), so logs and the optimizer match bit-for-bit given an
+// identical gradient.
+
+#include <math.h>
+
+#include "policy.cuh"
+
+namespace dp {
+namespace {
+
+// numpy pairwise_sum (np.add.reduce / np.mean on a contiguous float64 array)
+__device__ double np_pairwise(const double *a, int n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int i = 0; i < n; i++) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        int i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += a[i];
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+
+// single CTA; thread 0 runs the order-dependent scalar logic, the block copies
+__global__ void epilogue_kernel(int K, int T, const double *__restrict__ makespan,
+                                const uint8_t *__restrict__ feasible, const uint8_t *__restrict__ choice,
+                                double failing, double decay, long long success_only_after, long long k_offset,
+                                int K_local, dp_train_state *st, double *__restrict__ adv,
+                                uint8_t *__restrict__ best_choice, double *__restrict__ log_rows, long long log_cap,
+                                int controller_id) {
+    extern __shared__ double R[];   // [K] rewards, then [K] used rewards
+    __shared__ int s_best_k;
+    const int tid = threadIdx.x;
+    double *used_r = R + K;
+    if (tid == 0) {
+        const long long upd = st->update;
+        double best = st->best_r;
+        int best_k = -1, n_feas = 0, n_used = 0;
+        const bool all = upd < success_only_after;
+        for (int k = 0; k < K; k++) {
+            const bool ok = feasible[k] != 0;
+            const double m = makespan[k];
+            double r;
+            if (!ok) {
+                r = failing;
+            } else {
+                if (!isfinite(m) || m <= 0.0) st->error = 1;  // reward_of raises ValueError
+                r = sqrt(m);
+            }
+            R[k] = r;
+            n_feas += ok ? 1 : 0;
+            if (ok && r < best) {
+                best = r;
+                best_k = k;
+            }
+            if (all || ok) used_r[n_used++] = r;
+        }
+        const double b_old = st->baseline;
+        const double mean_r = np_pairwise(R, K) / (double)K;
+        double b_new = b_old;
+        if (n_used > 0) {
+            const double mu = np_pairwise(used_r, n_used) / (double)n_used;
+            b_new = decay * b_old + (1.0 - decay) * mu;
+        }
+        st->baseline = b_new;
+        st->baseline_prev = b_old;
+        st->n_used = n_used;
+        st->n_feasible = n_feas;
+        if (best_k >= 0) {
+            st->best_r = best;
+            st->best_k = best_k;
+            st->best_update = upd;
+        }
+        s_best_k = best_k;
+        if (upd < log_cap) {
+            double *row = log_rows + upd * 8;
+            row[0] = (double)upd;
+            row[1] = (double)controller_id;
+            row[3] = mean_r;
+            row[4] = b_new;
+            row[5] = st->best_r;
+            row[6] = (double)n_feas;
+            row[7] = (double)n_used;
+        }
+    }
+    __syncthreads();
+    // advantages for this rank's samples: (R - B_old) if used else 0
+    const bool all = st->update < success_only_after;
+    const double b_old = st->baseline_prev;
+    const bool any = st->n_used > 0;
+    for (int k = tid; k < K_local; k += blockDim.x) {
+        const long long kg = k_offset + k;
+        const bool use = any && (all || feasible[kg] != 0);
+        adv[k] = use ? R[kg] - b_old : 0.0;
+    }
+    const int bk = s_best_k;
+    if (bk >= 0)
+        for (int t = tid; t < T; t += blockDim.x) best_choice[t] = choice[(size_t)bk * T + t];
+}
+
+__global__ void finite_check_kernel(long long P, const double *__restrict__ g, int *__restrict__ flag) {
+    long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int bad = 0;
+    for (; i < P; i += (long long)gridDim.x * blockDim.x) bad |= !isfinite(g[i]);
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0 && bad) atomicOr(flag, 1);
+}
+
+// numpy order: m = b1*m + (1-b1)*g ; v = b2*v + (1-b2)*g*g ; mh = m/(1-b1^t) ;
+// vh = v/(1-b2^t) ; p -= lr*mh / (sqrt(vh) + eps)   (pkg/trainer.py:125-129)
+__global__ void adam_kernel(long long P, double *__restrict__ p, double *__restrict__ m, double *__restrict__ v,
+                            const double *__restrict__ grad, const double *__restrict__ bias_corr, long long t_cap,
+                            double lr, double b1, double b2, double eps, const dp_train_state *st,
+                            const int *__restrict__ flag) {
+    const long long nu = st->n_used;
+    if (nu <= 0 || *flag) return;
+    const long long t = st->adam_t + 1;
+    if (t > t_cap) return;
+    const double bc1 = bias_corr[2 * (t - 1)], bc2 = bias_corr[2 * (t - 1) + 1];
+    const double c1 = 1.0 - b1, c2 = 1.0 - b2;
+    const double n = (double)nu;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (long long)gridDim.x * blockDim.x) {
+        const double g = grad[i] / n;
+        const double mi = b1 * m[i] + c1 * g;
+        const double vi = b2 * v[i] + c2 * g * g;
+        m[i] = mi;
+        v[i] = vi;
+        const double mh = mi / bc1;
+        const double vh = vi / bc2;
+        p[i] = p[i] - lr * mh / (sqrt(vh) + eps);
+    }
+}
+
+__global__ void step_finalize_kernel(dp_train_state *st, int *flag, double *log_rows, long long log_cap) {
+    if (threadIdx.x != 0) return;
+    if (st->n_used > 0) {
+        if (*flag) {
+            st->rejected += 1;
+        } else {
+            st->adam_t += 1;
+            st->version += 1;
+        }
+    }
+    if (st->update < log_cap) log_rows[st->update * 8 + 2] = (double)st->version;
+    *flag = 0;
+    st->update += 1;
+}
+
+}  // namespace
+}  // namespace dp
+
+using namespace dp;
+
+extern "C" int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespan, const uint8_t *feasible,
+                                     const uint8_t *choice, double failing, double decay,
+                                     int64_t success_only_after, int64_t k_offset, int32_t K_local,
+                                     dp_train_state *state, double *adv, uint8_t *best_choice, double *log_rows,
+                                     int64_t log_cap, int32_t controller_id, void *stream) {
+    DP_REQUIRE(K >= 1 && K <= 16384, "dp_reinforce_epilogue: need 1 <= K <= 16384");
+    DP_REQUIRE(K_local >= 0 && k_offset >= 0 && k_offset + K_local <= K, "dp_reinforce_epilogue: bad shard");
+    DP_REQUIRE(makespan && feasible && choice && state && best_choice && log_rows,
+               "dp_reinforce_epilogue: NULL argument");
+    const size_t smem = sizeof(double) * 2 * (size_t)K;
+    DP_CUDA_TRY(allow_big_smem((const void *)epilogue_kernel, smem));
+    epilogue_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(K, T, makespan, feasible, choice, failing, decay,
+                                                            success_only_after, k_offset, K_local, state, adv,
+                                                            best_choice, log_rows, log_cap, controller_id);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+extern "C" int dp_adam_apply(int64_t P, double *params, double *m, double *v, const double *grad,
+                             const double *bias_corr, int64_t t_cap, double lr, double b1, double b2, double eps,
+                             dp_train_state *state, int32_t *flag, double *log_rows, int64_t log_cap, void *stream) {
+    DP_REQUIRE(P >= 1 && params && m && v && grad && bias_corr && state && flag,
+               "dp_adam_apply: NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = ceil_div(P, 256) < 2 * kNumSMs ? ceil_div(P, 256) : 2 * kNumSMs;
+    finite_check_kernel<<<blocks, 256, 0, st>>>(P, grad, flag);
+    DP_LAUNCH_CHECK();
+    adam_kernel<<<blocks, 256, 0, st>>>(P, params, m, v, grad, bias_corr, t_cap, lr, b1, b2, eps, state, flag);
+    DP_LAUNCH_CHECK();
+    step_finalize_kernel<<<1, 32, 0, st>>>(state, flag, log_rows, log_cap);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}

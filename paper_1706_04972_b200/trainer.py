@@ -1,0 +1,489 @@
+"""REINFORCE trainer — the batched hot path, device-resident.
+
+Drop-in for the reference ``pkg/trainer.py`` (same names, signatures, log
+format and determinism contract).  One update of one controller
+(``run_controller`` body, pkg/trainer.py:271-308) is a fixed sequence of
+sm_100a launches on one stream, with no host synchronisation:
+
+  dp_policy_encode   encoder once per snapshot
+  dp_policy_decode   K samples, PCG64 draws replayed from the controller stream
+  dp_simulate_batch  K placements scored (event-exact simulator)
+  dp_reinforce_epilogue  rewards, best, success-only, baseline, advantages
+  dp_policy_backward sum_k adv_k * grad log p_k
+  [NCCL all-reduce of the gradient when sharded over ranks]
+  dp_adam_apply      finite check, Adam, version/update counters, log row
+
+so the whole update can be captured once in a CUDA graph and replayed.
+"""
+
+from __future__ import annotations
+
+import io
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import policy as policy_mod
+from .policy import EmbeddingSpec, GroupFeatures, PolicyParams
+from .simulator import INFEASIBLE, SimReport, device_graph, simulate
+
+
+# ----------------------------------------------------------------------------- reference types
+@dataclass(frozen=True)
+class RewardSpec:
+    failing_signal: float
+
+    def __post_init__(self):
+        if not self.failing_signal > 0:
+            raise ValueError("failing_signal must be > 0")
+
+
+def suggest_failing_signal(gg, topo) -> float:
+    """2 x sqrt(total cost / slowest rate) (``pkg/trainer.py:46-53``)."""
+    slowest = min(d.compute_rate for d in topo.devices)
+    return 2.0 * math.sqrt(gg.total_compute_cost() / slowest)
+
+
+def validate_failing_signal(spec: RewardSpec, gg, topo):
+    slowest = min(d.compute_rate for d in topo.devices)
+    bound = math.sqrt(gg.total_compute_cost() / slowest)
+    if spec.failing_signal <= bound:
+        raise ValueError(
+            f"failing_signal {spec.failing_signal} does not exceed the "
+            f"slowest-single-device bound sqrt({gg.total_compute_cost()}/{slowest}) = {bound}")
+
+
+def reward_of(measurement: float, spec: RewardSpec) -> float:
+    """``pkg/trainer.py:66-72`` (scalar; the batched form runs in dp_reinforce_epilogue)."""
+    if measurement == INFEASIBLE:
+        return spec.failing_signal
+    if not math.isfinite(measurement) or measurement <= 0:
+        raise ValueError(f"measurement must be positive and finite, got {measurement}")
+    return math.sqrt(measurement)
+
+
+@dataclass
+class BaselineState:
+    value: float
+    decay: float = 0.9
+    initialized_from_failing_signal: bool = False
+
+    def update(self, mean_reward: float):
+        self.value = self.decay * self.value + (1.0 - self.decay) * mean_reward
+
+
+def _state_tensor(device, baseline=0.0):
+    import torch
+
+    from . import _native as nat
+
+    st = torch.zeros(nat.TRAIN_STATE_WORDS, dtype=torch.float64, device=device)
+    st[0] = baseline
+    st[2] = math.inf
+    return st
+
+
+def _state_read(st) -> dict:
+    from . import _native as nat
+
+    raw = st.cpu()
+    f = raw.numpy()
+    i = raw.view(dtype=__import__("torch").int64).numpy()
+    out = {}
+    for k, name in enumerate(nat.TRAIN_STATE_FIELDS):
+        out[name] = float(f[k]) if k < 3 else int(i[k])
+    return out
+
+
+class ParameterStore:
+    """Authoritative flat parameters + Adam moments on the GPU (``pkg/trainer.py:87-131``).
+
+    ``snapshot()`` returns a host copy; ``apply(g)`` runs the device Adam
+    kernel.  The controller loop uses the device tensors directly."""
+
+    def __init__(self, flat, learning_rate=1e-3, beta1=0.9, beta2=0.999, epsilon=1e-8, device=None,
+                 max_steps: int = 1 << 16):
+        import threading
+
+        import torch
+
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.params = torch.as_tensor(np.array(flat, dtype=np.float64), device=self.device).clone()
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.learning_rate, self.beta1, self.beta2, self.epsilon = learning_rate, beta1, beta2, epsilon
+        self.state = _state_tensor(self.device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._bias_cap = 0
+        self.bias = None
+        self._ensure_bias(max_steps)
+        self._lock = threading.Lock()
+        self._scratch_log = torch.zeros(8, dtype=torch.float64, device=self.device)
+
+    def _ensure_bias(self, steps):
+        import torch
+
+        if steps <= self._bias_cap:
+            return
+        tab = np.empty(2 * steps)
+        for t in range(1, steps + 1):  # Python float pow, as ParameterStore.apply computes it
+            tab[2 * (t - 1)] = 1.0 - self.beta1 ** t
+            tab[2 * (t - 1) + 1] = 1.0 - self.beta2 ** t
+        self.bias = torch.as_tensor(tab, device=self.device)
+        self._bias_cap = steps
+
+    @property
+    def version(self) -> int:
+        return _state_read(self.state)["version"]
+
+    @property
+    def rejected(self) -> int:
+        return _state_read(self.state)["rejected"]
+
+    def snapshot(self):
+        with self._lock:
+            return self.params.cpu().numpy().copy(), self.version
+
+    def adam(self, grad, log=None, log_cap=0, stream=None):
+        """Enqueue dp_adam_apply (grad = advantage-weighted sum; /n_used inside)."""
+        from . import _native as nat
+
+        rc = nat.lib().dp_adam_apply(
+            self.params.numel(), nat.ptr(self.params), nat.ptr(self.m), nat.ptr(self.v), nat.ptr(grad),
+            nat.ptr(self.bias), self._bias_cap, self.learning_rate, self.beta1, self.beta2, self.epsilon,
+            nat.ptr(self.state), nat.ptr(self.flag), nat.ptr(log if log is not None else self._scratch_log),
+            log_cap, nat.stream_ptr(stream))
+        nat.check(rc, "dp_adam_apply")
+
+    def apply(self, gradient) -> int:
+        """Adam step in the descent direction; returns the store version."""
+        import torch
+
+        g = np.asarray(gradient, dtype=np.float64)
+        with self._lock:
+            if g.shape != tuple(self.params.shape):
+                raise ValueError(f"gradient length {g.shape} != parameter length {tuple(self.params.shape)}")
+            st = _state_read(self.state)
+            self._ensure_bias(st["adam_t"] + 1)
+            self.state.view(torch.int64)[7] = 1  # n_used = 1: apply() receives the final gradient
+            self.adam(torch.as_tensor(g, device=self.device))
+            return _state_read(self.state)["version"]
+
+
+def apply_adam(store: ParameterStore, gradient) -> int:
+    return store.apply(gradient)
+
+
+def reinforce_update(params: PolicyParams, feats: GroupFeatures, samples, rewards, baseline: BaselineState):
+    """Advantage-weighted mean of log-prob gradients (``pkg/trainer.py:138-154``),
+    one batched teacher-forced pass + one backward on the GPU."""
+    if not samples:
+        return None
+    b = baseline.value
+    w = [r - b for r in rewards]
+    g = policy_mod.weighted_grad(params, feats, [s.placement for s in samples], w)
+    g = (g / len(samples)).cpu().numpy()
+    baseline.update(float(np.mean(rewards)))
+    return g
+
+
+@dataclass
+class TrainerConfig:
+    k: int = 4
+    total_updates: int = 200
+    success_only_after: int = 5000
+    learning_rate: float = 1e-3
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_epsilon: float = 1e-8
+    seed: int = 0
+    controllers: int = 1
+    workers_per_controller: int | None = None
+    baseline_decay: float = 0.9
+    failing_signal: float | None = None
+    noise_sigma: float = 0.0
+    measure_steps: int = 10
+    hidden: int = 64
+    dev_dim: int = 16
+    type_dim: int = 16
+    shape_slots: int = 8
+    adjacency_slots: int = 64
+    init_scale: float = 0.1
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ValueError("k must be >= 1")
+        if self.success_only_after < 0:
+            raise ValueError("success_only_after must be >= 0")
+
+
+@dataclass
+class LogRow:
+    update_index: int
+    controller_id: int
+    store_version: int
+    mean_r: float
+    baseline: float
+    best_r: float
+    n_feasible: int
+    n_used: int
+    wall_ms: float
+
+    CSV_HEADER = "update_index,controller_id,store_version,mean_R,baseline,best_R,n_feasible_of_K,wall_ms"
+
+    def csv_line(self, include_wall: bool = True) -> str:
+        cells = [str(self.update_index), str(self.controller_id), str(self.store_version),
+                 repr(self.mean_r), repr(self.baseline), repr(self.best_r), str(self.n_feasible)]
+        if include_wall:
+            cells.append(f"{self.wall_ms:.3f}")
+        return ",".join(cells)
+
+
+def log_to_csv(rows, include_wall: bool = True) -> str:
+    header = LogRow.CSV_HEADER if include_wall else LogRow.CSV_HEADER.rsplit(",", 1)[0]
+    buf = io.StringIO()
+    buf.write(header + "\n")
+    for row in rows:
+        buf.write(row.csv_line(include_wall) + "\n")
+    return buf.getvalue()
+
+
+@dataclass
+class TrainResult:
+    best_placement: list | None
+    best_report: SimReport | None
+    log: list
+    final_params: np.ndarray
+    store_versions: int
+    rejected_updates: int
+
+    @property
+    def found_feasible(self) -> bool:
+        return self.best_placement is not None
+
+    @property
+    def best_makespan(self):
+        return self.best_report.makespan_seconds if self.best_report else None
+
+
+@dataclass
+class _TrainTask:
+    gg: object
+    topo: object
+    feats: GroupFeatures
+    template: PolicyParams
+    reward_spec: RewardSpec
+    config: TrainerConfig
+
+
+@dataclass
+class _ControllerResult:
+    rows: list = field(default_factory=list)
+    best_r: float = math.inf
+    best_placement: list | None = None
+
+
+def policy_template(gg, topo, config: TrainerConfig) -> PolicyParams:
+    spec = EmbeddingSpec.build([gg], type_dim=config.type_dim, shape_slots=config.shape_slots,
+                               adjacency_slots=config.adjacency_slots)
+    return PolicyParams.init(spec, topo.num_devices, hidden=config.hidden, dev_dim=config.dev_dim,
+                             seed=config.seed, scale=config.init_scale)
+
+
+# ----------------------------------------------------------------------------- device controller
+class DeviceController:
+    """One controller's REINFORCE loop on one GPU (or one rank's shard of K).
+
+    ``world=(rank, size, group)`` shards the K samples (rank r owns samples
+    [r*K/size, (r+1)*K/size)); per update the ranks all-gather the scores and
+    placements (so every rank replays the reference's sequential best /
+    baseline logic bit-identically) and all-reduce the gradient (NCCL)."""
+
+    def __init__(self, task: _TrainTask, store: ParameterStore, seed_seq, controller_id: int = 0,
+                 world=None, log_cap: int | None = None):
+        import torch
+
+        cfg = task.config
+        if cfg.noise_sigma > 0.0:
+            raise NotImplementedError("measurement noise (noise_sigma > 0) is not on the device path yet "
+                                      "(SURVEY.md §8(f) row f2)")
+        self.task, self.store, self.cid = task, store, controller_id
+        self.device = store.device
+        self.rank, self.size, self.group = world if world is not None else (0, 1, None)
+        K = cfg.k
+        if K % self.size:
+            raise ValueError(f"k={K} must be divisible by the number of ranks {self.size}")
+        self.K, self.K_local = K, K // self.size
+        self.k_offset = self.rank * self.K_local
+        tmpl = task.template
+        self.eng = policy_mod.DevicePolicy(task.feats, tmpl.spec, tmpl.num_devices, tmpl.hidden, tmpl.dev_dim,
+                                           k_max=self.K_local)
+        self.dg = device_graph(task.gg, task.topo)
+        self.T = len(task.feats)
+        sample_seq, _noise_seq = seed_seq.spawn(2)
+        self.rng = np.random.default_rng(sample_seq)
+        self.pcg = policy_mod.generator_state(self.rng)
+        self.log_cap = log_cap if log_cap is not None else cfg.total_updates
+        store._ensure_bias(cfg.total_updates + 1)
+        st = store.state
+        st.zero_()
+        st[0] = task.reward_spec.failing_signal
+        st[2] = math.inf
+        dev = self.device
+        T = self.T
+        self.choice = torch.zeros(self.K_local, T, dtype=torch.uint8, device=dev)
+        self.logp = torch.zeros(self.K_local, dtype=torch.float64, device=dev)
+        self.sim_local = None
+        self.adv = torch.zeros(self.K_local, dtype=torch.float64, device=dev)
+        self.grad = torch.zeros(store.params.numel(), dtype=torch.float64, device=dev)
+        self.best_choice = torch.zeros(T, dtype=torch.uint8, device=dev)
+        self.log = torch.full((max(1, self.log_cap) * 8,), math.nan, dtype=torch.float64, device=dev)
+        if self.size > 1:
+            self.mk_all = torch.zeros(K, dtype=torch.float64, device=dev)
+            self.fe_all = torch.zeros(K, dtype=torch.uint8, device=dev)
+            self.ch_all = torch.zeros(K, T, dtype=torch.uint8, device=dev)
+        self.measure_ok = cfg.measure_steps >= 2
+        self.updates_done = 0
+        self._graph = None
+
+    # one update, enqueue-only (capturable)
+    def step(self, stream=None):
+        import torch
+
+        from . import _native as nat
+
+        cfg, st = self.task.config, self.store
+        p = st.params
+        self.eng.encode(p, stream)
+        self.eng.decode(p, self.K_local, pcg=self.pcg, draw_base=0, k_offset=self.k_offset,
+                        draw_counter=st.state.view(torch.int64)[3:4], draws_per_count=self.K * self.T,
+                        choice=self.choice, logp=self.logp, stream=stream)
+        self.sim_local = self.dg.simulate(self.choice, by_rank=True, stream=stream, out=self.sim_local)
+        mk, fe, ch = self.sim_local["makespan"], self.sim_local["feasible"], self.choice
+        if not self.measure_ok:
+            fe.zero_()  # measure() raises for steps < 2 -> every worker reports INFEASIBLE
+        if self.size > 1:
+            import torch.distributed as dist
+
+            dist.all_gather_into_tensor(self.mk_all, mk, group=self.group)
+            dist.all_gather_into_tensor(self.fe_all, fe, group=self.group)
+            dist.all_gather_into_tensor(self.ch_all, ch, group=self.group)
+            mk, fe, ch = self.mk_all, self.fe_all, self.ch_all
+        rc = nat.lib().dp_reinforce_epilogue(
+            self.K, self.T, nat.ptr(mk), nat.ptr(fe), nat.ptr(ch), self.task.reward_spec.failing_signal,
+            cfg.baseline_decay, cfg.success_only_after, self.k_offset, self.K_local, nat.ptr(st.state),
+            nat.ptr(self.adv), nat.ptr(self.best_choice), nat.ptr(self.log), self.log_cap, self.cid,
+            nat.stream_ptr(stream))
+        nat.check(rc, "dp_reinforce_epilogue")
+        self.eng.backward(p, self.K_local, self.adv, grad=self.grad, stream=stream)
+        if self.size > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(self.grad, group=self.group)
+        st.adam(self.grad, log=self.log, log_cap=self.log_cap, stream=stream)
+
+    def capture(self):
+        """Capture one update in a CUDA graph (after one eager warm-up update)."""
+        import torch
+
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        self._graph = g
+        return g
+
+    def run(self, updates: int, use_graph: bool = True, wall=None):
+        """Run ``updates`` updates; returns per-update wall ms (device-synchronised)."""
+        import torch
+
+        walls = []
+        for _ in range(updates):
+            t0 = time.perf_counter()
+            if use_graph and self._graph is not None:
+                self._graph.replay()
+            else:
+                self.step()
+            if wall is not None:
+                torch.cuda.current_stream().synchronize()
+                walls.append((time.perf_counter() - t0) * 1e3)
+            self.updates_done += 1
+        return walls
+
+    def check_errors(self):
+        st = _state_read(self.store.state)
+        if st["error"]:
+            raise ValueError("measurement must be positive and finite (a feasible placement has makespan <= 0)")
+        return st
+
+    def rows(self, walls=None) -> list:
+        arr = self.log.cpu().numpy().reshape(-1, 8)
+        out = []
+        for u in range(min(self.updates_done, self.log_cap)):
+            r = arr[u]
+            out.append(LogRow(int(r[0]), int(r[1]), int(r[2]), float(r[3]), float(r[4]), float(r[5]),
+                              int(r[6]), int(r[7]), float(walls[u]) if walls else 0.0))
+        return out
+
+    def best(self):
+        st = _state_read(self.store.state)
+        if not math.isfinite(st["best_r"]):
+            return math.inf, None
+        pl = self.eng.by_gid(self.best_choice.view(1, -1))[0].cpu().numpy().astype(int).tolist()
+        return st["best_r"], pl
+
+
+def _make_task(gg, topo, config: TrainerConfig) -> _TrainTask:
+    template = policy_template(gg, topo, config)
+    feats = GroupFeatures.from_grouped(gg, template.spec)
+    failing = config.failing_signal
+    if failing is None:
+        failing = suggest_failing_signal(gg, topo)
+    reward_spec = RewardSpec(failing)
+    validate_failing_signal(reward_spec, gg, topo)
+    return _TrainTask(gg, topo, feats, template, reward_spec, config)
+
+
+def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, seed_seq) -> _ControllerResult:
+    """``pkg/trainer.py:256-309`` on the device (CUDA-graph replay after update 0)."""
+    import torch
+
+    cfg = task.config
+    ctl = DeviceController(task, store, seed_seq, controller_id)
+    walls = []
+    if cfg.total_updates > 0:
+        walls += ctl.run(1, use_graph=False, wall=True)
+    if cfg.total_updates > 1:
+        ctl.capture()
+        walls += ctl.run(cfg.total_updates - 1, use_graph=True, wall=True)
+    torch.cuda.current_stream().synchronize()
+    ctl.check_errors()
+    res = _ControllerResult(rows=ctl.rows(walls))
+    res.best_r, res.best_placement = ctl.best()
+    return res
+
+
+def train(graph, topo, config: TrainerConfig | None = None) -> TrainResult:
+    """Train the policy; return the best feasible placement ever measured
+    (``pkg/trainer.py:341-393``)."""
+    from .graph import coalesce_sole_consumers
+
+    config = config or TrainerConfig()
+    gg = graph if hasattr(graph, "groups") else coalesce_sole_consumers(graph)
+    if config.controllers != 1:
+        raise NotImplementedError("asynchronous multi-controller training is SURVEY.md §8(f) row f1 "
+                                  "(not yet on the device path)")
+    task = _make_task(gg, topo, config)
+    store = ParameterStore(task.template.to_flat(), learning_rate=config.learning_rate, beta1=config.adam_beta1,
+                           beta2=config.adam_beta2, epsilon=config.adam_epsilon,
+                           max_steps=config.total_updates + 1)
+    root = np.random.SeedSequence(config.seed)
+    seqs = root.spawn(config.controllers)
+    res = run_controller(0, store, task, seqs[0])
+    rows = sorted(res.rows, key=lambda r: (r.controller_id, r.update_index))
+    best_pl = list(res.best_placement) if res.best_placement is not None else None
+    best_report = simulate(gg, topo, best_pl) if best_pl is not None else None
+    final, _ = store.snapshot()
+    return TrainResult(best_placement=best_pl, best_report=best_report, log=rows, final_params=final,
+                       store_versions=store.version, rejected_updates=store.rejected)

@@ -1,0 +1,146 @@
+"""GPU parity of the policy kernels (csrc/policy_fwd.cu, policy_bwd.cu) through the C-ABI.
+
+Bars (north_star): sampled indices / placements bit-exact; log-probs and
+probabilities within 1e-12 relative (fp64 path; stated tolerance 1e-5);
+gradients within 1e-9 norm-wise relative (stated tolerance 1e-5).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from fixtures import cfg, npz
+from oracle import policy as opol
+import paper_1706_04972_b200 as dp
+from paper_1706_04972_b200 import policy as P
+
+pytestmark = pytest.mark.gpu
+
+LP_RTOL = 1e-12
+GRAD_RTOL = 1e-9
+
+
+def _setup(name, seed=0):
+    gg, topo, _, _ = cfg(name)
+    tc = dp.TrainerConfig(seed=seed)
+    params = dp.trainer.policy_template(gg, topo, tc)
+    feats = P.GroupFeatures.from_grouped(gg, params.spec)
+    return gg, topo, params, feats
+
+
+def _rng_from(g):
+    s = g["pcg_state"].astype(object)
+    gen = np.random.Generator(np.random.PCG64())
+    gen.bit_generator.state = {"bit_generator": "PCG64",
+                               "state": {"state": (int(s[0]) << 64) | int(s[1]), "inc": (int(s[2]) << 64) | int(s[3])},
+                               "has_uint32": 0, "uinteger": 0}
+    return gen
+
+
+def _relnorm(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_forward_sample_matches_reference(name):
+    gg, topo, params, feats = _setup(name)
+    g = npz(f"policy_{name}.npz")
+    assert np.array_equal(params.to_flat(), g["flat"])
+    np.testing.assert_array_equal(P.embed_groups(params, feats), g["inputs"])
+    rng = _rng_from(g)
+    for k in range(len(g["placements"])):
+        s = P.forward_sample(params, feats, rng)
+        assert np.array_equal(s.placement, g["placements"][k]), f"sample {k} placement differs"
+        assert s.log_prob == pytest.approx(g["log_probs"][k], rel=LP_RTOL)
+    # the caller's generator advanced by exactly K*T draws
+    ref_rng = _rng_from(g)
+    ref_rng.bit_generator.advance(len(g["placements"]) * len(feats))
+    assert rng.bit_generator.state == ref_rng.bit_generator.state
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_teacher_forced_and_gradients_match_reference(name):
+    gg, topo, params, feats = _setup(name)
+    g = npz(f"policy_{name}.npz")
+    pl0 = [int(x) for x in g["placements"][0]]
+    np.testing.assert_allclose(P.step_distributions(params, feats, pl0), g["probs0"], rtol=1e-12, atol=1e-15)
+    other = [int(x) for x in g["other"]]
+    assert P.log_prob_of(params, feats, other) == pytest.approx(float(g["lp_other"]), rel=LP_RTOL)
+    assert _relnorm(P.grad_log_prob(params, feats, pl0), g["grad0"]) < GRAD_RTOL
+    assert _relnorm(P.grad_log_prob(params, feats, other), g["grad_other"]) < GRAD_RTOL
+
+
+@pytest.mark.parametrize("name,K", [("C1", 64), ("C2", 32), ("C3", 48), ("C5", 3)])
+def test_sample_batch_vs_oracle(name, K):
+    """K samples in one launch == K sequential oracle forward_sample calls."""
+    gg, topo, params, feats = _setup(name, seed=1)
+    rng_a = np.random.default_rng(2024)
+    rng_b = np.random.default_rng(2024)
+    pl, lp = P.sample_batch(params, feats, rng_a, K)
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    ofe = opol.features(gg, opol.vocab_of(gg))
+    pol = opol.Policy(params.to_flat(), dims, ofe)
+    for k in range(K):
+        opl, olp, _ = pol.sample(rng_b)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
+    assert rng_a.bit_generator.state == rng_b.bit_generator.state
+
+
+@pytest.mark.parametrize("name,K", [("C1", 16), ("C3", 8), ("C2", 5)])
+def test_weighted_gradient_vs_oracle(name, K):
+    gg, topo, params, feats = _setup(name, seed=3)
+    pls = np.random.default_rng(5).integers(0, topo.num_devices, (K, gg.num_groups))
+    w = np.random.default_rng(6).normal(size=K)
+    got = P.weighted_grad(params, feats, [list(map(int, p)) for p in pls], w).cpu().numpy()
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    ref = np.zeros(dims.n_params)
+    for k in range(K):
+        ref += w[k] * pol.grad([int(x) for x in pls[k]])
+    assert _relnorm(got, ref) < GRAD_RTOL
+
+
+def test_known_answers_zero_params_and_single_device():
+    """zero params -> -T ln D ; D=1 -> log p = 0, zero gradient."""
+    gg, topo, params, feats = _setup("C1")
+    z = params.with_flat(np.zeros(params.flat_size))
+    T = len(feats)
+    assert P.log_prob_of(z, feats, [1] * T) == pytest.approx(-T * np.log(topo.num_devices), rel=1e-13)
+    one = dp.DeviceTopology([dp.Device(0, "gpu", 1.0, 1 << 40)], [[0.0]])
+    p1 = dp.trainer.policy_template(gg, one, dp.TrainerConfig())
+    f1 = P.GroupFeatures.from_grouped(gg, p1.spec)
+    s = P.forward_sample(p1, f1, np.random.default_rng(0))
+    assert s.placement == [0] * T and s.log_prob == 0.0
+    assert not np.any(P.grad_log_prob(p1, f1, s.placement))
+
+
+def test_normalization_exhaustive_small():
+    """Sum over all D^T placements of exp(log p) == 1, T=4, D=2."""
+    ops = [dp.Operation(i, f"o{i}", "matmul" if i % 2 else "add", 1.0 + i, (4 + i,), 0) for i in range(4)]
+    g = dp.ComputationGraph(ops, [dp.Edge(0, 1, 8), dp.Edge(1, 2, 8), dp.Edge(0, 3, 4)])
+    gg = dp.singleton_groups(g)
+    topo = dp.default_topology(1)
+    params = dp.trainer.policy_template(gg, topo, dp.TrainerConfig(seed=4))
+    feats = P.GroupFeatures.from_grouped(gg, params.spec)
+    tot = 0.0
+    for code in range(16):
+        pl = [(code >> i) & 1 for i in range(4)]
+        tot += np.exp(P.log_prob_of(params, feats, pl))
+    assert abs(tot - 1.0) < 1e-12
+
+
+def test_placement_validation_errors():
+    gg, topo, params, feats = _setup("C1")
+    with pytest.raises(ValueError, match="placement length"):
+        P.log_prob_of(params, feats, [0, 1])
+    with pytest.raises(ValueError, match="out of range"):
+        P.grad_log_prob(params, feats, [topo.num_devices] * len(feats))
+
+
+def test_checkpoint_roundtrip(tmp_path):
+    gg, topo, params, feats = _setup("C1")
+    P.save_checkpoint(params, tmp_path / "p.json")
+    q = P.load_checkpoint(tmp_path / "p.json")
+    assert np.array_equal(q.to_flat(), params.to_flat())
+    torch.cuda.synchronize()
