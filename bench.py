@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: batched REINFORCE placement step on B200 (BASELINE.json metric).
+
+One "step" = one full REINFORCE update of the device-placement policy on the
+Inception-V3-shaped graph (config C3: 256 co-location groups, 4 simulated GPUs,
+K=256 samples per B200): encoder, K sampled placements (PCG64 replay of the
+reference's RNG stream), K event-exact simulations, rewards/baseline,
+policy-gradient backward, [NCCL all-reduce], Adam.  Nothing is skipped; the
+precision is the reference's (fp64).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (K per GPU fixed: weak scaling)
+
+Prints ONE JSON line (rank 0).  See DESIGN.md §6 for the roofline terms.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "placements sampled+scored/sec"
+UNIT = "placements/s"
+CFG_FILE = {"C1": "cfg_C1.npz", "C2": "cfg_C2.npz", "C3": "cfg_C3.npz", "C5": "cfg_C5.npz"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--k-per-gpu", type=int, default=None)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=None, help="placements in the CPU baseline sample")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--profile-phases", type=int, default=3)
+    return ap.parse_args()
+
+
+def load_config(name):
+    from paper_1706_04972_b200.instances import load_instance
+    import numpy as np
+
+    path = os.path.join(ROOT, "tests", "golden", CFG_FILE[name])
+    gg, topo = load_instance(path)
+    with np.load(path) as a:
+        K = int(a["K"])
+    return gg, topo, K
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- roofline terms
+def decoder_flops_per_placement(T, D, dd=16, H=64):
+    """Algorithmic FLOPs of the decoder kernel per sampled placement:
+    per step gates 2*H*4H, q = W_att^T h 2*H*H, scores 2*T*H, context 2*T*H,
+    output 2*2H*dd + 2*dd*D."""
+    return T * (2 * H * 4 * H + 2 * H * H + 4 * T * H + 2 * 2 * H * dd + 2 * dd * D)
+
+
+def policy_flops_per_placement(T, D, K):
+    """BASELINE.md §5 F_pol (forward + backward GEMM flops per placement)."""
+    return 3 * T * (45056 + 32 * D) + 768 * T * T + 258048 * T / K
+
+
+def fp64_peak_tflops(nat, torch):
+    scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
+    blocks, threads, iters = 148 * 8, 256, 4096
+    best = 0.0
+    for _ in range(4):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        nat.check(nat.lib().dp_fp64_fma_probe(blocks, threads, iters, scratch.data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream), "probe")
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e)
+        best = max(best, blocks * threads * iters * 16 / (ms * 1e-3) / 1e12)
+    return best
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_baseline(gg, topo, k_sample=None, workers=None):
+    sys.path.insert(0, ROOT)
+    from oracle.trainer import cpu_step_rate
+
+    workers = workers or len(os.sched_getaffinity(0))
+    k_sample = k_sample or 2 * workers
+    r = cpu_step_rate(gg, topo, k_sample, workers=workers)
+    return {"value": r["rate"], "unit": UNIT, "cores": r["workers"], "kind": "port",
+            "sample": f"{r['placements']} placements of config C3 (sample+score+grad per placement, "
+                      f"oracle/ numpy fp64 + C simulator restatement, {r['workers']} processes), "
+                      f"{r['seconds']:.2f} s; per-placement cost is K-independent"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    gg, topo, K = load_config(args.config)
+    workers = len(os.sched_getaffinity(0))
+    k_sample = args.cpu_sample or 2 * workers
+    from oracle.trainer import cpu_step_rate
+
+    for _ in range(max(0, args.warmup)):
+        cpu_step_rate(gg, topo, max(1, workers), workers=workers)
+    tot_p, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        r = cpu_step_rate(gg, topo, k_sample, workers=workers)
+        tot_p += r["placements"]
+        tot_s += r["seconds"]
+    value = tot_p / tot_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"{args.config}: inception_blocks B18 br4 (256 groups), "
+                                                    f"4 simulated GPUs, K={K}", "parallelism": "cpu processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
+                         "sample": f"{args.steps} steps x {k_sample} placements (sample+score+grad), "
+                                   f"oracle port of the reference (numpy fp64 + C simulator)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+
+    import paper_1706_04972_b200 as dp
+    from paper_1706_04972_b200 import _native as nat
+
+    gg, topo, K_cfg = load_config(args.config)
+    k_gpu = args.k_per_gpu or K_cfg
+    K = k_gpu * world
+    total_updates = args.warmup + 2 * args.steps + args.profile_phases + 8
+    cfg = dp.TrainerConfig(k=K, total_updates=total_updates, seed=0)
+    task = dp.trainer._make_task(gg, topo, cfg)
+    store = dp.ParameterStore(task.template.to_flat(), max_steps=total_updates + 1)
+    seq = np.random.SeedSequence(cfg.seed).spawn(1)[0]
+    ctl = dp.trainer.DeviceController(task, store, seq, 0, world=(rank, world, group))
+    stream = torch.cuda.current_stream()
+    T = len(task.feats)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- warm-up (first step eager: counts our launches; then graph capture) ----
+    l0 = nat.lib().dp_launch_count()
+    ctl.step()
+    torch.cuda.synchronize()
+    launches_per_step = nat.lib().dp_launch_count() - l0
+    use_graph = (world == 1) and not args.no_graph
+    if use_graph:
+        ctl.capture()
+
+    def one():
+        if use_graph:
+            ctl._graph.replay()
+        else:
+            ctl.step()
+
+    for _ in range(max(0, args.warmup - 1)):
+        one()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps, CUDA events ----
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            evs[i][0].record(stream)
+            one()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = K * args.steps / (tot_ms * 1e-3)
+    ctl.check_errors()
+
+    # ---- phase profile (eager, events at phase boundaries) ----
+    phases = {}
+    if args.profile_phases > 0:
+        marks = []
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            marks.append((name, e))
+
+        for _ in range(args.profile_phases):
+            flush.fill_(0.0)
+            marks.clear()
+            ctl.step(marks=mark)
+            torch.cuda.synchronize()
+            for (n0, e0), (_n1, e1) in zip(marks, marks[1:]):
+                phases.setdefault(n0, []).append(e0.elapsed_time(e1))
+        phases = {k: statistics.mean(v) for k, v in phases.items()}
+
+    # ---- e2e through the public API with host buffers ----
+    P = store.params.numel()
+    h_params = torch.empty(P, dtype=torch.float64, pin_memory=True)
+    h_params.copy_(store.params.cpu())
+    h_out = torch.empty(P, dtype=torch.float64, pin_memory=True)
+    h_log = torch.empty(8, dtype=torch.float64, pin_memory=True)
+    h_pl = torch.empty(ctl.K_local, T, dtype=torch.uint8, pin_memory=True)
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(1.0)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        store.params.copy_(h_params, non_blocking=True)
+        one()
+        h_out.copy_(store.params, non_blocking=True)
+        h_pl.copy_(ctl.choice, non_blocking=True)
+        h_log.copy_(ctl.log[:8], non_blocking=True)
+        e.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(s.elapsed_time(e))
+        h_params.copy_(h_out)
+    e2e_tot = sum(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e_value = K * args.steps / (e2e_tot * 1e-3)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----
+    D = topo.num_devices
+    peak64 = fp64_peak_tflops(nat, torch)
+    dom = max(phases, key=phases.get) if phases else "decode"
+    dec_ms = phases.get("decode", ms_per_step)
+    dec_flops = decoder_flops_per_placement(T, D) * ctl.K_local
+    achieved = dec_flops / (dec_ms * 1e-3) / 1e12
+    roofline = {
+        "kernel": "dec_kernel (dp_policy_decode)", "bound": "fp64", "achieved": achieved, "peak": peak64,
+        "unit": "TFLOP/s", "frac": achieved / peak64 if peak64 else None, "traffic": None,
+        "peak_source": "measured fp64 DFMA probe (dp_fp64_fma_probe) on this GPU; MEASURED_PEAKS.json "
+                       "has no fp64 figure (bf16 tensor peak is not the denominator of an fp64 kernel)",
+        "algorithmic_flops_per_launch": dec_flops, "avg_launch_ms": dec_ms,
+        "dominant_phase": dom, "phase_ms": phases,
+        "policy_flops_per_step": policy_flops_per_placement(T, D, K) * ctl.K_local,
+    }
+    cpu = None
+    if world == 1 and not args.skip_cpu:
+        try:
+            cpu = cpu_baseline(gg, topo, args.cpu_sample)
+        except Exception as ex:  # pragma: no cover
+            cpu = {"error": repr(ex)}
+    pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: inception_blocks B18 br4 -> 256 co-location groups, "
+                               f"454 group edges, 4 simulated GPUs (rate 10, 65536 B/s links)",
+                   "k_per_gpu": k_gpu, "global_k": K, "decoder_len": T, "parallelism": f"dp{world} (K sharded)",
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "cuda_graph": use_graph},
+        "steps_per_sec": 1e3 / ms_per_step,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": P * 8,
+                "d2h_bytes_per_step": P * 8 + ctl.K_local * T + 64,
+                "note": "params H2D from pinned host -> full update -> params, placements, log row D2H"},
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "measured_peaks": {k: pk.get(k) for k in ("hbm_gbs", "bf16_tflops")},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -44,6 +44,14 @@ typedef struct dp_policy dp_policy;
 /* Text of the last error raised on this thread ("" if none). */
 const char *dp_last_error(void);
 
+/* Number of kernel launches this library has enqueued (process-wide). */
+int64_t dp_launch_count(void);
+
+/* fp64 FMA throughput probe: blocks x threads threads each run 8 independent
+ * DFMA chains of `iters` steps (16*iters FLOP per thread).  Used by bench.py
+ * to measure the fp64 roofline denominator on the box. */
+int dp_fp64_fma_probe(int32_t blocks, int32_t threads, int32_t iters, double *scratch, void *stream);
+
 /* ------------------------------------------------------------------ graph */
 
 /* Upload a grouped graph + device topology (one-time, synchronous).

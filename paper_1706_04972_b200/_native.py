@@ -23,6 +23,8 @@ F64 = ctypes.c_double
 # name -> (restype, argtypes)
 SIGNATURES = {
     "dp_last_error": (ctypes.c_char_p, []),
+    "dp_launch_count": (I64, []),
+    "dp_fp64_fma_probe": (I32, [I32, I32, I32, P, P]),
     "dp_graph_create": (I32, [I32, I32, P, P, P, P, P, P, P, P, P, P, P]),
     "dp_graph_destroy": (None, [P]),
     "dp_simulate_batch": (I32, [P, I32, P, I32, P, P, P, P, P, P, P, P]),

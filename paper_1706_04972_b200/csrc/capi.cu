@@ -1,4 +1,7 @@
-// C-ABI plumbing shared by all entry points: error text, per-device setup.
+// C-ABI plumbing shared by all entry points: error text, per-device setup,
+// launch accounting, and an fp64 FMA throughput probe (roofline denominator
+// for the exact-mode policy kernels; MEASURED_PEAKS.json has no fp64 figure).
+#include <atomic>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -8,8 +11,11 @@
 namespace dp {
 
 static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
 
 void set_error(const std::string &msg) { g_last_error = msg; }
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 cudaError_t allow_big_smem(const void *func, size_t bytes) {
     static std::mutex mu;
@@ -25,6 +31,31 @@ cudaError_t allow_big_smem(const void *func, size_t bytes) {
     return e;
 }
 
+// 8 independent DFMA chains per thread; x stays bounded (a*x+b with |a|<1).
+__global__ void fp64_fma_probe_kernel(int iters, double a, double b, double *out) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = fma(a, x[i], b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) s += x[i];
+    if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+
 }  // namespace dp
 
 extern "C" const char *dp_last_error(void) { return dp::g_last_error.c_str(); }
+
+extern "C" int64_t dp_launch_count(void) { return dp::g_launches.load(); }
+
+extern "C" int dp_fp64_fma_probe(int32_t blocks, int32_t threads, int32_t iters, double *scratch, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(blocks > 0 && threads > 0 && iters > 0 && scratch, "dp_fp64_fma_probe: bad arguments");
+    dp::fp64_fma_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(iters, 0.999999, 1e-7, scratch);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}

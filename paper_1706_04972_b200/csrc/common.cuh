@@ -22,7 +22,12 @@ cudaError_t allow_big_smem(const void *func, size_t bytes);
         }                                                                                  \
     } while (0)
 
-#define DP_REQUIRE(cond, msg)                                                              \
+// Entry-point prologue: clear a stale runtime error left by an unrelated call
+// (e.g. a cudaFree from a destructor) so it is not misattributed.  Sticky
+// (context-corrupting) errors persist and still surface.
+#define DP_ENTRY() (void)cudaGetLastError()
+
+#define DP_REQUIRE(cond, msg)                                                            \
     do {                                                                                   \
         if (!(cond)) {                                                                     \
             ::dp::set_error(msg);                                                          \
@@ -30,7 +35,20 @@ cudaError_t allow_big_smem(const void *func, size_t bytes);
         }                                                                                  \
     } while (0)
 
-#define DP_LAUNCH_CHECK() DP_CUDA_TRY(cudaGetLastError())
+// Every kernel launch goes through DP_LAUNCH_CHECK, which also counts it
+// (dp_launch_count(): evidence of how many of our kernels a step enqueues).
+void count_launch();
+
+#define DP_LAUNCH_CHECK()                                                                  \
+    do {                                                                                   \
+        ::dp::count_launch();                                                              \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess) {                                                           \
+            ::dp::set_error(std::string("kernel launch at ") + __FILE__ + ":" +            \
+                            std::to_string(__LINE__) + ": " + cudaGetErrorString(e_));     \
+            return DP_ECUDA;                                                               \
+        }                                                                                  \
+    } while (0)
 
 constexpr int kNumSMs = 148;
 

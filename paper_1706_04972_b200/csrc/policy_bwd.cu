@@ -613,6 +613,7 @@ size_t dp_backward_partial_elems(const dp_policy *p) {
 
 extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
                                   void *stream) {
+    DP_ENTRY();
     DP_REQUIRE(p && params && adv && grad, "dp_policy_backward: NULL argument");
     DP_REQUIRE(K >= 1 && K == p->last_K, "dp_policy_backward: K must equal the last decode's K");
     const PolicyDims &dm = p->dims;

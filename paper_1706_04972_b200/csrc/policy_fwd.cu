@@ -504,6 +504,7 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc};
     for (void *q : ptrs)
         if (q) cudaFree(q);
+    (void)cudaGetLastError();
     delete p;
 }
 
@@ -513,6 +514,7 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
                                 int32_t shape_slots, int32_t adj_slots, int32_t vocab_rows,
                                 const int32_t *h_type_off, const int32_t *h_type_idx, const double *h_shape,
                                 const double *h_adj, int32_t k_max, dp_policy **out) {
+    DP_ENTRY();
     DP_REQUIRE(out != nullptr, "dp_policy_create: out is NULL");
     DP_REQUIRE(T >= 1, "cannot place an empty group sequence");
     DP_REQUIRE(hidden == kH, "dp_policy_create: this build supports hidden=64 (reference default)");
@@ -613,6 +615,7 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
 extern "C" int64_t dp_policy_num_params(const dp_policy *p) { return p ? p->dims.off.total : -1; }
 
 extern "C" int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream) {
+    DP_ENTRY();
     DP_REQUIRE(p && out, "dp_policy_read_inputs: NULL argument");
     DP_CUDA_TRY(cudaMemcpyAsync(out, p->X, sizeof(double) * p->dims.T * p->dims.F, cudaMemcpyDeviceToDevice,
                                 (cudaStream_t)stream));
@@ -620,6 +623,7 @@ extern "C" int dp_policy_read_inputs(const dp_policy *p, double *out, void *stre
 }
 
 extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream) {
+    DP_ENTRY();
     DP_REQUIRE(p && params, "dp_policy_encode: NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
     const PolicyDims &dm = p->dims;
@@ -700,6 +704,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
                                 const uint64_t *h_pcg, uint64_t draw_base, const int64_t *draw_counter,
                                 int64_t draws_per_count, const uint8_t *forced, uint8_t *choice_out,
                                 double *logp, double *probs_out, void *stream) {
+    DP_ENTRY();
     DP_REQUIRE(p && params && logp, "dp_policy_decode: NULL argument");
     DP_REQUIRE(K >= 1 && K <= p->k_max, "dp_policy_decode: K out of range (1..k_max)");
     DP_REQUIRE(forced || h_pcg, "dp_policy_decode: need a PCG64 state or a forced placement");
@@ -750,6 +755,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     DP_CUDA_TRY(allow_big_smem(fn, 227 * 1024));
     void *args[] = {&a};
     DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));
+    count_launch();
     p->last_K = K;
     return DP_OK;
 }

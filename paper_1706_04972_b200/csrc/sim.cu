@@ -271,6 +271,7 @@ extern "C" int dp_graph_create(int32_t n, int32_t d, const double *h_cost, const
                                const int32_t *h_out_off, const int32_t *h_out_dst, const int64_t *h_out_bytes,
                                const int64_t *h_resident, const int32_t *h_gid, const double *h_rate,
                                const double *h_bw, const int64_t *h_mem, dp_graph **out) {
+    DP_ENTRY();
     DP_REQUIRE(out != nullptr, "dp_graph_create: out is NULL");
     DP_REQUIRE(n >= 0 && n < 65536, "dp_graph_create: need 0 <= n < 65536 groups");
     DP_REQUIRE(d >= 1 && d <= 32, "dp_graph_create: need 1 <= d <= 32 devices");
@@ -332,12 +333,14 @@ extern "C" void dp_graph_destroy(dp_graph *g) {
                     g->resident, g->gid, g->rank, g->rate, g->bw, g->mem};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    (void)cudaGetLastError();
     delete g;
 }
 
 extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *placement, int32_t by_rank,
                                  double *makespan, double *busy, double *transfer, int64_t *peak,
                                  uint8_t *feasible, int32_t *order, uint8_t *err, void *stream) {
+    DP_ENTRY();
     DP_REQUIRE(g != nullptr, "dp_simulate_batch: graph is NULL");
     DP_REQUIRE(K >= 0, "dp_simulate_batch: K < 0");
     if (K == 0) return DP_OK;

@@ -178,6 +178,7 @@ extern "C" int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespa
                                      int64_t success_only_after, int64_t k_offset, int32_t K_local,
                                      dp_train_state *state, double *adv, uint8_t *best_choice, double *log_rows,
                                      int64_t log_cap, int32_t controller_id, void *stream) {
+    DP_ENTRY();
     DP_REQUIRE(K >= 1 && K <= 16384, "dp_reinforce_epilogue: need 1 <= K <= 16384");
     DP_REQUIRE(K_local >= 0 && k_offset >= 0 && k_offset + K_local <= K, "dp_reinforce_epilogue: bad shard");
     DP_REQUIRE(makespan && feasible && choice && state && best_choice && log_rows,
@@ -194,6 +195,7 @@ extern "C" int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespa
 extern "C" int dp_adam_apply(int64_t P, double *params, double *m, double *v, const double *grad,
                              const double *bias_corr, int64_t t_cap, double lr, double b1, double b2, double eps,
                              dp_train_state *state, int32_t *flag, double *log_rows, int64_t log_cap, void *stream) {
+    DP_ENTRY();
     DP_REQUIRE(P >= 1 && params && m && v && grad && bias_corr && state && flag,
                "dp_adam_apply: NULL argument");
     cudaStream_t st = (cudaStream_t)stream;

@@ -349,17 +349,23 @@ class DeviceController:
         self._graph = None
 
     # one update, enqueue-only (capturable)
-    def step(self, stream=None):
+    def step(self, stream=None, marks=None):
+        """Enqueue one update.  ``marks``: optional callable(name) recording a
+        CUDA event at each phase boundary (bench.py phase timing)."""
         import torch
 
         from . import _native as nat
 
+        mark = marks or (lambda _name: None)
         cfg, st = self.task.config, self.store
         p = st.params
+        mark("encode")
         self.eng.encode(p, stream)
+        mark("decode")
         self.eng.decode(p, self.K_local, pcg=self.pcg, draw_base=0, k_offset=self.k_offset,
                         draw_counter=st.state.view(torch.int64)[3:4], draws_per_count=self.K * self.T,
                         choice=self.choice, logp=self.logp, stream=stream)
+        mark("simulate")
         self.sim_local = self.dg.simulate(self.choice, by_rank=True, stream=stream, out=self.sim_local)
         mk, fe, ch = self.sim_local["makespan"], self.sim_local["feasible"], self.choice
         if not self.measure_ok:
@@ -371,26 +377,39 @@ class DeviceController:
             dist.all_gather_into_tensor(self.fe_all, fe, group=self.group)
             dist.all_gather_into_tensor(self.ch_all, ch, group=self.group)
             mk, fe, ch = self.mk_all, self.fe_all, self.ch_all
+        mark("epilogue")
         rc = nat.lib().dp_reinforce_epilogue(
             self.K, self.T, nat.ptr(mk), nat.ptr(fe), nat.ptr(ch), self.task.reward_spec.failing_signal,
             cfg.baseline_decay, cfg.success_only_after, self.k_offset, self.K_local, nat.ptr(st.state),
             nat.ptr(self.adv), nat.ptr(self.best_choice), nat.ptr(self.log), self.log_cap, self.cid,
             nat.stream_ptr(stream))
         nat.check(rc, "dp_reinforce_epilogue")
+        mark("backward")
         self.eng.backward(p, self.K_local, self.adv, grad=self.grad, stream=stream)
         if self.size > 1:
             import torch.distributed as dist
 
+            mark("allreduce")
             dist.all_reduce(self.grad, group=self.group)
+        mark("adam")
         st.adam(self.grad, log=self.log, log_cap=self.log_cap, stream=stream)
+        mark("end")
 
     def capture(self):
         """Capture one update in a CUDA graph (after one eager warm-up update)."""
+        import gc
+
         import torch
 
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.step()
+        # no destructor (cudaFree) may run while the stream is capturing
+        gc.collect()
+        gc.disable()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.step()
+        finally:
+            gc.enable()
         self._graph = g
         return g
 
