@@ -17,16 +17,27 @@ void set_error(const std::string &msg) { g_last_error = msg; }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Raise a kernel's dynamic shared-memory cap once per (kernel, device) to the
+// device opt-in maximum minus its static shared memory.  (Setting it to the
+// size of one launch would LOWER the cap for later, larger launches.)
 cudaError_t allow_big_smem(const void *func, size_t bytes) {
     static std::mutex mu;
-    static std::set<std::pair<std::pair<const void *, int>, size_t>> done;
+    static std::set<std::pair<const void *, int>> done;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair(std::make_pair(func, dev), bytes);
+    auto key = std::make_pair(func, dev);
     if (done.count(key)) return cudaSuccess;
-    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (e != cudaSuccess) return e;
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, func);
+    if (e != cudaSuccess) return e;
+    const int cap = optin - (int)fa.sharedSizeBytes;
+    if ((size_t)cap < bytes) return cudaErrorInvalidValue;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, cap);
     if (e == cudaSuccess) done.insert(key);
     return e;
 }

@@ -752,7 +752,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
                      : pl.MT == 4 ? (const void *)dec_kernel<4>
                      : pl.MT == 8 ? (const void *)dec_kernel<8>
                                   : (const void *)dec_kernel<16>;
-    DP_CUDA_TRY(allow_big_smem(fn, 227 * 1024));
+    DP_CUDA_TRY(allow_big_smem(fn, pl.smem));
     void *args[] = {&a};
     DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));
     count_launch();
