@@ -41,6 +41,7 @@ struct dp_policy {
     double *edev;   // [(D+1)*G] dev_table @ w_dec[:dd] + b_dec (decoder input projection)
     // decoder activations, [k][t][...] (the opaque forward cache)
     double *act_h, *act_c, *act_g, *act_ctx, *act_u, *act_p, *act_stat;
+    double *act_lz;       // [k*T*2] (zs[choice], sum exp zs) -> log-prob terms off the critical path
     uint8_t *act_choice;  // [k*T] by rank
     double *act_logp;     // [k]
     int last_K;

@@ -7,24 +7,26 @@
 // Restructuring — every step is linear in the per-sample
 // advantage, so adv[k] scales dz at the top and all cross-sample sums happen
 // inside the kernels:
-//   B0 row_prep    (parallel over rows (k,t)): dz, du, dhc -> dh_out, dctx;
+//   B0 row_prep    (row tiles, fp64 micro-GEMMs): dz, du, dhc -> dh_out, dctx;
 //                  q = W_att^T h; w = ctx.dctx (== alpha.dalpha); grads of
 //                  b_out, dev_table[:D] (dz x u), w_out (hc x du)
-//   B1 att_bwd     (parallel, tiled fp64 GEMMs over rows x T-chunks):
-//                  recompute s, alpha (forward softmax stats), dalpha = enc.dctx,
-//                  ds = alpha*(dalpha - w); dq += ds@enc;
-//                  d_enc += alpha^T dctx + ds^T q  (== d_enc + d_proj@W_att of
-//                  the reference, with proj@h restated as enc@(W_att^T h))
-//   B1f row_fin    (parallel): dh_ext = dh_out + W_att dq; w_att grad += h x dq
-//   B2 dec_lstm    (sequential over t, parallel over samples): LSTM backward,
-//                  dh_prev = W_dec[dd:] da; stores da per row
-//   B3 dec_wgrad   (parallel split-K): w_dec[dd:] += h_prev x da; per input row
-//                  sums of da give b_dec, w_dec[:dd] and dev_table row grads
-//   B4 enc_lstm    (sequential, ONE sequence): the encoder is shared by all
+//   B1 att_bwd     (row tiles x T-chunks): recompute s, alpha (forward softmax
+//                  stats), dalpha = enc.dctx, ds = alpha*(dalpha - w);
+//                  dq += ds@enc; d_enc += alpha^T dctx + ds^T q  (== d_enc +
+//                  d_proj@W_att of the reference, proj@h restated as enc@(W_att^T h))
+//   B1f row_fin    (row tiles): dh_ext = dh_out + dq@W_att^T; w_att grad += h^T dq
+//   B2 lstm_bwd    (sequential over t, parallel over samples): LSTM backward,
+//                  dh_prev = W_dec[dd:] da; da stored per row (in place)
+//   B3 dec_wgrad   (row tiles, split-K): w_dec[dd:] += h_prev^T da; per input
+//                  row sums of da give b_dec, w_dec[:dd] and dev_table row grads
+//   B4 lstm_bwd    (sequential, ONE sequence): the encoder is shared by all
 //                  samples, so its backward runs once on the summed inputs
 //                  (the reference runs it per sample)
 //   B5 enc_wgrad   w_enc, b_enc, type_table (np.add.at order)
-// Deterministic: fixed partition + ordered reductions, no float atomics.
+// Deterministic: fixed partitions + ordered reductions, no float atomics.
+// Measured B200 latencies that shaped the code (scripts/lat_probe.cu): DFMA
+// ~8 cycles, LDS ~47, shfl ~27, exp ~160, tanh ~290: inner products use
+// register micro-tiles (many independent FMAs per shared-memory load).
 
 #include <math.h>
 
@@ -34,136 +36,174 @@ namespace dp {
 
 namespace {
 
-constexpr int kRowsPerWarpBatch = 8;   // B0/B1f: one row per warp per batch
-constexpr int kTile = 32;              // B1: rows per tile
-constexpr int kChunk = 64;             // B1: enc rows per chunk
+constexpr int kTile = 32;   // rows per tile (B0, B1, B3)
+constexpr int kFinTile = 64;
+constexpr int kChunk = 64;  // B1: enc rows per chunk
 constexpr int kPad = 65;
 
-__device__ __forceinline__ double warp_sum(double v) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
 // ------------------------------------------------------------------ B0
-// grad partial layout per CTA: [b_out (D) | dev_table[:D] (D*dd) | w_out (128*dd)]
+// partial per CTA: [b_out (D) | dev_table[:D] (D*dd) | w_out (128*dd)]
+struct PrepSmem {
+    double watt[kH * kPad];        // W_att[l][j]
+    double woutT[kMaxDD * 2 * kH]; // W_out^T [o][i]
+    double devt[kMaxD * kMaxDD];   // dev_table[:D] [d][o]
+    double h[kTile * kPad];        // [r][l]
+    double ctx[kTile * kPad];
+    double dctx[kTile * kPad];
+    double u[kTile * (kMaxDD + 1)];
+    double du[kTile * (kMaxDD + 1)];
+    double dz[kTile * (kMaxD + 1)];
+};
+
 __global__ void __launch_bounds__(kThreads) row_prep_kernel(
-    PolicyDims dm, const double *__restrict__ P, int rows, int rows_per_cta, const double *__restrict__ adv,
+    PolicyDims dm, const double *__restrict__ P, int rows, int tiles_per_cta, const double *__restrict__ adv,
     const double *__restrict__ act_p, const uint8_t *__restrict__ choice, const double *__restrict__ act_u,
     const double *__restrict__ act_h, const double *__restrict__ act_ctx, double *__restrict__ row_q,
     double *__restrict__ row_dctx, double *__restrict__ row_w, double *__restrict__ row_dhx,
     double *__restrict__ partial) {
-    extern __shared__ __align__(16) double sm0[];
-    __shared__ double s_dz[kRowsPerWarpBatch][kMaxD];
-    __shared__ double s_u[kRowsPerWarpBatch][kMaxDD];
-    __shared__ double s_du[kRowsPerWarpBatch][kMaxDD];
-    __shared__ double s_hc[kRowsPerWarpBatch][2 * kH];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    extern __shared__ __align__(16) double smraw[];
+    PrepSmem &S = *reinterpret_cast<PrepSmem *>(smraw);
+    const int tid = threadIdx.x;
     const int D = dm.D, dd = dm.dd, T = dm.T;
-    double *watt = sm0;                  // [64*64]
-    double *wout = watt + kH * kH;       // [128*dd]
-    double *devt = wout + 2 * kH * dd;   // [D*dd]
-    for (int i = tid; i < kH * kH; i += kThreads) watt[i] = P[dm.off.w_att + i];
-    for (int i = tid; i < 2 * kH * dd; i += kThreads) wout[i] = P[dm.off.w_out + i];
-    for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
-    const int n_acc = D + D * dd + 2 * kH * dd;
-    // thread-owned accumulators (strided ownership of the partial layout)
-    constexpr int kMaxOwn = (kMaxD + kMaxD * kMaxDD + 2 * kH * kMaxDD + kThreads - 1) / kThreads;
-    double acc[kMaxOwn];
+    const int ddp = dd + 1, Dp = D + 1;
+    for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPad + (x & 63)] = P[dm.off.w_att + x];
+    for (int x = tid; x < 2 * kH * dd; x += kThreads) {
+        const int i = x / dd, o = x % dd;
+        S.woutT[o * 2 * kH + i] = P[dm.off.w_out + x];
+    }
+    for (int x = tid; x < D * dd; x += kThreads) S.devt[x] = P[dm.off.dev_table + x];
+    // owned grad accumulators
+    const int gi = tid >> 1, go = tid & 1;  // w_out grad: row i = gi, cols o = go + 2x
+    double gw[kMaxDD / 2];
 #pragma unroll
-    for (int i = 0; i < kMaxOwn; i++) acc[i] = 0.0;
-    const int r0 = blockIdx.x * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
-    __syncthreads();
-    for (int rb = r0; rb < r1; rb += kRowsPerWarpBatch) {
-        const int row = rb + warp;
-        const bool live = row < r1;
-        if (live) {
-            const int k = row / T;
-            const double a = adv[k];
-            const int c = choice[row];
+    for (int x = 0; x < kMaxDD / 2; x++) gw[x] = 0.0;
+    double gdev[4] = {0.0, 0.0, 0.0, 0.0};  // dev grad: e = tid + 256*y < D*dd
+    double gb = 0.0;                         // b_out: tid < D
+    const int n_tiles = (rows + kTile - 1) / kTile;
+    const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
+    for (int tl = t0; tl < t1; tl++) {
+        const int rb = tl * kTile;
+        __syncthreads();
+        for (int x = tid; x < kTile * kH; x += kThreads) {
+            const int r = x >> 6, j = x & 63, row = rb + r;
+            const bool ok = row < rows;
+            S.h[r * kPad + j] = ok ? act_h[(size_t)row * kH + j] : 0.0;
+            S.ctx[r * kPad + j] = ok ? act_ctx[(size_t)row * kH + j] : 0.0;
+        }
+        for (int x = tid; x < kTile * dd; x += kThreads) {
+            const int r = x / dd, o = x % dd, row = rb + r;
+            S.u[r * ddp + o] = row < rows ? act_u[(size_t)row * dd + o] : 0.0;
+        }
+        for (int x = tid; x < kTile * D; x += kThreads) {
+            const int r = x / D, d = x % D, row = rb + r;
             double dz = 0.0;
-            if (lane < D) {
-                dz = -act_p[(size_t)row * D + lane];
-                if (lane == c) dz += 1.0;
-                dz = a * dz;
-                s_dz[warp][lane] = dz;
+            if (row < rows) {
+                dz = -act_p[(size_t)row * D + d];
+                if (d == choice[row]) dz += 1.0;
+                dz = adv[row / T] * dz;
             }
-            if (lane < dd) s_u[warp][lane] = act_u[(size_t)row * dd + lane];
-            const double *h = act_h + (size_t)row * kH;
-            const double *cx = act_ctx + (size_t)row * kH;
-            s_hc[warp][lane] = h[lane];
-            s_hc[warp][lane + 32] = h[lane + 32];
-            s_hc[warp][lane + 64] = cx[lane];
-            s_hc[warp][lane + 96] = cx[lane + 32];
-            __syncwarp();
-            // du = dev_table[:D]^T dz
-            double du = 0.0;
-            if (lane < dd) {
-                for (int dv = 0; dv < D; dv++) du = fma(devt[dv * dd + lane], s_dz[warp][dv], du);
-                s_du[warp][lane] = du;
-            }
-            __syncwarp();
-            // dhc = w_out @ du  -> dh_out (rows 0..63), dctx (rows 64..127)
-            double dhc[4];
-#pragma unroll
-            for (int r = 0; r < 4; r++) {
-                const int i = lane + 32 * r;
-                double v = 0.0;
-                for (int o = 0; o < dd; o++) v = fma(wout[i * dd + o], s_du[warp][o], v);
-                dhc[r] = v;
-            }
-            row_dhx[(size_t)row * kH + lane] = dhc[0];
-            row_dhx[(size_t)row * kH + lane + 32] = dhc[1];
-            row_dctx[(size_t)row * kH + lane] = dhc[2];
-            row_dctx[(size_t)row * kH + lane + 32] = dhc[3];
-            // w = ctx . dctx  (== alpha . dalpha)
-            const double wv = warp_sum(fma(s_hc[warp][64 + lane], dhc[2], s_hc[warp][96 + lane] * dhc[3]));
-            if (lane == 0) row_w[row] = wv;
-            // q = W_att^T h
-#pragma unroll
-            for (int r = 0; r < 2; r++) {
-                const int j = lane + 32 * r;
-                double q0 = 0.0, q1 = 0.0;
-                for (int l = 0; l < kH; l += 2) {
-                    q0 = fma(watt[l * kH + j], s_hc[warp][l], q0);
-                    q1 = fma(watt[(l + 1) * kH + j], s_hc[warp][l + 1], q1);
-                }
-                row_q[(size_t)row * kH + j] = q0 + q1;
-            }
-        } else {
-            if (lane < D) s_dz[warp][lane] = 0.0;
-            if (lane < dd) {
-                s_u[warp][lane] = 0.0;
-                s_du[warp][lane] = 0.0;
-            }
-            for (int i = lane; i < 2 * kH; i += 32) s_hc[warp][i] = 0.0;
+            S.dz[r * Dp + d] = dz;
         }
         __syncthreads();
-        // accumulate owned grad elements over the batch's rows (in row order)
+        // du = dev_table[:D]^T dz ; q = W_att^T h (written to global)
+        for (int x = tid; x < kTile * dd; x += kThreads) {
+            const int r = x / dd, o = x % dd;
+            double v = 0.0;
+            for (int d = 0; d < D; d++) v = fma(S.devt[d * dd + o], S.dz[r * Dp + d], v);
+            S.du[r * ddp + o] = v;
+        }
+        {
+            const int r = tid >> 3, jb = tid & 7;
+            double q[8];
 #pragma unroll
-        for (int s = 0; s < kMaxOwn; s++) {
-            const int e = tid + s * kThreads;
-            if (e < n_acc) {
-                double v = acc[s];
-                for (int w8 = 0; w8 < kRowsPerWarpBatch; w8++) {
-                    if (e < D) {
-                        v += s_dz[w8][e];
-                    } else if (e < D + D * dd) {
-                        const int dv = (e - D) / dd, o = (e - D) % dd;
-                        v = fma(s_dz[w8][dv], s_u[w8][o], v);
-                    } else {
-                        const int i = (e - D - D * dd) / dd, o = (e - D - D * dd) % dd;
-                        v = fma(s_hc[w8][i], s_du[w8][o], v);
-                    }
+            for (int x = 0; x < 8; x++) q[x] = 0.0;
+            const double *hr = S.h + r * kPad;
+#pragma unroll 4
+            for (int l = 0; l < kH; l++) {
+                const double hv = hr[l];
+#pragma unroll
+                for (int x = 0; x < 8; x++) q[x] = fma(S.watt[l * kPad + jb + 8 * x], hv, q[x]);
+            }
+            const int row = rb + r;
+            if (row < rows)
+#pragma unroll
+                for (int x = 0; x < 8; x++) row_q[(size_t)row * kH + jb + 8 * x] = q[x];
+        }
+        __syncthreads();
+        // dhc = W_out du -> dh_out (i < 64) to global, dctx (i >= 64) to smem + global
+        {
+            const int r = tid >> 3, ib = tid & 7;
+            double v[16];
+#pragma unroll
+            for (int x = 0; x < 16; x++) v[x] = 0.0;
+            for (int o = 0; o < dd; o++) {
+                const double dv = S.du[r * ddp + o];
+#pragma unroll
+                for (int x = 0; x < 16; x++) v[x] = fma(S.woutT[o * 2 * kH + ib + 8 * x], dv, v[x]);
+            }
+            const int row = rb + r;
+#pragma unroll
+            for (int x = 0; x < 16; x++) {
+                const int i = ib + 8 * x;
+                if (i < kH) {
+                    if (row < rows) row_dhx[(size_t)row * kH + i] = v[x];
+                } else {
+                    S.dctx[r * kPad + i - kH] = v[x];
+                    if (row < rows) row_dctx[(size_t)row * kH + i - kH] = v[x];
                 }
-                acc[s] = v;
             }
         }
         __syncthreads();
+        // w = ctx . dctx (8 lanes per row)
+        {
+            const int r = tid >> 3, jb = tid & 7;
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int x = 0; x < 8; x += 2) {
+                s0 = fma(S.ctx[r * kPad + jb + 8 * x], S.dctx[r * kPad + jb + 8 * x], s0);
+                s1 = fma(S.ctx[r * kPad + jb + 8 * x + 8], S.dctx[r * kPad + jb + 8 * x + 8], s1);
+            }
+            double s = s0 + s1;
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            s += __shfl_xor_sync(0xffffffffu, s, 4);
+            const int row = rb + r;
+            if (jb == 0 && row < rows) row_w[row] = s;
+        }
+        // grads over the tile's rows
+        for (int r = 0; r < kTile; r++) {
+            const double hc = gi < kH ? S.h[r * kPad + gi] : S.ctx[r * kPad + gi - kH];
+#pragma unroll
+            for (int x = 0; x < kMaxDD / 2; x++) {
+                const int o = go + 2 * x;
+                if (o < dd) gw[x] = fma(hc, S.du[r * ddp + o], gw[x]);
+            }
+        }
+#pragma unroll
+        for (int y = 0; y < 4; y++) {
+            const int e = tid + kThreads * y;
+            if (e < D * dd) {
+                const int d = e / dd, o = e % dd;
+                double v = gdev[y];
+                for (int r = 0; r < kTile; r++) v = fma(S.dz[r * Dp + d], S.u[r * ddp + o], v);
+                gdev[y] = v;
+            }
+        }
+        if (tid < D)
+            for (int r = 0; r < kTile; r++) gb += S.dz[r * Dp + tid];
+    }
+    const size_t na = (size_t)D + D * dd + 2 * kH * dd;
+    double *out = partial + (size_t)blockIdx.x * na;
+    if (tid < D) out[tid] = gb;
+#pragma unroll
+    for (int y = 0; y < 4; y++) {
+        const int e = tid + kThreads * y;
+        if (e < D * dd) out[D + e] = gdev[y];
     }
 #pragma unroll
-    for (int s = 0; s < kMaxOwn; s++) {
-        const int e = tid + s * kThreads;
-        if (e < n_acc) partial[(size_t)blockIdx.x * n_acc + e] = acc[s];
+    for (int x = 0; x < kMaxDD / 2; x++) {
+        const int o = go + 2 * x;
+        if (o < dd) out[D + D * dd + gi * dd + o] = gw[x];
     }
 }
 
@@ -222,7 +262,6 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
                 S.w[tid] = ok ? row_w[row] : 0.0;
             }
             __syncthreads();
-            // S = Q enc^T, DA = DCTX enc^T over this chunk
             {
                 double sv[8], dv[8];
 #pragma unroll
@@ -253,7 +292,6 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
                 }
             }
             __syncthreads();
-            // dq[row, j] += sum_i ds[row, i] enc[i, j]
             {
                 const int row = rb + sr;
                 double acc[8];
@@ -274,7 +312,6 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
                     }
                 }
             }
-            // dE[i, j] += sum_r al[r, i] dc[r, j] + ds[r, i] q[r, j]
 #pragma unroll 2
             for (int r = 0; r < kTile; r++) {
                 double av[4], sv4[4], dcv[4], qv[4];
@@ -294,7 +331,6 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
                     for (int b = 0; b < 4; b++) dE[a][b] = fma(sv4[a], qv[b], fma(av[a], dcv[b], dE[a][b]));
             }
         }
-        // write this CTA's partial for the chunk
 #pragma unroll
         for (int a = 0; a < 4; a++) {
             const int i = i0 + ei + 16 * a;
@@ -309,65 +345,94 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
 }
 
 // ------------------------------------------------------------------ B1f
-// dh_ext = dh_out + W_att dq ; partial w_att grad (64x64) += h x dq
+// dh_ext[r, l] += sum_j W_att[l, j] dq[r, j] ; partial w_att grad [l, j] += sum_r h[r, l] dq[r, j]
+struct FinSmem {
+    double watt[kH * kPad];
+    double q[kFinTile * kPad];
+    double h[kFinTile * kPad];
+};
+
 __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const double *__restrict__ P, int rows,
-                                                           int rows_per_cta, const double *__restrict__ act_h,
+                                                           int tiles_per_cta, const double *__restrict__ act_h,
                                                            const double *__restrict__ row_dq,
                                                            double *__restrict__ row_dhx, double *__restrict__ partial) {
-    __shared__ double watt[kH * kH];
-    __shared__ double s_h[kRowsPerWarpBatch][kH];
-    __shared__ double s_q[kRowsPerWarpBatch][kH];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < kH * kH; i += kThreads) watt[i] = P[dm.off.w_att + i];
-    double acc[16];
+    extern __shared__ __align__(16) double smraw[];
+    FinSmem &S = *reinterpret_cast<FinSmem *>(smraw);
+    const int tid = threadIdx.x;
+    for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPad + (x & 63)] = P[dm.off.w_att + x];
+    const int rb4 = tid >> 4, lb = tid & 15;  // out micro-tile: r in {rb4+16a}, l in {lb+16b}
+    double g[4][4];
 #pragma unroll
-    for (int s = 0; s < 16; s++) acc[s] = 0.0;
-    const int r0 = blockIdx.x * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
-    __syncthreads();
-    for (int rb = r0; rb < r1; rb += kRowsPerWarpBatch) {
-        const int row = rb + warp;
-        if (row < r1) {
-            const double *dq = row_dq + (size_t)row * kH;
-            const double *h = act_h + (size_t)row * kH;
-            s_q[warp][lane] = dq[lane];
-            s_q[warp][lane + 32] = dq[lane + 32];
-            s_h[warp][lane] = h[lane];
-            s_h[warp][lane + 32] = h[lane + 32];
-            __syncwarp();
+    for (int a = 0; a < 4; a++)
 #pragma unroll
-            for (int r = 0; r < 2; r++) {
-                const int l = lane + 32 * r;
-                double v0 = 0.0, v1 = 0.0;
-                for (int j = 0; j < kH; j += 2) {
-                    v0 = fma(watt[l * kH + j], s_q[warp][j], v0);
-                    v1 = fma(watt[l * kH + j + 1], s_q[warp][j + 1], v1);
-                }
-                row_dhx[(size_t)row * kH + l] += v0 + v1;
+        for (int b = 0; b < 4; b++) g[a][b] = 0.0;
+    const int n_tiles = (rows + kFinTile - 1) / kFinTile;
+    const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
+    for (int tl = t0; tl < t1; tl++) {
+        const int rb = tl * kFinTile;
+        __syncthreads();
+        for (int x = tid; x < kFinTile * kH; x += kThreads) {
+            const int r = x >> 6, j = x & 63, row = rb + r;
+            const bool ok = row < rows;
+            S.q[r * kPad + j] = ok ? row_dq[(size_t)row * kH + j] : 0.0;
+            S.h[r * kPad + j] = ok ? act_h[(size_t)row * kH + j] : 0.0;
+        }
+        __syncthreads();
+        {
+            double o[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) o[a][b] = 0.0;
+#pragma unroll 4
+            for (int j = 0; j < kH; j++) {
+                double qv[4], wv[4];
+#pragma unroll
+                for (int a = 0; a < 4; a++) qv[a] = S.q[(rb4 + 16 * a) * kPad + j];
+#pragma unroll
+                for (int b = 0; b < 4; b++) wv[b] = S.watt[(lb + 16 * b) * kPad + j];
+#pragma unroll
+                for (int a = 0; a < 4; a++)
+#pragma unroll
+                    for (int b = 0; b < 4; b++) o[a][b] = fma(qv[a], wv[b], o[a][b]);
             }
-        } else {
-            s_q[warp][lane] = s_q[warp][lane + 32] = 0.0;
-            s_h[warp][lane] = s_h[warp][lane + 32] = 0.0;
-        }
-        __syncthreads();
 #pragma unroll
-        for (int s = 0; s < 16; s++) {
-            const int e = tid + s * kThreads;  // w_att grad element (l, j)
-            const int l = e >> 6, j = e & 63;
-            double v = acc[s];
-            for (int w8 = 0; w8 < kRowsPerWarpBatch; w8++) v = fma(s_h[w8][l], s_q[w8][j], v);
-            acc[s] = v;
+            for (int a = 0; a < 4; a++) {
+                const int row = rb + rb4 + 16 * a;
+                if (row < rows)
+#pragma unroll
+                    for (int b = 0; b < 4; b++) row_dhx[(size_t)row * kH + lb + 16 * b] += o[a][b];
+            }
         }
-        __syncthreads();
+        // grad: l in {rb4 + 16a} (reuse mapping), j in {lb + 16b}
+#pragma unroll 4
+        for (int r = 0; r < kFinTile; r++) {
+            double hv[4], qv[4];
+#pragma unroll
+            for (int a = 0; a < 4; a++) hv[a] = S.h[r * kPad + rb4 + 16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; b++) qv[b] = S.q[r * kPad + lb + 16 * b];
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+#pragma unroll
+                for (int b = 0; b < 4; b++) g[a][b] = fma(hv[a], qv[b], g[a][b]);
+        }
     }
 #pragma unroll
-    for (int s = 0; s < 16; s++) partial[(size_t)blockIdx.x * kH * kH + tid + s * kThreads] = acc[s];
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+        for (int b = 0; b < 4; b++)
+            partial[(size_t)blockIdx.x * kH * kH + (rb4 + 16 * a) * kH + lb + 16 * b] = g[a][b];
 }
 
 // ------------------------------------------------------------------ B2 / B4
-// Sequential LSTM backward (pkg/policy.py:236-253) for M sequences per CTA.
-// thread (r = tid>>2, part = tid&3) keeps W_h[r, part*64 : part*64+64] in
-// registers; dh_prev[r] = sum over 4 parts (shuffle).  In-place: the gate
-// activations of each row are replaced by da.
+// Sequential LSTM backward (pkg/policy.py:236-253) for M (<= 8) sequences per
+// CTA.  thread (r = tid>>2, part = tid&3) keeps W_h[r, part*64 : part*64+64]
+// in registers; dh_prev[r] = sum over the 4 parts (shuffle).  The next step's
+// gate activations / cells / incoming dh are prefetched into registers while
+// the current step's mat-vec runs.  In place: gate activations become da.
+constexpr int kMaxSeqPerCta = 8;
+
 __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
     int T, int n_seq, int M, const double *__restrict__ Wh /* [64 x 256] row-major, ld 256 */,
     double *__restrict__ gates /* [seq][T][256] in: i,f,o,g  out: da */, const double *__restrict__ cst /* [seq][T][64] */,
@@ -378,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
     double *s_dh = sm;                   // [M][64]
     double *s_dc = s_dh + M * kH;        // [M][64]
     double *s_da = s_dc + M * kH;        // [M][256]
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const int q0 = blockIdx.x * M;
     const int Mb = min(M, n_seq - q0);
     const int r = tid >> 2, part = tid & 3;
@@ -390,54 +455,80 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
         s_dh[x] = dh_in ? dh_in[(size_t)(q0 + m) * kH + u] : 0.0;
         s_dc[x] = dc_in ? dc_in[(size_t)(q0 + m) * kH + u] : 0.0;
     }
+    // per-thread (m, u) slots: x = tid + 256*y
+    constexpr int kY = kMaxSeqPerCta * kH / kThreads;
+    double pi[kY], pf[kY], po[kY], pg[kY], pc[kY], pcp[kY], pdx[kY];
+    auto prefetch = [&](int t) {
+#pragma unroll
+        for (int y = 0; y < kY; y++) {
+            const int x = tid + kThreads * y;
+            if (x < Mb * kH && t >= 0) {
+                const int m = x >> 6, u = x & 63;
+                const size_t row = (size_t)(q0 + m) * T + t;
+                const double *g = gates + row * kG;
+                pi[y] = g[u];
+                pf[y] = g[kH + u];
+                po[y] = g[2 * kH + u];
+                pg[y] = g[3 * kH + u];
+                pc[y] = cst[row * kH + u];
+                pcp[y] = t > 0 ? cst[(row - 1) * kH + u] : c_init[u];
+                pdx[y] = dh_ext[row * kH + u];
+            }
+        }
+    };
+    prefetch(T - 1);
     __syncthreads();
     for (int t = T - 1; t >= 0; t--) {
-        for (int x = tid; x < Mb * kH; x += kThreads) {
-            const int m = x >> 6, u = x & 63;
-            const size_t row = (size_t)(q0 + m) * T + t;
-            double *g = gates + row * kG;
-            const double iv = g[u], fv = g[kH + u], ov = g[2 * kH + u], gv = g[3 * kH + u];
-            const double c = cst[row * kH + u];
-            const double cp = t > 0 ? cst[(row - 1) * kH + u] : c_init[u];
-            const double dh = s_dh[x] + dh_ext[row * kH + u];
-            const double tc = tanh(c);
-            const double d_o = dh * tc;
-            const double dcv = s_dc[x] + dh * ov * (1.0 - tc * tc);
-            const double di = dcv * gv;
-            const double dg = dcv * iv;
-            const double df = dcv * cp;
-            s_dc[x] = dcv * fv;
-            const double da_i = di * iv * (1.0 - iv);
-            const double da_f = df * fv * (1.0 - fv);
-            const double da_o = d_o * ov * (1.0 - ov);
-            const double da_g = dg * (1.0 - gv * gv);
-            double *sd = s_da + m * kG;
-            sd[u] = da_i;
-            sd[kH + u] = da_f;
-            sd[2 * kH + u] = da_o;
-            sd[3 * kH + u] = da_g;
-            g[u] = da_i;
-            g[kH + u] = da_f;
-            g[2 * kH + u] = da_o;
-            g[3 * kH + u] = da_g;
+#pragma unroll
+        for (int y = 0; y < kY; y++) {
+            const int x = tid + kThreads * y;
+            if (x < Mb * kH) {
+                const int m = x >> 6, u = x & 63;
+                const double iv = pi[y], fv = pf[y], ov = po[y], gv = pg[y], c = pc[y], cp = pcp[y];
+                const double dh = s_dh[x] + pdx[y];
+                const double tc = tanh(c);
+                const double d_o = dh * tc;
+                const double dcv = s_dc[x] + dh * ov * (1.0 - tc * tc);
+                const double di = dcv * gv;
+                const double dg = dcv * iv;
+                const double df = dcv * cp;
+                s_dc[x] = dcv * fv;
+                const double da_i = di * iv * (1.0 - iv);
+                const double da_f = df * fv * (1.0 - fv);
+                const double da_o = d_o * ov * (1.0 - ov);
+                const double da_g = dg * (1.0 - gv * gv);
+                double *sd = s_da + m * kG;
+                sd[u] = da_i;
+                sd[kH + u] = da_f;
+                sd[2 * kH + u] = da_o;
+                sd[3 * kH + u] = da_g;
+                double *g = gates + ((size_t)(q0 + m) * T + t) * kG;
+                g[u] = da_i;
+                g[kH + u] = da_f;
+                g[2 * kH + u] = da_o;
+                g[3 * kH + u] = da_g;
+            }
         }
+        prefetch(t - 1);  // overlaps the barrier + mat-vec below
         __syncthreads();
         for (int m = 0; m < Mb; m++) {
-            const double *sd = s_da + m * kG + part * kH;
-            double a0 = 0.0, a1 = 0.0;
+            const double2 *sd = reinterpret_cast<const double2 *>(s_da + m * kG + part * kH);
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-            for (int i = 0; i < kH; i += 2) {
-                a0 = fma(w[i], sd[i], a0);
-                a1 = fma(w[i + 1], sd[i + 1], a1);
+            for (int i = 0; i < kH / 2; i += 2) {
+                const double2 v0 = sd[i], v1 = sd[i + 1];
+                a0 = fma(w[2 * i], v0.x, a0);
+                a1 = fma(w[2 * i + 1], v0.y, a1);
+                a2 = fma(w[2 * i + 2], v1.x, a2);
+                a3 = fma(w[2 * i + 3], v1.y, a3);
             }
-            double v = a0 + a1;
+            double v = (a0 + a1) + (a2 + a3);
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
             if (part == 0) s_dh[m * kH + r] = v;
         }
         __syncthreads();
     }
-    (void)lane;
     for (int x = tid; x < Mb * kH; x += kThreads) {
         const int m = x >> 6, u = x & 63;
         dh_out[(size_t)(q0 + m) * kH + u] = s_dh[x];
@@ -447,63 +538,93 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
 
 // ------------------------------------------------------------------ B3
 // partial per CTA: [Hg (64 x 256) | DAsum ((D+1) x 256)]
-__global__ void __launch_bounds__(kThreads) dec_wgrad_kernel(PolicyDims dm, int rows, int rows_per_cta,
-                                                             const double *__restrict__ act_h,
-                                                             const double *__restrict__ enc_h,
-                                                             const uint8_t *__restrict__ choice,
-                                                             const double *__restrict__ da,
-                                                             double *__restrict__ partial) {
-    __shared__ double s_h[kTile][kH];
+// thread (lb = tid>>5, jl = tid&31) owns Hg[lb*8 + a][jl + 32*b] (a, b < 8);
+// thread tid owns DAsum[:, tid].
+__global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, int rows, int tiles_per_cta,
+                                                                const double *__restrict__ act_h,
+                                                                const double *__restrict__ enc_h,
+                                                                const uint8_t *__restrict__ choice,
+                                                                const double *__restrict__ da,
+                                                                double *__restrict__ partial) {
+    extern __shared__ __align__(16) double sm[];
+    double *s_h = sm;                        // [kTile][64]
+    double *s_da = s_h + kTile * kH;         // [kTile][256]
+    double *s_dasum = s_da + kTile * kG;     // [(D+1)][256]
     __shared__ int s_prev[kTile];
-    extern __shared__ __align__(16) double s_dasum[];  // [(D+1)][256] thread-owned columns
     const int tid = threadIdx.x;
     const int T = dm.T, D = dm.D;
-    double acc[kH];
+    const int lb = tid >> 5, jl = tid & 31;
+    double acc[8][8];
 #pragma unroll
-    for (int l = 0; l < kH; l++) acc[l] = 0.0;
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 8; b++) acc[a][b] = 0.0;
     for (int p = 0; p <= D; p++) s_dasum[p * kG + tid] = 0.0;
-    const int r0 = blockIdx.x * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
-    for (int rb = r0; rb < r1; rb += kTile) {
+    const int n_tiles = (rows + kTile - 1) / kTile;
+    const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
+    for (int tl = t0; tl < t1; tl++) {
+        const int rb = tl * kTile;
         __syncthreads();
         for (int x = tid; x < kTile * kH; x += kThreads) {
-            const int r = x >> 6, l = x & 63;
-            const int row = rb + r;
+            const int r = x >> 6, l = x & 63, row = rb + r;
             double v = 0.0;
-            if (row < r1) {
+            if (row < rows) {
                 const int t = row % T;
                 v = t > 0 ? act_h[(size_t)(row - 1) * kH + l] : enc_h[(size_t)(T - 1) * kH + l];
             }
-            s_h[r][l] = v;
+            s_h[x] = v;
+        }
+        for (int x = tid; x < kTile * kG; x += kThreads) {
+            const int row = rb + (x >> 8);
+            s_da[x] = row < rows ? da[(size_t)rb * kG + x] : 0.0;
         }
         if (tid < kTile) {
             const int row = rb + tid;
             int pv = D;
-            if (row < r1 && row % T > 0) pv = choice[row - 1];
+            if (row < rows && row % T > 0) pv = choice[row - 1];
             s_prev[tid] = pv;
         }
         __syncthreads();
-        const int nr = min(kTile, r1 - rb);
-        for (int r = 0; r < nr; r++) {
-            const double d = da[(size_t)(rb + r) * kG + tid];
+#pragma unroll 2
+        for (int r = 0; r < kTile; r++) {
+            double hv[8], dv[8];
 #pragma unroll
-            for (int l = 0; l < kH; l++) acc[l] = fma(s_h[r][l], d, acc[l]);
-            s_dasum[s_prev[r] * kG + tid] += d;
+            for (int a = 0; a < 8; a++) hv[a] = s_h[r * kH + lb * 8 + a];
+#pragma unroll
+            for (int b = 0; b < 8; b++) dv[b] = s_da[r * kG + jl + 32 * b];
+#pragma unroll
+            for (int a = 0; a < 8; a++)
+#pragma unroll
+                for (int b = 0; b < 8; b++) acc[a][b] = fma(hv[a], dv[b], acc[a][b]);
         }
+        const int nr = min(kTile, rows - rb);
+        for (int r = 0; r < nr; r++) s_dasum[s_prev[r] * kG + tid] += s_da[r * kG + tid];
     }
     const size_t base = (size_t)blockIdx.x * (kH + D + 1) * kG;
 #pragma unroll
-    for (int l = 0; l < kH; l++) partial[base + (size_t)l * kG + tid] = acc[l];
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+        for (int b = 0; b < 8; b++) partial[base + (size_t)(lb * 8 + a) * kG + jl + 32 * b] = acc[a][b];
     for (int p = 0; p <= D; p++) partial[base + (size_t)(kH + p) * kG + tid] = s_dasum[p * kG + tid];
 }
 
 // ------------------------------------------------------------------ reductions
-// dst[e] (+)= sum_c src[c * stride + e] (c ascending)
+// dst[e] (+)= sum_c src[c * stride + e]: 4 interleaved accumulators (c mod 4),
+// combined in a fixed tree -> deterministic, latency-hidden.
 __global__ void reduce_partials_kernel(const double *__restrict__ src, int n_cta, size_t stride, int n,
                                        double *__restrict__ dst, int accumulate) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n) return;
-    double v = src[e];
-    for (int c = 1; c < n_cta; c++) v += src[(size_t)c * stride + e];
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    int c = 0;
+    for (; c + 4 <= n_cta; c += 4) {
+        v0 += src[(size_t)c * stride + e];
+        v1 += src[(size_t)(c + 1) * stride + e];
+        v2 += src[(size_t)(c + 2) * stride + e];
+        v3 += src[(size_t)(c + 3) * stride + e];
+    }
+    for (; c < n_cta; c++) v0 += src[(size_t)c * stride + e];
+    const double v = (v0 + v1) + (v2 + v3);
     dst[e] = accumulate ? dst[e] + v : v;
 }
 
@@ -521,21 +642,28 @@ __global__ void dec_finalize_kernel(PolicyDims dm, const double *__restrict__ P,
         for (int p = 0; p <= D; p++) v = fma(P[dm.off.dev_table + p * dd + i], dasum[p * kG + tid], v);
         grad[dm.off.w_dec + (size_t)i * kG + tid] = v;
     }
-    // dev_table rows: one (p, i) per thread
     for (int x = tid; x < (D + 1) * dd; x += blockDim.x) {
         const int p = x / dd, i = x % dd;
-        double v = 0.0;
-        for (int j = 0; j < kG; j++) v = fma(P[dm.off.w_dec + (size_t)i * kG + j], dasum[p * kG + j], v);
-        grad[dm.off.dev_table + x] += v;
+        double v0 = 0.0, v1 = 0.0;
+        for (int j = 0; j < kG; j += 2) {
+            v0 = fma(P[dm.off.w_dec + (size_t)i * kG + j], dasum[p * kG + j], v0);
+            v1 = fma(P[dm.off.w_dec + (size_t)i * kG + j + 1], dasum[p * kG + j + 1], v1);
+        }
+        grad[dm.off.dev_table + x] += v0 + v1;
     }
 }
 
 // sum over samples of the decoder's dh/dc at step 0 -> encoder final state grads
 __global__ void sum_rows_kernel(const double *__restrict__ src, int n_rows, double *__restrict__ dst) {
     const int j = threadIdx.x;  // 64
-    double v = src[j];
-    for (int r = 1; r < n_rows; r++) v += src[(size_t)r * kH + j];
-    dst[j] = v;
+    double v0 = 0.0, v1 = 0.0;
+    int r = 0;
+    for (; r + 2 <= n_rows; r += 2) {
+        v0 += src[(size_t)r * kH + j];
+        v1 += src[(size_t)(r + 1) * kH + j];
+    }
+    if (r < n_rows) v0 += src[(size_t)r * kH + j];
+    dst[j] = v0 + v1;
 }
 
 // B5: w_enc / b_enc grads (contraction over T) and the type-embedding scatter.
@@ -544,19 +672,25 @@ __global__ void enc_wgrad_kernel(PolicyDims dm, const double *__restrict__ X, co
     const int j = threadIdx.x;   // gate column
     const int r = blockIdx.x;    // row of w_enc (0..F+H-1), or F+H for b_enc
     const int T = dm.T, F = dm.F;
-    double v = 0.0;
+    double v0 = 0.0, v1 = 0.0;
     if (r == F + kH) {
-        for (int t = 0; t < T; t++) v += da_enc[(size_t)t * kG + j];
-        grad[dm.off.b_enc + j] = v;
+        int t = 0;
+        for (; t + 2 <= T; t += 2) {
+            v0 += da_enc[(size_t)t * kG + j];
+            v1 += da_enc[(size_t)(t + 1) * kG + j];
+        }
+        if (t < T) v0 += da_enc[(size_t)t * kG + j];
+        grad[dm.off.b_enc + j] = v0 + v1;
         return;
     }
     for (int t = 0; t < T; t++) {
         double x;
         if (r < F) x = X[(size_t)t * F + r];
         else x = t > 0 ? enc_h[(size_t)(t - 1) * kH + (r - F)] : 0.0;
-        v = fma(x, da_enc[(size_t)t * kG + j], v);
+        if (t & 1) v1 = fma(x, da_enc[(size_t)t * kG + j], v1);
+        else v0 = fma(x, da_enc[(size_t)t * kG + j], v0);
     }
-    grad[dm.off.w_enc + (size_t)r * kG + j] = v;
+    grad[dm.off.w_enc + (size_t)r * kG + j] = v0 + v1;
 }
 
 // dx_t[f] = W_enc[f, :] . da_enc[t]   (f < type_dim)
@@ -565,9 +699,12 @@ __global__ void enc_dx_kernel(PolicyDims dm, const double *__restrict__ P, const
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= dm.T * dm.td) return;
     const int t = idx / dm.td, f = idx % dm.td;
-    double v = 0.0;
-    for (int j = 0; j < kG; j++) v = fma(P[dm.off.w_enc + (size_t)f * kG + j], da_enc[(size_t)t * kG + j], v);
-    dx[idx] = v;
+    double v0 = 0.0, v1 = 0.0;
+    for (int j = 0; j < kG; j += 2) {
+        v0 = fma(P[dm.off.w_enc + (size_t)f * kG + j], da_enc[(size_t)t * kG + j], v0);
+        v1 = fma(P[dm.off.w_enc + (size_t)f * kG + j + 1], da_enc[(size_t)t * kG + j + 1], v1);
+    }
+    dx[idx] = v0 + v1;
 }
 
 // np.add.at(type_table, idx_t, dx_t / len(idx_t)) in (t, position) order
@@ -587,8 +724,8 @@ __global__ void type_scatter_kernel(PolicyDims dm, const int32_t *__restrict__ o
     grad[dm.off.type_table + idx] = s;
 }
 
-int n_cta_for(int rows, int min_rows) {
-    int n = ceil_div(rows, min_rows);
+int n_cta_for(int units, int min_units) {
+    int n = ceil_div(units, min_units);
     if (n > 2 * kNumSMs) n = 2 * kNumSMs;
     return n < 1 ? 1 : n;
 }
@@ -627,21 +764,25 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
 
     // B0
     {
-        const int n = n_cta_for(rows, 64);
-        const int rpc = ceil_div(rows, n);
-        const size_t smem = sizeof(double) * (kH * kH + 2 * kH * dm.dd + dm.D * dm.dd);
+        const int n_tiles = ceil_div(rows, kTile);
+        const int n = n_cta_for(n_tiles, 2);
+        const int tpc = ceil_div(n_tiles, n);
+        const int n_used = ceil_div(n_tiles, tpc);
+        const size_t smem = sizeof(PrepSmem);
         DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
-        row_prep_kernel<<<n, kThreads, smem, st>>>(dm, params, rows, rpc, adv, p->act_p, p->act_choice, p->act_u,
-                                                 p->act_h, p->act_ctx, p->row_q, p->row_dctx, p->row_w, p->row_dhx,
-                                                 part);
+        row_prep_kernel<<<n_used, kThreads, smem, st>>>(dm, params, rows, tpc, adv, p->act_p, p->act_choice,
+                                                        p->act_u, p->act_h, p->act_ctx, p->row_q, p->row_dctx,
+                                                        p->row_w, p->row_dhx, part);
         DP_LAUNCH_CHECK();
         const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
-        // [b_out | dev[:D] | w_out]
-        reduce_partials_kernel<<<ceil_div(dm.D, 256), 256, 0, st>>>(part, n, na, dm.D, grad + dm.off.b_out, 0);
-        reduce_partials_kernel<<<ceil_div(dm.D * dm.dd, 256), 256, 0, st>>>(part + dm.D, n, na, dm.D * dm.dd,
+        // [b_out | dev[:D] | w_out] are contiguous in neither layout -> three segments
+        reduce_partials_kernel<<<ceil_div(dm.D, 256), 256, 0, st>>>(part, n_used, na, dm.D, grad + dm.off.b_out, 0);
+        DP_LAUNCH_CHECK();
+        reduce_partials_kernel<<<ceil_div(dm.D * dm.dd, 256), 256, 0, st>>>(part + dm.D, n_used, na, dm.D * dm.dd,
                                                                             grad + dm.off.dev_table, 0);
+        DP_LAUNCH_CHECK();
         reduce_partials_kernel<<<ceil_div(2 * kH * dm.dd, 256), 256, 0, st>>>(
-            part + dm.D + dm.D * dm.dd, n, na, 2 * kH * dm.dd, grad + dm.off.w_out, 0);
+            part + dm.D + dm.D * dm.dd, n_used, na, 2 * kH * dm.dd, grad + dm.off.w_out, 0);
         DP_LAUNCH_CHECK();
     }
     // B1
@@ -661,18 +802,22 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     }
     // B1f
     {
-        const int n = n_cta_for(rows, 64);
-        const int rpc = ceil_div(rows, n);
-        row_fin_kernel<<<n, kThreads, 0, st>>>(dm, params, rows, rpc, p->act_h, p->row_dq, p->row_dhx, part);
+        const int n_tiles = ceil_div(rows, kFinTile);
+        const int n = n_cta_for(n_tiles, 2);
+        const int tpc = ceil_div(n_tiles, n);
+        const int n_used = ceil_div(n_tiles, tpc);
+        const size_t smem = sizeof(FinSmem);
+        DP_CUDA_TRY(allow_big_smem((const void *)row_fin_kernel, smem));
+        row_fin_kernel<<<n_used, kThreads, smem, st>>>(dm, params, rows, tpc, p->act_h, p->row_dq, p->row_dhx, part);
         DP_LAUNCH_CHECK();
-        reduce_partials_kernel<<<ceil_div(kH * kH, 256), 256, 0, st>>>(part, n, kH * kH, kH * kH,
+        reduce_partials_kernel<<<ceil_div(kH * kH, 256), 256, 0, st>>>(part, n_used, kH * kH, kH * kH,
                                                                        grad + dm.off.w_att, 0);
         DP_LAUNCH_CHECK();
     }
     // B2: decoder LSTM backward, per sample
     {
         int M = ceil_div(K, kNumSMs);
-        if (M > 8) M = 8;
+        if (M > kMaxSeqPerCta) M = kMaxSeqPerCta;
         const size_t smem = sizeof(double) * (size_t)M * (2 * kH + kG);
         DP_CUDA_TRY(allow_big_smem((const void *)lstm_bwd_kernel, smem));
         lstm_bwd_kernel<<<ceil_div(K, M), kThreads, smem, st>>>(
@@ -682,18 +827,21 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     }
     // B3
     {
-        const int n = n_cta_for(rows, 128);
-        const int rpc = ceil_div(rows, n);
-        const size_t smem = sizeof(double) * (dm.D + 1) * kG;
-        DP_CUDA_TRY(allow_big_smem((const void *)dec_wgrad_kernel, smem + 32 * 1024));
-        dec_wgrad_kernel<<<n, kThreads, smem, st>>>(dm, rows, rpc, p->act_h, p->enc_h, p->act_choice, p->act_g,
-                                                    part);
+        const int n_tiles = ceil_div(rows, kTile);
+        const int n = n_cta_for(n_tiles, 2);
+        const int tpc = ceil_div(n_tiles, n);
+        const int n_used = ceil_div(n_tiles, tpc);
+        const size_t smem = sizeof(double) * ((size_t)kTile * (kH + kG) + (size_t)(dm.D + 1) * kG);
+        DP_CUDA_TRY(allow_big_smem((const void *)dec_wgrad_kernel, smem));
+        dec_wgrad_kernel<<<n_used, kThreads, smem, st>>>(dm, rows, tpc, p->act_h, p->enc_h, p->act_choice, p->act_g,
+                                                         part);
         DP_LAUNCH_CHECK();
         const size_t stride = (size_t)(kH + dm.D + 1) * kG;
-        reduce_partials_kernel<<<ceil_div(kH * kG, 256), 256, 0, st>>>(part, n, stride, kH * kG,
+        reduce_partials_kernel<<<ceil_div(kH * kG, 256), 256, 0, st>>>(part, n_used, stride, kH * kG,
                                                                        grad + dm.off.w_dec + (size_t)dm.dd * kG, 0);
-        reduce_partials_kernel<<<ceil_div((dm.D + 1) * kG, 256), 256, 0, st>>>(part + (size_t)kH * kG, n, stride,
-                                                                               (dm.D + 1) * kG, p->gacc, 0);
+        DP_LAUNCH_CHECK();
+        reduce_partials_kernel<<<ceil_div((dm.D + 1) * kG, 256), 256, 0, st>>>(
+            part + (size_t)kH * kG, n_used, stride, (dm.D + 1) * kG, p->gacc, 0);
         DP_LAUNCH_CHECK();
         dec_finalize_kernel<<<1, kG, 0, st>>>(dm, params, p->gacc, grad);
         DP_LAUNCH_CHECK();
@@ -701,6 +849,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     // B4: encoder backward once on the summed inputs
     {
         sum_rows_kernel<<<1, kH, 0, st>>>(p->dh0, K, dhc_sum);
+        DP_LAUNCH_CHECK();
         sum_rows_kernel<<<1, kH, 0, st>>>(p->dc0, K, dhc_sum + kH);
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, st));

@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- decoder
+constexpr int kEncLd = 66;  // enc_states row stride in shared memory: 16-byte rows, conflict-free LDS.128
+
 struct DecArgs {
     PolicyDims dm;
     const double *params;
@@ -161,16 +163,27 @@ struct DecArgs {
     long long draws_per_count;
     const uint8_t *forced;
     const double *enc_h, *enc_c, *edev;
-    double *act_h, *act_c, *act_g, *act_ctx, *act_u, *act_p, *act_stat;
+    double *act_h, *act_c, *act_g, *act_ctx, *act_u, *act_p, *act_stat, *act_lz;
     uint8_t *choice, *choice_out;
     double *logp, *probs_out;
-    int M, enc_in_smem, Tpad;
+    int M, Tpad;
     // shared-memory offsets (doubles)
     int o_enc, o_watt, o_wout, o_devt, o_bout, o_edev, o_h, o_q, o_ctx, o_c, o_u, o_p, o_alpha, o_red,
         o_red2, o_pcg, o_misc;
 };
 
-template <int MT>
+constexpr int kCtxParts = 8;
+
+// One CTA owns M samples for all T decode steps.  Per step:
+//   A  gates = edev[prev] + h.W_h (thread per gate column, W_h in registers),
+//      LSTM cell, h/c/gates to the activation store
+//   B  q = W_att^T h
+//   C  s_i = enc_i . q (row per thread), softmax over T (block max, block sum)
+//   D  ctx = (sum_i e_i enc_i) / sum  (lane pairs over j, 8 row-parts)
+//   E  warp per sample: u = [h; ctx] W_out, z = dev_table[:D] u + b_out,
+//      p = softmax(z), PCG64 draw, cdf search -> choice; the log-prob term's
+//      log() is deferred to the end of the kernel (off the per-step path)
+template <int MT, bool ES>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -179,31 +192,28 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     const int k0 = blockIdx.x * M;
     const int Mb = min(M, a.K - k0);
     const double *P = a.params;
-
-    double *encS = a.enc_in_smem ? sm + a.o_enc : nullptr;
-    const int enc_ld = a.enc_in_smem ? kEncPad : kH;
-    const double *enc = a.enc_in_smem ? encS : a.enc_h;
+    constexpr int LD = ES ? kEncLd : kH;
+    const double *enc = ES ? (const double *)(sm + a.o_enc) : a.enc_h;
     double *watt = sm + a.o_watt;
     double *wout = sm + a.o_wout;
     double *devt = sm + a.o_devt;
     double *bout = sm + a.o_bout;
     double *edev = sm + a.o_edev;
-    double *hS = sm + a.o_h;      // [2][M][64]
-    double *qS = sm + a.o_q;      // [M][64]
-    double *ctxS = sm + a.o_ctx;  // [M][64]
-    double *cS = sm + a.o_c;      // [M][64]
-    double *uS = sm + a.o_u;      // [M][32]
-    double *pS = sm + a.o_p;      // [M][32]
-    double *alS = sm + a.o_alpha; // [M][Tpad]
-    double *red = sm + a.o_red;   // [8][M] x 2
-    double *red2 = sm + a.o_red2; // [4][M][64]
+    double *hS = sm + a.o_h;       // [2][M][64]
+    double *qS = sm + a.o_q;       // [M][64]
+    double *ctxS = sm + a.o_ctx;   // [M][64]
+    double *cS = sm + a.o_c;       // [M][64]
+    double *uS = sm + a.o_u;       // [M][32]
+    double *pS = sm + a.o_p;       // [M][32]
+    double *alS = sm + a.o_alpha;  // [M][Tpad] unnormalised e_i
+    double *red = sm + a.o_red;    // [2][8][MT]
+    double *red2 = sm + a.o_red2;  // [8 parts][M][64]
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);                               // [M]
-    double *lp = sm + a.o_misc + 16;                                                   // [M]
 
     // ---- stage weights ----
-    if (encS)
-        for (int i = tid; i < T * kH; i += kThreads) encS[(i >> 6) * kEncPad + (i & 63)] = a.enc_h[i];
+    if (ES)
+        for (int i = tid; i < T * kH; i += kThreads) sm[a.o_enc + (i >> 6) * kEncLd + (i & 63)] = a.enc_h[i];
     for (int i = tid; i < kH * kH; i += kThreads) watt[i] = P[dm.off.w_att + i];
     for (int i = tid; i < 2 * kH * dd; i += kThreads) wout[i] = P[dm.off.w_out + i];
     for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
@@ -215,7 +225,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     }
     if (tid < Mb) {
         prev[tid] = D;
-        lp[tid] = 0.0;
         if (!a.forced) {
             const long long kg = a.k_offset + k0 + tid;
             unsigned long long n0 = a.draw_base + (unsigned long long)kg * (unsigned long long)T;
@@ -235,27 +244,34 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     __syncthreads();
 
     const int base = lane & ~3;
-    const int Tq = (T + 3) / 4;
+    const int Tp = (T + kCtxParts - 1) / kCtxParts;
     for (int t = 0; t < T; t++) {
         const int cur = t & 1;
         // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
-        for (int m = 0; m < Mb; m++) {
-            const double *hc = hS + (cur * M + m) * kH;
-            const double av = edev[prev[m] * kG + col] + dot64_sh_reg(hc, w);
-            const double act = gate == 3 ? tanh(av) : sigmoid_ref(av);
-            const size_t row = (size_t)(k0 + m) * T + t;
-            a.act_g[row * kG + col] = act;
-            const double iv = __shfl_sync(0xffffffffu, act, base + 0);
-            const double fv = __shfl_sync(0xffffffffu, act, base + 1);
-            const double ov = __shfl_sync(0xffffffffu, act, base + 2);
-            const double gv = __shfl_sync(0xffffffffu, act, base + 3);
-            if (gate == 0) {
-                const double cn = fv * cS[m * kH + u] + iv * gv;
-                const double hn = ov * tanh(cn);
-                cS[m * kH + u] = cn;
-                hS[((cur ^ 1) * M + m) * kH + u] = hn;
-                a.act_h[row * kH + u] = hn;
-                a.act_c[row * kH + u] = cn;
+        {
+            double av[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) av[m] = edev[prev[m] * kG + col] + dot64_sh_reg(hS + (cur * M + m) * kH, w);
+#pragma unroll
+            for (int m = 0; m < MT; m++) {
+                if (m < Mb) {
+                    const double act = gate == 3 ? tanh(av[m]) : sigmoid_ref(av[m]);
+                    const size_t row = (size_t)(k0 + m) * T + t;
+                    a.act_g[row * kG + col] = act;
+                    const double iv = __shfl_sync(0xffffffffu, act, base + 0);
+                    const double fv = __shfl_sync(0xffffffffu, act, base + 1);
+                    const double ov = __shfl_sync(0xffffffffu, act, base + 2);
+                    const double gv = __shfl_sync(0xffffffffu, act, base + 3);
+                    if (gate == 0) {
+                        const double cn = fv * cS[m * kH + u] + iv * gv;
+                        const double hn = ov * tanh(cn);
+                        cS[m * kH + u] = cn;
+                        hS[((cur ^ 1) * M + m) * kH + u] = hn;
+                        a.act_h[row * kH + u] = hn;
+                        a.act_c[row * kH + u] = cn;
+                    }
+                }
             }
         }
         __syncthreads();
@@ -263,14 +279,17 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         // ---- B: q = W_att^T h ----
         for (int idx = tid; idx < Mb * kH; idx += kThreads) {
             const int m = idx >> 6, j = idx & 63;
-            const double *hv = hN + m * kH;
-            double q0 = 0.0, q1 = 0.0;
-#pragma unroll 8
-            for (int l = 0; l < kH; l += 2) {
-                q0 = fma(watt[l * kH + j], hv[l], q0);
-                q1 = fma(watt[(l + 1) * kH + j], hv[l + 1], q1);
+            const double2 *hv = reinterpret_cast<const double2 *>(hN + m * kH);
+            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+#pragma unroll
+            for (int l2 = 0; l2 < kH / 2; l2 += 2) {
+                const double2 h0 = hv[l2], h1 = hv[l2 + 1];
+                q0 = fma(watt[(2 * l2) * kH + j], h0.x, q0);
+                q1 = fma(watt[(2 * l2 + 1) * kH + j], h0.y, q1);
+                q2 = fma(watt[(2 * l2 + 2) * kH + j], h1.x, q2);
+                q3 = fma(watt[(2 * l2 + 3) * kH + j], h1.y, q3);
             }
-            qS[idx] = q0 + q1;
+            qS[idx] = (q0 + q1) + (q2 + q3);
         }
         __syncthreads();
         // ---- C: scores s_i = enc_i . q, softmax over T (policy.py:296-299) ----
@@ -278,21 +297,26 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
         for (int m = 0; m < MT; m++) mx[m] = -INFINITY;
         for (int i = tid; i < T; i += kThreads) {
-            const double *er = enc + (size_t)i * enc_ld;
-            double s[MT];
+            const double2 *er = reinterpret_cast<const double2 *>(enc + (size_t)i * LD);
+            double s0[MT], s1[MT];
 #pragma unroll
-            for (int m = 0; m < MT; m++) s[m] = 0.0;
-#pragma unroll 4
-            for (int j = 0; j < kH; j++) {
-                const double e = er[j];
+            for (int m = 0; m < MT; m++) s0[m] = s1[m] = 0.0;
+#pragma unroll 8
+            for (int j2 = 0; j2 < kH / 2; j2++) {
+                const double2 e = er[j2];
 #pragma unroll
-                for (int m = 0; m < MT; m++) s[m] = fma(e, qS[m * kH + j], s[m]);
+                for (int m = 0; m < MT; m++) {
+                    const double2 qq = reinterpret_cast<const double2 *>(qS + m * kH)[j2];
+                    s0[m] = fma(e.x, qq.x, s0[m]);
+                    s1[m] = fma(e.y, qq.y, s1[m]);
+                }
             }
 #pragma unroll
             for (int m = 0; m < MT; m++) {
                 if (m < Mb) {
-                    alS[m * a.Tpad + i] = s[m];
-                    mx[m] = fmax(mx[m], s[m]);
+                    const double s = s0[m] + s1[m];
+                    alS[m * a.Tpad + i] = s;
+                    mx[m] = fmax(mx[m], s);
                 }
             }
         }
@@ -307,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
         for (int m = 0; m < MT; m++) {
             double v = red[m];
+#pragma unroll
             for (int ww = 1; ww < kThreads / 32; ww++) v = fmax(v, red[ww * MT + m]);
             gmax[m] = v;
             sm_[m] = 0.0;
@@ -328,55 +353,56 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             if (lane == 0) red[8 * MT + warp * MT + m] = v;
         }
         __syncthreads();
-        double gsum[MT];
-#pragma unroll
-        for (int m = 0; m < MT; m++) {
-            double v = red[8 * MT + m];
-            for (int ww = 1; ww < kThreads / 32; ww++) v += red[8 * MT + ww * MT + m];
-            gsum[m] = v;
-        }
-        for (int i = tid; i < T; i += kThreads) {
-#pragma unroll
-            for (int m = 0; m < MT; m++)
-                if (m < Mb) alS[m * a.Tpad + i] = alS[m * a.Tpad + i] / gsum[m];
-        }
-        if (tid < Mb) {
-            const size_t row = (size_t)(k0 + tid) * T + t;
-            // stats for the backward's recompute of alpha
-#pragma unroll
-            for (int m = 0; m < MT; m++)
-                if (m == tid) {
-                    a.act_stat[row * 2] = gmax[m];
-                    a.act_stat[row * 2 + 1] = gsum[m];
-                }
-        }
-        __syncthreads();
-        // ---- D: ctx = alpha @ enc (policy.py:300) ----
+        // ---- D: ctx = alpha @ enc (policy.py:300), alpha = e / sum ----
         {
-            const int j = tid & 63, part = tid >> 6;
-            const int i0 = part * Tq, i1 = min(T, i0 + Tq);
-            double acc[MT];
+            const int jp = tid & 31, part = tid >> 5;
+            const int i0 = part * Tp, i1 = min(T, i0 + Tp);
+            double ax[MT], ay[MT];
 #pragma unroll
-            for (int m = 0; m < MT; m++) acc[m] = 0.0;
+            for (int m = 0; m < MT; m++) ax[m] = ay[m] = 0.0;
             for (int i = i0; i < i1; i++) {
-                const double e = enc[(size_t)i * enc_ld + j];
+                const double2 e = *reinterpret_cast<const double2 *>(enc + (size_t)i * LD + 2 * jp);
 #pragma unroll
-                for (int m = 0; m < MT; m++) acc[m] = fma(alS[m * a.Tpad + i], e, acc[m]);
+                for (int m = 0; m < MT; m++) {
+                    const double al = alS[m * a.Tpad + i];
+                    ax[m] = fma(al, e.x, ax[m]);
+                    ay[m] = fma(al, e.y, ay[m]);
+                }
             }
 #pragma unroll
             for (int m = 0; m < MT; m++)
-                if (m < Mb) red2[(part * M + m) * kH + j] = acc[m];
+                if (m < Mb)
+                    *reinterpret_cast<double2 *>(red2 + (part * M + m) * kH + 2 * jp) = make_double2(ax[m], ay[m]);
         }
         __syncthreads();
         for (int idx = tid; idx < Mb * kH; idx += kThreads) {
             const int m = idx >> 6, j = idx & 63;
-            const double v = ((red2[(0 * M + m) * kH + j] + red2[(1 * M + m) * kH + j]) +
-                              red2[(2 * M + m) * kH + j]) + red2[(3 * M + m) * kH + j];
+            double gs = red[8 * MT + m];
+#pragma unroll
+            for (int ww = 1; ww < kThreads / 32; ww++) gs += red[8 * MT + ww * MT + m];
+            double v = red2[m * kH + j];
+#pragma unroll
+            for (int p = 1; p < kCtxParts; p++) v += red2[(p * M + m) * kH + j];
+            v = v / gs;
             ctxS[idx] = v;
-            a.act_ctx[((size_t)(k0 + m) * T + t) * kH + j] = v;
+            const size_t row = (size_t)(k0 + m) * T + t;
+            a.act_ctx[row * kH + j] = v;
+        }
+        if (tid < Mb) {
+            // softmax stats for the backward's recompute of alpha
+            const size_t row = (size_t)(k0 + tid) * T + t;
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m == tid) {
+                    double gs = red[8 * MT + m];
+#pragma unroll
+                    for (int ww = 1; ww < kThreads / 32; ww++) gs += red[8 * MT + ww * MT + m];
+                    a.act_stat[row * 2] = gmax[m];
+                    a.act_stat[row * 2 + 1] = gs;
+                }
         }
         __syncthreads();
-        // ---- E: output layer, log-softmax, draw (policy.py:301-308, 320-323) ----
+        // ---- E: output layer, softmax over devices, draw (policy.py:301-308, 320-323) ----
         for (int m = warp; m < Mb; m += kThreads / 32) {
             const double *hv = hN + m * kH;
             const double *cv = ctxS + m * kH;
@@ -385,14 +411,17 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             if (dd <= 16) {
                 const int o = lane & 15, half = lane >> 4;
                 const double *src = half ? cv : hv;
-                double p0 = 0.0, p1 = 0.0;
+                double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
                 if (o < dd) {
-                    for (int i = 0; i < kH; i += 2) {
+#pragma unroll 4
+                    for (int i = 0; i < kH; i += 4) {
                         p0 = fma(src[i], wout[(half * kH + i) * dd + o], p0);
                         p1 = fma(src[i + 1], wout[(half * kH + i + 1) * dd + o], p1);
+                        p2 = fma(src[i + 2], wout[(half * kH + i + 2) * dd + o], p2);
+                        p3 = fma(src[i + 3], wout[(half * kH + i + 3) * dd + o], p3);
                     }
                 }
-                const double part = p0 + p1;
+                const double part = (p0 + p1) + (p2 + p3);
                 uo = part + __shfl_xor_sync(0xffffffffu, part, 16);
                 if (half) uo = 0.0;
             } else {
@@ -413,19 +442,25 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             __syncwarp();
             double z = -INFINITY;
             if (lane < D) {
-                double zz = 0.0;
-                for (int o = 0; o < dd; o++) zz = fma(devt[lane * dd + o], uS[m * 32 + o], zz);
-                z = zz + bout[lane];
+                double z0 = 0.0, z1 = 0.0;
+                int o = 0;
+                for (; o + 2 <= dd; o += 2) {
+                    z0 = fma(devt[lane * dd + o], uS[m * 32 + o], z0);
+                    z1 = fma(devt[lane * dd + o + 1], uS[m * 32 + o + 1], z1);
+                }
+                if (o < dd) z0 = fma(devt[lane * dd + o], uS[m * 32 + o], z0);
+                z = (z0 + z1) + bout[lane];
             }
             double zmax = z;
             for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
             const double zs = z - zmax;
-            if (lane < D) pS[m * 32 + lane] = exp(zs);
+            const double ez = exp(zs);
+            if (lane < D) pS[m * 32 + lane] = ez;
             __syncwarp();
-            double lse = 0.0;
-            if (lane == 0) lse = log(np_sum_small(pS + m * 32, D));
-            lse = __shfl_sync(0xffffffffu, lse, 0);
-            const double pr = exp(zs - lse);
+            double esum = 0.0;
+            if (lane == 0) esum = np_sum_small(pS + m * 32, D);
+            esum = __shfl_sync(0xffffffffu, esum, 0);
+            const double pr = ez / esum;
             __syncwarp();
             if (lane < D) {
                 pS[m * 32 + lane] = pr;
@@ -455,18 +490,32 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             ch = __shfl_sync(0xffffffffu, ch, 0);
             const double zc = __shfl_sync(0xffffffffu, zs, ch);
             if (lane == 0) {
-                lp[m] += zc - lse;
                 prev[m] = ch;
                 a.choice[row] = (uint8_t)ch;
                 if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
+                a.act_lz[row * 2] = zc;
+                a.act_lz[row * 2 + 1] = esum;
             }
         }
         __syncthreads();
     }
-    if (tid < Mb) a.logp[k0 + tid] = lp[tid];
+    // ---- log p = sum_t (zs[c_t] - log sum_t): logs in parallel, sum in t order ----
+    __threadfence_block();
+    for (int m = 0; m < Mb; m++) {
+        const size_t r0 = (size_t)(k0 + m) * T;
+        for (int t = tid; t < T; t += kThreads) alS[t] = a.act_lz[(r0 + t) * 2] - log(a.act_lz[(r0 + t) * 2 + 1]);
+        __syncthreads();
+        if (tid == 0) {
+            double lp = 0.0;
+            for (int t = 0; t < T; t++) lp += alS[t];
+            a.logp[k0 + m] = lp;
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace dp
+
 
 using namespace dp;
 
@@ -500,7 +549,7 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
     if (!p) return;
     void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
                     p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_ctx, p->act_u, p->act_p,
-                    p->act_stat, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
+                    p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc};
     for (void *q : ptrs)
         if (q) cudaFree(q);
@@ -587,6 +636,7 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     alloc((void **)&p->act_u, sizeof(double) * rows * dev_dim);
     alloc((void **)&p->act_p, sizeof(double) * rows * n_dev);
     alloc((void **)&p->act_stat, sizeof(double) * rows * 2);
+    alloc((void **)&p->act_lz, sizeof(double) * rows * 2);
     alloc((void **)&p->act_choice, rows);
     alloc((void **)&p->act_logp, sizeof(double) * k_max);
     alloc((void **)&p->row_q, sizeof(double) * rows * kH);
@@ -655,7 +705,7 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
     const size_t budget = 225 * 1024;
     int M = ceil_div(K, kNumSMs);
     if (M < 1) M = 1;
-    if (M > 16) M = 16;
+    if (M > 8) M = 8;
     for (; M >= 1; M = (M > 1 ? M - 1 : 0)) {
         for (int enc_smem = 1; enc_smem >= 0; enc_smem--) {
             DecArgs &a = pl.proto;
@@ -666,7 +716,7 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
                 o += (n + 1) & ~1;
                 return r;
             };
-            a.o_enc = enc_smem ? take(T * kEncPad) : 0;
+            a.o_enc = enc_smem ? take(T * kEncLd) : 0;
             a.o_watt = take(kH * kH);
             a.o_wout = take(2 * kH * dm.dd);
             a.o_devt = take(dm.D * dm.dd);
@@ -679,9 +729,9 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
             a.o_u = take(M * 32);
             a.o_p = take(M * 32);
             a.o_alpha = take(M * Tpad);
-            const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : M <= 8 ? 8 : 16;
+            const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
             a.o_red = take(2 * 8 * MT);
-            a.o_red2 = take(4 * M * kH);
+            a.o_red2 = take(kCtxParts * M * kH);
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + M);
             const size_t bytes = (size_t)o * sizeof(double);
@@ -738,20 +788,26 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.act_u = p->act_u;
     a.act_p = p->act_p;
     a.act_stat = p->act_stat;
+    a.act_lz = p->act_lz;
     a.choice = p->act_choice;
     a.choice_out = choice_out;
     a.logp = logp;
     a.probs_out = probs_out;
     a.M = pl.M;
-    a.enc_in_smem = pl.enc_in_smem;
     a.Tpad = pl.Tpad;
     const int grid = ceil_div(K, pl.M);
     cudaStream_t st = (cudaStream_t)stream;
-    const void *fn = pl.MT == 1 ? (const void *)dec_kernel<1>
-                     : pl.MT == 2 ? (const void *)dec_kernel<2>
-                     : pl.MT == 4 ? (const void *)dec_kernel<4>
-                     : pl.MT == 8 ? (const void *)dec_kernel<8>
-                                  : (const void *)dec_kernel<16>;
+    const void *fn;
+    if (pl.enc_in_smem)
+        fn = pl.MT == 1 ? (const void *)dec_kernel<1, true>
+             : pl.MT == 2 ? (const void *)dec_kernel<2, true>
+             : pl.MT == 4 ? (const void *)dec_kernel<4, true>
+                          : (const void *)dec_kernel<8, true>;
+    else
+        fn = pl.MT == 1 ? (const void *)dec_kernel<1, false>
+             : pl.MT == 2 ? (const void *)dec_kernel<2, false>
+             : pl.MT == 4 ? (const void *)dec_kernel<4, false>
+                          : (const void *)dec_kernel<8, false>;
     DP_CUDA_TRY(allow_big_smem(fn, pl.smem));
     void *args[] = {&a};
     DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));
