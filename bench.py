@@ -196,12 +196,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DP_DIST_BACKEND=gloo exercises the multi-rank path with several ranks per GPU
+    backend = os.environ.get("DP_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     group = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
 
     import paper_1706_04972_b200 as dp
@@ -222,6 +228,12 @@ def main():
     def barrier():
         if world > 1:
             torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        dev = "cuda" if backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
 
     # ---- warm-up (first step eager: counts our launches; then graph capture) ----
     l0 = nat.lib().dp_launch_count()
@@ -259,9 +271,7 @@ def main():
     step_ms = [s.elapsed_time(e) for s, e in evs]
     tot_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
+        tot_ms = max_over_ranks(tot_ms)
     ms_per_step = tot_ms / args.steps
     value = K * args.steps / (tot_ms * 1e-3)
     ctl.check_errors()
@@ -308,9 +318,7 @@ def main():
         h_params.copy_(h_out)
     e2e_tot = sum(e2e_ms)
     if world > 1:
-        t = torch.tensor([e2e_tot], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_tot = float(t.item())
+        e2e_tot = max_over_ranks(e2e_tot)
     e2e_value = K * args.steps / (e2e_tot * 1e-3)
 
     if rank != 0:

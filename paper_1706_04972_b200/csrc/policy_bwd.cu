@@ -609,23 +609,40 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
 }
 
 // ------------------------------------------------------------------ reductions
-// dst[e] (+)= sum_c src[c * stride + e]: 4 interleaved accumulators (c mod 4),
-// combined in a fixed tree -> deterministic, latency-hidden.
-__global__ void reduce_partials_kernel(const double *__restrict__ src, int n_cta, size_t stride, int n,
-                                       double *__restrict__ dst, int accumulate) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n) return;
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    int c = 0;
-    for (; c + 4 <= n_cta; c += 4) {
-        v0 += src[(size_t)c * stride + e];
-        v1 += src[(size_t)(c + 1) * stride + e];
-        v2 += src[(size_t)(c + 2) * stride + e];
-        v3 += src[(size_t)(c + 3) * stride + e];
+// dst[e] (+)= sum_c src[c * stride + e].  Block = 32 elements x 8 c-slices:
+// thread (e, s) sums c = s, s+8, ... with 2 accumulators; the 8 slice sums are
+// combined in a fixed order -> deterministic, and 8x the memory parallelism
+// of a thread-per-element loop (the partials are latency-, not BW-bound).
+constexpr int kRedSlices = 8;
+
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double *__restrict__ src, int n_cta,
+                                                              size_t stride, int n, double *__restrict__ dst,
+                                                              int accumulate) {
+    __shared__ double part[kRedSlices][32];
+    const int el = threadIdx.x & 31, s = threadIdx.x >> 5;
+    const int e = blockIdx.x * 32 + el;
+    double v0 = 0.0, v1 = 0.0;
+    if (e < n) {
+        int c = s;
+        for (; c + kRedSlices < n_cta; c += 2 * kRedSlices) {
+            v0 += src[(size_t)c * stride + e];
+            v1 += src[(size_t)(c + kRedSlices) * stride + e];
+        }
+        if (c < n_cta) v0 += src[(size_t)c * stride + e];
     }
-    for (; c < n_cta; c++) v0 += src[(size_t)c * stride + e];
-    const double v = (v0 + v1) + (v2 + v3);
-    dst[e] = accumulate ? dst[e] + v : v;
+    part[s][el] = v0 + v1;
+    __syncthreads();
+    if (s == 0 && e < n) {
+        double v = part[0][el];
+#pragma unroll
+        for (int q = 1; q < kRedSlices; q++) v += part[q][el];
+        dst[e] = accumulate ? dst[e] + v : v;
+    }
+}
+
+inline void launch_reduce(const double *src, int n_cta, size_t stride, int n, double *dst, int accumulate,
+                          cudaStream_t st) {
+    reduce_partials_kernel<<<(n + 31) / 32, 256, 0, st>>>(src, n_cta, stride, n, dst, accumulate);
 }
 
 // B3 finalize: b_dec = sum_p DAsum[p]; w_dec[:dd] = sum_p dev_table[p] x DAsum[p];
@@ -776,13 +793,13 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
         DP_LAUNCH_CHECK();
         const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
         // [b_out | dev[:D] | w_out] are contiguous in neither layout -> three segments
-        reduce_partials_kernel<<<ceil_div(dm.D, 256), 256, 0, st>>>(part, n_used, na, dm.D, grad + dm.off.b_out, 0);
+        launch_reduce(part, n_used, na, dm.D, grad + dm.off.b_out, 0, st);
         DP_LAUNCH_CHECK();
-        reduce_partials_kernel<<<ceil_div(dm.D * dm.dd, 256), 256, 0, st>>>(part + dm.D, n_used, na, dm.D * dm.dd,
-                                                                            grad + dm.off.dev_table, 0);
+        launch_reduce(part + dm.D, n_used, na, dm.D * dm.dd,
+                                                                            grad + dm.off.dev_table, 0, st);
         DP_LAUNCH_CHECK();
-        reduce_partials_kernel<<<ceil_div(2 * kH * dm.dd, 256), 256, 0, st>>>(
-            part + dm.D + dm.D * dm.dd, n_used, na, 2 * kH * dm.dd, grad + dm.off.w_out, 0);
+        launch_reduce(
+            part + dm.D + dm.D * dm.dd, n_used, na, 2 * kH * dm.dd, grad + dm.off.w_out, 0, st);
         DP_LAUNCH_CHECK();
     }
     // B1
@@ -796,8 +813,8 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
         att_bwd_kernel<<<n_used, kThreads, smem, st>>>(dm, rows, tpc, p->enc_h, p->act_stat, p->row_q, p->row_dctx,
                                                        p->row_w, p->row_dq, part);
         DP_LAUNCH_CHECK();
-        reduce_partials_kernel<<<ceil_div(T * kH, 256), 256, 0, st>>>(part, n_used, (size_t)T * kH, T * kH,
-                                                                      p->d_enc, 0);
+        launch_reduce(part, n_used, (size_t)T * kH, T * kH,
+                                                                      p->d_enc, 0, st);
         DP_LAUNCH_CHECK();
     }
     // B1f
@@ -810,8 +827,8 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
         DP_CUDA_TRY(allow_big_smem((const void *)row_fin_kernel, smem));
         row_fin_kernel<<<n_used, kThreads, smem, st>>>(dm, params, rows, tpc, p->act_h, p->row_dq, p->row_dhx, part);
         DP_LAUNCH_CHECK();
-        reduce_partials_kernel<<<ceil_div(kH * kH, 256), 256, 0, st>>>(part, n_used, kH * kH, kH * kH,
-                                                                       grad + dm.off.w_att, 0);
+        launch_reduce(part, n_used, kH * kH, kH * kH,
+                                                                       grad + dm.off.w_att, 0, st);
         DP_LAUNCH_CHECK();
     }
     // B2: decoder LSTM backward, per sample
@@ -837,11 +854,11 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
                                                          part);
         DP_LAUNCH_CHECK();
         const size_t stride = (size_t)(kH + dm.D + 1) * kG;
-        reduce_partials_kernel<<<ceil_div(kH * kG, 256), 256, 0, st>>>(part, n_used, stride, kH * kG,
-                                                                       grad + dm.off.w_dec + (size_t)dm.dd * kG, 0);
+        launch_reduce(part, n_used, stride, kH * kG,
+                                                                       grad + dm.off.w_dec + (size_t)dm.dd * kG, 0, st);
         DP_LAUNCH_CHECK();
-        reduce_partials_kernel<<<ceil_div((dm.D + 1) * kG, 256), 256, 0, st>>>(
-            part + (size_t)kH * kG, n_used, stride, (dm.D + 1) * kG, p->gacc, 0);
+        launch_reduce(
+            part + (size_t)kH * kG, n_used, stride, (dm.D + 1) * kG, p->gacc, 0, st);
         DP_LAUNCH_CHECK();
         dec_finalize_kernel<<<1, kG, 0, st>>>(dm, params, p->gacc, grad);
         DP_LAUNCH_CHECK();

@@ -311,12 +311,13 @@ class DeviceController:
                                       "(SURVEY.md §8(f) row f2)")
         self.task, self.store, self.cid = task, store, controller_id
         self.device = store.device
+        from .parallel import Exchange, shard
+
         self.rank, self.size, self.group = world if world is not None else (0, 1, None)
         K = cfg.k
-        if K % self.size:
-            raise ValueError(f"k={K} must be divisible by the number of ranks {self.size}")
-        self.K, self.K_local = K, K // self.size
-        self.k_offset = self.rank * self.K_local
+        self.K = K
+        self.k_offset, self.K_local = shard(K, self.rank, self.size)
+        self.xchg = Exchange(self.group) if self.size > 1 else None
         tmpl = task.template
         self.eng = policy_mod.DevicePolicy(task.feats, tmpl.spec, tmpl.num_devices, tmpl.hidden, tmpl.dev_dim,
                                            k_max=self.K_local)
@@ -371,11 +372,10 @@ class DeviceController:
         if not self.measure_ok:
             fe.zero_()  # measure() raises for steps < 2 -> every worker reports INFEASIBLE
         if self.size > 1:
-            import torch.distributed as dist
-
-            dist.all_gather_into_tensor(self.mk_all, mk, group=self.group)
-            dist.all_gather_into_tensor(self.fe_all, fe, group=self.group)
-            dist.all_gather_into_tensor(self.ch_all, ch, group=self.group)
+            mark("exchange")
+            self.xchg.all_gather(self.mk_all, mk)
+            self.xchg.all_gather(self.fe_all, fe)
+            self.xchg.all_gather(self.ch_all, ch)
             mk, fe, ch = self.mk_all, self.fe_all, self.ch_all
         mark("epilogue")
         rc = nat.lib().dp_reinforce_epilogue(
@@ -387,10 +387,8 @@ class DeviceController:
         mark("backward")
         self.eng.backward(p, self.K_local, self.adv, grad=self.grad, stream=stream)
         if self.size > 1:
-            import torch.distributed as dist
-
             mark("allreduce")
-            dist.all_reduce(self.grad, group=self.group)
+            self.xchg.all_reduce_sum(self.grad)
         mark("adam")
         st.adam(self.grad, log=self.log, log_cap=self.log_cap, stream=stream)
         mark("end")
