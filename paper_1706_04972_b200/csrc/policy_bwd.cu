@@ -432,6 +432,9 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
 // gate activations / cells / incoming dh are prefetched into registers while
 // the current step's mat-vec runs.  In place: gate activations become da.
 constexpr int kMaxSeqPerCta = 8;
+constexpr int kDaLd = kH + 2;  // 528-byte gate blocks: LDS.128 of 4 parts -> distinct banks
+
+inline size_t lstm_bwd_smem(int M) { return sizeof(double) * (size_t)M * (2 * kH + 4 * kDaLd); }
 
 __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
     int T, int n_seq, int M, const double *__restrict__ Wh /* [64 x 256] row-major, ld 256 */,
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
     extern __shared__ __align__(16) double sm[];
     double *s_dh = sm;                   // [M][64]
     double *s_dc = s_dh + M * kH;        // [M][64]
-    double *s_da = s_dc + M * kH;        // [M][256]
+    double *s_da = s_dc + M * kH;        // [M][4 gates][kDaLd]: padded so the 4 parts of a warp hit distinct banks
     const int tid = threadIdx.x;
     const int q0 = blockIdx.x * M;
     const int Mb = min(M, n_seq - q0);
@@ -497,11 +500,11 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
                 const double da_f = df * fv * (1.0 - fv);
                 const double da_o = d_o * ov * (1.0 - ov);
                 const double da_g = dg * (1.0 - gv * gv);
-                double *sd = s_da + m * kG;
+                double *sd = s_da + m * 4 * kDaLd;
                 sd[u] = da_i;
-                sd[kH + u] = da_f;
-                sd[2 * kH + u] = da_o;
-                sd[3 * kH + u] = da_g;
+                sd[kDaLd + u] = da_f;
+                sd[2 * kDaLd + u] = da_o;
+                sd[3 * kDaLd + u] = da_g;
                 double *g = gates + ((size_t)(q0 + m) * T + t) * kG;
                 g[u] = da_i;
                 g[kH + u] = da_f;
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
         prefetch(t - 1);  // overlaps the barrier + mat-vec below
         __syncthreads();
         for (int m = 0; m < Mb; m++) {
-            const double2 *sd = reinterpret_cast<const double2 *>(s_da + m * kG + part * kH);
+            const double2 *sd = reinterpret_cast<const double2 *>(s_da + (m * 4 + part) * kDaLd);
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
             for (int i = 0; i < kH / 2; i += 2) {
@@ -835,7 +838,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     {
         int M = ceil_div(K, kNumSMs);
         if (M > kMaxSeqPerCta) M = kMaxSeqPerCta;
-        const size_t smem = sizeof(double) * (size_t)M * (2 * kH + kG);
+        const size_t smem = lstm_bwd_smem(M);
         DP_CUDA_TRY(allow_big_smem((const void *)lstm_bwd_kernel, smem));
         lstm_bwd_kernel<<<ceil_div(K, M), kThreads, smem, st>>>(
             T, K, M, params + dm.off.w_dec + (size_t)dm.dd * kG, p->act_g, p->act_c, p->enc_c + (size_t)(T - 1) * kH,
@@ -870,7 +873,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
         sum_rows_kernel<<<1, kH, 0, st>>>(p->dc0, K, dhc_sum + kH);
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, st));
-        const size_t smem = sizeof(double) * (2 * kH + kG);
+        const size_t smem = lstm_bwd_smem(1);
         lstm_bwd_kernel<<<1, kThreads, smem, st>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
                                                    p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
                                                    p->dh0, p->dc0);

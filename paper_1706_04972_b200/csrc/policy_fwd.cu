@@ -402,44 +402,41 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
         __syncthreads();
-        // ---- E: output layer, softmax over devices, draw (policy.py:301-308, 320-323) ----
-        for (int m = warp; m < Mb; m += kThreads / 32) {
-            const double *hv = hN + m * kH;
-            const double *cv = ctxS + m * kH;
-            const size_t row = (size_t)(k0 + m) * T + t;
-            double uo = 0.0;
-            if (dd <= 16) {
-                const int o = lane & 15, half = lane >> 4;
-                const double *src = half ? cv : hv;
-                double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-                if (o < dd) {
-#pragma unroll 4
-                    for (int i = 0; i < kH; i += 4) {
-                        p0 = fma(src[i], wout[(half * kH + i) * dd + o], p0);
-                        p1 = fma(src[i + 1], wout[(half * kH + i + 1) * dd + o], p1);
-                        p2 = fma(src[i + 2], wout[(half * kH + i + 2) * dd + o], p2);
-                        p3 = fma(src[i + 3], wout[(half * kH + i + 3) * dd + o], p3);
-                    }
-                }
-                const double part = (p0 + p1) + (p2 + p3);
-                uo = part + __shfl_xor_sync(0xffffffffu, part, 16);
-                if (half) uo = 0.0;
-            } else {
-                const int o = lane;
-                if (o < dd) {
+        // ---- E1: u = [h; ctx] @ W_out for all samples, 8 lanes per output ----
+        {
+            const int total = Mb * dd * 8;
+            for (int b0 = 0; b0 < total; b0 += kThreads) {
+                const int idx = b0 + tid;
+                const bool ok = idx < total;
+                double part = 0.0;
+                int m = 0, o = 0;
+                if (ok) {
+                    const int pair = idx >> 3, pp = idx & 7;
+                    m = pair / dd;
+                    o = pair - m * dd;
+                    const double *src = (pp < 4 ? hN + m * kH : ctxS + m * kH) + (pp & 3) * 16;
+                    const double *wc = wout + (size_t)(pp * 16) * dd + o;
                     double p0 = 0.0, p1 = 0.0;
-                    for (int i = 0; i < kH; i++) {
-                        p0 = fma(hv[i], wout[i * dd + o], p0);
-                        p1 = fma(cv[i], wout[(kH + i) * dd + o], p1);
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        p0 = fma(src[i], wc[i * dd], p0);
+                        p1 = fma(src[i + 1], wc[(i + 1) * dd], p1);
                     }
-                    uo = p0 + p1;
+                    part = p0 + p1;
+                }
+                part += __shfl_xor_sync(0xffffffffu, part, 4);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                if (ok && (idx & 7) == 0) {
+                    uS[m * 32 + o] = part;
+                    a.act_u[((size_t)(k0 + m) * T + t) * dd + o] = part;
                 }
             }
-            if (lane < dd) {
-                uS[m * 32 + lane] = uo;
-                a.act_u[row * dd + lane] = uo;
-            }
-            __syncwarp();
+        }
+        __syncthreads();
+        // ---- E2: logits, softmax over devices, draw (policy.py:301-308, 320-323) ----
+        for (int m = warp; m < Mb; m += kThreads / 32) {
+            const size_t row = (size_t)(k0 + m) * T + t;
             double z = -INFINITY;
             if (lane < D) {
                 double z0 = 0.0, z1 = 0.0;

@@ -34,6 +34,15 @@ __device__ __forceinline__ bool key_less(double ta, int ra, double tb, int rb) {
     return ta < tb || (ta == tb && ra < rb);
 }
 
+// Bytes of the graph image staged in shared memory (GS=true).
+__host__ __device__ inline size_t graph_smem_bytes(int n, int d, int e) {
+    size_t b = 8 * ((size_t)n * d + e + (size_t)d * d) + 4 * (size_t)(n + 1) + 2 * ((size_t)e + 2 * n);
+    return (b + 15) & ~(size_t)15;
+}
+
+// GS: stage the graph (durations, CSR, bytes, bandwidths) in shared memory
+// once per CTA — every event's lookups become LDS instead of L2 round trips.
+template <bool GS>
 __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8_t *__restrict__ placement,
                                                   int by_rank, double *__restrict__ makespan,
                                                   double *__restrict__ busy_out, double *__restrict__ transfer_out,
@@ -42,12 +51,49 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     extern __shared__ __align__(16) unsigned char smem[];
     const int s = threadIdx.x;
     const int k = blockIdx.x * S + s;
-    if (s >= S || k >= K) return;
     const int n = g.n, D = g.d;
+    size_t gbytes = 0;
+    const double *g_dur = g.dur, *g_bytes = g.out_bytes, *g_bw = g.bw;
+    const int32_t *g_off = g.out_off;
+    const int32_t *g_dst32 = g.out_dst, *g_gid32 = g.gid, *g_indeg32 = g.indeg;
+    const uint16_t *g_dst16 = nullptr, *g_gid16 = nullptr, *g_indeg16 = nullptr;
+    if (GS) {
+        double *sdur = reinterpret_cast<double *>(smem);
+        double *sbytes = sdur + (size_t)n * D;
+        double *sbw = sbytes + g.e;
+        int32_t *soff = reinterpret_cast<int32_t *>(sbw + D * D);
+        uint16_t *sdst = reinterpret_cast<uint16_t *>(soff + n + 1);
+        uint16_t *sgid = sdst + g.e;
+        uint16_t *sind = sgid + n;
+        for (int i = s; i < n * D; i += blockDim.x) sdur[i] = g.dur[i];
+        for (int i = s; i < g.e; i += blockDim.x) {
+            sbytes[i] = g.out_bytes[i];
+            sdst[i] = (uint16_t)g.out_dst[i];
+        }
+        for (int i = s; i < D * D; i += blockDim.x) sbw[i] = g.bw[i];
+        for (int i = s; i <= n; i += blockDim.x) soff[i] = g.out_off[i];
+        for (int i = s; i < n; i += blockDim.x) {
+            sgid[i] = (uint16_t)g.gid[i];
+            sind[i] = (uint16_t)g.indeg[i];
+        }
+        __syncthreads();
+        g_dur = sdur;
+        g_bytes = sbytes;
+        g_bw = sbw;
+        g_off = soff;
+        g_dst16 = sdst;
+        g_gid16 = sgid;
+        g_indeg16 = sind;
+        gbytes = graph_smem_bytes(n, D, g.e);
+    }
+    auto dst_of = [&](int e) -> int { return GS ? (int)g_dst16[e] : g_dst32[e]; };
+    auto gid_of = [&](int r) -> int { return GS ? (int)g_gid16[r] : g_gid32[r]; };
+    auto indeg_of = [&](int r) -> int { return GS ? (int)g_indeg16[r] : g_indeg32[r]; };
+    if (s >= S || k >= K) return;
     const SimSlot q{S, s};
 
     // ---- shared-memory carve-up (all arrays slot-interleaved: [i*S + s]) ----
-    double *maxarr = reinterpret_cast<double *>(smem);  // [n]  READY time (max arrival)
+    double *maxarr = reinterpret_cast<double *>(smem + gbytes);  // [n]  READY time (max arrival)
     double *fin_t = maxarr + (size_t)n * S;              // [D]  pending FINISH time per device
     double *link = fin_t + (size_t)D * S;                // [D*D] link_free
     double *busy = link + (size_t)D * D * S;             // [D]
@@ -65,7 +111,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     const uint8_t *src = placement + (size_t)k * n;
     bool bad = false;
     for (int r = 0; r < n; r++) {
-        const uint8_t v = by_rank ? src[r] : src[g.gid[r]];
+        const uint8_t v = by_rank ? src[r] : src[gid_of(r)];
         bad |= (v >= D);
         pl[q.at(r)] = v;
     }
@@ -95,7 +141,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
         const int dv = pl[q.at(r)];
         qtail[q.at(dv)] += 1;
         peak[q.at(dv)] += (long long)g.resident[r];
-        left[q.at(r)] = (uint16_t)g.indeg[r];
+        left[q.at(r)] = (uint16_t)indeg_of(r);
         maxarr[q.at(r)] = 0.0;
     }
     {
@@ -109,7 +155,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     }
     // sources enter their device queue at t=0 in rank order (pkg/simulator.py:154-156)
     for (int r = 0; r < n; r++) {
-        if (g.indeg[r] == 0) {
+        if (indeg_of(r) == 0) {
             const int dv = pl[q.at(r)];
             const int pos = qtail[q.at(dv)];
             devq[q.at(pos)] = (uint16_t)r;
@@ -127,11 +173,11 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
         if (h >= qtail[q.at(dv)]) return;
         const int r = devq[q.at(h)];
         qhead[q.at(dv)] = (uint16_t)(h + 1);
-        const double dur = g.dur[(size_t)r * D + dv];
+        const double dur = g_dur[(size_t)r * D + dv];
         busy[q.at(dv)] += dur;
         fin_t[q.at(dv)] = now + dur;
         fin_r[q.at(dv)] = r;
-        if (ord) ord[n_order++] = g.gid[r];
+        if (ord) ord[n_order++] = gid_of(r);
     };
     for (int j = 0; j < D; j++) start_next(j, 0.0);
 
@@ -162,11 +208,11 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
             // ---- FINISH (pkg/simulator.py:162-178) ----
             fin_r[q.at(bd)] = -1;
             mk = bt > mk ? bt : mk;
-            const int e0 = g.out_off[br], e1 = g.out_off[br + 1];
+            const int e0 = g_off[br], e1 = g_off[br + 1];
             for (int e = e0; e < e1; e++) {
-                const int dst = g.out_dst[e];
+                const int dst = dst_of(e);
                 const int ddev = pl[q.at(dst)];
-                const double nbytes = g.out_bytes[e];
+                const double nbytes = g_bytes[e];
                 double arrive;
                 if (ddev == bd || nbytes == 0.0) {
                     arrive = bt;
@@ -174,7 +220,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
                     const int li = bd * D + ddev;
                     const double lf = link[q.at(li)];
                     const double begin = lf > bt ? lf : bt;
-                    const double dur = nbytes / g.bw[li];
+                    const double dur = nbytes / g_bw[li];
                     const double end = begin + dur;
                     link[q.at(li)] = end;
                     trans[q.at(bd)] += dur;
@@ -345,7 +391,10 @@ extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *pl
     DP_REQUIRE(K >= 0, "dp_simulate_batch: K < 0");
     if (K == 0) return DP_OK;
     const size_t per = g->sim_smem_per_placement;
-    int s_max = (int)(kSmemBudget / per);
+    const size_t gb = graph_smem_bytes(g->n, g->d, g->e);
+    // stage the graph in shared memory when it leaves room for the placements
+    const bool gs = gb <= kSmemBudget / 2 && (kSmemBudget - gb) / per >= 1;
+    int s_max = (int)((kSmemBudget - (gs ? gb : 0)) / per);
     if (s_max > 128) s_max = 128;
     DP_REQUIRE(s_max >= 1, "dp_simulate_batch: graph too large for the shared-memory simulator");
     // spread small batches over all SMs; pack large ones
@@ -353,11 +402,16 @@ extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *pl
     if (S > s_max) S = s_max;
     if (S < 1) S = 1;
     const int grid = dp::ceil_div(K, S);
-    const size_t smem = per * S + 16;
-    if (smem > 48 * 1024) DP_CUDA_TRY(dp::allow_big_smem((const void *)sim_kernel, kSmemBudget + 1024));
+    const size_t smem = per * S + (gs ? gb : 0) + 16;
+    const void *fn = gs ? (const void *)sim_kernel<true> : (const void *)sim_kernel<false>;
+    if (smem > 48 * 1024) DP_CUDA_TRY(dp::allow_big_smem(fn, smem));
     const int threads = ((S + 31) / 32) * 32;
-    sim_kernel<<<grid, threads, smem, (cudaStream_t)stream>>>(*g, K, placement, by_rank, makespan, busy,
-                                                              transfer, peak, feasible, order, err, S);
+    if (gs)
+        sim_kernel<true><<<grid, threads, smem, (cudaStream_t)stream>>>(*g, K, placement, by_rank, makespan, busy,
+                                                                        transfer, peak, feasible, order, err, S);
+    else
+        sim_kernel<false><<<grid, threads, smem, (cudaStream_t)stream>>>(*g, K, placement, by_rank, makespan, busy,
+                                                                         transfer, peak, feasible, order, err, S);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
