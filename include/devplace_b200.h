@@ -112,6 +112,10 @@ int64_t dp_policy_num_params(const dp_policy *p);
  * Runs once per snapshot; all decode calls reuse it. */
 int dp_policy_encode(dp_policy *p, const double *params, void *stream);
 
+/* Debug instrumentation: enable/disable per-phase cycle counters in the
+ * decoder (block 0) and read+reset the 8 sums into h_out[8] (may be NULL). */
+int dp_debug_phase_clocks(int32_t enable, int64_t *h_out);
+
 /* Copy the assembled encoder inputs of the last encode (embed_groups(),
  * pkg/policy.py:266-268) into out[T*input_dim] (device). */
 int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream);

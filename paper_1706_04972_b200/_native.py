@@ -33,6 +33,7 @@ SIGNATURES = {
     "dp_policy_num_params": (I64, [P]),
     "dp_policy_encode": (I32, [P, P, P]),
     "dp_policy_read_inputs": (I32, [P, P, P]),
+    "dp_debug_phase_clocks": (I32, [I32, P]),
     "dp_policy_decode": (I32, [P, P, I32, I64, P, U64, P, I64, P, P, P, P, P]),
     "dp_policy_backward": (I32, [P, P, I32, P, P, P]),
     "dp_reinforce_epilogue": (I32, [I32, I32, P, P, P, F64, F64, I64, I64, I32, P, P, P, P, I64, I32, P]),

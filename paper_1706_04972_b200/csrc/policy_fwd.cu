@@ -36,6 +36,10 @@ namespace dp {
 
 __device__ __forceinline__ double sigmoid_ref(double x) { return 1.0 / (1.0 + exp(-x)); }
 
+// Debug-only per-phase cycle counters of the decoder (block 0, thread 0).
+__device__ int g_dbg_clocks = 0;
+__device__ long long g_phase_clk[16];
+
 // numpy pairwise_sum order for n <= 128 (np.add.reduce on a contiguous array):
 // n < 8 sequential; otherwise 8 interleaved accumulators, fixed tree, tail.
 __device__ __forceinline__ double np_sum_small(const double *a, int n) {
@@ -173,6 +177,7 @@ struct DecArgs {
 };
 
 constexpr int kCtxParts = 8;
+constexpr int kWoutLd = 2 * kH + 8;  // W_out^T row stride in shared memory (== 8 mod 16 doubles)
 
 // One CTA owns M samples for all T decode steps.  Per step:
 //   A  gates = edev[prev] + h.W_h (thread per gate column, W_h in registers),
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     if (ES)
         for (int i = tid; i < T * kH; i += kThreads) sm[a.o_enc + (i >> 6) * kEncLd + (i & 63)] = a.enc_h[i];
     for (int i = tid; i < kH * kH; i += kThreads) watt[i] = P[dm.off.w_att + i];
-    for (int i = tid; i < 2 * kH * dd; i += kThreads) wout[i] = P[dm.off.w_out + i];
+    for (int i = tid; i < 2 * kH * dd; i += kThreads) wout[(i % dd) * kWoutLd + i / dd] = P[dm.off.w_out + i];
     for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
     for (int i = tid; i < D; i += kThreads) bout[i] = P[dm.off.b_out + i];
     for (int i = tid; i < (D + 1) * kG; i += kThreads) edev[i] = a.edev[i];
@@ -245,6 +250,15 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 
     const int base = lane & ~3;
     const int Tp = (T + kCtxParts - 1) / kCtxParts;
+    // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
+    const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
+    long long clk_last = clk_on ? clock64() : 0;
+#define DP_PHASE(i)                                       \
+    if (clk_on) {                                         \
+        const long long now_ = clock64();                 \
+        g_phase_clk[i] += now_ - clk_last;                \
+        clk_last = now_;                                  \
+    }
     for (int t = 0; t < T; t++) {
         const int cur = t & 1;
         // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
@@ -275,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             }
         }
         __syncthreads();
+        DP_PHASE(0);
         const double *hN = hS + (cur ^ 1) * M * kH;
         // ---- B: q = W_att^T h ----
         for (int idx = tid; idx < Mb * kH; idx += kThreads) {
@@ -292,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             qS[idx] = (q0 + q1) + (q2 + q3);
         }
         __syncthreads();
+        DP_PHASE(1);
         // ---- C: scores s_i = enc_i . q, softmax over T (policy.py:296-299) ----
         double mx[MT];
 #pragma unroll
@@ -327,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             if (lane == 0) red[warp * MT + m] = v;
         }
         __syncthreads();
+        DP_PHASE(2);
         double gmax[MT], sm_[MT];
 #pragma unroll
         for (int m = 0; m < MT; m++) {
@@ -353,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             if (lane == 0) red[8 * MT + warp * MT + m] = v;
         }
         __syncthreads();
+        DP_PHASE(3);
         // ---- D: ctx = alpha @ enc (policy.py:300), alpha = e / sum ----
         {
             const int jp = tid & 31, part = tid >> 5;
@@ -375,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     *reinterpret_cast<double2 *>(red2 + (part * M + m) * kH + 2 * jp) = make_double2(ax[m], ay[m]);
         }
         __syncthreads();
+        DP_PHASE(4);
         for (int idx = tid; idx < Mb * kH; idx += kThreads) {
             const int m = idx >> 6, j = idx & 63;
             double gs = red[8 * MT + m];
@@ -402,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
         __syncthreads();
+        DP_PHASE(5);
         // ---- E1: u = [h; ctx] @ W_out for all samples, 8 lanes per output ----
         {
             const int total = Mb * dd * 8;
@@ -411,16 +431,18 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 double part = 0.0;
                 int m = 0, o = 0;
                 if (ok) {
+                    // lane part pp sums i = pp + 8i' over [h; ctx]; W_out^T rows of
+                    // kWoutLd (== 8 mod 16) doubles -> conflict-free half-warps
                     const int pair = idx >> 3, pp = idx & 7;
                     m = pair / dd;
                     o = pair - m * dd;
-                    const double *src = (pp < 4 ? hN + m * kH : ctxS + m * kH) + (pp & 3) * 16;
-                    const double *wc = wout + (size_t)(pp * 16) * dd + o;
+                    const double *hv = hN + m * kH + pp, *cv = ctxS + m * kH + pp;
+                    const double *wc = wout + o * kWoutLd + pp;
                     double p0 = 0.0, p1 = 0.0;
 #pragma unroll
-                    for (int i = 0; i < 16; i += 2) {
-                        p0 = fma(src[i], wc[i * dd], p0);
-                        p1 = fma(src[i + 1], wc[(i + 1) * dd], p1);
+                    for (int i = 0; i < 8; i++) {
+                        p0 = fma(hv[8 * i], wc[8 * i], p0);
+                        p1 = fma(cv[8 * i], wc[kH + 8 * i], p1);
                     }
                     part = p0 + p1;
                 }
@@ -434,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             }
         }
         __syncthreads();
+        DP_PHASE(6);
         // ---- E2: logits, softmax over devices, draw (policy.py:301-308, 320-323) ----
         for (int m = warp; m < Mb; m += kThreads / 32) {
             const size_t row = (size_t)(k0 + m) * T + t;
@@ -495,7 +518,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             }
         }
         __syncthreads();
+        DP_PHASE(7);
     }
+#undef DP_PHASE
     // ---- log p = sum_t (zs[c_t] - log sum_t): logs in parallel, sum in t order ----
     __threadfence_block();
     for (int m = 0; m < Mb; m++) {
@@ -661,6 +686,18 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
 
 extern "C" int64_t dp_policy_num_params(const dp_policy *p) { return p ? p->dims.off.total : -1; }
 
+// Debug: enable (1) / disable (0) decoder phase clocks, then read and reset
+// the 8 per-phase cycle sums (block 0) into h_out[8].  Synchronous.
+extern "C" int dp_debug_phase_clocks(int32_t enable, int64_t *h_out) {
+    DP_ENTRY();
+    const int on = enable ? 1 : 0;
+    DP_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_clocks, &on, sizeof(int)));
+    if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_phase_clk, sizeof(long long) * 8));
+    long long z[16] = {0};
+    DP_CUDA_TRY(cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z)));
+    return DP_OK;
+}
+
 extern "C" int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream) {
     DP_ENTRY();
     DP_REQUIRE(p && out, "dp_policy_read_inputs: NULL argument");
@@ -715,7 +752,7 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
             };
             a.o_enc = enc_smem ? take(T * kEncLd) : 0;
             a.o_watt = take(kH * kH);
-            a.o_wout = take(2 * kH * dm.dd);
+            a.o_wout = take(kWoutLd * dm.dd);
             a.o_devt = take(dm.D * dm.dd);
             a.o_bout = take(dm.D);
             a.o_edev = take((dm.D + 1) * kG);
