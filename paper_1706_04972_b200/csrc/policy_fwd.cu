@@ -176,39 +176,20 @@ struct DecArgs {
         o_red2, o_pcg, o_misc;
 };
 
-constexpr int kDecThreads = 512;                // 16 warps: 2 threads per gate column
-constexpr int kDecWarps = kDecThreads / 32;
-constexpr int kCtxParts = kDecWarps;            // row parts of the context reduction
-constexpr int kWoutLd = 2 * kH + 8;             // W_out^T row stride in shared memory
+constexpr int kCtxParts = 8;
+constexpr int kWoutLd = 2 * kH + 8;  // W_out^T row stride in shared memory (== 8 mod 16 doubles)
 
-// 32-term dot: shared-memory vector (broadcast, 16-byte loads) x register column half
-__device__ __forceinline__ double dot32_sh_reg(const double *__restrict__ hs, const double (&w)[kH / 2]) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll
-    for (int k = 0; k < kH / 2; k += 4) {
-        const double2 h01 = *reinterpret_cast<const double2 *>(hs + k);
-        const double2 h23 = *reinterpret_cast<const double2 *>(hs + k + 2);
-        a0 = fma(h01.x, w[k], a0);
-        a1 = fma(h01.y, w[k + 1], a1);
-        a2 = fma(h23.x, w[k + 2], a2);
-        a3 = fma(h23.y, w[k + 3], a3);
-    }
-    return (a0 + a1) + (a2 + a3);
-}
-
-// One CTA (512 threads) owns M samples for all T decode steps.  Per step:
-//   A  gates = edev[prev] + h.W_h: thread (u, gate, half) holds half a gate
-//      column of W_h (32 doubles) in registers; halves combine by shuffle;
-//      LSTM cell; h/c/gates to the activation store
-//   B  q = W_att^T h (4 lanes per output)
-//   C  s_i = enc_i . q (2 lanes per row), softmax over T (block max, block sum)
-//   D  ctx = (sum_i e_i enc_i) / sum (lane pairs over j, 16 row-parts)
-//   E1 u = [h; ctx] W_out (16 lanes per output)
-//   E2 warp per sample: z = dev_table[:D] u + b_out, p = softmax(z), PCG64
-//      draw, cdf search -> choice; the log-prob term's log() is deferred to
-//      the end of the kernel (off the per-step path)
+// One CTA owns M samples for all T decode steps.  Per step:
+//   A  gates = edev[prev] + h.W_h (thread per gate column, W_h in registers),
+//      LSTM cell, h/c/gates to the activation store
+//   B  q = W_att^T h
+//   C  s_i = enc_i . q (row per thread), softmax over T (block max, block sum)
+//   D  ctx = (sum_i e_i enc_i) / sum  (lane pairs over j, 8 row-parts)
+//   E  warp per sample: u = [h; ctx] W_out, z = dev_table[:D] u + b_out,
+//      p = softmax(z), PCG64 draw, cdf search -> choice; the log-prob term's
+//      log() is deferred to the end of the kernel (off the per-step path)
 template <int MT, bool ES>
-__global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const PolicyDims &dm = a.dm;
@@ -219,7 +200,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
     constexpr int LD = ES ? kEncLd : kH;
     const double *enc = ES ? (const double *)(sm + a.o_enc) : a.enc_h;
     double *watt = sm + a.o_watt;
-    double *wout = sm + a.o_wout;   // W_out^T [o][kWoutLd]
+    double *wout = sm + a.o_wout;
     double *devt = sm + a.o_devt;
     double *bout = sm + a.o_bout;
     double *edev = sm + a.o_edev;
@@ -230,20 +211,20 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
     double *uS = sm + a.o_u;       // [M][32]
     double *pS = sm + a.o_p;       // [M][32]
     double *alS = sm + a.o_alpha;  // [M][Tpad] unnormalised e_i
-    double *red = sm + a.o_red;    // [2][16][MT]
-    double *red2 = sm + a.o_red2;  // [16 parts][M][64]
+    double *red = sm + a.o_red;    // [2][8][MT]
+    double *red2 = sm + a.o_red2;  // [8 parts][M][64]
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);                               // [M]
 
     // ---- stage weights ----
     if (ES)
-        for (int i = tid; i < T * kH; i += kDecThreads) sm[a.o_enc + (i >> 6) * kEncLd + (i & 63)] = a.enc_h[i];
-    for (int i = tid; i < kH * kH; i += kDecThreads) watt[i] = P[dm.off.w_att + i];
-    for (int i = tid; i < 2 * kH * dd; i += kDecThreads) wout[(i % dd) * kWoutLd + i / dd] = P[dm.off.w_out + i];
-    for (int i = tid; i < D * dd; i += kDecThreads) devt[i] = P[dm.off.dev_table + i];
-    for (int i = tid; i < D; i += kDecThreads) bout[i] = P[dm.off.b_out + i];
-    for (int i = tid; i < (D + 1) * kG; i += kDecThreads) edev[i] = a.edev[i];
-    for (int i = tid; i < Mb * kH; i += kDecThreads) {
+        for (int i = tid; i < T * kH; i += kThreads) sm[a.o_enc + (i >> 6) * kEncLd + (i & 63)] = a.enc_h[i];
+    for (int i = tid; i < kH * kH; i += kThreads) watt[i] = P[dm.off.w_att + i];
+    for (int i = tid; i < 2 * kH * dd; i += kThreads) wout[(i % dd) * kWoutLd + i / dd] = P[dm.off.w_out + i];
+    for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
+    for (int i = tid; i < D; i += kThreads) bout[i] = P[dm.off.b_out + i];
+    for (int i = tid; i < (D + 1) * kG; i += kThreads) edev[i] = a.edev[i];
+    for (int i = tid; i < Mb * kH; i += kThreads) {
         hS[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
         cS[i] = a.enc_c[(size_t)(T - 1) * kH + (i & 63)];
     }
@@ -258,16 +239,16 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
             pcg[2 * tid + 1] = s.lo;
         }
     }
-    const int u = tid >> 3, sub = tid & 7, gate = sub >> 1, half = sub & 1, col = gate * kH + u;
-    double w[kH / 2];
+    const int u = tid >> 2, gate = tid & 3, col = gate * kH + u;
+    double w[kH];
     {
-        const double *Wh = P + dm.off.w_dec + (size_t)(dd + half * (kH / 2)) * kG;
+        const double *Wh = P + dm.off.w_dec + (size_t)dd * kG;
 #pragma unroll
-        for (int k = 0; k < kH / 2; k++) w[k] = Wh[(size_t)k * kG + col];
+        for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
     }
     __syncthreads();
 
-    const int base = lane & ~7;
+    const int base = lane & ~3;
     const int Tp = (T + kCtxParts - 1) / kCtxParts;
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
     const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
@@ -284,24 +265,19 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
         {
             double av[MT];
 #pragma unroll
-            for (int m = 0; m < MT; m++) {
-                if (m < Mb) {
-                    const double p = dot32_sh_reg(hS + (cur * M + m) * kH + half * (kH / 2), w);
-                    const double o = __shfl_xor_sync(0xffffffffu, p, 1);
-                    av[m] = edev[prev[m] * kG + col] + (half ? o + p : p + o);
-                }
-            }
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) av[m] = edev[prev[m] * kG + col] + dot64_sh_reg(hS + (cur * M + m) * kH, w);
 #pragma unroll
             for (int m = 0; m < MT; m++) {
                 if (m < Mb) {
                     const double act = gate == 3 ? tanh(av[m]) : sigmoid_ref(av[m]);
                     const size_t row = (size_t)(k0 + m) * T + t;
-                    if (!half) a.act_g[row * kG + col] = act;
+                    a.act_g[row * kG + col] = act;
                     const double iv = __shfl_sync(0xffffffffu, act, base + 0);
-                    const double fv = __shfl_sync(0xffffffffu, act, base + 2);
-                    const double ov = __shfl_sync(0xffffffffu, act, base + 4);
-                    const double gv = __shfl_sync(0xffffffffu, act, base + 6);
-                    if (sub == 0) {
+                    const double fv = __shfl_sync(0xffffffffu, act, base + 1);
+                    const double ov = __shfl_sync(0xffffffffu, act, base + 2);
+                    const double gv = __shfl_sync(0xffffffffu, act, base + 3);
+                    if (gate == 0) {
                         const double cn = fv * cS[m * kH + u] + iv * gv;
                         const double hn = ov * tanh(cn);
                         cS[m * kH + u] = cn;
@@ -315,59 +291,47 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
         __syncthreads();
         DP_PHASE(0);
         const double *hN = hS + (cur ^ 1) * M * kH;
-        // ---- B: q = W_att^T h (4 lanes per output, 16 rows each) ----
-        for (int b0 = 0; b0 < Mb * kH * 4; b0 += kDecThreads) {
-            const int idx = b0 + tid;
-            double q = 0.0;
-            if (idx < Mb * kH * 4) {
-                const int o = idx >> 2, pp = idx & 3, m = o >> 6, j = o & 63;
-                const double2 *hv = reinterpret_cast<const double2 *>(hN + m * kH + pp * 16);
-                double q0 = 0.0, q1 = 0.0;
+        // ---- B: q = W_att^T h ----
+        for (int idx = tid; idx < Mb * kH; idx += kThreads) {
+            const int m = idx >> 6, j = idx & 63;
+            const double2 *hv = reinterpret_cast<const double2 *>(hN + m * kH);
+            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
 #pragma unroll
-                for (int l2 = 0; l2 < 8; l2++) {
-                    const double2 hh = hv[l2];
-                    q0 = fma(watt[(pp * 16 + 2 * l2) * kH + j], hh.x, q0);
-                    q1 = fma(watt[(pp * 16 + 2 * l2 + 1) * kH + j], hh.y, q1);
-                }
-                q = q0 + q1;
+            for (int l2 = 0; l2 < kH / 2; l2 += 2) {
+                const double2 h0 = hv[l2], h1 = hv[l2 + 1];
+                q0 = fma(watt[(2 * l2) * kH + j], h0.x, q0);
+                q1 = fma(watt[(2 * l2 + 1) * kH + j], h0.y, q1);
+                q2 = fma(watt[(2 * l2 + 2) * kH + j], h1.x, q2);
+                q3 = fma(watt[(2 * l2 + 3) * kH + j], h1.y, q3);
             }
-            q += __shfl_xor_sync(0xffffffffu, q, 1);
-            q += __shfl_xor_sync(0xffffffffu, q, 2);
-            if (idx < Mb * kH * 4 && (idx & 3) == 0) qS[idx >> 2] = q;
+            qS[idx] = (q0 + q1) + (q2 + q3);
         }
         __syncthreads();
         DP_PHASE(1);
-        // ---- C: scores s_i = enc_i . q (2 lanes per row), softmax over T (policy.py:296-299) ----
+        // ---- C: scores s_i = enc_i . q, softmax over T (policy.py:296-299) ----
         double mx[MT];
 #pragma unroll
         for (int m = 0; m < MT; m++) mx[m] = -INFINITY;
-        const int jh = tid & 1;
-        for (int i0 = 0; i0 < T; i0 += kDecThreads / 2) {
-            const int i = i0 + (tid >> 1);
-            const bool ok = i < T;
+        for (int i = tid; i < T; i += kThreads) {
+            const double2 *er = reinterpret_cast<const double2 *>(enc + (size_t)i * LD);
             double s0[MT], s1[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++) s0[m] = s1[m] = 0.0;
-            if (ok) {
-                const double2 *er = reinterpret_cast<const double2 *>(enc + (size_t)i * LD + jh * 32);
+#pragma unroll 8
+            for (int j2 = 0; j2 < kH / 2; j2++) {
+                const double2 e = er[j2];
 #pragma unroll
-                for (int j2 = 0; j2 < 16; j2++) {
-                    const double2 e = er[j2];
-#pragma unroll
-                    for (int m = 0; m < MT; m++) {
-                        const double2 qq = reinterpret_cast<const double2 *>(qS + m * kH + jh * 32)[j2];
-                        s0[m] = fma(e.x, qq.x, s0[m]);
-                        s1[m] = fma(e.y, qq.y, s1[m]);
-                    }
+                for (int m = 0; m < MT; m++) {
+                    const double2 qq = reinterpret_cast<const double2 *>(qS + m * kH)[j2];
+                    s0[m] = fma(e.x, qq.x, s0[m]);
+                    s1[m] = fma(e.y, qq.y, s1[m]);
                 }
             }
 #pragma unroll
             for (int m = 0; m < MT; m++) {
-                const double p = s0[m] + s1[m];
-                const double o = __shfl_xor_sync(0xffffffffu, p, 1);
-                const double s = jh ? o + p : p + o;
-                if (ok && m < Mb) {
-                    if (!jh) alS[m * a.Tpad + i] = s;
+                if (m < Mb) {
+                    const double s = s0[m] + s1[m];
+                    alS[m * a.Tpad + i] = s;
                     mx[m] = fmax(mx[m], s);
                 }
             }
@@ -385,11 +349,11 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
         for (int m = 0; m < MT; m++) {
             double v = red[m];
 #pragma unroll
-            for (int ww = 1; ww < kDecWarps; ww++) v = fmax(v, red[ww * MT + m]);
+            for (int ww = 1; ww < kThreads / 32; ww++) v = fmax(v, red[ww * MT + m]);
             gmax[m] = v;
             sm_[m] = 0.0;
         }
-        for (int i = tid; i < T; i += kDecThreads) {
+        for (int i = tid; i < T; i += kThreads) {
 #pragma unroll
             for (int m = 0; m < MT; m++) {
                 if (m < Mb) {
@@ -403,7 +367,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
         for (int m = 0; m < MT; m++) {
             double v = sm_[m];
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) red[kDecWarps * MT + warp * MT + m] = v;
+            if (lane == 0) red[8 * MT + warp * MT + m] = v;
         }
         __syncthreads();
         DP_PHASE(3);
@@ -430,64 +394,71 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
         }
         __syncthreads();
         DP_PHASE(4);
-        for (int idx = tid; idx < Mb * kH; idx += kDecThreads) {
+        for (int idx = tid; idx < Mb * kH; idx += kThreads) {
             const int m = idx >> 6, j = idx & 63;
-            double gs = red[kDecWarps * MT + m];
+            double gs = red[8 * MT + m];
 #pragma unroll
-            for (int ww = 1; ww < kDecWarps; ww++) gs += red[kDecWarps * MT + ww * MT + m];
-            double v0 = red2[m * kH + j], v1 = red2[(M + m) * kH + j];
+            for (int ww = 1; ww < kThreads / 32; ww++) gs += red[8 * MT + ww * MT + m];
+            double v = red2[m * kH + j];
 #pragma unroll
-            for (int p = 2; p < kCtxParts; p += 2) {
-                v0 += red2[(p * M + m) * kH + j];
-                v1 += red2[((p + 1) * M + m) * kH + j];
-            }
-            const double v = (v0 + v1) / gs;
+            for (int p = 1; p < kCtxParts; p++) v += red2[(p * M + m) * kH + j];
+            v = v / gs;
             ctxS[idx] = v;
             const size_t row = (size_t)(k0 + m) * T + t;
             a.act_ctx[row * kH + j] = v;
-            if (j == 0) {
-                // softmax stats for the backward's recompute of alpha
+        }
+        if (tid < Mb) {
+            // softmax stats for the backward's recompute of alpha
+            const size_t row = (size_t)(k0 + tid) * T + t;
 #pragma unroll
-                for (int mm = 0; mm < MT; mm++)
-                    if (mm == m) a.act_stat[row * 2] = gmax[mm];
-                a.act_stat[row * 2 + 1] = gs;
-            }
+            for (int m = 0; m < MT; m++)
+                if (m == tid) {
+                    double gs = red[8 * MT + m];
+#pragma unroll
+                    for (int ww = 1; ww < kThreads / 32; ww++) gs += red[8 * MT + ww * MT + m];
+                    a.act_stat[row * 2] = gmax[m];
+                    a.act_stat[row * 2 + 1] = gs;
+                }
         }
         __syncthreads();
         DP_PHASE(5);
-        // ---- E1: u = [h; ctx] @ W_out, 16 lanes per output (i = pp + 16i') ----
-        for (int b0 = 0; b0 < Mb * dd * 16; b0 += kDecThreads) {
-            const int idx = b0 + tid;
-            const bool ok = idx < Mb * dd * 16;
-            double part = 0.0;
-            int m = 0, o = 0;
-            if (ok) {
-                const int pair = idx >> 4, pp = idx & 15;
-                m = pair / dd;
-                o = pair - m * dd;
-                const double *hv = hN + m * kH + pp, *cv = ctxS + m * kH + pp;
-                const double *wc = wout + o * kWoutLd + pp;
-                double p0 = 0.0, p1 = 0.0;
+        // ---- E1: u = [h; ctx] @ W_out for all samples, 8 lanes per output ----
+        {
+            const int total = Mb * dd * 8;
+            for (int b0 = 0; b0 < total; b0 += kThreads) {
+                const int idx = b0 + tid;
+                const bool ok = idx < total;
+                double part = 0.0;
+                int m = 0, o = 0;
+                if (ok) {
+                    // lane part pp sums i = pp + 8i' over [h; ctx]; W_out^T rows of
+                    // kWoutLd (== 8 mod 16) doubles -> conflict-free half-warps
+                    const int pair = idx >> 3, pp = idx & 7;
+                    m = pair / dd;
+                    o = pair - m * dd;
+                    const double *hv = hN + m * kH + pp, *cv = ctxS + m * kH + pp;
+                    const double *wc = wout + o * kWoutLd + pp;
+                    double p0 = 0.0, p1 = 0.0;
 #pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    p0 = fma(hv[16 * i], wc[16 * i], p0);
-                    p1 = fma(cv[16 * i], wc[kH + 16 * i], p1);
+                    for (int i = 0; i < 8; i++) {
+                        p0 = fma(hv[8 * i], wc[8 * i], p0);
+                        p1 = fma(cv[8 * i], wc[kH + 8 * i], p1);
+                    }
+                    part = p0 + p1;
                 }
-                part = p0 + p1;
-            }
-            part += __shfl_xor_sync(0xffffffffu, part, 8);
-            part += __shfl_xor_sync(0xffffffffu, part, 4);
-            part += __shfl_xor_sync(0xffffffffu, part, 2);
-            part += __shfl_xor_sync(0xffffffffu, part, 1);
-            if (ok && (idx & 15) == 0) {
-                uS[m * 32 + o] = part;
-                a.act_u[((size_t)(k0 + m) * T + t) * dd + o] = part;
+                part += __shfl_xor_sync(0xffffffffu, part, 4);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                if (ok && (idx & 7) == 0) {
+                    uS[m * 32 + o] = part;
+                    a.act_u[((size_t)(k0 + m) * T + t) * dd + o] = part;
+                }
             }
         }
         __syncthreads();
         DP_PHASE(6);
         // ---- E2: logits, softmax over devices, draw (policy.py:301-308, 320-323) ----
-        for (int m = warp; m < Mb; m += kDecWarps) {
+        for (int m = warp; m < Mb; m += kThreads / 32) {
             const size_t row = (size_t)(k0 + m) * T + t;
             double z = -INFINITY;
             if (lane < D) {
@@ -551,9 +522,10 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_kernel(DecArgs a) {
     }
 #undef DP_PHASE
     // ---- log p = sum_t (zs[c_t] - log sum_t): logs in parallel, sum in t order ----
+    __threadfence_block();
     for (int m = 0; m < Mb; m++) {
         const size_t r0 = (size_t)(k0 + m) * T;
-        for (int t = tid; t < T; t += kDecThreads) alS[t] = a.act_lz[(r0 + t) * 2] - log(a.act_lz[(r0 + t) * 2 + 1]);
+        for (int t = tid; t < T; t += kThreads) alS[t] = a.act_lz[(r0 + t) * 2] - log(a.act_lz[(r0 + t) * 2 + 1]);
         __syncthreads();
         if (tid == 0) {
             double lp = 0.0;
@@ -792,7 +764,7 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
             a.o_p = take(M * 32);
             a.o_alpha = take(M * Tpad);
             const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
-            a.o_red = take(2 * kDecWarps * MT);
+            a.o_red = take(2 * 8 * MT);
             a.o_red2 = take(kCtxParts * M * kH);
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + M);
@@ -872,7 +844,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
                           : (const void *)dec_kernel<8, false>;
     DP_CUDA_TRY(allow_big_smem(fn, pl.smem));
     void *args[] = {&a};
-    DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kDecThreads), args, pl.smem, st));
+    DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));
     count_launch();
     p->last_K = K;
     return DP_OK;
