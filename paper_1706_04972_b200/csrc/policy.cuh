@@ -53,4 +53,7 @@ struct dp_policy {
     double *partial;                                     // per-CTA partial sums
     size_t partial_elems;
     double *gacc;                                        // [P] accumulator
+    // side stream: the encoder backward (one CTA) overlaps the decoder weight-gradient GEMM
+    cudaStream_t side;
+    cudaEvent_t ev_fork, ev_join;
 };

@@ -208,16 +208,20 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
 }
 
 // ------------------------------------------------------------------ B1
+constexpr int kAttTile = 64;  // rows per tile in att_bwd (2 rows per thread in the S/DA and dq passes)
+
 struct AttSmem {
     double enc[kChunk * kPad];
-    double q[kTile * kPad];
-    double dc[kTile * kPad];
-    double al[kTile * kPad];
-    double ds[kTile * kPad];
-    double mx[kTile], sm[kTile], w[kTile];
+    double q[kAttTile * kPad];
+    double dc[kAttTile * kPad];
+    double al[kAttTile * kPad];
+    double ds[kAttTile * kPad];
+    double mx[kAttTile], sm[kAttTile], w[kAttTile];
 };
 
-__global__ void __launch_bounds__(kThreads) att_bwd_kernel(
+// Register tiles: S/DA pass 2 rows x 8 enc rows per thread (12 LDS -> 32 FMA),
+// dq pass 2 rows x 8 columns, dE pass 4 x 4 (16 LDS -> 32 FMA).
+__global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
     const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ row_dctx,
     const double *__restrict__ row_w, double *__restrict__ row_dq, double *__restrict__ partial) {
@@ -227,12 +231,10 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
     const int T = dm.T;
     const int n_chunks = (T + kChunk - 1) / kChunk;
     const int tile0 = blockIdx.x * tiles_per_cta;
-    const int n_tiles_total = (rows + kTile - 1) / kTile;
+    const int n_tiles_total = (rows + kAttTile - 1) / kAttTile;
     const int tile1 = min(n_tiles_total, tile0 + tiles_per_cta);
-    // S/DA micro-tile: row = tid>>3, i in {ib + 8*ii}
-    const int sr = tid >> 3, ib = tid & 7;
-    // dE micro-tile: i in {ei + 16*a}, j in {ej + 16*b} (a,b < 4)
-    const int ei = tid >> 4, ej = tid & 15;
+    const int sr = tid >> 3, ib = tid & 7;  // rows {sr, sr+32}; i (or j) in {ib + 8*ii}
+    const int ei = tid >> 4, ej = tid & 15; // dE: i in {ei + 16a}, j in {ej + 16b}
     for (int ch = 0; ch < n_chunks; ch++) {
         const int i0 = ch * kChunk;
         for (int x = tid; x < kChunk * kH; x += kThreads) {
@@ -245,16 +247,16 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
 #pragma unroll
             for (int b = 0; b < 4; b++) dE[a][b] = 0.0;
         for (int tl = tile0; tl < tile1; tl++) {
-            const int rb = tl * kTile;
+            const int rb = tl * kAttTile;
             __syncthreads();
-            for (int x = tid; x < kTile * kH; x += kThreads) {
+            for (int x = tid; x < kAttTile * kH; x += kThreads) {
                 const int r = x >> 6, j = x & 63;
                 const int row = rb + r;
                 const bool ok = row < rows;
                 S.q[r * kPad + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
                 S.dc[r * kPad + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
             }
-            if (tid < kTile) {
+            if (tid < kAttTile) {
                 const int row = rb + tid;
                 const bool ok = row < rows;
                 S.mx[tid] = ok ? act_stat[(size_t)row * 2] : 0.0;
@@ -262,58 +264,76 @@ __global__ void __launch_bounds__(kThreads) att_bwd_kernel(
                 S.w[tid] = ok ? row_w[row] : 0.0;
             }
             __syncthreads();
+            // S = Q enc^T, DA = DCTX enc^T over this chunk -> alpha, ds
             {
-                double sv[8], dv[8];
+                double sv[2][8], dv[2][8];
 #pragma unroll
-                for (int ii = 0; ii < 8; ii++) sv[ii] = dv[ii] = 0.0;
-                const double *qr = S.q + sr * kPad;
-                const double *dr = S.dc + sr * kPad;
-#pragma unroll 4
+                for (int rr = 0; rr < 2; rr++)
+#pragma unroll
+                    for (int ii = 0; ii < 8; ii++) sv[rr][ii] = dv[rr][ii] = 0.0;
+#pragma unroll 2
                 for (int j = 0; j < kH; j++) {
-                    const double qj = qr[j], dj = dr[j];
+                    const double q0 = S.q[sr * kPad + j], q1 = S.q[(sr + 32) * kPad + j];
+                    const double d0 = S.dc[sr * kPad + j], d1 = S.dc[(sr + 32) * kPad + j];
 #pragma unroll
                     for (int ii = 0; ii < 8; ii++) {
                         const double e = S.enc[(ib + 8 * ii) * kPad + j];
-                        sv[ii] = fma(qj, e, sv[ii]);
-                        dv[ii] = fma(dj, e, dv[ii]);
+                        sv[0][ii] = fma(q0, e, sv[0][ii]);
+                        sv[1][ii] = fma(q1, e, sv[1][ii]);
+                        dv[0][ii] = fma(d0, e, dv[0][ii]);
+                        dv[1][ii] = fma(d1, e, dv[1][ii]);
                     }
                 }
-                const double m = S.mx[sr], l = S.sm[sr], w = S.w[sr];
 #pragma unroll
-                for (int ii = 0; ii < 8; ii++) {
-                    const int i = ib + 8 * ii;
-                    double al = 0.0, ds = 0.0;
-                    if (i0 + i < T) {
-                        al = exp(sv[ii] - m) / l;
-                        ds = al * (dv[ii] - w);
+                for (int rr = 0; rr < 2; rr++) {
+                    const int r = sr + 32 * rr;
+                    const double m = S.mx[r], l = S.sm[r], w = S.w[r];
+#pragma unroll
+                    for (int ii = 0; ii < 8; ii++) {
+                        const int i = ib + 8 * ii;
+                        double al = 0.0, ds = 0.0;
+                        if (i0 + i < T) {
+                            al = exp(sv[rr][ii] - m) / l;
+                            ds = al * (dv[rr][ii] - w);
+                        }
+                        S.al[r * kPad + i] = al;
+                        S.ds[r * kPad + i] = ds;
                     }
-                    S.al[sr * kPad + i] = al;
-                    S.ds[sr * kPad + i] = ds;
                 }
             }
             __syncthreads();
+            // dq[row, j] += sum_i ds[row, i] enc[i, j]
             {
-                const int row = rb + sr;
-                double acc[8];
+                double acc[2][8];
 #pragma unroll
-                for (int jj = 0; jj < 8; jj++) acc[jj] = 0.0;
-                const double *dsr = S.ds + sr * kPad;
-#pragma unroll 4
+                for (int rr = 0; rr < 2; rr++)
+#pragma unroll
+                    for (int jj = 0; jj < 8; jj++) acc[rr][jj] = 0.0;
+#pragma unroll 2
                 for (int i = 0; i < kChunk; i++) {
-                    const double d = dsr[i];
-#pragma unroll
-                    for (int jj = 0; jj < 8; jj++) acc[jj] = fma(d, S.enc[i * kPad + ib + 8 * jj], acc[jj]);
-                }
-                if (row < rows) {
+                    const double d0 = S.ds[sr * kPad + i], d1 = S.ds[(sr + 32) * kPad + i];
 #pragma unroll
                     for (int jj = 0; jj < 8; jj++) {
-                        double *dst = row_dq + (size_t)row * kH + ib + 8 * jj;
-                        *dst = ch == 0 ? acc[jj] : *dst + acc[jj];
+                        const double e = S.enc[i * kPad + ib + 8 * jj];
+                        acc[0][jj] = fma(d0, e, acc[0][jj]);
+                        acc[1][jj] = fma(d1, e, acc[1][jj]);
+                    }
+                }
+#pragma unroll
+                for (int rr = 0; rr < 2; rr++) {
+                    const int row = rb + sr + 32 * rr;
+                    if (row < rows) {
+#pragma unroll
+                        for (int jj = 0; jj < 8; jj++) {
+                            double *dst = row_dq + (size_t)row * kH + ib + 8 * jj;
+                            *dst = ch == 0 ? acc[rr][jj] : *dst + acc[rr][jj];
+                        }
                     }
                 }
             }
+            // dE[i, j] += sum_r al[r, i] dc[r, j] + ds[r, i] q[r, j]
 #pragma unroll 2
-            for (int r = 0; r < kTile; r++) {
+            for (int r = 0; r < kAttTile; r++) {
                 double av[4], sv4[4], dcv[4], qv[4];
 #pragma unroll
                 for (int a = 0; a < 4; a++) {
@@ -765,7 +785,7 @@ size_t dp_backward_partial_elems(const dp_policy *p) {
     size_t m = a > b ? a : b;
     m = m > c ? m : c;
     m = m > d ? m : d;
-    return m + (size_t)dm.T * dm.td + 2 * kH;  // + dx scratch + (dh, dc) sums
+    return m + (size_t)dm.T * dm.td + 4 * kH;  // + dx scratch + (dh, dc) sums + encoder (dh, dc) sink
 }
 
 extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
@@ -778,7 +798,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     const int T = dm.T;
     const int rows = K * T;
     double *part = p->partial;
-    double *dx_scratch = part + (p->partial_elems - (size_t)T * dm.td - 2 * kH);
+    double *dx_scratch = part + (p->partial_elems - (size_t)T * dm.td - 4 * kH);
     double *dhc_sum = dx_scratch + (size_t)T * dm.td;
     DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
 
@@ -807,7 +827,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     }
     // B1
     {
-        const int n_tiles = ceil_div(rows, kTile);
+        const int n_tiles = ceil_div(rows, kAttTile);
         const int n = n_cta_for(n_tiles, 2);
         const int tpc = ceil_div(n_tiles, n);
         const int n_used = ceil_div(n_tiles, tpc);
@@ -845,6 +865,33 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
             p->row_dhx, nullptr, nullptr, p->dh0, p->dc0);
         DP_LAUNCH_CHECK();
     }
+    // Fork: B4 + B5 (encoder backward: one CTA, sequential over T, then the
+    // encoder weight gradients) run on the side stream while B3 fills the
+    // other SMs.  Disjoint outputs (grad[w_enc,b_enc,type_table] vs
+    // grad[w_dec,b_dec,dev_table]) and scratch (partial tail vs head).
+    DP_CUDA_TRY(cudaEventRecord(p->ev_fork, st));
+    DP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
+    {
+        cudaStream_t ss = p->side;
+        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dh0, K, dhc_sum);
+        DP_LAUNCH_CHECK();
+        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dc0, K, dhc_sum + kH);
+        DP_LAUNCH_CHECK();
+        DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, ss));
+        const size_t smem = lstm_bwd_smem(1);
+        lstm_bwd_kernel<<<1, kThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
+                                                   p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
+                                                   dhc_sum + 2 * kH, dhc_sum + 3 * kH);
+        DP_LAUNCH_CHECK();
+        enc_wgrad_kernel<<<dm.F + kH + 1, kG, 0, ss>>>(dm, p->X, p->enc_h, p->da_enc, grad);
+        DP_LAUNCH_CHECK();
+        enc_dx_kernel<<<ceil_div(T * dm.td, 256), 256, 0, ss>>>(dm, params, p->da_enc, dx_scratch);
+        DP_LAUNCH_CHECK();
+        type_scatter_kernel<<<ceil_div(dm.V1 * dm.td, 128), 128, 0, ss>>>(dm, p->occ_off, p->occ_t, p->type_off,
+                                                                         dx_scratch, grad);
+        DP_LAUNCH_CHECK();
+        DP_CUDA_TRY(cudaEventRecord(p->ev_join, ss));
+    }
     // B3
     {
         const int n_tiles = ceil_div(rows, kTile);
@@ -866,28 +913,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
         dec_finalize_kernel<<<1, kG, 0, st>>>(dm, params, p->gacc, grad);
         DP_LAUNCH_CHECK();
     }
-    // B4: encoder backward once on the summed inputs
-    {
-        sum_rows_kernel<<<1, kH, 0, st>>>(p->dh0, K, dhc_sum);
-        DP_LAUNCH_CHECK();
-        sum_rows_kernel<<<1, kH, 0, st>>>(p->dc0, K, dhc_sum + kH);
-        DP_LAUNCH_CHECK();
-        DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, st));
-        const size_t smem = lstm_bwd_smem(1);
-        lstm_bwd_kernel<<<1, kThreads, smem, st>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
-                                                   p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
-                                                   p->dh0, p->dc0);
-        DP_LAUNCH_CHECK();
-    }
-    // B5
-    {
-        enc_wgrad_kernel<<<dm.F + kH + 1, kG, 0, st>>>(dm, p->X, p->enc_h, p->da_enc, grad);
-        DP_LAUNCH_CHECK();
-        enc_dx_kernel<<<ceil_div(T * dm.td, 256), 256, 0, st>>>(dm, params, p->da_enc, dx_scratch);
-        DP_LAUNCH_CHECK();
-        type_scatter_kernel<<<ceil_div(dm.V1 * dm.td, 128), 128, 0, st>>>(dm, p->occ_off, p->occ_t, p->type_off,
-                                                                          dx_scratch, grad);
-        DP_LAUNCH_CHECK();
-    }
+    // join the side stream (B4 + B5)
+    DP_CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
     return DP_OK;
 }

@@ -575,6 +575,9 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc};
     for (void *q : ptrs)
         if (q) cudaFree(q);
+    if (p->side) cudaStreamDestroy(p->side);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_join) cudaEventDestroy(p->ev_join);
     (void)cudaGetLastError();
     delete p;
 }
@@ -676,6 +679,13 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     if (!ok) {
         dp::set_error(std::string("dp_policy_create: allocation/upload failed: ") +
                       cudaGetErrorString(cudaGetLastError()));
+        dp_policy_destroy(p);
+        return DP_ECUDA;
+    }
+    if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        dp::set_error("dp_policy_create: stream/event creation failed");
         dp_policy_destroy(p);
         return DP_ECUDA;
     }
