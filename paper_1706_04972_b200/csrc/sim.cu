@@ -2,10 +2,12 @@
 //
 // Replaces simulate()/check_memory() of the reference cost model,
 // /root/reference/pkg/src/devplace/simulator.py:93-194, for K placements per
-// launch.  One thread owns one placement; its whole event state lives in
-// shared memory (SoA, slot-interleaved so lanes at the same step touch
-// consecutive words).  The graph (CSR by topo rank, durations, bytes) is
-// read-only and shared by all placements through L1/L2.
+// launch.  One thread owns one placement; its event state lives in shared
+// memory (SoA, slot-interleaved so lanes at the same step touch consecutive
+// words) and, for D <= 8 devices, its per-device state (pending FINISH slot,
+// ready-queue bounds, busy/transfer/peak accumulators) in registers.  The
+// graph (CSR by topo rank, durations, bytes, bandwidths) is staged once per
+// CTA in shared memory when it fits, else read through L1/L2.
 //
 // Exact restatement (verified bit-identical):
 //   * per-edge ARRIVAL events collapse into one READY event per group, fired at
@@ -25,14 +27,83 @@
 
 namespace {
 
-struct SimSlot {
-    int S, s;
-    __device__ __forceinline__ size_t at(int i) const { return (size_t)i * S + s; }
-};
-
 __device__ __forceinline__ bool key_less(double ta, int ra, double tb, int rb) {
     return ta < tb || (ta == tb && ra < rb);
 }
+
+// Per-device state, register-resident (DM >= D): runtime indices resolve to
+// unrolled predicated selects instead of shared-memory round trips.
+template <int DM>
+struct DevRegs {
+    double fin_t[DM], busy[DM], trans[DM];
+    long long peak[DM];
+    int fin_r[DM], qh[DM], qt[DM];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int j = 0; j < DM; j++) {
+            fin_t[j] = busy[j] = trans[j] = 0.0;
+            peak[j] = 0;
+            fin_r[j] = -1;
+            qh[j] = qt[j] = 0;
+        }
+    }
+#define DP_GET(name, T)                                            \
+    __device__ __forceinline__ T get_##name(int d) const {         \
+        T v = name[0];                                             \
+        _Pragma("unroll") for (int j = 1; j < DM; j++) if (j == d) v = name[j]; \
+        return v;                                                  \
+    }                                                              \
+    __device__ __forceinline__ void set_##name(int d, T v) {       \
+        _Pragma("unroll") for (int j = 0; j < DM; j++) if (j == d) name[j] = v; \
+    }
+    DP_GET(fin_t, double)
+    DP_GET(busy, double)
+    DP_GET(trans, double)
+    DP_GET(peak, long long)
+    DP_GET(fin_r, int)
+    DP_GET(qh, int)
+    DP_GET(qt, int)
+#undef DP_GET
+};
+
+// Same interface, shared-memory resident (any D <= 32).
+struct DevSmem {
+    double *fin_t, *busy, *trans;
+    long long *peak;
+    int *fin_r, *qh, *qt;
+    int S, s, D;
+    __device__ __forceinline__ int at(int j) const { return j * S + s; }
+    __device__ __forceinline__ void init() {
+        for (int j = 0; j < D; j++) {
+            fin_t[at(j)] = busy[at(j)] = trans[at(j)] = 0.0;
+            peak[at(j)] = 0;
+            fin_r[at(j)] = -1;
+            qh[at(j)] = qt[at(j)] = 0;
+        }
+    }
+#define DP_GET(name, T)                                                                  \
+    __device__ __forceinline__ T get_##name(int d) const { return name[at(d)]; }         \
+    __device__ __forceinline__ void set_##name(int d, T v) { name[at(d)] = v; }
+    DP_GET(fin_t, double)
+    DP_GET(busy, double)
+    DP_GET(trans, double)
+    DP_GET(peak, long long)
+    DP_GET(fin_r, int)
+    DP_GET(qh, int)
+    DP_GET(qt, int)
+#undef DP_GET
+};
+
+template <int DM>
+struct DevPick {  // register state when DM > 0
+    template <class A, class B>
+    __device__ __forceinline__ static A &get(A &a, B &) { return a; }
+};
+template <>
+struct DevPick<0> {  // shared-memory state
+    template <class A, class B>
+    __device__ __forceinline__ static B &get(A &, B &b) { return b; }
+};
 
 // Bytes of the graph image staged in shared memory (GS=true).
 __host__ __device__ inline size_t graph_smem_bytes(int n, int d, int e) {
@@ -40,9 +111,16 @@ __host__ __device__ inline size_t graph_smem_bytes(int n, int d, int e) {
     return (b + 15) & ~(size_t)15;
 }
 
-// GS: stage the graph (durations, CSR, bytes, bandwidths) in shared memory
-// once per CTA — every event's lookups become LDS instead of L2 round trips.
-template <bool GS>
+// Per-placement shared-memory bytes (DM > 0: device state in registers).
+__host__ __device__ inline size_t slot_bytes(int n, int d, bool reg_dev) {
+    size_t b = (size_t)n * 8 + (size_t)d * d * 8;  // maxarr, link_free
+    if (!reg_dev) b += (size_t)d * (8 * 4 + 4 + 2 * 4);  // fin_t busy trans peak | fin_r | qh qt (int)
+    b += (size_t)n * 2 * 3;                        // left, heap, devq (u16)
+    b += (size_t)n;                                // placement (u8)
+    return (b + 7) & ~(size_t)7;
+}
+
+template <bool GS, int DM>
 __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8_t *__restrict__ placement,
                                                   int by_rank, double *__restrict__ makespan,
                                                   double *__restrict__ busy_out, double *__restrict__ transfer_out,
@@ -90,22 +168,31 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     auto gid_of = [&](int r) -> int { return GS ? (int)g_gid16[r] : g_gid32[r]; };
     auto indeg_of = [&](int r) -> int { return GS ? (int)g_indeg16[r] : g_indeg32[r]; };
     if (s >= S || k >= K) return;
-    const SimSlot q{S, s};
+    auto at = [&](int i) -> int { return i * S + s; };
 
     // ---- shared-memory carve-up (all arrays slot-interleaved: [i*S + s]) ----
     double *maxarr = reinterpret_cast<double *>(smem + gbytes);  // [n]  READY time (max arrival)
-    double *fin_t = maxarr + (size_t)n * S;              // [D]  pending FINISH time per device
-    double *link = fin_t + (size_t)D * S;                // [D*D] link_free
-    double *busy = link + (size_t)D * D * S;             // [D]
-    double *trans = busy + (size_t)D * S;                // [D]
-    long long *peak = reinterpret_cast<long long *>(trans + (size_t)D * S);  // [D]
-    int *fin_r = reinterpret_cast<int *>(peak + (size_t)D * S);              // [D] -1 = idle
-    uint16_t *left = reinterpret_cast<uint16_t *>(fin_r + (size_t)D * S);    // [n] unfinished preds
-    uint16_t *heap = left + (size_t)n * S;                                   // [n] READY heap (ranks)
-    uint16_t *devq = heap + (size_t)n * S;                                   // [n] ready queues
-    uint16_t *qhead = devq + (size_t)n * S;                                  // [D]
-    uint16_t *qtail = qhead + (size_t)D * S;                                 // [D]
-    uint8_t *pl = reinterpret_cast<uint8_t *>(qtail + (size_t)D * S);        // [n] device of rank
+    double *link = maxarr + n * S;                                // [D*D] link_free
+    unsigned char *tail = reinterpret_cast<unsigned char *>(link + D * D * S);
+    DevSmem ds;
+    if (DM == 0) {
+        ds.fin_t = reinterpret_cast<double *>(tail);
+        ds.busy = ds.fin_t + D * S;
+        ds.trans = ds.busy + D * S;
+        ds.peak = reinterpret_cast<long long *>(ds.trans + D * S);
+        ds.fin_r = reinterpret_cast<int *>(ds.peak + D * S);
+        ds.qh = ds.fin_r + D * S;
+        ds.qt = ds.qh + D * S;
+        ds.S = S;
+        ds.s = s;
+        ds.D = D;
+        tail = reinterpret_cast<unsigned char *>(ds.qt + D * S);
+    }
+    uint16_t *left = reinterpret_cast<uint16_t *>(tail);  // [n] unfinished preds
+    uint16_t *heap = left + n * S;                         // [n] READY heap (ranks)
+    uint16_t *devq = heap + n * S;                         // [n] ready queues
+    uint8_t *pl = reinterpret_cast<uint8_t *>(devq + n * S);  // [n] device of rank
+    DevRegs<(DM > 0 ? DM : 1)> dr;
 
     // ---- placement load + validation (pkg/simulator.py:109-116) ----
     const uint8_t *src = placement + (size_t)k * n;
@@ -113,7 +200,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     for (int r = 0; r < n; r++) {
         const uint8_t v = by_rank ? src[r] : src[gid_of(r)];
         bad |= (v >= D);
-        pl[q.at(r)] = v;
+        pl[at(r)] = v;
     }
     if (bad) {
         makespan[k] = __longlong_as_double(0x7ff8000000000000LL);
@@ -126,40 +213,34 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
         if (err) *err = 1;
         return;
     }
-
-    for (int j = 0; j < D; j++) {
-        fin_r[q.at(j)] = -1;
-        busy[q.at(j)] = 0.0;
-        trans[q.at(j)] = 0.0;
-        peak[q.at(j)] = 0;
-        qtail[q.at(j)] = 0;
-    }
-    for (int j = 0; j < D * D; j++) link[q.at(j)] = 0.0;
+    auto &dv_ = DevPick<DM>::get(dr, ds);
+    dv_.init();
+    for (int j = 0; j < D * D; j++) link[at(j)] = 0.0;
 
     // counts per device (segment sizes), check_memory peaks (integer, exact)
     for (int r = 0; r < n; r++) {
-        const int dv = pl[q.at(r)];
-        qtail[q.at(dv)] += 1;
-        peak[q.at(dv)] += (long long)g.resident[r];
-        left[q.at(r)] = (uint16_t)indeg_of(r);
-        maxarr[q.at(r)] = 0.0;
+        const int d = pl[at(r)];
+        dv_.set_qt(d, dv_.get_qt(d) + 1);
+        dv_.set_peak(d, dv_.get_peak(d) + (long long)g.resident[r]);
+        left[at(r)] = (uint16_t)indeg_of(r);
+        maxarr[at(r)] = 0.0;
     }
     {
         int base = 0;
         for (int j = 0; j < D; j++) {
-            const int c = qtail[q.at(j)];
-            qhead[q.at(j)] = (uint16_t)base;
-            qtail[q.at(j)] = (uint16_t)base;
+            const int c = dv_.get_qt(j);
+            dv_.set_qh(j, base);
+            dv_.set_qt(j, base);
             base += c;
         }
     }
     // sources enter their device queue at t=0 in rank order (pkg/simulator.py:154-156)
     for (int r = 0; r < n; r++) {
         if (indeg_of(r) == 0) {
-            const int dv = pl[q.at(r)];
-            const int pos = qtail[q.at(dv)];
-            devq[q.at(pos)] = (uint16_t)r;
-            qtail[q.at(dv)] = (uint16_t)(pos + 1);
+            const int d = pl[at(r)];
+            const int pos = dv_.get_qt(d);
+            devq[at(pos)] = (uint16_t)r;
+            dv_.set_qt(d, pos + 1);
         }
     }
 
@@ -167,16 +248,16 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     int32_t *ord = order ? order + (size_t)k * n : nullptr;
 
     // start_next(dev, now): pkg/simulator.py:146-152
-    auto start_next = [&](int dv, double now) {
-        if (fin_r[q.at(dv)] >= 0) return;
-        const int h = qhead[q.at(dv)];
-        if (h >= qtail[q.at(dv)]) return;
-        const int r = devq[q.at(h)];
-        qhead[q.at(dv)] = (uint16_t)(h + 1);
-        const double dur = g_dur[(size_t)r * D + dv];
-        busy[q.at(dv)] += dur;
-        fin_t[q.at(dv)] = now + dur;
-        fin_r[q.at(dv)] = r;
+    auto start_next = [&](int d, double now) {
+        if (dv_.get_fin_r(d) >= 0) return;
+        const int h = dv_.get_qh(d);
+        if (h >= dv_.get_qt(d)) return;
+        const int r = devq[at(h)];
+        dv_.set_qh(d, h + 1);
+        const double dur = g_dur[r * D + d];
+        dv_.set_busy(d, dv_.get_busy(d) + dur);
+        dv_.set_fin_t(d, now + dur);
+        dv_.set_fin_r(d, r);
         if (ord) ord[n_order++] = gid_of(r);
     };
     for (int j = 0; j < D; j++) start_next(j, 0.0);
@@ -187,78 +268,98 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
         // next FINISH: min (t, rank) over busy devices
         int bd = -1, br = 0;
         double bt = 0.0;
-        for (int j = 0; j < D; j++) {
-            const int r = fin_r[q.at(j)];
-            if (r >= 0) {
-                const double t = fin_t[q.at(j)];
-                if (bd < 0 || key_less(t, r, bt, br)) {
-                    bd = j;
-                    bt = t;
-                    br = r;
+        if constexpr (DM > 0) {
+#pragma unroll
+            for (int j = 0; j < DM; j++) {
+                const int r = dr.fin_r[j];
+                if (j < D && r >= 0) {
+                    const double t = dr.fin_t[j];
+                    if (bd < 0 || key_less(t, r, bt, br)) {
+                        bd = j;
+                        bt = t;
+                        br = r;
+                    }
+                }
+            }
+        } else {
+            for (int j = 0; j < D; j++) {
+                const int r = ds.get_fin_r(j);
+                if (r >= 0) {
+                    const double t = ds.get_fin_t(j);
+                    if (bd < 0 || key_less(t, r, bt, br)) {
+                        bd = j;
+                        bt = t;
+                        br = r;
+                    }
                 }
             }
         }
         int hr = 0;
         double ht = 0.0;
         if (n_heap > 0) {
-            hr = heap[q.at(0)];
-            ht = maxarr[q.at(hr)];
+            hr = heap[at(0)];
+            ht = maxarr[at(hr)];
         }
         if (bd >= 0 && (n_heap == 0 || bt <= ht)) {
             // ---- FINISH (pkg/simulator.py:162-178) ----
-            fin_r[q.at(bd)] = -1;
+            dv_.set_fin_r(bd, -1);
             mk = bt > mk ? bt : mk;
             const int e0 = g_off[br], e1 = g_off[br + 1];
+            double tr = 0.0;
+            bool any_link = false;
             for (int e = e0; e < e1; e++) {
                 const int dst = dst_of(e);
-                const int ddev = pl[q.at(dst)];
+                const int ddev = pl[at(dst)];
                 const double nbytes = g_bytes[e];
                 double arrive;
                 if (ddev == bd || nbytes == 0.0) {
                     arrive = bt;
                 } else {
                     const int li = bd * D + ddev;
-                    const double lf = link[q.at(li)];
+                    const double lf = link[at(li)];
                     const double begin = lf > bt ? lf : bt;
                     const double dur = nbytes / g_bw[li];
                     const double end = begin + dur;
-                    link[q.at(li)] = end;
-                    trans[q.at(bd)] += dur;
+                    link[at(li)] = end;
+                    // transfer[dev] += dur, in edge order (sequential, same rounding)
+                    tr = any_link ? tr + dur : dv_.get_trans(bd) + dur;
+                    any_link = true;
                     arrive = end;
                 }
-                const double ma = maxarr[q.at(dst)];
-                maxarr[q.at(dst)] = arrive > ma ? arrive : ma;
-                const int l = left[q.at(dst)] - 1;
-                left[q.at(dst)] = (uint16_t)l;
+                const double ma = maxarr[at(dst)];
+                maxarr[at(dst)] = arrive > ma ? arrive : ma;
+                const int l = left[at(dst)] - 1;
+                left[at(dst)] = (uint16_t)l;
                 if (l == 0) {
                     // READY(dst) with key (maxarr, 1, rank): heap push
-                    const double t = maxarr[q.at(dst)];
+                    const double t = maxarr[at(dst)];
                     int i = n_heap++;
                     while (i > 0) {
                         const int p = (i - 1) >> 1;
-                        const int pr = heap[q.at(p)];
-                        if (!key_less(t, dst, maxarr[q.at(pr)], pr)) break;
-                        heap[q.at(i)] = (uint16_t)pr;
+                        const int pr = heap[at(p)];
+                        if (!key_less(t, dst, maxarr[at(pr)], pr)) break;
+                        heap[at(i)] = (uint16_t)pr;
                         i = p;
                     }
-                    heap[q.at(i)] = (uint16_t)dst;
+                    heap[at(i)] = (uint16_t)dst;
                 }
             }
+            if (any_link) dv_.set_trans(bd, tr);
             start_next(bd, bt);
         } else if (n_heap > 0) {
             // ---- READY (= the reference's final ARRIVAL, pkg/simulator.py:179-184) ----
-            const int last = heap[q.at(--n_heap)];
+            const int last = heap[at(--n_heap)];
             if (n_heap > 0) {
-                const double xt = maxarr[q.at(last)];
+                const double xt = maxarr[at(last)];
                 int i = 0;
                 for (;;) {
                     int c = 2 * i + 1;
                     if (c >= n_heap) break;
-                    int cr = heap[q.at(c)];
-                    double ct = maxarr[q.at(cr)];
+                    int cr = heap[at(c)];
+                    double ct = maxarr[at(cr)];
                     if (c + 1 < n_heap) {
-                        const int c2 = heap[q.at(c + 1)];
-                        const double t2 = maxarr[q.at(c2)];
+                        const int c2 = heap[at(c + 1)];
+                        const double t2 = maxarr[at(c2)];
                         if (key_less(t2, c2, ct, cr)) {
                             c++;
                             cr = c2;
@@ -266,24 +367,25 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
                         }
                     }
                     if (!key_less(ct, cr, xt, last)) break;
-                    heap[q.at(i)] = (uint16_t)cr;
+                    heap[at(i)] = (uint16_t)cr;
                     i = c;
                 }
-                heap[q.at(i)] = (uint16_t)last;
+                heap[at(i)] = (uint16_t)last;
             }
-            const int dv = pl[q.at(hr)];
+            const int d = pl[at(hr)];
             // sorted insertion into the device queue (tail, usually O(1))
-            int pos = qtail[q.at(dv)];
-            const int h = qhead[q.at(dv)];
+            const int qt = dv_.get_qt(d);
+            int pos = qt;
+            const int h = dv_.get_qh(d);
             while (pos > h) {
-                const int pr = devq[q.at(pos - 1)];
-                if (!key_less(ht, hr, maxarr[q.at(pr)], pr)) break;
-                devq[q.at(pos)] = (uint16_t)pr;
+                const int pr = devq[at(pos - 1)];
+                if (!key_less(ht, hr, maxarr[at(pr)], pr)) break;
+                devq[at(pos)] = (uint16_t)pr;
                 pos--;
             }
-            devq[q.at(pos)] = (uint16_t)hr;
-            qtail[q.at(dv)] = (uint16_t)(qtail[q.at(dv)] + 1);
-            start_next(dv, ht);
+            devq[at(pos)] = (uint16_t)hr;
+            dv_.set_qt(d, qt + 1);
+            start_next(d, ht);
         } else {
             break;
         }
@@ -292,24 +394,17 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     makespan[k] = mk;
     bool ok = true;
     for (int j = 0; j < D; j++) {
-        busy_out[(size_t)k * D + j] = busy[q.at(j)];
-        transfer_out[(size_t)k * D + j] = trans[q.at(j)];
-        const long long pk = peak[q.at(j)];
+        busy_out[(size_t)k * D + j] = dv_.get_busy(j);
+        transfer_out[(size_t)k * D + j] = dv_.get_trans(j);
+        const long long pk = dv_.get_peak(j);
         peak_out[(size_t)k * D + j] = pk;
         ok &= pk <= (long long)g.mem[j];
     }
     feasible[k] = ok ? 1 : 0;
 }
 
-size_t slot_bytes(int n, int d) {
-    size_t b = (size_t)n * 8 + (size_t)d * 8 * 4 + (size_t)d * d * 8 + (size_t)d * 8;  // f64/i64
-    b += (size_t)d * 4;                                                                  // fin_r
-    b += (size_t)n * 2 * 3 + (size_t)d * 2 * 2;                                          // u16
-    b += (size_t)n;                                                                      // u8
-    return b;
-}
-
 constexpr size_t kSmemBudget = 220 * 1024;
+constexpr int kRegDevMax = 8;
 
 }  // namespace
 
@@ -328,13 +423,12 @@ extern "C" int dp_graph_create(int32_t n, int32_t d, const double *h_cost, const
         DP_REQUIRE(h_indeg[r] >= 0 && h_indeg[r] < 65536, "dp_graph_create: in-degree out of range");
         max_indeg = h_indeg[r] > max_indeg ? h_indeg[r] : max_indeg;
     }
-    std::string why;
     dp_graph *g = new dp_graph();
     g->n = n;
     g->d = d;
     g->e = e;
     g->max_indeg = max_indeg;
-    g->sim_smem_per_placement = slot_bytes(n, d);
+    g->sim_smem_per_placement = slot_bytes(n, d, d <= kRegDevMax);
     double *h_dur = new double[(size_t)(n > 0 ? n : 1) * d];
     for (int r = 0; r < n; r++)
         for (int j = 0; j < d; j++) h_dur[(size_t)r * d + j] = h_cost[r] / h_rate[j];
@@ -383,6 +477,17 @@ extern "C" void dp_graph_destroy(dp_graph *g) {
     delete g;
 }
 
+template <bool GS, int DM>
+static int launch_sim(const dp_graph *g, int grid, int threads, size_t smem, cudaStream_t st, int K,
+                      const uint8_t *placement, int by_rank, double *makespan, double *busy, double *transfer,
+                      int64_t *peak, uint8_t *feasible, int32_t *order, uint8_t *err, int S) {
+    if (smem > 48 * 1024) DP_CUDA_TRY(dp::allow_big_smem((const void *)sim_kernel<GS, DM>, smem));
+    sim_kernel<GS, DM><<<grid, threads, smem, st>>>(*g, K, placement, by_rank, makespan, busy, transfer, peak,
+                                                    feasible, order, err, S);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
 extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *placement, int32_t by_rank,
                                  double *makespan, double *busy, double *transfer, int64_t *peak,
                                  uint8_t *feasible, int32_t *order, uint8_t *err, void *stream) {
@@ -403,15 +508,18 @@ extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *pl
     if (S < 1) S = 1;
     const int grid = dp::ceil_div(K, S);
     const size_t smem = per * S + (gs ? gb : 0) + 16;
-    const void *fn = gs ? (const void *)sim_kernel<true> : (const void *)sim_kernel<false>;
-    if (smem > 48 * 1024) DP_CUDA_TRY(dp::allow_big_smem(fn, smem));
     const int threads = ((S + 31) / 32) * 32;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool reg = g->d <= kRegDevMax;
+    if (gs && reg)
+        return launch_sim<true, kRegDevMax>(g, grid, threads, smem, st, K, placement, by_rank, makespan, busy,
+                                            transfer, peak, feasible, order, err, S);
     if (gs)
-        sim_kernel<true><<<grid, threads, smem, (cudaStream_t)stream>>>(*g, K, placement, by_rank, makespan, busy,
-                                                                        transfer, peak, feasible, order, err, S);
-    else
-        sim_kernel<false><<<grid, threads, smem, (cudaStream_t)stream>>>(*g, K, placement, by_rank, makespan, busy,
-                                                                         transfer, peak, feasible, order, err, S);
-    DP_LAUNCH_CHECK();
-    return DP_OK;
+        return launch_sim<true, 0>(g, grid, threads, smem, st, K, placement, by_rank, makespan, busy, transfer,
+                                   peak, feasible, order, err, S);
+    if (reg)
+        return launch_sim<false, kRegDevMax>(g, grid, threads, smem, st, K, placement, by_rank, makespan, busy,
+                                             transfer, peak, feasible, order, err, S);
+    return launch_sim<false, 0>(g, grid, threads, smem, st, K, placement, by_rank, makespan, busy, transfer, peak,
+                                feasible, order, err, S);
 }
