@@ -36,6 +36,20 @@ namespace dp {
 
 __device__ __forceinline__ double sigmoid_ref(double x) { return 1.0 / (1.0 + exp(-x)); }
 
+// LSTM gate activation without warp divergence between the sigmoid gates and
+// the tanh gate: both go through ONE expm1 and one division,
+//   sigmoid(x) = 1 / (2 + expm1(-x)),
+//   tanh(x)    = sign(x) * (-e / (2 + e)),  e = expm1(-2|x|)  (e in (-1, 0]).
+// expm1 keeps tanh's relative accuracy near 0 and nothing overflows; the
+// result differs from numpy's 1/(1+exp(-x)) / tanh(x) by ~1 ulp (same order
+// as the dot-product summation-order differences).
+__device__ __forceinline__ double gate_act(double x, bool is_tanh) {
+    const double e = expm1(is_tanh ? -2.0 * fabs(x) : -x);
+    const double r = (is_tanh ? -e : 1.0) / (2.0 + e);
+    return is_tanh ? copysign(r, x) : r;
+}
+__device__ __forceinline__ double tanh_x(double x) { return gate_act(x, true); }
+
 // Debug-only per-phase cycle counters of the decoder (block 0, thread 0).
 __device__ int g_dbg_clocks = 0;
 __device__ long long g_phase_clk[16];
@@ -136,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0; t < dm.T; t++) {
         const double a = xp + dot64_sh_reg(hbuf[t & 1], w);
         if (t + 1 < dm.T) xp = XP[(size_t)(t + 1) * kG + col];
-        const double act = gate == 3 ? tanh(a) : sigmoid_ref(a);
+        const double act = gate_act(a, gate == 3);
         enc_g[(size_t)t * kG + col] = act;
         const double iv = __shfl_sync(0xffffffffu, act, base + 0);
         const double fv = __shfl_sync(0xffffffffu, act, base + 1);
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const double gv = __shfl_sync(0xffffffffu, act, base + 3);
         if (gate == 0) {
             c = fv * c + iv * gv;
-            const double h = ov * tanh(c);
+            const double h = ov * tanh_x(c);
             hbuf[(t + 1) & 1][u] = h;
             enc_h[(size_t)t * kH + u] = h;
             enc_c[(size_t)t * kH + u] = c;
@@ -250,6 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 
     const int base = lane & ~3;
     const int Tp = (T + kCtxParts - 1) / kCtxParts;
+    int d_pow2 = 1;
+    while (d_pow2 < D) d_pow2 <<= 1;
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
     const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
     long long clk_last = clk_on ? clock64() : 0;
@@ -263,30 +279,38 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         const int cur = t & 1;
         // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
         {
-            double av[MT];
+            // stage-separated over the M samples so their transcendental chains overlap;
+            // one divergence-free activation path for all 4 gates (gate_act)
+            double av[MT], act[MT], cn[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) av[m] = edev[prev[m] * kG + col] + dot64_sh_reg(hS + (cur * M + m) * kH, w);
 #pragma unroll
-            for (int m = 0; m < MT; m++) {
+            for (int m = 0; m < MT; m++)
                 if (m < Mb) {
-                    const double act = gate == 3 ? tanh(av[m]) : sigmoid_ref(av[m]);
-                    const size_t row = (size_t)(k0 + m) * T + t;
-                    a.act_g[row * kG + col] = act;
-                    const double iv = __shfl_sync(0xffffffffu, act, base + 0);
-                    const double fv = __shfl_sync(0xffffffffu, act, base + 1);
-                    const double ov = __shfl_sync(0xffffffffu, act, base + 2);
-                    const double gv = __shfl_sync(0xffffffffu, act, base + 3);
-                    if (gate == 0) {
-                        const double cn = fv * cS[m * kH + u] + iv * gv;
-                        const double hn = ov * tanh(cn);
-                        cS[m * kH + u] = cn;
-                        hS[((cur ^ 1) * M + m) * kH + u] = hn;
-                        a.act_h[row * kH + u] = hn;
-                        a.act_c[row * kH + u] = cn;
-                    }
+                    act[m] = gate_act(av[m], gate == 3);
+                    a.act_g[((size_t)(k0 + m) * T + t) * kG + col] = act[m];
                 }
-            }
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) {
+                    const double iv = __shfl_sync(0xffffffffu, act[m], base + 0);
+                    const double fv = __shfl_sync(0xffffffffu, act[m], base + 1);
+                    const double ov = __shfl_sync(0xffffffffu, act[m], base + 2);
+                    const double gv = __shfl_sync(0xffffffffu, act[m], base + 3);
+                    cn[m] = fv * cS[m * kH + u] + iv * gv;
+                    act[m] = ov;
+                }
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb && gate == 0) {
+                    const double hn = act[m] * tanh_x(cn[m]);
+                    const size_t row = (size_t)(k0 + m) * T + t;
+                    cS[m * kH + u] = cn[m];
+                    hS[((cur ^ 1) * M + m) * kH + u] = hn;
+                    a.act_h[row * kH + u] = hn;
+                    a.act_c[row * kH + u] = cn[m];
+                }
         }
         __syncthreads();
         DP_PHASE(0);
@@ -471,43 +495,49 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 if (o < dd) z0 = fma(devt[lane * dd + o], uS[m * 32 + o], z0);
                 z = (z0 + z1) + bout[lane];
             }
+            // max over the D device lanes (order-free)
             double zmax = z;
-            for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+            for (int o = d_pow2 >> 1; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
             const double zs = z - zmax;
-            const double ez = exp(zs);
-            if (lane < D) pS[m * 32 + lane] = ez;
-            __syncwarp();
+            const double ez = lane < D ? exp(zs) : 0.0;
+            // sum exp(zs) in numpy's order, computed redundantly by every lane from
+            // shuffled values (no shared-memory round trip); D >= 8 uses the
+            // pairwise-8 order through shared memory
             double esum = 0.0;
-            if (lane == 0) esum = np_sum_small(pS + m * 32, D);
-            esum = __shfl_sync(0xffffffffu, esum, 0);
+            if (D < 8) {
+                for (int j = 0; j < D; j++) esum += __shfl_sync(0xffffffffu, ez, j);
+            } else {
+                if (lane < D) pS[m * 32 + lane] = ez;
+                __syncwarp();
+                esum = np_sum_small(pS + m * 32, D);
+                __syncwarp();
+            }
             const double pr = ez / esum;
-            __syncwarp();
             if (lane < D) {
-                pS[m * 32 + lane] = pr;
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
             }
-            __syncwarp();
-            int ch = 0;
-            if (lane == 0) {
-                if (a.forced) {
-                    ch = a.forced[row];
-                } else {
-                    u128 s{pcg[2 * m], pcg[2 * m + 1]};
-                    s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
+            int ch;
+            if (a.forced) {
+                ch = a.forced[row];
+            } else {
+                // every lane replays the PCG64 step and the cdf search (same result)
+                u128 s{pcg[2 * m], pcg[2 * m + 1]};
+                s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
+                const double r = pcg_double(s);
+                double cdf = 0.0;
+                int cnt = 0;
+                for (int j = 0; j < D; j++) {
+                    cdf += __shfl_sync(0xffffffffu, pr, j);
+                    cnt += (cdf <= r) ? 1 : 0;
+                }
+                ch = cnt < D - 1 ? cnt : D - 1;
+                __syncwarp();
+                if (lane == 0) {
                     pcg[2 * m] = s.hi;
                     pcg[2 * m + 1] = s.lo;
-                    const double r = pcg_double(s);
-                    double cdf = 0.0;
-                    int cnt = 0;
-                    for (int dv = 0; dv < D; dv++) {
-                        cdf += pS[m * 32 + dv];
-                        cnt += (cdf <= r) ? 1 : 0;
-                    }
-                    ch = cnt < D - 1 ? cnt : D - 1;
                 }
             }
-            ch = __shfl_sync(0xffffffffu, ch, 0);
             const double zc = __shfl_sync(0xffffffffu, zs, ch);
             if (lane == 0) {
                 prev[m] = ch;
