@@ -495,49 +495,43 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 if (o < dd) z0 = fma(devt[lane * dd + o], uS[m * 32 + o], z0);
                 z = (z0 + z1) + bout[lane];
             }
-            // max over the D device lanes (order-free)
             double zmax = z;
             for (int o = d_pow2 >> 1; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
             const double zs = z - zmax;
-            const double ez = lane < D ? exp(zs) : 0.0;
-            // sum exp(zs) in numpy's order, computed redundantly by every lane from
-            // shuffled values (no shared-memory round trip); D >= 8 uses the
-            // pairwise-8 order through shared memory
+            const double ez = exp(zs);
+            if (lane < D) pS[m * 32 + lane] = ez;
+            __syncwarp();
             double esum = 0.0;
-            if (D < 8) {
-                for (int j = 0; j < D; j++) esum += __shfl_sync(0xffffffffu, ez, j);
-            } else {
-                if (lane < D) pS[m * 32 + lane] = ez;
-                __syncwarp();
-                esum = np_sum_small(pS + m * 32, D);
-                __syncwarp();
-            }
+            if (lane == 0) esum = np_sum_small(pS + m * 32, D);
+            esum = __shfl_sync(0xffffffffu, esum, 0);
             const double pr = ez / esum;
+            __syncwarp();
             if (lane < D) {
+                pS[m * 32 + lane] = pr;
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
             }
-            int ch;
-            if (a.forced) {
-                ch = a.forced[row];
-            } else {
-                // every lane replays the PCG64 step and the cdf search (same result)
-                u128 s{pcg[2 * m], pcg[2 * m + 1]};
-                s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
-                const double r = pcg_double(s);
-                double cdf = 0.0;
-                int cnt = 0;
-                for (int j = 0; j < D; j++) {
-                    cdf += __shfl_sync(0xffffffffu, pr, j);
-                    cnt += (cdf <= r) ? 1 : 0;
-                }
-                ch = cnt < D - 1 ? cnt : D - 1;
-                __syncwarp();
-                if (lane == 0) {
+            __syncwarp();
+            int ch = 0;
+            if (lane == 0) {
+                if (a.forced) {
+                    ch = a.forced[row];
+                } else {
+                    u128 s{pcg[2 * m], pcg[2 * m + 1]};
+                    s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
                     pcg[2 * m] = s.hi;
                     pcg[2 * m + 1] = s.lo;
+                    const double r = pcg_double(s);
+                    double cdf = 0.0;
+                    int cnt = 0;
+                    for (int dv = 0; dv < D; dv++) {
+                        cdf += pS[m * 32 + dv];
+                        cnt += (cdf <= r) ? 1 : 0;
+                    }
+                    ch = cnt < D - 1 ? cnt : D - 1;
                 }
             }
+            ch = __shfl_sync(0xffffffffu, ch, 0);
             const double zc = __shfl_sync(0xffffffffu, zs, ch);
             if (lane == 0) {
                 prev[m] = ch;
