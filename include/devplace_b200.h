@@ -144,6 +144,16 @@ int dp_policy_decode(dp_policy *p, const double *params, int32_t K, int64_t k_of
 int dp_policy_backward(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
                        void *stream);
 
+/* The same gradient in two halves so the first overlaps the simulator:
+ * _rows: the advantage-independent per-(sample, step) work (everything is
+ *        linear in adv, so it runs with adv := 1) — needs no scores;
+ * _grads: the advantage-weighted cross-sample sums.  Falls back to the fused
+ *        pass when _rows did not run for this decode (or the alpha store would
+ *        exceed the memory budget). */
+int dp_policy_backward_rows(dp_policy *p, const double *params, int32_t K, void *stream);
+int dp_policy_backward_grads(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
+                             void *stream);
+
 /* ---------------------------------------------------------------- trainer */
 
 /* Device-resident controller state (one per controller); zero-initialise,

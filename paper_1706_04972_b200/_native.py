@@ -36,6 +36,8 @@ SIGNATURES = {
     "dp_debug_phase_clocks": (I32, [I32, P]),
     "dp_policy_decode": (I32, [P, P, I32, I64, P, U64, P, I64, P, P, P, P, P]),
     "dp_policy_backward": (I32, [P, P, I32, P, P, P]),
+    "dp_policy_backward_rows": (I32, [P, P, I32, P]),
+    "dp_policy_backward_grads": (I32, [P, P, I32, P, P, P]),
     "dp_reinforce_epilogue": (I32, [I32, I32, P, P, P, F64, F64, I64, I64, I32, P, P, P, P, I64, I32, P]),
     "dp_adam_apply": (I32, [I64, P, P, P, P, P, I64, F64, F64, F64, F64, P, P, P, I64, P]),
 }

@@ -53,6 +53,8 @@ struct dp_policy {
     double *partial;                                     // per-CTA partial sums
     size_t partial_elems;
     double *gacc;                                        // [P] accumulator
+    double *al_store, *ds_store;  // [k*T][T] alpha / unscaled ds (split backward), NULL if too large
+    int rows_ready;               // K of the last dp_policy_backward_rows (0: none)
     // side stream: the encoder backward (one CTA) overlaps the decoder weight-gradient GEMM
     cudaStream_t side;
     cudaEvent_t ev_fork, ev_join;

@@ -37,6 +37,10 @@ namespace dp {
 namespace {
 
 constexpr int kTile = 32;   // rows per tile (B0, B1, B3)
+// Backward phases: kFused = one pass with the advantages; kRowsOnly = the
+// advantage-independent per-row half (runs concurrently with the simulator);
+// kGradsOnly = the advantage-weighted cross-row sums.
+constexpr int kFused = 0, kRowsOnly = 1, kGradsOnly = 2;
 constexpr int kFinTile = 64;
 constexpr int kChunk = 64;  // B1: enc rows per chunk
 constexpr int kPad = 65;
@@ -60,9 +64,10 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     const double *__restrict__ act_p, const uint8_t *__restrict__ choice, const double *__restrict__ act_u,
     const double *__restrict__ act_h, const double *__restrict__ act_ctx, double *__restrict__ row_q,
     double *__restrict__ row_dctx, double *__restrict__ row_w, double *__restrict__ row_dhx,
-    double *__restrict__ partial) {
+    double *__restrict__ partial, int mode /* kFused | kRowsOnly (adv := 1) | kGradsOnly */) {
     extern __shared__ __align__(16) double smraw[];
     PrepSmem &S = *reinterpret_cast<PrepSmem *>(smraw);
+    const bool rows_out = mode != kGradsOnly, grads_out = mode != kRowsOnly;
     const int tid = threadIdx.x;
     const int D = dm.D, dd = dm.dd, T = dm.T;
     const int ddp = dd + 1, Dp = D + 1;
@@ -100,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             if (row < rows) {
                 dz = -act_p[(size_t)row * D + d];
                 if (d == choice[row]) dz += 1.0;
-                dz = adv[row / T] * dz;
+                if (grads_out) dz = adv[row / T] * dz;
             }
             S.dz[r * Dp + d] = dz;
         }
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
                 for (int x = 0; x < 8; x++) q[x] = fma(S.watt[l * kPad + jb + 8 * x], hv, q[x]);
             }
             const int row = rb + r;
-            if (row < rows)
+            if (rows_out && row < rows)
 #pragma unroll
                 for (int x = 0; x < 8; x++) row_q[(size_t)row * kH + jb + 8 * x] = q[x];
         }
@@ -146,10 +151,10 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             for (int x = 0; x < 16; x++) {
                 const int i = ib + 8 * x;
                 if (i < kH) {
-                    if (row < rows) row_dhx[(size_t)row * kH + i] = v[x];
+                    if (rows_out && row < rows) row_dhx[(size_t)row * kH + i] = v[x];
                 } else {
                     S.dctx[r * kPad + i - kH] = v[x];
-                    if (row < rows) row_dctx[(size_t)row * kH + i - kH] = v[x];
+                    if (rows_out && row < rows) row_dctx[(size_t)row * kH + i - kH] = v[x];
                 }
             }
         }
@@ -168,8 +173,9 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             s += __shfl_xor_sync(0xffffffffu, s, 2);
             s += __shfl_xor_sync(0xffffffffu, s, 4);
             const int row = rb + r;
-            if (jb == 0 && row < rows) row_w[row] = s;
+            if (rows_out && jb == 0 && row < rows) row_w[row] = s;
         }
+        if (!grads_out) continue;
         // grads over the tile's rows
         for (int r = 0; r < kTile; r++) {
             const double hc = gi < kH ? S.h[r * kPad + gi] : S.ctx[r * kPad + gi - kH];
@@ -192,6 +198,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
         if (tid < D)
             for (int r = 0; r < kTile; r++) gb += S.dz[r * Dp + tid];
     }
+    if (!grads_out) return;
     const size_t na = (size_t)D + D * dd + 2 * kH * dd;
     double *out = partial + (size_t)blockIdx.x * na;
     if (tid < D) out[tid] = gb;
@@ -224,7 +231,8 @@ struct AttSmem {
 __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
     const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ row_dctx,
-    const double *__restrict__ row_w, double *__restrict__ row_dq, double *__restrict__ partial) {
+    const double *__restrict__ row_w, double *__restrict__ row_dq, double *__restrict__ partial,
+    double *__restrict__ al_store, double *__restrict__ ds_store /* [rows][T] or NULL */, int do_denc) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
     const int tid = threadIdx.x;
@@ -298,6 +306,10 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                         }
                         S.al[r * kPad + i] = al;
                         S.ds[r * kPad + i] = ds;
+                        if (al_store && rb + r < rows && i0 + i < T) {
+                            al_store[(size_t)(rb + r) * T + i0 + i] = al;
+                            ds_store[(size_t)(rb + r) * T + i0 + i] = ds;
+                        }
                     }
                 }
             }
@@ -332,6 +344,87 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 }
             }
             // dE[i, j] += sum_r al[r, i] dc[r, j] + ds[r, i] q[r, j]
+            if (!do_denc) continue;
+#pragma unroll 2
+            for (int r = 0; r < kAttTile; r++) {
+                double av[4], sv4[4], dcv[4], qv[4];
+#pragma unroll
+                for (int a = 0; a < 4; a++) {
+                    av[a] = S.al[r * kPad + ei + 16 * a];
+                    sv4[a] = S.ds[r * kPad + ei + 16 * a];
+                }
+#pragma unroll
+                for (int b = 0; b < 4; b++) {
+                    dcv[b] = S.dc[r * kPad + ej + 16 * b];
+                    qv[b] = S.q[r * kPad + ej + 16 * b];
+                }
+#pragma unroll
+                for (int a = 0; a < 4; a++)
+#pragma unroll
+                    for (int b = 0; b < 4; b++) dE[a][b] = fma(sv4[a], qv[b], fma(av[a], dcv[b], dE[a][b]));
+            }
+        }
+        if (do_denc) {
+#pragma unroll
+            for (int a = 0; a < 4; a++) {
+                const int i = i0 + ei + 16 * a;
+                if (i < T) {
+#pragma unroll
+                    for (int b = 0; b < 4; b++)
+                        partial[((size_t)blockIdx.x * T + i) * kH + ej + 16 * b] = dE[a][b];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ B1g
+// d_enc[i, j] = sum_rows adv_k (alpha[r, i] dctx_u[r, j] + ds_u[r, i] q[r, j])
+// from the alpha / ds stored by the rows-only att_bwd pass (per-CTA partials).
+struct DencSmem {
+    double al[kAttTile * kPad];
+    double ds[kAttTile * kPad];
+    double dc[kAttTile * kPad];
+    double q[kAttTile * kPad];
+};
+
+__global__ void __launch_bounds__(kThreads, 1) denc_kernel(PolicyDims dm, int rows, int tiles_per_cta,
+                                                           const double *__restrict__ adv,
+                                                           const double *__restrict__ al_store,
+                                                           const double *__restrict__ ds_store,
+                                                           const double *__restrict__ row_q,
+                                                           const double *__restrict__ row_dctx,
+                                                           double *__restrict__ partial) {
+    extern __shared__ __align__(16) double smraw[];
+    DencSmem &S = *reinterpret_cast<DencSmem *>(smraw);
+    const int tid = threadIdx.x;
+    const int T = dm.T;
+    const int n_chunks = (T + kChunk - 1) / kChunk;
+    const int n_tiles = (rows + kAttTile - 1) / kAttTile;
+    const int tile0 = blockIdx.x * tiles_per_cta, tile1 = min(n_tiles, tile0 + tiles_per_cta);
+    const int ei = tid >> 4, ej = tid & 15;
+    for (int ch = 0; ch < n_chunks; ch++) {
+        const int i0 = ch * kChunk;
+        double dE[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+#pragma unroll
+            for (int b = 0; b < 4; b++) dE[a][b] = 0.0;
+        for (int tl = tile0; tl < tile1; tl++) {
+            const int rb = tl * kAttTile;
+            __syncthreads();
+            for (int x = tid; x < kAttTile * kH; x += kThreads) {
+                const int r = x >> 6, c = x & 63, row = rb + r;
+                const bool ok = row < rows;
+                const double w = ok ? adv[row / T] : 0.0;
+                S.dc[r * kPad + c] = ok ? w * row_dctx[(size_t)row * kH + c] : 0.0;
+                S.q[r * kPad + c] = ok ? w * row_q[(size_t)row * kH + c] : 0.0;
+                const bool oki = ok && i0 + c < T;
+                S.al[r * kPad + c] = oki ? al_store[(size_t)row * T + i0 + c] : 0.0;
+                S.ds[r * kPad + c] = oki ? ds_store[(size_t)row * T + i0 + c] : 0.0;
+            }
+            __syncthreads();
 #pragma unroll 2
             for (int r = 0; r < kAttTile; r++) {
                 double av[4], sv4[4], dcv[4], qv[4];
@@ -360,7 +453,6 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     partial[((size_t)blockIdx.x * T + i) * kH + ej + 16 * b] = dE[a][b];
             }
         }
-        __syncthreads();
     }
 }
 
@@ -375,10 +467,13 @@ struct FinSmem {
 __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const double *__restrict__ P, int rows,
                                                            int tiles_per_cta, const double *__restrict__ act_h,
                                                            const double *__restrict__ row_dq,
-                                                           double *__restrict__ row_dhx, double *__restrict__ partial) {
+                                                           double *__restrict__ row_dhx, double *__restrict__ partial,
+                                                           const double *__restrict__ adv, int mode) {
     extern __shared__ __align__(16) double smraw[];
     FinSmem &S = *reinterpret_cast<FinSmem *>(smraw);
     const int tid = threadIdx.x;
+    const bool rows_out = mode != kGradsOnly, grads_out = mode != kRowsOnly;
+    const int T = dm.T;
     for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPad + (x & 63)] = P[dm.off.w_att + x];
     const int rb4 = tid >> 4, lb = tid & 15;  // out micro-tile: r in {rb4+16a}, l in {lb+16b}
     double g[4][4];
@@ -395,10 +490,12 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
             const int r = x >> 6, j = x & 63, row = rb + r;
             const bool ok = row < rows;
             S.q[r * kPad + j] = ok ? row_dq[(size_t)row * kH + j] : 0.0;
-            S.h[r * kPad + j] = ok ? act_h[(size_t)row * kH + j] : 0.0;
+            // grads-only: dq is unscaled, fold the row's advantage into h
+            const double hv = ok ? act_h[(size_t)row * kH + j] : 0.0;
+            S.h[r * kPad + j] = (ok && mode == kGradsOnly) ? adv[row / T] * hv : hv;
         }
         __syncthreads();
-        {
+        if (rows_out) {
             double o[4][4];
 #pragma unroll
             for (int a = 0; a < 4; a++)
@@ -425,6 +522,7 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
             }
         }
         // grad: l in {rb4 + 16a} (reuse mapping), j in {lb + 16b}
+        if (!grads_out) continue;
 #pragma unroll 4
         for (int r = 0; r < kFinTile; r++) {
             double hv[4], qv[4];
@@ -438,6 +536,7 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
                 for (int b = 0; b < 4; b++) g[a][b] = fma(hv[a], qv[b], g[a][b]);
         }
     }
+    if (!grads_out) return;
 #pragma unroll
     for (int a = 0; a < 4; a++)
 #pragma unroll
@@ -568,7 +667,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
                                                                 const double *__restrict__ enc_h,
                                                                 const uint8_t *__restrict__ choice,
                                                                 const double *__restrict__ da,
-                                                                double *__restrict__ partial) {
+                                                                double *__restrict__ partial,
+                                                                const double *__restrict__ adv) {
     extern __shared__ __align__(16) double sm[];
     double *s_h = sm;                        // [kTile][64]
     double *s_da = s_h + kTile * kH;         // [kTile][256]
@@ -599,7 +699,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
         }
         for (int x = tid; x < kTile * kG; x += kThreads) {
             const int row = rb + (x >> 8);
-            s_da[x] = row < rows ? da[(size_t)rb * kG + x] : 0.0;
+            const double v = row < rows ? da[(size_t)rb * kG + x] : 0.0;
+            s_da[x] = (adv && row < rows) ? adv[row / T] * v : v;  // grads-only: da is unscaled
         }
         if (tid < kTile) {
             const int row = rb + tid;
@@ -694,15 +795,17 @@ __global__ void dec_finalize_kernel(PolicyDims dm, const double *__restrict__ P,
 }
 
 // sum over samples of the decoder's dh/dc at step 0 -> encoder final state grads
-__global__ void sum_rows_kernel(const double *__restrict__ src, int n_rows, double *__restrict__ dst) {
+// dst[j] = sum_r w[r] * src[r, j]  (w == NULL: weights 1)
+__global__ void sum_rows_kernel(const double *__restrict__ src, int n_rows, double *__restrict__ dst,
+                                const double *__restrict__ w) {
     const int j = threadIdx.x;  // 64
     double v0 = 0.0, v1 = 0.0;
     int r = 0;
     for (; r + 2 <= n_rows; r += 2) {
-        v0 += src[(size_t)r * kH + j];
-        v1 += src[(size_t)(r + 1) * kH + j];
+        v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
+        v1 = fma(w ? w[r + 1] : 1.0, src[(size_t)(r + 1) * kH + j], v1);
     }
-    if (r < n_rows) v0 += src[(size_t)r * kH + j];
+    if (r < n_rows) v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
     dst[j] = v0 + v1;
 }
 
@@ -788,83 +891,77 @@ size_t dp_backward_partial_elems(const dp_policy *p) {
     return m + (size_t)dm.T * dm.td + 4 * kH;  // + dx scratch + (dh, dc) sums + encoder (dh, dc) sink
 }
 
-extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
-                                  void *stream) {
-    DP_ENTRY();
-    DP_REQUIRE(p && params && adv && grad, "dp_policy_backward: NULL argument");
-    DP_REQUIRE(K >= 1 && K == p->last_K, "dp_policy_backward: K must equal the last decode's K");
+namespace {
+
+struct Grid {
+    int n_used, per;
+};
+Grid tiles_grid(int rows, int tile) {
+    const int n_tiles = ceil_div(rows, tile);
+    const int n = n_cta_for(n_tiles, 2);
+    const int per = ceil_div(n_tiles, n);
+    return {ceil_div(n_tiles, per), per};
+}
+
+// B0 in the given mode (+ its reductions when it produces gradients)
+int run_b0(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
+           cudaStream_t st) {
     const PolicyDims &dm = p->dims;
-    cudaStream_t st = (cudaStream_t)stream;
-    const int T = dm.T;
-    const int rows = K * T;
+    const Grid g = tiles_grid(rows, kTile);
+    const size_t smem = sizeof(PrepSmem);
+    DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
+    row_prep_kernel<<<g.n_used, kThreads, smem, st>>>(dm, params, rows, g.per, adv, p->act_p, p->act_choice, p->act_u,
+                                                      p->act_h, p->act_ctx, p->row_q, p->row_dctx, p->row_w,
+                                                      p->row_dhx, p->partial, mode);
+    DP_LAUNCH_CHECK();
+    if (mode == kRowsOnly) return DP_OK;
+    const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
+    double *part = p->partial;
+    launch_reduce(part, g.n_used, na, dm.D, grad + dm.off.b_out, 0, st);
+    DP_LAUNCH_CHECK();
+    launch_reduce(part + dm.D, g.n_used, na, dm.D * dm.dd, grad + dm.off.dev_table, 0, st);
+    DP_LAUNCH_CHECK();
+    launch_reduce(part + dm.D + dm.D * dm.dd, g.n_used, na, 2 * kH * dm.dd, grad + dm.off.w_out, 0, st);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+int run_b1f(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
+            cudaStream_t st) {
+    const PolicyDims &dm = p->dims;
+    const Grid g = tiles_grid(rows, kFinTile);
+    const size_t smem = sizeof(FinSmem);
+    DP_CUDA_TRY(allow_big_smem((const void *)row_fin_kernel, smem));
+    row_fin_kernel<<<g.n_used, kThreads, smem, st>>>(dm, params, rows, g.per, p->act_h, p->row_dq, p->row_dhx,
+                                                     p->partial, adv, mode);
+    DP_LAUNCH_CHECK();
+    if (mode == kRowsOnly) return DP_OK;
+    launch_reduce(p->partial, g.n_used, kH * kH, kH * kH, grad + dm.off.w_att, 0, st);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+// B2: decoder LSTM backward, per sample (inputs row_dhx; da in place of act_g)
+int run_b2(dp_policy *p, const double *params, int K, cudaStream_t st) {
+    const PolicyDims &dm = p->dims;
+    int M = ceil_div(K, kNumSMs);
+    if (M > kMaxSeqPerCta) M = kMaxSeqPerCta;
+    const size_t smem = lstm_bwd_smem(M);
+    DP_CUDA_TRY(allow_big_smem((const void *)lstm_bwd_kernel, smem));
+    lstm_bwd_kernel<<<ceil_div(K, M), kThreads, smem, st>>>(
+        dm.T, K, M, params + dm.off.w_dec + (size_t)dm.dd * kG, p->act_g, p->act_c, p->enc_c + (size_t)(dm.T - 1) * kH,
+        p->row_dhx, nullptr, nullptr, p->dh0, p->dc0);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+// B3 on the main stream, B4 + B5 forked onto the side stream; adv == NULL: da/dh0/dc0 already scaled
+int run_b345(dp_policy *p, const double *params, int K, const double *adv, double *grad, cudaStream_t st) {
+    const PolicyDims &dm = p->dims;
+    const int T = dm.T, rows = K * T;
     double *part = p->partial;
     double *dx_scratch = part + (p->partial_elems - (size_t)T * dm.td - 4 * kH);
     double *dhc_sum = dx_scratch + (size_t)T * dm.td;
-    DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
-
-    // B0
-    {
-        const int n_tiles = ceil_div(rows, kTile);
-        const int n = n_cta_for(n_tiles, 2);
-        const int tpc = ceil_div(n_tiles, n);
-        const int n_used = ceil_div(n_tiles, tpc);
-        const size_t smem = sizeof(PrepSmem);
-        DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
-        row_prep_kernel<<<n_used, kThreads, smem, st>>>(dm, params, rows, tpc, adv, p->act_p, p->act_choice,
-                                                        p->act_u, p->act_h, p->act_ctx, p->row_q, p->row_dctx,
-                                                        p->row_w, p->row_dhx, part);
-        DP_LAUNCH_CHECK();
-        const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
-        // [b_out | dev[:D] | w_out] are contiguous in neither layout -> three segments
-        launch_reduce(part, n_used, na, dm.D, grad + dm.off.b_out, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(part + dm.D, n_used, na, dm.D * dm.dd,
-                                                                            grad + dm.off.dev_table, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(
-            part + dm.D + dm.D * dm.dd, n_used, na, 2 * kH * dm.dd, grad + dm.off.w_out, 0, st);
-        DP_LAUNCH_CHECK();
-    }
-    // B1
-    {
-        const int n_tiles = ceil_div(rows, kAttTile);
-        const int n = n_cta_for(n_tiles, 2);
-        const int tpc = ceil_div(n_tiles, n);
-        const int n_used = ceil_div(n_tiles, tpc);
-        const size_t smem = sizeof(AttSmem);
-        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
-        att_bwd_kernel<<<n_used, kThreads, smem, st>>>(dm, rows, tpc, p->enc_h, p->act_stat, p->row_q, p->row_dctx,
-                                                       p->row_w, p->row_dq, part);
-        DP_LAUNCH_CHECK();
-        launch_reduce(part, n_used, (size_t)T * kH, T * kH,
-                                                                      p->d_enc, 0, st);
-        DP_LAUNCH_CHECK();
-    }
-    // B1f
-    {
-        const int n_tiles = ceil_div(rows, kFinTile);
-        const int n = n_cta_for(n_tiles, 2);
-        const int tpc = ceil_div(n_tiles, n);
-        const int n_used = ceil_div(n_tiles, tpc);
-        const size_t smem = sizeof(FinSmem);
-        DP_CUDA_TRY(allow_big_smem((const void *)row_fin_kernel, smem));
-        row_fin_kernel<<<n_used, kThreads, smem, st>>>(dm, params, rows, tpc, p->act_h, p->row_dq, p->row_dhx, part);
-        DP_LAUNCH_CHECK();
-        launch_reduce(part, n_used, kH * kH, kH * kH,
-                                                                       grad + dm.off.w_att, 0, st);
-        DP_LAUNCH_CHECK();
-    }
-    // B2: decoder LSTM backward, per sample
-    {
-        int M = ceil_div(K, kNumSMs);
-        if (M > kMaxSeqPerCta) M = kMaxSeqPerCta;
-        const size_t smem = lstm_bwd_smem(M);
-        DP_CUDA_TRY(allow_big_smem((const void *)lstm_bwd_kernel, smem));
-        lstm_bwd_kernel<<<ceil_div(K, M), kThreads, smem, st>>>(
-            T, K, M, params + dm.off.w_dec + (size_t)dm.dd * kG, p->act_g, p->act_c, p->enc_c + (size_t)(T - 1) * kH,
-            p->row_dhx, nullptr, nullptr, p->dh0, p->dc0);
-        DP_LAUNCH_CHECK();
-    }
     // Fork: B4 + B5 (encoder backward: one CTA, sequential over T, then the
     // encoder weight gradients) run on the side stream while B3 fills the
     // other SMs.  Disjoint outputs (grad[w_enc,b_enc,type_table] vs
@@ -873,9 +970,9 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     DP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {
         cudaStream_t ss = p->side;
-        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dh0, K, dhc_sum);
+        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dh0, K, dhc_sum, adv);
         DP_LAUNCH_CHECK();
-        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dc0, K, dhc_sum + kH);
+        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dc0, K, dhc_sum + kH, adv);
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, ss));
         const size_t smem = lstm_bwd_smem(1);
@@ -894,26 +991,110 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     }
     // B3
     {
-        const int n_tiles = ceil_div(rows, kTile);
-        const int n = n_cta_for(n_tiles, 2);
-        const int tpc = ceil_div(n_tiles, n);
-        const int n_used = ceil_div(n_tiles, tpc);
+        const Grid g = tiles_grid(rows, kTile);
         const size_t smem = sizeof(double) * ((size_t)kTile * (kH + kG) + (size_t)(dm.D + 1) * kG);
         DP_CUDA_TRY(allow_big_smem((const void *)dec_wgrad_kernel, smem));
-        dec_wgrad_kernel<<<n_used, kThreads, smem, st>>>(dm, rows, tpc, p->act_h, p->enc_h, p->act_choice, p->act_g,
-                                                         part);
+        dec_wgrad_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->act_h, p->enc_h, p->act_choice,
+                                                           p->act_g, part, adv);
         DP_LAUNCH_CHECK();
         const size_t stride = (size_t)(kH + dm.D + 1) * kG;
-        launch_reduce(part, n_used, stride, kH * kG,
-                                                                       grad + dm.off.w_dec + (size_t)dm.dd * kG, 0, st);
+        launch_reduce(part, g.n_used, stride, kH * kG, grad + dm.off.w_dec + (size_t)dm.dd * kG, 0, st);
         DP_LAUNCH_CHECK();
-        launch_reduce(
-            part + (size_t)kH * kG, n_used, stride, (dm.D + 1) * kG, p->gacc, 0, st);
+        launch_reduce(part + (size_t)kH * kG, g.n_used, stride, (dm.D + 1) * kG, p->gacc, 0, st);
         DP_LAUNCH_CHECK();
         dec_finalize_kernel<<<1, kG, 0, st>>>(dm, params, p->gacc, grad);
         DP_LAUNCH_CHECK();
     }
-    // join the side stream (B4 + B5)
     DP_CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
     return DP_OK;
+}
+
+#define DP_TRY(x)                       \
+    do {                                \
+        const int rc_ = (x);            \
+        if (rc_ != DP_OK) return rc_;   \
+    } while (0)
+
+}  // namespace
+
+// Fused single pass (advantages known up front).
+extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
+                                  void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(p && params && adv && grad, "dp_policy_backward: NULL argument");
+    DP_REQUIRE(K >= 1 && K == p->last_K, "dp_policy_backward: K must equal the last decode's K");
+    const PolicyDims &dm = p->dims;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int T = dm.T, rows = K * T;
+    DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
+    p->rows_ready = 0;
+    DP_TRY(run_b0(p, params, rows, adv, grad, kFused, st));
+    {
+        const Grid g = tiles_grid(rows, kAttTile);
+        const size_t smem = sizeof(AttSmem);
+        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
+        att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
+                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, nullptr,
+                                                         nullptr, 1);
+        DP_LAUNCH_CHECK();
+        launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
+        DP_LAUNCH_CHECK();
+    }
+    DP_TRY(run_b1f(p, params, rows, nullptr, grad, kFused, st));
+    DP_TRY(run_b2(p, params, K, st));
+    return run_b345(p, params, K, nullptr, grad, st);
+}
+
+// Advantage-independent half: everything per sample that is linear in adv,
+// computed with adv := 1 (B0, attention backward with alpha/ds stored, B1f,
+// the decoder LSTM backward).  Enqueue it concurrently with scoring.
+extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32_t K, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(p && params, "dp_policy_backward_rows: NULL argument");
+    DP_REQUIRE(K >= 1 && K == p->last_K, "dp_policy_backward_rows: K must equal the last decode's K");
+    p->rows_ready = 0;
+    if (!p->al_store) return DP_OK;  // problem too large to store alpha: grads() runs the fused pass
+    const PolicyDims &dm = p->dims;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int rows = K * dm.T;
+    DP_TRY(run_b0(p, params, rows, nullptr, nullptr, kRowsOnly, st));
+    {
+        const Grid g = tiles_grid(rows, kAttTile);
+        const size_t smem = sizeof(AttSmem);
+        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
+        att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
+                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, p->al_store,
+                                                         p->ds_store, 0);
+        DP_LAUNCH_CHECK();
+    }
+    DP_TRY(run_b1f(p, params, rows, nullptr, nullptr, kRowsOnly, st));
+    DP_TRY(run_b2(p, params, K, st));
+    p->rows_ready = K;
+    return DP_OK;
+}
+
+// Advantage-weighted half: cross-sample sums of the per-row quantities left
+// by dp_policy_backward_rows (falls back to the fused pass if that did not run).
+extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int32_t K, const double *adv,
+                                        double *grad, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(p && params && adv && grad, "dp_policy_backward_grads: NULL argument");
+    if (p->rows_ready != K) return dp_policy_backward(p, params, K, adv, grad, stream);
+    const PolicyDims &dm = p->dims;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int T = dm.T, rows = K * T;
+    DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
+    DP_TRY(run_b0(p, params, rows, adv, grad, kGradsOnly, st));
+    {
+        const Grid g = tiles_grid(rows, kAttTile);
+        const size_t smem = sizeof(DencSmem);
+        DP_CUDA_TRY(allow_big_smem((const void *)denc_kernel, smem));
+        denc_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, adv, p->al_store, p->ds_store, p->row_q,
+                                                      p->row_dctx, p->partial);
+        DP_LAUNCH_CHECK();
+        launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
+        DP_LAUNCH_CHECK();
+    }
+    DP_TRY(run_b1f(p, params, rows, adv, grad, kGradsOnly, st));
+    return run_b345(p, params, K, adv, grad, st);
 }

@@ -596,7 +596,8 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
     void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
                     p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_ctx, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
-                    p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc};
+                    p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
+                    p->al_store, p->ds_store};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p->side) cudaStreamDestroy(p->side);
@@ -700,6 +701,14 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     p->partial_elems = dp_backward_partial_elems(p);
     alloc((void **)&p->partial, sizeof(double) * p->partial_elems);
     alloc((void **)&p->gacc, sizeof(double) * dm.off.total);
+    // split backward (rows half overlapping the simulator) stores alpha and ds
+    // per (sample, step) row: only when that stays below 4 GiB (e.g. 268 MB at
+    // C3 K=256; C5 K=4096 would need 262 GB and uses the fused pass)
+    const size_t store_bytes = sizeof(double) * rows * (size_t)T;
+    if (ok && store_bytes <= (size_t)2 << 30) {
+        alloc((void **)&p->al_store, store_bytes);
+        alloc((void **)&p->ds_store, store_bytes);
+    }
     if (!ok) {
         dp::set_error(std::string("dp_policy_create: allocation/upload failed: ") +
                       cudaGetErrorString(cudaGetLastError()));
@@ -881,5 +890,6 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));
     count_launch();
     p->last_K = K;
+    p->rows_ready = 0;
     return DP_OK;
 }

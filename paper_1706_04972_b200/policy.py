@@ -249,6 +249,26 @@ class DevicePolicy:
         nat.check(rc, "dp_policy_backward")
         return grad
 
+    def backward_rows(self, params_dev, K, stream=None):
+        """Advantage-independent half of the backward (overlaps scoring)."""
+        from . import _native as nat
+
+        nat.check(nat.lib().dp_policy_backward_rows(self.handle, nat.ptr(params_dev), K, nat.stream_ptr(stream)),
+                  "dp_policy_backward_rows")
+
+    def backward_grads(self, params_dev, K, adv_dev, grad=None, stream=None):
+        """Advantage-weighted half; returns sum_k adv[k] grad log p_k."""
+        import torch
+
+        from . import _native as nat
+
+        if grad is None:
+            grad = torch.empty(self.P, dtype=torch.float64, device=self.device)
+        rc = nat.lib().dp_policy_backward_grads(self.handle, nat.ptr(params_dev), K, nat.ptr(adv_dev),
+                                                nat.ptr(grad), nat.stream_ptr(stream))
+        nat.check(rc, "dp_policy_backward_grads")
+        return grad
+
     def by_gid(self, choice_by_rank):
         """[K, T] by rank -> [K, T] indexed by group id."""
         import torch

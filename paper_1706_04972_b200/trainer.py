@@ -348,6 +348,7 @@ class DeviceController:
         self.measure_ok = cfg.measure_steps >= 2
         self.updates_done = 0
         self._graph = None
+        self.side = torch.cuda.Stream(device=dev)
 
     # one update, enqueue-only (capturable)
     def step(self, stream=None, marks=None):
@@ -360,6 +361,7 @@ class DeviceController:
         mark = marks or (lambda _name: None)
         cfg, st = self.task.config, self.store
         p = st.params
+        main = stream if stream is not None else torch.cuda.current_stream()
         mark("encode")
         self.eng.encode(p, stream)
         mark("decode")
@@ -367,6 +369,10 @@ class DeviceController:
                         draw_counter=st.state.view(torch.int64)[3:4], draws_per_count=self.K * self.T,
                         choice=self.choice, logp=self.logp, stream=stream)
         mark("simulate")
+        # the advantage-independent half of the backward runs on a side stream
+        # while the placements are scored
+        self.side.wait_stream(main)
+        self.eng.backward_rows(p, self.K_local, stream=self.side)
         self.sim_local = self.dg.simulate(self.choice, by_rank=True, stream=stream, out=self.sim_local)
         mk, fe, ch = self.sim_local["makespan"], self.sim_local["feasible"], self.choice
         if not self.measure_ok:
@@ -385,7 +391,8 @@ class DeviceController:
             nat.stream_ptr(stream))
         nat.check(rc, "dp_reinforce_epilogue")
         mark("backward")
-        self.eng.backward(p, self.K_local, self.adv, grad=self.grad, stream=stream)
+        main.wait_stream(self.side)
+        self.eng.backward_grads(p, self.K_local, self.adv, grad=self.grad, stream=stream)
         if self.size > 1:
             mark("allreduce")
             self.xchg.all_reduce_sum(self.grad)

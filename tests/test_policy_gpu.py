@@ -101,6 +101,23 @@ def test_weighted_gradient_vs_oracle(name, K):
     assert _relnorm(got, ref) < GRAD_RTOL
 
 
+@pytest.mark.parametrize("name,K", [("C3", 16), ("C2", 7)])
+def test_split_backward_equals_fused(name, K):
+    """rows (adv-independent, overlapped with scoring) + grads == fused single pass."""
+    gg, topo, params, feats = _setup(name, seed=2)
+    eng = P.engine_for(params, feats, K)
+    pdev = torch.as_tensor(params.to_flat(), device=eng.device)
+    eng.encode(pdev)
+    eng.decode(pdev, K, pcg=(12345, 67891))
+    adv = torch.as_tensor(np.random.default_rng(9).normal(size=K), device=eng.device)
+    fused = eng.backward(pdev, K, adv).cpu().numpy()
+    eng.decode(pdev, K, pcg=(12345, 67891))
+    eng.backward_rows(pdev, K)
+    split = eng.backward_grads(pdev, K, adv).cpu().numpy()
+    assert _relnorm(split, fused) < 1e-12
+    np.testing.assert_allclose(split, fused, rtol=1e-9, atol=1e-13)
+
+
 def test_known_answers_zero_params_and_single_device():
     """zero params -> -T ln D ; D=1 -> log p = 0, zero gradient."""
     gg, topo, params, feats = _setup("C1")
