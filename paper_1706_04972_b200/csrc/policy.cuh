@@ -53,7 +53,7 @@ struct dp_policy {
     double *partial;                                     // per-CTA partial sums
     size_t partial_elems;
     double *gacc;                                        // [P] accumulator
-    double *al_store, *ds_store;  // [k*T][T] alpha / unscaled ds (split backward), NULL if too large
+    double *tile_part;            // [k*ceil(T/64)][T][64] per-tile d_enc partials (split backward), NULL if too large
     int rows_ready;               // K of the last dp_policy_backward_rows (0: none)
     // side stream: the encoder backward (one CTA) overlaps the decoder weight-gradient GEMM
     cudaStream_t side;

@@ -44,6 +44,7 @@ constexpr int kFused = 0, kRowsOnly = 1, kGradsOnly = 2;
 constexpr int kFinTile = 64;
 constexpr int kChunk = 64;  // B1: enc rows per chunk
 constexpr int kPad = 65;
+constexpr int kRedSlicesW = 8;  // weighted_reduce slices
 
 // ------------------------------------------------------------------ B0
 // partial per CTA: [b_out (D) | dev_table[:D] (D*dd) | w_out (128*dd)]
@@ -232,14 +233,16 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
     const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ row_dctx,
     const double *__restrict__ row_w, double *__restrict__ row_dq, double *__restrict__ partial,
-    double *__restrict__ al_store, double *__restrict__ ds_store /* [rows][T] or NULL */, int do_denc) {
+    double *__restrict__ tile_partial /* [n_tiles][T][64] or NULL */, int do_denc) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
     const int tid = threadIdx.x;
     const int T = dm.T;
     const int n_chunks = (T + kChunk - 1) / kChunk;
+    // tiles never straddle two samples: tile = (sample k, 64-step block)
+    const int tps = (T + kAttTile - 1) / kAttTile;
     const int tile0 = blockIdx.x * tiles_per_cta;
-    const int n_tiles_total = (rows + kAttTile - 1) / kAttTile;
+    const int n_tiles_total = (rows / T) * tps;
     const int tile1 = min(n_tiles_total, tile0 + tiles_per_cta);
     const int sr = tid >> 3, ib = tid & 7;  // rows {sr, sr+32}; i (or j) in {ib + 8*ii}
     const int ei = tid >> 4, ej = tid & 15; // dE: i in {ei + 16a}, j in {ej + 16b}
@@ -255,18 +258,20 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 #pragma unroll
             for (int b = 0; b < 4; b++) dE[a][b] = 0.0;
         for (int tl = tile0; tl < tile1; tl++) {
-            const int rb = tl * kAttTile;
+            const int t0 = (tl % tps) * kAttTile;
+            const int rb = (tl / tps) * T + t0;
+            const int nrow = min(kAttTile, T - t0);
             __syncthreads();
             for (int x = tid; x < kAttTile * kH; x += kThreads) {
                 const int r = x >> 6, j = x & 63;
                 const int row = rb + r;
-                const bool ok = row < rows;
+                const bool ok = r < nrow;
                 S.q[r * kPad + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
                 S.dc[r * kPad + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
             }
             if (tid < kAttTile) {
                 const int row = rb + tid;
-                const bool ok = row < rows;
+                const bool ok = tid < nrow;
                 S.mx[tid] = ok ? act_stat[(size_t)row * 2] : 0.0;
                 S.sm[tid] = ok ? act_stat[(size_t)row * 2 + 1] : 1.0;
                 S.w[tid] = ok ? row_w[row] : 0.0;
@@ -306,10 +311,6 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                         }
                         S.al[r * kPad + i] = al;
                         S.ds[r * kPad + i] = ds;
-                        if (al_store && rb + r < rows && i0 + i < T) {
-                            al_store[(size_t)(rb + r) * T + i0 + i] = al;
-                            ds_store[(size_t)(rb + r) * T + i0 + i] = ds;
-                        }
                     }
                 }
             }
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 #pragma unroll
                 for (int rr = 0; rr < 2; rr++) {
                     const int row = rb + sr + 32 * rr;
-                    if (row < rows) {
+                    if (sr + 32 * rr < nrow) {
 #pragma unroll
                         for (int jj = 0; jj < 8; jj++) {
                             double *dst = row_dq + (size_t)row * kH + ib + 8 * jj;
@@ -363,8 +364,21 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 #pragma unroll
                     for (int b = 0; b < 4; b++) dE[a][b] = fma(sv4[a], qv[b], fma(av[a], dcv[b], dE[a][b]));
             }
+            if (tile_partial) {
+                // rows-only pass: this tile's (unscaled) contribution, weighted by
+                // its sample's advantage later (weighted_reduce)
+#pragma unroll
+                for (int a = 0; a < 4; a++) {
+                    const int i = i0 + ei + 16 * a;
+#pragma unroll
+                    for (int b = 0; b < 4; b++) {
+                        if (i < T) tile_partial[((size_t)tl * T + i) * kH + ej + 16 * b] = dE[a][b];
+                        dE[a][b] = 0.0;
+                    }
+                }
+            }
         }
-        if (do_denc) {
+        if (do_denc && !tile_partial) {
 #pragma unroll
             for (int a = 0; a < 4; a++) {
                 const int i = i0 + ei + 16 * a;
@@ -380,79 +394,32 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 }
 
 // ------------------------------------------------------------------ B1g
-// d_enc[i, j] = sum_rows adv_k (alpha[r, i] dctx_u[r, j] + ds_u[r, i] q[r, j])
-// from the alpha / ds stored by the rows-only att_bwd pass (per-CTA partials).
-struct DencSmem {
-    double al[kAttTile * kPad];
-    double ds[kAttTile * kPad];
-    double dc[kAttTile * kPad];
-    double q[kAttTile * kPad];
-};
-
-__global__ void __launch_bounds__(kThreads, 1) denc_kernel(PolicyDims dm, int rows, int tiles_per_cta,
-                                                           const double *__restrict__ adv,
-                                                           const double *__restrict__ al_store,
-                                                           const double *__restrict__ ds_store,
-                                                           const double *__restrict__ row_q,
-                                                           const double *__restrict__ row_dctx,
-                                                           double *__restrict__ partial) {
-    extern __shared__ __align__(16) double smraw[];
-    DencSmem &S = *reinterpret_cast<DencSmem *>(smraw);
-    const int tid = threadIdx.x;
-    const int T = dm.T;
-    const int n_chunks = (T + kChunk - 1) / kChunk;
-    const int n_tiles = (rows + kAttTile - 1) / kAttTile;
-    const int tile0 = blockIdx.x * tiles_per_cta, tile1 = min(n_tiles, tile0 + tiles_per_cta);
-    const int ei = tid >> 4, ej = tid & 15;
-    for (int ch = 0; ch < n_chunks; ch++) {
-        const int i0 = ch * kChunk;
-        double dE[4][4];
-#pragma unroll
-        for (int a = 0; a < 4; a++)
-#pragma unroll
-            for (int b = 0; b < 4; b++) dE[a][b] = 0.0;
-        for (int tl = tile0; tl < tile1; tl++) {
-            const int rb = tl * kAttTile;
-            __syncthreads();
-            for (int x = tid; x < kAttTile * kH; x += kThreads) {
-                const int r = x >> 6, c = x & 63, row = rb + r;
-                const bool ok = row < rows;
-                const double w = ok ? adv[row / T] : 0.0;
-                S.dc[r * kPad + c] = ok ? w * row_dctx[(size_t)row * kH + c] : 0.0;
-                S.q[r * kPad + c] = ok ? w * row_q[(size_t)row * kH + c] : 0.0;
-                const bool oki = ok && i0 + c < T;
-                S.al[r * kPad + c] = oki ? al_store[(size_t)row * T + i0 + c] : 0.0;
-                S.ds[r * kPad + c] = oki ? ds_store[(size_t)row * T + i0 + c] : 0.0;
-            }
-            __syncthreads();
-#pragma unroll 2
-            for (int r = 0; r < kAttTile; r++) {
-                double av[4], sv4[4], dcv[4], qv[4];
-#pragma unroll
-                for (int a = 0; a < 4; a++) {
-                    av[a] = S.al[r * kPad + ei + 16 * a];
-                    sv4[a] = S.ds[r * kPad + ei + 16 * a];
-                }
-#pragma unroll
-                for (int b = 0; b < 4; b++) {
-                    dcv[b] = S.dc[r * kPad + ej + 16 * b];
-                    qv[b] = S.q[r * kPad + ej + 16 * b];
-                }
-#pragma unroll
-                for (int a = 0; a < 4; a++)
-#pragma unroll
-                    for (int b = 0; b < 4; b++) dE[a][b] = fma(sv4[a], qv[b], fma(av[a], dcv[b], dE[a][b]));
-            }
+// d_enc[e] = sum_tile adv[k(tile)] * tile_partial[tile][e]: the advantage-
+// weighted sum of the per-tile attention-backward partials left by the
+// rows-only pass (tiles never straddle samples).  8 tile-slices per element,
+// fixed combine order -> deterministic.
+__global__ void __launch_bounds__(256) weighted_reduce_kernel(const double *__restrict__ src, int n_tiles,
+                                                              size_t stride, int n, double *__restrict__ dst,
+                                                              const double *__restrict__ adv, int tps) {
+    __shared__ double part[kRedSlicesW][32];
+    const int el = threadIdx.x & 31, s = threadIdx.x >> 5;
+    const int e = blockIdx.x * 32 + el;
+    double v0 = 0.0, v1 = 0.0;
+    if (e < n) {
+        int c = s;
+        for (; c + kRedSlicesW < n_tiles; c += 2 * kRedSlicesW) {
+            v0 = fma(adv[c / tps], src[(size_t)c * stride + e], v0);
+            v1 = fma(adv[(c + kRedSlicesW) / tps], src[(size_t)(c + kRedSlicesW) * stride + e], v1);
         }
+        if (c < n_tiles) v0 = fma(adv[c / tps], src[(size_t)c * stride + e], v0);
+    }
+    part[s][el] = v0 + v1;
+    __syncthreads();
+    if (s == 0 && e < n) {
+        double v = part[0][el];
 #pragma unroll
-        for (int a = 0; a < 4; a++) {
-            const int i = i0 + ei + 16 * a;
-            if (i < T) {
-#pragma unroll
-                for (int b = 0; b < 4; b++)
-                    partial[((size_t)blockIdx.x * T + i) * kH + ej + 16 * b] = dE[a][b];
-            }
-        }
+        for (int q = 1; q < kRedSlicesW; q++) v += part[q][el];
+        dst[e] = v;
     }
 }
 
@@ -903,6 +870,13 @@ Grid tiles_grid(int rows, int tile) {
     return {ceil_div(n_tiles, per), per};
 }
 
+Grid att_grid(int K, int T) {
+    const int n_tiles = K * ((T + kAttTile - 1) / kAttTile);
+    const int n = n_cta_for(n_tiles, 2);
+    const int per = ceil_div(n_tiles, n);
+    return {ceil_div(n_tiles, per), per};
+}
+
 // B0 in the given mode (+ its reductions when it produces gradients)
 int run_b0(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
            cudaStream_t st) {
@@ -1030,12 +1004,11 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     p->rows_ready = 0;
     DP_TRY(run_b0(p, params, rows, adv, grad, kFused, st));
     {
-        const Grid g = tiles_grid(rows, kAttTile);
+        const Grid g = att_grid(K, T);
         const size_t smem = sizeof(AttSmem);
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
         att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, nullptr,
-                                                         nullptr, 1);
+                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, nullptr, 1);
         DP_LAUNCH_CHECK();
         launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
         DP_LAUNCH_CHECK();
@@ -1053,18 +1026,18 @@ extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32
     DP_REQUIRE(p && params, "dp_policy_backward_rows: NULL argument");
     DP_REQUIRE(K >= 1 && K == p->last_K, "dp_policy_backward_rows: K must equal the last decode's K");
     p->rows_ready = 0;
-    if (!p->al_store) return DP_OK;  // problem too large to store alpha: grads() runs the fused pass
+    if (!p->tile_part) return DP_OK;  // partials too large: grads() runs the fused pass
     const PolicyDims &dm = p->dims;
     cudaStream_t st = (cudaStream_t)stream;
     const int rows = K * dm.T;
     DP_TRY(run_b0(p, params, rows, nullptr, nullptr, kRowsOnly, st));
     {
-        const Grid g = tiles_grid(rows, kAttTile);
+        const Grid g = att_grid(K, dm.T);
         const size_t smem = sizeof(AttSmem);
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
         att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, p->al_store,
-                                                         p->ds_store, 0);
+                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, p->tile_part,
+                                                         1);
         DP_LAUNCH_CHECK();
     }
     DP_TRY(run_b1f(p, params, rows, nullptr, nullptr, kRowsOnly, st));
@@ -1086,13 +1059,9 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
     DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
     DP_TRY(run_b0(p, params, rows, adv, grad, kGradsOnly, st));
     {
-        const Grid g = tiles_grid(rows, kAttTile);
-        const size_t smem = sizeof(DencSmem);
-        DP_CUDA_TRY(allow_big_smem((const void *)denc_kernel, smem));
-        denc_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, adv, p->al_store, p->ds_store, p->row_q,
-                                                      p->row_dctx, p->partial);
-        DP_LAUNCH_CHECK();
-        launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
+        const int tps = (T + kAttTile - 1) / kAttTile;
+        weighted_reduce_kernel<<<ceil_div(T * kH, 32), 256, 0, st>>>(p->tile_part, K * tps, (size_t)T * kH, T * kH,
+                                                                     p->d_enc, adv, tps);
         DP_LAUNCH_CHECK();
     }
     DP_TRY(run_b1f(p, params, rows, adv, grad, kGradsOnly, st));

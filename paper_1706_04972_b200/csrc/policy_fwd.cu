@@ -597,7 +597,7 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
                     p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_ctx, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
-                    p->al_store, p->ds_store};
+                    p->tile_part};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p->side) cudaStreamDestroy(p->side);
@@ -701,14 +701,13 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     p->partial_elems = dp_backward_partial_elems(p);
     alloc((void **)&p->partial, sizeof(double) * p->partial_elems);
     alloc((void **)&p->gacc, sizeof(double) * dm.off.total);
-    // split backward (rows half overlapping the simulator) stores alpha and ds
-    // per (sample, step) row: only when that stays below 4 GiB (e.g. 268 MB at
-    // C3 K=256; C5 K=4096 would need 262 GB and uses the fused pass)
-    const size_t store_bytes = sizeof(double) * rows * (size_t)T;
-    if (ok && store_bytes <= (size_t)2 << 30) {
-        alloc((void **)&p->al_store, store_bytes);
-        alloc((void **)&p->ds_store, store_bytes);
-    }
+    // split backward (rows half overlapping the simulator) keeps one T x 64
+    // d_enc partial per (sample, 64-step tile): K*T^2*8 bytes — allocated only
+    // below 2 GiB (134 MB at C3 K=256; C5 K=4096 would need 134 GB and uses
+    // the fused pass)
+    const size_t tiles = (size_t)k_max * ((T + 63) / 64);
+    const size_t part_bytes = sizeof(double) * tiles * (size_t)T * kH;
+    if (ok && part_bytes <= (size_t)2 << 30) alloc((void **)&p->tile_part, part_bytes);
     if (!ok) {
         dp::set_error(std::string("dp_policy_create: allocation/upload failed: ") +
                       cudaGetErrorString(cudaGetLastError()));
