@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             for (int d = 0; d < D; d++) v = fma(S.devt[d * dd + o], S.dz[r * Dp + d], v);
             S.du[r * ddp + o] = v;
         }
-        {
+        if (rows_out) {
             const int r = tid >> 3, jb = tid & 7;
             double q[8];
 #pragma unroll
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
         }
         __syncthreads();
         // dhc = W_out du -> dh_out (i < 64) to global, dctx (i >= 64) to smem + global
-        {
+        if (rows_out) {
             const int r = tid >> 3, ib = tid & 7;
             double v[16];
 #pragma unroll
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
         }
         __syncthreads();
         // w = ctx . dctx (8 lanes per row)
-        {
+        if (rows_out) {
             const int r = tid >> 3, jb = tid & 7;
             double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -513,16 +513,21 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
 
 // ------------------------------------------------------------------ B2 / B4
 // Sequential LSTM backward (pkg/policy.py:236-253) for M (<= 8) sequences per
-// CTA.  thread (r = tid>>2, part = tid&3) keeps W_h[r, part*64 : part*64+64]
-// in registers; dh_prev[r] = sum over the 4 parts (shuffle).  The next step's
-// gate activations / cells / incoming dh are prefetched into registers while
-// the current step's mat-vec runs.  In place: gate activations become da.
+// CTA, 512 threads.  Thread (r = tid>>3, part = tid&7) keeps
+// W_h[r, 32*part : 32*part+32] in registers; dh_prev[r] = sum over the 8
+// parts (3 shuffles).  One elementwise slot (m, u) per thread.  The next
+// step's gate activations / cells / incoming dh are prefetched into registers
+// while the current step's mat-vec runs.  In place: gate activations become da.
 constexpr int kMaxSeqPerCta = 8;
-constexpr int kDaLd = kH + 2;  // 528-byte gate blocks: LDS.128 of 4 parts -> distinct banks
+constexpr int kLstmThreads = 512;
+// da in shared memory: per (sample, gate) a 68-double block holding the two
+// 32-gate halves at offsets 0 and 34 -> the 8 parts of a warp start in 8
+// distinct 16-byte bank groups (conflict-free LDS.128)
+constexpr int kDaLd = 68, kDaHalf = 34;
 
 inline size_t lstm_bwd_smem(int M) { return sizeof(double) * (size_t)M * (2 * kH + 4 * kDaLd); }
 
-__global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
+__global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     int T, int n_seq, int M, const double *__restrict__ Wh /* [64 x 256] row-major, ld 256 */,
     double *__restrict__ gates /* [seq][T][256] in: i,f,o,g  out: da */, const double *__restrict__ cst /* [seq][T][64] */,
     const double *__restrict__ c_init /* [64] c before step 0 */, const double *__restrict__ dh_ext /* [seq][T][64] */,
@@ -531,80 +536,73 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
     extern __shared__ __align__(16) double sm[];
     double *s_dh = sm;                   // [M][64]
     double *s_dc = s_dh + M * kH;        // [M][64]
-    double *s_da = s_dc + M * kH;        // [M][4 gates][kDaLd]: padded so the 4 parts of a warp hit distinct banks
+    double *s_da = s_dc + M * kH;        // [M][4 gates][kDaLd]
     const int tid = threadIdx.x;
     const int q0 = blockIdx.x * M;
     const int Mb = min(M, n_seq - q0);
-    const int r = tid >> 2, part = tid & 3;
-    double w[kH];
+    const int r = tid >> 3, part = tid & 7;
+    double w[32];
 #pragma unroll
-    for (int i = 0; i < kH; i++) w[i] = Wh[(size_t)r * kG + part * kH + i];
-    for (int x = tid; x < Mb * kH; x += kThreads) {
+    for (int i = 0; i < 32; i++) w[i] = Wh[(size_t)r * kG + part * 32 + i];
+    for (int x = tid; x < Mb * kH; x += kLstmThreads) {
         const int m = x >> 6, u = x & 63;
         s_dh[x] = dh_in ? dh_in[(size_t)(q0 + m) * kH + u] : 0.0;
         s_dc[x] = dc_in ? dc_in[(size_t)(q0 + m) * kH + u] : 0.0;
     }
-    // per-thread (m, u) slots: x = tid + 256*y
-    constexpr int kY = kMaxSeqPerCta * kH / kThreads;
-    double pi[kY], pf[kY], po[kY], pg[kY], pc[kY], pcp[kY], pdx[kY];
+    // elementwise slot of this thread: x = tid (M <= 8 -> Mb*64 <= 512)
+    const int x = tid, xm = x >> 6, xu = x & 63;
+    const bool live = x < Mb * kH;
+    double pi = 0, pf = 0, po = 0, pg = 0, pc = 0, pcp = 0, pdx = 0;
     auto prefetch = [&](int t) {
-#pragma unroll
-        for (int y = 0; y < kY; y++) {
-            const int x = tid + kThreads * y;
-            if (x < Mb * kH && t >= 0) {
-                const int m = x >> 6, u = x & 63;
-                const size_t row = (size_t)(q0 + m) * T + t;
-                const double *g = gates + row * kG;
-                pi[y] = g[u];
-                pf[y] = g[kH + u];
-                po[y] = g[2 * kH + u];
-                pg[y] = g[3 * kH + u];
-                pc[y] = cst[row * kH + u];
-                pcp[y] = t > 0 ? cst[(row - 1) * kH + u] : c_init[u];
-                pdx[y] = dh_ext[row * kH + u];
-            }
+        if (live && t >= 0) {
+            const size_t row = (size_t)(q0 + xm) * T + t;
+            const double *g = gates + row * kG;
+            pi = g[xu];
+            pf = g[kH + xu];
+            po = g[2 * kH + xu];
+            pg = g[3 * kH + xu];
+            pc = cst[row * kH + xu];
+            pcp = t > 0 ? cst[(row - 1) * kH + xu] : c_init[xu];
+            pdx = dh_ext[row * kH + xu];
         }
     };
     prefetch(T - 1);
+    const int dslot = (xu >> 5) * kDaHalf + (xu & 31);
     __syncthreads();
     for (int t = T - 1; t >= 0; t--) {
-#pragma unroll
-        for (int y = 0; y < kY; y++) {
-            const int x = tid + kThreads * y;
-            if (x < Mb * kH) {
-                const int m = x >> 6, u = x & 63;
-                const double iv = pi[y], fv = pf[y], ov = po[y], gv = pg[y], c = pc[y], cp = pcp[y];
-                const double dh = s_dh[x] + pdx[y];
-                const double tc = tanh(c);
-                const double d_o = dh * tc;
-                const double dcv = s_dc[x] + dh * ov * (1.0 - tc * tc);
-                const double di = dcv * gv;
-                const double dg = dcv * iv;
-                const double df = dcv * cp;
-                s_dc[x] = dcv * fv;
-                const double da_i = di * iv * (1.0 - iv);
-                const double da_f = df * fv * (1.0 - fv);
-                const double da_o = d_o * ov * (1.0 - ov);
-                const double da_g = dg * (1.0 - gv * gv);
-                double *sd = s_da + m * 4 * kDaLd;
-                sd[u] = da_i;
-                sd[kDaLd + u] = da_f;
-                sd[2 * kDaLd + u] = da_o;
-                sd[3 * kDaLd + u] = da_g;
-                double *g = gates + ((size_t)(q0 + m) * T + t) * kG;
-                g[u] = da_i;
-                g[kH + u] = da_f;
-                g[2 * kH + u] = da_o;
-                g[3 * kH + u] = da_g;
-            }
+        if (live) {
+            const double iv = pi, fv = pf, ov = po, gv = pg, c = pc, cp = pcp;
+            const double dh = s_dh[x] + pdx;
+            const double tc = tanh(c);
+            const double d_o = dh * tc;
+            const double dcv = s_dc[x] + dh * ov * (1.0 - tc * tc);
+            const double di = dcv * gv;
+            const double dg = dcv * iv;
+            const double df = dcv * cp;
+            s_dc[x] = dcv * fv;
+            const double da_i = di * iv * (1.0 - iv);
+            const double da_f = df * fv * (1.0 - fv);
+            const double da_o = d_o * ov * (1.0 - ov);
+            const double da_g = dg * (1.0 - gv * gv);
+            double *sd = s_da + xm * 4 * kDaLd + dslot;
+            sd[0] = da_i;
+            sd[kDaLd] = da_f;
+            sd[2 * kDaLd] = da_o;
+            sd[3 * kDaLd] = da_g;
+            double *g = gates + ((size_t)(q0 + xm) * T + t) * kG;
+            g[xu] = da_i;
+            g[kH + xu] = da_f;
+            g[2 * kH + xu] = da_o;
+            g[3 * kH + xu] = da_g;
         }
         prefetch(t - 1);  // overlaps the barrier + mat-vec below
         __syncthreads();
         for (int m = 0; m < Mb; m++) {
-            const double2 *sd = reinterpret_cast<const double2 *>(s_da + (m * 4 + part) * kDaLd);
+            const double2 *sd =
+                reinterpret_cast<const double2 *>(s_da + (m * 4 + (part >> 1)) * kDaLd + (part & 1) * kDaHalf);
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-            for (int i = 0; i < kH / 2; i += 2) {
+            for (int i = 0; i < 16; i += 2) {
                 const double2 v0 = sd[i], v1 = sd[i + 1];
                 a0 = fma(w[2 * i], v0.x, a0);
                 a1 = fma(w[2 * i + 1], v0.y, a1);
@@ -614,14 +612,15 @@ __global__ void __launch_bounds__(kThreads, 1) lstm_bwd_kernel(
             double v = (a0 + a1) + (a2 + a3);
             v += __shfl_xor_sync(0xffffffffu, v, 1);
             v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
             if (part == 0) s_dh[m * kH + r] = v;
         }
         __syncthreads();
     }
-    for (int x = tid; x < Mb * kH; x += kThreads) {
-        const int m = x >> 6, u = x & 63;
-        dh_out[(size_t)(q0 + m) * kH + u] = s_dh[x];
-        dc_out[(size_t)(q0 + m) * kH + u] = s_dc[x];
+    for (int y = tid; y < Mb * kH; y += kLstmThreads) {
+        const int m = y >> 6, u = y & 63;
+        dh_out[(size_t)(q0 + m) * kH + u] = s_dh[y];
+        dc_out[(size_t)(q0 + m) * kH + u] = s_dc[y];
     }
 }
 
@@ -762,18 +761,27 @@ __global__ void dec_finalize_kernel(PolicyDims dm, const double *__restrict__ P,
 }
 
 // sum over samples of the decoder's dh/dc at step 0 -> encoder final state grads
-// dst[j] = sum_r w[r] * src[r, j]  (w == NULL: weights 1)
-__global__ void sum_rows_kernel(const double *__restrict__ src, int n_rows, double *__restrict__ dst,
-                                const double *__restrict__ w) {
-    const int j = threadIdx.x;  // 64
+// dst[j] = sum_r w[r] * src[r, j]  (w == NULL: weights 1); 512 threads =
+// 64 columns x 8 row-slices, fixed-order combine
+__global__ void __launch_bounds__(512) sum_rows_kernel(const double *__restrict__ src, int n_rows,
+                                                       double *__restrict__ dst, const double *__restrict__ w) {
+    __shared__ double part[8][kH];
+    const int j = threadIdx.x & 63, s = threadIdx.x >> 6;
     double v0 = 0.0, v1 = 0.0;
-    int r = 0;
-    for (; r + 2 <= n_rows; r += 2) {
+    int r = s;
+    for (; r + 8 < n_rows; r += 16) {
         v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
-        v1 = fma(w ? w[r + 1] : 1.0, src[(size_t)(r + 1) * kH + j], v1);
+        v1 = fma(w ? w[r + 8] : 1.0, src[(size_t)(r + 8) * kH + j], v1);
     }
     if (r < n_rows) v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
-    dst[j] = v0 + v1;
+    part[s][j] = v0 + v1;
+    __syncthreads();
+    if (s == 0) {
+        double v = part[0][j];
+#pragma unroll
+        for (int q = 1; q < 8; q++) v += part[q][j];
+        dst[j] = v;
+    }
 }
 
 // B5: w_enc / b_enc grads (contraction over T) and the type-embedding scatter.
@@ -922,7 +930,7 @@ int run_b2(dp_policy *p, const double *params, int K, cudaStream_t st) {
     if (M > kMaxSeqPerCta) M = kMaxSeqPerCta;
     const size_t smem = lstm_bwd_smem(M);
     DP_CUDA_TRY(allow_big_smem((const void *)lstm_bwd_kernel, smem));
-    lstm_bwd_kernel<<<ceil_div(K, M), kThreads, smem, st>>>(
+    lstm_bwd_kernel<<<ceil_div(K, M), kLstmThreads, smem, st>>>(
         dm.T, K, M, params + dm.off.w_dec + (size_t)dm.dd * kG, p->act_g, p->act_c, p->enc_c + (size_t)(dm.T - 1) * kH,
         p->row_dhx, nullptr, nullptr, p->dh0, p->dc0);
     DP_LAUNCH_CHECK();
@@ -944,13 +952,13 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
     DP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {
         cudaStream_t ss = p->side;
-        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dh0, K, dhc_sum, adv);
+        sum_rows_kernel<<<1, 512, 0, ss>>>(p->dh0, K, dhc_sum, adv);
         DP_LAUNCH_CHECK();
-        sum_rows_kernel<<<1, kH, 0, ss>>>(p->dc0, K, dhc_sum + kH, adv);
+        sum_rows_kernel<<<1, 512, 0, ss>>>(p->dc0, K, dhc_sum + kH, adv);
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, ss));
         const size_t smem = lstm_bwd_smem(1);
-        lstm_bwd_kernel<<<1, kThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
+        lstm_bwd_kernel<<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
                                                    p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
                                                    dhc_sum + 2 * kH, dhc_sum + 3 * kH);
         DP_LAUNCH_CHECK();
