@@ -552,27 +552,33 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     // elementwise slot of this thread: x = tid (M <= 8 -> Mb*64 <= 512)
     const int x = tid, xm = x >> 6, xu = x & 63;
     const bool live = x < Mb * kH;
-    double pi = 0, pf = 0, po = 0, pg = 0, pc = 0, pcp = 0, pdx = 0;
-    auto prefetch = [&](int t) {
+    // two-deep register prefetch (rotating cur <- nxt): step t-1's operands were
+    // issued a whole step earlier, t-2's are issued while step t runs
+    struct Ops {
+        double i, f, o, g, c, cp, dx;
+    };
+    Ops cur{0, 0, 0, 0, 0, 0, 0}, nxt{0, 0, 0, 0, 0, 0, 0};
+    auto load = [&](int t, Ops &d) {
         if (live && t >= 0) {
             const size_t row = (size_t)(q0 + xm) * T + t;
             const double *g = gates + row * kG;
-            pi = g[xu];
-            pf = g[kH + xu];
-            po = g[2 * kH + xu];
-            pg = g[3 * kH + xu];
-            pc = cst[row * kH + xu];
-            pcp = t > 0 ? cst[(row - 1) * kH + xu] : c_init[xu];
-            pdx = dh_ext[row * kH + xu];
+            d.i = g[xu];
+            d.f = g[kH + xu];
+            d.o = g[2 * kH + xu];
+            d.g = g[3 * kH + xu];
+            d.c = cst[row * kH + xu];
+            d.cp = t > 0 ? cst[(row - 1) * kH + xu] : c_init[xu];
+            d.dx = dh_ext[row * kH + xu];
         }
     };
-    prefetch(T - 1);
+    load(T - 1, cur);
+    load(T - 2, nxt);
     const int dslot = (xu >> 5) * kDaHalf + (xu & 31);
     __syncthreads();
     for (int t = T - 1; t >= 0; t--) {
         if (live) {
-            const double iv = pi, fv = pf, ov = po, gv = pg, c = pc, cp = pcp;
-            const double dh = s_dh[x] + pdx;
+            const double iv = cur.i, fv = cur.f, ov = cur.o, gv = cur.g, c = cur.c, cp = cur.cp;
+            const double dh = s_dh[x] + cur.dx;
             const double tc = tanh(c);
             const double d_o = dh * tc;
             const double dcv = s_dc[x] + dh * ov * (1.0 - tc * tc);
@@ -595,7 +601,8 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
             g[2 * kH + xu] = da_o;
             g[3 * kH + xu] = da_g;
         }
-        prefetch(t - 1);  // overlaps the barrier + mat-vec below
+        cur = nxt;
+        load(t - 2, nxt);  // lands during this and the next step's barrier + mat-vec
         __syncthreads();
         for (int m = 0; m < Mb; m++) {
             const double2 *sd =
