@@ -46,6 +46,16 @@ constexpr int kChunk = 64;  // B1: enc rows per chunk
 constexpr int kPad = 65;
 constexpr int kRedSlicesW = 8;  // weighted_reduce slices
 
+// 16-byte global -> shared async copy (LDGSTS); valid == false zero-fills.
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // ------------------------------------------------------------------ B0
 // partial per CTA: [b_out (D) | dev_table[:D] (D*dd) | w_out (128*dd)]
 struct PrepSmem {
@@ -643,10 +653,11 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
                                                                 double *__restrict__ partial,
                                                                 const double *__restrict__ adv) {
     extern __shared__ __align__(16) double sm[];
-    double *s_h = sm;                        // [kTile][64]
-    double *s_da = s_h + kTile * kH;         // [kTile][256]
-    double *s_dasum = s_da + kTile * kG;     // [(D+1)][256]
-    __shared__ int s_prev[kTile];
+    double *s_h = sm;                            // [2][kTile][64]   (cp.async double buffer)
+    double *s_da = s_h + 2 * kTile * kH;         // [2][kTile][256]
+    double *s_dasum = s_da + 2 * kTile * kG;     // [(D+1)][256]
+    __shared__ int s_prev[2][kTile];
+    __shared__ double s_w[2][kTile];             // per-row advantage (1 when already scaled)
     const int tid = threadIdx.x;
     const int T = dm.T, D = dm.D;
     const int lb = tid >> 5, jl = tid & 31;
@@ -658,44 +669,58 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
     for (int p = 0; p <= D; p++) s_dasum[p * kG + tid] = 0.0;
     const int n_tiles = (rows + kTile - 1) / kTile;
     const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
-    for (int tl = t0; tl < t1; tl++) {
+    // async copy of tile tl into buffer b (16-byte cp.async, zero-fill past the end)
+    auto stage = [&](int tl, int b) {
         const int rb = tl * kTile;
-        __syncthreads();
-        for (int x = tid; x < kTile * kH; x += kThreads) {
+        double *h = s_h + b * kTile * kH, *d = s_da + b * kTile * kG;
+        for (int x = tid * 2; x < kTile * kH; x += kThreads * 2) {
             const int r = x >> 6, l = x & 63, row = rb + r;
-            double v = 0.0;
-            if (row < rows) {
-                const int t = row % T;
-                v = t > 0 ? act_h[(size_t)(row - 1) * kH + l] : enc_h[(size_t)(T - 1) * kH + l];
-            }
-            s_h[x] = v;
+            const bool ok = row < rows;
+            const double *src = enc_h + (size_t)(T - 1) * kH + l;
+            if (ok && row % T > 0) src = act_h + (size_t)(row - 1) * kH + l;
+            cp_async16(h + x, src, ok);
         }
-        for (int x = tid; x < kTile * kG; x += kThreads) {
+        for (int x = tid * 2; x < kTile * kG; x += kThreads * 2) {
             const int row = rb + (x >> 8);
-            const double v = row < rows ? da[(size_t)rb * kG + x] : 0.0;
-            s_da[x] = (adv && row < rows) ? adv[row / T] * v : v;  // grads-only: da is unscaled
+            cp_async16(d + x, da + (size_t)rb * kG + (row < rows ? x : 0), row < rows);
         }
         if (tid < kTile) {
             const int row = rb + tid;
             int pv = D;
             if (row < rows && row % T > 0) pv = choice[row - 1];
-            s_prev[tid] = pv;
+            s_prev[b][tid] = pv;
+            s_w[b][tid] = row < rows ? (adv ? adv[row / T] : 1.0) : 0.0;
+        }
+        cp_async_commit();
+    };
+    if (t0 < t1) stage(t0, 0);
+    for (int tl = t0; tl < t1; tl++) {
+        const int b = (tl - t0) & 1;
+        const int rb = tl * kTile;
+        if (tl + 1 < t1) {
+            stage(tl + 1, b ^ 1);  // next tile in flight while this one is used
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
         __syncthreads();
+        const double *h = s_h + b * kTile * kH, *d = s_da + b * kTile * kG;
 #pragma unroll 2
         for (int r = 0; r < kTile; r++) {
+            const double wr = s_w[b][r];  // grads-only: da is unscaled -> scale h
             double hv[8], dv[8];
 #pragma unroll
-            for (int a = 0; a < 8; a++) hv[a] = s_h[r * kH + lb * 8 + a];
+            for (int a = 0; a < 8; a++) hv[a] = wr * h[r * kH + lb * 8 + a];
 #pragma unroll
-            for (int b = 0; b < 8; b++) dv[b] = s_da[r * kG + jl + 32 * b];
+            for (int c = 0; c < 8; c++) dv[c] = d[r * kG + jl + 32 * c];
 #pragma unroll
             for (int a = 0; a < 8; a++)
 #pragma unroll
-                for (int b = 0; b < 8; b++) acc[a][b] = fma(hv[a], dv[b], acc[a][b]);
+                for (int c = 0; c < 8; c++) acc[a][c] = fma(hv[a], dv[c], acc[a][c]);
         }
         const int nr = min(kTile, rows - rb);
-        for (int r = 0; r < nr; r++) s_dasum[s_prev[r] * kG + tid] += s_da[r * kG + tid];
+        for (int r = 0; r < nr; r++) s_dasum[s_prev[b][r] * kG + tid] += s_w[b][r] * d[r * kG + tid];
+        __syncthreads();  // buffer b is re-staged by the next iteration
     }
     const size_t base = (size_t)blockIdx.x * (kH + D + 1) * kG;
 #pragma unroll
@@ -981,7 +1006,7 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
     // B3
     {
         const Grid g = tiles_grid(rows, kTile);
-        const size_t smem = sizeof(double) * ((size_t)kTile * (kH + kG) + (size_t)(dm.D + 1) * kG);
+        const size_t smem = sizeof(double) * ((size_t)2 * kTile * (kH + kG) + (size_t)(dm.D + 1) * kG);
         DP_CUDA_TRY(allow_big_smem((const void *)dec_wgrad_kernel, smem));
         dec_wgrad_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->act_h, p->enc_h, p->act_choice,
                                                            p->act_g, part, adv);
