@@ -31,7 +31,16 @@ sys.path.insert(0, ROOT)
 
 METRIC = "placements sampled+scored/sec"
 UNIT = "placements/s"
-CFG_FILE = {"C1": "cfg_C1.npz", "C2": "cfg_C2.npz", "C3": "cfg_C3.npz", "C5": "cfg_C5.npz"}
+CFG_FILE = {"C1": "cfg_C1.npz", "C2": "cfg_C2.npz", "C3": "cfg_C3.npz", "C3tight": "cfg_C3tight.npz",
+            "C5": "cfg_C5.npz"}
+CFG_DESC = {
+    "C1": "rnnlm_grid L2 S16 -> 100 co-location groups, 252 group edges, cpu+1gpu",
+    "C2": "nmt_attention L4 S11 -> 243 co-location groups, 853 group edges, cpu+4gpu",
+    "C3": "inception_blocks B18 br4 -> 256 co-location groups, 454 group edges, 4 simulated GPUs "
+          "(rate 10, 65536 B/s links)",
+    "C3tight": "C3 graph, 30 MiB per simulated GPU (memory-tight)",
+    "C5": "random DAG 20k ops -> 2000 groups, 5969 group edges, cpu+7gpu",
+}
 
 
 def parse():
@@ -140,7 +149,7 @@ def fp64_peak_tflops(nat, torch):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_baseline(gg, topo, k_sample=None, workers=None):
+def cpu_baseline(gg, topo, k_sample=None, workers=None, name="C3"):
     sys.path.insert(0, ROOT)
     from oracle.trainer import cpu_step_rate
 
@@ -148,7 +157,7 @@ def cpu_baseline(gg, topo, k_sample=None, workers=None):
     k_sample = k_sample or 2 * workers
     r = cpu_step_rate(gg, topo, k_sample, workers=workers)
     return {"value": r["rate"], "unit": UNIT, "cores": r["workers"], "kind": "port",
-            "sample": f"{r['placements']} placements of config C3 (sample+score+grad per placement, "
+            "sample": f"{r['placements']} placements of config {name} (sample+score+grad per placement, "
                       f"oracle/ numpy fp64 + C simulator restatement, {r['workers']} processes), "
                       f"{r['seconds']:.2f} s; per-placement cost is K-independent"}
 
@@ -174,8 +183,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{args.config}: inception_blocks B18 br4 (256 groups), "
-                                                    f"4 simulated GPUs, K={K}", "parallelism": "cpu processes"},
+        "data": "synthetic", "config": {"workload": f"{args.config}: {CFG_DESC[args.config]}, K={K}",
+                                    "parallelism": "cpu processes"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
                          "sample": f"{args.steps} steps x {k_sample} placements (sample+score+grad), "
                                    f"oracle port of the reference (numpy fp64 + C simulator)"},
@@ -345,7 +354,7 @@ def main():
     cpu = None
     if world == 1 and not args.skip_cpu:
         try:
-            cpu = cpu_baseline(gg, topo, args.cpu_sample)
+            cpu = cpu_baseline(gg, topo, args.cpu_sample, name=args.config)
         except Exception as ex:  # pragma: no cover
             cpu = {"error": repr(ex)}
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -354,8 +363,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: inception_blocks B18 br4 -> 256 co-location groups, "
-                               f"454 group edges, 4 simulated GPUs (rate 10, 65536 B/s links)",
+        "config": {"workload": f"{args.config}: {CFG_DESC[args.config]}",
                    "k_per_gpu": k_gpu, "global_k": K, "decoder_len": T, "parallelism": f"dp{world} (K sharded)",
                    "l2": "flushed between timed steps (256 MiB write)",
                    "cuda_graph": use_graph},

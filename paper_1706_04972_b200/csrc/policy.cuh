@@ -40,13 +40,16 @@ struct dp_policy {
     double *enc_g;  // [T*G]   gate activations i,f,o,g
     double *edev;   // [(D+1)*G] dev_table @ w_dec[:dd] + b_dec (decoder input projection)
     // decoder activations, [k][t][...] (the opaque forward cache)
-    double *act_h, *act_c, *act_g, *act_ctx, *act_u, *act_p, *act_stat;
+    double *act_h, *act_c, *act_g, *act_u, *act_p, *act_stat;
+    double *act_uc;       // [k*T*dd] ctx @ W_out[64:] (the context enters u, and the backward, only through it)
+    double *proj, *encW;  // [T*64] enc @ W_att^T, [T*dd] enc @ W_out[64:] (decoder prologue, per snapshot)
     double *act_lz;       // [k*T*2] (zs[choice], sum exp zs) -> log-prob terms off the critical path
     uint8_t *act_choice;  // [k*T] by rank
     double *act_logp;     // [k]
     int last_K;
     // backward scratch
     double *row_q, *row_dctx, *row_w, *row_dq, *row_dhx;  // per (k,t)
+    double *row_du;                                      // [k*T*dd] du = dev_table[:D]^T dz
     double *dh0, *dc0;                                   // [k*H]
     double *d_enc;                                       // [T*H]
     double *da_enc;                                      // [T*G]
@@ -54,6 +57,9 @@ struct dp_policy {
     size_t partial_elems;
     double *gacc;                                        // [P] accumulator
     double *tile_part;            // [k*ceil(T/64)][T][64] per-tile d_enc partials (split backward), NULL if too large
+    double *tile_partA;           // [k*ceil(T/64)][T][dd] per-tile A = alpha^T du partials (split backward)
+    double *partA;                // [2*SMs][T][dd] per-CTA A partials (fused backward)
+    double *a_tot;                // [T][dd] A = sum_rows alpha^T du
     int rows_ready;               // K of the last dp_policy_backward_rows (0: none)
     // side stream: the encoder backward (one CTA) overlaps the decoder weight-gradient GEMM
     cudaStream_t side;

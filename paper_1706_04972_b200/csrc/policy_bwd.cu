@@ -63,7 +63,7 @@ struct PrepSmem {
     double woutT[kMaxDD * 2 * kH]; // W_out^T [o][i]
     double devt[kMaxD * kMaxDD];   // dev_table[:D] [d][o]
     double h[kTile * kPad];        // [r][l]
-    double ctx[kTile * kPad];
+    double uc[kTile * (kMaxDD + 1)];  // ctx @ W_out[64:]
     double dctx[kTile * kPad];
     double u[kTile * (kMaxDD + 1)];
     double du[kTile * (kMaxDD + 1)];
@@ -73,9 +73,10 @@ struct PrepSmem {
 __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     PolicyDims dm, const double *__restrict__ P, int rows, int tiles_per_cta, const double *__restrict__ adv,
     const double *__restrict__ act_p, const uint8_t *__restrict__ choice, const double *__restrict__ act_u,
-    const double *__restrict__ act_h, const double *__restrict__ act_ctx, double *__restrict__ row_q,
+    const double *__restrict__ act_h, const double *__restrict__ act_uc, double *__restrict__ row_q,
     double *__restrict__ row_dctx, double *__restrict__ row_w, double *__restrict__ row_dhx,
-    double *__restrict__ partial, int mode /* kFused | kRowsOnly (adv := 1) | kGradsOnly */) {
+    double *__restrict__ row_du, double *__restrict__ partial,
+    int mode /* kFused | kRowsOnly (adv := 1) | kGradsOnly */) {
     extern __shared__ __align__(16) double smraw[];
     PrepSmem &S = *reinterpret_cast<PrepSmem *>(smraw);
     const bool rows_out = mode != kGradsOnly, grads_out = mode != kRowsOnly;
@@ -89,10 +90,10 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     }
     for (int x = tid; x < D * dd; x += kThreads) S.devt[x] = P[dm.off.dev_table + x];
     // owned grad accumulators
-    const int gi = tid >> 1, go = tid & 1;  // w_out grad: row i = gi, cols o = go + 2x
-    double gw[kMaxDD / 2];
+    const int gi = tid >> 2, go = tid & 3;  // w_out grad (h rows): row i = gi, cols o = go + 4x
+    double gw[kMaxDD / 4];
 #pragma unroll
-    for (int x = 0; x < kMaxDD / 2; x++) gw[x] = 0.0;
+    for (int x = 0; x < kMaxDD / 4; x++) gw[x] = 0.0;
     double gdev[4] = {0.0, 0.0, 0.0, 0.0};  // dev grad: e = tid + 256*y < D*dd
     double gb = 0.0;                         // b_out: tid < D
     const int n_tiles = (rows + kTile - 1) / kTile;
@@ -104,11 +105,11 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             const int r = x >> 6, j = x & 63, row = rb + r;
             const bool ok = row < rows;
             S.h[r * kPad + j] = ok ? act_h[(size_t)row * kH + j] : 0.0;
-            S.ctx[r * kPad + j] = ok ? act_ctx[(size_t)row * kH + j] : 0.0;
         }
         for (int x = tid; x < kTile * dd; x += kThreads) {
             const int r = x / dd, o = x % dd, row = rb + r;
             S.u[r * ddp + o] = row < rows ? act_u[(size_t)row * dd + o] : 0.0;
+            S.uc[r * ddp + o] = row < rows ? act_uc[(size_t)row * dd + o] : 0.0;
         }
         for (int x = tid; x < kTile * D; x += kThreads) {
             const int r = x / D, d = x % D, row = rb + r;
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             double v = 0.0;
             for (int d = 0; d < D; d++) v = fma(S.devt[d * dd + o], S.dz[r * Dp + d], v);
             S.du[r * ddp + o] = v;
+            if (rows_out && rb + r < rows) row_du[(size_t)(rb + r) * dd + o] = v;
         }
         if (rows_out) {
             const int r = tid >> 3, jb = tid & 7;
@@ -170,14 +172,15 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             }
         }
         __syncthreads();
-        // w = ctx . dctx (8 lanes per row)
+        // w = ctx . dctx == (ctx W_out[64:]) . du = uc . du  (8 lanes per row)
         if (rows_out) {
             const int r = tid >> 3, jb = tid & 7;
             double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-            for (int x = 0; x < 8; x += 2) {
-                s0 = fma(S.ctx[r * kPad + jb + 8 * x], S.dctx[r * kPad + jb + 8 * x], s0);
-                s1 = fma(S.ctx[r * kPad + jb + 8 * x + 8], S.dctx[r * kPad + jb + 8 * x + 8], s1);
+            for (int x = 0; x < kMaxDD / 8; x += 2) {
+                const int o0 = jb + 8 * x, o1 = o0 + 8;
+                if (o0 < dd) s0 = fma(S.uc[r * ddp + o0], S.du[r * ddp + o0], s0);
+                if (o1 < dd) s1 = fma(S.uc[r * ddp + o1], S.du[r * ddp + o1], s1);
             }
             double s = s0 + s1;
             s += __shfl_xor_sync(0xffffffffu, s, 1);
@@ -187,12 +190,12 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             if (rows_out && jb == 0 && row < rows) row_w[row] = s;
         }
         if (!grads_out) continue;
-        // grads over the tile's rows
+        // grads over the tile's rows (w_out h-half; the ctx half is enc^T A, att_fin_kernel)
         for (int r = 0; r < kTile; r++) {
-            const double hc = gi < kH ? S.h[r * kPad + gi] : S.ctx[r * kPad + gi - kH];
+            const double hc = S.h[r * kPad + gi];
 #pragma unroll
-            for (int x = 0; x < kMaxDD / 2; x++) {
-                const int o = go + 2 * x;
+            for (int x = 0; x < kMaxDD / 4; x++) {
+                const int o = go + 4 * x;
                 if (o < dd) gw[x] = fma(hc, S.du[r * ddp + o], gw[x]);
             }
         }
@@ -219,8 +222,8 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
         if (e < D * dd) out[D + e] = gdev[y];
     }
 #pragma unroll
-    for (int x = 0; x < kMaxDD / 2; x++) {
-        const int o = go + 2 * x;
+    for (int x = 0; x < kMaxDD / 4; x++) {
+        const int o = go + 4 * x;
         if (o < dd) out[D + D * dd + gi * dd + o] = gw[x];
     }
 }
@@ -234,6 +237,7 @@ struct AttSmem {
     double dc[kAttTile * kPad];
     double al[kAttTile * kPad];
     double ds[kAttTile * kPad];
+    double du[kAttTile * (kMaxDD + 1)];
     double mx[kAttTile], sm[kAttTile], w[kAttTile];
 };
 
@@ -242,12 +246,14 @@ struct AttSmem {
 __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
     const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ row_dctx,
-    const double *__restrict__ row_w, double *__restrict__ row_dq, double *__restrict__ partial,
-    double *__restrict__ tile_partial /* [n_tiles][T][64] or NULL */, int do_denc) {
+    const double *__restrict__ row_w, const double *__restrict__ row_du, double *__restrict__ row_dq,
+    double *__restrict__ partial, double *__restrict__ partA,
+    double *__restrict__ tile_partial /* [n_tiles][T][64] or NULL */,
+    double *__restrict__ tile_partA /* [n_tiles][T][dd] */, int do_denc) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
     const int tid = threadIdx.x;
-    const int T = dm.T;
+    const int T = dm.T, dd = dm.dd, ddp = dd + 1;
     const int n_chunks = (T + kChunk - 1) / kChunk;
     // tiles never straddle two samples: tile = (sample k, 64-step block)
     const int tps = (T + kAttTile - 1) / kAttTile;
@@ -262,11 +268,13 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             const int i = x >> 6, j = x & 63;
             S.enc[i * kPad + j] = (i0 + i < T) ? enc_h[(size_t)(i0 + i) * kH + j] : 0.0;
         }
-        double dE[4][4];
+        double dE[4][4], dA[4][2];
 #pragma unroll
-        for (int a = 0; a < 4; a++)
+        for (int a = 0; a < 4; a++) {
 #pragma unroll
             for (int b = 0; b < 4; b++) dE[a][b] = 0.0;
+            dA[a][0] = dA[a][1] = 0.0;
+        }
         for (int tl = tile0; tl < tile1; tl++) {
             const int t0 = (tl % tps) * kAttTile;
             const int rb = (tl / tps) * T + t0;
@@ -278,6 +286,10 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 const bool ok = r < nrow;
                 S.q[r * kPad + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
                 S.dc[r * kPad + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
+            }
+            for (int x = tid; x < kAttTile * dd; x += kThreads) {
+                const int r = x / dd, o = x - r * dd;
+                S.du[r * ddp + o] = r < nrow ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
             }
             if (tid < kAttTile) {
                 const int row = rb + tid;
@@ -354,25 +366,28 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     }
                 }
             }
-            // dE[i, j] += sum_r al[r, i] dc[r, j] + ds[r, i] q[r, j]
+            // d_enc[i, j] += sum_r ds[r, i] q[r, j]  and  A[i, o] += sum_r al[r, i] du[r, o]
+            // (the reference's alpha^T dctx term is A W_out[64:]^T, formed once in att_fin_kernel)
             if (!do_denc) continue;
 #pragma unroll 2
             for (int r = 0; r < kAttTile; r++) {
-                double av[4], sv4[4], dcv[4], qv[4];
+                double av[4], sv4[4], duv[2], qv[4];
 #pragma unroll
                 for (int a = 0; a < 4; a++) {
                     av[a] = S.al[r * kPad + ei + 16 * a];
                     sv4[a] = S.ds[r * kPad + ei + 16 * a];
                 }
 #pragma unroll
-                for (int b = 0; b < 4; b++) {
-                    dcv[b] = S.dc[r * kPad + ej + 16 * b];
-                    qv[b] = S.q[r * kPad + ej + 16 * b];
+                for (int b = 0; b < 4; b++) qv[b] = S.q[r * kPad + ej + 16 * b];
+                duv[0] = S.du[r * ddp + ej];
+                duv[1] = ej + 16 < dd ? S.du[r * ddp + ej + 16] : 0.0;
+#pragma unroll
+                for (int a = 0; a < 4; a++) {
+#pragma unroll
+                    for (int b = 0; b < 4; b++) dE[a][b] = fma(sv4[a], qv[b], dE[a][b]);
+                    dA[a][0] = fma(av[a], duv[0], dA[a][0]);
+                    dA[a][1] = fma(av[a], duv[1], dA[a][1]);
                 }
-#pragma unroll
-                for (int a = 0; a < 4; a++)
-#pragma unroll
-                    for (int b = 0; b < 4; b++) dE[a][b] = fma(sv4[a], qv[b], fma(av[a], dcv[b], dE[a][b]));
             }
             if (tile_partial) {
                 // rows-only pass: this tile's (unscaled) contribution, weighted by
@@ -385,6 +400,12 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                         if (i < T) tile_partial[((size_t)tl * T + i) * kH + ej + 16 * b] = dE[a][b];
                         dE[a][b] = 0.0;
                     }
+#pragma unroll
+                    for (int b = 0; b < 2; b++) {
+                        const int o = ej + 16 * b;
+                        if (i < T && o < dd) tile_partA[((size_t)tl * T + i) * dd + o] = dA[a][b];
+                        dA[a][b] = 0.0;
+                    }
                 }
             }
         }
@@ -396,6 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 #pragma unroll
                     for (int b = 0; b < 4; b++)
                         partial[((size_t)blockIdx.x * T + i) * kH + ej + 16 * b] = dE[a][b];
+#pragma unroll
+                    for (int b = 0; b < 2; b++)
+                        if (ej + 16 * b < dd) partA[((size_t)blockIdx.x * T + i) * dd + ej + 16 * b] = dA[a][b];
                 }
             }
         }
@@ -431,6 +455,43 @@ __global__ void __launch_bounds__(256) weighted_reduce_kernel(const double *__re
         for (int q = 1; q < kRedSlicesW; q++) v += part[q][el];
         dst[e] = v;
     }
+}
+
+// ------------------------------------------------------------------ B1a
+// With A = sum_rows alpha^T du (T x dd, advantage-weighted):
+//   d_enc[i, j] += sum_o A[i, o] W_out[64 + j, o]   (== sum_rows alpha^T dctx)
+//   grad w_out[64 + j, o] = sum_i enc[i, j] A[i, o] (== sum_rows ctx^T du, policy.py:385)
+// Blocks [0, nb) do the first (thread per d_enc element), the rest the second.
+__global__ void __launch_bounds__(256) att_fin_kernel(PolicyDims dm, const double *__restrict__ P,
+                                                      const double *__restrict__ enc_h, const double *__restrict__ A,
+                                                      double *__restrict__ d_enc, double *__restrict__ grad, int nb) {
+    const int T = dm.T, dd = dm.dd;
+    const double *w2 = P + dm.off.w_out + (size_t)kH * dd;
+    if ((int)blockIdx.x < nb) {
+        const int e = blockIdx.x * 256 + threadIdx.x;
+        if (e >= T * kH) return;
+        const int i = e >> 6, j = e & 63;
+        double v0 = 0.0, v1 = 0.0;
+        int o = 0;
+        for (; o + 2 <= dd; o += 2) {
+            v0 = fma(A[(size_t)i * dd + o], w2[(size_t)j * dd + o], v0);
+            v1 = fma(A[(size_t)i * dd + o + 1], w2[(size_t)j * dd + o + 1], v1);
+        }
+        if (o < dd) v0 = fma(A[(size_t)i * dd + o], w2[(size_t)j * dd + o], v0);
+        d_enc[e] += v0 + v1;
+        return;
+    }
+    const int e = (blockIdx.x - nb) * 256 + threadIdx.x;
+    if (e >= kH * dd) return;
+    const int j = e / dd, o = e - j * dd;
+    double v0 = 0.0, v1 = 0.0;
+    int i = 0;
+    for (; i + 2 <= T; i += 2) {
+        v0 = fma(enc_h[(size_t)i * kH + j], A[(size_t)i * dd + o], v0);
+        v1 = fma(enc_h[(size_t)(i + 1) * kH + j], A[(size_t)(i + 1) * dd + o], v1);
+    }
+    if (i < T) v0 = fma(enc_h[(size_t)i * kH + j], A[(size_t)i * dd + o], v0);
+    grad[dm.off.w_out + (size_t)kH * dd + e] = v0 + v1;
 }
 
 // ------------------------------------------------------------------ B1f
@@ -917,6 +978,14 @@ Grid att_grid(int K, int T) {
     return {ceil_div(n_tiles, per), per};
 }
 
+int run_att_fin(dp_policy *p, const double *params, double *grad, cudaStream_t st) {
+    const PolicyDims &dm = p->dims;
+    const int nb = ceil_div(dm.T * kH, 256);
+    att_fin_kernel<<<nb + ceil_div(kH * dm.dd, 256), 256, 0, st>>>(dm, params, p->enc_h, p->a_tot, p->d_enc, grad, nb);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
 // B0 in the given mode (+ its reductions when it produces gradients)
 int run_b0(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
            cudaStream_t st) {
@@ -925,8 +994,8 @@ int run_b0(dp_policy *p, const double *params, int rows, const double *adv, doub
     const size_t smem = sizeof(PrepSmem);
     DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
     row_prep_kernel<<<g.n_used, kThreads, smem, st>>>(dm, params, rows, g.per, adv, p->act_p, p->act_choice, p->act_u,
-                                                      p->act_h, p->act_ctx, p->row_q, p->row_dctx, p->row_w,
-                                                      p->row_dhx, p->partial, mode);
+                                                      p->act_h, p->act_uc, p->row_q, p->row_dctx, p->row_w,
+                                                      p->row_dhx, p->row_du, p->partial, mode);
     DP_LAUNCH_CHECK();
     if (mode == kRowsOnly) return DP_OK;
     const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
@@ -935,7 +1004,7 @@ int run_b0(dp_policy *p, const double *params, int rows, const double *adv, doub
     DP_LAUNCH_CHECK();
     launch_reduce(part + dm.D, g.n_used, na, dm.D * dm.dd, grad + dm.off.dev_table, 0, st);
     DP_LAUNCH_CHECK();
-    launch_reduce(part + dm.D + dm.D * dm.dd, g.n_used, na, 2 * kH * dm.dd, grad + dm.off.w_out, 0, st);
+    launch_reduce(part + dm.D + dm.D * dm.dd, g.n_used, na, kH * dm.dd, grad + dm.off.w_out, 0, st);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
@@ -1048,10 +1117,14 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
         const size_t smem = sizeof(AttSmem);
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
         att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, nullptr, 1);
+                                                         p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
+                                                         p->partA, nullptr, nullptr, 1);
         DP_LAUNCH_CHECK();
         launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
         DP_LAUNCH_CHECK();
+        launch_reduce(p->partA, g.n_used, (size_t)T * dm.dd, T * dm.dd, p->a_tot, 0, st);
+        DP_LAUNCH_CHECK();
+        DP_TRY(run_att_fin(p, params, grad, st));
     }
     DP_TRY(run_b1f(p, params, rows, nullptr, grad, kFused, st));
     DP_TRY(run_b2(p, params, K, st));
@@ -1076,8 +1149,8 @@ extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32
         const size_t smem = sizeof(AttSmem);
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
         att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                         p->row_dctx, p->row_w, p->row_dq, p->partial, p->tile_part,
-                                                         1);
+                                                         p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
+                                                         p->partA, p->tile_part, p->tile_partA, 1);
         DP_LAUNCH_CHECK();
     }
     DP_TRY(run_b1f(p, params, rows, nullptr, nullptr, kRowsOnly, st));
@@ -1103,7 +1176,11 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
         weighted_reduce_kernel<<<ceil_div(T * kH, 32), 256, 0, st>>>(p->tile_part, K * tps, (size_t)T * kH, T * kH,
                                                                      p->d_enc, adv, tps);
         DP_LAUNCH_CHECK();
+        weighted_reduce_kernel<<<ceil_div(T * dm.dd, 32), 256, 0, st>>>(p->tile_partA, K * tps, (size_t)T * dm.dd,
+                                                                        T * dm.dd, p->a_tot, adv, tps);
+        DP_LAUNCH_CHECK();
     }
+    DP_TRY(run_att_fin(p, params, grad, st));
     DP_TRY(run_b1f(p, params, rows, adv, grad, kGradsOnly, st));
     return run_b345(p, params, K, adv, grad, st);
 }

@@ -168,7 +168,37 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- decoder
-constexpr int kEncLd = 66;  // enc_states row stride in shared memory: 16-byte rows, conflict-free LDS.128
+// Per-snapshot decoder prologue, shared by all K samples (once per update):
+//   proj = enc_states @ W_att^T    [T x 64]  (policy.py:287 — the reference's own order)
+//   encW = enc_states @ W_out[64:] [T x dd]  (ctx @ W_out[64:] == alpha @ encW, so the
+//                                            step's context never has to be formed)
+__global__ void dec_prep_kernel(PolicyDims dm, const double *__restrict__ params, const double *__restrict__ enc_h,
+                                double *__restrict__ proj, double *__restrict__ encW) {
+    __shared__ double e[kH];
+    const int t = blockIdx.x, tid = threadIdx.x, dd = dm.dd;
+    if (tid < kH) e[tid] = enc_h[(size_t)t * kH + tid];
+    __syncthreads();
+    double a0 = 0.0, a1 = 0.0;
+    if (tid < kH) {
+        const double *w = params + dm.off.w_att + (size_t)tid * kH;  // W_att[l][:]
+        for (int j = 0; j < kH; j += 2) {
+            a0 = fma(e[j], w[j], a0);
+            a1 = fma(e[j + 1], w[j + 1], a1);
+        }
+        proj[(size_t)t * kH + tid] = a0 + a1;
+    } else if (tid < kH + dd) {
+        const int o = tid - kH;
+        const double *w = params + dm.off.w_out + (size_t)kH * dd + o;  // W_out[64 + j][o]
+        for (int j = 0; j < kH; j += 2) {
+            a0 = fma(e[j], w[(size_t)j * dd], a0);
+            a1 = fma(e[j + 1], w[(size_t)(j + 1) * dd], a1);
+        }
+        encW[(size_t)t * dd + o] = a0 + a1;
+    }
+}
+
+constexpr int kProjLd = 66;  // proj row stride in shared memory: 16-byte rows, conflict-free LDS.128
+constexpr int kWarps = kThreads / 32;
 
 struct DecArgs {
     PolicyDims dm;
@@ -180,29 +210,40 @@ struct DecArgs {
     const long long *draw_counter;
     long long draws_per_count;
     const uint8_t *forced;
-    const double *enc_h, *enc_c, *edev;
-    double *act_h, *act_c, *act_g, *act_ctx, *act_u, *act_p, *act_stat, *act_lz;
+    const double *enc_h, *enc_c, *edev, *proj, *encW;
+    double *act_h, *act_c, *act_g, *act_uc, *act_u, *act_p, *act_stat, *act_lz;
     uint8_t *choice, *choice_out;
     double *logp, *probs_out;
     int M, Tpad;
     // shared-memory offsets (doubles)
-    int o_enc, o_watt, o_wout, o_devt, o_bout, o_edev, o_h, o_q, o_ctx, o_c, o_u, o_p, o_alpha, o_red,
-        o_red2, o_pcg, o_misc;
+    int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_u, o_uh, o_p, o_alpha, o_pm, o_ps, o_puc, o_pcg,
+        o_misc;
 };
 
-constexpr int kCtxParts = 8;
-constexpr int kWoutLd = 2 * kH + 8;  // W_out^T row stride in shared memory (== 8 mod 16 doubles)
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 
-// One CTA owns M samples for all T decode steps.  Per step:
-//   A  gates = edev[prev] + h.W_h (thread per gate column, W_h in registers),
-//      LSTM cell, h/c/gates to the activation store
-//   B  q = W_att^T h
-//   C  s_i = enc_i . q (row per thread), softmax over T (block max, block sum)
-//   D  ctx = (sum_i e_i enc_i) / sum  (lane pairs over j, 8 row-parts)
-//   E  warp per sample: u = [h; ctx] W_out, z = dev_table[:D] u + b_out,
-//      p = softmax(z), PCG64 draw, cdf search -> choice; the log-prob term's
-//      log() is deferred to the end of the kernel (off the per-step path)
-template <int MT, bool ES>
+// One CTA owns M samples for all T decode steps; three barriers per step:
+//   A  gates = edev[prev] + g (g = h_{t-1} W_h, computed during the previous
+//      step's phase C, off the critical path), LSTM cell -> h
+//   C  (every warp, its own rows i) s_i = proj_i . h, warp-local softmax
+//      statistics (max m_w, sum l_w) and the partial uc_w = sum_i e_i encW_i;
+//      alongside: next step's g = h W_h (register W_h columns) and
+//      uh = h W_out[:64]
+//   E  warp per sample: online-softmax combine of the 8 warp partials
+//      (M = max m_w, l = sum l_w e^{m_w - M}, uc = sum uc_w e^{m_w - M} / l),
+//      u = uh + uc, logits, softmax over devices, PCG64 draw, cdf search.
+// The context vector itself is not formed (the backward works from uc, and
+// dW_out[64:] = enc^T (sum alpha^T du)); the log-prob log() is deferred.
+template <int MT, bool PS>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -211,37 +252,34 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     const int k0 = blockIdx.x * M;
     const int Mb = min(M, a.K - k0);
     const double *P = a.params;
-    constexpr int LD = ES ? kEncLd : kH;
-    const double *enc = ES ? (const double *)(sm + a.o_enc) : a.enc_h;
-    double *watt = sm + a.o_watt;
-    double *wout = sm + a.o_wout;
+    constexpr int LD = PS ? kProjLd : kH;
+    const double *proj = PS ? (const double *)(sm + a.o_proj) : a.proj;
+    const double *encW = PS ? (const double *)(sm + a.o_encw) : a.encW;
+    double *wout1 = sm + a.o_wout;  // W_out[:64] [64][dd]
     double *devt = sm + a.o_devt;
     double *bout = sm + a.o_bout;
     double *edev = sm + a.o_edev;
-    double *hS = sm + a.o_h;       // [2][M][64]
-    double *qS = sm + a.o_q;       // [M][64]
-    double *ctxS = sm + a.o_ctx;   // [M][64]
-    double *cS = sm + a.o_c;       // [M][64]
-    double *uS = sm + a.o_u;       // [M][32]
-    double *pS = sm + a.o_p;       // [M][32]
-    double *alS = sm + a.o_alpha;  // [M][Tpad] unnormalised e_i
-    double *red = sm + a.o_red;    // [2][8][MT]
-    double *red2 = sm + a.o_red2;  // [8 parts][M][64]
+    double *hS = sm + a.o_h;        // [M][64]
+    double *uS = sm + a.o_u;        // [M][32]
+    double *uhS = sm + a.o_uh;      // [M][32]
+    double *pS = sm + a.o_p;        // [M][32]
+    double *alS = sm + a.o_alpha;   // [M][Tpad] scores -> e_i
+    double *pmx = sm + a.o_pm;      // [8][M] warp max
+    double *psm = sm + a.o_ps;      // [8][M] warp sum
+    double *puc = sm + a.o_puc;     // [8][M][dd] warp uc partials
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);                               // [M]
 
-    // ---- stage weights ----
-    if (ES)
-        for (int i = tid; i < T * kH; i += kThreads) sm[a.o_enc + (i >> 6) * kEncLd + (i & 63)] = a.enc_h[i];
-    for (int i = tid; i < kH * kH; i += kThreads) watt[i] = P[dm.off.w_att + i];
-    for (int i = tid; i < 2 * kH * dd; i += kThreads) wout[(i % dd) * kWoutLd + i / dd] = P[dm.off.w_out + i];
+    // ---- stage the snapshot-constant operands ----
+    if (PS) {
+        for (int i = tid; i < T * kH; i += kThreads) sm[a.o_proj + (i >> 6) * kProjLd + (i & 63)] = a.proj[i];
+        for (int i = tid; i < T * dd; i += kThreads) sm[a.o_encw + i] = a.encW[i];
+    }
+    for (int i = tid; i < kH * dd; i += kThreads) wout1[i] = P[dm.off.w_out + i];
     for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
     for (int i = tid; i < D; i += kThreads) bout[i] = P[dm.off.b_out + i];
     for (int i = tid; i < (D + 1) * kG; i += kThreads) edev[i] = a.edev[i];
-    for (int i = tid; i < Mb * kH; i += kThreads) {
-        hS[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
-        cS[i] = a.enc_c[(size_t)(T - 1) * kH + (i & 63)];
-    }
+    for (int i = tid; i < Mb * kH; i += kThreads) hS[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
     if (tid < Mb) {
         prev[tid] = D;
         if (!a.forced) {
@@ -260,10 +298,23 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
         for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
     }
+    // cell state of unit u, owned (in registers) by the unit's gate-0 thread
+    double cst[MT];
+    {
+        const double c0 = a.enc_c[(size_t)(T - 1) * kH + u];
+#pragma unroll
+        for (int m = 0; m < MT; m++) cst[m] = c0;
+    }
     __syncthreads();
+    // g = h W_h for the coming step (identical initial state for every sample)
+    double gn[MT];
+    {
+        const double g0 = dot64_sh_reg(hS, w);
+#pragma unroll
+        for (int m = 0; m < MT; m++) gn[m] = g0;
+    }
 
     const int base = lane & ~3;
-    const int Tp = (T + kCtxParts - 1) / kCtxParts;
     int d_pow2 = 1;
     while (d_pow2 < D) d_pow2 <<= 1;
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
@@ -276,19 +327,13 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         clk_last = now_;                                  \
     }
     for (int t = 0; t < T; t++) {
-        const int cur = t & 1;
         // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
         {
-            // stage-separated over the M samples so their transcendental chains overlap;
-            // one divergence-free activation path for all 4 gates (gate_act)
-            double av[MT], act[MT], cn[MT];
-#pragma unroll
-            for (int m = 0; m < MT; m++)
-                if (m < Mb) av[m] = edev[prev[m] * kG + col] + dot64_sh_reg(hS + (cur * M + m) * kH, w);
+            double act[MT], cn[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) {
-                    act[m] = gate_act(av[m], gate == 3);
+                    act[m] = gate_act(edev[prev[m] * kG + col] + gn[m], gate == 3);
                     a.act_g[((size_t)(k0 + m) * T + t) * kG + col] = act[m];
                 }
 #pragma unroll
@@ -298,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     const double fv = __shfl_sync(0xffffffffu, act[m], base + 1);
                     const double ov = __shfl_sync(0xffffffffu, act[m], base + 2);
                     const double gv = __shfl_sync(0xffffffffu, act[m], base + 3);
-                    cn[m] = fv * cS[m * kH + u] + iv * gv;
+                    cn[m] = fv * cst[m] + iv * gv;
                     act[m] = ov;
                 }
 #pragma unroll
@@ -306,147 +351,91 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 if (m < Mb && gate == 0) {
                     const double hn = act[m] * tanh_x(cn[m]);
                     const size_t row = (size_t)(k0 + m) * T + t;
-                    cS[m * kH + u] = cn[m];
-                    hS[((cur ^ 1) * M + m) * kH + u] = hn;
+                    cst[m] = cn[m];
+                    hS[m * kH + u] = hn;
                     a.act_h[row * kH + u] = hn;
                     a.act_c[row * kH + u] = cn[m];
                 }
         }
         __syncthreads();
         DP_PHASE(0);
-        const double *hN = hS + (cur ^ 1) * M * kH;
-        // ---- B: q = W_att^T h ----
-        for (int idx = tid; idx < Mb * kH; idx += kThreads) {
-            const int m = idx >> 6, j = idx & 63;
-            const double2 *hv = reinterpret_cast<const double2 *>(hN + m * kH);
-            double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
+        // ---- C: scores s = proj @ h (policy.py:296), warp-local softmax stats + uc partials ----
+        if (t + 1 < T) {
 #pragma unroll
-            for (int l2 = 0; l2 < kH / 2; l2 += 2) {
-                const double2 h0 = hv[l2], h1 = hv[l2 + 1];
-                q0 = fma(watt[(2 * l2) * kH + j], h0.x, q0);
-                q1 = fma(watt[(2 * l2 + 1) * kH + j], h0.y, q1);
-                q2 = fma(watt[(2 * l2 + 2) * kH + j], h1.x, q2);
-                q3 = fma(watt[(2 * l2 + 3) * kH + j], h1.y, q3);
-            }
-            qS[idx] = (q0 + q1) + (q2 + q3);
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) gn[m] = dot64_sh_reg(hS + m * kH, w);
         }
-        __syncthreads();
-        DP_PHASE(1);
-        // ---- C: scores s_i = enc_i . q, softmax over T (policy.py:296-299) ----
-        double mx[MT];
+        double lmx[MT], lsm[MT];
 #pragma unroll
-        for (int m = 0; m < MT; m++) mx[m] = -INFINITY;
+        for (int m = 0; m < MT; m++) {
+            lmx[m] = -INFINITY;
+            lsm[m] = 0.0;
+        }
         for (int i = tid; i < T; i += kThreads) {
-            const double2 *er = reinterpret_cast<const double2 *>(enc + (size_t)i * LD);
+            const double2 *pr = reinterpret_cast<const double2 *>(proj + (size_t)i * LD);
             double s0[MT], s1[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++) s0[m] = s1[m] = 0.0;
 #pragma unroll 8
             for (int j2 = 0; j2 < kH / 2; j2++) {
-                const double2 e = er[j2];
+                const double2 e = pr[j2];
 #pragma unroll
                 for (int m = 0; m < MT; m++) {
-                    const double2 qq = reinterpret_cast<const double2 *>(qS + m * kH)[j2];
-                    s0[m] = fma(e.x, qq.x, s0[m]);
-                    s1[m] = fma(e.y, qq.y, s1[m]);
+                    const double2 hh = reinterpret_cast<const double2 *>(hS + m * kH)[j2];
+                    s0[m] = fma(e.x, hh.x, s0[m]);
+                    s1[m] = fma(e.y, hh.y, s1[m]);
                 }
             }
 #pragma unroll
-            for (int m = 0; m < MT; m++) {
+            for (int m = 0; m < MT; m++)
                 if (m < Mb) {
                     const double s = s0[m] + s1[m];
                     alS[m * a.Tpad + i] = s;
-                    mx[m] = fmax(mx[m], s);
+                    lmx[m] = fmax(lmx[m], s);
                 }
-            }
         }
 #pragma unroll
-        for (int m = 0; m < MT; m++) {
-            double v = mx[m];
-            for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if (lane == 0) red[warp * MT + m] = v;
-        }
-        __syncthreads();
-        DP_PHASE(2);
-        double gmax[MT], sm_[MT];
-#pragma unroll
-        for (int m = 0; m < MT; m++) {
-            double v = red[m];
-#pragma unroll
-            for (int ww = 1; ww < kThreads / 32; ww++) v = fmax(v, red[ww * MT + m]);
-            gmax[m] = v;
-            sm_[m] = 0.0;
-        }
+        for (int m = 0; m < MT; m++) lmx[m] = warp_max(lmx[m]);
         for (int i = tid; i < T; i += kThreads) {
 #pragma unroll
-            for (int m = 0; m < MT; m++) {
+            for (int m = 0; m < MT; m++)
                 if (m < Mb) {
-                    const double e = exp(alS[m * a.Tpad + i] - gmax[m]);
+                    const double e = exp(alS[m * a.Tpad + i] - lmx[m]);
                     alS[m * a.Tpad + i] = e;
-                    sm_[m] += e;
+                    lsm[m] += e;
                 }
-            }
         }
 #pragma unroll
-        for (int m = 0; m < MT; m++) {
-            double v = sm_[m];
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) red[8 * MT + warp * MT + m] = v;
-        }
-        __syncthreads();
-        DP_PHASE(3);
-        // ---- D: ctx = alpha @ enc (policy.py:300), alpha = e / sum ----
-        {
-            const int jp = tid & 31, part = tid >> 5;
-            const int i0 = part * Tp, i1 = min(T, i0 + Tp);
-            double ax[MT], ay[MT];
-#pragma unroll
-            for (int m = 0; m < MT; m++) ax[m] = ay[m] = 0.0;
-            for (int i = i0; i < i1; i++) {
-                const double2 e = *reinterpret_cast<const double2 *>(enc + (size_t)i * LD + 2 * jp);
-#pragma unroll
-                for (int m = 0; m < MT; m++) {
-                    const double al = alS[m * a.Tpad + i];
-                    ax[m] = fma(al, e.x, ax[m]);
-                    ay[m] = fma(al, e.y, ay[m]);
+        for (int m = 0; m < MT; m++) lsm[m] = warp_sum(lsm[m]);
+        __syncwarp();
+        // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
+        for (int pi = lane; pi < Mb * dd; pi += 32) {
+            const int m = pi / dd, j = pi - m * dd;
+            const double *al = alS + m * a.Tpad;
+            double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+            for (int i0 = warp * 32; i0 < T; i0 += kThreads) {
+                const int n = min(32, T - i0);
+                int ii = 0;
+                for (; ii + 4 <= n; ii += 4) {
+                    const int i = i0 + ii;
+                    c0 = fma(al[i], encW[(size_t)i * dd + j], c0);
+                    c1 = fma(al[i + 1], encW[(size_t)(i + 1) * dd + j], c1);
+                    c2 = fma(al[i + 2], encW[(size_t)(i + 2) * dd + j], c2);
+                    c3 = fma(al[i + 3], encW[(size_t)(i + 3) * dd + j], c3);
                 }
+                for (; ii < n; ii++) c0 = fma(al[i0 + ii], encW[(size_t)(i0 + ii) * dd + j], c0);
             }
+            puc[(warp * M + m) * dd + j] = (c0 + c1) + (c2 + c3);
+        }
+        if (lane == 0) {
 #pragma unroll
             for (int m = 0; m < MT; m++)
-                if (m < Mb)
-                    *reinterpret_cast<double2 *>(red2 + (part * M + m) * kH + 2 * jp) = make_double2(ax[m], ay[m]);
-        }
-        __syncthreads();
-        DP_PHASE(4);
-        for (int idx = tid; idx < Mb * kH; idx += kThreads) {
-            const int m = idx >> 6, j = idx & 63;
-            double gs = red[8 * MT + m];
-#pragma unroll
-            for (int ww = 1; ww < kThreads / 32; ww++) gs += red[8 * MT + ww * MT + m];
-            double v = red2[m * kH + j];
-#pragma unroll
-            for (int p = 1; p < kCtxParts; p++) v += red2[(p * M + m) * kH + j];
-            v = v / gs;
-            ctxS[idx] = v;
-            const size_t row = (size_t)(k0 + m) * T + t;
-            a.act_ctx[row * kH + j] = v;
-        }
-        if (tid < Mb) {
-            // softmax stats for the backward's recompute of alpha
-            const size_t row = (size_t)(k0 + tid) * T + t;
-#pragma unroll
-            for (int m = 0; m < MT; m++)
-                if (m == tid) {
-                    double gs = red[8 * MT + m];
-#pragma unroll
-                    for (int ww = 1; ww < kThreads / 32; ww++) gs += red[8 * MT + ww * MT + m];
-                    a.act_stat[row * 2] = gmax[m];
-                    a.act_stat[row * 2 + 1] = gs;
+                if (m < Mb) {
+                    pmx[warp * M + m] = lmx[m];
+                    psm[warp * M + m] = lsm[m];
                 }
         }
-        __syncthreads();
-        DP_PHASE(5);
-        // ---- E1: u = [h; ctx] @ W_out for all samples, 8 lanes per output ----
+        // uh = h @ W_out[:64] (policy.py:302, h half), 8 lanes per output
         {
             const int total = Mb * dd * 8;
             for (int b0 = 0; b0 < total; b0 += kThreads) {
@@ -455,35 +444,59 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 double part = 0.0;
                 int m = 0, o = 0;
                 if (ok) {
-                    // lane part pp sums i = pp + 8i' over [h; ctx]; W_out^T rows of
-                    // kWoutLd (== 8 mod 16) doubles -> conflict-free half-warps
                     const int pair = idx >> 3, pp = idx & 7;
                     m = pair / dd;
                     o = pair - m * dd;
-                    const double *hv = hN + m * kH + pp, *cv = ctxS + m * kH + pp;
-                    const double *wc = wout + o * kWoutLd + pp;
+                    const double *hv = hS + m * kH + pp;
+                    const double *wc = wout1 + (size_t)pp * dd + o;
                     double p0 = 0.0, p1 = 0.0;
 #pragma unroll
-                    for (int i = 0; i < 8; i++) {
-                        p0 = fma(hv[8 * i], wc[8 * i], p0);
-                        p1 = fma(cv[8 * i], wc[kH + 8 * i], p1);
+                    for (int y = 0; y < 8; y += 2) {
+                        p0 = fma(hv[8 * y], wc[(size_t)8 * y * dd], p0);
+                        p1 = fma(hv[8 * y + 8], wc[(size_t)(8 * y + 8) * dd], p1);
                     }
                     part = p0 + p1;
                 }
                 part += __shfl_xor_sync(0xffffffffu, part, 4);
                 part += __shfl_xor_sync(0xffffffffu, part, 2);
                 part += __shfl_xor_sync(0xffffffffu, part, 1);
-                if (ok && (idx & 7) == 0) {
-                    uS[m * 32 + o] = part;
-                    a.act_u[((size_t)(k0 + m) * T + t) * dd + o] = part;
-                }
+                if (ok && (idx & 7) == 0) uhS[m * 32 + o] = part;
             }
         }
         __syncthreads();
-        DP_PHASE(6);
-        // ---- E2: logits, softmax over devices, draw (policy.py:301-308, 320-323) ----
-        for (int m = warp; m < Mb; m += kThreads / 32) {
+        DP_PHASE(1);
+        // ---- E: combine, u, logits, softmax over devices, draw (policy.py:297-308, 320-323) ----
+        for (int m = warp; m < Mb; m += kWarps) {
             const size_t row = (size_t)(k0 + m) * T + t;
+            const double pm = lane < kWarps ? pmx[lane * M + m] : -INFINITY;
+            double gmx = pm;
+#pragma unroll
+            for (int o = kWarps >> 1; o > 0; o >>= 1) gmx = fmax(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+            gmx = __shfl_sync(0xffffffffu, gmx, 0);
+            const double f = lane < kWarps ? exp(pm - gmx) : 0.0;
+            double ls = lane < kWarps ? psm[lane * M + m] * f : 0.0;
+#pragma unroll
+            for (int o = kWarps >> 1; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+            const double gsum = __shfl_sync(0xffffffffu, ls, 0);
+            double fw[kWarps];
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
+            if (lane < dd) {
+                double uc = 0.0;
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lane], fw[ww], uc);
+                const double ucn = uc / gsum;
+                const double uv = uhS[m * 32 + lane] + ucn;
+                uS[m * 32 + lane] = uv;
+                a.act_u[row * dd + lane] = uv;
+                a.act_uc[row * dd + lane] = ucn;
+            }
+            if (lane == 0) {
+                // softmax stats (max, sum) for the backward's recompute of alpha
+                a.act_stat[row * 2] = gmx;
+                a.act_stat[row * 2 + 1] = gsum;
+            }
+            __syncwarp();
             double z = -INFINITY;
             if (lane < D) {
                 double z0 = 0.0, z1 = 0.0;
@@ -542,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             }
         }
         __syncthreads();
-        DP_PHASE(7);
+        DP_PHASE(2);
     }
 #undef DP_PHASE
     // ---- log p = sum_t (zs[c_t] - log sum_t): logs in parallel, sum in t order ----
@@ -594,10 +607,10 @@ static ParamLayout layout_of(int V1, int D, int dd, int F, int td) {
 extern "C" void dp_policy_destroy(dp_policy *p) {
     if (!p) return;
     void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
-                    p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_ctx, p->act_u, p->act_p,
+                    p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
-                    p->tile_part};
+                    p->tile_part, p->tile_partA, p->partA, p->a_tot};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p->side) cudaStreamDestroy(p->side);
@@ -682,7 +695,10 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     alloc((void **)&p->act_h, sizeof(double) * rows * kH);
     alloc((void **)&p->act_c, sizeof(double) * rows * kH);
     alloc((void **)&p->act_g, sizeof(double) * rows * kG);
-    alloc((void **)&p->act_ctx, sizeof(double) * rows * kH);
+    alloc((void **)&p->act_uc, sizeof(double) * rows * dev_dim);
+    alloc((void **)&p->row_du, sizeof(double) * rows * dev_dim);
+    alloc((void **)&p->proj, sizeof(double) * T * kH);
+    alloc((void **)&p->encW, sizeof(double) * T * dev_dim);
     alloc((void **)&p->act_u, sizeof(double) * rows * dev_dim);
     alloc((void **)&p->act_p, sizeof(double) * rows * n_dev);
     alloc((void **)&p->act_stat, sizeof(double) * rows * 2);
@@ -707,7 +723,12 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     // the fused pass)
     const size_t tiles = (size_t)k_max * ((T + 63) / 64);
     const size_t part_bytes = sizeof(double) * tiles * (size_t)T * kH;
-    if (ok && part_bytes <= (size_t)2 << 30) alloc((void **)&p->tile_part, part_bytes);
+    if (ok && part_bytes <= (size_t)2 << 30) {
+        alloc((void **)&p->tile_part, part_bytes);
+        alloc((void **)&p->tile_partA, sizeof(double) * tiles * (size_t)T * dev_dim);
+    }
+    alloc((void **)&p->partA, sizeof(double) * 2 * kNumSMs * (size_t)T * dev_dim);
+    alloc((void **)&p->a_tot, sizeof(double) * (size_t)T * dev_dim);
     if (!ok) {
         dp::set_error(std::string("dp_policy_create: allocation/upload failed: ") +
                       cudaGetErrorString(cudaGetLastError()));
@@ -766,6 +787,8 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
     DP_LAUNCH_CHECK();
     enc_rec_kernel<<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
     DP_LAUNCH_CHECK();
+    dec_prep_kernel<<<dm.T, 128, 0, st>>>(dm, params, p->enc_h, p->proj, p->encW);
+    DP_LAUNCH_CHECK();
     return DP_OK;
 }
 
@@ -792,22 +815,21 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
                 o += (n + 1) & ~1;
                 return r;
             };
-            a.o_enc = enc_smem ? take(T * kEncLd) : 0;
-            a.o_watt = take(kH * kH);
-            a.o_wout = take(kWoutLd * dm.dd);
+            const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+            a.o_proj = enc_smem ? take(T * kProjLd) : 0;
+            a.o_encw = enc_smem ? take(T * dm.dd) : 0;
+            a.o_wout = take(kH * dm.dd);
             a.o_devt = take(dm.D * dm.dd);
             a.o_bout = take(dm.D);
             a.o_edev = take((dm.D + 1) * kG);
-            a.o_h = take(2 * M * kH);
-            a.o_q = take(M * kH);
-            a.o_ctx = take(M * kH);
-            a.o_c = take(M * kH);
+            a.o_h = take(M * kH);
             a.o_u = take(M * 32);
+            a.o_uh = take(M * 32);
             a.o_p = take(M * 32);
             a.o_alpha = take(M * Tpad);
-            const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
-            a.o_red = take(2 * 8 * MT);
-            a.o_red2 = take(kCtxParts * M * kH);
+            a.o_pm = take(kWarps * M);
+            a.o_ps = take(kWarps * M);
+            a.o_puc = take(kWarps * M * dm.dd);
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + M);
             const size_t bytes = (size_t)o * sizeof(double);
@@ -857,10 +879,12 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.enc_h = p->enc_h;
     a.enc_c = p->enc_c;
     a.edev = p->edev;
+    a.proj = p->proj;
+    a.encW = p->encW;
     a.act_h = p->act_h;
     a.act_c = p->act_c;
     a.act_g = p->act_g;
-    a.act_ctx = p->act_ctx;
+    a.act_uc = p->act_uc;
     a.act_u = p->act_u;
     a.act_p = p->act_p;
     a.act_stat = p->act_stat;

@@ -469,18 +469,24 @@ def _make_task(gg, topo, config: TrainerConfig) -> _TrainTask:
     return _TrainTask(gg, topo, feats, template, reward_spec, config)
 
 
-def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, seed_seq) -> _ControllerResult:
-    """``pkg/trainer.py:256-309`` on the device (CUDA-graph replay after update 0)."""
+def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, seed_seq,
+                   world=None) -> _ControllerResult:
+    """``pkg/trainer.py:256-309`` on the device (CUDA-graph replay after update 0).
+
+    ``world=(rank, size, group)`` runs this rank's K-shard (parallel.py); the
+    multi-rank step stays eager (collectives are enqueued asynchronously)."""
     import torch
 
     cfg = task.config
-    ctl = DeviceController(task, store, seed_seq, controller_id)
+    ctl = DeviceController(task, store, seed_seq, controller_id, world=world)
+    use_graph = ctl.size == 1
     walls = []
     if cfg.total_updates > 0:
         walls += ctl.run(1, use_graph=False, wall=True)
     if cfg.total_updates > 1:
-        ctl.capture()
-        walls += ctl.run(cfg.total_updates - 1, use_graph=True, wall=True)
+        if use_graph:
+            ctl.capture()
+        walls += ctl.run(cfg.total_updates - 1, use_graph=use_graph, wall=True)
     torch.cuda.current_stream().synchronize()
     ctl.check_errors()
     res = _ControllerResult(rows=ctl.rows(walls))
@@ -488,9 +494,13 @@ def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, 
     return res
 
 
-def train(graph, topo, config: TrainerConfig | None = None) -> TrainResult:
+def train(graph, topo, config: TrainerConfig | None = None, *, group=None) -> TrainResult:
     """Train the policy; return the best feasible placement ever measured
-    (``pkg/trainer.py:341-393``)."""
+    (``pkg/trainer.py:341-393``).
+
+    ``group``: optional torch.distributed process group; every rank calls
+    train() with the same arguments and owns K/size of the samples (one GPU
+    per rank, NCCL).  Every rank returns the same result."""
     from .graph import coalesce_sole_consumers
 
     config = config or TrainerConfig()
@@ -504,7 +514,12 @@ def train(graph, topo, config: TrainerConfig | None = None) -> TrainResult:
                            max_steps=config.total_updates + 1)
     root = np.random.SeedSequence(config.seed)
     seqs = root.spawn(config.controllers)
-    res = run_controller(0, store, task, seqs[0])
+    world = None
+    if group is not None:
+        import torch.distributed as dist
+
+        world = (dist.get_rank(group), dist.get_world_size(group), group)
+    res = run_controller(0, store, task, seqs[0], world=world)
     rows = sorted(res.rows, key=lambda r: (r.controller_id, r.update_index))
     best_pl = list(res.best_placement) if res.best_placement is not None else None
     best_report = simulate(gg, topo, best_pl) if best_pl is not None else None

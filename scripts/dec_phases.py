@@ -29,8 +29,8 @@ eng.decode(pdev, K, pcg=(1, 3))
 torch.cuda.synchronize()
 nat.check(nat.lib().dp_debug_phase_clocks(0, out), "dbg")
 T = len(feats)
-names = ["A gates+cell", "B q", "C scores+max", "C exp+sum", "D ctx partial", "D combine+stats", "E1 u", "E2 tail"]
+names = ["A gates+cell", "C scores/softmax/uc/uh/next-g", "E combine+draw"]
 tot = sum(out)
 print(f"{name} K={K} T={T}: {tot / T:.0f} cycles/step")
-for n, v in zip(names, out):
-    print(f"  {n:18s} {v / T:8.0f} cycles/step  {100 * v / tot:5.1f}%")
+for n, v in zip(names, out[:3]):
+    print(f"  {n:32s} {v / T:8.0f} cycles/step  {100 * v / tot:5.1f}%")
