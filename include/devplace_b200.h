@@ -116,6 +116,11 @@ int dp_policy_encode(dp_policy *p, const double *params, void *stream);
  * decoder (block 0) and read+reset the 8 sums into h_out[8] (may be NULL). */
 int dp_debug_phase_clocks(int32_t enable, int64_t *h_out);
 
+/* Decoder variant override (tests / measurement): 0 = automatic plan,
+ * 1 = force the speculative next-step cell (idle warps evaluate the LSTM
+ * cell for every possible choice during the draw), 2 = forbid it. */
+int dp_debug_decoder_variant(int32_t mode);
+
 /* Copy the assembled encoder inputs of the last encode (embed_groups(),
  * pkg/policy.py:266-268) into out[T*input_dim] (device). */
 int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream);

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
 constexpr int kAttTile = 64;  // rows per tile in att_bwd (2 rows per thread in the S/DA and dq passes)
 
 struct AttSmem {
-    double enc[kChunk * kPad];
+    double enc[2][kChunk * kPad];  // cp.async double buffer over the T chunks
     double q[kAttTile * kPad];
     double dc[kAttTile * kPad];
     double al[kAttTile * kPad];
@@ -241,15 +241,26 @@ struct AttSmem {
     double mx[kAttTile], sm[kAttTile], w[kAttTile];
 };
 
-// Register tiles: S/DA pass 2 rows x 8 enc rows per thread (12 LDS -> 32 FMA),
-// dq pass 2 rows x 8 columns, dE pass 4 x 4 (16 LDS -> 32 FMA).
+// Tile-outer: a CTA owns whole 64-step tiles of one sample; per tile its
+// q / dctx / du / stats are staged once, the 64-row chunks of enc_states
+// stream through a cp.async double buffer, and dq accumulates in registers
+// over the chunks (one store per tile, no read-modify-write).  Per chunk:
+//   S/DA  (2 rows x 8 i per thread) dalpha = dctx . enc_i, alpha (STORED:
+//         e_i * esc from the decoder; else exp(q . enc_i - max) / sum),
+//         ds = alpha (dalpha - w)
+//   dq    += ds @ enc_chunk
+//   dE    d_enc[i, j] = sum_r ds[r, i] q[r, j],  A[i, o] = sum_r alpha[r, i] du[r, o]
+// dE / A go to the per-tile partials (split backward) or accumulate in the
+// CTA's private partial (fused backward).
+template <bool STORED>
 __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
     const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ row_dctx,
     const double *__restrict__ row_w, const double *__restrict__ row_du, double *__restrict__ row_dq,
     double *__restrict__ partial, double *__restrict__ partA,
     double *__restrict__ tile_partial /* [n_tiles][T][64] or NULL */,
-    double *__restrict__ tile_partA /* [n_tiles][T][dd] */, int do_denc) {
+    double *__restrict__ tile_partA /* [n_tiles][T][dd] */, const double *__restrict__ act_e,
+    const double *__restrict__ act_esc, int do_denc) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
     const int tid = threadIdx.x;
@@ -262,44 +273,82 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     const int tile1 = min(n_tiles_total, tile0 + tiles_per_cta);
     const int sr = tid >> 3, ib = tid & 7;  // rows {sr, sr+32}; i (or j) in {ib + 8*ii}
     const int ei = tid >> 4, ej = tid & 15; // dE: i in {ei + 16a}, j in {ej + 16b}
-    for (int ch = 0; ch < n_chunks; ch++) {
-        const int i0 = ch * kChunk;
-        for (int x = tid; x < kChunk * kH; x += kThreads) {
-            const int i = x >> 6, j = x & 63;
-            S.enc[i * kPad + j] = (i0 + i < T) ? enc_h[(size_t)(i0 + i) * kH + j] : 0.0;
+    // enc chunk c -> buffer b (16-byte cp.async; rows past T zero-filled)
+    auto stage_enc = [&](int c, int b) {
+        const int i0 = c * kChunk;
+        for (int x = tid; x < kChunk * (kH / 2); x += kThreads) {
+            const int i = x >> 5, j2 = x & 31;
+            // kPad (65) rows are not 16-byte aligned: copy 8-byte pairs via two 8-byte lanes
+            const bool ok = i0 + i < T;
+            const double *src = enc_h + (size_t)(ok ? i0 + i : 0) * kH + 2 * j2;
+            double *dst = &S.enc[b][i * kPad + 2 * j2];
+            const unsigned s0 = (unsigned)__cvta_generic_to_shared(dst);
+            const unsigned s1 = (unsigned)__cvta_generic_to_shared(dst + 1);
+            const int n = ok ? 8 : 0;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s0), "l"(src), "r"(n) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s1), "l"(src + 1), "r"(n) : "memory");
         }
-        double dE[4][4], dA[4][2];
-#pragma unroll
-        for (int a = 0; a < 4; a++) {
-#pragma unroll
-            for (int b = 0; b < 4; b++) dE[a][b] = 0.0;
-            dA[a][0] = dA[a][1] = 0.0;
+        cp_async_commit();
+    };
+    bool first_cta_tile = true;
+    for (int tl = tile0; tl < tile1; tl++) {
+        const int t0 = (tl % tps) * kAttTile;
+        const int rb = (tl / tps) * T + t0;
+        const int nrow = min(kAttTile, T - t0);
+        __syncthreads();  // previous tile's readers are done with every buffer
+        stage_enc(0, 0);
+        for (int x = tid; x < kAttTile * kH; x += kThreads) {
+            const int r = x >> 6, j = x & 63;
+            const int row = rb + r;
+            const bool ok = r < nrow;
+            S.q[r * kPad + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
+            S.dc[r * kPad + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
         }
-        for (int tl = tile0; tl < tile1; tl++) {
-            const int t0 = (tl % tps) * kAttTile;
-            const int rb = (tl / tps) * T + t0;
-            const int nrow = min(kAttTile, T - t0);
+        for (int x = tid; x < kAttTile * dd; x += kThreads) {
+            const int r = x / dd, o = x - r * dd;
+            S.du[r * ddp + o] = r < nrow ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
+        }
+        if (tid < kAttTile) {
+            const int row = rb + tid;
+            const bool ok = tid < nrow;
+            S.mx[tid] = ok ? act_stat[(size_t)row * 2] : 0.0;
+            S.sm[tid] = ok ? act_stat[(size_t)row * 2 + 1] : 1.0;
+            S.w[tid] = ok ? row_w[row] : 0.0;
+        }
+        double acc[2][8];
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++)
+#pragma unroll
+            for (int jj = 0; jj < 8; jj++) acc[rr][jj] = 0.0;
+        for (int ch = 0; ch < n_chunks; ch++) {
+            const int i0 = ch * kChunk, b = ch & 1;
+            // this thread's stored numerators (issued before the wait: the loads
+            // overlap the chunk's cp.async and the DA mat-mul)
+            double ev[2][8], esc[2][2];
+            if (STORED) {
+#pragma unroll
+                for (int rr = 0; rr < 2; rr++) {
+                    const int r = sr + 32 * rr;
+                    const bool okr = r < nrow;
+                    const size_t row = (size_t)(rb + (okr ? r : 0));
+#pragma unroll
+                    for (int ii = 0; ii < 8; ii++) {
+                        const int ig = i0 + ib + 8 * ii;
+                        ev[rr][ii] = (okr && ig < T) ? __ldg(act_e + row * T + ig) : 0.0;
+                    }
+                    esc[rr][0] = __ldg(act_esc + row * 8 + ((i0 & 255) >> 5));
+                    esc[rr][1] = __ldg(act_esc + row * 8 + (((i0 + 32) & 255) >> 5));
+                }
+            }
+            if (ch + 1 < n_chunks) {
+                stage_enc(ch + 1, b ^ 1);
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
             __syncthreads();
-            for (int x = tid; x < kAttTile * kH; x += kThreads) {
-                const int r = x >> 6, j = x & 63;
-                const int row = rb + r;
-                const bool ok = r < nrow;
-                S.q[r * kPad + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
-                S.dc[r * kPad + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
-            }
-            for (int x = tid; x < kAttTile * dd; x += kThreads) {
-                const int r = x / dd, o = x - r * dd;
-                S.du[r * ddp + o] = r < nrow ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
-            }
-            if (tid < kAttTile) {
-                const int row = rb + tid;
-                const bool ok = tid < nrow;
-                S.mx[tid] = ok ? act_stat[(size_t)row * 2] : 0.0;
-                S.sm[tid] = ok ? act_stat[(size_t)row * 2 + 1] : 1.0;
-                S.w[tid] = ok ? row_w[row] : 0.0;
-            }
-            __syncthreads();
-            // S = Q enc^T, DA = DCTX enc^T over this chunk -> alpha, ds
+            const double *enc = S.enc[b];
+            // [S = Q enc^T,] DA = DCTX enc^T over this chunk -> alpha, ds
             {
                 double sv[2][8], dv[2][8];
 #pragma unroll
@@ -308,15 +357,24 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     for (int ii = 0; ii < 8; ii++) sv[rr][ii] = dv[rr][ii] = 0.0;
 #pragma unroll 2
                 for (int j = 0; j < kH; j++) {
-                    const double q0 = S.q[sr * kPad + j], q1 = S.q[(sr + 32) * kPad + j];
                     const double d0 = S.dc[sr * kPad + j], d1 = S.dc[(sr + 32) * kPad + j];
+                    if (STORED) {
 #pragma unroll
-                    for (int ii = 0; ii < 8; ii++) {
-                        const double e = S.enc[(ib + 8 * ii) * kPad + j];
-                        sv[0][ii] = fma(q0, e, sv[0][ii]);
-                        sv[1][ii] = fma(q1, e, sv[1][ii]);
-                        dv[0][ii] = fma(d0, e, dv[0][ii]);
-                        dv[1][ii] = fma(d1, e, dv[1][ii]);
+                        for (int ii = 0; ii < 8; ii++) {
+                            const double e = enc[(ib + 8 * ii) * kPad + j];
+                            dv[0][ii] = fma(d0, e, dv[0][ii]);
+                            dv[1][ii] = fma(d1, e, dv[1][ii]);
+                        }
+                    } else {
+                        const double q0 = S.q[sr * kPad + j], q1 = S.q[(sr + 32) * kPad + j];
+#pragma unroll
+                        for (int ii = 0; ii < 8; ii++) {
+                            const double e = enc[(ib + 8 * ii) * kPad + j];
+                            sv[0][ii] = fma(q0, e, sv[0][ii]);
+                            sv[1][ii] = fma(q1, e, sv[1][ii]);
+                            dv[0][ii] = fma(d0, e, dv[0][ii]);
+                            dv[1][ii] = fma(d1, e, dv[1][ii]);
+                        }
                     }
                 }
 #pragma unroll
@@ -327,8 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     for (int ii = 0; ii < 8; ii++) {
                         const int i = ib + 8 * ii;
                         double al = 0.0, ds = 0.0;
-                        if (i0 + i < T) {
-                            al = exp(sv[rr][ii] - m) / l;
+                        if (i0 + i < T && r < nrow) {
+                            al = STORED ? ev[rr][ii] * esc[rr][ii >> 2] : exp(sv[rr][ii] - m) / l;
                             ds = al * (dv[rr][ii] - w);
                         }
                         S.al[r * kPad + i] = al;
@@ -337,38 +395,27 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 }
             }
             __syncthreads();
-            // dq[row, j] += sum_i ds[row, i] enc[i, j]
-            {
-                double acc[2][8];
-#pragma unroll
-                for (int rr = 0; rr < 2; rr++)
-#pragma unroll
-                    for (int jj = 0; jj < 8; jj++) acc[rr][jj] = 0.0;
+            // dq[row, j] += sum_i ds[row, i] enc[i, j]   (registers across chunks)
 #pragma unroll 2
-                for (int i = 0; i < kChunk; i++) {
-                    const double d0 = S.ds[sr * kPad + i], d1 = S.ds[(sr + 32) * kPad + i];
+            for (int i = 0; i < kChunk; i++) {
+                const double d0 = S.ds[sr * kPad + i], d1 = S.ds[(sr + 32) * kPad + i];
 #pragma unroll
-                    for (int jj = 0; jj < 8; jj++) {
-                        const double e = S.enc[i * kPad + ib + 8 * jj];
-                        acc[0][jj] = fma(d0, e, acc[0][jj]);
-                        acc[1][jj] = fma(d1, e, acc[1][jj]);
-                    }
-                }
-#pragma unroll
-                for (int rr = 0; rr < 2; rr++) {
-                    const int row = rb + sr + 32 * rr;
-                    if (sr + 32 * rr < nrow) {
-#pragma unroll
-                        for (int jj = 0; jj < 8; jj++) {
-                            double *dst = row_dq + (size_t)row * kH + ib + 8 * jj;
-                            *dst = ch == 0 ? acc[rr][jj] : *dst + acc[rr][jj];
-                        }
-                    }
+                for (int jj = 0; jj < 8; jj++) {
+                    const double e = enc[i * kPad + ib + 8 * jj];
+                    acc[0][jj] = fma(d0, e, acc[0][jj]);
+                    acc[1][jj] = fma(d1, e, acc[1][jj]);
                 }
             }
+            if (!do_denc) continue;
             // d_enc[i, j] += sum_r ds[r, i] q[r, j]  and  A[i, o] += sum_r al[r, i] du[r, o]
             // (the reference's alpha^T dctx term is A W_out[64:]^T, formed once in att_fin_kernel)
-            if (!do_denc) continue;
+            double dE[4][4], dA[4][2];
+#pragma unroll
+            for (int a = 0; a < 4; a++) {
+#pragma unroll
+                for (int bb = 0; bb < 4; bb++) dE[a][bb] = 0.0;
+                dA[a][0] = dA[a][1] = 0.0;
+            }
 #pragma unroll 2
             for (int r = 0; r < kAttTile; r++) {
                 double av[4], sv4[4], duv[2], qv[4];
@@ -378,52 +425,54 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     sv4[a] = S.ds[r * kPad + ei + 16 * a];
                 }
 #pragma unroll
-                for (int b = 0; b < 4; b++) qv[b] = S.q[r * kPad + ej + 16 * b];
+                for (int bb = 0; bb < 4; bb++) qv[bb] = S.q[r * kPad + ej + 16 * bb];
                 duv[0] = S.du[r * ddp + ej];
                 duv[1] = ej + 16 < dd ? S.du[r * ddp + ej + 16] : 0.0;
 #pragma unroll
                 for (int a = 0; a < 4; a++) {
 #pragma unroll
-                    for (int b = 0; b < 4; b++) dE[a][b] = fma(sv4[a], qv[b], dE[a][b]);
+                    for (int bb = 0; bb < 4; bb++) dE[a][bb] = fma(sv4[a], qv[bb], dE[a][bb]);
                     dA[a][0] = fma(av[a], duv[0], dA[a][0]);
                     dA[a][1] = fma(av[a], duv[1], dA[a][1]);
                 }
             }
-            if (tile_partial) {
-                // rows-only pass: this tile's (unscaled) contribution, weighted by
-                // its sample's advantage later (weighted_reduce)
-#pragma unroll
-                for (int a = 0; a < 4; a++) {
-                    const int i = i0 + ei + 16 * a;
-#pragma unroll
-                    for (int b = 0; b < 4; b++) {
-                        if (i < T) tile_partial[((size_t)tl * T + i) * kH + ej + 16 * b] = dE[a][b];
-                        dE[a][b] = 0.0;
-                    }
-#pragma unroll
-                    for (int b = 0; b < 2; b++) {
-                        const int o = ej + 16 * b;
-                        if (i < T && o < dd) tile_partA[((size_t)tl * T + i) * dd + o] = dA[a][b];
-                        dA[a][b] = 0.0;
-                    }
-                }
-            }
-        }
-        if (do_denc && !tile_partial) {
 #pragma unroll
             for (int a = 0; a < 4; a++) {
                 const int i = i0 + ei + 16 * a;
-                if (i < T) {
+                if (i >= T) continue;
+                if (tile_partial) {
+                    // rows-only pass: this tile's (unscaled) contribution, weighted by
+                    // its sample's advantage later (weighted_reduce)
 #pragma unroll
-                    for (int b = 0; b < 4; b++)
-                        partial[((size_t)blockIdx.x * T + i) * kH + ej + 16 * b] = dE[a][b];
+                    for (int bb = 0; bb < 4; bb++) tile_partial[((size_t)tl * T + i) * kH + ej + 16 * bb] = dE[a][bb];
 #pragma unroll
-                    for (int b = 0; b < 2; b++)
-                        if (ej + 16 * b < dd) partA[((size_t)blockIdx.x * T + i) * dd + ej + 16 * b] = dA[a][b];
+                    for (int bb = 0; bb < 2; bb++)
+                        if (ej + 16 * bb < dd) tile_partA[((size_t)tl * T + i) * dd + ej + 16 * bb] = dA[a][bb];
+                } else {
+                    // fused pass: the CTA's private partial (first tile initialises it)
+#pragma unroll
+                    for (int bb = 0; bb < 4; bb++) {
+                        double *d = partial + ((size_t)blockIdx.x * T + i) * kH + ej + 16 * bb;
+                        *d = first_cta_tile ? dE[a][bb] : *d + dE[a][bb];
+                    }
+#pragma unroll
+                    for (int bb = 0; bb < 2; bb++)
+                        if (ej + 16 * bb < dd) {
+                            double *d = partA + ((size_t)blockIdx.x * T + i) * dd + ej + 16 * bb;
+                            *d = first_cta_tile ? dA[a][bb] : *d + dA[a][bb];
+                        }
                 }
             }
+            __syncthreads();  // al / ds / this enc buffer are overwritten by the next chunk
         }
-        __syncthreads();
+#pragma unroll
+        for (int rr = 0; rr < 2; rr++) {
+            const int r = sr + 32 * rr;
+            if (r < nrow)
+#pragma unroll
+                for (int jj = 0; jj < 8; jj++) row_dq[(size_t)(rb + r) * kH + ib + 8 * jj] = acc[rr][jj];
+        }
+        first_cta_tile = false;
     }
 }
 
@@ -481,17 +530,28 @@ __global__ void __launch_bounds__(256) att_fin_kernel(PolicyDims dm, const doubl
         d_enc[e] += v0 + v1;
         return;
     }
-    const int e = (blockIdx.x - nb) * 256 + threadIdx.x;
-    if (e >= kH * dd) return;
-    const int j = e / dd, o = e - j * dd;
+    // 32 outputs x 8 i-slices per block, fixed-order combine (deterministic)
+    __shared__ double part[8][32];
+    const int el = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const int e = (blockIdx.x - nb) * 32 + el;
     double v0 = 0.0, v1 = 0.0;
-    int i = 0;
-    for (; i + 2 <= T; i += 2) {
-        v0 = fma(enc_h[(size_t)i * kH + j], A[(size_t)i * dd + o], v0);
-        v1 = fma(enc_h[(size_t)(i + 1) * kH + j], A[(size_t)(i + 1) * dd + o], v1);
+    if (e < kH * dd) {
+        const int j = e / dd, o = e - j * dd;
+        int i = sl;
+        for (; i + 8 < T; i += 16) {
+            v0 = fma(enc_h[(size_t)i * kH + j], A[(size_t)i * dd + o], v0);
+            v1 = fma(enc_h[(size_t)(i + 8) * kH + j], A[(size_t)(i + 8) * dd + o], v1);
+        }
+        if (i < T) v0 = fma(enc_h[(size_t)i * kH + j], A[(size_t)i * dd + o], v0);
     }
-    if (i < T) v0 = fma(enc_h[(size_t)i * kH + j], A[(size_t)i * dd + o], v0);
-    grad[dm.off.w_out + (size_t)kH * dd + e] = v0 + v1;
+    part[sl][el] = v0 + v1;
+    __syncthreads();
+    if (sl == 0 && e < kH * dd) {
+        double v = part[0][el];
+#pragma unroll
+        for (int q = 1; q < 8; q++) v += part[q][el];
+        grad[dm.off.w_out + (size_t)kH * dd + e] = v;
+    }
 }
 
 // ------------------------------------------------------------------ B1f
@@ -598,6 +658,7 @@ constexpr int kDaLd = 68, kDaHalf = 34;
 
 inline size_t lstm_bwd_smem(int M) { return sizeof(double) * (size_t)M * (2 * kH + 4 * kDaLd); }
 
+template <int MT>
 __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     int T, int n_seq, int M, const double *__restrict__ Wh /* [64 x 256] row-major, ld 256 */,
     double *__restrict__ gates /* [seq][T][256] in: i,f,o,g  out: da */, const double *__restrict__ cst /* [seq][T][64] */,
@@ -624,7 +685,9 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     const int x = tid, xm = x >> 6, xu = x & 63;
     const bool live = x < Mb * kH;
     // two-deep register prefetch (rotating cur <- nxt): step t-1's operands were
-    // issued a whole step earlier, t-2's are issued while step t runs
+    // issued a whole step earlier, t-2's are issued while step t runs; tanh(c)
+    // of the coming step is evaluated inside the mat-vec section, where its
+    // latency overlaps the FMA chains instead of the elementwise critical path
     struct Ops {
         double i, f, o, g, c, cp, dx;
     };
@@ -644,13 +707,13 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     };
     load(T - 1, cur);
     load(T - 2, nxt);
+    double tc = tanh(cur.c);
     const int dslot = (xu >> 5) * kDaHalf + (xu & 31);
     __syncthreads();
     for (int t = T - 1; t >= 0; t--) {
         if (live) {
-            const double iv = cur.i, fv = cur.f, ov = cur.o, gv = cur.g, c = cur.c, cp = cur.cp;
+            const double iv = cur.i, fv = cur.f, ov = cur.o, gv = cur.g, cp = cur.cp;
             const double dh = s_dh[x] + cur.dx;
-            const double tc = tanh(c);
             const double d_o = dh * tc;
             const double dcv = s_dc[x] + dh * ov * (1.0 - tc * tc);
             const double di = dcv * gv;
@@ -675,23 +738,32 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         cur = nxt;
         load(t - 2, nxt);  // lands during this and the next step's barrier + mat-vec
         __syncthreads();
-        for (int m = 0; m < Mb; m++) {
-            const double2 *sd =
-                reinterpret_cast<const double2 *>(s_da + (m * 4 + (part >> 1)) * kDaLd + (part & 1) * kDaHalf);
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        tc = tanh(cur.c);  // independent of the mat-vec below: the two chains interleave
+        double v[MT];
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-                const double2 v0 = sd[i], v1 = sd[i + 1];
-                a0 = fma(w[2 * i], v0.x, a0);
-                a1 = fma(w[2 * i + 1], v0.y, a1);
-                a2 = fma(w[2 * i + 2], v1.x, a2);
-                a3 = fma(w[2 * i + 3], v1.y, a3);
+        for (int m = 0; m < MT; m++) {
+            v[m] = 0.0;
+            if (m < Mb) {
+                const double2 *sd =
+                    reinterpret_cast<const double2 *>(s_da + (m * 4 + (part >> 1)) * kDaLd + (part & 1) * kDaHalf);
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    const double2 v0 = sd[i], v1 = sd[i + 1];
+                    a0 = fma(w[2 * i], v0.x, a0);
+                    a1 = fma(w[2 * i + 1], v0.y, a1);
+                    a2 = fma(w[2 * i + 2], v1.x, a2);
+                    a3 = fma(w[2 * i + 3], v1.y, a3);
+                }
+                v[m] = (a0 + a1) + (a2 + a3);
             }
-            double v = (a0 + a1) + (a2 + a3);
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            v += __shfl_xor_sync(0xffffffffu, v, 4);
-            if (part == 0) s_dh[m * kH + r] = v;
+        }
+#pragma unroll
+        for (int m = 0; m < MT; m++) {
+            v[m] += __shfl_xor_sync(0xffffffffu, v[m], 1);
+            v[m] += __shfl_xor_sync(0xffffffffu, v[m], 2);
+            v[m] += __shfl_xor_sync(0xffffffffu, v[m], 4);
+            if (part == 0 && m < Mb) s_dh[m * kH + r] = v[m];
         }
         __syncthreads();
     }
@@ -700,6 +772,13 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         dh_out[(size_t)(q0 + m) * kH + u] = s_dh[y];
         dc_out[(size_t)(q0 + m) * kH + u] = s_dc[y];
     }
+}
+
+const void *lstm_bwd_fn(int M) {
+    return M <= 1 ? (const void *)lstm_bwd_kernel<1>
+           : M <= 2 ? (const void *)lstm_bwd_kernel<2>
+           : M <= 4 ? (const void *)lstm_bwd_kernel<4>
+                    : (const void *)lstm_bwd_kernel<8>;
 }
 
 // ------------------------------------------------------------------ B3
@@ -972,16 +1051,39 @@ Grid tiles_grid(int rows, int tile) {
 }
 
 Grid att_grid(int K, int T) {
+    // one wave: att_bwd holds ~220 KB of shared memory (1 CTA per SM).  It
+    // leaves kSimSMs SMs free: in the split backward it runs concurrently with
+    // the placement simulator (small latency-bound CTAs that cannot co-reside
+    // with an att_bwd CTA)
+    constexpr int kSimSMs = 20;
     const int n_tiles = K * ((T + kAttTile - 1) / kAttTile);
-    const int n = n_cta_for(n_tiles, 2);
+    const int n = n_tiles < kNumSMs - kSimSMs ? n_tiles : kNumSMs - kSimSMs;
     const int per = ceil_div(n_tiles, n);
     return {ceil_div(n_tiles, per), per};
+}
+
+int launch_att(dp_policy *p, const Grid &g, size_t smem, int rows, double *tile_part, double *tile_partA,
+               cudaStream_t st) {
+    const PolicyDims &dm = p->dims;
+    if (p->act_e) {
+        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<true>, smem));
+        att_bwd_kernel<true><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
+                                                               p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
+                                                               p->partA, tile_part, tile_partA, p->act_e, p->act_esc, 1);
+    } else {
+        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<false>, smem));
+        att_bwd_kernel<false><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
+                                                                p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
+                                                                p->partA, tile_part, tile_partA, nullptr, nullptr, 1);
+    }
+    DP_LAUNCH_CHECK();
+    return DP_OK;
 }
 
 int run_att_fin(dp_policy *p, const double *params, double *grad, cudaStream_t st) {
     const PolicyDims &dm = p->dims;
     const int nb = ceil_div(dm.T * kH, 256);
-    att_fin_kernel<<<nb + ceil_div(kH * dm.dd, 256), 256, 0, st>>>(dm, params, p->enc_h, p->a_tot, p->d_enc, grad, nb);
+    att_fin_kernel<<<nb + ceil_div(kH * dm.dd, 32), 256, 0, st>>>(dm, params, p->enc_h, p->a_tot, p->d_enc, grad, nb);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
@@ -1030,10 +1132,16 @@ int run_b2(dp_policy *p, const double *params, int K, cudaStream_t st) {
     int M = ceil_div(K, kNumSMs);
     if (M > kMaxSeqPerCta) M = kMaxSeqPerCta;
     const size_t smem = lstm_bwd_smem(M);
-    DP_CUDA_TRY(allow_big_smem((const void *)lstm_bwd_kernel, smem));
-    lstm_bwd_kernel<<<ceil_div(K, M), kLstmThreads, smem, st>>>(
-        dm.T, K, M, params + dm.off.w_dec + (size_t)dm.dd * kG, p->act_g, p->act_c, p->enc_c + (size_t)(dm.T - 1) * kH,
-        p->row_dhx, nullptr, nullptr, p->dh0, p->dc0);
+    const void *fn = lstm_bwd_fn(M);
+    DP_CUDA_TRY(allow_big_smem(fn, smem));
+    {
+        int T = dm.T, n_seq = K;
+        const double *Wh = params + dm.off.w_dec + (size_t)dm.dd * kG;
+        const double *c_init = p->enc_c + (size_t)(dm.T - 1) * kH;
+        const double *null = nullptr;
+        void *args[] = {&T, &n_seq, &M, &Wh, &p->act_g, &p->act_c, &c_init, &p->row_dhx, &null, &null, &p->dh0, &p->dc0};
+        DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(ceil_div(K, M)), dim3(kLstmThreads), args, smem, st));
+    }
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
@@ -1059,7 +1167,7 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, ss));
         const size_t smem = lstm_bwd_smem(1);
-        lstm_bwd_kernel<<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
+        lstm_bwd_kernel<1><<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
                                                    p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
                                                    dhc_sum + 2 * kH, dhc_sum + 3 * kH);
         DP_LAUNCH_CHECK();
@@ -1115,11 +1223,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     {
         const Grid g = att_grid(K, T);
         const size_t smem = sizeof(AttSmem);
-        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
-        att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                         p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
-                                                         p->partA, nullptr, nullptr, 1);
-        DP_LAUNCH_CHECK();
+        DP_TRY(launch_att(p, g, smem, rows, nullptr, nullptr, st));
         launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
         DP_LAUNCH_CHECK();
         launch_reduce(p->partA, g.n_used, (size_t)T * dm.dd, T * dm.dd, p->a_tot, 0, st);
@@ -1147,11 +1251,7 @@ extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32
     {
         const Grid g = att_grid(K, dm.T);
         const size_t smem = sizeof(AttSmem);
-        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel, smem));
-        att_bwd_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                         p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
-                                                         p->partA, p->tile_part, p->tile_partA, 1);
-        DP_LAUNCH_CHECK();
+        DP_TRY(launch_att(p, g, smem, rows, p->tile_part, p->tile_partA, st));
     }
     DP_TRY(run_b1f(p, params, rows, nullptr, nullptr, kRowsOnly, st));
     DP_TRY(run_b2(p, params, K, st));

@@ -197,7 +197,8 @@ __global__ void dec_prep_kernel(PolicyDims dm, const double *__restrict__ params
     }
 }
 
-constexpr int kProjLd = 66;  // proj row stride in shared memory: 16-byte rows, conflict-free LDS.128
+constexpr int kProjLd = 66;
+constexpr int kWout1Ld = kH + 8;  // W_out[:64]^T row stride (== 8 mod 16 doubles: 8-lane groups in distinct banks)  // proj row stride in shared memory: 16-byte rows, conflict-free LDS.128
 constexpr int kWarps = kThreads / 32;
 
 struct DecArgs {
@@ -211,14 +212,23 @@ struct DecArgs {
     long long draws_per_count;
     const uint8_t *forced;
     const double *enc_h, *enc_c, *edev, *proj, *encW;
-    double *act_h, *act_c, *act_g, *act_uc, *act_u, *act_p, *act_stat, *act_lz;
+    double *act_h, *act_c, *act_g, *act_uc, *act_u, *act_p, *act_stat, *act_lz, *act_e, *act_esc;
     uint8_t *choice, *choice_out;
     double *logp, *probs_out;
     int M, Tpad;
     // shared-memory offsets (doubles)
-    int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_u, o_uh, o_p, o_alpha, o_pm, o_ps, o_puc, o_pcg,
-        o_misc;
+    int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_uh, o_alpha, o_pm, o_ps, o_puc, o_pz, o_gn, o_hc,
+        o_cc, o_ac, o_pcg, o_misc;
 };
+
+// q = x / n for 0 <= x < MT * n without an integer division (MT <= 8)
+template <int MT>
+__device__ __forceinline__ int small_div(int x, int n) {
+    int q = 0;
+#pragma unroll
+    for (int k = 1; k < MT; k++) q += x >= k * n ? 1 : 0;
+    return q;
+}
 
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
@@ -231,19 +241,21 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// One CTA owns M samples for all T decode steps; three barriers per step:
-//   A  gates = edev[prev] + g (g = h_{t-1} W_h, computed during the previous
-//      step's phase C, off the critical path), LSTM cell -> h
-//   C  (every warp, its own rows i) s_i = proj_i . h, warp-local softmax
-//      statistics (max m_w, sum l_w) and the partial uc_w = sum_i e_i encW_i;
-//      alongside: next step's g = h W_h (register W_h columns) and
-//      uh = h W_out[:64]
-//   E  warp per sample: online-softmax combine of the 8 warp partials
-//      (M = max m_w, l = sum l_w e^{m_w - M}, uc = sum uc_w e^{m_w - M} / l),
-//      u = uh + uc, logits, softmax over devices, PCG64 draw, cdf search.
-// The context vector itself is not formed (the backward works from uc, and
-// dW_out[64:] = enc^T (sum alpha^T du)); the log-prob log() is deferred.
-template <int MT, bool PS>
+// One CTA owns M samples for all T decode steps.  Per step:
+//   [A] (non-speculative variant only) gates = edev[prev] + g, LSTM cell -> h
+//   C   (all warps) fused pass: s_i = proj_i . h for the thread's rows and the
+//       next step's g = h W_h for its gate column (shared h loads); warp-local
+//       softmax statistics (max m_w, sum l_w), partial uc_w = sum_i e_i encW_i
+//       and partial logits pz_w = dev_table[:D] uc_w; uh = h W_out[:64]
+//   E   warp per sample: online-softmax combine of the 8 warp partials
+//       (M = max m_w, l = sum l_w e^{m_w-M}), z = dev_table[:D] uh + b_out +
+//       (sum_w pz_w e^{m_w-M}) / l, softmax over devices, PCG64 draw, cdf search.
+//       SPEC: the idle warps meanwhile evaluate the next step's LSTM cell for
+//       every possible choice d (edev[d] + g), so the next step starts at C
+//       with h = candidate[choice] and phase A disappears from the chain.
+// The context vector is never formed: ctx @ W_out[64:] = alpha @ encW, and the
+// backward works from uc (w = uc.du, dW_out[64:] = enc^T sum alpha^T du).
+template <int MT, bool PS, bool SPEC>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -255,33 +267,40 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     constexpr int LD = PS ? kProjLd : kH;
     const double *proj = PS ? (const double *)(sm + a.o_proj) : a.proj;
     const double *encW = PS ? (const double *)(sm + a.o_encw) : a.encW;
-    double *wout1 = sm + a.o_wout;  // W_out[:64] [64][dd]
+    double *wout1 = sm + a.o_wout;  // W_out[:64]^T [dd][kWout1Ld]
     double *devt = sm + a.o_devt;
     double *bout = sm + a.o_bout;
-    double *edev = sm + a.o_edev;
-    double *hS = sm + a.o_h;        // [M][64]
-    double *uS = sm + a.o_u;        // [M][32]
+    double *edevS = sm + a.o_edev;  // (non-SPEC) edev staged
+    double *hS = sm + a.o_h;        // (non-SPEC) [M][64]
     double *uhS = sm + a.o_uh;      // [M][32]
-    double *pS = sm + a.o_p;        // [M][32]
     double *alS = sm + a.o_alpha;   // [M][Tpad] scores -> e_i
     double *pmx = sm + a.o_pm;      // [8][M] warp max
     double *psm = sm + a.o_ps;      // [8][M] warp sum
     double *puc = sm + a.o_puc;     // [8][M][dd] warp uc partials
+    double *pz = sm + a.o_pz;       // [8][M][D] warp partial logits
+    double *gnS = sm + a.o_gn;      // (SPEC) [M][256] next step's h W_h
+    double *hC = sm + a.o_hc;       // (SPEC) [M][D][64] candidate h
+    double *cC = sm + a.o_cc;       // (SPEC) [2][M][D][64] candidate c (step parity)
+    double *aC = sm + a.o_ac;       // (SPEC) [M][D][256] candidate gate activations
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
-    int *prev = reinterpret_cast<int *>(sm + a.o_misc);                               // [M]
+    int *prev = reinterpret_cast<int *>(sm + a.o_misc);  // [2][M] previous choice, by step parity
+    const double *edev = SPEC ? a.edev : edevS;
 
     // ---- stage the snapshot-constant operands ----
     if (PS) {
         for (int i = tid; i < T * kH; i += kThreads) sm[a.o_proj + (i >> 6) * kProjLd + (i & 63)] = a.proj[i];
         for (int i = tid; i < T * dd; i += kThreads) sm[a.o_encw + i] = a.encW[i];
     }
-    for (int i = tid; i < kH * dd; i += kThreads) wout1[i] = P[dm.off.w_out + i];
+    for (int i = tid; i < kH * dd; i += kThreads) wout1[(i % dd) * kWout1Ld + i / dd] = P[dm.off.w_out + i];
     for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
     for (int i = tid; i < D; i += kThreads) bout[i] = P[dm.off.b_out + i];
-    for (int i = tid; i < (D + 1) * kG; i += kThreads) edev[i] = a.edev[i];
-    for (int i = tid; i < Mb * kH; i += kThreads) hS[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
+    if (!SPEC)
+        for (int i = tid; i < (D + 1) * kG; i += kThreads) edevS[i] = a.edev[i];
+    // h_{-1} = encoder final state (SPEC: staged in alS, free until step 0's scores)
+    double *h0 = SPEC ? alS : hS;
+    for (int i = tid; i < (SPEC ? kH : Mb * kH); i += kThreads) h0[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
     if (tid < Mb) {
-        prev[tid] = D;
+        prev[tid] = SPEC ? 0 : D;  // SPEC: step 0's state lives in candidate slot 0
         if (!a.forced) {
             const long long kg = a.k_offset + k0 + tid;
             unsigned long long n0 = a.draw_base + (unsigned long long)kg * (unsigned long long)T;
@@ -298,23 +317,38 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
         for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
     }
-    // cell state of unit u, owned (in registers) by the unit's gate-0 thread
-    double cst[MT];
-    {
-        const double c0 = a.enc_c[(size_t)(T - 1) * kH + u];
+    const double c_init = a.enc_c[(size_t)(T - 1) * kH + u];
+    double cst[MT];  // (non-SPEC) cell state of unit u, owned by the unit's gate-0 thread
 #pragma unroll
-        for (int m = 0; m < MT; m++) cst[m] = c0;
-    }
+    for (int m = 0; m < MT; m++) cst[m] = c_init;
+    const int base = lane & ~3;
     __syncthreads();
-    // g = h W_h for the coming step (identical initial state for every sample)
+    // g = h W_h for the first step (identical initial state for every sample)
     double gn[MT];
     {
-        const double g0 = dot64_sh_reg(hS, w);
+        const double g0 = dot64_sh_reg(h0, w);
 #pragma unroll
         for (int m = 0; m < MT; m++) gn[m] = g0;
+        if (SPEC) {
+            // step 0 (prev = start row D) into candidate slot 0 of every sample
+            const double act = gate_act(edev[D * kG + col] + g0, gate == 3);
+            const double iv = __shfl_sync(0xffffffffu, act, base + 0);
+            const double fv = __shfl_sync(0xffffffffu, act, base + 1);
+            const double ov = __shfl_sync(0xffffffffu, act, base + 2);
+            const double gv = __shfl_sync(0xffffffffu, act, base + 3);
+            const double cn = fv * c_init + iv * gv;
+            const double hn = gate == 0 ? ov * tanh_x(cn) : 0.0;
+            for (int m = 0; m < Mb; m++) {
+                aC[(m * D) * kG + col] = act;
+                if (gate == 0) {
+                    hC[(m * D) * kH + u] = hn;
+                    cC[(m * D) * kH + u] = cn;
+                }
+            }
+        }
     }
+    __syncthreads();
 
-    const int base = lane & ~3;
     int d_pow2 = 1;
     while (d_pow2 < D) d_pow2 <<= 1;
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
@@ -327,13 +361,15 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         clk_last = now_;                                  \
     }
     for (int t = 0; t < T; t++) {
-        // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
-        {
+        const int par = t & 1;
+        const int *prv = prev + par * M;  // choices of step t-1 (SPEC: candidate slots)
+        if (!SPEC) {
+            // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
             double act[MT], cn[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) {
-                    act[m] = gate_act(edev[prev[m] * kG + col] + gn[m], gate == 3);
+                    act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
                     a.act_g[((size_t)(k0 + m) * T + t) * kG + col] = act[m];
                 }
 #pragma unroll
@@ -356,14 +392,26 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     a.act_h[row * kH + u] = hn;
                     a.act_c[row * kH + u] = cn[m];
                 }
+            __syncthreads();
         }
-        __syncthreads();
         DP_PHASE(0);
-        // ---- C: scores s = proj @ h (policy.py:296), warp-local softmax stats + uc partials ----
-        if (t + 1 < T) {
+        // ---- C: scores s = proj @ h (policy.py:296), warp-local softmax stats + partials ----
+        const double *hcur[MT];
+#pragma unroll
+        for (int m = 0; m < MT; m++) hcur[m] = SPEC ? hC + (m * D + (m < Mb ? prv[m] : 0)) * kH : hS + m * kH;
+        if (SPEC) {
+            // the selected candidate becomes step t's cached activations
 #pragma unroll
             for (int m = 0; m < MT; m++)
-                if (m < Mb) gn[m] = dot64_sh_reg(hS + m * kH, w);
+                if (m < Mb) {
+                    const size_t row = (size_t)(k0 + m) * T + t;
+                    const int slot = m * D + prv[m];
+                    a.act_g[row * kG + col] = aC[slot * kG + col];
+                    if (tid < kH) {
+                        a.act_h[row * kH + tid] = hcur[m][tid];
+                        a.act_c[row * kH + tid] = cC[(par * M * D + slot) * kH + tid];
+                    }
+                }
         }
         double lmx[MT], lsm[MT];
 #pragma unroll
@@ -371,7 +419,39 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             lmx[m] = -INFINITY;
             lsm[m] = 0.0;
         }
-        for (int i = tid; i < T; i += kThreads) {
+        {
+            // fused pass: this thread's first score row and its gate column of the
+            // next step's h W_h share every h load (W_h indices stay compile-time)
+            const int i = tid < T ? tid : T - 1;
+            const double2 *pr = reinterpret_cast<const double2 *>(proj + (size_t)i * LD);
+            double s0[MT], s1[MT], g0[MT], g1[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++) s0[m] = s1[m] = g0[m] = g1[m] = 0.0;
+#pragma unroll
+            for (int j2 = 0; j2 < kH / 2; j2++) {
+                const double2 e = pr[j2];
+#pragma unroll
+                for (int m = 0; m < MT; m++) {
+                    const double2 hh = reinterpret_cast<const double2 *>(hcur[m])[j2];
+                    s0[m] = fma(e.x, hh.x, s0[m]);
+                    s1[m] = fma(e.y, hh.y, s1[m]);
+                    g0[m] = fma(hh.x, w[2 * j2], g0[m]);
+                    g1[m] = fma(hh.y, w[2 * j2 + 1], g1[m]);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) {
+                    gn[m] = g0[m] + g1[m];
+                    if (SPEC) gnS[m * kG + col] = gn[m];
+                    if (tid < T) {
+                        const double s = s0[m] + s1[m];
+                        alS[m * a.Tpad + tid] = s;
+                        lmx[m] = s;
+                    }
+                }
+        }
+        for (int i = tid + kThreads; i < T; i += kThreads) {
             const double2 *pr = reinterpret_cast<const double2 *>(proj + (size_t)i * LD);
             double s0[MT], s1[MT];
 #pragma unroll
@@ -381,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 const double2 e = pr[j2];
 #pragma unroll
                 for (int m = 0; m < MT; m++) {
-                    const double2 hh = reinterpret_cast<const double2 *>(hS + m * kH)[j2];
+                    const double2 hh = reinterpret_cast<const double2 *>(hcur[m])[j2];
                     s0[m] = fma(e.x, hh.x, s0[m]);
                     s1[m] = fma(e.y, hh.y, s1[m]);
                 }
@@ -403,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     const double e = exp(alS[m * a.Tpad + i] - lmx[m]);
                     alS[m * a.Tpad + i] = e;
                     lsm[m] += e;
+                    if (a.act_e) a.act_e[((size_t)(k0 + m) * T + t) * T + i] = e;
                 }
         }
 #pragma unroll
@@ -410,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         __syncwarp();
         // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
         for (int pi = lane; pi < Mb * dd; pi += 32) {
-            const int m = pi / dd, j = pi - m * dd;
+            const int m = small_div<MT>(pi, dd), j = pi - m * dd;
             const double *al = alS + m * a.Tpad;
             double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
             for (int i0 = warp * 32; i0 < T; i0 += kThreads) {
@@ -435,6 +516,20 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     psm[warp * M + m] = lsm[m];
                 }
         }
+        __syncwarp();
+        // pz_w[m][d] = dev_table[d] . uc_w[m]
+        for (int pi = lane; pi < Mb * D; pi += 32) {
+            const int m = small_div<MT>(pi, D), d = pi - m * D;
+            const double *pv = puc + (warp * M + m) * dd;
+            double z0 = 0.0, z1 = 0.0;
+            int o = 0;
+            for (; o + 2 <= dd; o += 2) {
+                z0 = fma(devt[d * dd + o], pv[o], z0);
+                z1 = fma(devt[d * dd + o + 1], pv[o + 1], z1);
+            }
+            if (o < dd) z0 = fma(devt[d * dd + o], pv[o], z0);
+            pz[(warp * M + m) * D + d] = z0 + z1;
+        }
         // uh = h @ W_out[:64] (policy.py:302, h half), 8 lanes per output
         {
             const int total = Mb * dd * 8;
@@ -445,15 +540,15 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 int m = 0, o = 0;
                 if (ok) {
                     const int pair = idx >> 3, pp = idx & 7;
-                    m = pair / dd;
+                    m = small_div<MT>(pair, dd);
                     o = pair - m * dd;
-                    const double *hv = hS + m * kH + pp;
-                    const double *wc = wout1 + (size_t)pp * dd + o;
+                    const double *hv = (SPEC ? hC + (m * D + prv[m]) * kH : hS + m * kH) + pp;
+                    const double *wc = wout1 + o * kWout1Ld + pp;
                     double p0 = 0.0, p1 = 0.0;
 #pragma unroll
                     for (int y = 0; y < 8; y += 2) {
-                        p0 = fma(hv[8 * y], wc[(size_t)8 * y * dd], p0);
-                        p1 = fma(hv[8 * y + 8], wc[(size_t)(8 * y + 8) * dd], p1);
+                        p0 = fma(hv[8 * y], wc[8 * y], p0);
+                        p1 = fma(hv[8 * y + 8], wc[8 * y + 8], p1);
                     }
                     part = p0 + p1;
                 }
@@ -465,94 +560,130 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
         __syncthreads();
         DP_PHASE(1);
-        // ---- E: combine, u, logits, softmax over devices, draw (policy.py:297-308, 320-323) ----
+        // ---- E: combine, logits, softmax over devices, draw (policy.py:297-308, 320-323) ----
         for (int m = warp; m < Mb; m += kWarps) {
             const size_t row = (size_t)(k0 + m) * T + t;
-            const double pm = lane < kWarps ? pmx[lane * M + m] : -INFINITY;
-            double gmx = pm;
+            // next uniform (every lane steps the same PCG64 state; lane 0 keeps it)
+            double r = 0.0;
+            u128 rs{0, 0};
+            if (!a.forced) {
+                rs = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
+                r = pcg_double(rs);
+            }
+            double gmx = pmx[m];
 #pragma unroll
-            for (int o = kWarps >> 1; o > 0; o >>= 1) gmx = fmax(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
-            gmx = __shfl_sync(0xffffffffu, gmx, 0);
-            const double f = lane < kWarps ? exp(pm - gmx) : 0.0;
-            double ls = lane < kWarps ? psm[lane * M + m] * f : 0.0;
-#pragma unroll
-            for (int o = kWarps >> 1; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
-            const double gsum = __shfl_sync(0xffffffffu, ls, 0);
+            for (int ww = 1; ww < kWarps; ww++) gmx = fmax(gmx, pmx[ww * M + m]);
+            const double f = lane < kWarps ? exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
             double fw[kWarps];
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
+            double gsum = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
+            if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = f / gsum;
+            double z = -INFINITY;
+            if (lane < D) {
+                double zh0 = 0.0, zh1 = 0.0, zc = 0.0;
+                int o = 0;
+                for (; o + 2 <= dd; o += 2) {
+                    zh0 = fma(devt[lane * dd + o], uhS[m * 32 + o], zh0);
+                    zh1 = fma(devt[lane * dd + o + 1], uhS[m * 32 + o + 1], zh1);
+                }
+                if (o < dd) zh0 = fma(devt[lane * dd + o], uhS[m * 32 + o], zh0);
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + lane], fw[ww], zc);
+                z = ((zh0 + zh1) + zc / gsum) + bout[lane];
+            }
             if (lane < dd) {
+                // u (and its context half uc) for the backward
                 double uc = 0.0;
 #pragma unroll
                 for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lane], fw[ww], uc);
                 const double ucn = uc / gsum;
-                const double uv = uhS[m * 32 + lane] + ucn;
-                uS[m * 32 + lane] = uv;
-                a.act_u[row * dd + lane] = uv;
+                a.act_u[row * dd + lane] = uhS[m * 32 + lane] + ucn;
                 a.act_uc[row * dd + lane] = ucn;
-            }
-            if (lane == 0) {
-                // softmax stats (max, sum) for the backward's recompute of alpha
-                a.act_stat[row * 2] = gmx;
-                a.act_stat[row * 2 + 1] = gsum;
-            }
-            __syncwarp();
-            double z = -INFINITY;
-            if (lane < D) {
-                double z0 = 0.0, z1 = 0.0;
-                int o = 0;
-                for (; o + 2 <= dd; o += 2) {
-                    z0 = fma(devt[lane * dd + o], uS[m * 32 + o], z0);
-                    z1 = fma(devt[lane * dd + o + 1], uS[m * 32 + o + 1], z1);
-                }
-                if (o < dd) z0 = fma(devt[lane * dd + o], uS[m * 32 + o], z0);
-                z = (z0 + z1) + bout[lane];
             }
             double zmax = z;
             for (int o = d_pow2 >> 1; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
             const double zs = z - zmax;
-            const double ez = exp(zs);
-            if (lane < D) pS[m * 32 + lane] = ez;
-            __syncwarp();
-            double esum = 0.0;
-            if (lane == 0) esum = np_sum_small(pS + m * 32, D);
-            esum = __shfl_sync(0xffffffffu, esum, 0);
+            const double ez = exp(zs);  // 0 on lanes >= D
+            // numpy pairwise order over the D terms (np_sum_small), identical in every lane
+            double esum;
+            if (D < 8) {
+                esum = 0.0;
+                for (int dv = 0; dv < D; dv++) esum += __shfl_sync(0xffffffffu, ez, dv);
+            } else {
+                double rr[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) rr[j] = __shfl_sync(0xffffffffu, ez, j);
+                int i = 8;
+                for (; i < D - (D % 8); i += 8) {
+#pragma unroll
+                    for (int j = 0; j < 8; j++) rr[j] += __shfl_sync(0xffffffffu, ez, i + j);
+                }
+                esum = ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
+                for (; i < D; i++) esum += __shfl_sync(0xffffffffu, ez, i);
+            }
             const double pr = ez / esum;
-            __syncwarp();
             if (lane < D) {
-                pS[m * 32 + lane] = pr;
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
             }
-            __syncwarp();
-            int ch = 0;
-            if (lane == 0) {
-                if (a.forced) {
-                    ch = a.forced[row];
-                } else {
-                    u128 s{pcg[2 * m], pcg[2 * m + 1]};
-                    s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
-                    pcg[2 * m] = s.hi;
-                    pcg[2 * m + 1] = s.lo;
-                    const double r = pcg_double(s);
-                    double cdf = 0.0;
-                    int cnt = 0;
-                    for (int dv = 0; dv < D; dv++) {
-                        cdf += pS[m * 32 + dv];
-                        cnt += (cdf <= r) ? 1 : 0;
-                    }
-                    ch = cnt < D - 1 ? cnt : D - 1;
+            int ch;
+            if (a.forced) {
+                ch = a.forced[row];
+            } else {
+                double cdf = 0.0;
+                int cnt = 0;
+                for (int dv = 0; dv < D; dv++) {
+                    cdf += __shfl_sync(0xffffffffu, pr, dv);
+                    cnt += (cdf <= r) ? 1 : 0;
                 }
+                ch = cnt < D - 1 ? cnt : D - 1;
             }
-            ch = __shfl_sync(0xffffffffu, ch, 0);
             const double zc = __shfl_sync(0xffffffffu, zs, ch);
             if (lane == 0) {
-                prev[m] = ch;
+                if (!a.forced) {
+                    pcg[2 * m] = rs.hi;  // every lane has read the state by now (the cdf shuffles)
+                    pcg[2 * m + 1] = rs.lo;
+                }
+                prev[(par ^ 1) * M + m] = ch;
                 a.choice[row] = (uint8_t)ch;
                 if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
                 a.act_lz[row * 2] = zc;
                 a.act_lz[row * 2 + 1] = esum;
+                // softmax stats (max, sum) for the backward's recompute of alpha
+                a.act_stat[row * 2] = gmx;
+                a.act_stat[row * 2 + 1] = gsum;
             }
+        }
+        if (SPEC && warp >= Mb && t + 1 < T) {
+            // next step's LSTM cell for every possible choice d (the idle warps)
+            const int st = tid - Mb * 32, nst = kThreads - Mb * 32;
+            const int n_items = Mb * D * kH;
+#pragma unroll 2
+            for (int it = st; it < n_items; it += nst) {
+                const int m = it / (D * kH), rem = it - m * D * kH, d = rem >> 6, uu = rem & 63;
+                const double *g = gnS + m * kG + uu;
+                const double *ed = edev + d * kG + uu;
+                const double ai = gate_act(__ldg(ed) + g[0], false);
+                const double af = gate_act(__ldg(ed + kH) + g[kH], false);
+                const double ao = gate_act(__ldg(ed + 2 * kH) + g[2 * kH], false);
+                const double ag = gate_act(__ldg(ed + 3 * kH) + g[3 * kH], true);
+                const double cold = cC[(par * M * D + m * D + prv[m]) * kH + uu];
+                const double cn = af * cold + ai * ag;
+                const double hn = ao * tanh_x(cn);
+                double *ac = aC + (m * D + d) * kG + uu;
+                ac[0] = ai;
+                ac[kH] = af;
+                ac[2 * kH] = ao;
+                ac[3 * kH] = ag;
+                hC[(m * D + d) * kH + uu] = hn;
+                cC[((par ^ 1) * M * D + m * D + d) * kH + uu] = cn;
+            }
+        }
+        if (!SPEC) {
+            // gn for the non-speculative A of the next step is already in registers
         }
         __syncthreads();
         DP_PHASE(2);
@@ -610,7 +741,7 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
                     p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
-                    p->tile_part, p->tile_partA, p->partA, p->a_tot};
+                    p->tile_part, p->tile_partA, p->partA, p->a_tot, p->act_e, p->act_esc};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p->side) cudaStreamDestroy(p->side);
@@ -728,6 +859,12 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
         alloc((void **)&p->tile_partA, sizeof(double) * tiles * (size_t)T * dev_dim);
     }
     alloc((void **)&p->partA, sizeof(double) * 2 * kNumSMs * (size_t)T * dev_dim);
+    // stored attention numerators (the backward skips the score recompute): K*T^2*8 bytes,
+    // kept below 2 GiB (134 MB at C3 K=256)
+    if (ok && sizeof(double) * rows * (size_t)T <= ((size_t)2 << 30)) {
+        alloc((void **)&p->act_e, sizeof(double) * rows * (size_t)T);
+        alloc((void **)&p->act_esc, sizeof(double) * rows * kWarps);
+    }
     alloc((void **)&p->a_tot, sizeof(double) * (size_t)T * dev_dim);
     if (!ok) {
         dp::set_error(std::string("dp_policy_create: allocation/upload failed: ") +
@@ -751,6 +888,14 @@ extern "C" int64_t dp_policy_num_params(const dp_policy *p) { return p ? p->dims
 
 // Debug: enable (1) / disable (0) decoder phase clocks, then read and reset
 // the 8 per-phase cycle sums (block 0) into h_out[8].  Synchronous.
+static int g_dec_variant = 0;  // dp_debug_decoder_variant
+extern "C" int dp_debug_decoder_variant(int32_t mode) {
+    DP_ENTRY();
+    DP_REQUIRE(mode >= 0 && mode <= 2, "dp_debug_decoder_variant: mode must be 0, 1 or 2");
+    g_dec_variant = mode;
+    return DP_OK;
+}
+
 extern "C" int dp_debug_phase_clocks(int32_t enable, int64_t *h_out) {
     DP_ENTRY();
     const int on = enable ? 1 : 0;
@@ -794,19 +939,25 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
 
 namespace {
 struct DecPlan {
-    int M, MT, enc_in_smem, Tpad;
+    int M, MT, enc_in_smem, spec, Tpad;
     size_t smem;
     DecArgs proto;
 };
 
-bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
-    const int T = dm.T;
+bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
+    const int T = dm.T, D = dm.D, dd = dm.dd;
     const size_t budget = 225 * 1024;
     int M = ceil_div(K, kNumSMs);
     if (M < 1) M = 1;
     if (M > 8) M = 8;
     for (; M >= 1; M = (M > 1 ? M - 1 : 0)) {
-        for (int enc_smem = 1; enc_smem >= 0; enc_smem--) {
+        const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+        // preference: proj in smem + speculative cell, proj in smem, global proj (+spec), global
+        for (int variant = 0; variant < 4; variant++) {
+            // the speculative cell costs D x the gate transcendentals on 8-M warps:
+            // measured slower at C3 (D=4, M=2), so it is opt-in (mode 1)
+            const int enc_smem = variant < 2, spec = (variant % 2 == 0) && MT <= 4 && variant_mode == 1;
+            if (variant % 2 == 0 && !spec) continue;
             DecArgs &a = pl.proto;
             const int Tpad = (T + 1) & ~1;
             int o = 0;
@@ -815,28 +966,31 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
                 o += (n + 1) & ~1;
                 return r;
             };
-            const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
             a.o_proj = enc_smem ? take(T * kProjLd) : 0;
-            a.o_encw = enc_smem ? take(T * dm.dd) : 0;
-            a.o_wout = take(kH * dm.dd);
-            a.o_devt = take(dm.D * dm.dd);
-            a.o_bout = take(dm.D);
-            a.o_edev = take((dm.D + 1) * kG);
-            a.o_h = take(M * kH);
-            a.o_u = take(M * 32);
+            a.o_encw = enc_smem ? take(T * dd) : 0;
+            a.o_wout = take(kWout1Ld * dd);
+            a.o_devt = take(D * dd);
+            a.o_bout = take(D);
+            a.o_edev = spec ? 0 : take((D + 1) * kG);
+            a.o_h = spec ? 0 : take(M * kH);
             a.o_uh = take(M * 32);
-            a.o_p = take(M * 32);
-            a.o_alpha = take(M * Tpad);
+            a.o_alpha = take(M * (Tpad > kH ? Tpad : kH));
             a.o_pm = take(kWarps * M);
             a.o_ps = take(kWarps * M);
-            a.o_puc = take(kWarps * M * dm.dd);
+            a.o_puc = take(kWarps * M * dd);
+            a.o_pz = take(kWarps * M * D);
+            a.o_gn = spec ? take(M * kG) : 0;
+            a.o_hc = spec ? take(M * D * kH) : 0;
+            a.o_cc = spec ? take(2 * M * D * kH) : 0;
+            a.o_ac = spec ? take(M * D * kG) : 0;
             a.o_pcg = take(2 * M);
-            a.o_misc = take(16 + M);
+            a.o_misc = take(16 + 2 * M);
             const size_t bytes = (size_t)o * sizeof(double);
             if (bytes <= budget) {
                 pl.M = M;
                 pl.MT = MT;
                 pl.enc_in_smem = enc_smem;
+                pl.spec = spec;
                 pl.Tpad = Tpad;
                 pl.smem = bytes;
                 return true;
@@ -845,6 +999,18 @@ bool plan_decoder(const PolicyDims &dm, int K, DecPlan &pl) {
         if (M == 1) break;
     }
     return false;
+}
+
+template <bool PS, bool SPEC>
+const void *dec_fn(int MT) {
+    if (SPEC)
+        return MT == 1 ? (const void *)dec_kernel<1, PS, SPEC>
+               : MT == 2 ? (const void *)dec_kernel<2, PS, SPEC>
+                         : (const void *)dec_kernel<4, PS, SPEC>;
+    return MT == 1 ? (const void *)dec_kernel<1, PS, false>
+           : MT == 2 ? (const void *)dec_kernel<2, PS, false>
+           : MT == 4 ? (const void *)dec_kernel<4, PS, false>
+                     : (const void *)dec_kernel<8, PS, false>;
 }
 }  // namespace
 
@@ -858,7 +1024,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     DP_REQUIRE(forced || h_pcg, "dp_policy_decode: need a PCG64 state or a forced placement");
     const PolicyDims &dm = p->dims;
     DecPlan pl;
-    DP_REQUIRE(plan_decoder(dm, K, pl), "dp_policy_decode: shared-memory plan failed");
+    DP_REQUIRE(plan_decoder(dm, K, g_dec_variant, pl), "dp_policy_decode: shared-memory plan failed");
     DecArgs a = pl.proto;
     a.dm = dm;
     a.params = params;
@@ -885,6 +1051,8 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.act_c = p->act_c;
     a.act_g = p->act_g;
     a.act_uc = p->act_uc;
+    a.act_e = p->act_e;
+    a.act_esc = p->act_esc;
     a.act_u = p->act_u;
     a.act_p = p->act_p;
     a.act_stat = p->act_stat;
@@ -897,17 +1065,8 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.Tpad = pl.Tpad;
     const int grid = ceil_div(K, pl.M);
     cudaStream_t st = (cudaStream_t)stream;
-    const void *fn;
-    if (pl.enc_in_smem)
-        fn = pl.MT == 1 ? (const void *)dec_kernel<1, true>
-             : pl.MT == 2 ? (const void *)dec_kernel<2, true>
-             : pl.MT == 4 ? (const void *)dec_kernel<4, true>
-                          : (const void *)dec_kernel<8, true>;
-    else
-        fn = pl.MT == 1 ? (const void *)dec_kernel<1, false>
-             : pl.MT == 2 ? (const void *)dec_kernel<2, false>
-             : pl.MT == 4 ? (const void *)dec_kernel<4, false>
-                          : (const void *)dec_kernel<8, false>;
+    const void *fn = pl.enc_in_smem ? (pl.spec ? dec_fn<true, true>(pl.MT) : dec_fn<true, false>(pl.MT))
+                                    : (pl.spec ? dec_fn<false, true>(pl.MT) : dec_fn<false, false>(pl.MT));
     DP_CUDA_TRY(allow_big_smem(fn, pl.smem));
     void *args[] = {&a};
     DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));

@@ -15,6 +15,8 @@ from paper_1706_04972_b200 import _native as nat  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+variant = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+nat.check(nat.lib().dp_debug_decoder_variant(variant), "variant")
 gg, topo, _, _ = cfg(name)
 params = dp.trainer.policy_template(gg, topo, dp.TrainerConfig())
 feats = dp.GroupFeatures.from_grouped(gg, params.spec)
@@ -31,6 +33,6 @@ nat.check(nat.lib().dp_debug_phase_clocks(0, out), "dbg")
 T = len(feats)
 names = ["A gates+cell", "C scores/softmax/uc/uh/next-g", "E combine+draw"]
 tot = sum(out)
-print(f"{name} K={K} T={T}: {tot / T:.0f} cycles/step")
+print(f"{name} K={K} T={T} variant={variant}: {tot / T:.0f} cycles/step")
 for n, v in zip(names, out[:3]):
     print(f"  {n:32s} {v / T:8.0f} cycles/step  {100 * v / tot:5.1f}%")

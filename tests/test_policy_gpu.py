@@ -161,3 +161,41 @@ def test_checkpoint_roundtrip(tmp_path):
     q = P.load_checkpoint(tmp_path / "p.json")
     assert np.array_equal(q.to_flat(), params.to_flat())
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name,K,picks", [("C1", 700, (0, 1, 349, 699)), ("C2", 600, (0, 599))])
+def test_large_batch_non_speculative_decoder_vs_oracle(name, K, picks):
+    """K > 4*148 selects the 8-samples-per-CTA decoder without the speculative
+    cell (csrc/policy_fwd.cu plan_decoder); spot-check samples via PCG64 jumps."""
+    gg, topo, params, feats = _setup(name, seed=4)
+    T = len(feats)
+    pl, lp = P.sample_batch(params, feats, np.random.default_rng(77), K)
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    for k in picks:
+        rng = np.random.default_rng(77)
+        rng.bit_generator.advance(k * T)
+        opl, olp, _ = pol.sample(rng)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
+
+
+@pytest.mark.parametrize("name,K", [("C3", 16), ("C2", 8), ("C1", 300)])
+def test_speculative_cell_decoder_vs_oracle(name, K):
+    """The opt-in speculative-cell decoder (dp_debug_decoder_variant(1)) samples
+    the same placements as the oracle."""
+    from paper_1706_04972_b200 import _native as nat
+
+    gg, topo, params, feats = _setup(name, seed=5)
+    nat.check(nat.lib().dp_debug_decoder_variant(1), "variant")
+    try:
+        pl, lp = P.sample_batch(params, feats, np.random.default_rng(11), K)
+    finally:
+        nat.check(nat.lib().dp_debug_decoder_variant(0), "variant")
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    rng = np.random.default_rng(11)
+    for k in range(min(K, 16)):
+        opl, olp, _ = pol.sample(rng)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
