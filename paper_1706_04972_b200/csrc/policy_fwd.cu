@@ -53,6 +53,7 @@ __device__ __forceinline__ double tanh_x(double x) { return gate_act(x, true); }
 // Debug-only per-phase cycle counters of the decoder (block 0, thread 0).
 __device__ int g_dbg_clocks = 0;
 __device__ long long g_phase_clk[16];
+__device__ int g_dbg_skip = 0;  // debug-only ablation bits (timing experiments; results invalid when set)
 
 // numpy pairwise_sum order for n <= 128 (np.add.reduce on a contiguous array):
 // n < 8 sequential; otherwise 8 interleaved accumulators, fixed tree, tail.
@@ -172,9 +173,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   proj = enc_states @ W_att^T    [T x 64]  (policy.py:287 — the reference's own order)
 //   encW = enc_states @ W_out[64:] [T x dd]  (ctx @ W_out[64:] == alpha @ encW, so the
 //                                            step's context never has to be formed)
+// Also: proj_nmax = max_t ||proj_t||_2 (atomic max on the IEEE bits of a
+// non-negative double; zeroed by the caller).  |s_t| = |proj_t . h| <
+// 8 ||proj_t|| because |h_j| < 1 (h = o * tanh(c), 64 units), so when
+// 8 * proj_nmax <= kNoShiftBound the decoder's softmax over the T scores can
+// skip the max subtraction: exp() neither overflows nor underflows, and
+// alpha = exp(s) / sum exp(s) equals the reference's exp(s - max) / sum to
+// rounding (the shift cancels exactly in real arithmetic).
+constexpr double kNoShiftBound = 600.0;
+
 __global__ void dec_prep_kernel(PolicyDims dm, const double *__restrict__ params, const double *__restrict__ enc_h,
-                                double *__restrict__ proj, double *__restrict__ encW) {
+                                double *__restrict__ proj, double *__restrict__ encW,
+                                unsigned long long *__restrict__ proj_nmax) {
     __shared__ double e[kH];
+    __shared__ double sq[kH];
     const int t = blockIdx.x, tid = threadIdx.x, dd = dm.dd;
     if (tid < kH) e[tid] = enc_h[(size_t)t * kH + tid];
     __syncthreads();
@@ -186,6 +198,7 @@ __global__ void dec_prep_kernel(PolicyDims dm, const double *__restrict__ params
             a1 = fma(e[j + 1], w[j + 1], a1);
         }
         proj[(size_t)t * kH + tid] = a0 + a1;
+        sq[tid] = (a0 + a1) * (a0 + a1);
     } else if (tid < kH + dd) {
         const int o = tid - kH;
         const double *w = params + dm.off.w_out + (size_t)kH * dd + o;  // W_out[64 + j][o]
@@ -194,6 +207,12 @@ __global__ void dec_prep_kernel(PolicyDims dm, const double *__restrict__ params
             a1 = fma(e[j + 1], w[(size_t)(j + 1) * dd], a1);
         }
         encW[(size_t)t * dd + o] = a0 + a1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double n2 = 0.0;
+        for (int l = 0; l < kH; l++) n2 += sq[l];
+        atomicMax(proj_nmax, (unsigned long long)__double_as_longlong(sqrt(n2)));
     }
 }
 
@@ -212,10 +231,11 @@ struct DecArgs {
     long long draws_per_count;
     const uint8_t *forced;
     const double *enc_h, *enc_c, *edev, *proj, *encW;
+    const unsigned long long *proj_nmax;
     double *act_h, *act_c, *act_g, *act_uc, *act_u, *act_p, *act_stat, *act_lz, *act_e, *act_esc;
     uint8_t *choice, *choice_out;
     double *logp, *probs_out;
-    int M, Tpad;
+    int M, Tpad, ewld;
     // shared-memory offsets (doubles)
     int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_uh, o_alpha, o_pm, o_ps, o_puc, o_pz, o_gn, o_hc,
         o_cc, o_ac, o_pcg, o_misc;
@@ -285,11 +305,15 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);  // [2][M] previous choice, by step parity
     const double *edev = SPEC ? a.edev : edevS;
+    // softmax over the T scores without the max shift when |s| is provably small
+    const bool noshift = 8.0 * __longlong_as_double((long long)*a.proj_nmax) <= kNoShiftBound;
 
     // ---- stage the snapshot-constant operands ----
     if (PS) {
         for (int i = tid; i < T * kH; i += kThreads) sm[a.o_proj + (i >> 6) * kProjLd + (i & 63)] = a.proj[i];
-        for (int i = tid; i < T * dd; i += kThreads) sm[a.o_encw + i] = a.encW[i];
+        // transposed: encWT[j][i], row stride a.ewld (== 2 mod 32 words apart per j:
+        // conflict-free LDS.128 for 8 consecutive j)
+        for (int i = tid; i < T * dd; i += kThreads) sm[a.o_encw + (i % dd) * a.ewld + i / dd] = a.encW[i];
     }
     for (int i = tid; i < kH * dd; i += kThreads) wout1[(i % dd) * kWout1Ld + i / dd] = P[dm.off.w_out + i];
     for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
@@ -396,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
         DP_PHASE(0);
         // ---- C: scores s = proj @ h (policy.py:296), warp-local softmax stats + partials ----
+        const int skip = g_dbg_skip;
         const double *hcur[MT];
 #pragma unroll
         for (int m = 0; m < MT; m++) hcur[m] = SPEC ? hC + (m * D + (m < Mb ? prv[m] : 0)) * kH : hS + m * kH;
@@ -424,28 +449,34 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             // next step's h W_h share every h load (W_h indices stay compile-time)
             const int i = tid < T ? tid : T - 1;
             const double2 *pr = reinterpret_cast<const double2 *>(proj + (size_t)i * LD);
-            double s0[MT], s1[MT], g0[MT], g1[MT];
+            // 4 independent accumulators per dot (short FMA dependency chains)
+            double s0[MT], s1[MT], s2[MT], s3[MT], g0[MT], g1[MT], g2[MT], g3[MT];
 #pragma unroll
-            for (int m = 0; m < MT; m++) s0[m] = s1[m] = g0[m] = g1[m] = 0.0;
+            for (int m = 0; m < MT; m++) s0[m] = s1[m] = s2[m] = s3[m] = g0[m] = g1[m] = g2[m] = g3[m] = 0.0;
 #pragma unroll
-            for (int j2 = 0; j2 < kH / 2; j2++) {
-                const double2 e = pr[j2];
+            for (int j2 = 0; j2 < kH / 2; j2 += 2) {
+                const double2 e0 = pr[j2], e1 = pr[j2 + 1];
 #pragma unroll
                 for (int m = 0; m < MT; m++) {
-                    const double2 hh = reinterpret_cast<const double2 *>(hcur[m])[j2];
-                    s0[m] = fma(e.x, hh.x, s0[m]);
-                    s1[m] = fma(e.y, hh.y, s1[m]);
-                    g0[m] = fma(hh.x, w[2 * j2], g0[m]);
-                    g1[m] = fma(hh.y, w[2 * j2 + 1], g1[m]);
+                    const double2 h0 = reinterpret_cast<const double2 *>(hcur[m])[j2];
+                    const double2 h1 = reinterpret_cast<const double2 *>(hcur[m])[j2 + 1];
+                    s0[m] = fma(e0.x, h0.x, s0[m]);
+                    s1[m] = fma(e0.y, h0.y, s1[m]);
+                    s2[m] = fma(e1.x, h1.x, s2[m]);
+                    s3[m] = fma(e1.y, h1.y, s3[m]);
+                    g0[m] = fma(h0.x, w[2 * j2], g0[m]);
+                    g1[m] = fma(h0.y, w[2 * j2 + 1], g1[m]);
+                    g2[m] = fma(h1.x, w[2 * j2 + 2], g2[m]);
+                    g3[m] = fma(h1.y, w[2 * j2 + 3], g3[m]);
                 }
             }
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) {
-                    gn[m] = g0[m] + g1[m];
+                    gn[m] = (g0[m] + g1[m]) + (g2[m] + g3[m]);
                     if (SPEC) gnS[m * kG + col] = gn[m];
                     if (tid < T) {
-                        const double s = s0[m] + s1[m];
+                        const double s = (s0[m] + s1[m]) + (s2[m] + s3[m]);
                         alS[m * a.Tpad + tid] = s;
                         lmx[m] = s;
                     }
@@ -475,8 +506,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
 #pragma unroll
-        for (int m = 0; m < MT; m++) lmx[m] = warp_max(lmx[m]);
-        for (int i = tid; i < T; i += kThreads) {
+        for (int m = 0; m < MT; m++) lmx[m] = noshift ? 0.0 : warp_max(lmx[m]);
+        for (int i = tid; i < ((skip & 16) ? 0 : T); i += kThreads) {
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) {
@@ -487,26 +518,39 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
 #pragma unroll
-        for (int m = 0; m < MT; m++) lsm[m] = warp_sum(lsm[m]);
+        for (int m = 0; m < MT; m++) lsm[m] = (skip & 8) ? lsm[m] : warp_sum(lsm[m]);
         __syncwarp();
         // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
-        for (int pi = lane; pi < Mb * dd; pi += 32) {
+        // (lane = (m, j); full 32-row blocks read e and encW^T as 16-byte pairs)
+        double ucv = 0.0;  // this lane's uc_w[m][j] (first pass)
+        for (int pi = lane; pi < ((skip & 1) ? 0 : Mb * dd); pi += 32) {
             const int m = small_div<MT>(pi, dd), j = pi - m * dd;
             const double *al = alS + m * a.Tpad;
             double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
             for (int i0 = warp * 32; i0 < T; i0 += kThreads) {
                 const int n = min(32, T - i0);
-                int ii = 0;
-                for (; ii + 4 <= n; ii += 4) {
-                    const int i = i0 + ii;
-                    c0 = fma(al[i], encW[(size_t)i * dd + j], c0);
-                    c1 = fma(al[i + 1], encW[(size_t)(i + 1) * dd + j], c1);
-                    c2 = fma(al[i + 2], encW[(size_t)(i + 2) * dd + j], c2);
-                    c3 = fma(al[i + 3], encW[(size_t)(i + 3) * dd + j], c3);
+                if (PS && n == 32) {
+                    const double2 *ap = reinterpret_cast<const double2 *>(al + i0);
+                    const double2 *ep = reinterpret_cast<const double2 *>(encW + j * a.ewld + i0);
+#pragma unroll
+                    for (int q = 0; q < 16; q += 2) {
+                        const double2 a0 = ap[q], a1 = ap[q + 1], e0 = ep[q], e1 = ep[q + 1];
+                        c0 = fma(a0.x, e0.x, c0);
+                        c1 = fma(a0.y, e0.y, c1);
+                        c2 = fma(a1.x, e1.x, c2);
+                        c3 = fma(a1.y, e1.y, c3);
+                    }
+                } else {
+                    for (int ii = 0; ii < n; ii++) {
+                        const int i = i0 + ii;
+                        const double ew = PS ? encW[j * a.ewld + i] : encW[(size_t)i * dd + j];
+                        c0 = fma(al[i], ew, c0);
+                    }
                 }
-                for (; ii < n; ii++) c0 = fma(al[i0 + ii], encW[(size_t)(i0 + ii) * dd + j], c0);
             }
-            puc[(warp * M + m) * dd + j] = (c0 + c1) + (c2 + c3);
+            const double v = (c0 + c1) + (c2 + c3);
+            puc[(warp * M + m) * dd + j] = v;
+            if (pi == lane) ucv = v;
         }
         if (lane == 0) {
 #pragma unroll
@@ -516,9 +560,26 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     psm[warp * M + m] = lsm[m];
                 }
         }
-        __syncwarp();
         // pz_w[m][d] = dev_table[d] . uc_w[m]
-        for (int pi = lane; pi < Mb * D; pi += 32) {
+        if (dd == 16 && Mb <= 2) {
+            // lanes (m, j) hold uc_w[m][j]: per device, a 16-lane butterfly sum
+            const int m = lane >> 4, j = lane & 15;
+            for (int d0 = 0; d0 < ((skip & 2) ? 0 : D); d0 += 4) {
+                double v[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) v[q] = d0 + q < D ? devt[(d0 + q) * 16 + j] * ucv : 0.0;
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+                    for (int q = 0; q < 4; q++) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+                if (j == 0 && m < Mb)
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (d0 + q < D) pz[(warp * M + m) * D + d0 + q] = v[q];
+            }
+        } else {
+        __syncwarp();
+        for (int pi = lane; pi < ((skip & 2) ? 0 : Mb * D); pi += 32) {
             const int m = small_div<MT>(pi, D), d = pi - m * D;
             const double *pv = puc + (warp * M + m) * dd;
             double z0 = 0.0, z1 = 0.0;
@@ -530,9 +591,10 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             if (o < dd) z0 = fma(devt[d * dd + o], pv[o], z0);
             pz[(warp * M + m) * D + d] = z0 + z1;
         }
+        }
         // uh = h @ W_out[:64] (policy.py:302, h half), 8 lanes per output
         {
-            const int total = Mb * dd * 8;
+            const int total = (skip & 4) ? 0 : Mb * dd * 8;
             for (int b0 = 0; b0 < total; b0 += kThreads) {
                 const int idx = b0 + tid;
                 const bool ok = idx < total;
@@ -570,13 +632,18 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 rs = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
                 r = pcg_double(rs);
             }
-            double gmx = pmx[m];
-#pragma unroll
-            for (int ww = 1; ww < kWarps; ww++) gmx = fmax(gmx, pmx[ww * M + m]);
-            const double f = lane < kWarps ? exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
+            double gmx = 0.0, f = lane < kWarps ? 1.0 : 0.0;
             double fw[kWarps];
 #pragma unroll
-            for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
+            for (int ww = 0; ww < kWarps; ww++) fw[ww] = 1.0;
+            if (!noshift) {
+                gmx = pmx[m];
+#pragma unroll
+                for (int ww = 1; ww < kWarps; ww++) gmx = fmax(gmx, pmx[ww * M + m]);
+                f = lane < kWarps ? exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
+            }
             double gsum = 0.0;
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
@@ -738,7 +805,7 @@ static ParamLayout layout_of(int V1, int D, int dd, int F, int td) {
 extern "C" void dp_policy_destroy(dp_policy *p) {
     if (!p) return;
     void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
-                    p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->act_u, p->act_p,
+                    p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->proj_nmax, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
                     p->tile_part, p->tile_partA, p->partA, p->a_tot, p->act_e, p->act_esc};
@@ -830,6 +897,7 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     alloc((void **)&p->row_du, sizeof(double) * rows * dev_dim);
     alloc((void **)&p->proj, sizeof(double) * T * kH);
     alloc((void **)&p->encW, sizeof(double) * T * dev_dim);
+    alloc((void **)&p->proj_nmax, sizeof(unsigned long long));
     alloc((void **)&p->act_u, sizeof(double) * rows * dev_dim);
     alloc((void **)&p->act_p, sizeof(double) * rows * n_dev);
     alloc((void **)&p->act_stat, sizeof(double) * rows * 2);
@@ -899,6 +967,10 @@ extern "C" int dp_debug_decoder_variant(int32_t mode) {
 extern "C" int dp_debug_phase_clocks(int32_t enable, int64_t *h_out) {
     DP_ENTRY();
     const int on = enable ? 1 : 0;
+    {
+        const int skip = enable > 1 ? enable >> 1 : 0;  // debug ablation bits (enable = 1 | skip << 1)
+        DP_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_skip, &skip, sizeof(int)));
+    }
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_clocks, &on, sizeof(int)));
     if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_phase_clk, sizeof(long long) * 8));
     long long z[16] = {0};
@@ -932,7 +1004,8 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
     DP_LAUNCH_CHECK();
     enc_rec_kernel<<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
     DP_LAUNCH_CHECK();
-    dec_prep_kernel<<<dm.T, 128, 0, st>>>(dm, params, p->enc_h, p->proj, p->encW);
+    DP_CUDA_TRY(cudaMemsetAsync(p->proj_nmax, 0, sizeof(unsigned long long), st));
+    dec_prep_kernel<<<dm.T, 128, 0, st>>>(dm, params, p->enc_h, p->proj, p->encW, p->proj_nmax);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
@@ -967,7 +1040,8 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
                 return r;
             };
             a.o_proj = enc_smem ? take(T * kProjLd) : 0;
-            a.o_encw = enc_smem ? take(T * dd) : 0;
+            a.ewld = ((T + 1) & ~1) + 2;
+            a.o_encw = enc_smem ? take(a.ewld * dd) : 0;
             a.o_wout = take(kWout1Ld * dd);
             a.o_devt = take(D * dd);
             a.o_bout = take(D);
@@ -1047,6 +1121,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.edev = p->edev;
     a.proj = p->proj;
     a.encW = p->encW;
+    a.proj_nmax = p->proj_nmax;
     a.act_h = p->act_h;
     a.act_c = p->act_c;
     a.act_g = p->act_g;
@@ -1063,6 +1138,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.probs_out = probs_out;
     a.M = pl.M;
     a.Tpad = pl.Tpad;
+    a.ewld = ((dm.T + 1) & ~1) + 2;
     const int grid = ceil_div(K, pl.M);
     cudaStream_t st = (cudaStream_t)stream;
     const void *fn = pl.enc_in_smem ? (pl.spec ? dec_fn<true, true>(pl.MT) : dec_fn<true, false>(pl.MT))

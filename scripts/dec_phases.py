@@ -26,13 +26,14 @@ eng.encode(pdev)
 eng.decode(pdev, K, pcg=(1, 3))
 torch.cuda.synchronize()
 out = (ctypes.c_int64 * 8)()
-nat.check(nat.lib().dp_debug_phase_clocks(1, None), "dbg")
+skip = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+nat.check(nat.lib().dp_debug_phase_clocks(1 | (skip << 1), None), "dbg")
 eng.decode(pdev, K, pcg=(1, 3))
 torch.cuda.synchronize()
 nat.check(nat.lib().dp_debug_phase_clocks(0, out), "dbg")
 T = len(feats)
 names = ["A gates+cell", "C scores/softmax/uc/uh/next-g", "E combine+draw"]
 tot = sum(out)
-print(f"{name} K={K} T={T} variant={variant}: {tot / T:.0f} cycles/step")
+print(f"{name} K={K} T={T} variant={variant} skip={skip}: {tot / T:.0f} cycles/step")
 for n, v in zip(names, out[:3]):
     print(f"  {n:32s} {v / T:8.0f} cycles/step  {100 * v / tot:5.1f}%")

@@ -199,3 +199,22 @@ def test_speculative_cell_decoder_vs_oracle(name, K):
         opl, olp, _ = pol.sample(rng)
         assert np.array_equal(pl[k], opl), f"sample {k}"
         assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
+
+
+@pytest.mark.parametrize("scale", [1.0, 400.0])
+def test_attention_softmax_shift_paths_vs_oracle(scale):
+    """Large attention weights (8 max||proj_t|| > 600) take the max-shifted
+    softmax; small ones the shift-free path (csrc/policy_fwd.cu kNoShiftBound).
+    Both sample the oracle's placements and match its log-probs and gradient."""
+    gg, topo, params, feats = _setup("C1", seed=6)
+    params.w_att = params.w_att * scale
+    pl, lp = P.sample_batch(params, feats, np.random.default_rng(3), 6)
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    rng = np.random.default_rng(3)
+    for k in range(6):
+        opl, olp, _ = pol.sample(rng)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=1e-10)
+    got = P.grad_log_prob(params, feats, [int(x) for x in pl[0]])
+    assert _relnorm(got, pol.grad([int(x) for x in pl[0]])) < 1e-8
