@@ -178,6 +178,16 @@ typedef struct {
     int64_t error;        /* 1: a feasible measurement was not positive/finite */
 } dp_train_state;
 
+/* Batched search baselines on K-sim (pkg/baselines.py:227-273).
+ * dp_enumerate_placements: out[count*n] (by gid) = placements start..start+
+ *   count-1 of itertools.product(range(d), repeat=n) (last group fastest).
+ * dp_argmin_feasible: folds the first minimal feasible makespan of a batch
+ *   (global index base_index + k) into (*best_val, *best_idx) with a strict <
+ *   (earlier batches keep ties); *best_idx = -1 initially. */
+int dp_enumerate_placements(int32_t n, int32_t d, uint64_t start, int32_t count, uint8_t *out, void *stream);
+int dp_argmin_feasible(int32_t K, const double *makespan, const uint8_t *feasible, int64_t base_index,
+                       double *best_val, int64_t *best_idx, void *stream);
+
 /* Rewards, best-so-far, success-only filter, baseline and advantages for one
  * update (pkg/trainer.py:66-72, 83-84, 138-154, 281-304), on device:
  *   makespan[K], feasible[K], choice[K*T]: all K samples of the update
@@ -191,6 +201,15 @@ int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespan, const ui
                           int64_t k_offset, int32_t K_local, dp_train_state *state, double *adv,
                           uint8_t *best_choice, double *log_rows, int64_t log_cap, int32_t controller_id,
                           void *stream);
+
+/* measure() with lognormal noise (pkg/simulator.py:205-223, pkg/trainer.py:
+ * 244-253, 277): for every feasible k, makespan[k] <- np.mean(makespan[k] *
+ * factors[update][k][0..n_factors)) in numpy's pairwise order, update =
+ * state->update.  factors = exp(sigma * default_rng(seed_k).standard_normal(
+ * steps))[1:] per sample, seeds from the controller's noise stream (host).
+ * Sets state->error = 2 if update >= n_updates. */
+int dp_apply_measurement_noise(int32_t K, double *makespan, const uint8_t *feasible, const double *factors,
+                               int64_t n_updates, int32_t n_factors, dp_train_state *state, void *stream);
 
 /* ParameterStore.apply (pkg/trainer.py:113-131): grad is the advantage-weighted
  * SUM from dp_policy_backward; it is divided by n_used here.  Skips the step

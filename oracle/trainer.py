@@ -95,10 +95,19 @@ def run(gg, topo, cfg: dict, record=False):
     for upd in range(U):
         pol = opol.Policy(store.x.copy(), dims, feats)
         draws = [pol.sample(srng) for _ in range(K)]
-        for _ in range(K):
-            nrng.integers(1 << 62)  # noise seeds are drawn even with noise off (trainer.py:277)
+        # noise seeds are drawn even with noise off (trainer.py:277)
+        seeds = [int(nrng.integers(1 << 62)) for _ in range(K)]
         rep = og.simulate([s[0] for s in draws])
-        meas = [float(m) if f else INF for m, f in zip(rep["makespan"], rep["feasible"])]
+        sigma, steps = cfg.get("noise_sigma", 0.0), cfg.get("measure_steps", 10)
+        meas = []
+        for m, f, sd in zip(rep["makespan"], rep["feasible"], seeds):
+            if steps < 2 or not f:  # measure() raises (-> INFEASIBLE) / infeasible
+                meas.append(INF)
+            elif sigma > 0.0:  # simulator.py:221-223
+                fac = np.exp(sigma * np.random.default_rng(sd).standard_normal(steps))
+                meas.append(float(np.mean(float(m) * fac[1:])))
+            else:
+                meas.append(float(m))
         rw = [reward(m, fail) for m in meas]
         ok = [m != INF for m in meas]
         for s, r, good in zip(draws, rw, ok):

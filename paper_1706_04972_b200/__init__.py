@@ -21,4 +21,8 @@ from .trainer import (BaselineState, LogRow, ParameterStore, RewardSpec, Trainer
                       TrainResult, apply_adam, log_to_csv, reinforce_update, reward_of, run_controller,
                       suggest_failing_signal, train)
 
+from . import baselines  # noqa: F401,E402
+from .baselines import (NoFeasiblePlacement, SearchSpaceTooLarge, brute_force,  # noqa: F401,E402
+                        place_random_search, place_single)
+
 __version__ = "0.1.0"

@@ -403,6 +403,57 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     feasible[k] = ok ? 1 : 0;
 }
 
+// Lexicographic enumeration for brute force (itertools.product order:
+// the last group varies fastest), placements by gid.
+__global__ void enumerate_kernel(int n, int d, unsigned long long start, int count, uint8_t *__restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    unsigned long long c = start + (unsigned long long)k;
+    uint8_t *o = out + (size_t)k * n;
+    for (int g = n - 1; g >= 0; g--) {
+        o[g] = (uint8_t)(c % (unsigned long long)d);
+        c /= (unsigned long long)d;
+    }
+}
+
+// First (lowest index) minimal makespan among feasible placements, folded
+// into (best_val, best_idx) with a strict < so earlier batches win ties —
+// the reference's sequential `if makespan < best` (pkg/baselines.py:246-272).
+__global__ void argmin_feasible_kernel(int K, const double *__restrict__ makespan, const uint8_t *__restrict__ feasible,
+                                       long long base_index, double *best_val, long long *best_idx) {
+    __shared__ double sv[1024];
+    __shared__ long long si[1024];
+    const int tid = threadIdx.x;
+    double v = INFINITY;
+    long long idx = -1;
+    for (int k = tid; k < K; k += blockDim.x) {
+        if (!feasible[k]) continue;
+        const double m = makespan[k];
+        if (idx < 0 || m < v) {  // k ascending per thread: first minimum kept
+            v = m;
+            idx = base_index + k;
+        }
+    }
+    sv[tid] = v;
+    si[tid] = idx;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (tid < s) {
+            const double v2 = sv[tid + s];
+            const long long i2 = si[tid + s];
+            if (i2 >= 0 && (si[tid] < 0 || v2 < sv[tid] || (v2 == sv[tid] && i2 < si[tid]))) {
+                sv[tid] = v2;
+                si[tid] = i2;
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0 && si[0] >= 0 && (*best_idx < 0 || sv[0] < *best_val)) {
+        *best_val = sv[0];
+        *best_idx = si[0];
+    }
+}
+
 constexpr size_t kSmemBudget = 220 * 1024;
 constexpr int kRegDevMax = 8;
 
@@ -522,4 +573,25 @@ extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *pl
                                              transfer, peak, feasible, order, err, S);
     return launch_sim<false, 0>(g, grid, threads, smem, st, K, placement, by_rank, makespan, busy, transfer, peak,
                                 feasible, order, err, S);
+}
+
+extern "C" int dp_enumerate_placements(int32_t n, int32_t d, uint64_t start, int32_t count, uint8_t *out,
+                                       void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(n >= 1 && d >= 1 && d <= 255 && count >= 0 && out, "dp_enumerate_placements: bad argument");
+    if (count == 0) return DP_OK;
+    enumerate_kernel<<<dp::ceil_div(count, 256), 256, 0, (cudaStream_t)stream>>>(n, d, start, count, out);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+extern "C" int dp_argmin_feasible(int32_t K, const double *makespan, const uint8_t *feasible, int64_t base_index,
+                                  double *best_val, int64_t *best_idx, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(K >= 0 && makespan && feasible && best_val && best_idx, "dp_argmin_feasible: NULL argument");
+    if (K == 0) return DP_OK;
+    argmin_feasible_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(K, makespan, feasible, base_index, best_val,
+                                                                  (long long *)best_idx);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
 }

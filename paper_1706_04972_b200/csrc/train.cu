@@ -120,6 +120,28 @@ __global__ void epilogue_kernel(int K, int T, const double *__restrict__ makespa
         for (int t = tid; t < T; t += blockDim.x) best_choice[t] = choice[(size_t)bk * T + t];
 }
 
+// measure() with lognormal noise (pkg/simulator.py:218-223): a feasible
+// sample's measurement is np.mean(base * factors[1:]) — the factors row of
+// (update, k) comes from the host (the reference's own numpy streams,
+// pkg/trainer.py:277), the product and numpy's pairwise mean run here.
+__global__ void noise_kernel(int K, double *__restrict__ makespan, const uint8_t *__restrict__ feasible,
+                             const double *__restrict__ factors, long long n_updates, int n_factors,
+                             dp_train_state *st) {
+    const long long u = st->update;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    if (u < 0 || u >= n_updates) {
+        st->error = 2;  // noise table exhausted
+        return;
+    }
+    if (!feasible[k]) return;
+    const double base = makespan[k];
+    const double *f = factors + ((size_t)u * K + k) * n_factors;
+    double prod[64];
+    for (int s = 0; s < n_factors; s++) prod[s] = base * f[s];
+    makespan[k] = np_pairwise(prod, n_factors) / (double)n_factors;
+}
+
 __global__ void finite_check_kernel(long long P, const double *__restrict__ g, int *__restrict__ flag) {
     long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     int bad = 0;
@@ -188,6 +210,18 @@ extern "C" int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespa
     epilogue_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(K, T, makespan, feasible, choice, failing, decay,
                                                             success_only_after, k_offset, K_local, state, adv,
                                                             best_choice, log_rows, log_cap, controller_id);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+extern "C" int dp_apply_measurement_noise(int32_t K, double *makespan, const uint8_t *feasible,
+                                          const double *factors, int64_t n_updates, int32_t n_factors,
+                                          dp_train_state *state, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(K >= 1 && makespan && feasible && factors && state, "dp_apply_measurement_noise: NULL argument");
+    DP_REQUIRE(n_factors >= 1 && n_factors <= 64, "dp_apply_measurement_noise: need 1 <= steps-1 <= 64");
+    noise_kernel<<<ceil_div(K, 128), 128, 0, (cudaStream_t)stream>>>(K, makespan, feasible, factors, n_updates,
+                                                                       n_factors, state);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }

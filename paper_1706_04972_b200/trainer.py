@@ -306,9 +306,6 @@ class DeviceController:
         import torch
 
         cfg = task.config
-        if cfg.noise_sigma > 0.0:
-            raise NotImplementedError("measurement noise (noise_sigma > 0) is not on the device path yet "
-                                      "(SURVEY.md §8(f) row f2)")
         self.task, self.store, self.cid = task, store, controller_id
         self.device = store.device
         from .parallel import Exchange, shard
@@ -323,7 +320,7 @@ class DeviceController:
                                            k_max=self.K_local)
         self.dg = device_graph(task.gg, task.topo)
         self.T = len(task.feats)
-        sample_seq, _noise_seq = seed_seq.spawn(2)
+        sample_seq, noise_seq = seed_seq.spawn(2)
         self.rng = np.random.default_rng(sample_seq)
         self.pcg = policy_mod.generator_state(self.rng)
         self.log_cap = log_cap if log_cap is not None else cfg.total_updates
@@ -346,6 +343,12 @@ class DeviceController:
             self.fe_all = torch.zeros(K, dtype=torch.uint8, device=dev)
             self.ch_all = torch.zeros(K, T, dtype=torch.uint8, device=dev)
         self.measure_ok = cfg.measure_steps >= 2
+        # measurement noise (f2): the factor rows of every update, drawn up front
+        # from the controller's noise stream exactly as the reference does
+        self.noise = None
+        if cfg.noise_sigma > 0.0 and self.measure_ok and cfg.total_updates > 0:
+            tab = noise_factor_table(noise_seq, K, cfg.total_updates, cfg.noise_sigma, cfg.measure_steps)
+            self.noise = torch.as_tensor(tab, device=dev).contiguous()
         self.updates_done = 0
         self._graph = None
         self.side = torch.cuda.Stream(device=dev)
@@ -383,6 +386,10 @@ class DeviceController:
             self.xchg.all_gather(self.fe_all, fe)
             self.xchg.all_gather(self.ch_all, ch)
             mk, fe, ch = self.mk_all, self.fe_all, self.ch_all
+        if self.noise is not None:
+            nat.check(nat.lib().dp_apply_measurement_noise(
+                self.K, nat.ptr(mk), nat.ptr(fe), nat.ptr(self.noise), self.noise.shape[0], self.noise.shape[2],
+                nat.ptr(st.state), nat.stream_ptr(stream)), "dp_apply_measurement_noise")
         mark("epilogue")
         rc = nat.lib().dp_reinforce_epilogue(
             self.K, self.T, nat.ptr(mk), nat.ptr(fe), nat.ptr(ch), self.task.reward_spec.failing_signal,
@@ -437,6 +444,8 @@ class DeviceController:
 
     def check_errors(self):
         st = _state_read(self.store.state)
+        if st["error"] == 2:
+            raise RuntimeError("measurement-noise table exhausted (more updates than total_updates)")
         if st["error"]:
             raise ValueError("measurement must be positive and finite (a feasible placement has makespan <= 0)")
         return st
@@ -456,6 +465,37 @@ class DeviceController:
             return math.inf, None
         pl = self.eng.by_gid(self.best_choice.view(1, -1))[0].cpu().numpy().astype(int).tolist()
         return st["best_r"], pl
+
+
+def _noise_rows(args):
+    seeds, sigma, steps = args
+    out = np.empty((len(seeds), steps - 1))
+    for i, sd in enumerate(seeds):
+        out[i] = np.exp(sigma * np.random.default_rng(sd).standard_normal(steps))[1:]
+    return out
+
+
+def noise_factor_table(noise_seq, K: int, updates: int, sigma: float, steps: int) -> np.ndarray:
+    """[updates, K, steps-1] lognormal factors of the reference's noisy measure()
+    (``pkg/trainer.py:262, 277`` seeds; ``pkg/simulator.py:221-223`` factors):
+    seeds come sequentially from the controller's noise stream, each
+    measurement's factors from ``default_rng(seed).standard_normal(steps)``.
+    Large tables fan the per-seed generators out over host processes."""
+    rng = np.random.default_rng(noise_seq)
+    seeds = [int(rng.integers(1 << 62)) for _ in range(updates * K)]
+    n = len(seeds)
+    if n > 20000:
+        import concurrent.futures as cf
+        import os
+
+        w = max(1, min(32, len(os.sched_getaffinity(0))))
+        chunk = (n + w - 1) // w
+        with cf.ProcessPoolExecutor(w) as ex:
+            parts = list(ex.map(_noise_rows, [(seeds[i:i + chunk], sigma, steps) for i in range(0, n, chunk)]))
+        flat = np.concatenate(parts)
+    else:
+        flat = _noise_rows((seeds, sigma, steps))
+    return flat.reshape(updates, K, steps - 1)
 
 
 def _make_task(gg, topo, config: TrainerConfig) -> _TrainTask:

@@ -56,3 +56,18 @@ def train_golden(name):
     a["cfg"] = json.loads(str(a["cfg"]))
     a["csv"] = str(a["csv"])
     return a
+
+
+def baseline_cases():
+    """tests/golden/baselines.npz: [(gg, topo, bf_placement | None, bf_makespan, rs_budget, rs_placement | None)]
+    from the reference's brute_force / place_random_search (make_golden.py baselines)."""
+    a = npz("baselines.npz")
+    out = []
+    for i in range(int(a["n"])):
+        pre = f"i{i}_"
+        inst = {k[len(pre):]: v for k, v in a.items() if k.startswith(pre)}
+        gg, topo = instance_from_arrays(inst)
+        bf = [int(x) for x in inst["bf_placement"]] if inst["bf_placement"].size else None
+        rs = [int(x) for x in inst["rs_placement"]] if inst["rs_placement"].size else None
+        out.append((gg, topo, bf, float(inst["bf_makespan"]), int(inst["rs_budget"]), rs))
+    return out, [int(x) for x in a["c1_rs_placement"]]

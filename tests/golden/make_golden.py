@@ -287,6 +287,56 @@ def train_golden(gg, topo, cfg):
     return out, csv
 
 
+NOISE_RUNS = {
+    # f2: lognormal measurement noise on (pkg/trainer.py:244-253, simulator.py:205-223)
+    "C1noise": ("C1", dict(k=8, total_updates=3, seed=3, noise_sigma=0.25)),
+    "C3noise": ("C3tight", dict(k=8, total_updates=3, seed=4, noise_sigma=0.5, success_only_after=1,
+                                measure_steps=5)),
+}
+
+
+def baselines_golden(n=14, seed=777):
+    """f3: reference brute_force / place_random_search on small instances
+    (pkg/baselines.py:227-273), some memory-tight, plus random search on C1."""
+    rng = np.random.default_rng(seed)
+    out = {}
+    for i in range(n):
+        gg, topo = ref_util.random_instance(rng, max_groups=9, max_devices=3)
+        if i % 3 == 2:  # memory-tight: some (or all) placements infeasible
+            foot = sum(g.param_bytes + g.out_bytes for g in gg.groups)
+            mem = int(foot * (0.35 if i % 2 else 0.05)) + 1
+            topo = ref.DeviceTopology([ref.Device(d.id, d.kind, d.compute_rate, mem) for d in topo.devices],
+                                      topo.bandwidth)
+        for k, v in instance_arrays(gg, topo).items():
+            out[f"i{i}_{k}"] = v
+        try:
+            pl, mk = ref.brute_force(gg, topo)
+            out[f"i{i}_bf_placement"] = np.array(pl, np.uint8)
+            out[f"i{i}_bf_makespan"] = np.float64(mk)
+        except ref.NoFeasiblePlacement:
+            out[f"i{i}_bf_placement"] = np.zeros(0, np.uint8)
+            out[f"i{i}_bf_makespan"] = np.float64(np.nan)
+        rs = ref.place_random_search(gg, topo, budget=5 + 3 * i, seed=i)
+        out[f"i{i}_rs_budget"] = np.int64(5 + 3 * i)
+        out[f"i{i}_rs_placement"] = np.array(rs if rs is not None else [], np.uint8)
+    out["n"] = np.int64(n)
+    gg, topo, _ = configs()["C1"]
+    rs = ref.place_random_search(gg, topo, budget=300, seed=11)
+    out["c1_rs_placement"] = np.array(rs, np.uint8)
+    return out
+
+
+def main_noise():
+    cfgs = configs()
+    for name, (base, kw) in NOISE_RUNS.items():
+        gg, topo, _ = cfgs[base]
+        out, csv = train_golden(gg, topo, ref.TrainerConfig(**kw))
+        np.savez_compressed(os.path.join(HERE, f"train_{name}.npz"), **out)
+        with open(os.path.join(HERE, f"train_{name}.csv"), "w") as fh:
+            fh.write(csv)
+        print("train", name, flush=True)
+
+
 def main():
     t0 = time.time()
     cfgs = configs()
@@ -328,4 +378,10 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "noise":
+        main_noise()
+    elif len(sys.argv) > 1 and sys.argv[1] == "baselines":
+        np.savez_compressed(os.path.join(HERE, "baselines.npz"), **baselines_golden())
+        print("baselines")
+    else:
+        main()

@@ -85,3 +85,15 @@ def test_trainer_oracle_matches_reference(name):
     assert out["versions"] == int(g["store_versions"])
     if out["best_placement"] is not None:
         assert np.array_equal(out["best_placement"], g["best_placement"])
+
+
+@pytest.mark.parametrize("name,graph", [("C1noise", "C1"), ("C3noise", "C3tight")])
+def test_trainer_oracle_with_measurement_noise_matches_reference(name, graph):
+    """f2: lognormal measurement noise (reference train() with noise_sigma > 0)."""
+    gg, topo, _, _ = cfg(graph)
+    g = train_golden(name)
+    out = otr.run(gg, topo, g["cfg"], record=True)
+    assert otr.csv_of(out["rows"]) == g["csv"]
+    assert np.array_equal(np.array(out["placements"], np.uint8), g["placements"])
+    np.testing.assert_allclose(out["final"], g["final_params"], rtol=1e-12, atol=1e-15)
+    assert out["versions"] == int(g["store_versions"])

@@ -85,3 +85,17 @@ def test_train_is_deterministic_and_graph_replay_equals_eager():
     torch.cuda.synchronize()
     assert dp.log_to_csv(ctl.rows(), False) == dp.log_to_csv(a.log, False)
     assert np.array_equal(store.snapshot()[0], a.final_params)
+
+
+@pytest.mark.parametrize("name,graph", [("C1noise", "C1"), ("C3noise", "C3tight")])
+def test_train_with_measurement_noise_matches_reference(name, graph):
+    """f2 on the device path: host-drawn factor table + dp_apply_measurement_noise."""
+    gg, topo, _, _ = cfg(graph)
+    g = train_golden(name)
+    res = dp.train(gg, topo, _cfg(g["cfg"]))
+    assert dp.log_to_csv(res.log, include_wall=False) == g["csv"]
+    assert res.store_versions == int(g["store_versions"])
+    rel = np.linalg.norm(res.final_params - g["final_params"]) / np.linalg.norm(g["final_params"])
+    assert rel < 1e-12
+    if len(g["best_placement"]):
+        assert res.best_placement == [int(x) for x in g["best_placement"]]
