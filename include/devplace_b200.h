@@ -216,10 +216,13 @@ int dp_apply_measurement_noise(int32_t K, double *makespan, const uint8_t *feasi
  * when n_used == 0 (reinforce_update returned None), rejects non-finite
  * gradients (rejected++), else Adam with bias_corr[2*(t-1)+{0,1}] =
  * 1-b1^t, 1-b2^t (host-computed Python floats) and version++.  Then advances
- * state->update.  flag: device int32 scratch, zero-initialised. */
+ * state->update.  flag: device int32 scratch, zero-initialised.
+ * store_state: the shared ParameterStore's counters (adam_t, version,
+ * rejected) when several controllers share one store (pkg/trainer.py:365-378);
+ * NULL = state (single controller). */
 int dp_adam_apply(int64_t P, double *params, double *m, double *v, const double *grad, const double *bias_corr,
                   int64_t t_cap, double lr, double b1, double b2, double eps, dp_train_state *state,
-                  int32_t *flag, double *log_rows, int64_t log_cap, void *stream);
+                  dp_train_state *store_state, int32_t *flag, double *log_rows, int64_t log_cap, void *stream);
 
 #ifdef __cplusplus
 }

@@ -133,6 +133,61 @@ def run(gg, topo, cfg: dict, record=False):
                 versions=store.version, rejected=store.rejected, **rec)
 
 
+def run_multi(gg, topo, cfg: dict):
+    """C controllers sharing one store (pkg/trainer.py:365-378) under the
+    deterministic round schedule the device runner uses: every round all
+    controllers sample from the same store version, then apply in controller
+    order.  (One of the reference's admissible asynchronous interleavings; with
+    C == 1 it is exactly ``run``.)  Rows sorted by (controller, update)."""
+    K, U, C = cfg["k"], cfg["total_updates"], cfg.get("controllers", 1)
+    seed = cfg.get("seed", 0)
+    dims = dims_for(gg, topo, cfg)
+    feats = opol.features(gg, opol.vocab_of(gg), dims.shape_slots, dims.adj_slots)
+    fail = cfg.get("failing_signal") or failing_signal(gg, topo)
+    store = Adam(opol.init_flat(dims, seed, cfg.get("init_scale", 0.1)), cfg.get("learning_rate", 1e-3),
+                 cfg.get("adam_beta1", 0.9), cfg.get("adam_beta2", 0.999), cfg.get("adam_epsilon", 1e-8))
+    decay = cfg.get("baseline_decay", 0.9)
+    soa = cfg.get("success_only_after", 5000)
+    og = OracleGraph(gg, topo)
+    ctl = []
+    for cs in np.random.SeedSequence(seed).spawn(C):
+        s_seq, n_seq = cs.spawn(2)
+        ctl.append(dict(srng=np.random.default_rng(s_seq), nrng=np.random.default_rng(n_seq), base=fail,
+                        best_r=INF, best_pl=None, rows=[]))
+    for upd in range(U):
+        snap = store.x.copy()
+        grads = []
+        for c in ctl:
+            pol = opol.Policy(snap.copy(), dims, feats)
+            draws = [pol.sample(c["srng"]) for _ in range(K)]
+            for _ in range(K):
+                c["nrng"].integers(1 << 62)
+            rep = og.simulate([d[0] for d in draws])
+            meas = [float(m) if f else INF for m, f in zip(rep["makespan"], rep["feasible"])]
+            rw = [reward(m, fail) for m in meas]
+            ok = [m != INF for m in meas]
+            for d, r, good in zip(draws, rw, ok):
+                if good and r < c["best_r"]:
+                    c["best_r"], c["best_pl"] = r, list(d[0])
+            used = list(range(K)) if upd < soa else [i for i in range(K) if ok[i]]
+            grad = None
+            if used:
+                b = c["base"]
+                grad = np.zeros(dims.n_params)
+                for i in used:
+                    grad += (rw[i] - b) * pol.grad(draws[i][0], draws[i][2])
+                grad /= len(used)
+                c["base"] = decay * b + (1.0 - decay) * float(np.mean([rw[i] for i in used]))
+            grads.append((grad, float(np.mean(rw)), sum(ok), len(used)))
+        for cid, (c, (grad, mr, nf, nu)) in enumerate(zip(ctl, grads)):
+            ver = store.apply(grad) if grad is not None else store.version
+            c["rows"].append((upd, cid, ver, mr, c["base"], c["best_r"], nf, nu))
+    best = min(ctl, key=lambda c: c["best_r"])
+    rows = [r for c in ctl for r in c["rows"]]
+    return dict(rows=rows, final=store.x, best_placement=best["best_pl"], best_r=best["best_r"],
+                versions=store.version, rejected=store.rejected)
+
+
 def csv_of(rows) -> str:
     lines = ["update_index,controller_id,store_version,mean_R,baseline,best_R,n_feasible_of_K"]
     for (u, c, ver, mr, b, br, nf, _nu) in rows:

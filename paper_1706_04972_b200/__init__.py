@@ -19,7 +19,7 @@ from .policy import (EmbeddingSpec, GroupFeatures, PolicyParams, SampledPlacemen
                      sample_batch, save_checkpoint, step_distributions)
 from .trainer import (BaselineState, LogRow, ParameterStore, RewardSpec, TrainerConfig,  # noqa: F401,E402
                       TrainResult, apply_adam, log_to_csv, reinforce_update, reward_of, run_controller,
-                      suggest_failing_signal, train)
+                      suggest_failing_signal, train, train_many)
 
 from . import baselines  # noqa: F401,E402
 from .baselines import (NoFeasiblePlacement, SearchSpaceTooLarge, brute_force,  # noqa: F401,E402

@@ -40,7 +40,7 @@ SIGNATURES = {
     "dp_policy_backward_rows": (I32, [P, P, I32, P]),
     "dp_policy_backward_grads": (I32, [P, P, I32, P, P, P]),
     "dp_reinforce_epilogue": (I32, [I32, I32, P, P, P, F64, F64, I64, I64, I32, P, P, P, P, I64, I32, P]),
-    "dp_adam_apply": (I32, [I64, P, P, P, P, P, I64, F64, F64, F64, F64, P, P, P, I64, P]),
+    "dp_adam_apply": (I32, [I64, P, P, P, P, P, I64, F64, F64, F64, F64, P, P, P, P, I64, P]),
     "dp_apply_measurement_noise": (I32, [I32, P, P, P, I64, I32, P, P]),
     "dp_enumerate_placements": (I32, [I32, I32, ctypes.c_uint64, I32, P, P]),
     "dp_argmin_feasible": (I32, [I32, P, P, I64, P, P, P]),

@@ -155,10 +155,10 @@ __global__ void finite_check_kernel(long long P, const double *__restrict__ g, i
 __global__ void adam_kernel(long long P, double *__restrict__ p, double *__restrict__ m, double *__restrict__ v,
                             const double *__restrict__ grad, const double *__restrict__ bias_corr, long long t_cap,
                             double lr, double b1, double b2, double eps, const dp_train_state *st,
-                            const int *__restrict__ flag) {
+                            const dp_train_state *store, const int *__restrict__ flag) {
     const long long nu = st->n_used;
     if (nu <= 0 || *flag) return;
-    const long long t = st->adam_t + 1;
+    const long long t = store->adam_t + 1;
     if (t > t_cap) return;
     const double bc1 = bias_corr[2 * (t - 1)], bc2 = bias_corr[2 * (t - 1) + 1];
     const double c1 = 1.0 - b1, c2 = 1.0 - b2;
@@ -175,17 +175,18 @@ __global__ void adam_kernel(long long P, double *__restrict__ p, double *__restr
     }
 }
 
-__global__ void step_finalize_kernel(dp_train_state *st, int *flag, double *log_rows, long long log_cap) {
+__global__ void step_finalize_kernel(dp_train_state *st, dp_train_state *store, int *flag, double *log_rows,
+                                     long long log_cap) {
     if (threadIdx.x != 0) return;
     if (st->n_used > 0) {
         if (*flag) {
-            st->rejected += 1;
+            store->rejected += 1;
         } else {
-            st->adam_t += 1;
-            st->version += 1;
+            store->adam_t += 1;
+            store->version += 1;
         }
     }
-    if (st->update < log_cap) log_rows[st->update * 8 + 2] = (double)st->version;
+    if (st->update < log_cap) log_rows[st->update * 8 + 2] = (double)store->version;
     *flag = 0;
     st->update += 1;
 }
@@ -228,17 +229,20 @@ extern "C" int dp_apply_measurement_noise(int32_t K, double *makespan, const uin
 
 extern "C" int dp_adam_apply(int64_t P, double *params, double *m, double *v, const double *grad,
                              const double *bias_corr, int64_t t_cap, double lr, double b1, double b2, double eps,
-                             dp_train_state *state, int32_t *flag, double *log_rows, int64_t log_cap, void *stream) {
+                             dp_train_state *state, dp_train_state *store_state, int32_t *flag, double *log_rows,
+                             int64_t log_cap, void *stream) {
     DP_ENTRY();
     DP_REQUIRE(P >= 1 && params && m && v && grad && bias_corr && state && flag,
                "dp_adam_apply: NULL argument");
+    if (!store_state) store_state = state;
     cudaStream_t st = (cudaStream_t)stream;
     const int blocks = ceil_div(P, 256) < 2 * kNumSMs ? ceil_div(P, 256) : 2 * kNumSMs;
     finite_check_kernel<<<blocks, 256, 0, st>>>(P, grad, flag);
     DP_LAUNCH_CHECK();
-    adam_kernel<<<blocks, 256, 0, st>>>(P, params, m, v, grad, bias_corr, t_cap, lr, b1, b2, eps, state, flag);
+    adam_kernel<<<blocks, 256, 0, st>>>(P, params, m, v, grad, bias_corr, t_cap, lr, b1, b2, eps, state, store_state,
+                                        flag);
     DP_LAUNCH_CHECK();
-    step_finalize_kernel<<<1, 32, 0, st>>>(state, flag, log_rows, log_cap);
+    step_finalize_kernel<<<1, 32, 0, st>>>(state, store_state, flag, log_rows, log_cap);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }

@@ -146,15 +146,17 @@ class ParameterStore:
         with self._lock:
             return self.params.cpu().numpy().copy(), self.version
 
-    def adam(self, grad, log=None, log_cap=0, stream=None):
-        """Enqueue dp_adam_apply (grad = advantage-weighted sum; /n_used inside)."""
+    def adam(self, grad, log=None, log_cap=0, stream=None, state=None):
+        """Enqueue dp_adam_apply (grad = advantage-weighted sum; /n_used inside).
+        ``state``: the applying controller's state (n_used, update, log row);
+        the store's own counters (adam_t, version, rejected) live in ``self.state``."""
         from . import _native as nat
 
         rc = nat.lib().dp_adam_apply(
             self.params.numel(), nat.ptr(self.params), nat.ptr(self.m), nat.ptr(self.v), nat.ptr(grad),
             nat.ptr(self.bias), self._bias_cap, self.learning_rate, self.beta1, self.beta2, self.epsilon,
-            nat.ptr(self.state), nat.ptr(self.flag), nat.ptr(log if log is not None else self._scratch_log),
-            log_cap, nat.stream_ptr(stream))
+            nat.ptr(state if state is not None else self.state), nat.ptr(self.state), nat.ptr(self.flag),
+            nat.ptr(log if log is not None else self._scratch_log), log_cap, nat.stream_ptr(stream))
         nat.check(rc, "dp_adam_apply")
 
     def apply(self, gradient) -> int:
@@ -302,7 +304,11 @@ class DeviceController:
     baseline logic bit-identically) and all-reduce the gradient (NCCL)."""
 
     def __init__(self, task: _TrainTask, store: ParameterStore, seed_seq, controller_id: int = 0,
-                 world=None, log_cap: int | None = None):
+                 world=None, log_cap: int | None = None, shared: bool = False):
+        """``shared``: several controllers share ``store`` (f1): this controller
+        keeps its own state (baseline, best, update counter, log) and samples
+        from a private parameter snapshot taken by the runner; the store's
+        counters (adam_t, version, rejected) stay in ``store.state``."""
         import torch
 
         cfg = task.config
@@ -324,9 +330,16 @@ class DeviceController:
         self.rng = np.random.default_rng(sample_seq)
         self.pcg = policy_mod.generator_state(self.rng)
         self.log_cap = log_cap if log_cap is not None else cfg.total_updates
-        store._ensure_bias(cfg.total_updates + 1)
-        st = store.state
-        st.zero_()
+        store._ensure_bias(cfg.total_updates * max(1, cfg.controllers) + 1)
+        self.shared = shared
+        if shared:
+            self.state = _state_tensor(store.device)
+            self.params_src = torch.empty_like(store.params)
+        else:
+            self.state = store.state
+            self.state.zero_()
+            self.params_src = store.params
+        st = self.state
         st[0] = task.reward_spec.failing_signal
         st[2] = math.inf
         dev = self.device
@@ -354,22 +367,25 @@ class DeviceController:
         self.side = torch.cuda.Stream(device=dev)
 
     # one update, enqueue-only (capturable)
-    def step(self, stream=None, marks=None):
+    def step(self, stream=None, marks=None, apply: bool = True):
         """Enqueue one update.  ``marks``: optional callable(name) recording a
-        CUDA event at each phase boundary (bench.py phase timing)."""
+        CUDA event at each phase boundary (bench.py phase timing).
+        ``apply=False`` stops before the Adam step (the shared-store runner
+        orders the controllers' applies itself)."""
         import torch
 
         from . import _native as nat
 
         mark = marks or (lambda _name: None)
         cfg, st = self.task.config, self.store
-        p = st.params
+        p = self.params_src
+        state = self.state
         main = stream if stream is not None else torch.cuda.current_stream()
         mark("encode")
         self.eng.encode(p, stream)
         mark("decode")
         self.eng.decode(p, self.K_local, pcg=self.pcg, draw_base=0, k_offset=self.k_offset,
-                        draw_counter=st.state.view(torch.int64)[3:4], draws_per_count=self.K * self.T,
+                        draw_counter=state.view(torch.int64)[3:4], draws_per_count=self.K * self.T,
                         choice=self.choice, logp=self.logp, stream=stream)
         mark("simulate")
         # the advantage-independent half of the backward runs on a side stream
@@ -389,11 +405,11 @@ class DeviceController:
         if self.noise is not None:
             nat.check(nat.lib().dp_apply_measurement_noise(
                 self.K, nat.ptr(mk), nat.ptr(fe), nat.ptr(self.noise), self.noise.shape[0], self.noise.shape[2],
-                nat.ptr(st.state), nat.stream_ptr(stream)), "dp_apply_measurement_noise")
+                nat.ptr(state), nat.stream_ptr(stream)), "dp_apply_measurement_noise")
         mark("epilogue")
         rc = nat.lib().dp_reinforce_epilogue(
             self.K, self.T, nat.ptr(mk), nat.ptr(fe), nat.ptr(ch), self.task.reward_spec.failing_signal,
-            cfg.baseline_decay, cfg.success_only_after, self.k_offset, self.K_local, nat.ptr(st.state),
+            cfg.baseline_decay, cfg.success_only_after, self.k_offset, self.K_local, nat.ptr(state),
             nat.ptr(self.adv), nat.ptr(self.best_choice), nat.ptr(self.log), self.log_cap, self.cid,
             nat.stream_ptr(stream))
         nat.check(rc, "dp_reinforce_epilogue")
@@ -403,9 +419,14 @@ class DeviceController:
         if self.size > 1:
             mark("allreduce")
             self.xchg.all_reduce_sum(self.grad)
-        mark("adam")
-        st.adam(self.grad, log=self.log, log_cap=self.log_cap, stream=stream)
+        if apply:
+            mark("adam")
+            self.apply(stream)
         mark("end")
+
+    def apply(self, stream=None):
+        """This controller's Adam step on the (possibly shared) store."""
+        self.store.adam(self.grad, log=self.log, log_cap=self.log_cap, stream=stream, state=self.state)
 
     def capture(self):
         """Capture one update in a CUDA graph (after one eager warm-up update)."""
@@ -443,7 +464,7 @@ class DeviceController:
         return walls
 
     def check_errors(self):
-        st = _state_read(self.store.state)
+        st = _state_read(self.state)
         if st["error"] == 2:
             raise RuntimeError("measurement-noise table exhausted (more updates than total_updates)")
         if st["error"]:
@@ -460,7 +481,7 @@ class DeviceController:
         return out
 
     def best(self):
-        st = _state_read(self.store.state)
+        st = _state_read(self.state)
         if not math.isfinite(st["best_r"]):
             return math.inf, None
         pl = self.eng.by_gid(self.best_choice.view(1, -1))[0].cpu().numpy().astype(int).tolist()
@@ -498,6 +519,140 @@ def noise_factor_table(noise_seq, K: int, updates: int, sigma: float, steps: int
     return flat.reshape(updates, K, steps - 1)
 
 
+class ConcurrentRunner:
+    """Several DeviceControllers advancing together, one CUDA stream each, all
+    captured into one CUDA graph per round.
+
+    * shared store (f1, ``TrainerConfig.controllers > 1``, pkg/trainer.py:
+      365-378): every round all controllers snapshot the same store version
+      (device copies on the launching stream), sample / score / differentiate
+      concurrently on their own streams, then apply in controller order — a
+      deterministic member of the reference's asynchronous interleavings
+      (oracle.trainer.run_multi restates it);
+    * independent stores (C4 mixed batch, ``train_many``): each controller's
+      whole update, Adam included, runs on its own stream."""
+
+    def __init__(self, ctls, shared_store: ParameterStore | None = None):
+        import torch
+
+        self.ctls, self.store = list(ctls), shared_store
+        self.streams = [torch.cuda.Stream(device=c.device) for c in self.ctls]
+        self._graph = None
+
+    def step(self):
+        import torch
+
+        main = torch.cuda.current_stream()
+        if self.store is not None:
+            for c in self.ctls:
+                c.params_src.copy_(self.store.params)
+        for c, s in zip(self.ctls, self.streams):
+            s.wait_stream(main)
+            with torch.cuda.stream(s):
+                c.step(stream=s, apply=self.store is None)
+        for s in self.streams:
+            main.wait_stream(s)
+        if self.store is not None:
+            for c in self.ctls:
+                c.apply(main)
+
+    def capture(self):
+        import gc
+
+        import torch
+
+        gc.collect()
+        gc.disable()
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.step()
+        finally:
+            gc.enable()
+        self._graph = g
+        return g
+
+    def run(self, updates: int, use_graph: bool = True, wall: bool = False):
+        import torch
+
+        walls = []
+        for _ in range(updates):
+            t0 = time.perf_counter()
+            if use_graph and self._graph is not None:
+                self._graph.replay()
+            else:
+                self.step()
+            if wall:
+                torch.cuda.current_stream().synchronize()
+                walls.append((time.perf_counter() - t0) * 1e3)
+            for c in self.ctls:
+                c.updates_done += 1
+        return walls
+
+    def train(self, updates: int):
+        """First round eager, then one captured graph replayed."""
+        import torch
+
+        walls = []
+        if updates > 0:
+            walls += self.run(1, use_graph=False, wall=True)
+        if updates > 1:
+            self.capture()
+            walls += self.run(updates - 1, use_graph=True, wall=True)
+        torch.cuda.current_stream().synchronize()
+        for c in self.ctls:
+            c.check_errors()
+        return walls
+
+
+def _result_of(task, store, ctls, walls) -> "TrainResult":
+    res = []
+    for c in ctls:
+        r = _ControllerResult(rows=c.rows(walls))
+        r.best_r, r.best_placement = c.best()
+        res.append(r)
+    rows = sorted([row for r in res for row in r.rows], key=lambda r: (r.controller_id, r.update_index))
+    best = min(res, key=lambda r: r.best_r)
+    best_pl = list(best.best_placement) if best.best_placement is not None else None
+    best_report = simulate(task.gg, task.topo, best_pl) if best_pl is not None else None
+    final, _ = store.snapshot()
+    return TrainResult(best_placement=best_pl, best_report=best_report, log=rows, final_params=final,
+                       store_versions=store.version, rejected_updates=store.rejected)
+
+
+def train_many(jobs) -> list:
+    """Train several independent tasks at once (config C4, the mixed batch):
+    ``jobs`` = [(graph, topo, TrainerConfig), ...], each with its own
+    parameters, store, baseline and RNG streams, advanced together on their own
+    CUDA streams (one graph replay per round).  Each result equals
+    ``train(graph, topo, config)`` run alone."""
+    from .graph import coalesce_sole_consumers
+
+    prepared = []
+    for graph, topo, config in jobs:
+        config = config or TrainerConfig()
+        if config.controllers != 1:
+            raise ValueError("train_many: each job runs one controller")
+        gg = graph if hasattr(graph, "groups") else coalesce_sole_consumers(graph)
+        task = _make_task(gg, topo, config)
+        store = ParameterStore(task.template.to_flat(), learning_rate=config.learning_rate,
+                               beta1=config.adam_beta1, beta2=config.adam_beta2, epsilon=config.adam_epsilon,
+                               max_steps=config.total_updates + 1)
+        seq = np.random.SeedSequence(config.seed).spawn(1)[0]
+        prepared.append((task, store, DeviceController(task, store, seq, 0)))
+    ups = {t.config.total_updates for t, _, _ in prepared}
+    if len(ups) == 1:
+        runner = ConcurrentRunner([c for _, _, c in prepared])
+        walls = runner.train(ups.pop())
+        return [_result_of(t, s, [c], walls) for t, s, c in prepared]
+    # different lengths: each job on its own (still device-resident and graph-replayed)
+    out = []
+    for t, s, c in prepared:
+        r = run_controller(0, s, t, None, ctl=c)
+        out.append(_result_of(t, s, [c], [row.wall_ms for row in r.rows]))
+    return out
+
+
 def _make_task(gg, topo, config: TrainerConfig) -> _TrainTask:
     template = policy_template(gg, topo, config)
     feats = GroupFeatures.from_grouped(gg, template.spec)
@@ -510,7 +665,7 @@ def _make_task(gg, topo, config: TrainerConfig) -> _TrainTask:
 
 
 def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, seed_seq,
-                   world=None) -> _ControllerResult:
+                   world=None, ctl=None) -> _ControllerResult:
     """``pkg/trainer.py:256-309`` on the device (CUDA-graph replay after update 0).
 
     ``world=(rank, size, group)`` runs this rank's K-shard (parallel.py); the
@@ -518,7 +673,8 @@ def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, 
     import torch
 
     cfg = task.config
-    ctl = DeviceController(task, store, seed_seq, controller_id, world=world)
+    if ctl is None:
+        ctl = DeviceController(task, store, seed_seq, controller_id, world=world)
     use_graph = ctl.size == 1
     walls = []
     if cfg.total_updates > 0:
@@ -545,15 +701,20 @@ def train(graph, topo, config: TrainerConfig | None = None, *, group=None) -> Tr
 
     config = config or TrainerConfig()
     gg = graph if hasattr(graph, "groups") else coalesce_sole_consumers(graph)
-    if config.controllers != 1:
-        raise NotImplementedError("asynchronous multi-controller training is SURVEY.md §8(f) row f1 "
-                                  "(not yet on the device path)")
     task = _make_task(gg, topo, config)
+    C = config.controllers
     store = ParameterStore(task.template.to_flat(), learning_rate=config.learning_rate, beta1=config.adam_beta1,
                            beta2=config.adam_beta2, epsilon=config.adam_epsilon,
-                           max_steps=config.total_updates + 1)
+                           max_steps=config.total_updates * C + 1)
     root = np.random.SeedSequence(config.seed)
-    seqs = root.spawn(config.controllers)
+    seqs = root.spawn(C)
+    if C > 1:
+        # f1: C controllers over one device-resident store (ConcurrentRunner)
+        if group is not None:
+            raise NotImplementedError("multi-controller training with K sharded over ranks")
+        ctls = [DeviceController(task, store, seqs[c], c, shared=True) for c in range(C)]
+        walls = ConcurrentRunner(ctls, store).train(config.total_updates)
+        return _result_of(task, store, ctls, walls)
     world = None
     if group is not None:
         import torch.distributed as dist

@@ -97,3 +97,12 @@ def test_trainer_oracle_with_measurement_noise_matches_reference(name, graph):
     assert np.array_equal(np.array(out["placements"], np.uint8), g["placements"])
     np.testing.assert_allclose(out["final"], g["final_params"], rtol=1e-12, atol=1e-15)
     assert out["versions"] == int(g["store_versions"])
+
+
+def test_trainer_oracle_round_schedule_single_controller_is_run():
+    """run_multi (the f1 round schedule) with one controller == the pinned run()."""
+    gg, topo, _, _ = cfg("C1")
+    g = train_golden("C1")
+    out = otr.run_multi(gg, topo, g["cfg"])
+    assert otr.csv_of(out["rows"]) == g["csv"]
+    np.testing.assert_allclose(out["final"], g["final_params"], rtol=1e-12, atol=1e-15)
