@@ -40,6 +40,8 @@ CFG_DESC = {
           "(rate 10, 65536 B/s links)",
     "C3tight": "C3 graph, 30 MiB per simulated GPU (memory-tight)",
     "C5": "random DAG 20k ops -> 2000 groups, 5969 group edges, cpu+7gpu",
+    "C4": "mixed batch: C1 (rnnlm, 100 groups, cpu+1gpu) + C2 (nmt, 243 groups, cpu+4gpu) as two independent "
+          "tasks (own parameters, stores, RNG), K=512 each per GPU, one CUDA-graph replay per round",
 }
 
 
@@ -166,18 +168,21 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    gg, topo, K = load_config(args.config)
+    names = ["C1", "C2"] if args.config == "C4" else [args.config]
     workers = len(os.sched_getaffinity(0))
     k_sample = args.cpu_sample or 2 * workers
     from oracle.trainer import cpu_step_rate
 
-    for _ in range(max(0, args.warmup)):
-        cpu_step_rate(gg, topo, max(1, workers), workers=workers)
-    tot_p, tot_s = 0, 0.0
-    for _ in range(args.steps):
-        r = cpu_step_rate(gg, topo, k_sample, workers=workers)
-        tot_p += r["placements"]
-        tot_s += r["seconds"]
+    tot_p, tot_s, K = 0, 0.0, 0
+    for name in names:
+        gg, topo, Kc = load_config(name)
+        K += 512 if args.config == "C4" else Kc
+        for _ in range(max(0, args.warmup)):
+            cpu_step_rate(gg, topo, max(1, workers), workers=workers)
+        for _ in range(args.steps):
+            r = cpu_step_rate(gg, topo, k_sample, workers=workers)
+            tot_p += r["placements"]
+            tot_s += r["seconds"]
     value = tot_p / tot_s
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -222,17 +227,28 @@ def main():
     import paper_1706_04972_b200 as dp
     from paper_1706_04972_b200 import _native as nat
 
-    gg, topo, K_cfg = load_config(args.config)
-    k_gpu = args.k_per_gpu or K_cfg
-    K = k_gpu * world
+    # C4 = the mixed batch: the C1 and C2 tasks (own parameters, stores, RNG
+    # streams) advanced together, K=512 each
+    names = ["C1", "C2"] if args.config == "C4" else [args.config]
     total_updates = args.warmup + 2 * args.steps + args.profile_phases + 8
-    cfg = dp.TrainerConfig(k=K, total_updates=total_updates, seed=0)
-    task = dp.trainer._make_task(gg, topo, cfg)
-    store = dp.ParameterStore(task.template.to_flat(), max_steps=total_updates + 1)
-    seq = np.random.SeedSequence(cfg.seed).spawn(1)[0]
-    ctl = dp.trainer.DeviceController(task, store, seq, 0, world=(rank, world, group))
+    ctls, stores, K = [], [], 0
+    for name in names:
+        gg, topo, K_cfg = load_config(name)
+        k_gpu = args.k_per_gpu or (512 if args.config == "C4" else K_cfg)
+        cfg = dp.TrainerConfig(k=k_gpu * world, total_updates=total_updates, seed=0)
+        task = dp.trainer._make_task(gg, topo, cfg)
+        store = dp.ParameterStore(task.template.to_flat(), max_steps=total_updates + 1)
+        seq = np.random.SeedSequence(cfg.seed).spawn(1)[0]
+        ctls.append(dp.trainer.DeviceController(task, store, seq, 0, world=(rank, world, group)))
+        stores.append(store)
+        K += cfg.k
+    ctl, store = ctls[0], stores[0]
+    # several tasks: one stream each (one graph replay per round); under
+    # torch.distributed they run back to back so every rank issues the same
+    # collective order
+    runner = ctl if len(ctls) == 1 else dp.trainer.ConcurrentRunner(ctls, concurrent=world == 1)
     stream = torch.cuda.current_stream()
-    T = len(task.feats)
+    T = ctl.T
 
     def barrier():
         if world > 1:
@@ -246,18 +262,18 @@ def main():
 
     # ---- warm-up (first step eager: counts our launches; then graph capture) ----
     l0 = nat.lib().dp_launch_count()
-    ctl.step()
+    runner.step()
     torch.cuda.synchronize()
     launches_per_step = nat.lib().dp_launch_count() - l0
     use_graph = (world == 1) and not args.no_graph
     if use_graph:
-        ctl.capture()
+        runner.capture()
 
     def one():
         if use_graph:
-            ctl._graph.replay()
+            runner._graph.replay()
         else:
-            ctl.step()
+            runner.step()
 
     for _ in range(max(0, args.warmup - 1)):
         one()
@@ -283,11 +299,12 @@ def main():
         tot_ms = max_over_ranks(tot_ms)
     ms_per_step = tot_ms / args.steps
     value = K * args.steps / (tot_ms * 1e-3)
-    ctl.check_errors()
+    for c in ctls:
+        c.check_errors()
 
     # ---- phase profile (eager, events at phase boundaries) ----
     phases = {}
-    if args.profile_phases > 0:
+    if args.profile_phases > 0 and len(ctls) == 1:
         marks = []
 
         def mark(name):
@@ -305,26 +322,31 @@ def main():
         phases = {k: statistics.mean(v) for k, v in phases.items()}
 
     # ---- e2e through the public API with host buffers ----
-    P = store.params.numel()
-    h_params = torch.empty(P, dtype=torch.float64, pin_memory=True)
-    h_params.copy_(store.params.cpu())
-    h_out = torch.empty(P, dtype=torch.float64, pin_memory=True)
-    h_log = torch.empty(8, dtype=torch.float64, pin_memory=True)
-    h_pl = torch.empty(ctl.K_local, T, dtype=torch.uint8, pin_memory=True)
+    hp = [torch.empty(st.params.numel(), dtype=torch.float64, pin_memory=True) for st in stores]
+    for h, st in zip(hp, stores):
+        h.copy_(st.params.cpu())
+    ho = [torch.empty_like(h, pin_memory=True) for h in hp]
+    hl = [torch.empty(8, dtype=torch.float64, pin_memory=True) for _ in ctls]
+    hpl = [torch.empty(c.K_local, c.T, dtype=torch.uint8, pin_memory=True) for c in ctls]
+    h2d = sum(h.numel() * 8 for h in hp)
+    d2h = h2d + sum(c.K_local * c.T + 64 for c in ctls)
     e2e_ms = []
     for i in range(args.steps):
         flush.fill_(1.0)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        store.params.copy_(h_params, non_blocking=True)
+        for h, st in zip(hp, stores):
+            st.params.copy_(h, non_blocking=True)
         one()
-        h_out.copy_(store.params, non_blocking=True)
-        h_pl.copy_(ctl.choice, non_blocking=True)
-        h_log.copy_(ctl.log[:8], non_blocking=True)
+        for j, c in enumerate(ctls):
+            ho[j].copy_(stores[j].params, non_blocking=True)
+            hpl[j].copy_(c.choice, non_blocking=True)
+            hl[j].copy_(c.log[:8], non_blocking=True)
         e.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(s.elapsed_time(e))
-        h_params.copy_(h_out)
+        for h, o in zip(hp, ho):
+            h.copy_(o)
     e2e_tot = sum(e2e_ms)
     if world > 1:
         e2e_tot = max_over_ranks(e2e_tot)
@@ -336,11 +358,12 @@ def main():
         return
 
     # ---- roofline of the dominant kernel ----
-    D = topo.num_devices
     peak64 = fp64_peak_tflops(nat, torch)
     dom = max(phases, key=phases.get) if phases else "decode"
+    # C4 has no per-phase profile: its decoders are timed as the whole round
     dec_ms = phases.get("decode", ms_per_step)
-    dec_flops = decoder_flops_per_placement(T, D) * ctl.K_local
+    dec_flops = sum(decoder_flops_per_placement(c.T, c.task.topo.num_devices) * c.K_local for c in ctls)
+    pol_flops = sum(policy_flops_per_placement(c.T, c.task.topo.num_devices, c.K) * c.K_local for c in ctls)
     achieved = dec_flops / (dec_ms * 1e-3) / 1e12
     roofline = {
         "kernel": "dec_kernel (dp_policy_decode)", "bound": "fp64", "achieved": achieved, "peak": peak64,
@@ -349,12 +372,19 @@ def main():
                        "has no fp64 figure (bf16 tensor peak is not the denominator of an fp64 kernel)",
         "algorithmic_flops_per_launch": dec_flops, "avg_launch_ms": dec_ms,
         "dominant_phase": dom, "phase_ms": phases,
-        "policy_flops_per_step": policy_flops_per_placement(T, D, K) * ctl.K_local,
+        "policy_flops_per_step": pol_flops,
     }
     cpu = None
     if world == 1 and not args.skip_cpu:
         try:
-            cpu = cpu_baseline(gg, topo, args.cpu_sample, name=args.config)
+            if len(ctls) == 1:
+                cpu = cpu_baseline(ctl.task.gg, ctl.task.topo, args.cpu_sample, name=args.config)
+            else:
+                # mixed batch: per-task CPU rates combined over the same K mix
+                parts = [cpu_baseline(c.task.gg, c.task.topo, args.cpu_sample, name=n) for c, n in zip(ctls, names)]
+                ks = [c.K for c in ctls]
+                cpu = dict(parts[0], value=sum(ks) / sum(k / p["value"] for k, p in zip(ks, parts)),
+                           sample=" + ".join(p["sample"] for p in parts) + "; combined over the K mix")
         except Exception as ex:  # pragma: no cover
             cpu = {"error": repr(ex)}
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -364,12 +394,13 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config}: {CFG_DESC[args.config]}",
-                   "k_per_gpu": k_gpu, "global_k": K, "decoder_len": T, "parallelism": f"dp{world} (K sharded)",
+                   "k_per_gpu": k_gpu, "global_k": K, "decoder_len": [c.T for c in ctls] if len(ctls) > 1 else T,
+                   "parallelism": f"dp{world} (K sharded)",
                    "l2": "flushed between timed steps (256 MiB write)",
                    "cuda_graph": use_graph},
         "steps_per_sec": 1e3 / ms_per_step,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": P * 8,
-                "d2h_bytes_per_step": P * 8 + ctl.K_local * T + 64,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
                 "note": "params H2D from pinned host -> full update -> params, placements, log row D2H"},
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step,

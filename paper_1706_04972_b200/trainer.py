@@ -532,11 +532,15 @@ class ConcurrentRunner:
     * independent stores (C4 mixed batch, ``train_many``): each controller's
       whole update, Adam included, runs on its own stream."""
 
-    def __init__(self, ctls, shared_store: ParameterStore | None = None):
+    def __init__(self, ctls, shared_store: ParameterStore | None = None, concurrent: bool = True):
+        """``concurrent=False`` enqueues the controllers one after another on
+        the launching stream (required when their steps issue collectives on
+        one communicator: every rank must see the same collective order)."""
         import torch
 
         self.ctls, self.store = list(ctls), shared_store
-        self.streams = [torch.cuda.Stream(device=c.device) for c in self.ctls]
+        self.concurrent = concurrent
+        self.streams = [torch.cuda.Stream(device=c.device) for c in self.ctls] if concurrent else None
         self._graph = None
 
     def step(self):
@@ -546,6 +550,13 @@ class ConcurrentRunner:
         if self.store is not None:
             for c in self.ctls:
                 c.params_src.copy_(self.store.params)
+        if not self.concurrent:
+            for c in self.ctls:
+                c.step(stream=main, apply=self.store is None)
+            if self.store is not None:
+                for c in self.ctls:
+                    c.apply(main)
+            return
         for c, s in zip(self.ctls, self.streams):
             s.wait_stream(main)
             with torch.cuda.stream(s):
