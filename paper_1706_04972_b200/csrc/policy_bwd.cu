@@ -228,6 +228,172 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     }
 }
 
+// ------------------------------------------------------------------ B0g / B1fg
+// Advantage-weighted halves of B0 and B1f in the split backward.  With
+// dz0 = onehot(choice) - p and du0 = dev_table[:D]^T dz0 (row_du, unscaled):
+//   b_out      += sum_r adv_r dz0[r]
+//   dev_table  += sum_r adv_r dz0[r] (x) u[r]
+//   w_out[:64] += sum_r adv_r h[r] (x) du0[r]          (out_grads_kernel)
+//   w_att      += sum_r adv_r h[r] (x) dq[r]           (watt_grad_kernel)
+// Rows are split evenly over 2 x SMs CTAs; operands stream from L2 with no
+// staging (many resident CTAs hide the latency); partials use row_prep's /
+// row_fin's layouts and the same ordered reductions.
+// CTA = a range of (sample k, slice of its T steps) units: the advantage is
+// one scalar per unit; rows are staged through shared memory in 32-row tiles
+// (coalesced loads, one latency per tile), then reduced from shared memory.
+constexpr int kGT = 32;  // rows per staged tile
+
+struct OutGradSmem {
+    double h[kGT][kH];
+    double du[kGT][kMaxDD];
+    double u[kGT][kMaxDD];
+    double dz[kGT][kMaxD];
+};
+
+__global__ void __launch_bounds__(kThreads) out_grads_kernel(PolicyDims dm, int parts, int n_units, int units_per_cta,
+                                                             const double *__restrict__ adv,
+                                                             const double *__restrict__ act_p,
+                                                             const uint8_t *__restrict__ choice,
+                                                             const double *__restrict__ act_u,
+                                                             const double *__restrict__ act_h,
+                                                             const double *__restrict__ row_du,
+                                                             double *__restrict__ partial) {
+    __shared__ OutGradSmem S;
+    const int tid = threadIdx.x;
+    const int T = dm.T, D = dm.D, dd = dm.dd;
+    const int tp = (T + parts - 1) / parts;
+    const int gi = tid >> 2, go = tid & 3;  // w_out rows i = gi, cols o = go + 4x
+    double tw[kMaxDD / 4], tdev[4] = {0.0, 0.0, 0.0, 0.0}, tb = 0.0;  // advantage-weighted totals
+#pragma unroll
+    for (int x = 0; x < kMaxDD / 4; x++) tw[x] = 0.0;
+    const int u0 = blockIdx.x * units_per_cta, u1 = min(n_units, u0 + units_per_cta);
+    for (int un = u0; un < u1; un++) {
+        const int k = un / parts, part = un - k * parts;
+        const int r0 = k * T + part * tp, r1 = k * T + min(T, (part + 1) * tp);
+        const double w = adv[k];
+        double gw[kMaxDD / 4], gdev[4] = {0.0, 0.0, 0.0, 0.0}, gb = 0.0;
+#pragma unroll
+        for (int x = 0; x < kMaxDD / 4; x++) gw[x] = 0.0;
+        for (int rb = r0; rb < r1; rb += kGT) {
+            const int nr = min(kGT, r1 - rb);
+            __syncthreads();
+            for (int x = tid; x < kGT * kH; x += kThreads) {
+                const int r = x >> 6, i = x & 63;
+                S.h[r][i] = r < nr ? act_h[(size_t)(rb + r) * kH + i] : 0.0;
+            }
+            for (int x = tid; x < kGT * dd; x += kThreads) {
+                const int r = x / dd, o = x - r * dd;
+                const bool ok = r < nr;
+                S.du[r][o] = ok ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
+                S.u[r][o] = ok ? act_u[(size_t)(rb + r) * dd + o] : 0.0;
+            }
+            for (int x = tid; x < kGT * D; x += kThreads) {
+                const int r = x / D, d = x - r * D;
+                S.dz[r][d] = r < nr ? (d == choice[rb + r] ? 1.0 : 0.0) - act_p[(size_t)(rb + r) * D + d] : 0.0;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int r = 0; r < kGT; r++) {
+                const double hv = S.h[r][gi];
+#pragma unroll
+                for (int x = 0; x < kMaxDD / 4; x++) {
+                    const int o = go + 4 * x;
+                    if (o < dd) gw[x] = fma(hv, S.du[r][o], gw[x]);
+                }
+            }
+#pragma unroll
+            for (int y = 0; y < 4; y++) {
+                const int e = tid + kThreads * y;
+                if (e < D * dd) {
+                    const int d = e / dd, o = e - d * dd;
+                    double v = gdev[y];
+                    for (int r = 0; r < kGT; r++) v = fma(S.dz[r][d], S.u[r][o], v);
+                    gdev[y] = v;
+                }
+            }
+            if (tid < D)
+                for (int r = 0; r < kGT; r++) gb += S.dz[r][tid];
+        }
+        tb = fma(w, gb, tb);
+#pragma unroll
+        for (int y = 0; y < 4; y++) tdev[y] = fma(w, gdev[y], tdev[y]);
+#pragma unroll
+        for (int x = 0; x < kMaxDD / 4; x++) tw[x] = fma(w, gw[x], tw[x]);
+    }
+    const size_t na = (size_t)D + D * dd + 2 * kH * dd;
+    double *out = partial + (size_t)blockIdx.x * na;
+    if (tid < D) out[tid] = tb;
+#pragma unroll
+    for (int y = 0; y < 4; y++) {
+        const int e = tid + kThreads * y;
+        if (e < D * dd) out[D + e] = tdev[y];
+    }
+#pragma unroll
+    for (int x = 0; x < kMaxDD / 4; x++) {
+        const int o = go + 4 * x;
+        if (o < dd) out[D + D * dd + gi * dd + o] = tw[x];
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) watt_grad_kernel(int T, int parts, int n_units, int units_per_cta,
+                                                             const double *__restrict__ adv,
+                                                             const double *__restrict__ act_h,
+                                                             const double *__restrict__ row_dq,
+                                                             double *__restrict__ partial) {
+    __shared__ double sh[kGT][kH], sq[kGT][kH];
+    const int tid = threadIdx.x;
+    const int a = tid >> 4, b = tid & 15;  // l in {a + 16i}, j in {b + 16jj}
+    const int tp = (T + parts - 1) / parts;
+    double tot[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) tot[i][jj] = 0.0;
+    const int u0 = blockIdx.x * units_per_cta, u1 = min(n_units, u0 + units_per_cta);
+    for (int un = u0; un < u1; un++) {
+        const int k = un / parts, part = un - k * parts;
+        const int r0 = k * T + part * tp, r1 = k * T + min(T, (part + 1) * tp);
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) acc[i][jj] = 0.0;
+        for (int rb = r0; rb < r1; rb += kGT) {
+            const int nr = min(kGT, r1 - rb);
+            __syncthreads();
+            for (int x = tid; x < kGT * kH; x += kThreads) {
+                const int r = x >> 6, i = x & 63;
+                const bool ok = r < nr;
+                sh[r][i] = ok ? act_h[(size_t)(rb + r) * kH + i] : 0.0;
+                sq[r][i] = ok ? row_dq[(size_t)(rb + r) * kH + i] : 0.0;
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int r = 0; r < kGT; r++) {
+                double hv[4], qv[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) hv[i] = sh[r][a + 16 * i];
+#pragma unroll
+                for (int jj = 0; jj < 4; jj++) qv[jj] = sq[r][b + 16 * jj];
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int jj = 0; jj < 4; jj++) acc[i][jj] = fma(hv[i], qv[jj], acc[i][jj]);
+            }
+        }
+        const double w = adv[k];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) tot[i][jj] = fma(w, acc[i][jj], tot[i][jj]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++)
+            partial[(size_t)blockIdx.x * kH * kH + (a + 16 * i) * kH + b + 16 * jj] = tot[i][jj];
+}
+
 // ------------------------------------------------------------------ B1
 constexpr int kAttTile = 64;  // rows per tile in att_bwd (2 rows per thread in the S/DA and dq passes)
 
@@ -260,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     double *__restrict__ partial, double *__restrict__ partA,
     double *__restrict__ tile_partial /* [n_tiles][T][64] or NULL */,
     double *__restrict__ tile_partA /* [n_tiles][T][dd] */, const double *__restrict__ act_e,
-    const double *__restrict__ act_esc, int do_denc) {
+    const double *__restrict__ act_esc, int do_denc, int per_sample /* partials per sample, not per tile */) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
     const int tid = threadIdx.x;
@@ -442,12 +608,27 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 if (i >= T) continue;
                 if (tile_partial) {
                     // rows-only pass: this tile's (unscaled) contribution, weighted by
-                    // its sample's advantage later (weighted_reduce)
+                    // its sample's advantage later (weighted_reduce).  per_sample: the
+                    // CTA owns whole samples, so it sums its tiles per sample in place
+                    // (same thread, same elements: no hazard) and the reduce reads 1/tps
+                    // Later tiles add with fire-and-forget reductions (RED, no
+                    // round trip); one thread owns each element, and its operations
+                    // on one address stay in program order: deterministic sums
+                    const size_t unit = per_sample ? (size_t)(tl / tps) : (size_t)tl;
+                    const bool first = !per_sample || tl % tps == 0;
 #pragma unroll
-                    for (int bb = 0; bb < 4; bb++) tile_partial[((size_t)tl * T + i) * kH + ej + 16 * bb] = dE[a][bb];
+                    for (int bb = 0; bb < 4; bb++) {
+                        double *d = tile_partial + (unit * T + i) * kH + ej + 16 * bb;
+                        if (first) *d = dE[a][bb];
+                        else atomicAdd(d, dE[a][bb]);
+                    }
 #pragma unroll
                     for (int bb = 0; bb < 2; bb++)
-                        if (ej + 16 * bb < dd) tile_partA[((size_t)tl * T + i) * dd + ej + 16 * bb] = dA[a][bb];
+                        if (ej + 16 * bb < dd) {
+                            double *d = tile_partA + (unit * T + i) * dd + ej + 16 * bb;
+                            if (first) *d = dA[a][bb];
+                            else atomicAdd(d, dA[a][bb]);
+                        }
                 } else {
                     // fused pass: the CTA's private partial (first tile initialises it)
 #pragma unroll
@@ -957,60 +1138,101 @@ __global__ void __launch_bounds__(512) sum_rows_kernel(const double *__restrict_
 }
 
 // B5: w_enc / b_enc grads (contraction over T) and the type-embedding scatter.
-__global__ void enc_wgrad_kernel(PolicyDims dm, const double *__restrict__ X, const double *__restrict__ enc_h,
-                                 const double *__restrict__ da_enc, double *__restrict__ grad) {
-    const int j = threadIdx.x;   // gate column
-    const int r = blockIdx.x;    // row of w_enc (0..F+H-1), or F+H for b_enc
-    const int T = dm.T, F = dm.F;
-    double v0 = 0.0, v1 = 0.0;
-    if (r == F + kH) {
-        int t = 0;
-        for (; t + 2 <= T; t += 2) {
-            v0 += da_enc[(size_t)t * kG + j];
-            v1 += da_enc[(size_t)(t + 1) * kG + j];
+// enc_wgrad: block = 4 rows r of [X | h_prev] (or b_enc) x 256 gate columns;
+// the 4 input rows are staged in shared memory, da_enc streams from L2.
+constexpr int kWgRows = 4;
+__global__ void __launch_bounds__(kG) enc_wgrad_kernel(PolicyDims dm, const double *__restrict__ X,
+                                                       const double *__restrict__ enc_h,
+                                                       const double *__restrict__ da_enc, double *__restrict__ grad) {
+    extern __shared__ double xs[];  // [kWgRows][T]
+    const int j = threadIdx.x;
+    const int T = dm.T, F = dm.F, R = F + kH + 1;
+    const int r0 = blockIdx.x * kWgRows;
+    for (int x = j; x < kWgRows * T; x += kG) {
+        const int a = x / T, t = x - a * T, r = r0 + a;
+        double v = 0.0;
+        if (r < F) v = X[(size_t)t * F + r];
+        else if (r < F + kH) v = t > 0 ? enc_h[(size_t)(t - 1) * kH + (r - F)] : 0.0;
+        else if (r == F + kH) v = 1.0;  // b_enc row
+        xs[x] = v;
+    }
+    __syncthreads();
+    double acc[kWgRows][2];
+#pragma unroll
+    for (int a = 0; a < kWgRows; a++) acc[a][0] = acc[a][1] = 0.0;
+    int t = 0;
+#pragma unroll 4
+    for (; t + 2 <= T; t += 2) {
+        const double d0 = da_enc[(size_t)t * kG + j], d1 = da_enc[(size_t)(t + 1) * kG + j];
+#pragma unroll
+        for (int a = 0; a < kWgRows; a++) {
+            acc[a][0] = fma(xs[a * T + t], d0, acc[a][0]);
+            acc[a][1] = fma(xs[a * T + t + 1], d1, acc[a][1]);
         }
-        if (t < T) v0 += da_enc[(size_t)t * kG + j];
-        grad[dm.off.b_enc + j] = v0 + v1;
-        return;
     }
-    for (int t = 0; t < T; t++) {
-        double x;
-        if (r < F) x = X[(size_t)t * F + r];
-        else x = t > 0 ? enc_h[(size_t)(t - 1) * kH + (r - F)] : 0.0;
-        if (t & 1) v1 = fma(x, da_enc[(size_t)t * kG + j], v1);
-        else v0 = fma(x, da_enc[(size_t)t * kG + j], v0);
+    if (t < T) {
+        const double d0 = da_enc[(size_t)t * kG + j];
+#pragma unroll
+        for (int a = 0; a < kWgRows; a++) acc[a][0] = fma(xs[a * T + t], d0, acc[a][0]);
     }
-    grad[dm.off.w_enc + (size_t)r * kG + j] = v0 + v1;
+#pragma unroll
+    for (int a = 0; a < kWgRows; a++) {
+        const int r = r0 + a;
+        if (r < F + kH) grad[dm.off.w_enc + (size_t)r * kG + j] = acc[a][0] + acc[a][1];
+        else if (r == F + kH) grad[dm.off.b_enc + j] = acc[a][0] + acc[a][1];
+    }
+    (void)R;
 }
 
-// dx_t[f] = W_enc[f, :] . da_enc[t]   (f < type_dim)
-__global__ void enc_dx_kernel(PolicyDims dm, const double *__restrict__ P, const double *__restrict__ da_enc,
-                              double *__restrict__ dx) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= dm.T * dm.td) return;
-    const int t = idx / dm.td, f = idx % dm.td;
-    double v0 = 0.0, v1 = 0.0;
-    for (int j = 0; j < kG; j += 2) {
-        v0 = fma(P[dm.off.w_enc + (size_t)f * kG + j], da_enc[(size_t)t * kG + j], v0);
-        v1 = fma(P[dm.off.w_enc + (size_t)f * kG + j + 1], da_enc[(size_t)t * kG + j + 1], v1);
+// dx_t[f] = W_enc[f, :] . da_enc[t]   (f < type_dim): block per t, block reduction over the 256 gates
+__global__ void __launch_bounds__(kG) enc_dx_kernel(PolicyDims dm, const double *__restrict__ P,
+                                                    const double *__restrict__ da_enc, double *__restrict__ dx) {
+    __shared__ double part[kG / 32][32];
+    const int t = blockIdx.x, j = threadIdx.x, lane = j & 31, w = j >> 5;
+    const double d = da_enc[(size_t)t * kG + j];
+    for (int f0 = 0; f0 < dm.td; f0 += 32) {
+        // each warp reduces its 32 gates for up to 32 f values (f on lanes after the transpose)
+        double mine = 0.0;
+        for (int q = 0; q < 32 && f0 + q < dm.td; q++) {
+            double v = P[dm.off.w_enc + (size_t)(f0 + q) * kG + j] * d;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == q) mine = v;
+        }
+        part[w][lane] = mine;
+        __syncthreads();
+        if (w == 0 && f0 + lane < dm.td) {
+            double v = part[0][lane];
+#pragma unroll
+            for (int q = 1; q < kG / 32; q++) v += part[q][lane];
+            dx[(size_t)t * dm.td + f0 + lane] = v;
+        }
+        __syncthreads();
     }
-    dx[idx] = v0 + v1;
 }
 
 // np.add.at(type_table, idx_t, dx_t / len(idx_t)) in (t, position) order
-// (pkg/policy.py:405-407): thread (v, f) walks its occurrence list.
+// (pkg/policy.py:405-407).  Pass 1 (parallel): every occurrence's term
+// dx[t][f] / len(idx_t) into occ_val; pass 2: thread (v, f) adds its terms in
+// occurrence order (contiguous, pipelined loads) — the reference's order.
+__global__ void type_terms_kernel(PolicyDims dm, int n_occ, const int32_t *__restrict__ occ_t,
+                                  const int32_t *__restrict__ type_off, const double *__restrict__ dx,
+                                  double *__restrict__ occ_val) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n_occ * dm.td) return;
+    const int o = idx / dm.td, f = idx - o * dm.td;
+    const int t = occ_t[o];
+    occ_val[idx] = dx[(size_t)t * dm.td + f] / (double)(type_off[t + 1] - type_off[t]);
+}
+
 __global__ void type_scatter_kernel(PolicyDims dm, const int32_t *__restrict__ occ_off,
-                                    const int32_t *__restrict__ occ_t, const int32_t *__restrict__ type_off,
-                                    const double *__restrict__ dx, double *__restrict__ grad) {
+                                    const double *__restrict__ occ_val, double *__restrict__ grad) {
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= dm.V1 * dm.td) return;
     const int v = idx / dm.td, f = idx % dm.td;
     double s = 0.0;
-    for (int o = occ_off[v]; o < occ_off[v + 1]; o++) {
-        const int t = occ_t[o];
-        const double len = (double)(type_off[t + 1] - type_off[t]);
-        s = s + dx[(size_t)t * dm.td + f] / len;
-    }
+#pragma unroll 8
+    for (int o = occ_off[v]; o < occ_off[v + 1]; o++) s = s + occ_val[(size_t)o * dm.td + f];
     grad[dm.off.type_table + idx] = s;
 }
 
@@ -1054,27 +1276,35 @@ Grid att_grid(int K, int T) {
     // one wave: att_bwd holds ~220 KB of shared memory (1 CTA per SM).  It
     // leaves kSimSMs SMs free: in the split backward it runs concurrently with
     // the placement simulator (small latency-bound CTAs that cannot co-reside
-    // with an att_bwd CTA)
+    // with an att_bwd CTA).  When a CTA gets at least one whole sample, its
+    // tile range is rounded to whole samples (per-sample partials).
     constexpr int kSimSMs = 20;
-    const int n_tiles = K * ((T + kAttTile - 1) / kAttTile);
+    const int tps = (T + kAttTile - 1) / kAttTile;
+    const int n_tiles = K * tps;
     const int n = n_tiles < kNumSMs - kSimSMs ? n_tiles : kNumSMs - kSimSMs;
-    const int per = ceil_div(n_tiles, n);
+    int per = ceil_div(n_tiles, n);
+    if (per >= tps) per = ceil_div(per, tps) * tps;
     return {ceil_div(n_tiles, per), per};
 }
 
 int launch_att(dp_policy *p, const Grid &g, size_t smem, int rows, double *tile_part, double *tile_partA,
                cudaStream_t st) {
     const PolicyDims &dm = p->dims;
+    const int tps = (dm.T + kAttTile - 1) / kAttTile;
+    const int per_sample = tile_part && g.per % tps == 0 ? 1 : 0;
+    p->att_per_sample = per_sample;
     if (p->act_e) {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<true>, smem));
         att_bwd_kernel<true><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
                                                                p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
-                                                               p->partA, tile_part, tile_partA, p->act_e, p->act_esc, 1);
+                                                               p->partA, tile_part, tile_partA, p->act_e, p->act_esc, 1,
+                                                               per_sample);
     } else {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<false>, smem));
         att_bwd_kernel<false><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
                                                                 p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
-                                                                p->partA, tile_part, tile_partA, nullptr, nullptr, 1);
+                                                                p->partA, tile_part, tile_partA, nullptr, nullptr, 1,
+                                                                per_sample);
     }
     DP_LAUNCH_CHECK();
     return DP_OK;
@@ -1092,6 +1322,21 @@ int run_att_fin(dp_policy *p, const double *params, double *grad, cudaStream_t s
 int run_b0(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
            cudaStream_t st) {
     const PolicyDims &dm = p->dims;
+    if (mode == kGradsOnly) {
+        const int K = rows / dm.T, parts = K >= 2 * kNumSMs ? 1 : ceil_div(2 * kNumSMs, K);
+        const int n_units = K * parts, upc = ceil_div(n_units, 2 * kNumSMs), used = ceil_div(n_units, upc);
+        out_grads_kernel<<<used, kThreads, 0, st>>>(dm, parts, n_units, upc, adv, p->act_p, p->act_choice, p->act_u,
+                                                    p->act_h, p->row_du, p->partial);
+        DP_LAUNCH_CHECK();
+        const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
+        launch_reduce(p->partial, used, na, dm.D, grad + dm.off.b_out, 0, st);
+        DP_LAUNCH_CHECK();
+        launch_reduce(p->partial + dm.D, used, na, dm.D * dm.dd, grad + dm.off.dev_table, 0, st);
+        DP_LAUNCH_CHECK();
+        launch_reduce(p->partial + dm.D + dm.D * dm.dd, used, na, kH * dm.dd, grad + dm.off.w_out, 0, st);
+        DP_LAUNCH_CHECK();
+        return DP_OK;
+    }
     const Grid g = tiles_grid(rows, kTile);
     const size_t smem = sizeof(PrepSmem);
     DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
@@ -1114,6 +1359,15 @@ int run_b0(dp_policy *p, const double *params, int rows, const double *adv, doub
 int run_b1f(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
             cudaStream_t st) {
     const PolicyDims &dm = p->dims;
+    if (mode == kGradsOnly) {
+        const int K = rows / dm.T, parts = K >= 2 * kNumSMs ? 1 : ceil_div(2 * kNumSMs, K);
+        const int n_units = K * parts, upc = ceil_div(n_units, 2 * kNumSMs), used = ceil_div(n_units, upc);
+        watt_grad_kernel<<<used, kThreads, 0, st>>>(dm.T, parts, n_units, upc, adv, p->act_h, p->row_dq, p->partial);
+        DP_LAUNCH_CHECK();
+        launch_reduce(p->partial, used, kH * kH, kH * kH, grad + dm.off.w_att, 0, st);
+        DP_LAUNCH_CHECK();
+        return DP_OK;
+    }
     const Grid g = tiles_grid(rows, kFinTile);
     const size_t smem = sizeof(FinSmem);
     DP_CUDA_TRY(allow_big_smem((const void *)row_fin_kernel, smem));
@@ -1171,12 +1425,18 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
                                                    p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
                                                    dhc_sum + 2 * kH, dhc_sum + 3 * kH);
         DP_LAUNCH_CHECK();
-        enc_wgrad_kernel<<<dm.F + kH + 1, kG, 0, ss>>>(dm, p->X, p->enc_h, p->da_enc, grad);
+        {
+            const size_t xs = sizeof(double) * kWgRows * T;
+            DP_CUDA_TRY(allow_big_smem((const void *)enc_wgrad_kernel, xs));
+            enc_wgrad_kernel<<<ceil_div(dm.F + kH + 1, kWgRows), kG, xs, ss>>>(dm, p->X, p->enc_h, p->da_enc, grad);
+        }
         DP_LAUNCH_CHECK();
-        enc_dx_kernel<<<ceil_div(T * dm.td, 256), 256, 0, ss>>>(dm, params, p->da_enc, dx_scratch);
+        enc_dx_kernel<<<T, kG, 0, ss>>>(dm, params, p->da_enc, dx_scratch);
         DP_LAUNCH_CHECK();
-        type_scatter_kernel<<<ceil_div(dm.V1 * dm.td, 128), 128, 0, ss>>>(dm, p->occ_off, p->occ_t, p->type_off,
-                                                                         dx_scratch, grad);
+        type_terms_kernel<<<ceil_div(p->n_occ * dm.td, 256), 256, 0, ss>>>(dm, p->n_occ, p->occ_t, p->type_off, dx_scratch,
+                                                                          p->occ_val);
+        DP_LAUNCH_CHECK();
+        type_scatter_kernel<<<ceil_div(dm.V1 * dm.td, 128), 128, 0, ss>>>(dm, p->occ_off, p->occ_val, grad);
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaEventRecord(p->ev_join, ss));
     }
@@ -1272,7 +1532,8 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
     DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
     DP_TRY(run_b0(p, params, rows, adv, grad, kGradsOnly, st));
     {
-        const int tps = (T + kAttTile - 1) / kAttTile;
+        // per-sample partials (1 unit per sample) or per-tile (tps units per sample)
+        const int tps = p->att_per_sample ? 1 : (T + kAttTile - 1) / kAttTile;
         weighted_reduce_kernel<<<ceil_div(T * kH, 32), 256, 0, st>>>(p->tile_part, K * tps, (size_t)T * kH, T * kH,
                                                                      p->d_enc, adv, tps);
         DP_LAUNCH_CHECK();

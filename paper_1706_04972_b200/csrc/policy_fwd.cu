@@ -804,7 +804,7 @@ static ParamLayout layout_of(int V1, int D, int dd, int F, int td) {
 
 extern "C" void dp_policy_destroy(dp_policy *p) {
     if (!p) return;
-    void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
+    void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->occ_val, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
                     p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->proj_nmax, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
@@ -879,6 +879,8 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
             for (int i = h_type_off[t]; i < h_type_off[t + 1]; i++) occ_t[fill[h_type_idx[i]]++] = t;
         upload((void **)&p->occ_off, occ_off.data(), sizeof(int32_t) * (vocab_rows + 1));
         upload((void **)&p->occ_t, occ_t.data(), sizeof(int32_t) * n_idx);
+        p->n_occ = n_idx;
+        alloc((void **)&p->occ_val, sizeof(double) * (size_t)n_idx * type_dim);
         std::vector<double> z(kH, 0.0);
         upload((void **)&p->zeros, z.data(), sizeof(double) * kH);
     }

@@ -21,3 +21,7 @@ for n, v in step:
 print(f"step total {tot:.1f} us over {len(step)} launches")
 for n, v in sorted(agg.items(), key=lambda x: -x[1]):
     print(f"{v:10.1f} us  {100 * v / tot:5.1f}%  {n}")
+if len(sys.argv) > 2 and sys.argv[2] == "seq":
+    print("\nlaunch order:")
+    for n, v in step:
+        print(f"{v:10.1f} us  {n}")
