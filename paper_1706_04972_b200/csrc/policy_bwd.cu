@@ -56,17 +56,29 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// ------------------------------------------------------------------ fp64 tensor core
+// mma.sync m8n8k4 f64 (DMMA): D[8x8] += A[8x4] B[4x8], one warp.  Fragments
+// (lane = 4 g + t): a = A[g][t], b = B[t][g], c/d = {C[g][2t], C[g][2t+1]}.
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
 // ------------------------------------------------------------------ B0
 // partial per CTA: [b_out (D) | dev_table[:D] (D*dd) | w_out (128*dd)]
+// Operand tiles of the DMMA products use row strides == 8 (mod 32) words
+// (68 / 132 / 36 doubles): the 4 k-rows x 8 lanes of a fragment load hit each
+// bank pair at most twice (2 wavefronts for 256 bytes, the minimum).
+constexpr int kPadH = 68, kWoLd = 2 * kH + 4, kDuLd = kMaxDD + 4;
 struct PrepSmem {
-    double watt[kH * kPad];        // W_att[l][j]
-    double woutT[kMaxDD * 2 * kH]; // W_out^T [o][i]
-    double devt[kMaxD * kMaxDD];   // dev_table[:D] [d][o]
-    double h[kTile * kPad];        // [r][l]
+    double watt[kH * kPadH];        // W_att[l][j]
+    double woutT[kMaxDD * kWoLd];   // W_out^T [o][i]  (rows o >= dd zero)
+    double devt[kMaxD * kMaxDD];    // dev_table[:D] [d][o]
+    double h[kTile * kPadH];        // [r][l]
     double uc[kTile * (kMaxDD + 1)];  // ctx @ W_out[64:]
-    double dctx[kTile * kPad];
     double u[kTile * (kMaxDD + 1)];
-    double du[kTile * (kMaxDD + 1)];
+    double du[kTile * kDuLd];       // (cols >= dd zero)
     double dz[kTile * (kMaxD + 1)];
 };
 
@@ -83,10 +95,11 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     const int tid = threadIdx.x;
     const int D = dm.D, dd = dm.dd, T = dm.T;
     const int ddp = dd + 1, Dp = D + 1;
-    for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPad + (x & 63)] = P[dm.off.w_att + x];
-    for (int x = tid; x < 2 * kH * dd; x += kThreads) {
-        const int i = x / dd, o = x % dd;
-        S.woutT[o * 2 * kH + i] = P[dm.off.w_out + x];
+    const int dd4 = (dd + 3) & ~3;  // DMMA k extent of the du @ W_out^T product
+    for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPadH + (x & 63)] = P[dm.off.w_att + x];
+    for (int x = tid; x < 2 * kH * dd4; x += kThreads) {
+        const int i = x / dd4, o = x % dd4;
+        S.woutT[o * kWoLd + i] = o < dd ? P[dm.off.w_out + (size_t)i * dd + o] : 0.0;
     }
     for (int x = tid; x < D * dd; x += kThreads) S.devt[x] = P[dm.off.dev_table + x];
     // owned grad accumulators
@@ -104,7 +117,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
         for (int x = tid; x < kTile * kH; x += kThreads) {
             const int r = x >> 6, j = x & 63, row = rb + r;
             const bool ok = row < rows;
-            S.h[r * kPad + j] = ok ? act_h[(size_t)row * kH + j] : 0.0;
+            S.h[r * kPadH + j] = ok ? act_h[(size_t)row * kH + j] : 0.0;
         }
         for (int x = tid; x < kTile * dd; x += kThreads) {
             const int r = x / dd, o = x % dd, row = rb + r;
@@ -122,56 +135,59 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             S.dz[r * Dp + d] = dz;
         }
         __syncthreads();
-        // du = dev_table[:D]^T dz ; q = W_att^T h (written to global)
-        for (int x = tid; x < kTile * dd; x += kThreads) {
-            const int r = x / dd, o = x % dd;
+        // du = dev_table[:D]^T dz (columns dd..dd4 zero for the DMMA k padding)
+        for (int x = tid; x < kTile * dd4; x += kThreads) {
+            const int r = x / dd4, o = x % dd4;
             double v = 0.0;
-            for (int d = 0; d < D; d++) v = fma(S.devt[d * dd + o], S.dz[r * Dp + d], v);
-            S.du[r * ddp + o] = v;
-            if (rows_out && rb + r < rows) row_du[(size_t)(rb + r) * dd + o] = v;
+            if (o < dd) {
+                for (int d = 0; d < D; d++) v = fma(S.devt[d * dd + o], S.dz[r * Dp + d], v);
+                if (rows_out && rb + r < rows) row_du[(size_t)(rb + r) * dd + o] = v;
+            }
+            S.du[r * kDuLd + o] = v;
         }
         if (rows_out) {
-            const int r = tid >> 3, jb = tid & 7;
-            double q[8];
+            // q = h W_att (== W_att^T h per row) on the fp64 tensor cores:
+            // warp w: rows 8 (w >> 1) .., columns 32 (w & 1) .. (4 n-tiles)
+            const int lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+            const int mt = w >> 1, nb = (w & 1) * 4;
+            double acc[4][2];
 #pragma unroll
-            for (int x = 0; x < 8; x++) q[x] = 0.0;
-            const double *hr = S.h + r * kPad;
+            for (int n = 0; n < 4; n++) acc[n][0] = acc[n][1] = 0.0;
 #pragma unroll 4
-            for (int l = 0; l < kH; l++) {
-                const double hv = hr[l];
+            for (int ks = 0; ks < kH / 4; ks++) {
+                const double a = S.h[(mt * 8 + g) * kPadH + ks * 4 + t];
 #pragma unroll
-                for (int x = 0; x < 8; x++) q[x] = fma(S.watt[l * kPad + jb + 8 * x], hv, q[x]);
+                for (int n = 0; n < 4; n++) dmma884(acc[n], a, S.watt[(ks * 4 + t) * kPadH + (nb + n) * 8 + g]);
             }
-            const int row = rb + r;
-            if (rows_out && row < rows)
+            const int row = rb + mt * 8 + g;
+            if (row < rows)
 #pragma unroll
-                for (int x = 0; x < 8; x++) row_q[(size_t)row * kH + jb + 8 * x] = q[x];
+                for (int n = 0; n < 4; n++)
+                    *reinterpret_cast<double2 *>(row_q + (size_t)row * kH + (nb + n) * 8 + 2 * t) =
+                        make_double2(acc[n][0], acc[n][1]);
         }
         __syncthreads();
-        // dhc = W_out du -> dh_out (i < 64) to global, dctx (i >= 64) to smem + global
+        // dhc = W_out du (DMMA, k = dd4): i < 64 -> dh_out, i >= 64 -> dctx
         if (rows_out) {
-            const int r = tid >> 3, ib = tid & 7;
-            double v[16];
+            const int lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
+            const int mt = w >> 1, nb = (w & 1) * 8;
+            double acc[8][2];
 #pragma unroll
-            for (int x = 0; x < 16; x++) v[x] = 0.0;
-            for (int o = 0; o < dd; o++) {
-                const double dv = S.du[r * ddp + o];
+            for (int n = 0; n < 8; n++) acc[n][0] = acc[n][1] = 0.0;
+            for (int ks = 0; ks < dd4 / 4; ks++) {
+                const double a = S.du[(mt * 8 + g) * kDuLd + ks * 4 + t];
 #pragma unroll
-                for (int x = 0; x < 16; x++) v[x] = fma(S.woutT[o * 2 * kH + ib + 8 * x], dv, v[x]);
+                for (int n = 0; n < 8; n++) dmma884(acc[n], a, S.woutT[(ks * 4 + t) * kWoLd + (nb + n) * 8 + g]);
             }
-            const int row = rb + r;
+            const int row = rb + mt * 8 + g;
+            if (row < rows)
 #pragma unroll
-            for (int x = 0; x < 16; x++) {
-                const int i = ib + 8 * x;
-                if (i < kH) {
-                    if (rows_out && row < rows) row_dhx[(size_t)row * kH + i] = v[x];
-                } else {
-                    S.dctx[r * kPad + i - kH] = v[x];
-                    if (rows_out && row < rows) row_dctx[(size_t)row * kH + i - kH] = v[x];
+                for (int n = 0; n < 8; n++) {
+                    const int i = (nb + n) * 8 + 2 * t;
+                    double *dst = i < kH ? row_dhx + (size_t)row * kH + i : row_dctx + (size_t)row * kH + i - kH;
+                    *reinterpret_cast<double2 *>(dst) = make_double2(acc[n][0], acc[n][1]);
                 }
-            }
         }
-        __syncthreads();
         // w = ctx . dctx == (ctx W_out[64:]) . du = uc . du  (8 lanes per row)
         if (rows_out) {
             const int r = tid >> 3, jb = tid & 7;
@@ -179,8 +195,8 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
 #pragma unroll
             for (int x = 0; x < kMaxDD / 8; x += 2) {
                 const int o0 = jb + 8 * x, o1 = o0 + 8;
-                if (o0 < dd) s0 = fma(S.uc[r * ddp + o0], S.du[r * ddp + o0], s0);
-                if (o1 < dd) s1 = fma(S.uc[r * ddp + o1], S.du[r * ddp + o1], s1);
+                if (o0 < dd) s0 = fma(S.uc[r * ddp + o0], S.du[r * kDuLd + o0], s0);
+                if (o1 < dd) s1 = fma(S.uc[r * ddp + o1], S.du[r * kDuLd + o1], s1);
             }
             double s = s0 + s1;
             s += __shfl_xor_sync(0xffffffffu, s, 1);
@@ -192,11 +208,11 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
         if (!grads_out) continue;
         // grads over the tile's rows (w_out h-half; the ctx half is enc^T A, att_fin_kernel)
         for (int r = 0; r < kTile; r++) {
-            const double hc = S.h[r * kPad + gi];
+            const double hc = S.h[r * kPadH + gi];
 #pragma unroll
             for (int x = 0; x < kMaxDD / 4; x++) {
                 const int o = go + 4 * x;
-                if (o < dd) gw[x] = fma(hc, S.du[r * ddp + o], gw[x]);
+                if (o < dd) gw[x] = fma(hc, S.du[r * kDuLd + o], gw[x]);
             }
         }
 #pragma unroll
@@ -398,61 +414,55 @@ __global__ void __launch_bounds__(kThreads) watt_grad_kernel(int T, int parts, i
 constexpr int kAttTile = 64;  // rows per tile in att_bwd (2 rows per thread in the S/DA and dq passes)
 
 struct AttSmem {
-    double enc[2][kChunk * kPad];  // cp.async double buffer over the T chunks
-    double q[kAttTile * kPad];
-    double dc[kAttTile * kPad];
-    double al[kAttTile * kPad];
-    double ds[kAttTile * kPad];
-    double du[kAttTile * (kMaxDD + 1)];
+    double enc[2][kChunk * kPadH];  // cp.async double buffer over the T chunks
+    double q[kAttTile * kPadH];
+    double dc[kAttTile * kPadH];
+    double al[kAttTile * kPadH];
+    double ds[kAttTile * kPadH];
+    double du[kAttTile * kDuLd];
     double mx[kAttTile], sm[kAttTile], w[kAttTile];
 };
 
 // Tile-outer: a CTA owns whole 64-step tiles of one sample; per tile its
 // q / dctx / du / stats are staged once, the 64-row chunks of enc_states
 // stream through a cp.async double buffer, and dq accumulates in registers
-// over the chunks (one store per tile, no read-modify-write).  Per chunk:
-//   S/DA  (2 rows x 8 i per thread) dalpha = dctx . enc_i, alpha (STORED:
-//         e_i * esc from the decoder; else exp(q . enc_i - max) / sum),
+// over the chunks (one store per tile).  Every contraction is a 64x64x64 (or
+// 64 x dd x 64) product on the fp64 tensor cores (mma.sync m8n8k4 DMMA);
+// warp w owns the 8-row m-tile w of each product:
+//   DA    dalpha[r, i] = dctx[r] . enc_i          (S = q . enc_i too, unless STORED)
+//         alpha (STORED: e_i * esc from the decoder; else exp(s - max) / sum),
 //         ds = alpha (dalpha - w)
 //   dq    += ds @ enc_chunk
 //   dE    d_enc[i, j] = sum_r ds[r, i] q[r, j],  A[i, o] = sum_r alpha[r, i] du[r, o]
-// dE / A go to the per-tile partials (split backward) or accumulate in the
-// CTA's private partial (fused backward).
+// dE / A go to the per-sample (or per-tile) partials of the split backward,
+// or accumulate in the CTA's private partial (fused backward).
 template <bool STORED>
 __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
     const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ row_dctx,
     const double *__restrict__ row_w, const double *__restrict__ row_du, double *__restrict__ row_dq,
     double *__restrict__ partial, double *__restrict__ partA,
-    double *__restrict__ tile_partial /* [n_tiles][T][64] or NULL */,
-    double *__restrict__ tile_partA /* [n_tiles][T][dd] */, const double *__restrict__ act_e,
+    double *__restrict__ tile_partial /* [units][T][64] or NULL */,
+    double *__restrict__ tile_partA /* [units][T][dd] */, const double *__restrict__ act_e,
     const double *__restrict__ act_esc, int do_denc, int per_sample /* partials per sample, not per tile */) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
-    const int tid = threadIdx.x;
-    const int T = dm.T, dd = dm.dd, ddp = dd + 1;
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int T = dm.T, dd = dm.dd;
+    const int dd8 = (dd + 7) & ~7;  // n extent of the A product (8-column tiles)
     const int n_chunks = (T + kChunk - 1) / kChunk;
-    // tiles never straddle two samples: tile = (sample k, 64-step block)
     const int tps = (T + kAttTile - 1) / kAttTile;
     const int tile0 = blockIdx.x * tiles_per_cta;
     const int n_tiles_total = (rows / T) * tps;
     const int tile1 = min(n_tiles_total, tile0 + tiles_per_cta);
-    const int sr = tid >> 3, ib = tid & 7;  // rows {sr, sr+32}; i (or j) in {ib + 8*ii}
-    const int ei = tid >> 4, ej = tid & 15; // dE: i in {ei + 16a}, j in {ej + 16b}
+    const int mr = wp * 8 + g;  // this lane's row of the m-tile (r for DA / dq, i for dE / A)
     // enc chunk c -> buffer b (16-byte cp.async; rows past T zero-filled)
     auto stage_enc = [&](int c, int b) {
         const int i0 = c * kChunk;
         for (int x = tid; x < kChunk * (kH / 2); x += kThreads) {
             const int i = x >> 5, j2 = x & 31;
-            // kPad (65) rows are not 16-byte aligned: copy 8-byte pairs via two 8-byte lanes
             const bool ok = i0 + i < T;
-            const double *src = enc_h + (size_t)(ok ? i0 + i : 0) * kH + 2 * j2;
-            double *dst = &S.enc[b][i * kPad + 2 * j2];
-            const unsigned s0 = (unsigned)__cvta_generic_to_shared(dst);
-            const unsigned s1 = (unsigned)__cvta_generic_to_shared(dst + 1);
-            const int n = ok ? 8 : 0;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s0), "l"(src), "r"(n) : "memory");
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s1), "l"(src + 1), "r"(n) : "memory");
+            cp_async16(&S.enc[b][i * kPadH + 2 * j2], enc_h + (size_t)(ok ? i0 + i : 0) * kH + 2 * j2, ok);
         }
         cp_async_commit();
     };
@@ -467,12 +477,12 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             const int r = x >> 6, j = x & 63;
             const int row = rb + r;
             const bool ok = r < nrow;
-            S.q[r * kPad + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
-            S.dc[r * kPad + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
+            S.q[r * kPadH + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
+            S.dc[r * kPadH + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
         }
-        for (int x = tid; x < kAttTile * dd; x += kThreads) {
-            const int r = x / dd, o = x - r * dd;
-            S.du[r * ddp + o] = r < nrow ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
+        for (int x = tid; x < kAttTile * dd8; x += kThreads) {
+            const int r = x / dd8, o = x - r * dd8;
+            S.du[r * kDuLd + o] = (r < nrow && o < dd) ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
         }
         if (tid < kAttTile) {
             const int row = rb + tid;
@@ -481,30 +491,31 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             S.sm[tid] = ok ? act_stat[(size_t)row * 2 + 1] : 1.0;
             S.w[tid] = ok ? row_w[row] : 0.0;
         }
-        double acc[2][8];
+        double dq[8][2];  // dq[mr][n*8 + 2t + {0,1}], accumulated over the chunks
 #pragma unroll
-        for (int rr = 0; rr < 2; rr++)
-#pragma unroll
-            for (int jj = 0; jj < 8; jj++) acc[rr][jj] = 0.0;
+        for (int n = 0; n < 8; n++) dq[n][0] = dq[n][1] = 0.0;
+        const bool rok = mr < nrow;
         for (int ch = 0; ch < n_chunks; ch++) {
             const int i0 = ch * kChunk, b = ch & 1;
-            // this thread's stored numerators (issued before the wait: the loads
-            // overlap the chunk's cp.async and the DA mat-mul)
-            double ev[2][8], esc[2][2];
+            // this lane's stored numerators (issued before the wait: the loads
+            // overlap the chunk's cp.async and the DA product)
+            double ev[8][2], esc0 = 0.0, esc1 = 0.0;
             if (STORED) {
+                const size_t row = (size_t)(rb + (rok ? mr : 0));
 #pragma unroll
-                for (int rr = 0; rr < 2; rr++) {
-                    const int r = sr + 32 * rr;
-                    const bool okr = r < nrow;
-                    const size_t row = (size_t)(rb + (okr ? r : 0));
-#pragma unroll
-                    for (int ii = 0; ii < 8; ii++) {
-                        const int ig = i0 + ib + 8 * ii;
-                        ev[rr][ii] = (okr && ig < T) ? __ldg(act_e + row * T + ig) : 0.0;
+                for (int n = 0; n < 8; n++) {
+                    const int ig = i0 + n * 8 + 2 * t;
+                    if (rok && ig + 1 < T && ((row * T) & 1) == 0) {  // 16-byte aligned pair
+                        const double2 e2 = __ldg(reinterpret_cast<const double2 *>(act_e + row * T + ig));
+                        ev[n][0] = e2.x;
+                        ev[n][1] = e2.y;
+                    } else {
+                        ev[n][0] = (rok && ig < T) ? __ldg(act_e + row * T + ig) : 0.0;
+                        ev[n][1] = (rok && ig + 1 < T) ? __ldg(act_e + row * T + ig + 1) : 0.0;
                     }
-                    esc[rr][0] = __ldg(act_esc + row * 8 + ((i0 & 255) >> 5));
-                    esc[rr][1] = __ldg(act_esc + row * 8 + (((i0 + 32) & 255) >> 5));
                 }
+                esc0 = __ldg(act_esc + row * 8 + ((i0 & 255) >> 5));
+                esc1 = __ldg(act_esc + row * 8 + (((i0 + 32) & 255) >> 5));
             }
             if (ch + 1 < n_chunks) {
                 stage_enc(ch + 1, b ^ 1);
@@ -514,145 +525,103 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             }
             __syncthreads();
             const double *enc = S.enc[b];
-            // [S = Q enc^T,] DA = DCTX enc^T over this chunk -> alpha, ds
+            // DA (and S) for rows mr, columns i = n*8 + 2t + {0,1}
             {
-                double sv[2][8], dv[2][8];
+                double da[8][2], sv[8][2];
 #pragma unroll
-                for (int rr = 0; rr < 2; rr++)
-#pragma unroll
-                    for (int ii = 0; ii < 8; ii++) sv[rr][ii] = dv[rr][ii] = 0.0;
+                for (int n = 0; n < 8; n++) da[n][0] = da[n][1] = sv[n][0] = sv[n][1] = 0.0;
 #pragma unroll 2
-                for (int j = 0; j < kH; j++) {
-                    const double d0 = S.dc[sr * kPad + j], d1 = S.dc[(sr + 32) * kPad + j];
-                    if (STORED) {
+                for (int ks = 0; ks < kH / 4; ks++) {
+                    const double a = S.dc[mr * kPadH + ks * 4 + t];
+                    double aq = 0.0;
+                    if (!STORED) aq = S.q[mr * kPadH + ks * 4 + t];
 #pragma unroll
-                        for (int ii = 0; ii < 8; ii++) {
-                            const double e = enc[(ib + 8 * ii) * kPad + j];
-                            dv[0][ii] = fma(d0, e, dv[0][ii]);
-                            dv[1][ii] = fma(d1, e, dv[1][ii]);
-                        }
-                    } else {
-                        const double q0 = S.q[sr * kPad + j], q1 = S.q[(sr + 32) * kPad + j];
-#pragma unroll
-                        for (int ii = 0; ii < 8; ii++) {
-                            const double e = enc[(ib + 8 * ii) * kPad + j];
-                            sv[0][ii] = fma(q0, e, sv[0][ii]);
-                            sv[1][ii] = fma(q1, e, sv[1][ii]);
-                            dv[0][ii] = fma(d0, e, dv[0][ii]);
-                            dv[1][ii] = fma(d1, e, dv[1][ii]);
-                        }
+                    for (int n = 0; n < 8; n++) {
+                        const double bb = enc[(n * 8 + g) * kPadH + ks * 4 + t];  // B[j][i] = enc[i][j]
+                        dmma884(da[n], a, bb);
+                        if (!STORED) dmma884(sv[n], aq, bb);
                     }
                 }
+                const double m = S.mx[mr], l = S.sm[mr], wv = S.w[mr];
 #pragma unroll
-                for (int rr = 0; rr < 2; rr++) {
-                    const int r = sr + 32 * rr;
-                    const double m = S.mx[r], l = S.sm[r], w = S.w[r];
+                for (int n = 0; n < 8; n++)
 #pragma unroll
-                    for (int ii = 0; ii < 8; ii++) {
-                        const int i = ib + 8 * ii;
-                        double al = 0.0, ds = 0.0;
-                        if (i0 + i < T && r < nrow) {
-                            al = STORED ? ev[rr][ii] * esc[rr][ii >> 2] : exp(sv[rr][ii] - m) / l;
-                            ds = al * (dv[rr][ii] - w);
+                    for (int e = 0; e < 2; e++) {
+                        const int i = n * 8 + 2 * t + e;
+                        double al = 0.0, dsv = 0.0;
+                        if (i0 + i < T && rok) {
+                            al = STORED ? ev[n][e] * (n < 4 ? esc0 : esc1) : exp(sv[n][e] - m) / l;
+                            dsv = al * (da[n][e] - wv);
                         }
-                        S.al[r * kPad + i] = al;
-                        S.ds[r * kPad + i] = ds;
+                        S.al[mr * kPadH + i] = al;
+                        S.ds[mr * kPadH + i] = dsv;
                     }
-                }
             }
             __syncthreads();
-            // dq[row, j] += sum_i ds[row, i] enc[i, j]   (registers across chunks)
+            // dq[mr, j] += sum_i ds[mr, i] enc[i, j]
 #pragma unroll 2
-            for (int i = 0; i < kChunk; i++) {
-                const double d0 = S.ds[sr * kPad + i], d1 = S.ds[(sr + 32) * kPad + i];
+            for (int ks = 0; ks < kChunk / 4; ks++) {
+                const double a = S.ds[mr * kPadH + ks * 4 + t];
 #pragma unroll
-                for (int jj = 0; jj < 8; jj++) {
-                    const double e = enc[i * kPad + ib + 8 * jj];
-                    acc[0][jj] = fma(d0, e, acc[0][jj]);
-                    acc[1][jj] = fma(d1, e, acc[1][jj]);
-                }
+                for (int n = 0; n < 8; n++) dmma884(dq[n], a, enc[(ks * 4 + t) * kPadH + n * 8 + g]);
             }
-            if (!do_denc) continue;
-            // d_enc[i, j] += sum_r ds[r, i] q[r, j]  and  A[i, o] += sum_r al[r, i] du[r, o]
-            // (the reference's alpha^T dctx term is A W_out[64:]^T, formed once in att_fin_kernel)
-            double dE[4][4], dA[4][2];
-#pragma unroll
-            for (int a = 0; a < 4; a++) {
-#pragma unroll
-                for (int bb = 0; bb < 4; bb++) dE[a][bb] = 0.0;
-                dA[a][0] = dA[a][1] = 0.0;
+            if (!do_denc) {
+                __syncthreads();
+                continue;
             }
+            // dE[i = mr, j] = sum_r ds[r, i] q[r, j] ; A[i = mr, o] = sum_r al[r, i] du[r, o]
+            double dE[8][2], dA[4][2];
+#pragma unroll
+            for (int n = 0; n < 8; n++) dE[n][0] = dE[n][1] = 0.0;
+#pragma unroll
+            for (int n = 0; n < 4; n++) dA[n][0] = dA[n][1] = 0.0;
 #pragma unroll 2
-            for (int r = 0; r < kAttTile; r++) {
-                double av[4], sv4[4], duv[2], qv[4];
+            for (int ks = 0; ks < kAttTile / 4; ks++) {
+                const int r = ks * 4 + t;
+                const double a = S.ds[r * kPadH + mr];
+                const double aa = S.al[r * kPadH + mr];
 #pragma unroll
-                for (int a = 0; a < 4; a++) {
-                    av[a] = S.al[r * kPad + ei + 16 * a];
-                    sv4[a] = S.ds[r * kPad + ei + 16 * a];
-                }
+                for (int n = 0; n < 8; n++) dmma884(dE[n], a, S.q[r * kPadH + n * 8 + g]);
 #pragma unroll
-                for (int bb = 0; bb < 4; bb++) qv[bb] = S.q[r * kPad + ej + 16 * bb];
-                duv[0] = S.du[r * ddp + ej];
-                duv[1] = ej + 16 < dd ? S.du[r * ddp + ej + 16] : 0.0;
-#pragma unroll
-                for (int a = 0; a < 4; a++) {
-#pragma unroll
-                    for (int bb = 0; bb < 4; bb++) dE[a][bb] = fma(sv4[a], qv[bb], dE[a][bb]);
-                    dA[a][0] = fma(av[a], duv[0], dA[a][0]);
-                    dA[a][1] = fma(av[a], duv[1], dA[a][1]);
-                }
+                for (int n = 0; n < 4; n++)
+                    if (n * 8 < dd8) dmma884(dA[n], aa, S.du[r * kDuLd + n * 8 + g]);
             }
+            const int i = i0 + mr;
+            if (i < T) {
+                const size_t unit = per_sample ? (size_t)(tl / tps) : (size_t)tl;
+                const bool first = tile_partial ? (!per_sample || tl % tps == 0) : first_cta_tile;
+                double *pe = tile_partial ? tile_partial + (unit * T + i) * kH
+                                          : partial + ((size_t)blockIdx.x * T + i) * kH;
+                double *pa = tile_partial ? tile_partA + (unit * T + i) * dd : partA + ((size_t)blockIdx.x * T + i) * dd;
+                // first contribution stores; later ones add with fire-and-forget
+                // reductions (RED).  One thread owns each element and its
+                // operations on one address stay in program order: deterministic.
 #pragma unroll
-            for (int a = 0; a < 4; a++) {
-                const int i = i0 + ei + 16 * a;
-                if (i >= T) continue;
-                if (tile_partial) {
-                    // rows-only pass: this tile's (unscaled) contribution, weighted by
-                    // its sample's advantage later (weighted_reduce).  per_sample: the
-                    // CTA owns whole samples, so it sums its tiles per sample in place
-                    // (same thread, same elements: no hazard) and the reduce reads 1/tps
-                    // Later tiles add with fire-and-forget reductions (RED, no
-                    // round trip); one thread owns each element, and its operations
-                    // on one address stay in program order: deterministic sums
-                    const size_t unit = per_sample ? (size_t)(tl / tps) : (size_t)tl;
-                    const bool first = !per_sample || tl % tps == 0;
+                for (int n = 0; n < 8; n++)
 #pragma unroll
-                    for (int bb = 0; bb < 4; bb++) {
-                        double *d = tile_partial + (unit * T + i) * kH + ej + 16 * bb;
-                        if (first) *d = dE[a][bb];
-                        else atomicAdd(d, dE[a][bb]);
+                    for (int e = 0; e < 2; e++) {
+                        double *d = pe + n * 8 + 2 * t + e;
+                        if (first) *d = dE[n][e];
+                        else atomicAdd(d, dE[n][e]);
                     }
 #pragma unroll
-                    for (int bb = 0; bb < 2; bb++)
-                        if (ej + 16 * bb < dd) {
-                            double *d = tile_partA + (unit * T + i) * dd + ej + 16 * bb;
-                            if (first) *d = dA[a][bb];
-                            else atomicAdd(d, dA[a][bb]);
-                        }
-                } else {
-                    // fused pass: the CTA's private partial (first tile initialises it)
+                for (int n = 0; n < 4; n++)
 #pragma unroll
-                    for (int bb = 0; bb < 4; bb++) {
-                        double *d = partial + ((size_t)blockIdx.x * T + i) * kH + ej + 16 * bb;
-                        *d = first_cta_tile ? dE[a][bb] : *d + dE[a][bb];
+                    for (int e = 0; e < 2; e++) {
+                        const int o = n * 8 + 2 * t + e;
+                        if (o < dd) {
+                            if (first) pa[o] = dA[n][e];
+                            else atomicAdd(pa + o, dA[n][e]);
+                        }
                     }
-#pragma unroll
-                    for (int bb = 0; bb < 2; bb++)
-                        if (ej + 16 * bb < dd) {
-                            double *d = partA + ((size_t)blockIdx.x * T + i) * dd + ej + 16 * bb;
-                            *d = first_cta_tile ? dA[a][bb] : *d + dA[a][bb];
-                        }
-                }
             }
             __syncthreads();  // al / ds / this enc buffer are overwritten by the next chunk
         }
+        if (rok)
 #pragma unroll
-        for (int rr = 0; rr < 2; rr++) {
-            const int r = sr + 32 * rr;
-            if (r < nrow)
-#pragma unroll
-                for (int jj = 0; jj < 8; jj++) row_dq[(size_t)(rb + r) * kH + ib + 8 * jj] = acc[rr][jj];
-        }
+            for (int n = 0; n < 8; n++)
+                *reinterpret_cast<double2 *>(row_dq + (size_t)(rb + mr) * kH + n * 8 + 2 * t) =
+                    make_double2(dq[n][0], dq[n][1]);
         first_cta_tile = false;
     }
 }
