@@ -1370,7 +1370,11 @@ int run_b2(dp_policy *p, const double *params, int K, cudaStream_t st) {
 }
 
 // B3 on the main stream, B4 + B5 forked onto the side stream; adv == NULL: da/dh0/dc0 already scaled
-int run_b345(dp_policy *p, const double *params, int K, const double *adv, double *grad, cudaStream_t st) {
+// split_grads: also run the advantage-weighted B0 / B1f reductions on the main
+// stream inside the fork window (they only need adv and the rows-pass outputs),
+// concurrently with the sequential encoder backward.
+int run_b345(dp_policy *p, const double *params, int K, const double *adv, double *grad, cudaStream_t st,
+             bool split_grads = false) {
     const PolicyDims &dm = p->dims;
     const int T = dm.T, rows = K * T;
     double *part = p->partial;
@@ -1408,6 +1412,12 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         type_scatter_kernel<<<ceil_div(dm.V1 * dm.td, 128), 128, 0, ss>>>(dm, p->occ_off, p->occ_val, grad);
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaEventRecord(p->ev_join, ss));
+    }
+    if (split_grads) {
+        const int rc0 = run_b0(p, params, rows, adv, grad, kGradsOnly, st);
+        if (rc0 != DP_OK) return rc0;
+        const int rc1 = run_b1f(p, params, rows, adv, grad, kGradsOnly, st);
+        if (rc1 != DP_OK) return rc1;
     }
     // B3
     {
@@ -1499,7 +1509,6 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
     cudaStream_t st = (cudaStream_t)stream;
     const int T = dm.T, rows = K * T;
     DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
-    DP_TRY(run_b0(p, params, rows, adv, grad, kGradsOnly, st));
     {
         // per-sample partials (1 unit per sample) or per-tile (tps units per sample)
         const int tps = p->att_per_sample ? 1 : (T + kAttTile - 1) / kAttTile;
@@ -1511,6 +1520,6 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
         DP_LAUNCH_CHECK();
     }
     DP_TRY(run_att_fin(p, params, grad, st));
-    DP_TRY(run_b1f(p, params, rows, adv, grad, kGradsOnly, st));
-    return run_b345(p, params, K, adv, grad, st);
+    // the encoder backward (sequential) forks first; B0 / B1f grads and B3 fill the other SMs
+    return run_b345(p, params, K, adv, grad, st, true);
 }
