@@ -123,10 +123,28 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- roofline terms
 def decoder_flops_per_placement(T, D, dd=16, H=64):
-    """Algorithmic FLOPs of the decoder kernel per sampled placement:
-    per step gates 2*H*4H, q = W_att^T h 2*H*H, scores 2*T*H, context 2*T*H,
-    output 2*2H*dd + 2*dd*D."""
-    return T * (2 * H * 4 * H + 2 * H * H + 4 * T * H + 2 * 2 * H * dd + 2 * dd * D)
+    """Algorithmic FLOPs of one sampled placement in the reference's decoder
+    (pkg/policy.py:291-306): per step the gate contraction
+    [x; h] @ W_dec 2*(dd+H)*4H, scores proj @ h 2*T*H, context alpha @ enc
+    2*T*H, u = hc @ W_out 2*2H*dd, logits 2*dd*D.  (The kernel does less: the
+    x half is a (D+1)-row table lookup and the context is folded into uc.)"""
+    return T * (2 * (dd + H) * 4 * H + 4 * T * H + 2 * 2 * H * dd + 2 * dd * D)
+
+
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel`` from
+    the latest committed ncu --set full capture (profiles/rNN_ncu_summary.json)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    for f in reversed(files):
+        try:
+            d = json.load(open(f)).get(kernel)
+        except Exception:
+            continue
+        if d and "dram_bytes_per_launch" in d:
+            return {"bytes_per_launch": d["dram_bytes_per_launch"], "source": os.path.relpath(f, ROOT)}
+    return None
 
 
 def policy_flops_per_placement(T, D, K):
@@ -367,7 +385,7 @@ def main():
     achieved = dec_flops / (dec_ms * 1e-3) / 1e12
     roofline = {
         "kernel": "dec_kernel (dp_policy_decode)", "bound": "fp64", "achieved": achieved, "peak": peak64,
-        "unit": "TFLOP/s", "frac": achieved / peak64 if peak64 else None, "traffic": None,
+        "unit": "TFLOP/s", "frac": achieved / peak64 if peak64 else None, "traffic": ncu_traffic("dec_kernel"),
         "peak_source": "measured fp64 DFMA probe (dp_fp64_fma_probe) on this GPU; MEASURED_PEAKS.json "
                        "has no fp64 figure (bf16 tensor peak is not the denominator of an fp64 kernel)",
         "algorithmic_flops_per_launch": dec_flops, "avg_launch_ms": dec_ms,

@@ -19,6 +19,7 @@ METRICS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "achieved_occupancy_pct",
     "sm__inst_executed.avg.per_cycle_active": "ipc_per_sm",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "smem_wavefronts",
     "launch__registers_per_thread": "registers",
     "launch__grid_size": "grid",
@@ -77,12 +78,12 @@ def main(tag, reps):
         json.dump(res, fh, indent=1)
     with open(f"profiles/{tag}_ncu_summary.md", "w") as fh:
         fh.write(f"# ncu --set full summaries ({tag}), one launch each, bench.py C3 K=256\n\n")
-        fh.write("| kernel | ms | DRAM MB/launch | SM % | mem % | fp64 pipe % | occ % | IPC/SM | top stalls |\n")
-        fh.write("|---|---|---|---|---|---|---|---|---|\n")
+        fh.write("| kernel | ms | DRAM MB/launch | SM % | mem % | fp64 pipe % | DMMA pipe % | occ % | IPC/SM | top stalls |\n")
+        fh.write("|---|---|---|---|---|---|---|---|---|---|\n")
         for n, d in res.items():
             fh.write(f"| {n} | {d.get('duration_ns', 0) / 1e6:.3f} | {d.get('dram_bytes_per_launch', 0) / 1e6:.1f} | "
                      f"{d.get('sm_throughput_pct', 0):.1f} | {d.get('mem_throughput_pct', 0):.1f} | "
-                     f"{d.get('fp64_pipe_pct', 0) if isinstance(d.get('fp64_pipe_pct'), float) else '-'} | "
+                     f"{d.get('fp64_pipe_pct', 0):.1f} | {d.get('dmma_pipe_pct', 0):.1f} | "
                      f"{d.get('achieved_occupancy_pct', 0):.1f} | {d.get("ipc_per_sm", 0):.2f} | "
                      f"{', '.join(f'{k} {v}%' for k, v in d['stall_pct'].items())} |\n")
     print(json.dumps(res, indent=1)[:3000])
