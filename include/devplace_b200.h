@@ -178,6 +178,10 @@ typedef struct {
     int64_t error;        /* 1: a feasible measurement was not positive/finite */
 } dp_train_state;
 
+/* Simulator variant override (tests / measurement): 0 = automatic, 1 = one
+ * warp per placement, 2 = one thread per placement. */
+int dp_debug_sim_variant(int32_t mode);
+
 /* Batched search baselines on K-sim (pkg/baselines.py:227-273).
  * dp_enumerate_placements: out[count*n] (by gid) = placements start..start+
  *   count-1 of itertools.product(range(d), repeat=n) (last group fastest).

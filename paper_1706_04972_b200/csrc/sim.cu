@@ -403,6 +403,322 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
     feasible[k] = ok ? 1 : 0;
 }
 
+// ---------------------------------------------------------------- warp per placement
+// One warp scores one placement (the north-star K-sim design) — the latency
+// path for small K; the CTA's warps share the graph image staged in shared
+// memory.  Lane d (< D) keeps device d's state in registers (pending FINISH,
+// ready-queue bounds, busy / transfer / peak).  The next event is a warp
+// shuffle argmin over the devices' FINISH keys against the READY-heap top.  A
+// FINISH's out-edges go lane-parallel (link durations — the fp64 divisions —
+// arrival max-reduction into maxarr, in-degree countdown); only the link-queue
+// chain (link_free, transfer[dev] += dur) is walked in edge order, and heap
+// updates are executed redundantly by every lane (broadcast reads) with lane 0
+// writing.  Same event semantics and fp64 operation order as sim_kernel
+// (SURVEY.md Appendix A.2): bit-identical outputs, dispatch order included.
+constexpr int kSimWarps = 4;
+
+__host__ __device__ inline size_t warp_slot_bytes(int n, int d) {
+    size_t b = (size_t)n * 8 + (size_t)d * d * 8;  // maxarr, link_free
+    b += (size_t)n * 2 * 3;                        // left, heap, devq (u16)
+    b += (size_t)n;                                // placement (u8)
+    return (b + 15) & ~(size_t)15;
+}
+
+template <bool GS>
+__global__ void __launch_bounds__(32 * kSimWarps) sim_warp_kernel(
+    dp_graph g, int K, const uint8_t *__restrict__ placement, int by_rank, double *__restrict__ makespan,
+    double *__restrict__ busy_out, double *__restrict__ transfer_out, int64_t *__restrict__ peak_out,
+    uint8_t *__restrict__ feasible, int32_t *__restrict__ order, uint8_t *__restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr unsigned kFull = 0xffffffffu;
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const int n = g.n, D = g.d;
+    size_t gbytes = 0;
+    const double *g_dur = g.dur, *g_bytes = g.out_bytes, *g_bw = g.bw;
+    const int32_t *g_off = g.out_off;
+    const int32_t *g_dst32 = g.out_dst, *g_gid32 = g.gid, *g_indeg32 = g.indeg;
+    const uint16_t *g_dst16 = nullptr, *g_gid16 = nullptr, *g_indeg16 = nullptr;
+    if (GS) {
+        double *sdur = reinterpret_cast<double *>(smem);
+        double *sbytes = sdur + (size_t)n * D;
+        double *sbw = sbytes + g.e;
+        int32_t *soff = reinterpret_cast<int32_t *>(sbw + D * D);
+        uint16_t *sdst = reinterpret_cast<uint16_t *>(soff + n + 1);
+        uint16_t *sgid = sdst + g.e;
+        uint16_t *sind = sgid + n;
+        for (int i = tid; i < n * D; i += blockDim.x) sdur[i] = g.dur[i];
+        for (int i = tid; i < g.e; i += blockDim.x) {
+            sbytes[i] = g.out_bytes[i];
+            sdst[i] = (uint16_t)g.out_dst[i];
+        }
+        for (int i = tid; i < D * D; i += blockDim.x) sbw[i] = g.bw[i];
+        for (int i = tid; i <= n; i += blockDim.x) soff[i] = g.out_off[i];
+        for (int i = tid; i < n; i += blockDim.x) {
+            sgid[i] = (uint16_t)g.gid[i];
+            sind[i] = (uint16_t)g.indeg[i];
+        }
+        __syncthreads();
+        g_dur = sdur;
+        g_bytes = sbytes;
+        g_bw = sbw;
+        g_off = soff;
+        g_dst16 = sdst;
+        g_gid16 = sgid;
+        g_indeg16 = sind;
+        gbytes = graph_smem_bytes(n, D, g.e);
+    }
+    auto dst_of = [&](int e) -> int { return GS ? (int)g_dst16[e] : g_dst32[e]; };
+    auto gid_of = [&](int r) -> int { return GS ? (int)g_gid16[r] : g_gid32[r]; };
+    auto indeg_of = [&](int r) -> int { return GS ? (int)g_indeg16[r] : g_indeg32[r]; };
+    const int k = blockIdx.x * (blockDim.x >> 5) + wp;
+    if (k >= K) return;  // whole warps only; no CTA barrier follows
+    unsigned char *base = smem + gbytes + (size_t)wp * warp_slot_bytes(n, D);
+    double *maxarr = reinterpret_cast<double *>(base);  // [n] READY time (max arrival)
+    double *link = maxarr + n;                          // [D*D] link_free
+    uint16_t *left = reinterpret_cast<uint16_t *>(link + D * D);
+    uint16_t *heap = left + n;
+    uint16_t *devq = heap + n;
+    uint8_t *pl = reinterpret_cast<uint8_t *>(devq + n);
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    // ---- placement load + validation (pkg/simulator.py:109-116) ----
+    const uint8_t *src = placement + (size_t)k * n;
+    bool bad = false;
+    for (int r = lane; r < n; r += 32) {
+        const uint8_t v = by_rank ? src[r] : src[gid_of(r)];
+        bad |= (v >= D);
+        pl[r] = v;
+        left[r] = (uint16_t)indeg_of(r);
+        maxarr[r] = 0.0;
+    }
+    if (__any_sync(kFull, bad)) {
+        if (lane == 0) {
+            makespan[k] = __longlong_as_double(0x7ff8000000000000LL);
+            feasible[k] = 0;
+            if (err) *err = 1;
+        }
+        for (int j = lane; j < D; j += 32) {
+            busy_out[(size_t)k * D + j] = 0.0;
+            transfer_out[(size_t)k * D + j] = 0.0;
+            peak_out[(size_t)k * D + j] = 0;
+        }
+        return;
+    }
+    for (int j = lane; j < D * D; j += 32) link[j] = 0.0;
+    __syncwarp();
+    // ---- per-device counts and check_memory peaks (integer, exact) -> lane d ----
+    int qh = 0, qt = 0;
+    long long pk = 0;
+    for (int d = 0; d < D; d++) {
+        int c = 0;
+        long long p = 0;
+        for (int r = lane; r < n; r += 32)
+            if (pl[r] == d) {
+                c++;
+                p += (long long)g.resident[r];
+            }
+        c = __reduce_add_sync(kFull, c);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(kFull, p, o);
+        if (lane == d) {
+            qt = c;
+            pk = p;
+        }
+    }
+    {
+        // exclusive prefix over devices -> queue segment bases
+        int incl = lane < D ? qt : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+        }
+        qh = qt = incl - (lane < D ? qt : 0);
+    }
+    // sources enter their device queue at t=0 in rank order (pkg/simulator.py:154-156)
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        const int r = c0 + lane;
+        const int dv = (r < n && left[r] == 0) ? (int)pl[r] : -1;
+        for (int d = 0; d < D; d++) {
+            const unsigned m = __ballot_sync(kFull, dv == d);
+            if (!m) continue;
+            const int qd = __shfl_sync(kFull, qt, d);
+            if (dv == d) devq[qd + __popc(m & lt_mask)] = (uint16_t)r;
+            if (lane == d) qt += __popc(m);
+        }
+    }
+    __syncwarp();
+    double fin_t = 0.0, busy = 0.0, trans = 0.0;
+    int fin_r = -1;
+    int n_order = 0;
+    int32_t *ord = order ? order + (size_t)k * n : nullptr;
+    // start_next(dev, now) on the lanes that ask, device order for the dispatch log (pkg/simulator.py:146-152)
+    auto start_next = [&](bool want, double now) {
+        const bool go = want && lane < D && fin_r < 0 && qh < qt;
+        const unsigned m = __ballot_sync(kFull, go);
+        if (go) {
+            const int r = devq[qh];
+            qh++;
+            const double du = g_dur[r * D + lane];
+            busy += du;
+            fin_t = now + du;
+            fin_r = r;
+            if (ord) ord[n_order + __popc(m & lt_mask)] = gid_of(r);
+        }
+        n_order += __popc(m);
+    };
+    start_next(true, 0.0);
+    int d_pow2 = 1;
+    while (d_pow2 < D) d_pow2 <<= 1;
+    int n_heap = 0;
+    double mk = 0.0;
+    for (;;) {
+        // next FINISH: min (t, rank) over busy devices (shuffle argmin)
+        const bool act = lane < D && fin_r >= 0;
+        double bt = act ? fin_t : 0.0;
+        int br = act ? fin_r : -1, bd = lane;
+        for (int o = d_pow2 >> 1; o > 0; o >>= 1) {
+            const double ot = __shfl_xor_sync(kFull, bt, o);
+            const int orr = __shfl_xor_sync(kFull, br, o), od = __shfl_xor_sync(kFull, bd, o);
+            if (orr >= 0 && (br < 0 || key_less(ot, orr, bt, br))) {
+                bt = ot;
+                br = orr;
+                bd = od;
+            }
+        }
+        bt = __shfl_sync(kFull, bt, 0);
+        br = __shfl_sync(kFull, br, 0);
+        bd = __shfl_sync(kFull, bd, 0);
+        int hr = 0;
+        double ht = 0.0;
+        if (n_heap > 0) {
+            hr = heap[0];
+            ht = maxarr[hr];
+        }
+        if (br >= 0 && (n_heap == 0 || bt <= ht)) {
+            // ---- FINISH (pkg/simulator.py:162-178) ----
+            if (lane == bd) fin_r = -1;
+            mk = bt > mk ? bt : mk;
+            const int e0 = g_off[br], e1 = g_off[br + 1];
+            double tr = __shfl_sync(kFull, trans, bd);
+            for (int eb = e0; eb < e1; eb += 32) {
+                const int e = eb + lane;
+                const bool has = e < e1;
+                int dst = 0, ddev = 0;
+                double dur = 0.0;
+                bool lk = false;
+                if (has) {
+                    dst = dst_of(e);
+                    ddev = pl[dst];
+                    const double nbytes = g_bytes[e];
+                    lk = ddev != bd && nbytes != 0.0;
+                    if (lk) dur = nbytes / g_bw[bd * D + ddev];
+                }
+                double arrive = bt;
+                // link queues in edge order: begin = max(t, link_free), transfer[dev] += dur
+                unsigned lm = __ballot_sync(kFull, lk);
+                while (lm) {
+                    const int j = __ffs(lm) - 1;
+                    lm &= lm - 1;
+                    const int li = bd * D + __shfl_sync(kFull, ddev, j);
+                    const double dj = __shfl_sync(kFull, dur, j);
+                    const double lf = link[li];
+                    const double begin = lf > bt ? lf : bt;
+                    const double end = begin + dj;
+                    __syncwarp();
+                    if (lane == 0) link[li] = end;
+                    __syncwarp();
+                    tr = tr + dj;
+                    if (lane == j) arrive = end;
+                }
+                // arrivals fold into maxarr, in-degrees count down (one edge per dst: lane-parallel)
+                bool ready = false;
+                if (has) {
+                    const double ma = maxarr[dst];
+                    maxarr[dst] = arrive > ma ? arrive : ma;
+                    const int l = left[dst] - 1;
+                    left[dst] = (uint16_t)l;
+                    ready = l == 0;
+                }
+                __syncwarp();
+                // READY pushes, key (maxarr, rank): keys are unique, so push order is immaterial
+                unsigned rm = __ballot_sync(kFull, ready);
+                while (rm) {
+                    const int j = __ffs(rm) - 1;
+                    rm &= rm - 1;
+                    const int r = __shfl_sync(kFull, dst, j);
+                    const double t = maxarr[r];
+                    int i = n_heap++;
+                    while (i > 0) {
+                        const int p = (i - 1) >> 1;
+                        const int pr = heap[p];
+                        if (!key_less(t, r, maxarr[pr], pr)) break;
+                        if (lane == 0) heap[i] = (uint16_t)pr;
+                        i = p;
+                    }
+                    if (lane == 0) heap[i] = (uint16_t)r;
+                    __syncwarp();
+                }
+            }
+            if (lane == bd) trans = tr;
+            start_next(lane == bd, bt);
+        } else if (n_heap > 0) {
+            // ---- READY (= the reference's final ARRIVAL, pkg/simulator.py:179-184) ----
+            const int last = heap[--n_heap];
+            if (n_heap > 0) {
+                const double xt = maxarr[last];
+                int i = 0;
+                for (;;) {
+                    int c = 2 * i + 1;
+                    if (c >= n_heap) break;
+                    int cr = heap[c];
+                    double ct = maxarr[cr];
+                    if (c + 1 < n_heap) {
+                        const int c2 = heap[c + 1];
+                        const double t2 = maxarr[c2];
+                        if (key_less(t2, c2, ct, cr)) {
+                            c++;
+                            cr = c2;
+                            ct = t2;
+                        }
+                    }
+                    if (!key_less(ct, cr, xt, last)) break;
+                    if (lane == 0) heap[i] = (uint16_t)cr;
+                    i = c;
+                }
+                if (lane == 0) heap[i] = (uint16_t)last;
+            }
+            __syncwarp();
+            const int d = pl[hr];
+            // sorted insertion into the device queue (tail, usually O(1))
+            const int qtd = __shfl_sync(kFull, qt, d), qhd = __shfl_sync(kFull, qh, d);
+            int pos = qtd;
+            while (pos > qhd) {
+                const int pr = devq[pos - 1];
+                if (!key_less(ht, hr, maxarr[pr], pr)) break;
+                if (lane == 0) devq[pos] = (uint16_t)pr;
+                pos--;
+            }
+            if (lane == 0) devq[pos] = (uint16_t)hr;
+            __syncwarp();
+            if (lane == d) qt++;
+            start_next(lane == d, ht);
+        } else {
+            break;
+        }
+    }
+    if (lane == 0) makespan[k] = mk;
+    bool ok = true;
+    if (lane < D) {
+        busy_out[(size_t)k * D + lane] = busy;
+        transfer_out[(size_t)k * D + lane] = trans;
+        peak_out[(size_t)k * D + lane] = pk;
+        ok = pk <= (long long)g.mem[lane];
+    }
+    ok = __all_sync(kFull, ok);
+    if (lane == 0) feasible[k] = ok ? 1 : 0;
+}
+
 // Lexicographic enumeration for brute force (itertools.product order:
 // the last group varies fastest), placements by gid.
 __global__ void enumerate_kernel(int n, int d, unsigned long long start, int count, uint8_t *__restrict__ out) {
@@ -539,6 +855,35 @@ static int launch_sim(const dp_graph *g, int grid, int threads, size_t smem, cud
     return DP_OK;
 }
 
+static int g_sim_variant = 0;  // dp_debug_sim_variant
+extern "C" int dp_debug_sim_variant(int32_t mode) {
+    DP_ENTRY();
+    DP_REQUIRE(mode >= 0 && mode <= 2, "dp_debug_sim_variant: mode must be 0, 1 or 2");
+    g_sim_variant = mode;
+    return DP_OK;
+}
+
+// Kernel choice (measured, profiles/r01_sim_throughput.txt): one warp per
+// placement everywhere except many placements of small graphs, where one
+// thread per placement keeps 32x more placements in flight per warp (C1 at
+// K=65536: 42M/s vs 29M/s).
+inline bool sim_warp_preferred(const dp_graph *g, int K) { return !(g->n <= 128 && K >= 32768); }
+
+template <bool GS>
+static int launch_sim_warp(const dp_graph *g, int K, size_t gb, cudaStream_t st, const uint8_t *placement,
+                           int by_rank, double *makespan, double *busy, double *transfer, int64_t *peak,
+                           uint8_t *feasible, int32_t *order, uint8_t *err) {
+    // with the graph staged, 4 warps share one copy; otherwise 1-warp CTAs
+    // (more resident placements per SM for large graphs)
+    const int W = GS ? kSimWarps : 1;
+    const size_t smem = warp_slot_bytes(g->n, g->d) * W + (GS ? gb : 0) + 16;
+    if (smem > 48 * 1024) DP_CUDA_TRY(dp::allow_big_smem((const void *)sim_warp_kernel<GS>, smem));
+    sim_warp_kernel<GS><<<dp::ceil_div(K, W), 32 * W, smem, st>>>(
+        *g, K, placement, by_rank, makespan, busy, transfer, peak, feasible, order, err);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
 extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *placement, int32_t by_rank,
                                  double *makespan, double *busy, double *transfer, int64_t *peak,
                                  uint8_t *feasible, int32_t *order, uint8_t *err, void *stream) {
@@ -546,6 +891,21 @@ extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *pl
     DP_REQUIRE(g != nullptr, "dp_simulate_batch: graph is NULL");
     DP_REQUIRE(K >= 0, "dp_simulate_batch: K < 0");
     if (K == 0) return DP_OK;
+    {
+        const size_t gb = graph_smem_bytes(g->n, g->d, g->e);
+        const size_t ws = warp_slot_bytes(g->n, g->d) * kSimWarps;
+        const bool fits_gs = gb + ws + 16 <= kSmemBudget;
+        const bool fits = warp_slot_bytes(g->n, g->d) + 16 <= kSmemBudget;
+        const bool want = g_sim_variant == 1 || (g_sim_variant == 0 && sim_warp_preferred(g, K));
+        if (want && fits) {
+            cudaStream_t st = (cudaStream_t)stream;
+            if (fits_gs)
+                return launch_sim_warp<true>(g, K, gb, st, placement, by_rank, makespan, busy, transfer, peak,
+                                             feasible, order, err);
+            return launch_sim_warp<false>(g, K, gb, st, placement, by_rank, makespan, busy, transfer, peak,
+                                          feasible, order, err);
+        }
+    }
     const size_t per = g->sim_smem_per_placement;
     const size_t gb = graph_smem_bytes(g->n, g->d, g->e);
     // stage the graph in shared memory when it leaves room for the placements

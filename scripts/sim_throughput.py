@@ -6,6 +6,10 @@ import numpy as np, torch
 from fixtures import cfg
 import paper_1706_04972_b200.simulator as S
 
+from paper_1706_04972_b200 import _native as nat
+
+variant = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # 0 auto, 1 warp/placement, 2 thread/placement
+nat.check(nat.lib().dp_debug_sim_variant(variant), "variant")
 res = {}
 for name, Ks in (("C1", [8, 256, 4096, 65536]), ("C2", [64, 4096, 32768]), ("C3", [256, 4096, 65536]), ("C5", [512, 4096])):
     gg, topo, _, _ = cfg(name)
@@ -24,5 +28,5 @@ for name, Ks in (("C1", [8, 256, 4096, 65536]), ("C2", [64, 4096, 32768]), ("C3"
         e.record(); torch.cuda.synchronize()
         ms = s.elapsed_time(e) / it
         res[f"{name}_K{K}"] = dict(ms=ms, placements_per_s=K / ms * 1e3)
-        print(name, K, f"{ms:.3f} ms", f"{K/ms*1e3:,.0f} placements/s", flush=True)
-json.dump(res, open("gpurun_out/sim_throughput.json", "w"), indent=1)
+        print(name, K, f"variant={variant}", f"{ms:.3f} ms", f"{K/ms*1e3:,.0f} placements/s", flush=True)
+json.dump(res, open(f"gpurun_out/sim_throughput_v{variant}.json", "w"), indent=1)

@@ -16,6 +16,17 @@ pytestmark = pytest.mark.gpu
 CONFIGS = ["C1", "C2", "C3", "C3tight", "C5"]
 
 
+@pytest.fixture(params=["warp", "thread"], autouse=True)
+def sim_variant(request):
+    """Every test runs on both simulator kernels: one warp per placement and
+    one thread per placement (dp_debug_sim_variant)."""
+    from paper_1706_04972_b200 import _native as nat
+
+    nat.check(nat.lib().dp_debug_sim_variant(1 if request.param == "warp" else 2), "variant")
+    yield request.param
+    nat.check(nat.lib().dp_debug_sim_variant(0), "variant")
+
+
 def _host(out):
     return {k: v.cpu().numpy() for k, v in out.items()}
 
