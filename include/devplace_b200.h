@@ -116,6 +116,9 @@ int dp_policy_encode(dp_policy *p, const double *params, void *stream);
  * decoder (block 0) and read+reset the 8 sums into h_out[8] (may be NULL). */
 int dp_debug_phase_clocks(int32_t enable, int64_t *h_out);
 
+/* Debug instrumentation: LSTM-backward phase clocks (block 0) into h_out[8]. */
+int dp_debug_lstm_clocks(int32_t enable, int64_t *h_out);
+
 /* Decoder variant override (tests / measurement): 0 = automatic plan,
  * 1 = force the speculative next-step cell (idle warps evaluate the LSTM
  * cell for every possible choice during the draw), 2 = forbid it. */

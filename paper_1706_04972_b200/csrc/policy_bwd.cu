@@ -801,6 +801,8 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
 // while the current step's mat-vec runs.  In place: gate activations become da.
 constexpr int kMaxSeqPerCta = 8;
 constexpr int kLstmThreads = 512;
+__device__ int g_lstm_dbg = 0;            // debug-only phase clocks of lstm_bwd (block 0, thread 0)
+__device__ long long g_lstm_clk[2][4];    // [M == 1 ? 0 : 1][phase]
 // da in shared memory: per (sample, gate) a 68-double block holding the two
 // 32-gate halves at offsets 0 and 34 -> the 8 parts of a warp start in 8
 // distinct 16-byte bank groups (conflict-free LDS.128)
@@ -859,6 +861,15 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     load(T - 2, nxt);
     double tc = tanh(cur.c);
     const int dslot = (xu >> 5) * kDaHalf + (xu & 31);
+    const bool clk_on = g_lstm_dbg && blockIdx.x == 0 && tid == 0;
+    const int ci = M == 1 ? 0 : 1;
+    long long clk_last = clk_on ? clock64() : 0;
+#define DP_LPHASE(i)                                   \
+    if (clk_on) {                                      \
+        const long long now_ = clock64();              \
+        g_lstm_clk[ci][i] += now_ - clk_last;          \
+        clk_last = now_;                               \
+    }
     __syncthreads();
     for (int t = T - 1; t >= 0; t--) {
         if (live) {
@@ -887,8 +898,10 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         }
         cur = nxt;
         load(t - 2, nxt);  // lands during this and the next step's barrier + mat-vec
+        DP_LPHASE(0);
         __syncthreads();
-        tc = tanh(cur.c);  // independent of the mat-vec below: the two chains interleave
+        DP_LPHASE(1);
+        if (live) tc = tanh(cur.c);  // independent of the mat-vec below: the two chains interleave
         double v[MT];
 #pragma unroll
         for (int m = 0; m < MT; m++) {
@@ -915,8 +928,11 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
             v[m] += __shfl_xor_sync(0xffffffffu, v[m], 4);
             if (part == 0 && m < Mb) s_dh[m * kH + r] = v[m];
         }
+        DP_LPHASE(2);
         __syncthreads();
+        DP_LPHASE(3);
     }
+#undef DP_LPHASE
     for (int y = tid; y < Mb * kH; y += kLstmThreads) {
         const int m = y >> 6, u = y & 63;
         dh_out[(size_t)(q0 + m) * kH + u] = s_dh[y];
@@ -1215,6 +1231,18 @@ int n_cta_for(int units, int min_units) {
 }  // namespace dp
 
 using namespace dp;
+
+// Debug: LSTM-backward phase clocks [encoder (M=1) / decoder (M>1)][elementwise,
+// barrier 1, tanh + mat-vec, barrier 2] into h_out[8]; read + reset.
+extern "C" int dp_debug_lstm_clocks(int32_t enable, int64_t *h_out) {
+    DP_ENTRY();
+    const int on = enable ? 1 : 0;
+    DP_CUDA_TRY(cudaMemcpyToSymbol(g_lstm_dbg, &on, sizeof(int)));
+    if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_lstm_clk, sizeof(long long) * 8));
+    long long z[8] = {0};
+    DP_CUDA_TRY(cudaMemcpyToSymbol(g_lstm_clk, z, sizeof(z)));
+    return DP_OK;
+}
 
 size_t dp_backward_partial_elems(const dp_policy *p) {
     const PolicyDims &dm = p->dims;
