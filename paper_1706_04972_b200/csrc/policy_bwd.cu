@@ -803,12 +803,13 @@ constexpr int kMaxSeqPerCta = 8;
 constexpr int kLstmThreads = 512;
 __device__ int g_lstm_dbg = 0;            // debug-only phase clocks of lstm_bwd (block 0, thread 0)
 __device__ long long g_lstm_clk[2][4];    // [M == 1 ? 0 : 1][phase]
-// da in shared memory: per (sample, gate) a 68-double block holding the two
-// 32-gate halves at offsets 0 and 34 -> the 8 parts of a warp start in 8
-// distinct 16-byte bank groups (conflict-free LDS.128)
-constexpr int kDaLd = 68, kDaHalf = 34;
-
-inline size_t lstm_bwd_smem(int M) { return sizeof(double) * (size_t)M * (2 * kH + 4 * kDaLd); }
+// Mat-vec mapping: lane j of warp w owns gate columns {j + 32q} (q < 8) of
+// W_h rows 4w..4w+3 (32 weights in registers).  Every lane reads a DIFFERENT
+// da value (8 conflict-free LDS.64 per sample per thread: 16 shared-memory
+// wavefronts per warp, 4x fewer than a part-per-row layout whose lanes re-read
+// the same slices), then a reduce-scatter butterfly (6 shuffles) leaves row
+// sums on lanes 0, 8, 16, 24.
+inline size_t lstm_bwd_smem(int M) { return sizeof(double) * (size_t)M * (2 * kH + kG); }
 
 template <int MT>
 __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
@@ -820,14 +821,16 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     extern __shared__ __align__(16) double sm[];
     double *s_dh = sm;                   // [M][64]
     double *s_dc = s_dh + M * kH;        // [M][64]
-    double *s_da = s_dc + M * kH;        // [M][4 gates][kDaLd]
+    double *s_da = s_dc + M * kH;        // [M][256] gate columns (i, f, o, g blocks of 64)
     const int tid = threadIdx.x;
     const int q0 = blockIdx.x * M;
     const int Mb = min(M, n_seq - q0);
-    const int r = tid >> 3, part = tid & 7;
-    double w[32];
+    const int lane = tid & 31, wrow = (tid >> 5) * 4;  // rows wrow..wrow+3, columns lane + 32q
+    double w[4][8];
 #pragma unroll
-    for (int i = 0; i < 32; i++) w[i] = Wh[(size_t)r * kG + part * 32 + i];
+    for (int rr = 0; rr < 4; rr++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) w[rr][q] = Wh[(size_t)(wrow + rr) * kG + lane + 32 * q];
     for (int x = tid; x < Mb * kH; x += kLstmThreads) {
         const int m = x >> 6, u = x & 63;
         s_dh[x] = dh_in ? dh_in[(size_t)(q0 + m) * kH + u] : 0.0;
@@ -860,14 +863,15 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     load(T - 1, cur);
     load(T - 2, nxt);
     double tc = tanh(cur.c);
-    const int dslot = (xu >> 5) * kDaHalf + (xu & 31);
+
     const bool clk_on = g_lstm_dbg && blockIdx.x == 0 && tid == 0;
     const int ci = M == 1 ? 0 : 1;
     long long clk_last = clk_on ? clock64() : 0;
+    long long clk_acc[4] = {0, 0, 0, 0};  // in registers; one global write at the end
 #define DP_LPHASE(i)                                   \
     if (clk_on) {                                      \
         const long long now_ = clock64();              \
-        g_lstm_clk[ci][i] += now_ - clk_last;          \
+        clk_acc[i] += now_ - clk_last;                 \
         clk_last = now_;                               \
     }
     __syncthreads();
@@ -885,11 +889,11 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
             const double da_f = df * fv * (1.0 - fv);
             const double da_o = d_o * ov * (1.0 - ov);
             const double da_g = dg * (1.0 - gv * gv);
-            double *sd = s_da + xm * 4 * kDaLd + dslot;
+            double *sd = s_da + xm * kG + xu;
             sd[0] = da_i;
-            sd[kDaLd] = da_f;
-            sd[2 * kDaLd] = da_o;
-            sd[3 * kDaLd] = da_g;
+            sd[kH] = da_f;
+            sd[2 * kH] = da_o;
+            sd[3 * kH] = da_g;
             double *g = gates + ((size_t)(q0 + xm) * T + t) * kG;
             g[xu] = da_i;
             g[kH + xu] = da_f;
@@ -902,37 +906,47 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         __syncthreads();
         DP_LPHASE(1);
         if (live) tc = tanh(cur.c);  // independent of the mat-vec below: the two chains interleave
-        double v[MT];
+        // per sample: partial row sums over this lane's 8 columns, then a
+        // reduce-scatter butterfly (xor 16 and 8 halve the rows, xor 4, 2, 1 sum)
+        const bool hi16 = lane & 16, hi8 = lane & 8;
 #pragma unroll
         for (int m = 0; m < MT; m++) {
-            v[m] = 0.0;
-            if (m < Mb) {
-                const double2 *sd =
-                    reinterpret_cast<const double2 *>(s_da + (m * 4 + (part >> 1)) * kDaLd + (part & 1) * kDaHalf);
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            if (m >= Mb) break;
+            double p[4];
+            {
+                double dv[8];
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) {
-                    const double2 v0 = sd[i], v1 = sd[i + 1];
-                    a0 = fma(w[2 * i], v0.x, a0);
-                    a1 = fma(w[2 * i + 1], v0.y, a1);
-                    a2 = fma(w[2 * i + 2], v1.x, a2);
-                    a3 = fma(w[2 * i + 3], v1.y, a3);
+                for (int q = 0; q < 8; q++) dv[q] = s_da[m * kG + lane + 32 * q];
+#pragma unroll
+                for (int rr = 0; rr < 4; rr++) {
+                    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 8; q += 2) {
+                        a0 = fma(w[rr][q], dv[q], a0);
+                        a1 = fma(w[rr][q + 1], dv[q + 1], a1);
+                    }
+                    p[rr] = a0 + a1;
                 }
-                v[m] = (a0 + a1) + (a2 + a3);
             }
-        }
-#pragma unroll
-        for (int m = 0; m < MT; m++) {
-            v[m] += __shfl_xor_sync(0xffffffffu, v[m], 1);
-            v[m] += __shfl_xor_sync(0xffffffffu, v[m], 2);
-            v[m] += __shfl_xor_sync(0xffffffffu, v[m], 4);
-            if (part == 0 && m < Mb) s_dh[m * kH + r] = v[m];
+            const double s0 = hi16 ? p[0] : p[2], s1 = hi16 ? p[1] : p[3];
+            const double k0 = hi16 ? p[2] : p[0], k1 = hi16 ? p[3] : p[1];
+            const double q0v = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+            const double q1v = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+            double v = (hi8 ? q1v : q0v) + __shfl_xor_sync(0xffffffffu, hi8 ? q0v : q1v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            // lane (hi16, hi8, 0) holds row wrow + 2*hi16 + hi8
+            if ((lane & 7) == 0) s_dh[m * kH + wrow + (hi16 ? 2 : 0) + (hi8 ? 1 : 0)] = v;
         }
         DP_LPHASE(2);
         __syncthreads();
         DP_LPHASE(3);
     }
 #undef DP_LPHASE
+    if (clk_on)
+#pragma unroll
+        for (int i = 0; i < 4; i++) g_lstm_clk[ci][i] += clk_acc[i];
     for (int y = tid; y < Mb * kH; y += kLstmThreads) {
         const int m = y >> 6, u = y & 63;
         dh_out[(size_t)(q0 + m) * kH + u] = s_dh[y];

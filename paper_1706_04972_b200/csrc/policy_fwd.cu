@@ -378,10 +378,11 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
     const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
     long long clk_last = clk_on ? clock64() : 0;
+    long long clk_acc[3] = {0, 0, 0};  // in registers; one global write at the end
 #define DP_PHASE(i)                                       \
     if (clk_on) {                                         \
         const long long now_ = clock64();                 \
-        g_phase_clk[i] += now_ - clk_last;                \
+        clk_acc[i] += now_ - clk_last;                    \
         clk_last = now_;                                  \
     }
     for (int t = 0; t < T; t++) {
@@ -756,6 +757,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         DP_PHASE(2);
     }
 #undef DP_PHASE
+    if (clk_on)
+#pragma unroll
+        for (int i = 0; i < 3; i++) g_phase_clk[i] += clk_acc[i];
     // ---- log p = sum_t (zs[c_t] - log sum_t): logs in parallel, sum in t order ----
     __threadfence_block();
     for (int m = 0; m < Mb; m++) {
