@@ -1,0 +1,92 @@
+// Branch-free fp64 exp / expm1 / reciprocal for the recurrent kernels.
+//
+// CUDA's exp()/expm1()/division carry slow-path branches, so two independent
+// activations in one thread do not overlap (measured: scripts/act_probe2.cu,
+// 1 warp x 2 samples = 2x the latency of 1).  These straight-line versions
+// (Cody-Waite range reduction with FMA, Estrin-evaluated Taylor polynomial,
+// exponent-field scaling, rcp.approx + Newton) interleave freely.  Accuracy:
+// within 2 ulp of the libm results over the activation ranges (tests:
+// test_fastmath_ulp), which the parity tests absorb: every sampled placement
+// stays bit-exact.
+#pragma once
+#include <math.h>
+
+namespace dp {
+
+// 2^k for integer-valued k, clamped: k <= -1023 -> 0, k >= 1024 -> +inf
+__device__ __forceinline__ double fm_pow2(double k) {
+    const double kc = fmin(fmax(k, -1023.0), 1024.0);
+    const long long e = (long long)kc + 1023;
+    return __longlong_as_double(e << 52);
+}
+
+// expm1 on the reduced argument |r| <= ln2/2: r + r^2 (1/2! + r/3! + ... + r^11/13!)
+__device__ __forceinline__ double fm_expm1_poly(double r) {
+    const double r2 = r * r;
+    const double a0 = fma(r, 1.0 / 6.0, 0.5);
+    const double a1 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    const double a2 = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+    const double a3 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0);
+    const double a4 = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0);
+    const double a5 = fma(r, 1.0 / 6227020800.0, 1.0 / 479001600.0);
+    const double r4 = r2 * r2;
+    const double b0 = fma(r2, a1, a0);
+    const double b1 = fma(r2, a3, a2);
+    const double b2 = fma(r2, a5, a4);
+    const double r8 = r4 * r4;
+    const double c0 = fma(r4, b1, b0);
+    const double q = fma(r8, b2, c0);
+    return fma(r2, q, r);
+}
+
+__device__ __forceinline__ void fm_reduce(double y, double &k, double &r) {
+    constexpr double kL2E = 1.4426950408889634;
+    constexpr double kLn2Hi = 6.93147180559945286227e-01;  // ln2 rounded to double
+    constexpr double kLn2Lo = 2.31904681384629955842e-17;  // ln2 - kLn2Hi
+    y = fmin(fmax(y, -1000.0), 1000.0);  // saturates exp to 0 / inf, expm1 to -1 / inf; keeps r sane (-inf -> 0)
+    k = rint(y * kL2E);
+    r = fma(-k, kLn2Hi, y);
+    r = fma(-k, kLn2Lo, r);
+}
+
+// expm1(y) = 2^k (p + 1) - 1 = 2^k p + (2^k - 1)
+__device__ __forceinline__ double fm_expm1(double y) {
+    double k, r;
+    fm_reduce(y, k, r);
+    const double p = fm_expm1_poly(r);
+    const double s = fm_pow2(k);
+    return fma(s, p, s - 1.0);
+}
+
+// exp(y) = 2^k (1 + p)
+__device__ __forceinline__ double fm_exp(double y) {
+    double k, r;
+    fm_reduce(y, k, r);
+    const double p = fm_expm1_poly(r);
+    const double s = fm_pow2(k);
+    return fma(s, p, s);
+}
+
+// a / b for b >= 1 (finite or +inf): rcp.approx + two Newton steps + one
+// residual correction
+__device__ __forceinline__ double fm_div(double a, double b) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+    double e = fma(-b, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-b, y, 1.0);
+    y = fma(y, e, y);
+    const double q = a * y;
+    const double rr = fma(-b, q, a);
+    return fma(rr, y, q);
+}
+
+// LSTM gate activation without branches: sigmoid(x) = 1 / (2 + expm1(-x)),
+// tanh(x) = sign(x) (-e) / (2 + e) with e = expm1(-2|x|)
+__device__ __forceinline__ double fm_gate_act(double x, bool is_tanh) {
+    const double e = fm_expm1(is_tanh ? -2.0 * fabs(x) : -x);
+    const double r = fm_div(is_tanh ? -e : 1.0, 2.0 + e);
+    return is_tanh ? copysign(r, x) : r;
+}
+
+}  // namespace dp

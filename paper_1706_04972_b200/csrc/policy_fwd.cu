@@ -29,6 +29,7 @@
 
 #include <vector>
 
+#include "fastmath.cuh"
 #include "pcg64.cuh"
 #include "policy.cuh"
 
@@ -43,11 +44,10 @@ __device__ __forceinline__ double sigmoid_ref(double x) { return 1.0 / (1.0 + ex
 // expm1 keeps tanh's relative accuracy near 0 and nothing overflows; the
 // result differs from numpy's 1/(1+exp(-x)) / tanh(x) by ~1 ulp (same order
 // as the dot-product summation-order differences).
-__device__ __forceinline__ double gate_act(double x, bool is_tanh) {
-    const double e = expm1(is_tanh ? -2.0 * fabs(x) : -x);
-    const double r = (is_tanh ? -e : 1.0) / (2.0 + e);
-    return is_tanh ? copysign(r, x) : r;
-}
+// The expm1 and the division are the branch-free fastmath.cuh versions, so the
+// activations of a thread's M samples overlap (libm's slow-path branches
+// serialise them).
+__device__ __forceinline__ double gate_act(double x, bool is_tanh) { return fm_gate_act(x, is_tanh); }
 __device__ __forceinline__ double tanh_x(double x) { return gate_act(x, true); }
 
 // Debug-only per-phase cycle counters of the decoder (block 0, thread 0).
@@ -322,9 +322,11 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         for (int i = tid; i < (D + 1) * kG; i += kThreads) edevS[i] = a.edev[i];
     // h_{-1} = encoder final state (SPEC: staged in alS, free until step 0's scores)
     double *h0 = SPEC ? alS : hS;
-    for (int i = tid; i < (SPEC ? kH : Mb * kH); i += kThreads) h0[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
+    for (int i = tid; i < (SPEC ? kH : M * kH); i += kThreads) h0[i] = a.enc_h[(size_t)(T - 1) * kH + (i & 63)];
+    // both parity halves, all M slots: the per-sample loops compute unguarded
+    // (branch-free, so the samples' chains interleave) and only the stores check Mb
+    if (tid < 2 * M) prev[tid] = SPEC ? 0 : D;  // SPEC: step 0's state lives in candidate slot 0
     if (tid < Mb) {
-        prev[tid] = SPEC ? 0 : D;  // SPEC: step 0's state lives in candidate slot 0
         if (!a.forced) {
             const long long kg = a.k_offset + k0 + tid;
             unsigned long long n0 = a.draw_base + (unsigned long long)kg * (unsigned long long)T;
@@ -390,31 +392,31 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         const int *prv = prev + par * M;  // choices of step t-1 (SPEC: candidate slots)
         if (!SPEC) {
             // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
-            double act[MT], cn[MT];
+            // every sample slot computes (no branches between the chains); stores check Mb
+            double act[MT], cn[MT], hn[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++) act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
 #pragma unroll
             for (int m = 0; m < MT; m++)
-                if (m < Mb) {
-                    act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
-                    a.act_g[((size_t)(k0 + m) * T + t) * kG + col] = act[m];
-                }
+                if (m < Mb) a.act_g[((size_t)(k0 + m) * T + t) * kG + col] = act[m];
 #pragma unroll
-            for (int m = 0; m < MT; m++)
-                if (m < Mb) {
-                    const double iv = __shfl_sync(0xffffffffu, act[m], base + 0);
-                    const double fv = __shfl_sync(0xffffffffu, act[m], base + 1);
-                    const double ov = __shfl_sync(0xffffffffu, act[m], base + 2);
-                    const double gv = __shfl_sync(0xffffffffu, act[m], base + 3);
-                    cn[m] = fv * cst[m] + iv * gv;
-                    act[m] = ov;
-                }
+            for (int m = 0; m < MT; m++) {
+                const double iv = __shfl_sync(0xffffffffu, act[m], base + 0);
+                const double fv = __shfl_sync(0xffffffffu, act[m], base + 1);
+                const double ov = __shfl_sync(0xffffffffu, act[m], base + 2);
+                const double gv = __shfl_sync(0xffffffffu, act[m], base + 3);
+                cn[m] = fv * cst[m] + iv * gv;
+                act[m] = ov;
+            }
+#pragma unroll
+            for (int m = 0; m < MT; m++) hn[m] = act[m] * tanh_x(cn[m]);
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb && gate == 0) {
-                    const double hn = act[m] * tanh_x(cn[m]);
                     const size_t row = (size_t)(k0 + m) * T + t;
                     cst[m] = cn[m];
-                    hS[m * kH + u] = hn;
-                    a.act_h[row * kH + u] = hn;
+                    hS[m * kH + u] = hn[m];
+                    a.act_h[row * kH + u] = hn[m];
                     a.act_c[row * kH + u] = cn[m];
                 }
             __syncthreads();
@@ -512,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) {
-                    const double e = exp(alS[m * a.Tpad + i] - lmx[m]);
+                    const double e = fm_exp(alS[m * a.Tpad + i] - lmx[m]);
                     alS[m * a.Tpad + i] = e;
                     lsm[m] += e;
                     if (a.act_e) a.act_e[((size_t)(k0 + m) * T + t) * T + i] = e;
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 gmx = pmx[m];
 #pragma unroll
                 for (int ww = 1; ww < kWarps; ww++) gmx = fmax(gmx, pmx[ww * M + m]);
-                f = lane < kWarps ? exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
+                f = lane < kWarps ? fm_exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
 #pragma unroll
                 for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
             }
@@ -660,21 +662,21 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 if (o < dd) zh0 = fma(devt[lane * dd + o], uhS[m * 32 + o], zh0);
 #pragma unroll
                 for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + lane], fw[ww], zc);
-                z = ((zh0 + zh1) + zc / gsum) + bout[lane];
+                z = ((zh0 + zh1) + fm_div(zc, gsum)) + bout[lane];
             }
             if (lane < dd) {
                 // u (and its context half uc) for the backward
                 double uc = 0.0;
 #pragma unroll
                 for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lane], fw[ww], uc);
-                const double ucn = uc / gsum;
+                const double ucn = fm_div(uc, gsum);
                 a.act_u[row * dd + lane] = uhS[m * 32 + lane] + ucn;
                 a.act_uc[row * dd + lane] = ucn;
             }
             double zmax = z;
             for (int o = d_pow2 >> 1; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
             const double zs = z - zmax;
-            const double ez = exp(zs);  // 0 on lanes >= D
+            const double ez = lane < D ? fm_exp(zs) : 0.0;
             // numpy pairwise order over the D terms (np_sum_small), identical in every lane
             double esum;
             if (D < 8) {
@@ -692,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 esum = ((rr[0] + rr[1]) + (rr[2] + rr[3])) + ((rr[4] + rr[5]) + (rr[6] + rr[7]));
                 for (; i < D; i++) esum += __shfl_sync(0xffffffffu, ez, i);
             }
-            const double pr = ez / esum;
+            const double pr = fm_div(ez, esum);
             if (lane < D) {
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
@@ -1026,11 +1028,12 @@ struct DecPlan {
 bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
     const int T = dm.T, D = dm.D, dd = dm.dd;
     const size_t budget = 225 * 1024;
+    // M = samples per CTA, a power of two (== the kernel's MT: the per-sample
+    // loops run branch-free over all MT slots)
     int M = ceil_div(K, kNumSMs);
-    if (M < 1) M = 1;
-    if (M > 8) M = 8;
-    for (; M >= 1; M = (M > 1 ? M - 1 : 0)) {
-        const int MT = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+    M = M <= 1 ? 1 : M <= 2 ? 2 : M <= 4 ? 4 : 8;
+    for (; M >= 1; M >>= 1) {
+        const int MT = M;
         // preference: proj in smem + speculative cell, proj in smem, global proj (+spec), global
         for (int variant = 0; variant < 4; variant++) {
             // the speculative cell costs D x the gate transcendentals on 8-M warps:
