@@ -30,6 +30,7 @@
 
 #include <math.h>
 
+#include "fastmath.cuh"
 #include "policy.cuh"
 
 namespace dp {
@@ -862,7 +863,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     };
     load(T - 1, cur);
     load(T - 2, nxt);
-    double tc = tanh(cur.c);
+    double tc = fm_gate_act(cur.c, true);  // tanh (branch-free, fastmath.cuh)
 
     const bool clk_on = g_lstm_dbg && blockIdx.x == 0 && tid == 0;
     const int ci = M == 1 ? 0 : 1;
@@ -905,7 +906,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         DP_LPHASE(0);
         __syncthreads();
         DP_LPHASE(1);
-        if (live) tc = tanh(cur.c);  // independent of the mat-vec below: the two chains interleave
+        if (live) tc = fm_gate_act(cur.c, true);  // tanh; independent of the mat-vec below: the chains interleave
         // per sample: partial row sums over this lane's 8 columns, then a
         // reduce-scatter butterfly (xor 16 and 8 halve the rows, xor 4, 2, 1 sum)
         const bool hi16 = lane & 16, hi8 = lane & 8;

@@ -511,13 +511,15 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
         for (int m = 0; m < MT; m++) lmx[m] = noshift ? 0.0 : warp_max(lmx[m]);
         for (int i = tid; i < ((skip & 16) ? 0 : T); i += kThreads) {
+            double ev[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++) ev[m] = fm_exp(alS[m * a.Tpad + i] - lmx[m]);
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) {
-                    const double e = fm_exp(alS[m * a.Tpad + i] - lmx[m]);
-                    alS[m * a.Tpad + i] = e;
-                    lsm[m] += e;
-                    if (a.act_e) a.act_e[((size_t)(k0 + m) * T + t) * T + i] = e;
+                    alS[m * a.Tpad + i] = ev[m];
+                    lsm[m] += ev[m];
+                    if (a.act_e) a.act_e[((size_t)(k0 + m) * T + t) * T + i] = ev[m];
                 }
         }
 #pragma unroll
@@ -650,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             double gsum = 0.0;
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
-            if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = f / gsum;
+            if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
             double z = -INFINITY;
             if (lane < D) {
                 double zh0 = 0.0, zh1 = 0.0, zc = 0.0;
