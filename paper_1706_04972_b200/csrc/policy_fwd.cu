@@ -653,37 +653,47 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
             if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
-            double z = -INFINITY;
-            if (lane < D) {
-                double zh0 = 0.0, zh1 = 0.0, zc = 0.0;
-                int o = 0;
-                for (; o + 2 <= dd; o += 2) {
-                    zh0 = fma(devt[lane * dd + o], uhS[m * 32 + o], zh0);
-                    zh1 = fma(devt[lane * dd + o + 1], uhS[m * 32 + o + 1], zh1);
-                }
-                if (o < dd) zh0 = fma(devt[lane * dd + o], uhS[m * 32 + o], zh0);
+            // all lanes compute (clamped indices, no divergent branches: the z, uc
+            // and pcg chains interleave); lanes >= D / >= dd are masked at the end
+            const int ld = lane < D ? lane : D - 1, lo = lane < dd ? lane : dd - 1;
+            double zh0 = 0.0, zh1 = 0.0, zc = 0.0, uc = 0.0;
 #pragma unroll
-                for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + lane], fw[ww], zc);
-                z = ((zh0 + zh1) + fm_div(zc, gsum)) + bout[lane];
+            for (int o = 0; o < kMaxDD; o += 2) {
+                if (o < dd) zh0 = fma(devt[ld * dd + o], uhS[m * 32 + o], zh0);
+                if (o + 1 < dd) zh1 = fma(devt[ld * dd + o + 1], uhS[m * 32 + o + 1], zh1);
             }
-            if (lane < dd) {
-                // u (and its context half uc) for the backward
-                double uc = 0.0;
 #pragma unroll
-                for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lane], fw[ww], uc);
+            for (int ww = 0; ww < kWarps; ww++) {
+                zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
+                uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
+            }
+            const double zv = ((zh0 + zh1) + fm_div(zc, gsum)) + bout[ld];
+            const double z = lane < D ? zv : -INFINITY;
+            {
+                // u (and its context half uc) for the backward
                 const double ucn = fm_div(uc, gsum);
-                a.act_u[row * dd + lane] = uhS[m * 32 + lane] + ucn;
-                a.act_uc[row * dd + lane] = ucn;
+                if (lane < dd) {
+                    a.act_u[row * dd + lane] = uhS[m * 32 + lane] + ucn;
+                    a.act_uc[row * dd + lane] = ucn;
+                }
             }
             double zmax = z;
-            for (int o = d_pow2 >> 1; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                if (o < d_pow2) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
             const double zs = z - zmax;
-            const double ez = lane < D ? fm_exp(zs) : 0.0;
+            const double ezv = fm_exp(lane < D ? zs : -1000.0);
+            const double ez = lane < D ? ezv : 0.0;
             // numpy pairwise order over the D terms (np_sum_small), identical in every lane
             double esum;
             if (D < 8) {
+                double ev[8];
+#pragma unroll
+                for (int dv = 0; dv < 8; dv++) ev[dv] = __shfl_sync(0xffffffffu, ez, dv);
                 esum = 0.0;
-                for (int dv = 0; dv < D; dv++) esum += __shfl_sync(0xffffffffu, ez, dv);
+#pragma unroll
+                for (int dv = 0; dv < 8; dv++)
+                    if (dv < D) esum += ev[dv];
             } else {
                 double rr[8];
 #pragma unroll
@@ -707,13 +717,25 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             } else {
                 double cdf = 0.0;
                 int cnt = 0;
-                for (int dv = 0; dv < D; dv++) {
-                    cdf += __shfl_sync(0xffffffffu, pr, dv);
-                    cnt += (cdf <= r) ? 1 : 0;
+                if (D <= 8) {
+                    double pv[8];
+#pragma unroll
+                    for (int dv = 0; dv < 8; dv++) pv[dv] = __shfl_sync(0xffffffffu, pr, dv);
+#pragma unroll
+                    for (int dv = 0; dv < 8; dv++)
+                        if (dv < D) {
+                            cdf += pv[dv];
+                            cnt += (cdf <= r) ? 1 : 0;
+                        }
+                } else {
+                    for (int dv = 0; dv < D; dv++) {
+                        cdf += __shfl_sync(0xffffffffu, pr, dv);
+                        cnt += (cdf <= r) ? 1 : 0;
+                    }
                 }
                 ch = cnt < D - 1 ? cnt : D - 1;
             }
-            const double zc = __shfl_sync(0xffffffffu, zs, ch);
+            const double zsc = __shfl_sync(0xffffffffu, zs, ch);
             if (lane == 0) {
                 if (!a.forced) {
                     pcg[2 * m] = rs.hi;  // every lane has read the state by now (the cdf shuffles)
@@ -722,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 prev[(par ^ 1) * M + m] = ch;
                 a.choice[row] = (uint8_t)ch;
                 if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
-                a.act_lz[row * 2] = zc;
+                a.act_lz[row * 2] = zsc;
                 a.act_lz[row * 2 + 1] = esum;
                 // softmax stats (max, sum) for the backward's recompute of alpha
                 a.act_stat[row * 2] = gmx;
