@@ -966,6 +966,12 @@ const void *lstm_bwd_fn(int M) {
 // partial per CTA: [Hg (64 x 256) | DAsum ((D+1) x 256)]
 // thread (lb = tid>>5, jl = tid&31) owns Hg[lb*8 + a][jl + 32*b] (a, b < 8);
 // thread tid owns DAsum[:, tid].
+// h_prev^T da on the fp64 tensor cores (DMMA m8n8k4): warp w owns m-tiles
+// 2(w&3), 2(w&3)+1 (rows l of Hg) x n-tiles 16(w>>2) .. +16 (columns j);
+// tiles of 32 rows stream through a cp.async double buffer with row strides
+// == 8 (mod 32) words (conflict-free fragment loads); the advantage scales h
+// in shared memory before the products.
+constexpr int kWgHLd = kH + 4, kWgDLd = kG + 4;
 __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, int rows, int tiles_per_cta,
                                                                 const double *__restrict__ act_h,
                                                                 const double *__restrict__ enc_h,
@@ -974,36 +980,36 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
                                                                 double *__restrict__ partial,
                                                                 const double *__restrict__ adv) {
     extern __shared__ __align__(16) double sm[];
-    double *s_h = sm;                            // [2][kTile][64]   (cp.async double buffer)
-    double *s_da = s_h + 2 * kTile * kH;         // [2][kTile][256]
-    double *s_dasum = s_da + 2 * kTile * kG;     // [(D+1)][256]
+    double *s_h = sm;                              // [2][kTile][kWgHLd]   (cp.async double buffer)
+    double *s_da = s_h + 2 * kTile * kWgHLd;       // [2][kTile][kWgDLd]
+    double *s_dasum = s_da + 2 * kTile * kWgDLd;   // [(D+1)][256]
     __shared__ int s_prev[2][kTile];
-    __shared__ double s_w[2][kTile];             // per-row advantage (1 when already scaled)
-    const int tid = threadIdx.x;
+    __shared__ double s_w[2][kTile];               // per-row advantage (1 when already scaled)
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int T = dm.T, D = dm.D;
-    const int lb = tid >> 5, jl = tid & 31;
-    double acc[8][8];
+    const int mt0 = (wp & 3) * 2, nt0 = (wp >> 2) * 16;
+    double acc[2][16][2];
 #pragma unroll
-    for (int a = 0; a < 8; a++)
+    for (int a = 0; a < 2; a++)
 #pragma unroll
-        for (int b = 0; b < 8; b++) acc[a][b] = 0.0;
+        for (int n = 0; n < 16; n++) acc[a][n][0] = acc[a][n][1] = 0.0;
     for (int p = 0; p <= D; p++) s_dasum[p * kG + tid] = 0.0;
     const int n_tiles = (rows + kTile - 1) / kTile;
     const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
     // async copy of tile tl into buffer b (16-byte cp.async, zero-fill past the end)
     auto stage = [&](int tl, int b) {
         const int rb = tl * kTile;
-        double *h = s_h + b * kTile * kH, *d = s_da + b * kTile * kG;
+        double *h = s_h + b * kTile * kWgHLd, *d = s_da + b * kTile * kWgDLd;
         for (int x = tid * 2; x < kTile * kH; x += kThreads * 2) {
             const int r = x >> 6, l = x & 63, row = rb + r;
             const bool ok = row < rows;
             const double *src = enc_h + (size_t)(T - 1) * kH + l;
             if (ok && row % T > 0) src = act_h + (size_t)(row - 1) * kH + l;
-            cp_async16(h + x, src, ok);
+            cp_async16(h + r * kWgHLd + l, src, ok);
         }
         for (int x = tid * 2; x < kTile * kG; x += kThreads * 2) {
-            const int row = rb + (x >> 8);
-            cp_async16(d + x, da + (size_t)rb * kG + (row < rows ? x : 0), row < rows);
+            const int r = x >> 8, c = x & 255, row = rb + r;
+            cp_async16(d + r * kWgDLd + c, da + (size_t)rb * kG + (row < rows ? x : 0), row < rows);
         }
         if (tid < kTile) {
             const int row = rb + tid;
@@ -1025,29 +1031,37 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
             cp_async_wait<0>();
         }
         __syncthreads();
-        const double *h = s_h + b * kTile * kH, *d = s_da + b * kTile * kG;
+        double *h = s_h + b * kTile * kWgHLd;
+        const double *d = s_da + b * kTile * kWgDLd;
+        if (adv) {  // grads-only: da is unscaled -> scale h by the row's advantage
+            for (int x = tid; x < kTile * kH; x += kThreads) {
+                const int r = x >> 6, l = x & 63;
+                h[r * kWgHLd + l] *= s_w[b][r];
+            }
+            __syncthreads();
+        }
 #pragma unroll 2
-        for (int r = 0; r < kTile; r++) {
-            const double wr = s_w[b][r];  // grads-only: da is unscaled -> scale h
-            double hv[8], dv[8];
+        for (int ks = 0; ks < kTile / 4; ks++) {
+            const int r = ks * 4 + t;
+            const double a0 = h[r * kWgHLd + mt0 * 8 + g], a1 = h[r * kWgHLd + (mt0 + 1) * 8 + g];
 #pragma unroll
-            for (int a = 0; a < 8; a++) hv[a] = wr * h[r * kH + lb * 8 + a];
-#pragma unroll
-            for (int c = 0; c < 8; c++) dv[c] = d[r * kG + jl + 32 * c];
-#pragma unroll
-            for (int a = 0; a < 8; a++)
-#pragma unroll
-                for (int c = 0; c < 8; c++) acc[a][c] = fma(hv[a], dv[c], acc[a][c]);
+            for (int n = 0; n < 16; n++) {
+                const double bb = d[r * kWgDLd + (nt0 + n) * 8 + g];
+                dmma884(acc[0][n], a0, bb);
+                dmma884(acc[1][n], a1, bb);
+            }
         }
         const int nr = min(kTile, rows - rb);
-        for (int r = 0; r < nr; r++) s_dasum[s_prev[b][r] * kG + tid] += s_w[b][r] * d[r * kG + tid];
+        for (int r = 0; r < nr; r++) s_dasum[s_prev[b][r] * kG + tid] += s_w[b][r] * d[r * kWgDLd + tid];
         __syncthreads();  // buffer b is re-staged by the next iteration
     }
     const size_t base = (size_t)blockIdx.x * (kH + D + 1) * kG;
 #pragma unroll
-    for (int a = 0; a < 8; a++)
+    for (int a = 0; a < 2; a++)
 #pragma unroll
-        for (int b = 0; b < 8; b++) partial[base + (size_t)(lb * 8 + a) * kG + jl + 32 * b] = acc[a][b];
+        for (int n = 0; n < 16; n++)
+            *reinterpret_cast<double2 *>(partial + base + (size_t)((mt0 + a) * 8 + g) * kG + (nt0 + n) * 8 + 2 * t) =
+                make_double2(acc[a][n][0], acc[a][n][1]);
     for (int p = 0; p <= D; p++) partial[base + (size_t)(kH + p) * kG + tid] = s_dasum[p * kG + tid];
 }
 
@@ -1465,7 +1479,7 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
     // B3
     {
         const Grid g = tiles_grid(rows, kTile);
-        const size_t smem = sizeof(double) * ((size_t)2 * kTile * (kH + kG) + (size_t)(dm.D + 1) * kG);
+        const size_t smem = sizeof(double) * ((size_t)2 * kTile * (kWgHLd + kWgDLd) + (size_t)(dm.D + 1) * kG);
         DP_CUDA_TRY(allow_big_smem((const void *)dec_wgrad_kernel, smem));
         dec_wgrad_kernel<<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->act_h, p->enc_h, p->act_choice,
                                                            p->act_g, part, adv);
