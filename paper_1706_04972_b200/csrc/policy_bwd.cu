@@ -794,14 +794,16 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
 }
 
 // ------------------------------------------------------------------ B2 / B4
-// Sequential LSTM backward (pkg/policy.py:236-253) for M (<= 8) sequences per
-// CTA, 512 threads.  Thread (r = tid>>3, part = tid&7) keeps
-// W_h[r, 32*part : 32*part+32] in registers; dh_prev[r] = sum over the 8
-// parts (3 shuffles).  One elementwise slot (m, u) per thread.  The next
+// Sequential LSTM backward (pkg/policy.py:236-253) for M (<= 4) sequences per
+// CTA, 256 threads (8 warps: fewer barrier participants than 16 measured
+// faster).  Lane j of warp w keeps W_h[8w .. 8w+7, j + 32q] (q < 8) in
+// registers; dh_prev = W_h da by lane-parallel partial sums and a
+// reduce-scatter butterfly.  One elementwise slot (m, u) per thread.  The next
 // step's gate activations / cells / incoming dh are prefetched into registers
 // while the current step's mat-vec runs.  In place: gate activations become da.
-constexpr int kMaxSeqPerCta = 8;
-constexpr int kLstmThreads = 512;
+constexpr int kLstmThreads = 256;
+constexpr int kMaxSeqPerCta = kLstmThreads / 64;   // one elementwise slot (sample, unit) per thread
+constexpr int kRpw = kH / (kLstmThreads / 32);     // W_h rows per warp in the mat-vec
 __device__ int g_lstm_dbg = 0;            // debug-only phase clocks of lstm_bwd (block 0, thread 0)
 __device__ long long g_lstm_clk[2][4];    // [M == 1 ? 0 : 1][phase]
 // Mat-vec mapping: lane j of warp w owns gate columns {j + 32q} (q < 8) of
@@ -826,10 +828,10 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     const int tid = threadIdx.x;
     const int q0 = blockIdx.x * M;
     const int Mb = min(M, n_seq - q0);
-    const int lane = tid & 31, wrow = (tid >> 5) * 4;  // rows wrow..wrow+3, columns lane + 32q
-    double w[4][8];
+    const int lane = tid & 31, wrow = (tid >> 5) * kRpw;  // rows wrow.., columns lane + 32q
+    double w[kRpw][8];
 #pragma unroll
-    for (int rr = 0; rr < 4; rr++)
+    for (int rr = 0; rr < kRpw; rr++)
 #pragma unroll
         for (int q = 0; q < 8; q++) w[rr][q] = Wh[(size_t)(wrow + rr) * kG + lane + 32 * q];
     for (int x = tid; x < Mb * kH; x += kLstmThreads) {
@@ -908,18 +910,18 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         DP_LPHASE(1);
         if (live) tc = fm_gate_act(cur.c, true);  // tanh; independent of the mat-vec below: the chains interleave
         // per sample: partial row sums over this lane's 8 columns, then a
-        // reduce-scatter butterfly (xor 16 and 8 halve the rows, xor 4, 2, 1 sum)
-        const bool hi16 = lane & 16, hi8 = lane & 8;
+        // reduce-scatter butterfly: each xor level halves the rows a lane
+        // carries until one is left, the remaining levels sum (fixed tree)
 #pragma unroll
         for (int m = 0; m < MT; m++) {
             if (m >= Mb) break;
-            double p[4];
+            double p[kRpw];
             {
                 double dv[8];
 #pragma unroll
                 for (int q = 0; q < 8; q++) dv[q] = s_da[m * kG + lane + 32 * q];
 #pragma unroll
-                for (int rr = 0; rr < 4; rr++) {
+                for (int rr = 0; rr < kRpw; rr++) {
                     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
                     for (int q = 0; q < 8; q += 2) {
@@ -929,16 +931,26 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
                     p[rr] = a0 + a1;
                 }
             }
-            const double s0 = hi16 ? p[0] : p[2], s1 = hi16 ? p[1] : p[3];
-            const double k0 = hi16 ? p[2] : p[0], k1 = hi16 ? p[3] : p[1];
-            const double q0v = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
-            const double q1v = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
-            double v = (hi8 ? q1v : q0v) + __shfl_xor_sync(0xffffffffu, hi8 ? q0v : q1v, 8);
-            v += __shfl_xor_sync(0xffffffffu, v, 4);
-            v += __shfl_xor_sync(0xffffffffu, v, 2);
-            v += __shfl_xor_sync(0xffffffffu, v, 1);
-            // lane (hi16, hi8, 0) holds row wrow + 2*hi16 + hi8
-            if ((lane & 7) == 0) s_dh[m * kH + wrow + (hi16 ? 2 : 0) + (hi8 ? 1 : 0)] = v;
+            int rbase = 0;
+#pragma unroll
+            for (int o = 16, cnt = kRpw; o >= 1; o >>= 1) {
+                const bool hi = lane & o;
+                if (cnt > 1) {
+                    const int half = cnt / 2;
+#pragma unroll
+                    for (int i2 = 0; i2 < kRpw / 2; i2++)
+                        if (i2 < half) {
+                            const double send = hi ? p[i2] : p[i2 + half];
+                            const double keep = hi ? p[i2 + half] : p[i2];
+                            p[i2] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                        }
+                    rbase += hi ? half : 0;
+                    cnt = half;
+                } else {
+                    p[0] += __shfl_xor_sync(0xffffffffu, p[0], o);
+                }
+            }
+            if ((lane & (32 / kRpw - 1)) == 0) s_dh[m * kH + wrow + rbase] = p[0];
         }
         DP_LPHASE(2);
         __syncthreads();
@@ -956,10 +968,10 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
 }
 
 const void *lstm_bwd_fn(int M) {
+    static_assert(kMaxSeqPerCta == 4, "lstm_bwd_fn instantiates MT <= 4");
     return M <= 1 ? (const void *)lstm_bwd_kernel<1>
            : M <= 2 ? (const void *)lstm_bwd_kernel<2>
-           : M <= 4 ? (const void *)lstm_bwd_kernel<4>
-                    : (const void *)lstm_bwd_kernel<8>;
+                    : (const void *)lstm_bwd_kernel<4>;
 }
 
 // ------------------------------------------------------------------ B3
