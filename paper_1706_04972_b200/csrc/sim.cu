@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
 // updates are executed redundantly by every lane (broadcast reads) with lane 0
 // writing.  Same event semantics and fp64 operation order as sim_kernel
 // (SURVEY.md Appendix A.2): bit-identical outputs, dispatch order included.
-constexpr int kSimWarps = 4;
+constexpr int kSimWarps = 16;  // max warps per CTA (placements sharing one staged graph)
 
 __host__ __device__ inline size_t warp_slot_bytes(int n, int d) {
     size_t b = (size_t)n * 8 + (size_t)d * d * 8;  // maxarr, link_free
@@ -873,9 +873,18 @@ template <bool GS>
 static int launch_sim_warp(const dp_graph *g, int K, size_t gb, cudaStream_t st, const uint8_t *placement,
                            int by_rank, double *makespan, double *busy, double *transfer, int64_t *peak,
                            uint8_t *feasible, int32_t *order, uint8_t *err) {
-    // with the graph staged, 4 warps share one copy; otherwise 1-warp CTAs
-    // (more resident placements per SM for large graphs)
-    const int W = GS ? kSimWarps : 1;
+    // With the graph staged, up to 16 warps share one copy and the batch is
+    // packed onto <= ~20 SMs: in the training step the scorer runs beside the
+    // attention backward, whose 1-CTA-per-SM tiles leave 20 SMs free
+    // (att_grid) — a scorer CTA on any other SM would block one of them.
+    // Without staging (large graphs): 1-warp CTAs, more resident per SM.
+    int W = 1;
+    if (GS) {
+        W = dp::ceil_div(K, 20);
+        W = W < 4 ? 4 : W > kSimWarps ? kSimWarps : W;
+        const size_t per = warp_slot_bytes(g->n, g->d);
+        while (W > 1 && per * W + gb + 16 > kSmemBudget) W--;
+    }
     const size_t smem = warp_slot_bytes(g->n, g->d) * W + (GS ? gb : 0) + 16;
     if (smem > 48 * 1024) DP_CUDA_TRY(dp::allow_big_smem((const void *)sim_warp_kernel<GS>, smem));
     sim_warp_kernel<GS><<<dp::ceil_div(K, W), 32 * W, smem, st>>>(
@@ -893,7 +902,7 @@ extern "C" int dp_simulate_batch(const dp_graph *g, int32_t K, const uint8_t *pl
     if (K == 0) return DP_OK;
     {
         const size_t gb = graph_smem_bytes(g->n, g->d, g->e);
-        const size_t ws = warp_slot_bytes(g->n, g->d) * kSimWarps;
+        const size_t ws = warp_slot_bytes(g->n, g->d) * 4;
         const bool fits_gs = gb + ws + 16 <= kSmemBudget;
         const bool fits = warp_slot_bytes(g->n, g->d) + 16 <= kSmemBudget;
         const bool want = g_sim_variant == 1 || (g_sim_variant == 0 && sim_warp_preferred(g, K));
