@@ -42,6 +42,7 @@ constexpr int kTile = 32;   // rows per tile (B0, B1, B3)
 // advantage-independent per-row half (runs concurrently with the simulator);
 // kGradsOnly = the advantage-weighted cross-row sums.
 constexpr int kFused = 0, kRowsOnly = 1, kGradsOnly = 2;
+constexpr int kFusedGrads = 3;  // B1f in the fused pass: grads only, rows already scaled (att_bwd did dh_ext)
 constexpr int kFinTile = 64;
 constexpr int kChunk = 64;  // B1: enc rows per chunk
 constexpr int kPad = 65;
@@ -445,7 +446,8 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     double *__restrict__ partial, double *__restrict__ partA,
     double *__restrict__ tile_partial /* [units][T][64] or NULL */,
     double *__restrict__ tile_partA /* [units][T][dd] */, const double *__restrict__ act_e,
-    const double *__restrict__ act_esc, int do_denc, int per_sample /* partials per sample, not per tile */) {
+    const double *__restrict__ act_esc, int do_denc, int per_sample /* partials per sample, not per tile */,
+    const double *__restrict__ w_att, double *__restrict__ row_dhx /* dh_ext += dq W_att^T (B1f rows part) */) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -623,6 +625,33 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             for (int n = 0; n < 8; n++)
                 *reinterpret_cast<double2 *>(row_dq + (size_t)(rb + mr) * kH + n * 8 + 2 * t) =
                     make_double2(dq[n][0], dq[n][1]);
+        // B1f rows part fused here: dh_ext[r, l] += sum_j dq[r, j] W_att[l, j]
+        // (dq -> S.q, W_att -> S.al: both free once the chunks are done)
+        for (int x = tid; x < kH * kH; x += kThreads) S.al[(x >> 6) * kPadH + (x & 63)] = w_att[x];
+#pragma unroll
+        for (int n = 0; n < 8; n++) {
+            S.q[mr * kPadH + n * 8 + 2 * t] = dq[n][0];
+            S.q[mr * kPadH + n * 8 + 2 * t + 1] = dq[n][1];
+        }
+        __syncthreads();
+        {
+            double o[8][2];
+#pragma unroll
+            for (int n = 0; n < 8; n++) o[n][0] = o[n][1] = 0.0;
+#pragma unroll 2
+            for (int ks = 0; ks < kH / 4; ks++) {
+                const double a = S.q[mr * kPadH + ks * 4 + t];
+#pragma unroll
+                for (int n = 0; n < 8; n++) dmma884(o[n], a, S.al[(n * 8 + g) * kPadH + ks * 4 + t]);
+            }
+            if (rok)
+#pragma unroll
+                for (int n = 0; n < 8; n++) {
+                    double2 *dst = reinterpret_cast<double2 *>(row_dhx + (size_t)(rb + mr) * kH + n * 8 + 2 * t);
+                    const double2 v = *dst;
+                    *dst = make_double2(v.x + o[n][0], v.y + o[n][1]);
+                }
+        }
         first_cta_tile = false;
     }
 }
@@ -721,7 +750,7 @@ __global__ void __launch_bounds__(kThreads) row_fin_kernel(PolicyDims dm, const 
     extern __shared__ __align__(16) double smraw[];
     FinSmem &S = *reinterpret_cast<FinSmem *>(smraw);
     const int tid = threadIdx.x;
-    const bool rows_out = mode != kGradsOnly, grads_out = mode != kRowsOnly;
+    const bool rows_out = mode == kFused || mode == kRowsOnly, grads_out = mode != kRowsOnly;
     const int T = dm.T;
     for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPad + (x & 63)] = P[dm.off.w_att + x];
     const int rb4 = tid >> 4, lb = tid & 15;  // out micro-tile: r in {rb4+16a}, l in {lb+16b}
@@ -1116,27 +1145,36 @@ inline void launch_reduce(const double *src, int n_cta, size_t stride, int n, do
 
 // B3 finalize: b_dec = sum_p DAsum[p]; w_dec[:dd] = sum_p dev_table[p] x DAsum[p];
 // dev_table[p] += W_dec[:dd] . DAsum[p]
-__global__ void dec_finalize_kernel(PolicyDims dm, const double *__restrict__ P, const double *__restrict__ dasum,
-                                    double *__restrict__ grad) {
-    const int tid = threadIdx.x;  // 256 threads: gate column
+// Block 0: thread per gate column (b_dec, w_dec[:dd]); blocks >= 1: one warp
+// per dev_table output (p, i), lanes split the 256 gates, fixed butterfly.
+__global__ void __launch_bounds__(kG) dec_finalize_kernel(PolicyDims dm, const double *__restrict__ P,
+                                                          const double *__restrict__ dasum,
+                                                          double *__restrict__ grad) {
+    const int tid = threadIdx.x;
     const int D = dm.D, dd = dm.dd;
-    double b = 0.0;
-    for (int p = 0; p <= D; p++) b += dasum[p * kG + tid];
-    grad[dm.off.b_dec + tid] = b;
-    for (int i = 0; i < dd; i++) {
-        double v = 0.0;
-        for (int p = 0; p <= D; p++) v = fma(P[dm.off.dev_table + p * dd + i], dasum[p * kG + tid], v);
-        grad[dm.off.w_dec + (size_t)i * kG + tid] = v;
-    }
-    for (int x = tid; x < (D + 1) * dd; x += blockDim.x) {
-        const int p = x / dd, i = x % dd;
-        double v0 = 0.0, v1 = 0.0;
-        for (int j = 0; j < kG; j += 2) {
-            v0 = fma(P[dm.off.w_dec + (size_t)i * kG + j], dasum[p * kG + j], v0);
-            v1 = fma(P[dm.off.w_dec + (size_t)i * kG + j + 1], dasum[p * kG + j + 1], v1);
+    if (blockIdx.x == 0) {
+        double b = 0.0;
+        for (int p = 0; p <= D; p++) b += dasum[p * kG + tid];
+        grad[dm.off.b_dec + tid] = b;
+        for (int i = 0; i < dd; i++) {
+            double v = 0.0;
+            for (int p = 0; p <= D; p++) v = fma(P[dm.off.dev_table + p * dd + i], dasum[p * kG + tid], v);
+            grad[dm.off.w_dec + (size_t)i * kG + tid] = v;
         }
-        grad[dm.off.dev_table + x] += v0 + v1;
+        return;
     }
+    const int x = (blockIdx.x - 1) * (kG / 32) + (tid >> 5), lane = tid & 31;
+    if (x >= (D + 1) * dd) return;
+    const int p = x / dd, i = x - p * dd;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kG / 32; q++) {
+        const int j = lane + 32 * q;
+        v = fma(P[dm.off.w_dec + (size_t)i * kG + j], dasum[p * kG + j], v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) grad[dm.off.dev_table + x] += v;
 }
 
 // sum over samples of the decoder's dh/dc at step 0 -> encoder final state grads
@@ -1325,8 +1363,8 @@ Grid att_grid(int K, int T) {
     return {ceil_div(n_tiles, per), per};
 }
 
-int launch_att(dp_policy *p, const Grid &g, size_t smem, int rows, double *tile_part, double *tile_partA,
-               cudaStream_t st) {
+int launch_att(dp_policy *p, const double *params, const Grid &g, size_t smem, int rows, double *tile_part,
+               double *tile_partA, cudaStream_t st) {
     const PolicyDims &dm = p->dims;
     const int tps = (dm.T + kAttTile - 1) / kAttTile;
     const int per_sample = tile_part && g.per % tps == 0 ? 1 : 0;
@@ -1336,13 +1374,13 @@ int launch_att(dp_policy *p, const Grid &g, size_t smem, int rows, double *tile_
         att_bwd_kernel<true><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
                                                                p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
                                                                p->partA, tile_part, tile_partA, p->act_e, p->act_esc, 1,
-                                                               per_sample);
+                                                               per_sample, params + p->dims.off.w_att, p->row_dhx);
     } else {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<false>, smem));
         att_bwd_kernel<false><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
                                                                 p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
                                                                 p->partA, tile_part, tile_partA, nullptr, nullptr, 1,
-                                                                per_sample);
+                                                                per_sample, params + p->dims.off.w_att, p->row_dhx);
     }
     DP_LAUNCH_CHECK();
     return DP_OK;
@@ -1501,7 +1539,7 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         DP_LAUNCH_CHECK();
         launch_reduce(part + (size_t)kH * kG, g.n_used, stride, (dm.D + 1) * kG, p->gacc, 0, st);
         DP_LAUNCH_CHECK();
-        dec_finalize_kernel<<<1, kG, 0, st>>>(dm, params, p->gacc, grad);
+        dec_finalize_kernel<<<1 + ceil_div((dm.D + 1) * dm.dd, kG / 32), kG, 0, st>>>(dm, params, p->gacc, grad);
         DP_LAUNCH_CHECK();
     }
     DP_CUDA_TRY(cudaStreamWaitEvent(st, p->ev_join, 0));
@@ -1531,14 +1569,14 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     {
         const Grid g = att_grid(K, T);
         const size_t smem = sizeof(AttSmem);
-        DP_TRY(launch_att(p, g, smem, rows, nullptr, nullptr, st));
+        DP_TRY(launch_att(p, params, g, smem, rows, nullptr, nullptr, st));
         launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
         DP_LAUNCH_CHECK();
         launch_reduce(p->partA, g.n_used, (size_t)T * dm.dd, T * dm.dd, p->a_tot, 0, st);
         DP_LAUNCH_CHECK();
         DP_TRY(run_att_fin(p, params, grad, st));
     }
-    DP_TRY(run_b1f(p, params, rows, nullptr, grad, kFused, st));
+    DP_TRY(run_b1f(p, params, rows, nullptr, grad, kFusedGrads, st));
     DP_TRY(run_b2(p, params, K, st));
     return run_b345(p, params, K, nullptr, grad, st);
 }
@@ -1559,9 +1597,8 @@ extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32
     {
         const Grid g = att_grid(K, dm.T);
         const size_t smem = sizeof(AttSmem);
-        DP_TRY(launch_att(p, g, smem, rows, p->tile_part, p->tile_partA, st));
+        DP_TRY(launch_att(p, params, g, smem, rows, p->tile_part, p->tile_partA, st));
     }
-    DP_TRY(run_b1f(p, params, rows, nullptr, nullptr, kRowsOnly, st));
     DP_TRY(run_b2(p, params, K, st));
     p->rows_ready = K;
     return DP_OK;
