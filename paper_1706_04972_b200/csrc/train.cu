@@ -21,26 +21,58 @@
 namespace dp {
 namespace {
 
-// numpy pairwise_sum (np.add.reduce / np.mean on a contiguous float64 array)
-__device__ double np_pairwise(const double *a, int n) {
+// numpy pairwise_sum (np.add.reduce / np.mean on a contiguous float64 array):
+// blocks of <= 128 summed with 8 interleaved accumulators, larger ranges split
+// at n/2 rounded down to a multiple of 8 — restated with an explicit stack
+// (device recursion overflowed the default thread stack at K = 4096).
+__device__ double np_pairwise_leaf(const double *a, int n) {
     if (n < 8) {
         double r = 0.0;
         for (int i = 0; i < n; i++) r += a[i];
         return r;
     }
-    if (n <= 128) {
-        double r[8];
-        for (int j = 0; j < 8; j++) r[j] = a[j];
-        int i = 8;
-        for (; i < n - (n % 8); i += 8)
-            for (int j = 0; j < 8; j++) r[j] += a[i + j];
-        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-        for (; i < n; i++) res += a[i];
-        return res;
+    double r[8];
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; j++) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; i++) res += a[i];
+    return res;
+}
+
+__device__ double np_pairwise(const double *a, int n) {
+    constexpr int kDepth = 32;
+    int off[kDepth], len[kDepth], stage[kDepth];
+    double left[kDepth];
+    int sp = 0;
+    off[0] = 0;
+    len[0] = n;
+    stage[0] = 0;
+    double ret = 0.0;
+    for (;;) {
+        const int m = len[sp];
+        if (m <= 128 || stage[sp] == 2) {
+            ret = m <= 128 ? np_pairwise_leaf(a + off[sp], m) : left[sp] + ret;
+            if (sp == 0) return ret;
+            sp--;
+            continue;
+        }
+        int n2 = m / 2;
+        n2 -= n2 % 8;
+        if (stage[sp] == 0) {
+            stage[sp] = 1;
+            off[sp + 1] = off[sp];
+            len[sp + 1] = n2;
+        } else {  // left half done
+            left[sp] = ret;
+            stage[sp] = 2;
+            off[sp + 1] = off[sp] + n2;
+            len[sp + 1] = m - n2;
+        }
+        sp++;
+        stage[sp] = 0;
     }
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
 }
 
 // single CTA; thread 0 runs the order-dependent scalar logic, the block copies

@@ -99,3 +99,24 @@ def test_train_with_measurement_noise_matches_reference(name, graph):
     assert rel < 1e-12
     if len(g["best_placement"]):
         assert res.best_placement == [int(x) for x in g["best_placement"]]
+
+
+@pytest.mark.parametrize("K", [300, 4096])
+def test_epilogue_pairwise_mean_large_k(K):
+    """mean_R over K > 128 rewards follows numpy's recursive pairwise sum
+    (restated iteratively on device) — byte-equal to np.mean."""
+    import math
+
+    gg, topo, _, _ = cfg("C1")
+    c = dp.TrainerConfig(k=K, total_updates=1, seed=2)
+    task = dp.trainer._make_task(gg, topo, c)
+    store = dp.ParameterStore(task.template.to_flat(), max_steps=4)
+    ctl = dp.trainer.DeviceController(task, store, np.random.SeedSequence(2).spawn(1)[0], 0)
+    ctl.run(1, use_graph=False)
+    torch.cuda.synchronize()
+    row = ctl.rows()[0]
+    out = ctl.dg.simulate(ctl.choice, by_rank=True)
+    mk, fe = out["makespan"].cpu().numpy(), out["feasible"].cpu().numpy()
+    fail = task.reward_spec.failing_signal
+    rewards = [math.sqrt(m) if f else fail for m, f in zip(mk, fe)]
+    assert row.mean_r == float(np.mean(rewards))
