@@ -628,6 +628,38 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         __syncthreads();
         DP_PHASE(1);
         // ---- E: combine, logits, softmax over devices, draw (policy.py:297-308, 320-323) ----
+        // warp m < Mb runs sample m's draw chain; when there are spare warps, warp
+        // Mb + m does the sample's off-chain stores (u, uc, the alpha scales)
+        const bool split = 2 * Mb <= kWarps;
+        if (split && warp >= Mb && warp < 2 * Mb) {
+            const int m = warp - Mb;
+            const size_t row = (size_t)(k0 + m) * T + t;
+            double gmx = 0.0, f = lane < kWarps ? 1.0 : 0.0;
+            double fw[kWarps];
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) fw[ww] = 1.0;
+            if (!noshift) {
+                gmx = pmx[m];
+#pragma unroll
+                for (int ww = 1; ww < kWarps; ww++) gmx = fmax(gmx, pmx[ww * M + m]);
+                f = lane < kWarps ? fm_exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
+            }
+            double gsum = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
+            if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
+            const int lo = lane < dd ? lane : dd - 1;
+            double uc = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
+            const double ucn = fm_div(uc, gsum);
+            if (lane < dd) {
+                a.act_u[row * dd + lane] = uhS[m * 32 + lane] + ucn;
+                a.act_uc[row * dd + lane] = ucn;
+            }
+        }
         for (int m = warp; m < Mb; m += kWarps) {
             const size_t row = (size_t)(k0 + m) * T + t;
             // next uniform (every lane steps the same PCG64 state; lane 0 keeps it)
@@ -652,25 +684,40 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             double gsum = 0.0;
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
-            if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
+            if (!split && a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
             // all lanes compute (clamped indices, no divergent branches: the z, uc
             // and pcg chains interleave); lanes >= D / >= dd are masked at the end
             const int ld = lane < D ? lane : D - 1, lo = lane < dd ? lane : dd - 1;
-            double zh0 = 0.0, zh1 = 0.0, zc = 0.0, uc = 0.0;
-#pragma unroll
-            for (int o = 0; o < kMaxDD; o += 2) {
+            double zh;
+            if (D <= 4 && dd <= 16) {
+                // lanes (d = lane / 8, part = lane % 8): 2 terms each + a 3-level butterfly
+                const int dz = min(lane >> 3, D - 1), op = lane & 7;
+                double v = op < dd ? devt[dz * dd + op] * uhS[m * 32 + op] : 0.0;
+                if (op + 8 < dd) v = fma(devt[dz * dd + op + 8], uhS[m * 32 + op + 8], v);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                zh = __shfl_sync(0xffffffffu, v, ld * 8);
+            } else {
+                double zh0 = 0.0, zh1 = 0.0;
+                int o = 0;
+                for (; o + 2 <= dd; o += 2) {
+                    zh0 = fma(devt[ld * dd + o], uhS[m * 32 + o], zh0);
+                    zh1 = fma(devt[ld * dd + o + 1], uhS[m * 32 + o + 1], zh1);
+                }
                 if (o < dd) zh0 = fma(devt[ld * dd + o], uhS[m * 32 + o], zh0);
-                if (o + 1 < dd) zh1 = fma(devt[ld * dd + o + 1], uhS[m * 32 + o + 1], zh1);
+                zh = zh0 + zh1;
             }
+            double zc = 0.0;
 #pragma unroll
-            for (int ww = 0; ww < kWarps; ww++) {
-                zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
-                uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
-            }
-            const double zv = ((zh0 + zh1) + fm_div(zc, gsum)) + bout[ld];
+            for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
+            const double zv = (zh + fm_div(zc, gsum)) + bout[ld];
             const double z = lane < D ? zv : -INFINITY;
-            {
+            if (!split) {
                 // u (and its context half uc) for the backward
+                double uc = 0.0;
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
                 const double ucn = fm_div(uc, gsum);
                 if (lane < dd) {
                     a.act_u[row * dd + lane] = uhS[m * 32 + lane] + ucn;
