@@ -565,8 +565,12 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     psm[warp * M + m] = lsm[m];
                 }
         }
+        // fast E (D <= 4, dd <= 16, spare warps): the draw warp forms the logits'
+        // context half as dev_table . (sum_w uc_w) itself -> no pz partials here
+        const bool fastE = D <= 4 && dd <= 16 && 2 * Mb <= kWarps;
         // pz_w[m][d] = dev_table[d] . uc_w[m]
-        if (dd == 16 && Mb <= 2) {
+        if (fastE) {
+        } else if (dd == 16 && Mb <= 2) {
             // lanes (m, j) hold uc_w[m][j]: per device, a 16-lane butterfly sum
             const int m = lane >> 4, j = lane & 15;
             for (int d0 = 0; d0 < ((skip & 2) ? 0 : D); d0 += 4) {
@@ -655,8 +659,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
             const double ucn = fm_div(uc, gsum);
+            const double uh = uhS[m * 32 + lo];
             if (lane < dd) {
-                a.act_u[row * dd + lane] = uhS[m * 32 + lane] + ucn;
+                a.act_u[row * dd + lane] = uh + ucn;
                 a.act_uc[row * dd + lane] = ucn;
             }
         }
@@ -688,8 +693,27 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             // all lanes compute (clamped indices, no divergent branches: the z, uc
             // and pcg chains interleave); lanes >= D / >= dd are masked at the end
             const int ld = lane < D ? lane : D - 1, lo = lane < dd ? lane : dd - 1;
-            double zh;
-            if (D <= 4 && dd <= 16) {
+            double zh, zcd = 0.0;
+            if (fastE) {
+                // lanes (d = lane / 8, part = lane % 8): dev_table[d] . uh and
+                // dev_table[d] . sum_w uc_w (2 terms each), 3-level butterflies
+                const int dz = min(lane >> 3, D - 1), op = lane & 7;
+                double v = op < dd ? devt[dz * dd + op] * uhS[m * 32 + op] : 0.0;
+                if (op + 8 < dd) v = fma(devt[dz * dd + op + 8], uhS[m * 32 + op + 8], v);
+                double ucr = 0.0;  // lane j < dd: sum_w fw[w] uc_w[j]
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ww++) ucr = fma(puc[(ww * M + m) * dd + lo], fw[ww], ucr);
+                const double ua = __shfl_sync(0xffffffffu, ucr, op), ub = __shfl_sync(0xffffffffu, ucr, op + 8);
+                double c = op < dd ? devt[dz * dd + op] * ua : 0.0;
+                if (op + 8 < dd) c = fma(devt[dz * dd + op + 8], ub, c);
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    v += __shfl_xor_sync(0xffffffffu, v, o);
+                    c += __shfl_xor_sync(0xffffffffu, c, o);
+                }
+                zh = __shfl_sync(0xffffffffu, v, ld * 8);
+                zcd = __shfl_sync(0xffffffffu, c, ld * 8);
+            } else if (D <= 4 && dd <= 16) {
                 // lanes (d = lane / 8, part = lane % 8): 2 terms each + a 3-level butterfly
                 const int dz = min(lane >> 3, D - 1), op = lane & 7;
                 double v = op < dd ? devt[dz * dd + op] * uhS[m * 32 + op] : 0.0;
@@ -708,9 +732,10 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 if (o < dd) zh0 = fma(devt[ld * dd + o], uhS[m * 32 + o], zh0);
                 zh = zh0 + zh1;
             }
-            double zc = 0.0;
+            double zc = zcd;
+            if (!fastE)
 #pragma unroll
-            for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
+                for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
             const double zv = (zh + fm_div(zc, gsum)) + bout[ld];
             const double z = lane < D ? zv : -INFINITY;
             if (!split) {
