@@ -46,6 +46,7 @@ struct dp_policy {
     double *act_uc;       // [k*T*dd] ctx @ W_out[64:] (the context enters u, and the backward, only through it)
     double *proj, *encW;  // [T*64] enc @ W_att^T, [T*dd] enc @ W_out[64:] (decoder prologue, per snapshot)
     unsigned long long *proj_nmax;  // max_t ||proj_t|| (IEEE bits): the decoder's no-shift softmax test
+    double *vdev;                   // [64*D] W_out[:64] @ dev_table[:D]^T (logits' h half)
     double *act_e;        // [k*T][T] attention numerators e_i = exp(s_i - m_w) (NULL: the backward recomputes)
     double *act_esc;      // [k*T][8] per-warp-slice scale exp(m_w - M) / sum: alpha_i = e_i * esc[(i % 256) / 32]
     double *act_lz;       // [k*T*2] (zs[choice], sum exp zs) -> log-prob terms off the critical path

@@ -182,13 +182,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 // rounding (the shift cancels exactly in real arithmetic).
 constexpr double kNoShiftBound = 600.0;
 
+// Block 0 also forms vdev = W_out[:64] @ dev_table[:D]^T [64][D]: the logits'
+// h half becomes one 64-term dot per device (zh_d = h . vdev[:, d]).
 __global__ void dec_prep_kernel(PolicyDims dm, const double *__restrict__ params, const double *__restrict__ enc_h,
                                 double *__restrict__ proj, double *__restrict__ encW,
-                                unsigned long long *__restrict__ proj_nmax) {
+                                unsigned long long *__restrict__ proj_nmax, double *__restrict__ vdev) {
     __shared__ double e[kH];
     __shared__ double sq[kH];
     const int t = blockIdx.x, tid = threadIdx.x, dd = dm.dd;
     if (tid < kH) e[tid] = enc_h[(size_t)t * kH + tid];
+    if (t == 0)
+        for (int x = tid; x < kH * dm.D; x += blockDim.x) {
+            const int l = x / dm.D, d = x - l * dm.D;
+            double v = 0.0;
+            for (int o = 0; o < dd; o++)
+                v = fma(params[dm.off.w_out + (size_t)l * dd + o], params[dm.off.dev_table + (size_t)d * dd + o], v);
+            vdev[x] = v;
+        }
     __syncthreads();
     double a0 = 0.0, a1 = 0.0;
     if (tid < kH) {
@@ -232,13 +242,14 @@ struct DecArgs {
     const uint8_t *forced;
     const double *enc_h, *enc_c, *edev, *proj, *encW;
     const unsigned long long *proj_nmax;
+    const double *vdev;
     double *act_h, *act_c, *act_g, *act_uc, *act_u, *act_p, *act_stat, *act_lz, *act_e, *act_esc;
     uint8_t *choice, *choice_out;
     double *logp, *probs_out;
     int M, Tpad, ewld;
     // shared-memory offsets (doubles)
     int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_uh, o_alpha, o_pm, o_ps, o_puc, o_pz, o_gn, o_hc,
-        o_cc, o_ac, o_pcg, o_misc;
+        o_cc, o_ac, o_pcg, o_misc, o_v, o_wo;
 };
 
 // q = x / n for 0 <= x < MT * n without an integer division (MT <= 8)
@@ -317,6 +328,10 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     }
     for (int i = tid; i < kH * dd; i += kThreads) wout1[(i % dd) * kWout1Ld + i / dd] = P[dm.off.w_out + i];
     for (int i = tid; i < D * dd; i += kThreads) devt[i] = P[dm.off.dev_table + i];
+    double *vS = sm + a.o_v;    // vdev [64][D]
+    double *woS = sm + a.o_wo;  // W_out[:64] [64][dd] (row-major: lanes o read consecutive words)
+    for (int i = tid; i < kH * D; i += kThreads) vS[i] = a.vdev[i];
+    for (int i = tid; i < kH * dd; i += kThreads) woS[i] = P[dm.off.w_out + i];
     for (int i = tid; i < D; i += kThreads) bout[i] = P[dm.off.b_out + i];
     if (!SPEC)
         for (int i = tid; i < (D + 1) * kG; i += kThreads) edevS[i] = a.edev[i];
@@ -565,8 +580,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     psm[warp * M + m] = lsm[m];
                 }
         }
-        // fast E (D <= 4, dd <= 16, spare warps): the draw warp forms the logits'
-        // context half as dev_table . (sum_w uc_w) itself -> no pz partials here
+        // fast E (D <= 4, dd <= 16, spare warps): the draw warp forms the logits
+        // itself (h . vdev + dev_table . sum_w uc_w) -> no pz partials, no uh here
         const bool fastE = D <= 4 && dd <= 16 && 2 * Mb <= kWarps;
         // pz_w[m][d] = dev_table[d] . uc_w[m]
         if (fastE) {
@@ -602,7 +617,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
         }
         // uh = h @ W_out[:64] (policy.py:302, h half), 8 lanes per output
-        {
+        // (fast E: the spare warps form it during E, off the draw chain)
+        if (!fastE) {
             const int total = (skip & 4) ? 0 : Mb * dd * 8;
             for (int b0 = 0; b0 < total; b0 += kThreads) {
                 const int idx = b0 + tid;
@@ -659,7 +675,24 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
             const double ucn = fm_div(uc, gsum);
-            const double uh = uhS[m * 32 + lo];
+            double uh;
+            if (fastE) {
+                // uh[o] = h . W_out[:64, o]: lanes (o, half) sum 32 terms each
+                const double *hv = (SPEC ? hC + (m * D + prv[m]) * kH : hS + m * kH) + (lane >> 4) * 32;
+                const double *wc = woS + (lane >> 4) * 32 * dd + ((lane & 15) < dd ? (lane & 15) : dd - 1);
+                double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+#pragma unroll
+                for (int l = 0; l < 32; l += 4) {
+                    u0 = fma(hv[l], wc[l * dd], u0);
+                    u1 = fma(hv[l + 1], wc[(l + 1) * dd], u1);
+                    u2 = fma(hv[l + 2], wc[(l + 2) * dd], u2);
+                    u3 = fma(hv[l + 3], wc[(l + 3) * dd], u3);
+                }
+                const double part = (u0 + u1) + (u2 + u3);
+                uh = part + __shfl_xor_sync(0xffffffffu, part, 16);
+            } else {
+                uh = uhS[m * 32 + lo];
+            }
             if (lane < dd) {
                 a.act_u[row * dd + lane] = uh + ucn;
                 a.act_uc[row * dd + lane] = ucn;
@@ -695,11 +728,17 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             const int ld = lane < D ? lane : D - 1, lo = lane < dd ? lane : dd - 1;
             double zh, zcd = 0.0;
             if (fastE) {
-                // lanes (d = lane / 8, part = lane % 8): dev_table[d] . uh and
-                // dev_table[d] . sum_w uc_w (2 terms each), 3-level butterflies
+                // lanes (d = lane / 8, part = lane % 8): h . vdev[:, d] (8 terms each)
+                // and dev_table[d] . sum_w uc_w (2 terms each), 3-level butterflies
                 const int dz = min(lane >> 3, D - 1), op = lane & 7;
-                double v = op < dd ? devt[dz * dd + op] * uhS[m * 32 + op] : 0.0;
-                if (op + 8 < dd) v = fma(devt[dz * dd + op + 8], uhS[m * 32 + op + 8], v);
+                const double *hv = SPEC ? hC + (m * D + prv[m]) * kH : hS + m * kH;
+                double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+                for (int y = 0; y < 8; y += 2) {
+                    v0 = fma(hv[op + 8 * y], vS[(op + 8 * y) * D + dz], v0);
+                    v1 = fma(hv[op + 8 * y + 8], vS[(op + 8 * y + 8) * D + dz], v1);
+                }
+                double v = v0 + v1;
                 double ucr = 0.0;  // lane j < dd: sum_w fw[w] uc_w[j]
 #pragma unroll
                 for (int ww = 0; ww < kWarps; ww++) ucr = fma(puc[(ww * M + m) * dd + lo], fw[ww], ucr);
@@ -907,7 +946,7 @@ static ParamLayout layout_of(int V1, int D, int dd, int F, int td) {
 extern "C" void dp_policy_destroy(dp_policy *p) {
     if (!p) return;
     void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->occ_val, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
-                    p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->proj_nmax, p->act_u, p->act_p,
+                    p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->proj_nmax, p->vdev, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
                     p->tile_part, p->tile_partA, p->partA, p->a_tot, p->act_e, p->act_esc};
@@ -1002,6 +1041,7 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     alloc((void **)&p->proj, sizeof(double) * T * kH);
     alloc((void **)&p->encW, sizeof(double) * T * dev_dim);
     alloc((void **)&p->proj_nmax, sizeof(unsigned long long));
+    alloc((void **)&p->vdev, sizeof(double) * kH * n_dev);
     alloc((void **)&p->act_u, sizeof(double) * rows * dev_dim);
     alloc((void **)&p->act_p, sizeof(double) * rows * n_dev);
     alloc((void **)&p->act_stat, sizeof(double) * rows * 2);
@@ -1109,7 +1149,7 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
     enc_rec_kernel<<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
     DP_LAUNCH_CHECK();
     DP_CUDA_TRY(cudaMemsetAsync(p->proj_nmax, 0, sizeof(unsigned long long), st));
-    dec_prep_kernel<<<dm.T, 128, 0, st>>>(dm, params, p->enc_h, p->proj, p->encW, p->proj_nmax);
+    dec_prep_kernel<<<dm.T, 128, 0, st>>>(dm, params, p->enc_h, p->proj, p->encW, p->proj_nmax, p->vdev);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
@@ -1164,6 +1204,8 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             a.o_ac = spec ? take(M * D * kG) : 0;
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + 2 * M);
+            a.o_v = take(kH * D);
+            a.o_wo = take(kH * dd);
             const size_t bytes = (size_t)o * sizeof(double);
             if (bytes <= budget) {
                 pl.M = M;
@@ -1227,6 +1269,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.proj = p->proj;
     a.encW = p->encW;
     a.proj_nmax = p->proj_nmax;
+    a.vdev = p->vdev;
     a.act_h = p->act_h;
     a.act_c = p->act_c;
     a.act_g = p->act_g;
