@@ -130,28 +130,66 @@ __device__ __forceinline__ double dot64_sh_reg(const double *__restrict__ hs, co
 }
 
 // ---------------------------------------------------------------- encoder
-// One CTA, 256 threads: thread (u, gate) = (tid>>2, tid&3) owns gate column
-// col = gate*64 + u of W_enc's h-rows in registers.  Per step: a = XP[t] + h.W_h,
-// activation, 4-lane shuffle to the unit's owner, c/h update, one barrier.
+// One CTA, 256 threads: thread (u, q) = (tid>>2, tid&3) holds unit u's four
+// gate columns of W_enc's h-rows for the input quarter k in [16q, 16q+16) in
+// registers.  Per step: 8 h loads (the warp's 4 quarters are 4 distinct
+// addresses per load, not a 64-value broadcast per lane), 4 partial dots, a
+// 4-lane reduce-scatter that leaves gate q's full pre-activation in lane q
+// (= the gate column col = q*64 + u), activation, 4-lane shuffle to the
+// unit's owner, c/h update, one barrier.
 __global__ void __launch_bounds__(kThreads, 1)
     enc_rec_kernel(PolicyDims dm, const double *__restrict__ params, const double *__restrict__ XP,
                    double *__restrict__ enc_h, double *__restrict__ enc_c, double *__restrict__ enc_g) {
-    __shared__ __align__(16) double hbuf[2][kH];
+    __shared__ __align__(16) double hbuf[2][kH + 8];  // quarter q at 18q: conflict-free
     const int tid = threadIdx.x, lane = tid & 31;
     const int u = tid >> 2, gate = tid & 3, col = gate * kH + u;
     const double *Wh = params + dm.off.w_enc + (size_t)dm.F * kG;
-    double w[kH];
+    double w[4][16];
 #pragma unroll
-    for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
-    if (tid < kH) hbuf[0][tid] = 0.0;
+    for (int g = 0; g < 4; g++)
+#pragma unroll
+        for (int k = 0; k < 16; k++) w[g][k] = Wh[(size_t)(16 * gate + k) * kG + g * kH + u];
+    if (tid < kH + 8) hbuf[0][tid] = 0.0;
     double c = 0.0;
     double xp = dm.T > 0 ? XP[col] : 0.0;
     __syncthreads();
     const int base = lane & ~3;
+    const bool hi = gate & 2, lo = gate & 1;
+    const bool clk_on = g_dbg_clocks && tid == 0;  // debug phase clocks -> g_phase_clk[4..7]
+    long long ck[4] = {0, 0, 0, 0}, c_last = clk_on ? clock64() : 0;
+#define DP_ENC_PHASE(i)                      \
+    if (clk_on) {                            \
+        const long long now_ = clock64();    \
+        ck[i] += now_ - c_last;              \
+        c_last = now_;                       \
+    }
     for (int t = 0; t < dm.T; t++) {
-        const double a = xp + dot64_sh_reg(hbuf[t & 1], w);
+        const double2 *hq = reinterpret_cast<const double2 *>(hbuf[t & 1] + 18 * gate);
+        double p[4][2];
+#pragma unroll
+        for (int g = 0; g < 4; g++) p[g][0] = p[g][1] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const double2 hv = hq[k];
+#pragma unroll
+            for (int g = 0; g < 4; g++) {
+                p[g][0] = fma(hv.x, w[g][2 * k], p[g][0]);
+                p[g][1] = fma(hv.y, w[g][2 * k + 1], p[g][1]);
+            }
+        }
+        const double p0 = p[0][0] + p[0][1], p1 = p[1][0] + p[1][1];
+        const double p2 = p[2][0] + p[2][1], p3 = p[3][0] + p[3][1];
+        // reduce-scatter over the 4 quarter lanes: lane q ends with gate q's sum
+        double k0 = hi ? p2 : p0, k1 = hi ? p3 : p1;
+        k0 += __shfl_xor_sync(0xffffffffu, hi ? p0 : p2, 2);
+        k1 += __shfl_xor_sync(0xffffffffu, hi ? p1 : p3, 2);
+        double kk = lo ? k1 : k0;
+        kk += __shfl_xor_sync(0xffffffffu, lo ? k0 : k1, 1);
+        const double a = xp + kk;
+        DP_ENC_PHASE(0);
         if (t + 1 < dm.T) xp = XP[(size_t)(t + 1) * kG + col];
         const double act = gate_act(a, gate == 3);
+        DP_ENC_PHASE(1);
         enc_g[(size_t)t * kG + col] = act;
         const double iv = __shfl_sync(0xffffffffu, act, base + 0);
         const double fv = __shfl_sync(0xffffffffu, act, base + 1);
@@ -160,12 +198,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (gate == 0) {
             c = fv * c + iv * gv;
             const double h = ov * tanh_x(c);
-            hbuf[(t + 1) & 1][u] = h;
+            hbuf[(t + 1) & 1][u + 2 * (u >> 4)] = h;
             enc_h[(size_t)t * kH + u] = h;
             enc_c[(size_t)t * kH + u] = c;
         }
+        DP_ENC_PHASE(2);
         __syncthreads();
+        DP_ENC_PHASE(3);
     }
+#undef DP_ENC_PHASE
+    if (clk_on)
+        for (int i = 0; i < 4; i++) g_phase_clk[4 + i] += ck[i];
 }
 
 // ---------------------------------------------------------------- decoder

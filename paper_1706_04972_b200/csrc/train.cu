@@ -75,33 +75,35 @@ __device__ double np_pairwise(const double *a, int n) {
     }
 }
 
-// single CTA; thread 0 runs the order-dependent scalar logic, the block copies
+// single CTA: the block forms the rewards (global loads + sqrt) in parallel,
+// then thread 0 runs the order-dependent scalar logic over shared memory
 __global__ void epilogue_kernel(int K, int T, const double *__restrict__ makespan,
                                 const uint8_t *__restrict__ feasible, const uint8_t *__restrict__ choice,
                                 double failing, double decay, long long success_only_after, long long k_offset,
                                 int K_local, dp_train_state *st, double *__restrict__ adv,
                                 uint8_t *__restrict__ best_choice, double *__restrict__ log_rows, long long log_cap,
                                 int controller_id) {
-    extern __shared__ double R[];   // [K] rewards, then [K] used rewards
+    extern __shared__ double R[];   // [K] rewards, [K] used rewards, [K] feasibility bytes
     __shared__ int s_best_k;
     const int tid = threadIdx.x;
     double *used_r = R + K;
+    uint8_t *okS = reinterpret_cast<uint8_t *>(R + 2 * K);
+    for (int k = tid; k < K; k += blockDim.x) {
+        const bool ok = feasible[k] != 0;
+        const double m = makespan[k];
+        if (ok && (!isfinite(m) || m <= 0.0)) st->error = 1;  // reward_of raises ValueError
+        R[k] = ok ? sqrt(m) : failing;
+        okS[k] = ok ? 1 : 0;
+    }
+    __syncthreads();
     if (tid == 0) {
         const long long upd = st->update;
         double best = st->best_r;
         int best_k = -1, n_feas = 0, n_used = 0;
         const bool all = upd < success_only_after;
         for (int k = 0; k < K; k++) {
-            const bool ok = feasible[k] != 0;
-            const double m = makespan[k];
-            double r;
-            if (!ok) {
-                r = failing;
-            } else {
-                if (!isfinite(m) || m <= 0.0) st->error = 1;  // reward_of raises ValueError
-                r = sqrt(m);
-            }
-            R[k] = r;
+            const bool ok = okS[k] != 0;
+            const double r = R[k];
             n_feas += ok ? 1 : 0;
             if (ok && r < best) {
                 best = r;
@@ -144,7 +146,7 @@ __global__ void epilogue_kernel(int K, int T, const double *__restrict__ makespa
     const bool any = st->n_used > 0;
     for (int k = tid; k < K_local; k += blockDim.x) {
         const long long kg = k_offset + k;
-        const bool use = any && (all || feasible[kg] != 0);
+        const bool use = any && (all || okS[kg] != 0);
         adv[k] = use ? R[kg] - b_old : 0.0;
     }
     const int bk = s_best_k;
@@ -234,11 +236,11 @@ extern "C" int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespa
                                      dp_train_state *state, double *adv, uint8_t *best_choice, double *log_rows,
                                      int64_t log_cap, int32_t controller_id, void *stream) {
     DP_ENTRY();
-    DP_REQUIRE(K >= 1 && K <= 16384, "dp_reinforce_epilogue: need 1 <= K <= 16384");
+    DP_REQUIRE(K >= 1 && K <= 12288, "dp_reinforce_epilogue: need 1 <= K <= 12288");
     DP_REQUIRE(K_local >= 0 && k_offset >= 0 && k_offset + K_local <= K, "dp_reinforce_epilogue: bad shard");
     DP_REQUIRE(makespan && feasible && choice && state && best_choice && log_rows,
                "dp_reinforce_epilogue: NULL argument");
-    const size_t smem = sizeof(double) * 2 * (size_t)K;
+    const size_t smem = sizeof(double) * 2 * (size_t)K + (size_t)K;
     DP_CUDA_TRY(allow_big_smem((const void *)epilogue_kernel, smem));
     epilogue_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(K, T, makespan, feasible, choice, failing, decay,
                                                             success_only_after, k_offset, K_local, state, adv,
