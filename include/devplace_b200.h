@@ -113,7 +113,8 @@ int64_t dp_policy_num_params(const dp_policy *p);
 int dp_policy_encode(dp_policy *p, const double *params, void *stream);
 
 /* Debug instrumentation: enable/disable per-phase cycle counters in the
- * decoder (block 0) and read+reset the 8 sums into h_out[8] (may be NULL). */
+ * decoder (block 0) and the encoder and read+reset the 16 sums into h_out[16]
+ * (may be NULL). */
 int dp_debug_phase_clocks(int32_t enable, int64_t *h_out);
 
 /* Debug instrumentation: LSTM-backward phase clocks (block 0) into h_out[8]. */

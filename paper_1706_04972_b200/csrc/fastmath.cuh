@@ -14,10 +14,10 @@
 namespace dp {
 
 // 2^k for integer-valued k, clamped: k <= -1023 -> 0, k >= 1024 -> +inf
+// (integer clamp: fp64 fmin/fmax cost ~6 instructions each here)
 __device__ __forceinline__ double fm_pow2(double k) {
-    const double kc = fmin(fmax(k, -1023.0), 1024.0);
-    const long long e = (long long)kc + 1023;
-    return __longlong_as_double(e << 52);
+    const int ki = min(max(__double2int_rn(k), -1023), 1024);
+    return __hiloint2double((ki + 1023) << 20, 0);
 }
 
 // expm1 on the reduced argument |r| <= ln2/2: r + r^2 (1/2! + r/3! + ... + r^11/13!)
@@ -43,7 +43,10 @@ __device__ __forceinline__ void fm_reduce(double y, double &k, double &r) {
     constexpr double kL2E = 1.4426950408889634;
     constexpr double kLn2Hi = 6.93147180559945286227e-01;  // ln2 rounded to double
     constexpr double kLn2Lo = 2.31904681384629955842e-17;  // ln2 - kLn2Hi
-    y = fmin(fmax(y, -1000.0), 1000.0);  // saturates exp to 0 / inf, expm1 to -1 / inf; keeps r sane (-inf -> 0)
+    // clamp to [-1000, 1000] with fmin/fmax's NaN rule (NaN -> -1000) as two
+    // compare-selects: saturates exp to 0 / inf, expm1 to -1 / inf; keeps r sane
+    y = !(y >= -1000.0) ? -1000.0 : y;
+    y = y > 1000.0 ? 1000.0 : y;
     k = rint(y * kL2E);
     r = fma(-k, kLn2Hi, y);
     r = fma(-k, kLn2Lo, r);

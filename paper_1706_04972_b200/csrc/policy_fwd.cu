@@ -438,14 +438,25 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
     const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
     long long clk_last = clk_on ? clock64() : 0;
-    long long clk_acc[3] = {0, 0, 0};  // in registers; one global write at the end
+    long long clk_acc[16] = {};  // in registers; one global write at the end
+#define DP_MARK(i, dep)                                                                           \
+    if (clk_on) {                                                                                 \
+        const long long now_ = clock64() + (long long)((dep) * 0.0);                              \
+        clk_acc[i] += now_ - clk_last;                                                            \
+        clk_last = now_;                                                                          \
+    }
 #define DP_PHASE(i)                                       \
     if (clk_on) {                                         \
         const long long now_ = clock64();                 \
         clk_acc[i] += now_ - clk_last;                    \
         clk_last = now_;                                  \
     }
-    for (int t = 0; t < T; t++) {
+    // running row pointers of the step's cached activations (sample m at + m * T rows)
+    const size_t sG = (size_t)T * kG, sH = (size_t)T * kH;
+    double *actg = a.act_g + (size_t)k0 * sG + col;
+    double *acth = a.act_h + (size_t)k0 * sH + u;
+    double *actc = a.act_c + (size_t)k0 * sH + u;
+    for (int t = 0; t < T; t++, actg += kG, acth += kH, actc += kH) {
         const int par = t & 1;
         const int *prv = prev + par * M;  // choices of step t-1 (SPEC: candidate slots)
         if (!SPEC) {
@@ -454,9 +465,10 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             double act[MT], cn[MT], hn[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++) act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
+            DP_MARK(8, act[0] + act[MT - 1]);
 #pragma unroll
             for (int m = 0; m < MT; m++)
-                if (m < Mb) a.act_g[((size_t)(k0 + m) * T + t) * kG + col] = act[m];
+                if (m < Mb) actg[m * sG] = act[m];
 #pragma unroll
             for (int m = 0; m < MT; m++) {
                 const double iv = __shfl_sync(0xffffffffu, act[m], base + 0);
@@ -466,17 +478,19 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 cn[m] = fv * cst[m] + iv * gv;
                 act[m] = ov;
             }
+            DP_MARK(9, cn[0] + cn[MT - 1]);
 #pragma unroll
             for (int m = 0; m < MT; m++) hn[m] = act[m] * tanh_x(cn[m]);
+            DP_MARK(10, hn[0] + hn[MT - 1]);
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb && gate == 0) {
-                    const size_t row = (size_t)(k0 + m) * T + t;
                     cst[m] = cn[m];
                     hS[m * kH + u] = hn[m];
-                    a.act_h[row * kH + u] = hn[m];
-                    a.act_c[row * kH + u] = cn[m];
+                    acth[m * sH] = hn[m];
+                    actc[m * sH] = cn[m];
                 }
+            DP_MARK(11, 0.0);
             __syncthreads();
         }
         DP_PHASE(0);
@@ -765,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             double gsum = 0.0;
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
+            if (clk_on) { const long long now_ = clock64() + (long long)(gsum * 0.0); clk_acc[3] += now_ - clk_last; clk_last = now_; }
             if (!split && a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
             // all lanes compute (clamped indices, no divergent branches: the z, uc
             // and pcg chains interleave); lanes >= D / >= dd are masked at the end
@@ -820,6 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
             const double zv = (zh + fm_div(zc, gsum)) + bout[ld];
             const double z = lane < D ? zv : -INFINITY;
+            if (clk_on) { const long long now_ = clock64() + (long long)(z * 0.0 + 0.5); clk_acc[4] += now_ - clk_last; clk_last = now_; }
             if (!split) {
                 // u (and its context half uc) for the backward
                 double uc = 0.0;
@@ -861,6 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 for (; i < D; i++) esum += __shfl_sync(0xffffffffu, ez, i);
             }
             const double pr = fm_div(ez, esum);
+            if (clk_on) { const long long now_ = clock64() + (long long)(pr * 0.0); clk_acc[5] += now_ - clk_last; clk_last = now_; }
             if (lane < D) {
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
@@ -890,6 +907,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 ch = cnt < D - 1 ? cnt : D - 1;
             }
             const double zsc = __shfl_sync(0xffffffffu, zs, ch);
+            if (clk_on) { const long long now_ = clock64() + ch * 0; clk_acc[6] += now_ - clk_last; clk_last = now_; }
             if (lane == 0) {
                 if (!a.forced) {
                     pcg[2 * m] = rs.hi;  // every lane has read the state by now (the cdf shuffles)
@@ -933,13 +951,14 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         if (!SPEC) {
             // gn for the non-speculative A of the next step is already in registers
         }
+        if (clk_on) { const long long now_ = clock64(); clk_acc[7] += now_ - clk_last; clk_last = now_; }
         __syncthreads();
         DP_PHASE(2);
     }
 #undef DP_PHASE
     if (clk_on)
 #pragma unroll
-        for (int i = 0; i < 3; i++) g_phase_clk[i] += clk_acc[i];
+        for (int i = 0; i < 16; i++) g_phase_clk[i] += clk_acc[i];
     // ---- log p = sum_t (zs[c_t] - log sum_t): logs in parallel, sum in t order ----
     __threadfence_block();
     for (int m = 0; m < Mb; m++) {
@@ -1159,7 +1178,7 @@ extern "C" int dp_debug_phase_clocks(int32_t enable, int64_t *h_out) {
         DP_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_skip, &skip, sizeof(int)));
     }
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_clocks, &on, sizeof(int)));
-    if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_phase_clk, sizeof(long long) * 8));
+    if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_phase_clk, sizeof(long long) * 16));
     long long z[16] = {0};
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z)));
     return DP_OK;

@@ -25,7 +25,7 @@ pdev = torch.as_tensor(params.to_flat(), device="cuda")
 eng.encode(pdev)
 eng.decode(pdev, K, pcg=(1, 3))
 torch.cuda.synchronize()
-out = (ctypes.c_int64 * 8)()
+out = (ctypes.c_int64 * 16)()
 skip = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 nat.check(nat.lib().dp_debug_phase_clocks(1 | (skip << 1), None), "dbg")
 eng.decode(pdev, K, pcg=(1, 3))
@@ -33,7 +33,13 @@ torch.cuda.synchronize()
 nat.check(nat.lib().dp_debug_phase_clocks(0, out), "dbg")
 T = len(feats)
 names = ["A gates+cell", "C scores/softmax/uc/uh/next-g", "E combine+draw"]
-tot = sum(out)
+tot = sum(out[:3]) + sum(out[3:8])
 print(f"{name} K={K} T={T} variant={variant} skip={skip}: {tot / T:.0f} cycles/step")
 for n, v in zip(names, out[:3]):
     print(f"  {n:32s} {v / T:8.0f} cycles/step  {100 * v / tot:5.1f}%")
+if any(out[3:8]):
+    for n, v in zip(["E: ->gsum", "E: ->z", "E: ->pr", "E: ->ch", "E: ->pre-barrier"], out[3:8]):
+        print(f"  {n:32s} {v / T:8.0f} cycles/step")
+if any(out[8:12]):
+    for n, v in zip(["A: ->act", "A: ->cn", "A: ->hn", "A: ->stores"], out[8:12]):
+        print(f"  {n:32s} {v / T:8.0f} cycles/step")

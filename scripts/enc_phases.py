@@ -20,7 +20,7 @@ eng = dp.policy.engine_for(params, feats, 8)
 pdev = torch.as_tensor(params.to_flat(), device="cuda")
 eng.encode(pdev)
 torch.cuda.synchronize()
-out = (ctypes.c_int64 * 8)()
+out = (ctypes.c_int64 * 16)()
 nat.check(nat.lib().dp_debug_phase_clocks(1, None), "dbg")
 eng.encode(pdev)
 torch.cuda.synchronize()
