@@ -31,7 +31,6 @@ struct dp_policy {
     int32_t *type_off, *type_idx;
     int32_t *occ_off, *occ_t;  // per type row: decode steps using it (with multiplicity), t-ascending
     int n_occ;                 // total occurrences (sum of member-type counts)
-    double *occ_val;           // [n_occ * type_dim] type-table gradient terms (backward scratch)
     double *zeros;             // [64] zero cell state (encoder step 0)
     double *shape, *adj;
     // encoder activations (one sequence, shared by all samples)
@@ -69,6 +68,6 @@ struct dp_policy {
     int rows_ready;               // K of the last dp_policy_backward_rows (0: none)
     int att_per_sample;           // the last rows pass left per-sample (1) or per-tile (0) partials
     // side stream: the encoder backward (one CTA) overlaps the decoder weight-gradient GEMM
-    cudaStream_t side;
-    cudaEvent_t ev_fork, ev_join;
+    cudaStream_t side, side2;
+    cudaEvent_t ev_fork, ev_join, ev_fork2, ev_join2;
 };

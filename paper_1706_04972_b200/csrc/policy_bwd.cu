@@ -1178,17 +1178,19 @@ __global__ void __launch_bounds__(kG) dec_finalize_kernel(PolicyDims dm, const d
 }
 
 // sum over samples of the decoder's dh/dc at step 0 -> encoder final state grads
-// dst[j] = sum_r w[r] * src[r, j]  (w == NULL: weights 1); 512 threads =
-// 64 columns x 8 row-slices, fixed-order combine
-__global__ void __launch_bounds__(512) sum_rows_kernel(const double *__restrict__ src, int n_rows,
-                                                       double *__restrict__ dst, const double *__restrict__ w) {
-    __shared__ double part[8][kH];
+// dst[blockIdx.x][j] = sum_r w[r] * src_b[r, j] (w == NULL: weights 1), src_0 =
+// dh, src_1 = dc; 1024 threads = 64 columns x 16 row-slices, fixed-order combine
+__global__ void __launch_bounds__(1024) sum_rows_kernel(const double *__restrict__ dh, const double *__restrict__ dc,
+                                                        int n_rows, double *__restrict__ dst,
+                                                        const double *__restrict__ w) {
+    __shared__ double part[16][kH];
     const int j = threadIdx.x & 63, s = threadIdx.x >> 6;
+    const double *src = blockIdx.x ? dc : dh;
     double v0 = 0.0, v1 = 0.0;
     int r = s;
-    for (; r + 8 < n_rows; r += 16) {
+    for (; r + 16 < n_rows; r += 32) {
         v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
-        v1 = fma(w ? w[r + 8] : 1.0, src[(size_t)(r + 8) * kH + j], v1);
+        v1 = fma(w ? w[r + 16] : 1.0, src[(size_t)(r + 16) * kH + j], v1);
     }
     if (r < n_rows) v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
     part[s][j] = v0 + v1;
@@ -1196,22 +1198,37 @@ __global__ void __launch_bounds__(512) sum_rows_kernel(const double *__restrict_
     if (s == 0) {
         double v = part[0][j];
 #pragma unroll
-        for (int q = 1; q < 8; q++) v += part[q][j];
-        dst[j] = v;
+        for (int q = 1; q < 16; q++) v += part[q][j];
+        dst[blockIdx.x * kH + j] = v;
     }
 }
 
 // B5: w_enc / b_enc grads (contraction over T) and the type-embedding scatter.
 // enc_wgrad: block = 4 rows r of [X | h_prev] (or b_enc) x 256 gate columns;
-// the 4 input rows are staged in shared memory, da_enc streams from L2.
-constexpr int kWgRows = 4;
+// the 4 input rows are staged in shared memory, da_enc streams through a
+// cp.async double buffer of 16-step chunks (bulk loads instead of one L2
+// latency per step and thread).
+constexpr int kWgRows = 4, kWgChunk = 16;
+inline size_t enc_wgrad_smem(int T) { return sizeof(double) * ((size_t)kWgRows * T + 2 * kWgChunk * kG); }
 __global__ void __launch_bounds__(kG) enc_wgrad_kernel(PolicyDims dm, const double *__restrict__ X,
                                                        const double *__restrict__ enc_h,
                                                        const double *__restrict__ da_enc, double *__restrict__ grad) {
-    extern __shared__ double xs[];  // [kWgRows][T]
+    extern __shared__ __align__(16) double xs[];  // [kWgRows][T], then [2][kWgChunk][256]
     const int j = threadIdx.x;
-    const int T = dm.T, F = dm.F, R = F + kH + 1;
+    const int T = dm.T, F = dm.F;
     const int r0 = blockIdx.x * kWgRows;
+    double *dab = xs + kWgRows * T;
+    const int n_chunks = (T + kWgChunk - 1) / kWgChunk;
+    auto stage = [&](int c, int b) {
+        double *dst = dab + b * kWgChunk * kG;
+        const double *src = da_enc + (size_t)c * kWgChunk * kG;
+        for (int x = j * 2; x < kWgChunk * kG; x += kG * 2) {
+            const bool ok = c * kWgChunk + x / kG < T;
+            cp_async16(dst + x, ok ? src + x : da_enc, ok);
+        }
+        cp_async_commit();
+    };
+    stage(0, 0);
     for (int x = j; x < kWgRows * T; x += kG) {
         const int a = x / T, t = x - a * T, r = r0 + a;
         double v = 0.0;
@@ -1220,24 +1237,38 @@ __global__ void __launch_bounds__(kG) enc_wgrad_kernel(PolicyDims dm, const doub
         else if (r == F + kH) v = 1.0;  // b_enc row
         xs[x] = v;
     }
-    __syncthreads();
     double acc[kWgRows][2];
 #pragma unroll
     for (int a = 0; a < kWgRows; a++) acc[a][0] = acc[a][1] = 0.0;
-    int t = 0;
-#pragma unroll 4
-    for (; t + 2 <= T; t += 2) {
-        const double d0 = da_enc[(size_t)t * kG + j], d1 = da_enc[(size_t)(t + 1) * kG + j];
-#pragma unroll
-        for (int a = 0; a < kWgRows; a++) {
-            acc[a][0] = fma(xs[a * T + t], d0, acc[a][0]);
-            acc[a][1] = fma(xs[a * T + t + 1], d1, acc[a][1]);
+    for (int c = 0; c < n_chunks; c++) {
+        const int b = c & 1;
+        if (c + 1 < n_chunks) {
+            stage(c + 1, b ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
-    }
-    if (t < T) {
-        const double d0 = da_enc[(size_t)t * kG + j];
+        __syncthreads();
+        const double *d = dab + b * kWgChunk * kG;
+        const int tb = c * kWgChunk, nt = min(kWgChunk, T - tb);
+        if (nt == kWgChunk) {
+#pragma unroll 8
+            for (int tt = 0; tt < kWgChunk; tt += 2) {
+                const double d0 = d[tt * kG + j], d1 = d[(tt + 1) * kG + j];
 #pragma unroll
-        for (int a = 0; a < kWgRows; a++) acc[a][0] = fma(xs[a * T + t], d0, acc[a][0]);
+                for (int a = 0; a < kWgRows; a++) {
+                    acc[a][0] = fma(xs[a * T + tb + tt], d0, acc[a][0]);
+                    acc[a][1] = fma(xs[a * T + tb + tt + 1], d1, acc[a][1]);
+                }
+            }
+        } else {
+            for (int tt = 0; tt < nt; tt++) {
+                const double d0 = d[tt * kG + j];
+#pragma unroll
+                for (int a = 0; a < kWgRows; a++) acc[a][0] = fma(xs[a * T + tb + tt], d0, acc[a][0]);
+            }
+        }
+        __syncthreads();  // buffer b is re-staged two chunks on
     }
 #pragma unroll
     for (int a = 0; a < kWgRows; a++) {
@@ -1245,59 +1276,73 @@ __global__ void __launch_bounds__(kG) enc_wgrad_kernel(PolicyDims dm, const doub
         if (r < F + kH) grad[dm.off.w_enc + (size_t)r * kG + j] = acc[a][0] + acc[a][1];
         else if (r == F + kH) grad[dm.off.b_enc + j] = acc[a][0] + acc[a][1];
     }
-    (void)R;
 }
 
-// dx_t[f] = W_enc[f, :] . da_enc[t]   (f < type_dim): block per t, block reduction over the 256 gates
+// dx_t[f] = W_enc[f, :] . da_enc[t]   (f < type_dim): block per t.  Per 32-wide f
+// chunk every lane forms its 32 products (loads issued together), a
+// reduce-scatter butterfly (31 shuffles) leaves f = f0 + lane's warp sum in
+// lane f - f0, and the 8 warp sums combine in a fixed order.
 __global__ void __launch_bounds__(kG) enc_dx_kernel(PolicyDims dm, const double *__restrict__ P,
                                                     const double *__restrict__ da_enc, double *__restrict__ dx) {
     __shared__ double part[kG / 32][32];
     const int t = blockIdx.x, j = threadIdx.x, lane = j & 31, w = j >> 5;
     const double d = da_enc[(size_t)t * kG + j];
     for (int f0 = 0; f0 < dm.td; f0 += 32) {
-        // each warp reduces its 32 gates for up to 32 f values (f on lanes after the transpose)
-        double mine = 0.0;
-        for (int q = 0; q < 32 && f0 + q < dm.td; q++) {
-            double v = P[dm.off.w_enc + (size_t)(f0 + q) * kG + j] * d;
+        double v[32];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == q) mine = v;
+        for (int q = 0; q < 32; q++) v[q] = f0 + q < dm.td ? P[dm.off.w_enc + (size_t)(f0 + q) * kG + j] * d : 0.0;
+#pragma unroll
+        for (int lv = 0; lv < 5; lv++) {
+            const int o = 16 >> lv, half = 16 >> lv;  // values carried: 2 * half
+            const bool hi = lane & o;
+#pragma unroll
+            for (int i = 0; i < half; i++) {
+                const double send = hi ? v[i] : v[i + half];
+                const double keep = hi ? v[i + half] : v[i];
+                v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
         }
-        part[w][lane] = mine;
+        part[w][lane] = v[0];
         __syncthreads();
         if (w == 0 && f0 + lane < dm.td) {
-            double v = part[0][lane];
+            double s = part[0][lane];
 #pragma unroll
-            for (int q = 1; q < kG / 32; q++) v += part[q][lane];
-            dx[(size_t)t * dm.td + f0 + lane] = v;
+            for (int q = 1; q < kG / 32; q++) s += part[q][lane];
+            dx[(size_t)t * dm.td + f0 + lane] = s;
         }
         __syncthreads();
     }
 }
 
 // np.add.at(type_table, idx_t, dx_t / len(idx_t)) in (t, position) order
-// (pkg/policy.py:405-407).  Pass 1 (parallel): every occurrence's term
-// dx[t][f] / len(idx_t) into occ_val; pass 2: thread (v, f) adds its terms in
-// occurrence order (contiguous, pipelined loads) — the reference's order.
-__global__ void type_terms_kernel(PolicyDims dm, int n_occ, const int32_t *__restrict__ occ_t,
-                                  const int32_t *__restrict__ type_off, const double *__restrict__ dx,
-                                  double *__restrict__ occ_val) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= n_occ * dm.td) return;
-    const int o = idx / dm.td, f = idx - o * dm.td;
-    const int t = occ_t[o];
-    occ_val[idx] = dx[(size_t)t * dm.td + f] / (double)(type_off[t + 1] - type_off[t]);
-}
-
-__global__ void type_scatter_kernel(PolicyDims dm, const int32_t *__restrict__ occ_off,
-                                    const double *__restrict__ occ_val, double *__restrict__ grad) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= dm.V1 * dm.td) return;
-    const int v = idx / dm.td, f = idx % dm.td;
+// (pkg/policy.py:405-407).  Block per vocabulary row v: its occurrences' terms
+// dx[t][f] / len(idx_t) are staged in shared memory in chunks (all loads in
+// flight at once), then thread f adds them in occurrence order — the
+// reference's order.
+constexpr int kScatterVals = 4096;
+__global__ void __launch_bounds__(256) type_scatter_kernel(PolicyDims dm, const int32_t *__restrict__ occ_off,
+                                                           const int32_t *__restrict__ occ_t,
+                                                           const int32_t *__restrict__ type_off,
+                                                           const double *__restrict__ dx, double *__restrict__ grad) {
+    __shared__ double vals[kScatterVals];
+    const int v = blockIdx.x, tid = threadIdx.x, td = dm.td;
+    const int o0 = occ_off[v], o1 = occ_off[v + 1];
+    const int per = kScatterVals / td;  // occurrences per chunk
     double s = 0.0;
+    for (int c0 = o0; c0 < o1; c0 += per) {
+        const int nc = min(per, o1 - c0);
+        for (int x = tid; x < nc * td; x += blockDim.x) {
+            const int o = c0 + x / td, f = x - (x / td) * td;
+            const int t = occ_t[o];
+            vals[x] = dx[(size_t)t * td + f] / (double)(type_off[t + 1] - type_off[t]);
+        }
+        __syncthreads();
+        if (tid < td)
 #pragma unroll 8
-    for (int o = occ_off[v]; o < occ_off[v + 1]; o++) s = s + occ_val[(size_t)o * dm.td + f];
-    grad[dm.off.type_table + idx] = s;
+            for (int i = 0; i < nc; i++) s = s + vals[i * td + tid];
+        __syncthreads();
+    }
+    if (tid < td) grad[dm.off.type_table + (size_t)v * td + tid] = s;
 }
 
 int n_cta_for(int units, int min_units) {
@@ -1495,9 +1540,7 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
     DP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {
         cudaStream_t ss = p->side;
-        sum_rows_kernel<<<1, 512, 0, ss>>>(p->dh0, K, dhc_sum, adv);
-        DP_LAUNCH_CHECK();
-        sum_rows_kernel<<<1, 512, 0, ss>>>(p->dc0, K, dhc_sum + kH, adv);
+        sum_rows_kernel<<<2, 1024, 0, ss>>>(p->dh0, p->dc0, K, dhc_sum, adv);
         DP_LAUNCH_CHECK();
         DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, ss));
         const size_t smem = lstm_bwd_smem(1);
@@ -1505,19 +1548,23 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
                                                    p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
                                                    dhc_sum + 2 * kH, dhc_sum + 3 * kH);
         DP_LAUNCH_CHECK();
+        // the encoder weight grads and the type-table chain both only need
+        // da_enc: fork the former onto a second side stream
+        DP_CUDA_TRY(cudaEventRecord(p->ev_fork2, ss));
+        DP_CUDA_TRY(cudaStreamWaitEvent(p->side2, p->ev_fork2, 0));
         {
-            const size_t xs = sizeof(double) * kWgRows * T;
+            const size_t xs = enc_wgrad_smem(T);
             DP_CUDA_TRY(allow_big_smem((const void *)enc_wgrad_kernel, xs));
-            enc_wgrad_kernel<<<ceil_div(dm.F + kH + 1, kWgRows), kG, xs, ss>>>(dm, p->X, p->enc_h, p->da_enc, grad);
+            enc_wgrad_kernel<<<ceil_div(dm.F + kH + 1, kWgRows), kG, xs, p->side2>>>(dm, p->X, p->enc_h, p->da_enc,
+                                                                                   grad);
         }
         DP_LAUNCH_CHECK();
+        DP_CUDA_TRY(cudaEventRecord(p->ev_join2, p->side2));
         enc_dx_kernel<<<T, kG, 0, ss>>>(dm, params, p->da_enc, dx_scratch);
         DP_LAUNCH_CHECK();
-        type_terms_kernel<<<ceil_div(p->n_occ * dm.td, 256), 256, 0, ss>>>(dm, p->n_occ, p->occ_t, p->type_off, dx_scratch,
-                                                                          p->occ_val);
+        type_scatter_kernel<<<dm.V1, 256, 0, ss>>>(dm, p->occ_off, p->occ_t, p->type_off, dx_scratch, grad);
         DP_LAUNCH_CHECK();
-        type_scatter_kernel<<<ceil_div(dm.V1 * dm.td, 128), 128, 0, ss>>>(dm, p->occ_off, p->occ_val, grad);
-        DP_LAUNCH_CHECK();
+        DP_CUDA_TRY(cudaStreamWaitEvent(ss, p->ev_join2, 0));
         DP_CUDA_TRY(cudaEventRecord(p->ev_join, ss));
     }
     if (split_grads) {

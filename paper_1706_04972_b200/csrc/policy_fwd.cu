@@ -1007,7 +1007,7 @@ static ParamLayout layout_of(int V1, int D, int dd, int F, int td) {
 
 extern "C" void dp_policy_destroy(dp_policy *p) {
     if (!p) return;
-    void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->occ_val, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
+    void *ptrs[] = {p->type_off, p->type_idx, p->occ_off, p->occ_t, p->zeros, p->shape, p->adj, p->X, p->XP, p->enc_h, p->enc_c,
                     p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->proj_nmax, p->vdev, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_dctx, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->da_enc, p->partial, p->gacc,
@@ -1015,8 +1015,11 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p->side) cudaStreamDestroy(p->side);
+    if (p->side2) cudaStreamDestroy(p->side2);
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_join) cudaEventDestroy(p->ev_join);
+    if (p->ev_fork2) cudaEventDestroy(p->ev_fork2);
+    if (p->ev_join2) cudaEventDestroy(p->ev_join2);
     (void)cudaGetLastError();
     delete p;
 }
@@ -1083,7 +1086,6 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
         upload((void **)&p->occ_off, occ_off.data(), sizeof(int32_t) * (vocab_rows + 1));
         upload((void **)&p->occ_t, occ_t.data(), sizeof(int32_t) * n_idx);
         p->n_occ = n_idx;
-        alloc((void **)&p->occ_val, sizeof(double) * (size_t)n_idx * type_dim);
         std::vector<double> z(kH, 0.0);
         upload((void **)&p->zeros, z.data(), sizeof(double) * kH);
     }
@@ -1147,8 +1149,11 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
         return DP_ECUDA;
     }
     if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->side2, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming) != cudaSuccess) {
         dp::set_error("dp_policy_create: stream/event creation failed");
         dp_policy_destroy(p);
         return DP_ECUDA;
