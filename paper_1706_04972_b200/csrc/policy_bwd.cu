@@ -54,6 +54,12 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, boo
     const int n = valid ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(n) : "memory");
 }
+// 8-byte variant (L1-allocating .ca; 8 is a legal .ca size, .cg takes only 16)
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool valid) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const int n = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(n) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -410,6 +416,142 @@ __global__ void __launch_bounds__(kThreads) watt_grad_kernel(int T, int parts, i
 #pragma unroll
         for (int jj = 0; jj < 4; jj++)
             partial[(size_t)blockIdx.x * kH * kH + (a + 16 * i) * kH + b + 16 * jj] = tot[i][jj];
+}
+
+// B0g + B1fg fused: one pass over the rows computes every advantage-weighted
+// output-side gradient,
+//   [w_att | w_out[:64]] += (adv o H)^T [DQ | DU]     (64 x (64 + dd), DMMA)
+//   dev_table          += (adv o DZ)^T U            (D x dd, SIMT)
+//   b_out              += sum_r adv_r dz[r]
+// with dz = onehot(choice) - p.  32-row tiles of h and [dq | du] stream through
+// a cp.async double buffer (row strides == 8 mod 32 words: conflict-free
+// fragment loads); warp w owns m-tile w (h units 8w..8w+7) x all n-tiles.
+// partial per CTA: [b_out D | dev_table D*dd | w_out[:64] 64*dd | w_att 64*64].
+constexpr int kAgLdH = kH + 4, kAgLdB = kH + kMaxDD + 4, kAgNt = (kH + kMaxDD) / 8;
+struct AdvGradSmem {
+    double h[2][kTile][kAgLdH];
+    double b[2][kTile][kAgLdB];      // [dq (64) | du (dd) | 0]
+    double u[2][kTile][kMaxDD];
+    double p[2][kTile][kMaxD];
+    double w[2][kTile];
+    uint8_t ch[2][kTile];
+};
+__host__ __device__ inline size_t adv_grads_partial(const PolicyDims &dm) {
+    return (size_t)dm.D + dm.D * dm.dd + kH * dm.dd + kH * kH;
+}
+__global__ void __launch_bounds__(kThreads, 1) adv_grads_kernel(PolicyDims dm, int rows, int tiles_per_cta,
+                                                                const double *__restrict__ adv,
+                                                                const double *__restrict__ act_h,
+                                                                const double *__restrict__ row_dq,
+                                                                const double *__restrict__ row_du,
+                                                                const double *__restrict__ act_u,
+                                                                const double *__restrict__ act_p,
+                                                                const uint8_t *__restrict__ choice,
+                                                                double *__restrict__ partial) {
+    extern __shared__ __align__(16) double sm_raw[];
+    AdvGradSmem &S = *reinterpret_cast<AdvGradSmem *>(sm_raw);
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int T = dm.T, D = dm.D, dd = dm.dd;
+    const int nt_used = (kH + dd + 7) / 8;
+    double acc[kAgNt][2];
+#pragma unroll
+    for (int n = 0; n < kAgNt; n++) acc[n][0] = acc[n][1] = 0.0;
+    double gdev = 0.0, gb = 0.0;  // thread tid < D*dd: dev_table[d][o]; tid < D: b_out[d]
+    const int dv_d = tid / (dd > 0 ? dd : 1), dv_o = tid - dv_d * dd;
+    const int n_tiles = (rows + kTile - 1) / kTile;
+    const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
+    // zero the padding columns of both B buffers once (never written by the copies)
+    for (int x = tid; x < 2 * kTile * (kAgLdB - kH - dd); x += kThreads) {
+        const int bb = x / (kTile * (kAgLdB - kH - dd)), rem = x - bb * kTile * (kAgLdB - kH - dd);
+        const int r = rem / (kAgLdB - kH - dd), c = rem - r * (kAgLdB - kH - dd);
+        S.b[bb][r][kH + dd + c] = 0.0;
+    }
+    auto stage = [&](int tl, int bf) {
+        const int rb = tl * kTile;
+        for (int x = tid * 2; x < kTile * kH; x += kThreads * 2) {
+            const int r = x >> 6, c = x & 63;
+            const bool ok = rb + r < rows;
+            cp_async16(&S.h[bf][r][c], act_h + (ok ? (size_t)rb * kH + x : 0), ok);
+            cp_async16(&S.b[bf][r][c], row_dq + (ok ? (size_t)rb * kH + x : 0), ok);
+        }
+        // the small per-row operands also go asynchronously (8-byte copies; a
+        // plain load would stall this thread before the current tile's math)
+        for (int x = tid; x < kTile * dd; x += kThreads) {
+            const int r = x / dd, c = x - r * dd;
+            const bool ok = rb + r < rows;
+            cp_async8(&S.b[bf][r][kH + c], row_du + (ok ? (size_t)rb * dd + x : 0), ok);
+            cp_async8(&S.u[bf][r][c], act_u + (ok ? (size_t)rb * dd + x : 0), ok);
+        }
+        for (int x = tid; x < kTile * D; x += kThreads) {
+            const int r = x / D;
+            const bool ok = rb + r < rows;
+            cp_async8(&S.p[bf][r][x - r * D], act_p + (ok ? (size_t)rb * D + x : 0), ok);
+        }
+        if (tid < kTile) {
+            const int row = rb + tid;
+            const bool ok = row < rows;
+            cp_async8(&S.w[bf][tid], adv + (ok ? row / T : 0), ok);
+        } else if (tid < kTile + kTile / 8) {
+            // choices: 8-byte words of the tile's 32 bytes (rows are 32-aligned)
+            const int q = tid - kTile, row = rb + 8 * q;
+            if (row + 8 <= rows) {
+                cp_async8(&S.ch[bf][8 * q], choice + row, true);
+            } else {
+                for (int e = 0; e < 8; e++) S.ch[bf][8 * q + e] = row + e < rows ? choice[row + e] : 0;
+            }
+        }
+        cp_async_commit();
+    };
+    if (t0 < t1) stage(t0, 0);
+    for (int tl = t0; tl < t1; tl++) {
+        const int bf = (tl - t0) & 1;
+        if (tl + 1 < t1) {
+            stage(tl + 1, bf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int ks = 0; ks < kTile / 4; ks++) {
+            const int r = ks * 4 + t;
+            const double a = S.h[bf][r][wp * 8 + g] * S.w[bf][r];
+#pragma unroll
+            for (int n = 0; n < kAgNt; n++)
+                if (n < nt_used) dmma884(acc[n], a, S.b[bf][r][n * 8 + g]);
+        }
+        if (tid < D * dd) {
+            double v0 = 0.0, v1 = 0.0;
+#pragma unroll 4
+            for (int r = 0; r < kTile; r += 2) {
+                const double z0 = (S.ch[bf][r] == dv_d ? 1.0 : 0.0) - S.p[bf][r][dv_d];
+                const double z1 = (S.ch[bf][r + 1] == dv_d ? 1.0 : 0.0) - S.p[bf][r + 1][dv_d];
+                v0 = fma(S.w[bf][r] * z0, S.u[bf][r][dv_o], v0);
+                v1 = fma(S.w[bf][r + 1] * z1, S.u[bf][r + 1][dv_o], v1);
+            }
+            gdev += v0 + v1;
+        }
+        if (tid < D) {
+            double v = 0.0;
+            for (int r = 0; r < kTile; r++)
+                v = fma(S.w[bf][r], (S.ch[bf][r] == tid ? 1.0 : 0.0) - S.p[bf][r][tid], v);
+            gb += v;
+        }
+        __syncthreads();  // buffer bf is re-staged by the next iteration
+    }
+    double *out = partial + (size_t)blockIdx.x * adv_grads_partial(dm);
+    if (tid < D) out[tid] = gb;
+    if (tid < D * dd) out[D + tid] = gdev;
+    double *o1 = out + D + D * dd, *oa = o1 + kH * dd;
+    const int l = wp * 8 + g;
+#pragma unroll
+    for (int n = 0; n < kAgNt; n++)
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+            const int c = n * 8 + 2 * t + e;
+            if (c < kH) oa[l * kH + c] = acc[n][e];
+            else if (c < kH + dd) o1[l * dd + (c - kH)] = acc[n][e];
+        }
 }
 
 // ------------------------------------------------------------------ B1
@@ -1375,7 +1517,9 @@ size_t dp_backward_partial_elems(const dp_policy *p) {
     size_t b = ncta * (size_t)dm.T * kH;
     size_t c = ncta * (size_t)kH * kH;
     size_t d = ncta * (size_t)(kH + dm.D + 1) * kG;
+    size_t e = ncta * adv_grads_partial(dm);
     size_t m = a > b ? a : b;
+    m = m > e ? m : e;
     m = m > c ? m : c;
     m = m > d ? m : d;
     return m + (size_t)dm.T * dm.td + 4 * kH;  // + dx scratch + (dh, dc) sums + encoder (dh, dc) sink
@@ -1568,10 +1712,25 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         DP_CUDA_TRY(cudaEventRecord(p->ev_join, ss));
     }
     if (split_grads) {
-        const int rc0 = run_b0(p, params, rows, adv, grad, kGradsOnly, st);
-        if (rc0 != DP_OK) return rc0;
-        const int rc1 = run_b1f(p, params, rows, adv, grad, kGradsOnly, st);
-        if (rc1 != DP_OK) return rc1;
+        // B0g + B1fg in one pass over the rows
+        const Grid g = tiles_grid(rows, kTile);
+        const int n_cta = ceil_div(ceil_div(rows, kTile), ceil_div(ceil_div(rows, kTile), kNumSMs));
+        const int per = ceil_div(ceil_div(rows, kTile), n_cta);
+        (void)g;
+        const size_t smem = sizeof(AdvGradSmem);
+        DP_CUDA_TRY(allow_big_smem((const void *)adv_grads_kernel, smem));
+        adv_grads_kernel<<<n_cta, kThreads, smem, st>>>(dm, rows, per, adv, p->act_h, p->row_dq, p->row_du, p->act_u,
+                                                         p->act_p, p->act_choice, part);
+        DP_LAUNCH_CHECK();
+        const size_t na = adv_grads_partial(dm);
+        launch_reduce(part, n_cta, na, dm.D, grad + dm.off.b_out, 0, st);
+        DP_LAUNCH_CHECK();
+        launch_reduce(part + dm.D, n_cta, na, dm.D * dm.dd, grad + dm.off.dev_table, 0, st);
+        DP_LAUNCH_CHECK();
+        launch_reduce(part + dm.D + dm.D * dm.dd, n_cta, na, kH * dm.dd, grad + dm.off.w_out, 0, st);
+        DP_LAUNCH_CHECK();
+        launch_reduce(part + dm.D + dm.D * dm.dd + kH * dm.dd, n_cta, na, kH * kH, grad + dm.off.w_att, 0, st);
+        DP_LAUNCH_CHECK();
     }
     // B3
     {
