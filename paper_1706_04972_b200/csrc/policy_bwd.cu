@@ -46,7 +46,6 @@ constexpr int kFusedGrads = 3;  // B1f in the fused pass: grads only, rows alrea
 constexpr int kFinTile = 64;
 constexpr int kChunk = 64;  // B1: enc rows per chunk
 constexpr int kPad = 65;
-constexpr int kRedSlicesW = 8;  // weighted_reduce slices
 
 // 16-byte global -> shared async copy (LDGSTS); valid == false zero-fills.
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, bool valid) {
@@ -798,36 +797,6 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     }
 }
 
-// ------------------------------------------------------------------ B1g
-// d_enc[e] = sum_tile adv[k(tile)] * tile_partial[tile][e]: the advantage-
-// weighted sum of the per-tile attention-backward partials left by the
-// rows-only pass (tiles never straddle samples).  8 tile-slices per element,
-// fixed combine order -> deterministic.
-__global__ void __launch_bounds__(256) weighted_reduce_kernel(const double *__restrict__ src, int n_tiles,
-                                                              size_t stride, int n, double *__restrict__ dst,
-                                                              const double *__restrict__ adv, int tps) {
-    __shared__ double part[kRedSlicesW][32];
-    const int el = threadIdx.x & 31, s = threadIdx.x >> 5;
-    const int e = blockIdx.x * 32 + el;
-    double v0 = 0.0, v1 = 0.0;
-    if (e < n) {
-        int c = s;
-        for (; c + kRedSlicesW < n_tiles; c += 2 * kRedSlicesW) {
-            v0 = fma(adv[c / tps], src[(size_t)c * stride + e], v0);
-            v1 = fma(adv[(c + kRedSlicesW) / tps], src[(size_t)(c + kRedSlicesW) * stride + e], v1);
-        }
-        if (c < n_tiles) v0 = fma(adv[c / tps], src[(size_t)c * stride + e], v0);
-    }
-    part[s][el] = v0 + v1;
-    __syncthreads();
-    if (s == 0 && e < n) {
-        double v = part[0][el];
-#pragma unroll
-        for (int q = 1; q < kRedSlicesW; q++) v += part[q][el];
-        dst[e] = v;
-    }
-}
-
 // ------------------------------------------------------------------ B1a
 // With A = sum_rows alpha^T du (T x dd, advantage-weighted):
 //   d_enc[i, j] += sum_o A[i, o] W_out[64 + j, o]   (== sum_rows alpha^T dctx)
@@ -1147,13 +1116,15 @@ const void *lstm_bwd_fn(int M) {
 
 // ------------------------------------------------------------------ B3
 // partial per CTA: [Hg (64 x 256) | DAsum ((D+1) x 256)]
-// thread (lb = tid>>5, jl = tid&31) owns Hg[lb*8 + a][jl + 32*b] (a, b < 8);
-// thread tid owns DAsum[:, tid].
-// h_prev^T da on the fp64 tensor cores (DMMA m8n8k4): warp w owns m-tiles
-// 2(w&3), 2(w&3)+1 (rows l of Hg) x n-tiles 16(w>>2) .. +16 (columns j);
-// tiles of 32 rows stream through a cp.async double buffer with row strides
-// == 8 (mod 32) words (conflict-free fragment loads); the advantage scales h
-// in shared memory before the products.
+// Hg = (adv o H_prev)^T DA and DAsum[p] = sum over rows whose previous choice
+// is p of adv * da, on the fp64 tensor cores (DMMA m8n8k4): warp w owns
+// m-tiles 2(w&3), 2(w&3)+1 (rows l of Hg) x n-tiles 16(w>>2) .. +16 (columns
+// j); for D+1 <= 8 DAsum is one more m-tile whose A fragment is the one-hot
+// of the row's previous choice times its advantage (warp w: n-tiles
+// 16(w>>2) + 4(w&3) .. +4, reusing the B fragments it already loaded).
+// Tiles of 32 rows (h_prev, da, advantages, choice bytes) stream through a
+// cp.async double buffer with row strides == 8 (mod 32) words (conflict-free
+// fragment loads); the advantage scales the A fragments in registers.
 constexpr int kWgHLd = kH + 4, kWgDLd = kG + 4;
 __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, int rows, int tiles_per_cta,
                                                                 const double *__restrict__ act_h,
@@ -1165,21 +1136,25 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
     extern __shared__ __align__(16) double sm[];
     double *s_h = sm;                              // [2][kTile][kWgHLd]   (cp.async double buffer)
     double *s_da = s_h + 2 * kTile * kWgHLd;       // [2][kTile][kWgDLd]
-    double *s_dasum = s_da + 2 * kTile * kWgDLd;   // [(D+1)][256]
-    __shared__ int s_prev[2][kTile];
+    double *s_dasum = s_da + 2 * kTile * kWgDLd;   // [(D+1)][256] (D+1 > 8 only)
     __shared__ double s_w[2][kTile];               // per-row advantage (1 when already scaled)
+    __shared__ __align__(8) uint8_t s_ch[2][kTile + 8];  // choices of rows rb-8 .. rb+31
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int T = dm.T, D = dm.D;
-    const int mt0 = (wp & 3) * 2, nt0 = (wp >> 2) * 16;
-    double acc[2][16][2];
+    const bool oh = D + 1 <= 8;
+    const int mt0 = (wp & 3) * 2, nt0 = (wp >> 2) * 16, no0 = (wp & 3) * 4;
+    double acc[2][16][2], acc_oh[4][2];
 #pragma unroll
     for (int a = 0; a < 2; a++)
 #pragma unroll
         for (int n = 0; n < 16; n++) acc[a][n][0] = acc[a][n][1] = 0.0;
-    for (int p = 0; p <= D; p++) s_dasum[p * kG + tid] = 0.0;
+#pragma unroll
+    for (int n = 0; n < 4; n++) acc_oh[n][0] = acc_oh[n][1] = 0.0;
+    if (!oh)
+        for (int p = 0; p <= D; p++) s_dasum[p * kG + tid] = 0.0;
     const int n_tiles = (rows + kTile - 1) / kTile;
     const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
-    // async copy of tile tl into buffer b (16-byte cp.async, zero-fill past the end)
+    // async copy of tile tl into buffer b (cp.async, zero-fill past the end)
     auto stage = [&](int tl, int b) {
         const int rb = tl * kTile;
         double *h = s_h + b * kTile * kWgHLd, *d = s_da + b * kTile * kWgDLd;
@@ -1196,10 +1171,17 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
         }
         if (tid < kTile) {
             const int row = rb + tid;
-            int pv = D;
-            if (row < rows && row % T > 0) pv = choice[row - 1];
-            s_prev[b][tid] = pv;
-            s_w[b][tid] = row < rows ? (adv ? adv[row / T] : 1.0) : 0.0;
+            const bool ok = row < rows;
+            if (adv) cp_async8(&s_w[b][tid], adv + (ok ? row / T : 0), ok);
+            else s_w[b][tid] = ok ? 1.0 : 0.0;
+        } else if (tid < kTile + (kTile + 8) / 8) {
+            // 8-byte words of the choice bytes of rows rb-8 .. rb+31 (rb is 32-aligned)
+            const int q = tid - kTile, row = rb - 8 + 8 * q;
+            if (row >= 0 && row + 8 <= rows) {
+                cp_async8(&s_ch[b][8 * q], choice + row, true);
+            } else {
+                for (int e = 0; e < 8; e++) s_ch[b][8 * q + e] = row + e >= 0 && row + e < rows ? choice[row + e] : 0;
+            }
         }
         cp_async_commit();
     };
@@ -1214,28 +1196,34 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
             cp_async_wait<0>();
         }
         __syncthreads();
-        double *h = s_h + b * kTile * kWgHLd;
+        const double *h = s_h + b * kTile * kWgHLd;
         const double *d = s_da + b * kTile * kWgDLd;
-        if (adv) {  // grads-only: da is unscaled -> scale h by the row's advantage
-            for (int x = tid; x < kTile * kH; x += kThreads) {
-                const int r = x >> 6, l = x & 63;
-                h[r * kWgHLd + l] *= s_w[b][r];
-            }
-            __syncthreads();
-        }
 #pragma unroll 2
         for (int ks = 0; ks < kTile / 4; ks++) {
-            const int r = ks * 4 + t;
-            const double a0 = h[r * kWgHLd + mt0 * 8 + g], a1 = h[r * kWgHLd + (mt0 + 1) * 8 + g];
+            const int r = ks * 4 + t, row = rb + r;
+            const double wr = s_w[b][r];
+            const double a0 = h[r * kWgHLd + mt0 * 8 + g] * wr, a1 = h[r * kWgHLd + (mt0 + 1) * 8 + g] * wr;
+            // one-hot A fragment: row r's previous choice (D at the sequence start)
+            const int pv = row % T > 0 ? (int)s_ch[b][r + 7] : D;
+            const double ao = pv == g ? wr : 0.0;
 #pragma unroll
             for (int n = 0; n < 16; n++) {
                 const double bb = d[r * kWgDLd + (nt0 + n) * 8 + g];
                 dmma884(acc[0][n], a0, bb);
                 dmma884(acc[1][n], a1, bb);
             }
+            if (oh)
+#pragma unroll
+                for (int n = 0; n < 4; n++) dmma884(acc_oh[n], ao, d[r * kWgDLd + (nt0 + no0 + n) * 8 + g]);
         }
-        const int nr = min(kTile, rows - rb);
-        for (int r = 0; r < nr; r++) s_dasum[s_prev[b][r] * kG + tid] += s_w[b][r] * d[r * kWgDLd + tid];
+        if (!oh) {
+            const int nr = min(kTile, rows - rb);
+            for (int r = 0; r < nr; r++) {
+                const int row = rb + r;
+                const int pv = row % T > 0 ? (int)s_ch[b][r + 7] : D;
+                s_dasum[pv * kG + tid] += s_w[b][r] * d[r * kWgDLd + tid];
+            }
+        }
         __syncthreads();  // buffer b is re-staged by the next iteration
     }
     const size_t base = (size_t)blockIdx.x * (kH + D + 1) * kG;
@@ -1245,44 +1233,100 @@ __global__ void __launch_bounds__(kThreads, 1) dec_wgrad_kernel(PolicyDims dm, i
         for (int n = 0; n < 16; n++)
             *reinterpret_cast<double2 *>(partial + base + (size_t)((mt0 + a) * 8 + g) * kG + (nt0 + n) * 8 + 2 * t) =
                 make_double2(acc[a][n][0], acc[a][n][1]);
-    for (int p = 0; p <= D; p++) partial[base + (size_t)(kH + p) * kG + tid] = s_dasum[p * kG + tid];
+    if (oh) {
+        if (g <= D)
+#pragma unroll
+            for (int n = 0; n < 4; n++)
+                *reinterpret_cast<double2 *>(partial + base + (size_t)(kH + g) * kG + (nt0 + no0 + n) * 8 + 2 * t) =
+                    make_double2(acc_oh[n][0], acc_oh[n][1]);
+    } else {
+        for (int p = 0; p <= D; p++) partial[base + (size_t)(kH + p) * kG + tid] = s_dasum[p * kG + tid];
+    }
 }
 
 // ------------------------------------------------------------------ reductions
-// dst[e] (+)= sum_c src[c * stride + e].  Block = 32 elements x 8 c-slices:
-// thread (e, s) sums c = s, s+8, ... with 2 accumulators; the 8 slice sums are
-// combined in a fixed order -> deterministic, and 8x the memory parallelism
-// of a thread-per-element loop (the partials are latency-, not BW-bound).
-constexpr int kRedSlices = 8;
-
-__global__ void __launch_bounds__(256) reduce_partials_kernel(const double *__restrict__ src, int n_cta,
-                                                              size_t stride, int n, double *__restrict__ dst,
-                                                              int accumulate) {
-    __shared__ double part[kRedSlices][32];
+// dst[e] (+)= sum_c (w[c / tps] *) src[c * stride + e] for up to 4 (src,
+// stride, n, dst) segments in one launch (block ranges b0[i] .. b0[i+1]).
+// Block = 32 elements x 16 c-slices, 4 loads in flight per thread; the slice
+// sums combine in a fixed order -> deterministic (the partials are latency-,
+// not bandwidth-bound).  w != NULL: advantage-weighted per-sample partials.
+constexpr int kRedSl = 16;
+struct RedSegs {
+    const double *src[4];
+    double *dst[4];
+    size_t stride[4];
+    int n[4];
+    int b0[5];
+    int count;
+};
+__global__ void __launch_bounds__(32 * kRedSl) reduce_multi_kernel(RedSegs sg, int n_cta, int accumulate,
+                                                                   const double *__restrict__ w, int tps) {
+    __shared__ double part[kRedSl][32];
     const int el = threadIdx.x & 31, s = threadIdx.x >> 5;
-    const int e = blockIdx.x * 32 + el;
-    double v0 = 0.0, v1 = 0.0;
+    int i = 0;
+    while (i + 1 < sg.count && (int)blockIdx.x >= sg.b0[i + 1]) i++;
+    const double *src = sg.src[i];
+    const size_t stride = sg.stride[i];
+    const int n = sg.n[i];
+    const int e = (blockIdx.x - sg.b0[i]) * 32 + el;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
     if (e < n) {
         int c = s;
-        for (; c + kRedSlices < n_cta; c += 2 * kRedSlices) {
-            v0 += src[(size_t)c * stride + e];
-            v1 += src[(size_t)(c + kRedSlices) * stride + e];
+        for (; c + 3 * kRedSl < n_cta; c += 4 * kRedSl) {
+            const double x0 = src[(size_t)c * stride + e], x1 = src[(size_t)(c + kRedSl) * stride + e];
+            const double x2 = src[(size_t)(c + 2 * kRedSl) * stride + e];
+            const double x3 = src[(size_t)(c + 3 * kRedSl) * stride + e];
+            if (w) {
+                v0 = fma(w[c / tps], x0, v0);
+                v1 = fma(w[(c + kRedSl) / tps], x1, v1);
+                v2 = fma(w[(c + 2 * kRedSl) / tps], x2, v2);
+                v3 = fma(w[(c + 3 * kRedSl) / tps], x3, v3);
+            } else {
+                v0 += x0;
+                v1 += x1;
+                v2 += x2;
+                v3 += x3;
+            }
         }
-        if (c < n_cta) v0 += src[(size_t)c * stride + e];
+        for (; c < n_cta; c += kRedSl) {
+            const double x = src[(size_t)c * stride + e];
+            v0 = w ? fma(w[c / tps], x, v0) : v0 + x;
+        }
     }
-    part[s][el] = v0 + v1;
+    part[s][el] = (v0 + v1) + (v2 + v3);
     __syncthreads();
     if (s == 0 && e < n) {
         double v = part[0][el];
 #pragma unroll
-        for (int q = 1; q < kRedSlices; q++) v += part[q][el];
+        for (int q = 1; q < kRedSl; q++) v += part[q][el];
+        double *dst = sg.dst[i];
         dst[e] = accumulate ? dst[e] + v : v;
     }
 }
 
+struct RedBuilder {
+    RedSegs sg{};
+    int blocks = 0;
+    void add(const double *src, size_t stride, int n, double *dst) {
+        const int i = sg.count++;
+        sg.src[i] = src;
+        sg.dst[i] = dst;
+        sg.stride[i] = stride;
+        sg.n[i] = n;
+        sg.b0[i] = blocks;
+        blocks += (n + 31) / 32;
+        sg.b0[i + 1] = blocks;
+    }
+    void launch(int n_cta, int accumulate, cudaStream_t st, const double *w = nullptr, int tps = 1) {
+        if (blocks) reduce_multi_kernel<<<blocks, 32 * kRedSl, 0, st>>>(sg, n_cta, accumulate, w, tps);
+    }
+};
+
 inline void launch_reduce(const double *src, int n_cta, size_t stride, int n, double *dst, int accumulate,
                           cudaStream_t st) {
-    reduce_partials_kernel<<<(n + 31) / 32, 256, 0, st>>>(src, n_cta, stride, n, dst, accumulate);
+    RedBuilder rb;
+    rb.add(src, stride, n, dst);
+    rb.launch(n_cta, accumulate, st);
 }
 
 // B3 finalize: b_dec = sum_p DAsum[p]; w_dec[:dd] = sum_p dev_table[p] x DAsum[p];
@@ -1723,13 +1767,12 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
                                                          p->act_p, p->act_choice, part);
         DP_LAUNCH_CHECK();
         const size_t na = adv_grads_partial(dm);
-        launch_reduce(part, n_cta, na, dm.D, grad + dm.off.b_out, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(part + dm.D, n_cta, na, dm.D * dm.dd, grad + dm.off.dev_table, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(part + dm.D + dm.D * dm.dd, n_cta, na, kH * dm.dd, grad + dm.off.w_out, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(part + dm.D + dm.D * dm.dd + kH * dm.dd, n_cta, na, kH * kH, grad + dm.off.w_att, 0, st);
+        RedBuilder rb;
+        rb.add(part, na, dm.D, grad + dm.off.b_out);
+        rb.add(part + dm.D, na, dm.D * dm.dd, grad + dm.off.dev_table);
+        rb.add(part + dm.D + dm.D * dm.dd, na, kH * dm.dd, grad + dm.off.w_out);
+        rb.add(part + dm.D + dm.D * dm.dd + kH * dm.dd, na, kH * kH, grad + dm.off.w_att);
+        rb.launch(n_cta, 0, st);
         DP_LAUNCH_CHECK();
     }
     // B3
@@ -1741,9 +1784,10 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
                                                            p->act_g, part, adv);
         DP_LAUNCH_CHECK();
         const size_t stride = (size_t)(kH + dm.D + 1) * kG;
-        launch_reduce(part, g.n_used, stride, kH * kG, grad + dm.off.w_dec + (size_t)dm.dd * kG, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(part + (size_t)kH * kG, g.n_used, stride, (dm.D + 1) * kG, p->gacc, 0, st);
+        RedBuilder rb;
+        rb.add(part, stride, kH * kG, grad + dm.off.w_dec + (size_t)dm.dd * kG);
+        rb.add(part + (size_t)kH * kG, stride, (dm.D + 1) * kG, p->gacc);
+        rb.launch(g.n_used, 0, st);
         DP_LAUNCH_CHECK();
         dec_finalize_kernel<<<1 + ceil_div((dm.D + 1) * dm.dd, kG / 32), kG, 0, st>>>(dm, params, p->gacc, grad);
         DP_LAUNCH_CHECK();
@@ -1824,11 +1868,10 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
     {
         // per-sample partials (1 unit per sample) or per-tile (tps units per sample)
         const int tps = p->att_per_sample ? 1 : (T + kAttTile - 1) / kAttTile;
-        weighted_reduce_kernel<<<ceil_div(T * kH, 32), 256, 0, st>>>(p->tile_part, K * tps, (size_t)T * kH, T * kH,
-                                                                     p->d_enc, adv, tps);
-        DP_LAUNCH_CHECK();
-        weighted_reduce_kernel<<<ceil_div(T * dm.dd, 32), 256, 0, st>>>(p->tile_partA, K * tps, (size_t)T * dm.dd,
-                                                                        T * dm.dd, p->a_tot, adv, tps);
+        RedBuilder rb;
+        rb.add(p->tile_part, (size_t)T * kH, T * kH, p->d_enc);
+        rb.add(p->tile_partA, (size_t)T * dm.dd, T * dm.dd, p->a_tot);
+        rb.launch(K * tps, 0, st, adv, tps);
         DP_LAUNCH_CHECK();
     }
     DP_TRY(run_att_fin(p, params, grad, st));
