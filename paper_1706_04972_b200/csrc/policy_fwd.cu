@@ -292,7 +292,7 @@ struct DecArgs {
     int M, Tpad, ewld;
     // shared-memory offsets (doubles)
     int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_uh, o_alpha, o_pm, o_ps, o_puc, o_pz, o_gn, o_hc,
-        o_cc, o_ac, o_pcg, o_misc, o_v, o_wo;
+        o_cc, o_ac, o_pcg, o_misc, o_v, o_wo, o_rn;
 };
 
 // q = x / n for 0 <= x < MT * n without an integer division (MT <= 8)
@@ -329,7 +329,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 //       with h = candidate[choice] and phase A disappears from the chain.
 // The context vector is never formed: ctx @ W_out[64:] = alpha @ encW, and the
 // backward works from uc (w = uc.du, dW_out[64:] = enc^T sum alpha^T du).
-template <int MT, bool PS, bool SPEC>
+// FAST (MT <= 2, D <= 4, dd <= 16, T <= 256, proj in shared memory, no SPEC):
+// the generic alternatives are compiled out, so the per-step loop's hot code
+// is compact (the draw chain measurably stalls on instruction fetch when it
+// jumps across the cold paths).
+template <int MT, bool PS, bool SPEC, bool FAST = false>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -358,6 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     double *aC = sm + a.o_ac;       // (SPEC) [M][D][256] candidate gate activations
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);  // [2][M] previous choice, by step parity
+    double *rnext = sm + a.o_rn;  // [2][M] the step's uniform, by step parity (pcg warps)
+    // pcg warps: with 3 Mb <= 8 warps, warp 2 Mb + m steps sample m's PCG64 stream
+    // during E and leaves the next step's uniform in rnext (off the draw chain)
+    const bool pcgw = FAST || 3 * Mb <= kWarps;
     const double *edev = SPEC ? a.edev : edevS;
     // softmax over the T scores without the max shift when |s| is provably small
     const bool noshift = 8.0 * __longlong_as_double((long long)*a.proj_nmax) <= kNoShiftBound;
@@ -389,7 +397,11 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             const long long kg = a.k_offset + k0 + tid;
             unsigned long long n0 = a.draw_base + (unsigned long long)kg * (unsigned long long)T;
             if (a.draw_counter) n0 += (unsigned long long)(*a.draw_counter) * (unsigned long long)a.draws_per_count;
-            const u128 s = pcg_jump(u128{a.st_hi, a.st_lo}, u128{a.inc_hi, a.inc_lo}, n0);
+            u128 s = pcg_jump(u128{a.st_hi, a.st_lo}, u128{a.inc_hi, a.inc_lo}, n0);
+            if (3 * Mb <= kWarps) {  // pcgw: step 0's uniform up front
+                s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
+                rnext[tid] = pcg_double(s);
+            }
             pcg[2 * tid] = s.hi;
             pcg[2 * tid + 1] = s.lo;
         }
@@ -557,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     }
                 }
         }
-        for (int i = tid + kThreads; i < T; i += kThreads) {
+        for (int i = tid + kThreads; i < (FAST ? 0 : T); i += kThreads) {
             const double2 *pr = reinterpret_cast<const double2 *>(proj + (size_t)i * LD);
             double s0[MT], s1[MT];
 #pragma unroll
@@ -639,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
         // fast E (D <= 4, dd <= 16, spare warps): the draw warp forms the logits
         // itself (h . vdev + dev_table . sum_w uc_w) -> no pz partials, no uh here
-        const bool fastE = D <= 4 && dd <= 16 && 2 * Mb <= kWarps;
+        const bool fastE = FAST || (D <= 4 && dd <= 16 && 2 * Mb <= kWarps);
         // pz_w[m][d] = dev_table[d] . uc_w[m]
         if (fastE) {
         } else if (dd == 16 && Mb <= 2) {
@@ -707,63 +719,22 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         // ---- E: combine, logits, softmax over devices, draw (policy.py:297-308, 320-323) ----
         // warp m < Mb runs sample m's draw chain; when there are spare warps, warp
         // Mb + m does the sample's off-chain stores (u, uc, the alpha scales)
-        const bool split = 2 * Mb <= kWarps;
-        if (split && warp >= Mb && warp < 2 * Mb) {
-            const int m = warp - Mb;
-            const size_t row = (size_t)(k0 + m) * T + t;
-            double gmx = 0.0, f = lane < kWarps ? 1.0 : 0.0;
-            double fw[kWarps];
-#pragma unroll
-            for (int ww = 0; ww < kWarps; ww++) fw[ww] = 1.0;
-            if (!noshift) {
-                gmx = pmx[m];
-#pragma unroll
-                for (int ww = 1; ww < kWarps; ww++) gmx = fmax(gmx, pmx[ww * M + m]);
-                f = lane < kWarps ? fm_exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
-#pragma unroll
-                for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
-            }
-            double gsum = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
-            if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
-            const int lo = lane < dd ? lane : dd - 1;
-            double uc = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
-            const double ucn = fm_div(uc, gsum);
-            double uh;
-            if (fastE) {
-                // uh[o] = h . W_out[:64, o]: lanes (o, half) sum 32 terms each
-                const double *hv = (SPEC ? hC + (m * D + prv[m]) * kH : hS + m * kH) + (lane >> 4) * 32;
-                const double *wc = woS + (lane >> 4) * 32 * dd + ((lane & 15) < dd ? (lane & 15) : dd - 1);
-                double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
-#pragma unroll
-                for (int l = 0; l < 32; l += 4) {
-                    u0 = fma(hv[l], wc[l * dd], u0);
-                    u1 = fma(hv[l + 1], wc[(l + 1) * dd], u1);
-                    u2 = fma(hv[l + 2], wc[(l + 2) * dd], u2);
-                    u3 = fma(hv[l + 3], wc[(l + 3) * dd], u3);
-                }
-                const double part = (u0 + u1) + (u2 + u3);
-                uh = part + __shfl_xor_sync(0xffffffffu, part, 16);
-            } else {
-                uh = uhS[m * 32 + lo];
-            }
-            if (lane < dd) {
-                a.act_u[row * dd + lane] = uh + ucn;
-                a.act_uc[row * dd + lane] = ucn;
-            }
-        }
+        const bool split = FAST || 2 * Mb <= kWarps;
+        // the draw warps' chain first in program order: they fall through into it
+        // after the barrier (the helper / pcg warps jump)
         for (int m = warp; m < Mb; m += kWarps) {
             const size_t row = (size_t)(k0 + m) * T + t;
-            // next uniform (every lane steps the same PCG64 state; lane 0 keeps it)
-            double r = 0.0;
+            // the step's uniform: precomputed by the pcg warp, or (no spare warps)
+            // stepped here — every lane steps the same PCG64 state, lane 0 keeps it
             u128 rs{0, 0};
-            if (!a.forced) {
+            double r;
+            if (pcgw) {
+                r = rnext[par * M + m];
+            } else {
                 rs = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
                 r = pcg_double(rs);
             }
+            DP_MARK(12, r);
             double gmx = 0.0, f = lane < kWarps ? 1.0 : 0.0;
             double fw[kWarps];
 #pragma unroll
@@ -856,7 +827,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             const double ez = lane < D ? ezv : 0.0;
             // numpy pairwise order over the D terms (np_sum_small), identical in every lane
             double esum;
-            if (D < 8) {
+            if (FAST || D < 8) {
                 double ev[8];
 #pragma unroll
                 for (int dv = 0; dv < 8; dv++) ev[dv] = __shfl_sync(0xffffffffu, ez, dv);
@@ -888,7 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             } else {
                 double cdf = 0.0;
                 int cnt = 0;
-                if (D <= 8) {
+                if (FAST || D <= 8) {
                     double pv[8];
 #pragma unroll
                     for (int dv = 0; dv < 8; dv++) pv[dv] = __shfl_sync(0xffffffffu, pr, dv);
@@ -909,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             const double zsc = __shfl_sync(0xffffffffu, zs, ch);
             if (clk_on) { const long long now_ = clock64() + ch * 0; clk_acc[6] += now_ - clk_last; clk_last = now_; }
             if (lane == 0) {
-                if (!a.forced) {
+                if (!a.forced && !pcgw) {
                     pcg[2 * m] = rs.hi;  // every lane has read the state by now (the cdf shuffles)
                     pcg[2 * m + 1] = rs.lo;
                 }
@@ -922,6 +893,60 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 a.act_stat[row * 2] = gmx;
                 a.act_stat[row * 2 + 1] = gsum;
             }
+        }
+        if (split && warp >= Mb && warp < 2 * Mb) {
+            const int m = warp - Mb;
+            const size_t row = (size_t)(k0 + m) * T + t;
+            double gmx = 0.0, f = lane < kWarps ? 1.0 : 0.0;
+            double fw[kWarps];
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) fw[ww] = 1.0;
+            if (!noshift) {
+                gmx = pmx[m];
+#pragma unroll
+                for (int ww = 1; ww < kWarps; ww++) gmx = fmax(gmx, pmx[ww * M + m]);
+                f = lane < kWarps ? fm_exp(pmx[(lane & (kWarps - 1)) * M + m] - gmx) : 0.0;
+#pragma unroll
+                for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
+            }
+            double gsum = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
+            if (a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
+            const int lo = lane < dd ? lane : dd - 1;
+            double uc = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < kWarps; ww++) uc = fma(puc[(ww * M + m) * dd + lo], fw[ww], uc);
+            const double ucn = fm_div(uc, gsum);
+            double uh;
+            if (fastE) {
+                // uh[o] = h . W_out[:64, o]: lanes (o, half) sum 32 terms each
+                const double *hv = (SPEC ? hC + (m * D + prv[m]) * kH : hS + m * kH) + (lane >> 4) * 32;
+                const double *wc = woS + (lane >> 4) * 32 * dd + ((lane & 15) < dd ? (lane & 15) : dd - 1);
+                double u0 = 0.0, u1 = 0.0, u2 = 0.0, u3 = 0.0;
+#pragma unroll
+                for (int l = 0; l < 32; l += 4) {
+                    u0 = fma(hv[l], wc[l * dd], u0);
+                    u1 = fma(hv[l + 1], wc[(l + 1) * dd], u1);
+                    u2 = fma(hv[l + 2], wc[(l + 2) * dd], u2);
+                    u3 = fma(hv[l + 3], wc[(l + 3) * dd], u3);
+                }
+                const double part = (u0 + u1) + (u2 + u3);
+                uh = part + __shfl_xor_sync(0xffffffffu, part, 16);
+            } else {
+                uh = uhS[m * 32 + lo];
+            }
+            if (lane < dd) {
+                a.act_u[row * dd + lane] = uh + ucn;
+                a.act_uc[row * dd + lane] = ucn;
+            }
+        }
+        if (pcgw && !a.forced && warp >= 2 * Mb && warp < 3 * Mb && lane == 0) {
+            const int m = warp - 2 * Mb;
+            const u128 ns = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
+            pcg[2 * m] = ns.hi;
+            pcg[2 * m + 1] = ns.lo;
+            rnext[(par ^ 1) * M + m] = pcg_double(ns);
         }
         if (SPEC && warp >= Mb && t + 1 < T) {
             // next step's LSTM cell for every possible choice d (the idle warps)
@@ -1271,6 +1296,7 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             a.o_ac = spec ? take(M * D * kG) : 0;
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + 2 * M);
+            a.o_rn = take(2 * M);
             a.o_v = take(kH * D);
             a.o_wo = take(kH * dd);
             const size_t bytes = (size_t)o * sizeof(double);
@@ -1290,7 +1316,9 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
 }
 
 template <bool PS, bool SPEC>
-const void *dec_fn(int MT) {
+const void *dec_fn(int MT, bool fast) {
+    if (PS && !SPEC && fast) return MT == 1 ? (const void *)dec_kernel<1, PS, false, true>
+                                            : (const void *)dec_kernel<2, PS, false, true>;
     if (SPEC)
         return MT == 1 ? (const void *)dec_kernel<1, PS, SPEC>
                : MT == 2 ? (const void *)dec_kernel<2, PS, SPEC>
@@ -1356,8 +1384,9 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.ewld = ((dm.T + 1) & ~1) + 2;
     const int grid = ceil_div(K, pl.M);
     cudaStream_t st = (cudaStream_t)stream;
-    const void *fn = pl.enc_in_smem ? (pl.spec ? dec_fn<true, true>(pl.MT) : dec_fn<true, false>(pl.MT))
-                                    : (pl.spec ? dec_fn<false, true>(pl.MT) : dec_fn<false, false>(pl.MT));
+    const bool fast = pl.MT <= 2 && dm.D <= 4 && dm.dd <= 16 && dm.T <= kThreads;
+    const void *fn = pl.enc_in_smem ? (pl.spec ? dec_fn<true, true>(pl.MT, false) : dec_fn<true, false>(pl.MT, fast))
+                                    : (pl.spec ? dec_fn<false, true>(pl.MT, false) : dec_fn<false, false>(pl.MT, false));
     DP_CUDA_TRY(allow_big_smem(fn, pl.smem));
     void *args[] = {&a};
     DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));

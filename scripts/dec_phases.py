@@ -40,6 +40,6 @@ for n, v in zip(names, out[:3]):
 if any(out[3:8]):
     for n, v in zip(["E: ->gsum", "E: ->z", "E: ->pr", "E: ->ch", "E: ->pre-barrier"], out[3:8]):
         print(f"  {n:32s} {v / T:8.0f} cycles/step")
-if any(out[8:12]):
-    for n, v in zip(["A: ->act", "A: ->cn", "A: ->hn", "A: ->stores"], out[8:12]):
+if any(out[8:14]):
+    for n, v in zip(["A: ->act", "A: ->cn", "A: ->hn", "A: ->stores", "E: ->r", "E: (13)"], out[8:14]):
         print(f"  {n:32s} {v / T:8.0f} cycles/step")
