@@ -450,13 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
     const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
     long long clk_last = clk_on ? clock64() : 0;
-    long long clk_acc[16] = {};  // in registers; one global write at the end
-#define DP_MARK(i, dep)                                                                           \
-    if (clk_on) {                                                                                 \
-        const long long now_ = clock64() + (long long)((dep) * 0.0);                              \
-        clk_acc[i] += now_ - clk_last;                                                            \
-        clk_last = now_;                                                                          \
-    }
+    long long clk_acc[3] = {0, 0, 0};  // in registers; one global write at the end
 #define DP_PHASE(i)                                       \
     if (clk_on) {                                         \
         const long long now_ = clock64();                 \
@@ -477,7 +471,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             double act[MT], cn[MT], hn[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++) act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
-            DP_MARK(8, act[0] + act[MT - 1]);
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) actg[m * sG] = act[m];
@@ -490,10 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 cn[m] = fv * cst[m] + iv * gv;
                 act[m] = ov;
             }
-            DP_MARK(9, cn[0] + cn[MT - 1]);
 #pragma unroll
             for (int m = 0; m < MT; m++) hn[m] = act[m] * tanh_x(cn[m]);
-            DP_MARK(10, hn[0] + hn[MT - 1]);
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb && gate == 0) {
@@ -502,7 +493,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     acth[m * sH] = hn[m];
                     actc[m * sH] = cn[m];
                 }
-            DP_MARK(11, 0.0);
             __syncthreads();
         }
         DP_PHASE(0);
@@ -734,7 +724,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 rs = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
                 r = pcg_double(rs);
             }
-            DP_MARK(12, r);
             double gmx = 0.0, f = lane < kWarps ? 1.0 : 0.0;
             double fw[kWarps];
 #pragma unroll
@@ -750,7 +739,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             double gsum = 0.0;
 #pragma unroll
             for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
-            if (clk_on) { const long long now_ = clock64() + (long long)(gsum * 0.0); clk_acc[3] += now_ - clk_last; clk_last = now_; }
             if (!split && a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
             // all lanes compute (clamped indices, no divergent branches: the z, uc
             // and pcg chains interleave); lanes >= D / >= dd are masked at the end
@@ -806,7 +794,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
             const double zv = (zh + fm_div(zc, gsum)) + bout[ld];
             const double z = lane < D ? zv : -INFINITY;
-            if (clk_on) { const long long now_ = clock64() + (long long)(z * 0.0 + 0.5); clk_acc[4] += now_ - clk_last; clk_last = now_; }
             if (!split) {
                 // u (and its context half uc) for the backward
                 double uc = 0.0;
@@ -848,7 +835,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 for (; i < D; i++) esum += __shfl_sync(0xffffffffu, ez, i);
             }
             const double pr = fm_div(ez, esum);
-            if (clk_on) { const long long now_ = clock64() + (long long)(pr * 0.0); clk_acc[5] += now_ - clk_last; clk_last = now_; }
             if (lane < D) {
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
@@ -878,7 +864,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 ch = cnt < D - 1 ? cnt : D - 1;
             }
             const double zsc = __shfl_sync(0xffffffffu, zs, ch);
-            if (clk_on) { const long long now_ = clock64() + ch * 0; clk_acc[6] += now_ - clk_last; clk_last = now_; }
             if (lane == 0) {
                 if (!a.forced && !pcgw) {
                     pcg[2 * m] = rs.hi;  // every lane has read the state by now (the cdf shuffles)
@@ -976,14 +961,13 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         if (!SPEC) {
             // gn for the non-speculative A of the next step is already in registers
         }
-        if (clk_on) { const long long now_ = clock64(); clk_acc[7] += now_ - clk_last; clk_last = now_; }
         __syncthreads();
         DP_PHASE(2);
     }
 #undef DP_PHASE
     if (clk_on)
 #pragma unroll
-        for (int i = 0; i < 16; i++) g_phase_clk[i] += clk_acc[i];
+        for (int i = 0; i < 3; i++) g_phase_clk[i] += clk_acc[i];
     // ---- log p = sum_t (zs[c_t] - log sum_t): logs in parallel, sum in t order ----
     __threadfence_block();
     for (int m = 0; m < Mb; m++) {

@@ -33,13 +33,7 @@ torch.cuda.synchronize()
 nat.check(nat.lib().dp_debug_phase_clocks(0, out), "dbg")
 T = len(feats)
 names = ["A gates+cell", "C scores/softmax/uc/uh/next-g", "E combine+draw"]
-tot = sum(out[:3]) + sum(out[3:8])
+tot = sum(out[:3])
 print(f"{name} K={K} T={T} variant={variant} skip={skip}: {tot / T:.0f} cycles/step")
 for n, v in zip(names, out[:3]):
     print(f"  {n:32s} {v / T:8.0f} cycles/step  {100 * v / tot:5.1f}%")
-if any(out[3:8]):
-    for n, v in zip(["E: ->gsum", "E: ->z", "E: ->pr", "E: ->ch", "E: ->pre-barrier"], out[3:8]):
-        print(f"  {n:32s} {v / T:8.0f} cycles/step")
-if any(out[8:14]):
-    for n, v in zip(["A: ->act", "A: ->cn", "A: ->hn", "A: ->stores", "E: ->r", "E: (13)"], out[8:14]):
-        print(f"  {n:32s} {v / T:8.0f} cycles/step")
