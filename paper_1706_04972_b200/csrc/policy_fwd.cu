@@ -807,20 +807,21 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             }
             double zmax = z;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-                if (o < d_pow2) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+            for (int o = FAST ? 2 : 16; o > 0; o >>= 1)  // FAST: D <= 4, lanes >= D hold -inf
+                if (FAST || o < d_pow2) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
             const double zs = z - zmax;
             const double ezv = fm_exp(lane < D ? zs : -1000.0);
             const double ez = lane < D ? ezv : 0.0;
             // numpy pairwise order over the D terms (np_sum_small), identical in every lane
             double esum;
             if (FAST || D < 8) {
-                double ev[8];
+                constexpr int DG = FAST ? 4 : 8;  // lanes gathered
+                double ev[DG];
 #pragma unroll
-                for (int dv = 0; dv < 8; dv++) ev[dv] = __shfl_sync(0xffffffffu, ez, dv);
+                for (int dv = 0; dv < DG; dv++) ev[dv] = __shfl_sync(0xffffffffu, ez, dv);
                 esum = 0.0;
 #pragma unroll
-                for (int dv = 0; dv < 8; dv++)
+                for (int dv = 0; dv < DG; dv++)
                     if (dv < D) esum += ev[dv];
             } else {
                 double rr[8];
@@ -846,11 +847,12 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 double cdf = 0.0;
                 int cnt = 0;
                 if (FAST || D <= 8) {
-                    double pv[8];
+                    constexpr int DG = FAST ? 4 : 8;  // lanes gathered
+                    double pv[DG];
 #pragma unroll
-                    for (int dv = 0; dv < 8; dv++) pv[dv] = __shfl_sync(0xffffffffu, pr, dv);
+                    for (int dv = 0; dv < DG; dv++) pv[dv] = __shfl_sync(0xffffffffu, pr, dv);
 #pragma unroll
-                    for (int dv = 0; dv < 8; dv++)
+                    for (int dv = 0; dv < DG; dv++)
                         if (dv < D) {
                             cdf += pv[dv];
                             cnt += (cdf <= r) ? 1 : 0;
