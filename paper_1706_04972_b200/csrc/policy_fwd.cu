@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
     }
     const double c_init = a.enc_c[(size_t)(T - 1) * kH + u];
-    double cst[MT];  // (non-SPEC) cell state of unit u, owned by the unit's gate-0 thread
+    double cst[MT];  // (non-SPEC) cell state of unit u, sample m: owned by lane m of the quad (MT <= 4), else gate 0
 #pragma unroll
     for (int m = 0; m < MT; m++) cst[m] = c_init;
     const int base = lane & ~3;
@@ -483,16 +483,37 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 cn[m] = fv * cst[m] + iv * gv;
                 act[m] = ov;
             }
+            if (MT <= 4) {
+                // lane q of the unit's quad finishes sample q: one tanh per lane
+                // (cst[m] is current only in lane m, which is the only reader)
+                double cq = cn[0], oq = act[0];
 #pragma unroll
-            for (int m = 0; m < MT; m++) hn[m] = act[m] * tanh_x(cn[m]);
+                for (int m = 1; m < MT; m++)
+                    if (gate == m) {
+                        cq = cn[m];
+                        oq = act[m];
+                    }
+                const double hq = oq * tanh_x(cq);
 #pragma unroll
-            for (int m = 0; m < MT; m++)
-                if (m < Mb && gate == 0) {
-                    cst[m] = cn[m];
-                    hS[m * kH + u] = hn[m];
-                    acth[m * sH] = hn[m];
-                    actc[m * sH] = cn[m];
-                }
+                for (int m = 0; m < MT; m++)
+                    if (gate == m && m < Mb) {
+                        cst[m] = cq;
+                        hS[m * kH + u] = hq;
+                        acth[m * sH] = hq;
+                        actc[m * sH] = cq;
+                    }
+            } else {
+#pragma unroll
+                for (int m = 0; m < MT; m++) hn[m] = act[m] * tanh_x(cn[m]);
+#pragma unroll
+                for (int m = 0; m < MT; m++)
+                    if (m < Mb && gate == 0) {
+                        cst[m] = cn[m];
+                        hS[m * kH + u] = hn[m];
+                        acth[m * sH] = hn[m];
+                        actc[m * sH] = cn[m];
+                    }
+            }
             __syncthreads();
         }
         DP_PHASE(0);
