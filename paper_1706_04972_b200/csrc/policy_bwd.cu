@@ -82,9 +82,13 @@ struct PrepSmem {
     double watt[kH * kPadH];        // W_att[l][j]
     double woutT[kMaxDD * kWoLd];   // W_out^T [o][i]  (rows o >= dd zero)
     double devt[kMaxD * kMaxDD];    // dev_table[:D] [d][o]
-    double h[kTile * kPadH];        // [r][l]
-    double uc[kTile * (kMaxDD + 1)];  // ctx @ W_out[64:]
-    double u[kTile * (kMaxDD + 1)];
+    // cp.async double buffer of the tile's row operands (raw copies)
+    double h[2][kTile * kPadH];     // [r][l]
+    double uc[2][kTile * kMaxDD];   // ctx @ W_out[64:], rows of dd
+    double u[2][kTile * kMaxDD];    // rows of dd
+    double p[2][kTile * kMaxD];     // rows of D
+    double w[2][kTile];             // per-row advantage (grads modes)
+    uint8_t ch[2][kTile];
     double du[kTile * kDuLd];       // (cols >= dd zero)
     double dz[kTile * (kMaxD + 1)];
 };
@@ -101,8 +105,42 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     const bool rows_out = mode != kGradsOnly, grads_out = mode != kRowsOnly;
     const int tid = threadIdx.x;
     const int D = dm.D, dd = dm.dd, T = dm.T;
-    const int ddp = dd + 1, Dp = D + 1;
+    const int Dp = D + 1;
     const int dd4 = (dd + 3) & ~3;  // DMMA k extent of the du @ W_out^T product
+    const int n_tiles = (rows + kTile - 1) / kTile;
+    const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
+    // tile tl's rows -> buffer b, all asynchronous (zero-filled past the end)
+    auto stage = [&](int tl, int b) {
+        const int rb = tl * kTile;
+        for (int x = tid * 2; x < kTile * kH; x += kThreads * 2) {
+            const int r = x >> 6, j = x & 63;
+            const bool ok = rb + r < rows;
+            cp_async16(&S.h[b][r * kPadH + j], act_h + (ok ? (size_t)rb * kH + x : 0), ok);
+        }
+        for (int x = tid; x < kTile * dd; x += kThreads) {
+            const bool ok = rb + x / dd < rows;
+            cp_async8(&S.u[b][x], act_u + (ok ? (size_t)rb * dd + x : 0), ok);
+            cp_async8(&S.uc[b][x], act_uc + (ok ? (size_t)rb * dd + x : 0), ok);
+        }
+        for (int x = tid; x < kTile * D; x += kThreads) {
+            const bool ok = rb + x / D < rows;
+            cp_async8(&S.p[b][x], act_p + (ok ? (size_t)rb * D + x : 0), ok);
+        }
+        if (tid < kTile) {
+            const int row = rb + tid;
+            const bool ok = row < rows;
+            if (grads_out) cp_async8(&S.w[b][tid], adv + (ok ? row / T : 0), ok);
+        } else if (tid < kTile + kTile / 8) {
+            const int q = tid - kTile, row = rb + 8 * q;
+            if (row + 8 <= rows) {
+                cp_async8(&S.ch[b][8 * q], choice + row, true);
+            } else {
+                for (int e = 0; e < 8; e++) S.ch[b][8 * q + e] = row + e < rows ? choice[row + e] : 0;
+            }
+        }
+        cp_async_commit();
+    };
+    if (t0 < t1) stage(t0, 0);
     for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPadH + (x & 63)] = P[dm.off.w_att + x];
     for (int x = tid; x < 2 * kH * dd4; x += kThreads) {
         const int i = x / dd4, o = x % dd4;
@@ -116,28 +154,23 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     for (int x = 0; x < kMaxDD / 4; x++) gw[x] = 0.0;
     double gdev[4] = {0.0, 0.0, 0.0, 0.0};  // dev grad: e = tid + 256*y < D*dd
     double gb = 0.0;                         // b_out: tid < D
-    const int n_tiles = (rows + kTile - 1) / kTile;
-    const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
     for (int tl = t0; tl < t1; tl++) {
-        const int rb = tl * kTile;
+        const int rb = tl * kTile, b = (tl - t0) & 1;
+        if (tl + 1 < t1) {
+            stage(tl + 1, b ^ 1);  // the next tile lands while this one is processed
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        for (int x = tid; x < kTile * kH; x += kThreads) {
-            const int r = x >> 6, j = x & 63, row = rb + r;
-            const bool ok = row < rows;
-            S.h[r * kPadH + j] = ok ? act_h[(size_t)row * kH + j] : 0.0;
-        }
-        for (int x = tid; x < kTile * dd; x += kThreads) {
-            const int r = x / dd, o = x % dd, row = rb + r;
-            S.u[r * ddp + o] = row < rows ? act_u[(size_t)row * dd + o] : 0.0;
-            S.uc[r * ddp + o] = row < rows ? act_uc[(size_t)row * dd + o] : 0.0;
-        }
+        const double *Sh = S.h[b], *Su = S.u[b], *Suc = S.uc[b];
         for (int x = tid; x < kTile * D; x += kThreads) {
-            const int r = x / D, d = x % D, row = rb + r;
+            const int r = x / D, d = x - r * D;
             double dz = 0.0;
-            if (row < rows) {
-                dz = -act_p[(size_t)row * D + d];
-                if (d == choice[row]) dz += 1.0;
-                if (grads_out) dz = adv[row / T] * dz;
+            if (rb + r < rows) {
+                dz = -S.p[b][x];
+                if (d == S.ch[b][r]) dz += 1.0;
+                if (grads_out) dz = S.w[b][r] * dz;
             }
             S.dz[r * Dp + d] = dz;
         }
@@ -162,7 +195,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             for (int n = 0; n < 4; n++) acc[n][0] = acc[n][1] = 0.0;
 #pragma unroll 4
             for (int ks = 0; ks < kH / 4; ks++) {
-                const double a = S.h[(mt * 8 + g) * kPadH + ks * 4 + t];
+                const double a = Sh[(mt * 8 + g) * kPadH + ks * 4 + t];
 #pragma unroll
                 for (int n = 0; n < 4; n++) dmma884(acc[n], a, S.watt[(ks * 4 + t) * kPadH + (nb + n) * 8 + g]);
             }
@@ -202,8 +235,8 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
 #pragma unroll
             for (int x = 0; x < kMaxDD / 8; x += 2) {
                 const int o0 = jb + 8 * x, o1 = o0 + 8;
-                if (o0 < dd) s0 = fma(S.uc[r * ddp + o0], S.du[r * kDuLd + o0], s0);
-                if (o1 < dd) s1 = fma(S.uc[r * ddp + o1], S.du[r * kDuLd + o1], s1);
+                if (o0 < dd) s0 = fma(Suc[r * dd + o0], S.du[r * kDuLd + o0], s0);
+                if (o1 < dd) s1 = fma(Suc[r * dd + o1], S.du[r * kDuLd + o1], s1);
             }
             double s = s0 + s1;
             s += __shfl_xor_sync(0xffffffffu, s, 1);
@@ -212,28 +245,30 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             const int row = rb + r;
             if (rows_out && jb == 0 && row < rows) row_w[row] = s;
         }
-        if (!grads_out) continue;
-        // grads over the tile's rows (w_out h-half; the ctx half is enc^T A, att_fin_kernel)
-        for (int r = 0; r < kTile; r++) {
-            const double hc = S.h[r * kPadH + gi];
+        if (grads_out) {
+            // grads over the tile's rows (w_out h-half; the ctx half is enc^T A, att_fin_kernel)
+            for (int r = 0; r < kTile; r++) {
+                const double hc = Sh[r * kPadH + gi];
 #pragma unroll
-            for (int x = 0; x < kMaxDD / 4; x++) {
-                const int o = go + 4 * x;
-                if (o < dd) gw[x] = fma(hc, S.du[r * kDuLd + o], gw[x]);
+                for (int x = 0; x < kMaxDD / 4; x++) {
+                    const int o = go + 4 * x;
+                    if (o < dd) gw[x] = fma(hc, S.du[r * kDuLd + o], gw[x]);
+                }
             }
-        }
 #pragma unroll
-        for (int y = 0; y < 4; y++) {
-            const int e = tid + kThreads * y;
-            if (e < D * dd) {
-                const int d = e / dd, o = e % dd;
-                double v = gdev[y];
-                for (int r = 0; r < kTile; r++) v = fma(S.dz[r * Dp + d], S.u[r * ddp + o], v);
-                gdev[y] = v;
+            for (int y = 0; y < 4; y++) {
+                const int e = tid + kThreads * y;
+                if (e < D * dd) {
+                    const int d = e / dd, o = e % dd;
+                    double v = gdev[y];
+                    for (int r = 0; r < kTile; r++) v = fma(S.dz[r * Dp + d], Su[r * dd + o], v);
+                    gdev[y] = v;
+                }
             }
+            if (tid < D)
+                for (int r = 0; r < kTile; r++) gb += S.dz[r * Dp + tid];
         }
-        if (tid < D)
-            for (int r = 0; r < kTile; r++) gb += S.dz[r * Dp + tid];
+        __syncthreads();  // buffer b and du / dz are rewritten next iteration
     }
     if (!grads_out) return;
     const size_t na = (size_t)D + D * dd + 2 * kH * dd;
@@ -1581,6 +1616,15 @@ Grid tiles_grid(int rows, int tile) {
     return {ceil_div(n_tiles, per), per};
 }
 
+// one CTA per SM, each streaming a contiguous run of tiles through its
+// cp.async pipeline
+Grid persist_grid(int rows, int tile) {
+    const int n_tiles = ceil_div(rows, tile);
+    const int n = n_tiles < kNumSMs ? n_tiles : kNumSMs;
+    const int per = ceil_div(n_tiles, n);
+    return {ceil_div(n_tiles, per), per};
+}
+
 Grid att_grid(int K, int T) {
     // one wave: att_bwd holds ~220 KB of shared memory (1 CTA per SM).  It
     // leaves kSimSMs SMs free: in the split backward it runs concurrently with
@@ -1646,7 +1690,7 @@ int run_b0(dp_policy *p, const double *params, int rows, const double *adv, doub
         DP_LAUNCH_CHECK();
         return DP_OK;
     }
-    const Grid g = tiles_grid(rows, kTile);
+    const Grid g = persist_grid(rows, kTile);
     const size_t smem = sizeof(PrepSmem);
     DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
     row_prep_kernel<<<g.n_used, kThreads, smem, st>>>(dm, params, rows, g.per, adv, p->act_p, p->act_choice, p->act_u,
