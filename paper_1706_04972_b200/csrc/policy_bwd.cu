@@ -594,7 +594,7 @@ constexpr int kAttTile = 64;  // rows per tile in att_bwd (2 rows per thread in 
 struct AttSmem {
     double enc[2][kChunk * kPadH];  // cp.async double buffer over the T chunks
     double q[kAttTile * kPadH];
-    double dc[kAttTile * kPadH];
+    double watt[kH * kPadH];        // W_att[l][j], staged once per CTA
     double al[kAttTile * kPadH];
     double ds[kAttTile * kPadH];
     double du[kAttTile * kDuLd];
@@ -645,31 +645,56 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
         }
         cp_async_commit();
     };
+    // the tile's q / du / softmax stats -> shared memory (cp.async; du columns
+    // dd..dd8 stay zero from the prologue), and this lane's 16 dctx values of
+    // its DA rows -> registers (the A fragments of the DA product)
+    auto stage_tile = [&](int tl) {
+        const int t0 = (tl % tps) * kAttTile;
+        const int rb = (tl / tps) * T + t0;
+        const int nrow = min(kAttTile, T - t0);
+        for (int x = tid * 2; x < kAttTile * kH; x += kThreads * 2) {
+            const int r = x >> 6, j = x & 63;
+            const bool ok = r < nrow;
+            cp_async16(&S.q[r * kPadH + j], row_q + (ok ? (size_t)(rb + r) * kH + j : 0), ok);
+        }
+        for (int x = tid; x < kAttTile * dd; x += kThreads) {
+            const int r = x / dd;
+            const bool ok = r < nrow;
+            cp_async8(&S.du[r * kDuLd + (x - r * dd)], row_du + (ok ? (size_t)rb * dd + x : 0), ok);
+        }
+        if (tid < kAttTile) {
+            const bool ok = tid < nrow;
+            const size_t row = ok ? (size_t)(rb + tid) : 0;
+            cp_async8(&S.mx[tid], act_stat + row * 2, ok);
+            cp_async8(&S.sm[tid], act_stat + row * 2 + 1, ok);
+            cp_async8(&S.w[tid], row_w + row, ok);
+        }
+        cp_async_commit();
+    };
+    double dcr[kH / 4];  // dctx[mr][4 ks + t]
+    auto load_dc = [&](int tl) {
+        const int t0 = (tl % tps) * kAttTile;
+        const int rb = (tl / tps) * T + t0;
+        const bool ok = mr < min(kAttTile, T - t0);
+        const double *src = row_dctx + (size_t)(rb + (ok ? mr : 0)) * kH + t;
+#pragma unroll
+        for (int ks = 0; ks < kH / 4; ks++) dcr[ks] = ok ? __ldg(src + 4 * ks) : 0.0;
+    };
+    for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPadH + (x & 63)] = w_att[x];
+    for (int x = tid; x < kAttTile * (kDuLd - dd); x += kThreads) {
+        const int r = x / (kDuLd - dd);
+        S.du[r * kDuLd + dd + (x - r * (kDuLd - dd))] = 0.0;
+    }
+    if (tile0 < tile1) {
+        stage_tile(tile0);
+        stage_enc(0, 0);
+        load_dc(tile0);
+    }
     bool first_cta_tile = true;
     for (int tl = tile0; tl < tile1; tl++) {
         const int t0 = (tl % tps) * kAttTile;
         const int rb = (tl / tps) * T + t0;
         const int nrow = min(kAttTile, T - t0);
-        __syncthreads();  // previous tile's readers are done with every buffer
-        stage_enc(0, 0);
-        for (int x = tid; x < kAttTile * kH; x += kThreads) {
-            const int r = x >> 6, j = x & 63;
-            const int row = rb + r;
-            const bool ok = r < nrow;
-            S.q[r * kPadH + j] = ok ? row_q[(size_t)row * kH + j] : 0.0;
-            S.dc[r * kPadH + j] = ok ? row_dctx[(size_t)row * kH + j] : 0.0;
-        }
-        for (int x = tid; x < kAttTile * dd8; x += kThreads) {
-            const int r = x / dd8, o = x - r * dd8;
-            S.du[r * kDuLd + o] = (r < nrow && o < dd) ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
-        }
-        if (tid < kAttTile) {
-            const int row = rb + tid;
-            const bool ok = tid < nrow;
-            S.mx[tid] = ok ? act_stat[(size_t)row * 2] : 0.0;
-            S.sm[tid] = ok ? act_stat[(size_t)row * 2 + 1] : 1.0;
-            S.w[tid] = ok ? row_w[row] : 0.0;
-        }
         double dq[8][2];  // dq[mr][n*8 + 2t + {0,1}], accumulated over the chunks
 #pragma unroll
         for (int n = 0; n < 8; n++) dq[n][0] = dq[n][1] = 0.0;
@@ -709,9 +734,9 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 double da[8][2], sv[8][2];
 #pragma unroll
                 for (int n = 0; n < 8; n++) da[n][0] = da[n][1] = sv[n][0] = sv[n][1] = 0.0;
-#pragma unroll 2
+#pragma unroll
                 for (int ks = 0; ks < kH / 4; ks++) {
-                    const double a = S.dc[mr * kPadH + ks * 4 + t];
+                    const double a = dcr[ks];
                     double aq = 0.0;
                     if (!STORED) aq = S.q[mr * kPadH + ks * 4 + t];
 #pragma unroll
@@ -802,12 +827,18 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 *reinterpret_cast<double2 *>(row_dq + (size_t)(rb + mr) * kH + n * 8 + 2 * t) =
                     make_double2(dq[n][0], dq[n][1]);
         // B1f rows part fused here: dh_ext[r, l] += sum_j dq[r, j] W_att[l, j]
-        // (dq -> S.q, W_att -> S.al: both free once the chunks are done)
-        for (int x = tid; x < kH * kH; x += kThreads) S.al[(x >> 6) * kPadH + (x & 63)] = w_att[x];
+        // (dq -> S.ds, free after the last chunk; W_att is resident).  The next
+        // tile's q / du / stats / first enc chunk / dctx are issued first, so
+        // they land while this product runs.
 #pragma unroll
         for (int n = 0; n < 8; n++) {
-            S.q[mr * kPadH + n * 8 + 2 * t] = dq[n][0];
-            S.q[mr * kPadH + n * 8 + 2 * t + 1] = dq[n][1];
+            S.ds[mr * kPadH + n * 8 + 2 * t] = dq[n][0];
+            S.ds[mr * kPadH + n * 8 + 2 * t + 1] = dq[n][1];
+        }
+        if (tl + 1 < tile1) {
+            stage_tile(tl + 1);
+            stage_enc(0, 0);
+            load_dc(tl + 1);
         }
         __syncthreads();
         {
@@ -816,9 +847,9 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             for (int n = 0; n < 8; n++) o[n][0] = o[n][1] = 0.0;
 #pragma unroll 2
             for (int ks = 0; ks < kH / 4; ks++) {
-                const double a = S.q[mr * kPadH + ks * 4 + t];
+                const double a = S.ds[mr * kPadH + ks * 4 + t];
 #pragma unroll
-                for (int n = 0; n < 8; n++) dmma884(o[n], a, S.al[(n * 8 + g) * kPadH + ks * 4 + t]);
+                for (int n = 0; n < 8; n++) dmma884(o[n], a, S.watt[(n * 8 + g) * kPadH + ks * 4 + t]);
             }
             if (rok)
 #pragma unroll
@@ -828,6 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     *dst = make_double2(v.x + o[n][0], v.y + o[n][1]);
                 }
         }
+        __syncthreads();  // S.ds / S.al are rewritten by the next tile's first chunk
         first_cta_tile = false;
     }
 }
