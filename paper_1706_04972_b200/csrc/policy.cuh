@@ -53,7 +53,7 @@ struct dp_policy {
     double *act_logp;     // [k]
     int last_K;
     // backward scratch
-    double *row_q, *row_dctx, *row_w, *row_dq, *row_dhx;  // per (k,t)
+    double *row_q, *row_w, *row_dq, *row_dhx;  // per (k,t)
     double *row_du;                                      // [k*T*dd] du = dev_table[:D]^T dz
     double *dh0, *dc0;                                   // [k*H]
     double *d_enc;                                       // [T*H]

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     PolicyDims dm, const double *__restrict__ P, int rows, int tiles_per_cta, const double *__restrict__ adv,
     const double *__restrict__ act_p, const uint8_t *__restrict__ choice, const double *__restrict__ act_u,
     const double *__restrict__ act_h, const double *__restrict__ act_uc, double *__restrict__ row_q,
-    double *__restrict__ row_dctx, double *__restrict__ row_w, double *__restrict__ row_dhx,
+    double *__restrict__ row_w, double *__restrict__ row_dhx,
     double *__restrict__ row_du, double *__restrict__ partial,
     int mode /* kFused | kRowsOnly (adv := 1) | kGradsOnly */) {
     extern __shared__ __align__(16) double smraw[];
@@ -207,26 +207,25 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
                         make_double2(acc[n][0], acc[n][1]);
         }
         __syncthreads();
-        // dhc = W_out du (DMMA, k = dd4): i < 64 -> dh_out, i >= 64 -> dctx
+        // dh_out = W_out[:64] du (DMMA, k = dd4).  The context half W_out[64:] du
+        // is never formed: att_bwd contracts du with encW = enc W_out[64:].
         if (rows_out) {
             const int lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
-            const int mt = w >> 1, nb = (w & 1) * 8;
-            double acc[8][2];
+            const int mt = w >> 1, nb = (w & 1) * 4;
+            double acc[4][2];
 #pragma unroll
-            for (int n = 0; n < 8; n++) acc[n][0] = acc[n][1] = 0.0;
+            for (int n = 0; n < 4; n++) acc[n][0] = acc[n][1] = 0.0;
             for (int ks = 0; ks < dd4 / 4; ks++) {
                 const double a = S.du[(mt * 8 + g) * kDuLd + ks * 4 + t];
 #pragma unroll
-                for (int n = 0; n < 8; n++) dmma884(acc[n], a, S.woutT[(ks * 4 + t) * kWoLd + (nb + n) * 8 + g]);
+                for (int n = 0; n < 4; n++) dmma884(acc[n], a, S.woutT[(ks * 4 + t) * kWoLd + (nb + n) * 8 + g]);
             }
             const int row = rb + mt * 8 + g;
             if (row < rows)
 #pragma unroll
-                for (int n = 0; n < 8; n++) {
-                    const int i = (nb + n) * 8 + 2 * t;
-                    double *dst = i < kH ? row_dhx + (size_t)row * kH + i : row_dctx + (size_t)row * kH + i - kH;
-                    *reinterpret_cast<double2 *>(dst) = make_double2(acc[n][0], acc[n][1]);
-                }
+                for (int n = 0; n < 4; n++)
+                    *reinterpret_cast<double2 *>(row_dhx + (size_t)row * kH + (nb + n) * 8 + 2 * t) =
+                        make_double2(acc[n][0], acc[n][1]);
         }
         // w = ctx . dctx == (ctx W_out[64:]) . du = uc . du  (8 lanes per row)
         if (rows_out) {
@@ -593,8 +592,8 @@ constexpr int kAttTile = 64;  // rows per tile in att_bwd (2 rows per thread in 
 
 struct AttSmem {
     double enc[2][kChunk * kPadH];  // cp.async double buffer over the T chunks
+    double encw[2][kChunk * kDuLd]; // encW = enc W_out[64:] rows of the chunk (cols >= dd zero)
     double q[kAttTile * kPadH];
-    double watt[kH * kPadH];        // W_att[l][j], staged once per CTA
     double al[kAttTile * kPadH];
     double ds[kAttTile * kPadH];
     double du[kAttTile * kDuLd];
@@ -607,7 +606,9 @@ struct AttSmem {
 // over the chunks (one store per tile).  Every contraction is a 64x64x64 (or
 // 64 x dd x 64) product on the fp64 tensor cores (mma.sync m8n8k4 DMMA);
 // warp w owns the 8-row m-tile w of each product:
-//   DA    dalpha[r, i] = dctx[r] . enc_i          (S = q . enc_i too, unless STORED)
+//   DA    dalpha[r, i] = dctx[r] . enc_i = du[r] . encW_i   (dctx = W_out[64:] du, so a
+//         k = dd product on encW = enc W_out[64:] from the forward; S = q . enc_i too,
+//         unless STORED)
 //         alpha (STORED: e_i * esc from the decoder; else exp(s - max) / sum),
 //         ds = alpha (dalpha - w)
 //   dq    += ds @ enc_chunk
@@ -617,7 +618,7 @@ struct AttSmem {
 template <bool STORED>
 __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
-    const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ row_dctx,
+    const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ encW,
     const double *__restrict__ row_w, const double *__restrict__ row_du, double *__restrict__ row_dq,
     double *__restrict__ partial, double *__restrict__ partA,
     double *__restrict__ tile_partial /* [units][T][64] or NULL */,
@@ -642,6 +643,11 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             const int i = x >> 5, j2 = x & 31;
             const bool ok = i0 + i < T;
             cp_async16(&S.enc[b][i * kPadH + 2 * j2], enc_h + (size_t)(ok ? i0 + i : 0) * kH + 2 * j2, ok);
+        }
+        for (int x = tid; x < kChunk * dd; x += kThreads) {
+            const int i = x / dd;
+            const bool ok = i0 + i < T;
+            cp_async8(&S.encw[b][i * kDuLd + (x - i * dd)], encW + (ok ? (size_t)i0 * dd + x : 0), ok);
         }
         cp_async_commit();
     };
@@ -671,24 +677,18 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
         }
         cp_async_commit();
     };
-    double dcr[kH / 4];  // dctx[mr][4 ks + t]
-    auto load_dc = [&](int tl) {
-        const int t0 = (tl % tps) * kAttTile;
-        const int rb = (tl / tps) * T + t0;
-        const bool ok = mr < min(kAttTile, T - t0);
-        const double *src = row_dctx + (size_t)(rb + (ok ? mr : 0)) * kH + t;
-#pragma unroll
-        for (int ks = 0; ks < kH / 4; ks++) dcr[ks] = ok ? __ldg(src + 4 * ks) : 0.0;
-    };
-    for (int x = tid; x < kH * kH; x += kThreads) S.watt[(x >> 6) * kPadH + (x & 63)] = w_att[x];
+    // zero k-padding columns (dd .. kDuLd) of du and of both encW buffers once:
+    // the copies never write them
     for (int x = tid; x < kAttTile * (kDuLd - dd); x += kThreads) {
-        const int r = x / (kDuLd - dd);
-        S.du[r * kDuLd + dd + (x - r * (kDuLd - dd))] = 0.0;
+        const int r = x / (kDuLd - dd), c = dd + (x - r * (kDuLd - dd));
+        S.du[r * kDuLd + c] = 0.0;
+        S.encw[0][r * kDuLd + c] = 0.0;
+        S.encw[1][r * kDuLd + c] = 0.0;
     }
+    const int dd4 = (dd + 3) & ~3;  // k extent of the DA product
     if (tile0 < tile1) {
         stage_tile(tile0);
         stage_enc(0, 0);
-        load_dc(tile0);
     }
     bool first_cta_tile = true;
     for (int tl = tile0; tl < tile1; tl++) {
@@ -734,18 +734,19 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 double da[8][2], sv[8][2];
 #pragma unroll
                 for (int n = 0; n < 8; n++) da[n][0] = da[n][1] = sv[n][0] = sv[n][1] = 0.0;
+                const double *ew = S.encw[b];
+                for (int ks = 0; ks < dd4 / 4; ks++) {
+                    const double a = S.du[mr * kDuLd + ks * 4 + t];
 #pragma unroll
-                for (int ks = 0; ks < kH / 4; ks++) {
-                    const double a = dcr[ks];
-                    double aq = 0.0;
-                    if (!STORED) aq = S.q[mr * kPadH + ks * 4 + t];
-#pragma unroll
-                    for (int n = 0; n < 8; n++) {
-                        const double bb = enc[(n * 8 + g) * kPadH + ks * 4 + t];  // B[j][i] = enc[i][j]
-                        dmma884(da[n], a, bb);
-                        if (!STORED) dmma884(sv[n], aq, bb);
-                    }
+                    for (int n = 0; n < 8; n++) dmma884(da[n], a, ew[(n * 8 + g) * kDuLd + ks * 4 + t]);  // B[o][i] = encW[i][o]
                 }
+                if (!STORED)
+#pragma unroll
+                    for (int ks = 0; ks < kH / 4; ks++) {
+                        const double aq = S.q[mr * kPadH + ks * 4 + t];
+#pragma unroll
+                        for (int n = 0; n < 8; n++) dmma884(sv[n], aq, enc[(n * 8 + g) * kPadH + ks * 4 + t]);
+                    }
                 const double m = S.mx[mr], l = S.sm[mr], wv = S.w[mr];
 #pragma unroll
                 for (int n = 0; n < 8; n++)
@@ -827,9 +828,9 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 *reinterpret_cast<double2 *>(row_dq + (size_t)(rb + mr) * kH + n * 8 + 2 * t) =
                     make_double2(dq[n][0], dq[n][1]);
         // B1f rows part fused here: dh_ext[r, l] += sum_j dq[r, j] W_att[l, j]
-        // (dq -> S.ds, free after the last chunk; W_att is resident).  The next
-        // tile's q / du / stats / first enc chunk / dctx are issued first, so
-        // they land while this product runs.
+        // (dq -> S.ds and W_att -> S.al, both free after the last chunk).  The
+        // next tile's q / du / stats / first enc chunk are issued first, so they
+        // land while this product runs.
 #pragma unroll
         for (int n = 0; n < 8; n++) {
             S.ds[mr * kPadH + n * 8 + 2 * t] = dq[n][0];
@@ -838,8 +839,8 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
         if (tl + 1 < tile1) {
             stage_tile(tl + 1);
             stage_enc(0, 0);
-            load_dc(tl + 1);
         }
+        for (int x = tid; x < kH * kH; x += kThreads) S.al[(x >> 6) * kPadH + (x & 63)] = __ldg(w_att + x);
         __syncthreads();
         {
             double o[8][2];
@@ -849,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             for (int ks = 0; ks < kH / 4; ks++) {
                 const double a = S.ds[mr * kPadH + ks * 4 + t];
 #pragma unroll
-                for (int n = 0; n < 8; n++) dmma884(o[n], a, S.watt[(n * 8 + g) * kPadH + ks * 4 + t]);
+                for (int n = 0; n < 8; n++) dmma884(o[n], a, S.al[(n * 8 + g) * kPadH + ks * 4 + t]);
             }
             if (rok)
 #pragma unroll
@@ -1681,13 +1682,13 @@ int launch_att(dp_policy *p, const double *params, const Grid &g, size_t smem, i
     if (p->act_e) {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<true>, smem));
         att_bwd_kernel<true><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                               p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
+                                                               p->encW, p->row_w, p->row_du, p->row_dq, p->partial,
                                                                p->partA, tile_part, tile_partA, p->act_e, p->act_esc, 1,
                                                                per_sample, params + p->dims.off.w_att, p->row_dhx);
     } else {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<false>, smem));
         att_bwd_kernel<false><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
-                                                                p->row_dctx, p->row_w, p->row_du, p->row_dq, p->partial,
+                                                                p->encW, p->row_w, p->row_du, p->row_dq, p->partial,
                                                                 p->partA, tile_part, tile_partA, nullptr, nullptr, 1,
                                                                 per_sample, params + p->dims.off.w_att, p->row_dhx);
     }
@@ -1726,7 +1727,7 @@ int run_b0(dp_policy *p, const double *params, int rows, const double *adv, doub
     const size_t smem = sizeof(PrepSmem);
     DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
     row_prep_kernel<<<g.n_used, kThreads, smem, st>>>(dm, params, rows, g.per, adv, p->act_p, p->act_choice, p->act_u,
-                                                      p->act_h, p->act_uc, p->row_q, p->row_dctx, p->row_w,
+                                                      p->act_h, p->act_uc, p->row_q, p->row_w,
                                                       p->row_dhx, p->row_du, p->partial, mode);
     DP_LAUNCH_CHECK();
     if (mode == kRowsOnly) return DP_OK;

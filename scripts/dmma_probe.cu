@@ -62,6 +62,17 @@ int main() {
         double flops = 2.0 * 256 * 8 * (double)iters * warps * sms;  // 256 FMA per warp-mma
         printf("DMMA  %2d warps/SM, 8 chains: %.2f TFLOP/s\n", warps, flops / ms / 1e9);
     }
+    // latency: one warp per SM, CH independent chains
+    {
+        float ms1 = time_it([&] { dmma_kernel<1><<<sms, 32>>>(iters, out); });
+        float ms2 = time_it([&] { dmma_kernel<2><<<sms, 32>>>(iters, out); });
+        float ms4 = time_it([&] { dmma_kernel<4><<<sms, 32>>>(iters, out); });
+        float ms8 = time_it([&] { dmma_kernel<8><<<sms, 32>>>(iters, out); });
+        const double clk = 1.9e9;  // approximate SM clock for the cycle conversion
+        printf("DMMA 1 warp/SM: cycles per mma with 1/2/4/8 chains: %.1f %.1f %.1f %.1f\n",
+               ms1 * 1e-3 * clk / iters, ms2 * 1e-3 * clk / (2.0 * iters), ms4 * 1e-3 * clk / (4.0 * iters),
+               ms8 * 1e-3 * clk / (8.0 * iters));
+    }
     for (int warps : {8, 16, 32}) {
         const int threads = 32 * warps;
         float ms = time_it([&] { dfma_kernel<<<sms, threads>>>(iters, out); });
