@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         clk_acc[i] += now_ - clk_last;                    \
         clk_last = now_;                                  \
     }
+    const int skip = g_dbg_skip;  // debug ablation bits (dp_debug_phase_clocks), read once
     // running row pointers of the step's cached activations (sample m at + m * T rows)
     const size_t sG = (size_t)T * kG, sH = (size_t)T * kH;
     double *actg = a.act_g + (size_t)k0 * sG + col;
@@ -518,7 +519,6 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
         DP_PHASE(0);
         // ---- C: scores s = proj @ h (policy.py:296), warp-local softmax stats + partials ----
-        const int skip = g_dbg_skip;
         const double *hcur[MT];
 #pragma unroll
         for (int m = 0; m < MT; m++) hcur[m] = SPEC ? hC + (m * D + (m < Mb ? prv[m] : 0)) * kH : hS + m * kH;
