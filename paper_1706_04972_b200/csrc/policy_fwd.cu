@@ -77,41 +77,59 @@ __device__ __forceinline__ double np_sum_small(const double *a, int n) {
 }
 
 // ---------------------------------------------------------------- prologue
-// X[t] = [mean(type_table[idx_t]) | shape_t | adj_t]   (policy.py:256-263)
-__global__ void enc_inputs_kernel(PolicyDims dm, const double *__restrict__ params,
-                                  const int32_t *__restrict__ type_off, const int32_t *__restrict__ type_idx,
-                                  const double *__restrict__ shape, const double *__restrict__ adj,
-                                  double *__restrict__ X) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= dm.T * dm.F) return;
-    const int t = idx / dm.F, f = idx % dm.F;
-    double v;
-    if (f < dm.td) {
-        // numpy mean(axis=0): first row, then sequential adds, then / count
-        const double *tab = params + dm.off.type_table;
-        const int a = type_off[t], b = type_off[t + 1];
-        double s = tab[(size_t)type_idx[a] * dm.td + f];
-        for (int i = a + 1; i < b; i++) s = s + tab[(size_t)type_idx[i] * dm.td + f];
-        v = s / (double)(b - a);
-    } else if (f < dm.td + dm.ss) {
-        v = shape[(size_t)t * dm.ss + (f - dm.td)];
+// One launch for the encoder prologue.  Blocks t < T: the input row
+//   X[t] = [mean(type_table[idx_t]) | shape_t | adj_t]   (policy.py:256-263)
+// (kept in X for the w_enc gradient) and its gate pre-activation
+//   XP[t] = X[t] W_enc[:F] + b_enc;
+// blocks T .. T+D: edev[d] = dev_table[d] W_dec[:dd] + b_dec (d = D: the start
+// row, dev_table[D]).  Thread j owns gate column j; 4 accumulators keep the
+// weight loads in flight.
+__global__ void __launch_bounds__(kG) enc_prologue_kernel(PolicyDims dm, const double *__restrict__ params,
+                                                          const int32_t *__restrict__ type_off,
+                                                          const int32_t *__restrict__ type_idx,
+                                                          const double *__restrict__ shape,
+                                                          const double *__restrict__ adj, double *__restrict__ X,
+                                                          double *__restrict__ XP, double *__restrict__ edev) {
+    __shared__ double xs[512];
+    const int j = threadIdx.x;
+    const bool enc = blockIdx.x < dm.T;
+    const int t = blockIdx.x, d = blockIdx.x - dm.T;
+    const int K = enc ? dm.F : dm.dd;
+    if (enc) {
+        for (int f = j; f < dm.F; f += kG) {
+            double v;
+            if (f < dm.td) {
+                // numpy mean(axis=0): first row, then sequential adds, then / count
+                const double *tab = params + dm.off.type_table;
+                const int a = type_off[t], b = type_off[t + 1];
+                double s = tab[(size_t)type_idx[a] * dm.td + f];
+                for (int i = a + 1; i < b; i++) s = s + tab[(size_t)type_idx[i] * dm.td + f];
+                v = s / (double)(b - a);
+            } else if (f < dm.td + dm.ss) {
+                v = shape[(size_t)t * dm.ss + (f - dm.td)];
+            } else {
+                v = adj[(size_t)t * dm.as + (f - dm.td - dm.ss)];
+            }
+            xs[f] = v;
+            X[(size_t)t * dm.F + f] = v;
+        }
     } else {
-        v = adj[(size_t)t * dm.as + (f - dm.td - dm.ss)];
+        for (int o = j; o < dm.dd; o += kG) xs[o] = params[dm.off.dev_table + (size_t)d * dm.dd + o];
     }
-    X[idx] = v;
-}
-
-// C[r, j] = sum_i A[r, i] * B[i, j] + bias[j]   (small dense projections)
-__global__ void gemm_bias_kernel(int R, int N, int Kd, const double *__restrict__ A, int lda,
-                                 const double *__restrict__ B, int ldb, const double *__restrict__ bias,
-                                 double *__restrict__ C, int ldc) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = blockIdx.y;
-    if (j >= N || r >= R) return;
-    const double *a = A + (size_t)r * lda;
-    double acc = 0.0;
-    for (int i = 0; i < Kd; i++) acc = fma(a[i], B[(size_t)i * ldb + j], acc);
-    C[(size_t)r * ldc + j] = acc + bias[j];
+    __syncthreads();
+    const double *W = params + (enc ? dm.off.w_enc : dm.off.w_dec) + j;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int i = 0;
+    for (; i + 4 <= K; i += 4) {
+        a0 = fma(xs[i], W[(size_t)i * kG], a0);
+        a1 = fma(xs[i + 1], W[(size_t)(i + 1) * kG], a1);
+        a2 = fma(xs[i + 2], W[(size_t)(i + 2) * kG], a2);
+        a3 = fma(xs[i + 3], W[(size_t)(i + 3) * kG], a3);
+    }
+    for (; i < K; i++) a0 = fma(xs[i], W[(size_t)i * kG], a0);
+    const double v = ((a0 + a1) + (a2 + a3)) + params[(enc ? dm.off.b_enc : dm.off.b_dec) + j];
+    if (enc) XP[(size_t)t * kG + j] = v;
+    else edev[(size_t)d * kG + j] = v;
 }
 
 // 64-term dot of a shared-memory vector (broadcast) with a register column.
@@ -1233,16 +1251,9 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
     DP_REQUIRE(p && params, "dp_policy_encode: NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
     const PolicyDims &dm = p->dims;
-    const int nx = dm.T * dm.F;
-    enc_inputs_kernel<<<ceil_div(nx, 256), 256, 0, st>>>(dm, params, p->type_off, p->type_idx, p->shape, p->adj,
-                                                          p->X);
-    DP_LAUNCH_CHECK();
-    gemm_bias_kernel<<<dim3(1, dm.T), kG, 0, st>>>(dm.T, kG, dm.F, p->X, dm.F, params + dm.off.w_enc, kG,
-                                                   params + dm.off.b_enc, p->XP, kG);
-    DP_LAUNCH_CHECK();
-    gemm_bias_kernel<<<dim3(1, dm.D + 1), kG, 0, st>>>(dm.D + 1, kG, dm.dd, params + dm.off.dev_table, dm.dd,
-                                                       params + dm.off.w_dec, kG, params + dm.off.b_dec, p->edev,
-                                                       kG);
+    DP_REQUIRE(dm.F <= 512 && dm.dd <= 512, "dp_policy_encode: input width above 512");
+    enc_prologue_kernel<<<dm.T + dm.D + 1, kG, 0, st>>>(dm, params, p->type_off, p->type_idx, p->shape, p->adj, p->X,
+                                                       p->XP, p->edev);
     DP_LAUNCH_CHECK();
     enc_rec_kernel<<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
     DP_LAUNCH_CHECK();

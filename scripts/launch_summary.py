@@ -11,8 +11,8 @@ for r in data:
         nm = nm.replace(pre, "")
     nm = nm.split("(")[0]
     seq.append((nm, float(r[vi].replace(",", "")) / 1000.0))
-# the step starts at enc_inputs_kernel: take the last occurrence
-starts = [i for i, (n, _) in enumerate(seq) if n.startswith("enc_inputs_kernel")]
+# the step starts at enc_prologue_kernel: take the last occurrence
+starts = [i for i, (n, _) in enumerate(seq) if n.startswith("enc_prologue_kernel")]
 step = seq[starts[-1]:] if starts else seq
 tot = sum(v for _, v in step)
 agg = collections.OrderedDict()
