@@ -641,6 +641,37 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
         // (lane = (m, j); full 32-row blocks read e and encW^T as 16-byte pairs)
         double ucv = 0.0;  // this lane's uc_w[m][j] (first pass)
+        if (FAST && MT == 2) {
+            // lane (j, half): 16 of the warp's 32 rows for both samples, so each
+            // encW^T pair is loaded once for the two samples; halves combine
+            // with one shuffle (2/3 of the generic loop's shared-memory wavefronts)
+            const int j = lane & 15, hh = lane >> 4, jj = j < dd ? j : dd - 1;
+            const int i0 = warp * 32 + hh * 16, n = (skip & 1) ? 0 : max(0, min(16, T - i0));
+            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+            if (n == 16) {
+                const double2 *ap0 = reinterpret_cast<const double2 *>(alS + i0);
+                const double2 *ap1 = reinterpret_cast<const double2 *>(alS + a.Tpad + i0);
+                const double2 *ep = reinterpret_cast<const double2 *>(encW + jj * a.ewld + i0);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const double2 e = ep[q], x = ap0[q], y = ap1[q];
+                    c0 = fma(x.x, e.x, c0);
+                    c1 = fma(x.y, e.y, c1);
+                    d0 = fma(y.x, e.x, d0);
+                    d1 = fma(y.y, e.y, d1);
+                }
+            } else {
+                for (int ii = 0; ii < n; ii++) {
+                    const double e = encW[jj * a.ewld + i0 + ii];
+                    c0 = fma(alS[i0 + ii], e, c0);
+                    d0 = fma(alS[a.Tpad + i0 + ii], e, d0);
+                }
+            }
+            double v0 = c0 + c1, v1 = d0 + d1;
+            v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
+            v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
+            if (j < dd) puc[(warp * M + hh) * dd + j] = hh ? v1 : v0;
+        } else
         for (int pi = lane; pi < ((skip & 1) ? 0 : Mb * dd); pi += 32) {
             const int m = small_div<MT>(pi, dd), j = pi - m * dd;
             const double *al = alS + m * a.Tpad;
