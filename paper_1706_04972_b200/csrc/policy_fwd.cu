@@ -169,7 +169,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < 16; k++) w[g][k] = Wh[(size_t)(16 * gate + k) * kG + g * kH + u];
     if (tid < kH + 8) hbuf[0][tid] = 0.0;
     double c = 0.0;
-    double xp = dm.T > 0 ? XP[col] : 0.0;
+    // XP two steps ahead in registers (a step is ~1.4K cycles, an L2/HBM load can take most of one)
+    double xp = dm.T > 0 ? XP[col] : 0.0, xp2 = dm.T > 1 ? XP[kG + col] : 0.0;
     __syncthreads();
     const int base = lane & ~3;
     const bool hi = gate & 2, lo = gate & 1;
@@ -205,7 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         kk += __shfl_xor_sync(0xffffffffu, lo ? k0 : k1, 1);
         const double a = xp + kk;
         DP_ENC_PHASE(0);
-        if (t + 1 < dm.T) xp = XP[(size_t)(t + 1) * kG + col];
+        xp = xp2;
+        if (t + 2 < dm.T) xp2 = XP[(size_t)(t + 2) * kG + col];
         const double act = gate_act(a, gate == 3);
         DP_ENC_PHASE(1);
         enc_g[(size_t)t * kG + col] = act;
