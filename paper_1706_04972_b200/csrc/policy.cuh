@@ -57,6 +57,7 @@ struct dp_policy {
     double *row_du;                                      // [k*T*dd] du = dev_table[:D]^T dz
     double *dh0, *dc0;                                   // [k*H]
     double *d_enc;                                       // [T*H]
+    double *gsum;                                        // [T*H] GM: sum_k adv_k ds_k^T H_k
     double *da_enc;                                      // [T*G]
     double *partial;                                     // per-CTA partial sums
     size_t partial_elems;
@@ -67,6 +68,7 @@ struct dp_policy {
     double *a_tot;                // [T][dd] A = sum_rows alpha^T du
     int rows_ready;               // K of the last dp_policy_backward_rows (0: none)
     int att_per_sample;           // the last rows pass left per-sample (1) or per-tile (0) partials
+    int att_gmode;                // ... holding G = ds^T H (1, grads pass forms d_enc = G W_att) or d_enc (0)
     // side stream: the encoder backward (one CTA) overlaps the decoder weight-gradient GEMM
     cudaStream_t side, side2;
     cudaEvent_t ev_fork, ev_join, ev_fork2, ev_join2;

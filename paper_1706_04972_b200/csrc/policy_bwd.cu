@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
     const double *__restrict__ act_h, const double *__restrict__ act_uc, double *__restrict__ row_q,
     double *__restrict__ row_w, double *__restrict__ row_dhx,
     double *__restrict__ row_du, double *__restrict__ partial,
-    int mode /* kFused | kRowsOnly (adv := 1) | kGradsOnly */) {
+    int mode /* kFused | kRowsOnly (adv := 1) | kGradsOnly */, int want_q /* 0: the attention backward runs in GM */) {
     extern __shared__ __align__(16) double smraw[];
     PrepSmem &S = *reinterpret_cast<PrepSmem *>(smraw);
     const bool rows_out = mode != kGradsOnly, grads_out = mode != kRowsOnly;
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
             }
             S.du[r * kDuLd + o] = v;
         }
-        if (rows_out) {
+        if (rows_out && want_q) {
             // q = h W_att (== W_att^T h per row) on the fp64 tensor cores:
             // warp w: rows 8 (w >> 1) .., columns 32 (w & 1) .. (4 n-tiles)
             const int lane = tid & 31, w = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -480,12 +480,13 @@ __global__ void __launch_bounds__(kThreads, 1) adv_grads_kernel(PolicyDims dm, i
                                                                 const double *__restrict__ act_u,
                                                                 const double *__restrict__ act_p,
                                                                 const uint8_t *__restrict__ choice,
-                                                                double *__restrict__ partial) {
+                                                                double *__restrict__ partial,
+                                                                int nq /* dq columns: 64, or 0 when the grads pass forms W_att from G */) {
     extern __shared__ __align__(16) double sm_raw[];
     AdvGradSmem &S = *reinterpret_cast<AdvGradSmem *>(sm_raw);
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, g = lane >> 2, t = lane & 3;
     const int T = dm.T, D = dm.D, dd = dm.dd;
-    const int nt_used = (kH + dd + 7) / 8;
+    const int nt_used = (nq + dd + 7) / 8;
     double acc[kAgNt][2];
 #pragma unroll
     for (int n = 0; n < kAgNt; n++) acc[n][0] = acc[n][1] = 0.0;
@@ -494,10 +495,11 @@ __global__ void __launch_bounds__(kThreads, 1) adv_grads_kernel(PolicyDims dm, i
     const int n_tiles = (rows + kTile - 1) / kTile;
     const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
     // zero the padding columns of both B buffers once (never written by the copies)
-    for (int x = tid; x < 2 * kTile * (kAgLdB - kH - dd); x += kThreads) {
-        const int bb = x / (kTile * (kAgLdB - kH - dd)), rem = x - bb * kTile * (kAgLdB - kH - dd);
-        const int r = rem / (kAgLdB - kH - dd), c = rem - r * (kAgLdB - kH - dd);
-        S.b[bb][r][kH + dd + c] = 0.0;
+    const int npad = kAgLdB - nq - dd;
+    for (int x = tid; x < 2 * kTile * npad; x += kThreads) {
+        const int bb = x / (kTile * npad), rem = x - bb * kTile * npad;
+        const int r = rem / npad, c = rem - r * npad;
+        S.b[bb][r][nq + dd + c] = 0.0;
     }
     auto stage = [&](int tl, int bf) {
         const int rb = tl * kTile;
@@ -505,14 +507,14 @@ __global__ void __launch_bounds__(kThreads, 1) adv_grads_kernel(PolicyDims dm, i
             const int r = x >> 6, c = x & 63;
             const bool ok = rb + r < rows;
             cp_async16(&S.h[bf][r][c], act_h + (ok ? (size_t)rb * kH + x : 0), ok);
-            cp_async16(&S.b[bf][r][c], row_dq + (ok ? (size_t)rb * kH + x : 0), ok);
+            if (nq) cp_async16(&S.b[bf][r][c], row_dq + (ok ? (size_t)rb * kH + x : 0), ok);
         }
         // the small per-row operands also go asynchronously (8-byte copies; a
         // plain load would stall this thread before the current tile's math)
         for (int x = tid; x < kTile * dd; x += kThreads) {
             const int r = x / dd, c = x - r * dd;
             const bool ok = rb + r < rows;
-            cp_async8(&S.b[bf][r][kH + c], row_du + (ok ? (size_t)rb * dd + x : 0), ok);
+            cp_async8(&S.b[bf][r][nq + c], row_du + (ok ? (size_t)rb * dd + x : 0), ok);
             cp_async8(&S.u[bf][r][c], act_u + (ok ? (size_t)rb * dd + x : 0), ok);
         }
         for (int x = tid; x < kTile * D; x += kThreads) {
@@ -582,8 +584,8 @@ __global__ void __launch_bounds__(kThreads, 1) adv_grads_kernel(PolicyDims dm, i
 #pragma unroll
         for (int e = 0; e < 2; e++) {
             const int c = n * 8 + 2 * t + e;
-            if (c < kH) oa[l * kH + c] = acc[n][e];
-            else if (c < kH + dd) o1[l * dd + (c - kH)] = acc[n][e];
+            if (c < nq) oa[l * kH + c] = acc[n][e];
+            else if (c < nq + dd) o1[l * dd + (c - nq)] = acc[n][e];
         }
 }
 
@@ -615,7 +617,13 @@ struct AttSmem {
 //   dE    d_enc[i, j] = sum_r ds[r, i] q[r, j],  A[i, o] = sum_r alpha[r, i] du[r, o]
 // dE / A go to the per-sample (or per-tile) partials of the split backward,
 // or accumulate in the CTA's private partial (fused backward).
-template <bool STORED>
+// GM (split backward with stored numerators): the launch passes proj for
+// enc_h and act_h for row_q, so the same products give dh_ext = ds proj
+// (instead of dq; dh_ext = dq W_att^T = ds enc W_att^T) and the per-sample
+// G = ds^T H (instead of d_enc = ds^T q = G W_att); the grads pass forms
+// d_enc = (sum adv G) W_att and dW_att = (sum adv G)^T enc once.  No dh_ext
+// epilogue product, no row_dq.
+template <bool STORED, bool GM = false>
 __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     PolicyDims dm, int rows, int tiles_per_cta, const double *__restrict__ enc_h,
     const double *__restrict__ act_stat, const double *__restrict__ row_q, const double *__restrict__ encW,
@@ -822,6 +830,22 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             }
             __syncthreads();  // al / ds / this enc buffer are overwritten by the next chunk
         }
+        if (GM) {
+            // dq holds ds proj = this tile's dh_ext contribution
+            if (rok)
+#pragma unroll
+                for (int n = 0; n < 8; n++) {
+                    double2 *dst = reinterpret_cast<double2 *>(row_dhx + (size_t)(rb + mr) * kH + n * 8 + 2 * t);
+                    const double2 v = *dst;
+                    *dst = make_double2(v.x + dq[n][0], v.y + dq[n][1]);
+                }
+            if (tl + 1 < tile1) {
+                stage_tile(tl + 1);
+                stage_enc(0, 0);
+            }
+            first_cta_tile = false;
+            continue;
+        }
         if (rok)
 #pragma unroll
             for (int n = 0; n < 8; n++)
@@ -862,6 +886,53 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
         }
         __syncthreads();  // S.ds / S.al are rewritten by the next tile's first chunk
         first_cta_tile = false;
+    }
+}
+
+// ------------------------------------------------------------------ B1g (GM)
+// From G = sum_k adv_k ds_k^T H_k [T][64]:
+//   blocks b < nb:  d_enc[i] = G[i] W_att for rows i = 4b .. 4b+3 (W_att and the
+//                   rows staged in shared memory; att_fin adds the context part)
+//   blocks nb + l:  grad W_att[l][:] = sum_i G[i][l] enc[i][:]  (4 row slices per
+//                   column, fixed-order combine)
+constexpr int kGfRows = 4;
+__global__ void __launch_bounds__(256) gsum_fin_kernel(int T, int nb, const double *__restrict__ G,
+                                                       const double *__restrict__ w_att,
+                                                       const double *__restrict__ enc_h, double *__restrict__ d_enc,
+                                                       double *__restrict__ g_watt) {
+    __shared__ double wa[kH * kH];
+    __shared__ double gr[kGfRows][kH];
+    __shared__ double part[4][kH];
+    const int tid = threadIdx.x, j = tid & 63, q = tid >> 6;
+    if ((int)blockIdx.x < nb) {
+        const int i0 = blockIdx.x * kGfRows;
+        for (int x = tid; x < kH * kH; x += 256) wa[x] = w_att[x];
+        const int i = i0 + q;
+        gr[q][j] = i < T ? G[(size_t)i * kH + j] : 0.0;
+        __syncthreads();
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int l = 0; l < kH; l += 4) {
+            a0 = fma(gr[q][l], wa[l * kH + j], a0);
+            a1 = fma(gr[q][l + 1], wa[(l + 1) * kH + j], a1);
+            a2 = fma(gr[q][l + 2], wa[(l + 2) * kH + j], a2);
+            a3 = fma(gr[q][l + 3], wa[(l + 3) * kH + j], a3);
+        }
+        if (i < T) d_enc[(size_t)i * kH + j] = (a0 + a1) + (a2 + a3);
+    } else {
+        const int l = blockIdx.x - nb;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int i = q;
+        for (; i + 12 < T; i += 16) {
+            a0 = fma(G[(size_t)i * kH + l], enc_h[(size_t)i * kH + j], a0);
+            a1 = fma(G[(size_t)(i + 4) * kH + l], enc_h[(size_t)(i + 4) * kH + j], a1);
+            a2 = fma(G[(size_t)(i + 8) * kH + l], enc_h[(size_t)(i + 8) * kH + j], a2);
+            a3 = fma(G[(size_t)(i + 12) * kH + l], enc_h[(size_t)(i + 12) * kH + j], a3);
+        }
+        for (; i < T; i += 4) a0 = fma(G[(size_t)i * kH + l], enc_h[(size_t)i * kH + j], a0);
+        part[q][j] = (a0 + a1) + (a2 + a3);
+        __syncthreads();
+        if (q == 0) g_watt[(size_t)l * kH + j] = (part[0][j] + part[1][j]) + (part[2][j] + part[3][j]);
     }
 }
 
@@ -1679,7 +1750,14 @@ int launch_att(dp_policy *p, const double *params, const Grid &g, size_t smem, i
     const int tps = (dm.T + kAttTile - 1) / kAttTile;
     const int per_sample = tile_part && g.per % tps == 0 ? 1 : 0;
     p->att_per_sample = per_sample;
-    if (p->act_e) {
+    p->att_gmode = p->act_e && tile_part ? 1 : 0;
+    if (p->att_gmode) {
+        DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<true, true>, smem));
+        att_bwd_kernel<true, true><<<g.n_used, kThreads, smem, st>>>(
+            dm, rows, g.per, p->proj, p->act_stat, p->act_h, p->encW, p->row_w, p->row_du, p->row_dq, p->partial,
+            p->partA, tile_part, tile_partA, p->act_e, p->act_esc, 1, per_sample, params + p->dims.off.w_att,
+            p->row_dhx);
+    } else if (p->act_e) {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<true>, smem));
         att_bwd_kernel<true><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
                                                                p->encW, p->row_w, p->row_du, p->row_dq, p->partial,
@@ -1728,7 +1806,8 @@ int run_b0(dp_policy *p, const double *params, int rows, const double *adv, doub
     DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
     row_prep_kernel<<<g.n_used, kThreads, smem, st>>>(dm, params, rows, g.per, adv, p->act_p, p->act_choice, p->act_u,
                                                       p->act_h, p->act_uc, p->row_q, p->row_w,
-                                                      p->row_dhx, p->row_du, p->partial, mode);
+                                                      p->row_dhx, p->row_du, p->partial, mode,
+                                                      !(mode == kRowsOnly && p->act_e && p->tile_part));
     DP_LAUNCH_CHECK();
     if (mode == kRowsOnly) return DP_OK;
     const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
@@ -1840,15 +1919,16 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         (void)g;
         const size_t smem = sizeof(AdvGradSmem);
         DP_CUDA_TRY(allow_big_smem((const void *)adv_grads_kernel, smem));
+        const int nq = p->att_gmode ? 0 : kH;  // GM: W_att comes from G (gsum_fin_kernel)
         adv_grads_kernel<<<n_cta, kThreads, smem, st>>>(dm, rows, per, adv, p->act_h, p->row_dq, p->row_du, p->act_u,
-                                                         p->act_p, p->act_choice, part);
+                                                         p->act_p, p->act_choice, part, nq);
         DP_LAUNCH_CHECK();
         const size_t na = adv_grads_partial(dm);
         RedBuilder rb;
         rb.add(part, na, dm.D, grad + dm.off.b_out);
         rb.add(part + dm.D, na, dm.D * dm.dd, grad + dm.off.dev_table);
         rb.add(part + dm.D + dm.D * dm.dd, na, kH * dm.dd, grad + dm.off.w_out);
-        rb.add(part + dm.D + dm.D * dm.dd + kH * dm.dd, na, kH * kH, grad + dm.off.w_att);
+        if (nq) rb.add(part + dm.D + dm.D * dm.dd + kH * dm.dd, na, kH * kH, grad + dm.off.w_att);
         rb.launch(n_cta, 0, st);
         DP_LAUNCH_CHECK();
     }
@@ -1946,10 +2026,16 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
         // per-sample partials (1 unit per sample) or per-tile (tps units per sample)
         const int tps = p->att_per_sample ? 1 : (T + kAttTile - 1) / kAttTile;
         RedBuilder rb;
-        rb.add(p->tile_part, (size_t)T * kH, T * kH, p->d_enc);
+        rb.add(p->tile_part, (size_t)T * kH, T * kH, p->att_gmode ? p->gsum : p->d_enc);
         rb.add(p->tile_partA, (size_t)T * dm.dd, T * dm.dd, p->a_tot);
         rb.launch(K * tps, 0, st, adv, tps);
         DP_LAUNCH_CHECK();
+        if (p->att_gmode) {
+            const int nb = ceil_div(T, kGfRows);
+            gsum_fin_kernel<<<nb + kH, 256, 0, st>>>(T, nb, p->gsum, params + dm.off.w_att, p->enc_h, p->d_enc,
+                                                    grad + dm.off.w_att);
+            DP_LAUNCH_CHECK();
+        }
     }
     DP_TRY(run_att_fin(p, params, grad, st));
     // the encoder backward (sequential) forks first; B0 / B1f grads and B3 fill the other SMs
