@@ -895,11 +895,16 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 //                   rows staged in shared memory; att_fin adds the context part)
 //   blocks nb + l:  grad W_att[l][:] = sum_i G[i][l] enc[i][:]  (4 row slices per
 //                   column, fixed-order combine)
+// plus the context part of B1a (att_fin_kernel, fused here): d_enc[i] +=
+// A[i] W_out[64:]^T, and blocks nb + 64 + x: grad W_out[64:] = enc^T A.
 constexpr int kGfRows = 4;
-__global__ void __launch_bounds__(256) gsum_fin_kernel(int T, int nb, const double *__restrict__ G,
-                                                       const double *__restrict__ w_att,
+__global__ void __launch_bounds__(256) gsum_fin_kernel(PolicyDims dm, const double *__restrict__ P, int nb,
+                                                       const double *__restrict__ G, const double *__restrict__ A,
                                                        const double *__restrict__ enc_h, double *__restrict__ d_enc,
-                                                       double *__restrict__ g_watt) {
+                                                       double *__restrict__ grad) {
+    const int T = dm.T, dd = dm.dd;
+    const double *w_att = P + dm.off.w_att, *w2 = P + dm.off.w_out + (size_t)kH * dd;
+    double *g_watt = grad + dm.off.w_att;
     __shared__ double wa[kH * kH];
     __shared__ double gr[kGfRows][kH];
     __shared__ double part[4][kH];
@@ -918,7 +923,27 @@ __global__ void __launch_bounds__(256) gsum_fin_kernel(int T, int nb, const doub
             a2 = fma(gr[q][l + 2], wa[(l + 2) * kH + j], a2);
             a3 = fma(gr[q][l + 3], wa[(l + 3) * kH + j], a3);
         }
-        if (i < T) d_enc[(size_t)i * kH + j] = (a0 + a1) + (a2 + a3);
+        double c0 = 0.0;
+        if (i < T)
+            for (int o = 0; o < dd; o++) c0 = fma(A[(size_t)i * dd + o], w2[(size_t)j * dd + o], c0);
+        if (i < T) d_enc[(size_t)i * kH + j] = ((a0 + a1) + (a2 + a3)) + c0;
+    } else if ((int)blockIdx.x >= nb + kH) {
+        // grad W_out[64:][j][o] = sum_i enc[i][j] A[i][o]: 64 outputs x 4 i-slices per block
+        const int e = (blockIdx.x - nb - kH) * kH + j;
+        double v0 = 0.0, v1 = 0.0;
+        if (e < kH * dd) {
+            const int jj = e / dd, o = e - jj * dd;
+            int i = q;
+            for (; i + 4 < T; i += 8) {
+                v0 = fma(enc_h[(size_t)i * kH + jj], A[(size_t)i * dd + o], v0);
+                v1 = fma(enc_h[(size_t)(i + 4) * kH + jj], A[(size_t)(i + 4) * dd + o], v1);
+            }
+            if (i < T) v0 = fma(enc_h[(size_t)i * kH + jj], A[(size_t)i * dd + o], v0);
+        }
+        part[q][j] = v0 + v1;
+        __syncthreads();
+        if (q == 0 && e < kH * dd)
+            grad[dm.off.w_out + (size_t)kH * dd + e] = (part[0][j] + part[1][j]) + (part[2][j] + part[3][j]);
     } else {
         const int l = blockIdx.x - nb;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -2032,12 +2057,12 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
         DP_LAUNCH_CHECK();
         if (p->att_gmode) {
             const int nb = ceil_div(T, kGfRows);
-            gsum_fin_kernel<<<nb + kH, 256, 0, st>>>(T, nb, p->gsum, params + dm.off.w_att, p->enc_h, p->d_enc,
-                                                    grad + dm.off.w_att);
+            gsum_fin_kernel<<<nb + kH + ceil_div(kH * dm.dd, kH), 256, 0, st>>>(dm, params, nb, p->gsum, p->a_tot,
+                                                                              p->enc_h, p->d_enc, grad);
             DP_LAUNCH_CHECK();
         }
     }
-    DP_TRY(run_att_fin(p, params, grad, st));
+    if (!p->att_gmode) DP_TRY(run_att_fin(p, params, grad, st));
     // the encoder backward (sequential) forks first; B0 / B1f grads and B3 fill the other SMs
     return run_b345(p, params, K, adv, grad, st, true);
 }
