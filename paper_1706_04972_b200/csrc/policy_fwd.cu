@@ -293,6 +293,16 @@ constexpr int kProjLd = 66;
 constexpr int kWout1Ld = kH + 8;  // W_out[:64]^T row stride (== 8 mod 16 doubles: 8-lane groups in distinct banks)  // proj row stride in shared memory: 16-byte rows, conflict-free LDS.128
 constexpr int kWarps = kThreads / 32;
 
+// sum_w fw[w] p[w * stride] over the 8 warp partials as a tree (depth 4)
+__device__ __forceinline__ double wsum8(const double *p, int stride, const double (&fw)[kWarps]) {
+    const double a = fma(p[stride], fw[1], p[0] * fw[0]);
+    const double b = fma(p[3 * stride], fw[3], p[2 * stride] * fw[2]);
+    const double c = fma(p[5 * stride], fw[5], p[4 * stride] * fw[4]);
+    const double d = fma(p[7 * stride], fw[7], p[6 * stride] * fw[6]);
+    return (a + b) + (c + d);
+}
+
+
 struct DecArgs {
     PolicyDims dm;
     const double *params;
@@ -808,9 +818,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
                 for (int ww = 0; ww < kWarps; ww++) fw[ww] = __shfl_sync(0xffffffffu, f, ww);
             }
-            double gsum = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < kWarps; ww++) gsum = fma(psm[ww * M + m], fw[ww], gsum);
+            // sum of the 8 warp partials as a 3-level tree (chain depth 4, not 8)
+            const double gsum = wsum8(psm + m, M, fw);
             if (!split && a.act_esc && lane < kWarps) a.act_esc[row * kWarps + lane] = fm_div(f, gsum);
             // all lanes compute (clamped indices, no divergent branches: the z, uc
             // and pcg chains interleave); lanes >= D / >= dd are masked at the end
@@ -827,20 +836,17 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     v0 = fma(hv[op + 8 * y], vS[(op + 8 * y) * D + dz], v0);
                     v1 = fma(hv[op + 8 * y + 8], vS[(op + 8 * y + 8) * D + dz], v1);
                 }
-                double v = v0 + v1;
-                double ucr = 0.0;  // lane j < dd: sum_w fw[w] uc_w[j]
-#pragma unroll
-                for (int ww = 0; ww < kWarps; ww++) ucr = fma(puc[(ww * M + m) * dd + lo], fw[ww], ucr);
+                // 1 / gsum off the chain (the loads above are in flight); the context
+                // half joins the h half before one butterfly
+                const double rg = fm_div(1.0, gsum);
+                const double ucr = wsum8(puc + m * dd + lo, M * dd, fw);  // lane j < dd: sum_w fw[w] uc_w[j]
                 const double ua = __shfl_sync(0xffffffffu, ucr, op), ub = __shfl_sync(0xffffffffu, ucr, op + 8);
                 double c = op < dd ? devt[dz * dd + op] * ua : 0.0;
                 if (op + 8 < dd) c = fma(devt[dz * dd + op + 8], ub, c);
+                double v = fma(c, rg, v0 + v1);
 #pragma unroll
-                for (int o = 1; o < 8; o <<= 1) {
-                    v += __shfl_xor_sync(0xffffffffu, v, o);
-                    c += __shfl_xor_sync(0xffffffffu, c, o);
-                }
+                for (int o = 1; o < 8; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                 zh = __shfl_sync(0xffffffffu, v, ld * 8);
-                zcd = __shfl_sync(0xffffffffu, c, ld * 8);
             } else if (D <= 4 && dd <= 16) {
                 // lanes (d = lane / 8, part = lane % 8): 2 terms each + a 3-level butterfly
                 const int dz = min(lane >> 3, D - 1), op = lane & 7;
@@ -860,11 +866,15 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 if (o < dd) zh0 = fma(devt[ld * dd + o], uhS[m * 32 + o], zh0);
                 zh = zh0 + zh1;
             }
-            double zc = zcd;
-            if (!fastE)
+            double zv;
+            if (fastE) {
+                zv = zh + bout[ld];  // zh carries the context half
+            } else {
+                double zc = zcd;
 #pragma unroll
                 for (int ww = 0; ww < kWarps; ww++) zc = fma(pz[(ww * M + m) * D + ld], fw[ww], zc);
-            const double zv = (zh + fm_div(zc, gsum)) + bout[ld];
+                zv = (zh + fm_div(zc, gsum)) + bout[ld];
+            }
             const double z = lane < D ? zv : -INFINITY;
             if (!split) {
                 // u (and its context half uc) for the backward
