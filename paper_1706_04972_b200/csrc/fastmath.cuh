@@ -74,15 +74,19 @@ __device__ __forceinline__ double fm_exp(double y) {
 // a / b for b >= 1 (finite or +inf): rcp.approx, one Newton step (~2x the
 // seed's bits), then the residual correction q + (a - b q) y, whose error is
 // the product of q's and y's (tests/test_fastmath_gpu.py: 0 ulp vs a / b)
-__device__ __forceinline__ double fm_div(double a, double b) {
+__device__ __forceinline__ double fm_rcp(double b) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
     const double e = fma(-b, y, 1.0);
-    y = fma(y, e, y);
+    return fma(y, e, y);
+}
+// the quotient given y = fm_rcp(b) (shared by several quotients of one b)
+__device__ __forceinline__ double fm_div_y(double a, double b, double y) {
     const double q = a * y;
     const double rr = fma(-b, q, a);
     return fma(rr, y, q);
 }
+__device__ __forceinline__ double fm_div(double a, double b) { return fm_div_y(a, b, fm_rcp(b)); }
 
 // LSTM gate activation without branches: sigmoid(x) = 1 / (2 + expm1(-x)),
 // tanh(x) = sign(x) (-e) / (2 + e) with e = expm1(-2|x|)
