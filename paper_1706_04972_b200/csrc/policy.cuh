@@ -72,4 +72,5 @@ struct dp_policy {
     // side stream: the encoder backward (one CTA) overlaps the decoder weight-gradient GEMM
     cudaStream_t side, side2;
     cudaEvent_t ev_fork, ev_join, ev_fork2, ev_join2;
+    cudaEvent_t ev_att, ev_rows;  // rows pass: attention backward done / whole pass done
 };

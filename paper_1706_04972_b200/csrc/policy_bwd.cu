@@ -2031,7 +2031,9 @@ extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32
         const size_t smem = sizeof(AttSmem);
         DP_TRY(launch_att(p, params, g, smem, rows, p->tile_part, p->tile_partA, st));
     }
+    DP_CUDA_TRY(cudaEventRecord(p->ev_att, st));  // the grads pass's reductions may start here
     DP_TRY(run_b2(p, params, K, st));
+    DP_CUDA_TRY(cudaEventRecord(p->ev_rows, st));
     p->rows_ready = K;
     return DP_OK;
 }
@@ -2046,6 +2048,9 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
     const PolicyDims &dm = p->dims;
     cudaStream_t st = (cudaStream_t)stream;
     const int T = dm.T, rows = K * T;
+    // the advantage-weighted attention sums need only the attention backward:
+    // they run beside the decoder LSTM backward; the rest waits for the rows pass
+    DP_CUDA_TRY(cudaStreamWaitEvent(st, p->ev_att, 0));
     DP_CUDA_TRY(cudaMemsetAsync(grad, 0, sizeof(double) * dm.off.total, st));
     {
         // per-sample partials (1 unit per sample) or per-tile (tps units per sample)
@@ -2063,6 +2068,7 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
         }
     }
     if (!p->att_gmode) DP_TRY(run_att_fin(p, params, grad, st));
+    DP_CUDA_TRY(cudaStreamWaitEvent(st, p->ev_rows, 0));
     // the encoder backward (sequential) forks first; B0 / B1f grads and B3 fill the other SMs
     return run_b345(p, params, K, adv, grad, st, true);
 }

@@ -1113,6 +1113,8 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
     if (p->ev_join) cudaEventDestroy(p->ev_join);
     if (p->ev_fork2) cudaEventDestroy(p->ev_fork2);
     if (p->ev_join2) cudaEventDestroy(p->ev_join2);
+    if (p->ev_att) cudaEventDestroy(p->ev_att);
+    if (p->ev_rows) cudaEventDestroy(p->ev_rows);
     (void)cudaGetLastError();
     delete p;
 }
@@ -1246,7 +1248,9 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
         cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_fork2, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_att, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_rows, cudaEventDisableTiming) != cudaSuccess) {
         dp::set_error("dp_policy_create: stream/event creation failed");
         dp_policy_destroy(p);
         return DP_ECUDA;

@@ -414,8 +414,10 @@ class DeviceController:
             nat.stream_ptr(stream))
         nat.check(rc, "dp_reinforce_epilogue")
         mark("backward")
-        main.wait_stream(self.side)
+        # backward_grads waits on the rows pass itself (its attention sums start
+        # as soon as the attention backward is done, beside the LSTM backward)
         self.eng.backward_grads(p, self.K_local, self.adv, grad=self.grad, stream=stream)
+        main.wait_stream(self.side)
         if self.size > 1:
             mark("allreduce")
             self.xchg.all_reduce_sum(self.grad)
