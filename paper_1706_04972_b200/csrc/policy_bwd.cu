@@ -1124,7 +1124,10 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     double *__restrict__ gates /* [seq][T][256] in: i,f,o,g  out: da */, const double *__restrict__ cst /* [seq][T][64] */,
     const double *__restrict__ c_init /* [64] c before step 0 */, const double *__restrict__ dh_ext /* [seq][T][64] */,
     const double *__restrict__ dh_in /* [seq][64] or NULL */, const double *__restrict__ dc_in,
-    double *__restrict__ dh_out /* [seq][64] */, double *__restrict__ dc_out) {
+    double *__restrict__ dh_out /* [seq][64] */, double *__restrict__ dc_out,
+    const double *__restrict__ gates_in /* activations read (== gates: in place) */,
+    const double *__restrict__ sum_dh /* M == 1, non-NULL: dh_in = sum_r sum_w[r] sum_dh[r], dc_in likewise */,
+    const double *__restrict__ sum_dc, const double *__restrict__ sum_w, int sum_rows) {
     extern __shared__ __align__(16) double sm[];
     double *s_dh = sm;                   // [M][64]
     double *s_dc = s_dh + M * kH;        // [M][64]
@@ -1138,10 +1141,32 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     for (int rr = 0; rr < kRpw; rr++)
 #pragma unroll
         for (int q = 0; q < 8; q++) w[rr][q] = Wh[(size_t)(wrow + rr) * kG + lane + 32 * q];
-    for (int x = tid; x < Mb * kH; x += kLstmThreads) {
-        const int m = x >> 6, u = x & 63;
-        s_dh[x] = dh_in ? dh_in[(size_t)(q0 + m) * kH + u] : 0.0;
-        s_dc[x] = dc_in ? dc_in[(size_t)(q0 + m) * kH + u] : 0.0;
+    if (sum_dh) {
+        // encoder: the decoders' step-0 state gradients, advantage-weighted and
+        // summed over the samples: thread (u, which = dh|dc, slice of 2), fixed-
+        // order combine; scratch in s_da (256 doubles, free until the first step)
+        double *part = s_da;  // [which][slice][64]
+        const int u = tid & 63, sl = (tid >> 6) & 1, which = tid >> 7;
+        const double *src = which ? sum_dc : sum_dh;
+        double a0 = 0.0, a1 = 0.0;
+        int r = sl;
+        for (; r + 2 < sum_rows; r += 4) {
+            a0 = fma(sum_w ? sum_w[r] : 1.0, src[(size_t)r * kH + u], a0);
+            a1 = fma(sum_w ? sum_w[r + 2] : 1.0, src[(size_t)(r + 2) * kH + u], a1);
+        }
+        if (r < sum_rows) a0 = fma(sum_w ? sum_w[r] : 1.0, src[(size_t)r * kH + u], a0);
+        part[(which * 2 + sl) * kH + u] = a0 + a1;
+        __syncthreads();
+        if (tid < kH) {
+            s_dh[tid] = part[tid] + part[kH + tid];
+            s_dc[tid] = part[2 * kH + tid] + part[3 * kH + tid];
+        }
+    } else {
+        for (int x = tid; x < Mb * kH; x += kLstmThreads) {
+            const int m = x >> 6, u = x & 63;
+            s_dh[x] = dh_in ? dh_in[(size_t)(q0 + m) * kH + u] : 0.0;
+            s_dc[x] = dc_in ? dc_in[(size_t)(q0 + m) * kH + u] : 0.0;
+        }
     }
     // elementwise slot of this thread: x = tid (M <= 8 -> Mb*64 <= 512)
     const int x = tid, xm = x >> 6, xu = x & 63;
@@ -1157,7 +1182,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     auto load = [&](int t, Ops &d) {
         if (live && t >= 0) {
             const size_t row = (size_t)(q0 + xm) * T + t;
-            const double *g = gates + row * kG;
+            const double *g = gates_in + row * kG;
             d.i = g[xu];
             d.f = g[kH + xu];
             d.o = g[2 * kH + xu];
@@ -1527,32 +1552,6 @@ __global__ void __launch_bounds__(kG) dec_finalize_kernel(PolicyDims dm, const d
     if (lane == 0) grad[dm.off.dev_table + x] += v;
 }
 
-// sum over samples of the decoder's dh/dc at step 0 -> encoder final state grads
-// dst[blockIdx.x][j] = sum_r w[r] * src_b[r, j] (w == NULL: weights 1), src_0 =
-// dh, src_1 = dc; 1024 threads = 64 columns x 16 row-slices, fixed-order combine
-__global__ void __launch_bounds__(1024) sum_rows_kernel(const double *__restrict__ dh, const double *__restrict__ dc,
-                                                        int n_rows, double *__restrict__ dst,
-                                                        const double *__restrict__ w) {
-    __shared__ double part[16][kH];
-    const int j = threadIdx.x & 63, s = threadIdx.x >> 6;
-    const double *src = blockIdx.x ? dc : dh;
-    double v0 = 0.0, v1 = 0.0;
-    int r = s;
-    for (; r + 16 < n_rows; r += 32) {
-        v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
-        v1 = fma(w ? w[r + 16] : 1.0, src[(size_t)(r + 16) * kH + j], v1);
-    }
-    if (r < n_rows) v0 = fma(w ? w[r] : 1.0, src[(size_t)r * kH + j], v0);
-    part[s][j] = v0 + v1;
-    __syncthreads();
-    if (s == 0) {
-        double v = part[0][j];
-#pragma unroll
-        for (int q = 1; q < 16; q++) v += part[q][j];
-        dst[blockIdx.x * kH + j] = v;
-    }
-}
-
 // B5: w_enc / b_enc grads (contraction over T) and the type-embedding scatter.
 // enc_wgrad: block = 4 rows r of [X | h_prev] (or b_enc) x 256 gate columns;
 // the 4 input rows are staged in shared memory, da_enc streams through a
@@ -1883,7 +1882,10 @@ int run_b2(dp_policy *p, const double *params, int K, cudaStream_t st) {
         const double *Wh = params + dm.off.w_dec + (size_t)dm.dd * kG;
         const double *c_init = p->enc_c + (size_t)(dm.T - 1) * kH;
         const double *null = nullptr;
-        void *args[] = {&T, &n_seq, &M, &Wh, &p->act_g, &p->act_c, &c_init, &p->row_dhx, &null, &null, &p->dh0, &p->dc0};
+        const double *gin = p->act_g;
+        int zero = 0;
+        void *args[] = {&T,       &n_seq,   &M,    &Wh,   &p->act_g, &p->act_c, &c_init, &p->row_dhx, &null,
+                        &null,    &p->dh0,  &p->dc0, &gin, &null,     &null,     &null,   &zero};
         DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(ceil_div(K, M)), dim3(kLstmThreads), args, smem, st));
     }
     DP_LAUNCH_CHECK();
@@ -1909,13 +1911,13 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
     DP_CUDA_TRY(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {
         cudaStream_t ss = p->side;
-        sum_rows_kernel<<<2, 1024, 0, ss>>>(p->dh0, p->dc0, K, dhc_sum, adv);
-        DP_LAUNCH_CHECK();
-        DP_CUDA_TRY(cudaMemcpyAsync(p->da_enc, p->enc_g, sizeof(double) * T * kG, cudaMemcpyDeviceToDevice, ss));
+        // encoder backward: reads the gate activations from enc_g, writes da to
+        // da_enc, and sums the decoders' step-0 state gradients in its prologue
         const size_t smem = lstm_bwd_smem(1);
         lstm_bwd_kernel<1><<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
-                                                   p->enc_c, p->zeros, p->d_enc, dhc_sum, dhc_sum + kH,
-                                                   dhc_sum + 2 * kH, dhc_sum + 3 * kH);
+                                                   p->enc_c, p->zeros, p->d_enc, nullptr, nullptr,
+                                                   dhc_sum + 2 * kH, dhc_sum + 3 * kH, p->enc_g, p->dh0, p->dc0, adv,
+                                                   K);
         DP_LAUNCH_CHECK();
         // the encoder weight grads and the type-table chain both only need
         // da_enc: fork the former onto a second side stream
