@@ -163,7 +163,10 @@ int dp_policy_backward(dp_policy *p, const double *params, int32_t K, const doub
  *        linear in adv, so it runs with adv := 1) — needs no scores;
  * _grads: the advantage-weighted cross-sample sums.  Falls back to the fused
  *        pass when _rows did not run for this decode (or the alpha store would
- *        exceed the memory budget). */
+ *        exceed the memory budget).  _rows and _grads may run on different
+ *        streams: _grads orders itself after _rows with events recorded by
+ *        _rows (its attention sums start when the attention backward is done,
+ *        the rest when the whole rows pass is). */
 int dp_policy_backward_rows(dp_policy *p, const double *params, int32_t K, void *stream);
 int dp_policy_backward_grads(dp_policy *p, const double *params, int32_t K, const double *adv, double *grad,
                              void *stream);
