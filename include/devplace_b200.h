@@ -120,6 +120,11 @@ int dp_debug_phase_clocks(int32_t enable, int64_t *h_out);
 /* Debug instrumentation: LSTM-backward phase clocks (block 0) into h_out[8]. */
 int dp_debug_lstm_clocks(int32_t enable, int64_t *h_out);
 
+/* Debug instrumentation: attention-backward phase clocks (block 0, summed over
+ * its chunks) into h_out[8]: wait + barrier, DA + ds, barrier, dq, dE + dA,
+ * partial stores, barrier, tile prologue/epilogue. */
+int dp_debug_att_clocks(int32_t enable, int64_t *h_out);
+
 /* Accuracy check of the branch-free fp64 transcendentals (fastmath.cuh) the
  * recurrent kernels use, against the CUDA libm over n arguments per function:
  * h_max_ulps[5] = max ulp distance of {sigmoid, tanh, exp, expm1, division}. */

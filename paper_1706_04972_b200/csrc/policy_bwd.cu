@@ -63,6 +63,9 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+__device__ int g_att_dbg = 0;             // debug-only phase clocks of att_bwd (block 0, thread 0)
+__device__ long long g_att_clk[8];
+
 // ------------------------------------------------------------------ fp64 tensor core
 // mma.sync m8n8k4 f64 (DMMA): D[8x8] += A[8x4] B[4x8], one warp.  Fragments
 // (lane = 4 g + t): a = A[g][t], b = B[t][g], c/d = {C[g][2t], C[g][2t+1]}.
@@ -698,6 +701,14 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
         stage_tile(tile0);
         stage_enc(0, 0);
     }
+    const bool aclk = g_att_dbg && blockIdx.x == 0 && tid == 0;
+    long long ac_last = aclk ? clock64() : 0, ac[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define DP_APHASE(i)                        \
+    if (aclk) {                             \
+        const long long now_ = clock64();   \
+        ac[i] += now_ - ac_last;            \
+        ac_last = now_;                     \
+    }
     bool first_cta_tile = true;
     for (int tl = tile0; tl < tile1; tl++) {
         const int t0 = (tl % tps) * kAttTile;
@@ -736,6 +747,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 cp_async_wait<0>();
             }
             __syncthreads();
+            DP_APHASE(0);
             const double *enc = S.enc[b];
             // DA (and S) for rows mr, columns i = n*8 + 2t + {0,1}
             {
@@ -770,7 +782,9 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                         S.ds[mr * kPadH + i] = dsv;
                     }
             }
+            DP_APHASE(1);
             __syncthreads();
+            DP_APHASE(2);
             // dq[mr, j] += sum_i ds[mr, i] enc[i, j]
 #pragma unroll 2
             for (int ks = 0; ks < kChunk / 4; ks++) {
@@ -778,6 +792,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 #pragma unroll
                 for (int n = 0; n < 8; n++) dmma884(dq[n], a, enc[(ks * 4 + t) * kPadH + n * 8 + g]);
             }
+            DP_APHASE(3);
             if (!do_denc) {
                 __syncthreads();
                 continue;
@@ -799,6 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 for (int n = 0; n < 4; n++)
                     if (n * 8 < dd8) dmma884(dA[n], aa, S.du[r * kDuLd + n * 8 + g]);
             }
+            DP_APHASE(4);
             const int i = i0 + mr;
             if (i < T) {
                 const size_t unit = per_sample ? (size_t)(tl / tps) : (size_t)tl;
@@ -828,7 +844,9 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                         }
                     }
             }
+            DP_APHASE(5);
             __syncthreads();  // al / ds / this enc buffer are overwritten by the next chunk
+            DP_APHASE(6);
         }
         if (GM) {
             // dq holds ds proj = this tile's dh_ext contribution
@@ -844,6 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 stage_enc(0, 0);
             }
             first_cta_tile = false;
+            DP_APHASE(7);
             continue;
         }
         if (rok)
@@ -886,7 +905,11 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
         }
         __syncthreads();  // S.ds / S.al are rewritten by the next tile's first chunk
         first_cta_tile = false;
+        DP_APHASE(7);
     }
+#undef DP_APHASE
+    if (aclk)
+        for (int k = 0; k < 8; k++) g_att_clk[k] += ac[k];
 }
 
 // ------------------------------------------------------------------ B1g (GM)
@@ -1714,6 +1737,16 @@ extern "C" int dp_debug_lstm_clocks(int32_t enable, int64_t *h_out) {
     if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_lstm_clk, sizeof(long long) * 8));
     long long z[8] = {0};
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_lstm_clk, z, sizeof(z)));
+    return DP_OK;
+}
+
+extern "C" int dp_debug_att_clocks(int32_t enable, int64_t *h_out) {
+    DP_ENTRY();
+    const int on = enable ? 1 : 0;
+    DP_CUDA_TRY(cudaMemcpyToSymbol(g_att_dbg, &on, sizeof(int)));
+    if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_att_clk, sizeof(long long) * 8));
+    long long z[8] = {0};
+    DP_CUDA_TRY(cudaMemcpyToSymbol(g_att_clk, z, sizeof(z)));
     return DP_OK;
 }
 
