@@ -132,6 +132,14 @@ __global__ void __launch_bounds__(kG) enc_prologue_kernel(PolicyDims dm, const d
     else edev[(size_t)d * kG + j] = v;
 }
 
+// mma.sync m8n8k4 f64 (DMMA): D[8x8] += A[8x4] B[4x8], one warp; lane = 4 g + t:
+// a = A[g][t], b = B[t][g], d = {D[g][2t], D[g][2t+1]}
+__device__ __forceinline__ void dmma_f64(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
 // 64-term dot of a shared-memory vector (broadcast) with a register column.
 __device__ __forceinline__ double dot64_sh_reg(const double *__restrict__ hs, const double (&w)[kH]) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -572,7 +580,51 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             lmx[m] = -INFINITY;
             lsm[m] = 0.0;
         }
-        {
+        // DM (8 samples per CTA, proj too large for shared memory: C5-sized T):
+        // the scores are fp64 tensor-core tiles, S[i][m] = proj[i] . h[m] with
+        // the 8 samples exactly the DMMA n extent; proj streams from L2
+        constexpr bool DM = MT == 8 && !PS && !SPEC;
+        if (DM) {
+            // next step's gate column g = h W_h (W_h column in registers)
+            double g0[MT], g1[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++) g0[m] = g1[m] = 0.0;
+#pragma unroll
+            for (int j2 = 0; j2 < kH / 2; j2++) {
+#pragma unroll
+                for (int m = 0; m < MT; m++) {
+                    const double2 hh = reinterpret_cast<const double2 *>(hcur[m])[j2];
+                    g0[m] = fma(hh.x, w[2 * j2], g0[m]);
+                    g1[m] = fma(hh.y, w[2 * j2 + 1], g1[m]);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb) gn[m] = g0[m] + g1[m];
+            // B fragments (h of sample g, k = 4 ks + t), reused by every row block
+            const int fg = lane >> 2, ft = lane & 3;
+            double bf[kH / 4];
+#pragma unroll
+            for (int ks = 0; ks < kH / 4; ks++) bf[ks] = hS[fg * kH + 4 * ks + ft];
+            const int nblk = (T + 7) >> 3;
+#pragma unroll 2
+            for (int blk = warp; blk < nblk; blk += kWarps) {
+                const int i = blk * 8 + fg;
+                const double *pr = proj + (size_t)(i < T ? i : T - 1) * kH + ft;
+                double acc[2] = {0.0, 0.0};
+#pragma unroll
+                for (int ks = 0; ks < kH / 4; ks++) dmma_f64(acc, __ldg(pr + 4 * ks), bf[ks]);
+                if (i < T) {
+                    alS[(2 * ft) * a.Tpad + i] = acc[0];      // sample 2t
+                    alS[(2 * ft + 1) * a.Tpad + i] = acc[1];  // sample 2t + 1
+                }
+            }
+            __syncthreads();  // the exp loop reads rows other warps scored
+            if (!noshift)
+                for (int i = tid; i < T; i += kThreads)
+#pragma unroll
+                    for (int m = 0; m < MT; m++) lmx[m] = fmax(lmx[m], alS[m * a.Tpad + i]);
+        } else {
             // fused pass: this thread's first score row and its gate column of the
             // next step's h W_h share every h load (W_h indices stay compile-time)
             const int i = tid < T ? tid : T - 1;
@@ -610,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     }
                 }
         }
-        for (int i = tid + kThreads; i < (FAST ? 0 : T); i += kThreads) {
+        for (int i = tid + kThreads; i < ((FAST || DM) ? 0 : T); i += kThreads) {
             const double2 *pr = reinterpret_cast<const double2 *>(proj + (size_t)i * LD);
             double s0[MT], s1[MT];
 #pragma unroll
