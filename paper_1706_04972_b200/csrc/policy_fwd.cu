@@ -705,7 +705,38 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
         // (lane = (m, j); full 32-row blocks read e and encW^T as 16-byte pairs)
         double ucv = 0.0;  // this lane's uc_w[m][j] (first pass)
-        if (FAST && MT == 2) {
+        if (DM) {
+            // fp64 tensor-core tiles: uc_w[m][j] = sum over the warp's rows of e[m][i]
+            // encW[i][j] (m = the 8 samples, j in 8-column tiles, k = rows)
+            const int fg = lane >> 2, ft = lane & 3;
+            constexpr int kNtMax = kMaxDD / 8;
+            const int ntl = (dd + 7) >> 3;
+            double acc[kNtMax][2];
+#pragma unroll
+            for (int n = 0; n < kNtMax; n++) acc[n][0] = acc[n][1] = 0.0;
+            for (int ib = warp * 32; ib < ((skip & 1) ? 0 : T); ib += kThreads) {
+#pragma unroll 2
+                for (int ks = 0; ks < 8; ks++) {
+                    const int i = ib + 4 * ks + ft;
+                    const bool ok = i < T;
+                    const double ae = ok ? alS[fg * a.Tpad + i] : 0.0;  // A[m = g][k = t]
+                    const double *ew = encW + (size_t)(ok ? i : 0) * dd;
+#pragma unroll
+                    for (int n = 0; n < kNtMax; n++)
+                        if (n < ntl) {
+                            const int j = 8 * n + fg;
+                            dmma_f64(acc[n], ae, j < dd ? __ldg(ew + j) : 0.0);  // B[k = t][n = g]
+                        }
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < kNtMax; n++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const int j = 8 * n + 2 * ft + e;
+                    if (n < ntl && j < dd && fg < Mb) puc[(warp * M + fg) * dd + j] = acc[n][e];
+                }
+        } else if (FAST && MT == 2) {
             // lane (j, half): 16 of the warp's 32 rows for both samples, so each
             // encW^T pair is loaded once for the two samples; halves combine
             // with one shuffle (2/3 of the generic loop's shared-memory wavefronts)
