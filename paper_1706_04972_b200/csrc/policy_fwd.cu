@@ -715,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
             for (int n = 0; n < kNtMax; n++) acc[n][0] = acc[n][1] = 0.0;
             for (int ib = warp * 32; ib < ((skip & 1) ? 0 : T); ib += kThreads) {
-#pragma unroll 2
+#pragma unroll
                 for (int ks = 0; ks < 8; ks++) {
                     const int i = ib + 4 * ks + ft;
                     const bool ok = i < T;
