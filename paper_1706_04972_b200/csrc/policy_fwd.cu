@@ -1417,7 +1417,9 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             const int enc_smem = variant < 2, spec = (variant % 2 == 0) && MT <= 4 && variant_mode == 1;
             if (variant % 2 == 0 && !spec) continue;
             DecArgs &a = pl.proto;
-            const int Tpad = (T + 1) & ~1;
+            // score rows [M][Tpad] with Tpad == 4 (mod 16) doubles: the DM path's
+            // fragment loads (8 samples x 4 rows) hit distinct banks
+            const int Tpad = ((T + 11) & ~15) + 4;
             int o = 0;
             auto take = [&](int n) {
                 const int r = o;
