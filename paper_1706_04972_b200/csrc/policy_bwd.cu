@@ -1168,6 +1168,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         // encoder: the decoders' step-0 state gradients, advantage-weighted and
         // summed over the samples: thread (u, which = dh|dc, slice of 2), fixed-
         // order combine; scratch in s_da (256 doubles, free until the first step)
+        static_assert(kLstmThreads == 4 * kH, "the prologue sum maps 256 threads to (u, which, slice)");
         double *part = s_da;  // [which][slice][64]
         const int u = tid & 63, sl = (tid >> 6) & 1, which = tid >> 7;
         const double *src = which ? sum_dc : sum_dh;
