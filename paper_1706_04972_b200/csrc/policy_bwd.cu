@@ -815,6 +815,16 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     if (n * 8 < dd8) dmma884(dA[n], aa, S.du[r * kDuLd + n * 8 + g]);
             }
             DP_APHASE(4);
+            // every shared operand of this chunk is consumed: the barrier comes
+            // before the partial stores (registers only), and after a tile's
+            // last chunk (GM) the next tile's operands go out now, so they land
+            // while the stores drain
+            __syncthreads();  // al / ds / q / du / this enc buffer are overwritten next
+            if (GM && ch == n_chunks - 1 && tl + 1 < tile1) {
+                stage_tile(tl + 1);
+                stage_enc(0, 0);
+            }
+            DP_APHASE(6);
             const int i = i0 + mr;
             if (i < T) {
                 const size_t unit = per_sample ? (size_t)(tl / tps) : (size_t)tl;
@@ -845,8 +855,6 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     }
             }
             DP_APHASE(5);
-            __syncthreads();  // al / ds / this enc buffer are overwritten by the next chunk
-            DP_APHASE(6);
         }
         if (GM) {
             // dq holds ds proj = this tile's dh_ext contribution
@@ -857,10 +865,6 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                     const double2 v = *dst;
                     *dst = make_double2(v.x + dq[n][0], v.y + dq[n][1]);
                 }
-            if (tl + 1 < tile1) {
-                stage_tile(tl + 1);
-                stage_enc(0, 0);
-            }
             first_cta_tile = false;
             DP_APHASE(7);
             continue;
