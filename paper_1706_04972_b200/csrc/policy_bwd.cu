@@ -289,172 +289,9 @@ __global__ void __launch_bounds__(kThreads) row_prep_kernel(
 }
 
 // ------------------------------------------------------------------ B0g / B1fg
-// Advantage-weighted halves of B0 and B1f in the split backward.  With
-// dz0 = onehot(choice) - p and du0 = dev_table[:D]^T dz0 (row_du, unscaled):
-//   b_out      += sum_r adv_r dz0[r]
-//   dev_table  += sum_r adv_r dz0[r] (x) u[r]
-//   w_out[:64] += sum_r adv_r h[r] (x) du0[r]          (out_grads_kernel)
-//   w_att      += sum_r adv_r h[r] (x) dq[r]           (watt_grad_kernel)
-// Rows are split evenly over 2 x SMs CTAs; operands stream from L2 with no
-// staging (many resident CTAs hide the latency); partials use row_prep's /
-// row_fin's layouts and the same ordered reductions.
-// CTA = a range of (sample k, slice of its T steps) units: the advantage is
-// one scalar per unit; rows are staged through shared memory in 32-row tiles
-// (coalesced loads, one latency per tile), then reduced from shared memory.
-constexpr int kGT = 32;  // rows per staged tile
-
-struct OutGradSmem {
-    double h[kGT][kH];
-    double du[kGT][kMaxDD];
-    double u[kGT][kMaxDD];
-    double dz[kGT][kMaxD];
-};
-
-__global__ void __launch_bounds__(kThreads) out_grads_kernel(PolicyDims dm, int parts, int n_units, int units_per_cta,
-                                                             const double *__restrict__ adv,
-                                                             const double *__restrict__ act_p,
-                                                             const uint8_t *__restrict__ choice,
-                                                             const double *__restrict__ act_u,
-                                                             const double *__restrict__ act_h,
-                                                             const double *__restrict__ row_du,
-                                                             double *__restrict__ partial) {
-    __shared__ OutGradSmem S;
-    const int tid = threadIdx.x;
-    const int T = dm.T, D = dm.D, dd = dm.dd;
-    const int tp = (T + parts - 1) / parts;
-    const int gi = tid >> 2, go = tid & 3;  // w_out rows i = gi, cols o = go + 4x
-    double tw[kMaxDD / 4], tdev[4] = {0.0, 0.0, 0.0, 0.0}, tb = 0.0;  // advantage-weighted totals
-#pragma unroll
-    for (int x = 0; x < kMaxDD / 4; x++) tw[x] = 0.0;
-    const int u0 = blockIdx.x * units_per_cta, u1 = min(n_units, u0 + units_per_cta);
-    for (int un = u0; un < u1; un++) {
-        const int k = un / parts, part = un - k * parts;
-        const int r0 = k * T + part * tp, r1 = k * T + min(T, (part + 1) * tp);
-        const double w = adv[k];
-        double gw[kMaxDD / 4], gdev[4] = {0.0, 0.0, 0.0, 0.0}, gb = 0.0;
-#pragma unroll
-        for (int x = 0; x < kMaxDD / 4; x++) gw[x] = 0.0;
-        for (int rb = r0; rb < r1; rb += kGT) {
-            const int nr = min(kGT, r1 - rb);
-            __syncthreads();
-            for (int x = tid; x < kGT * kH; x += kThreads) {
-                const int r = x >> 6, i = x & 63;
-                S.h[r][i] = r < nr ? act_h[(size_t)(rb + r) * kH + i] : 0.0;
-            }
-            for (int x = tid; x < kGT * dd; x += kThreads) {
-                const int r = x / dd, o = x - r * dd;
-                const bool ok = r < nr;
-                S.du[r][o] = ok ? row_du[(size_t)(rb + r) * dd + o] : 0.0;
-                S.u[r][o] = ok ? act_u[(size_t)(rb + r) * dd + o] : 0.0;
-            }
-            for (int x = tid; x < kGT * D; x += kThreads) {
-                const int r = x / D, d = x - r * D;
-                S.dz[r][d] = r < nr ? (d == choice[rb + r] ? 1.0 : 0.0) - act_p[(size_t)(rb + r) * D + d] : 0.0;
-            }
-            __syncthreads();
-#pragma unroll 4
-            for (int r = 0; r < kGT; r++) {
-                const double hv = S.h[r][gi];
-#pragma unroll
-                for (int x = 0; x < kMaxDD / 4; x++) {
-                    const int o = go + 4 * x;
-                    if (o < dd) gw[x] = fma(hv, S.du[r][o], gw[x]);
-                }
-            }
-#pragma unroll
-            for (int y = 0; y < 4; y++) {
-                const int e = tid + kThreads * y;
-                if (e < D * dd) {
-                    const int d = e / dd, o = e - d * dd;
-                    double v = gdev[y];
-                    for (int r = 0; r < kGT; r++) v = fma(S.dz[r][d], S.u[r][o], v);
-                    gdev[y] = v;
-                }
-            }
-            if (tid < D)
-                for (int r = 0; r < kGT; r++) gb += S.dz[r][tid];
-        }
-        tb = fma(w, gb, tb);
-#pragma unroll
-        for (int y = 0; y < 4; y++) tdev[y] = fma(w, gdev[y], tdev[y]);
-#pragma unroll
-        for (int x = 0; x < kMaxDD / 4; x++) tw[x] = fma(w, gw[x], tw[x]);
-    }
-    const size_t na = (size_t)D + D * dd + 2 * kH * dd;
-    double *out = partial + (size_t)blockIdx.x * na;
-    if (tid < D) out[tid] = tb;
-#pragma unroll
-    for (int y = 0; y < 4; y++) {
-        const int e = tid + kThreads * y;
-        if (e < D * dd) out[D + e] = tdev[y];
-    }
-#pragma unroll
-    for (int x = 0; x < kMaxDD / 4; x++) {
-        const int o = go + 4 * x;
-        if (o < dd) out[D + D * dd + gi * dd + o] = tw[x];
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) watt_grad_kernel(int T, int parts, int n_units, int units_per_cta,
-                                                             const double *__restrict__ adv,
-                                                             const double *__restrict__ act_h,
-                                                             const double *__restrict__ row_dq,
-                                                             double *__restrict__ partial) {
-    __shared__ double sh[kGT][kH], sq[kGT][kH];
-    const int tid = threadIdx.x;
-    const int a = tid >> 4, b = tid & 15;  // l in {a + 16i}, j in {b + 16jj}
-    const int tp = (T + parts - 1) / parts;
-    double tot[4][4];
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) tot[i][jj] = 0.0;
-    const int u0 = blockIdx.x * units_per_cta, u1 = min(n_units, u0 + units_per_cta);
-    for (int un = u0; un < u1; un++) {
-        const int k = un / parts, part = un - k * parts;
-        const int r0 = k * T + part * tp, r1 = k * T + min(T, (part + 1) * tp);
-        double acc[4][4];
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int jj = 0; jj < 4; jj++) acc[i][jj] = 0.0;
-        for (int rb = r0; rb < r1; rb += kGT) {
-            const int nr = min(kGT, r1 - rb);
-            __syncthreads();
-            for (int x = tid; x < kGT * kH; x += kThreads) {
-                const int r = x >> 6, i = x & 63;
-                const bool ok = r < nr;
-                sh[r][i] = ok ? act_h[(size_t)(rb + r) * kH + i] : 0.0;
-                sq[r][i] = ok ? row_dq[(size_t)(rb + r) * kH + i] : 0.0;
-            }
-            __syncthreads();
-#pragma unroll 4
-            for (int r = 0; r < kGT; r++) {
-                double hv[4], qv[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) hv[i] = sh[r][a + 16 * i];
-#pragma unroll
-                for (int jj = 0; jj < 4; jj++) qv[jj] = sq[r][b + 16 * jj];
-#pragma unroll
-                for (int i = 0; i < 4; i++)
-#pragma unroll
-                    for (int jj = 0; jj < 4; jj++) acc[i][jj] = fma(hv[i], qv[jj], acc[i][jj]);
-            }
-        }
-        const double w = adv[k];
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int jj = 0; jj < 4; jj++) tot[i][jj] = fma(w, acc[i][jj], tot[i][jj]);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++)
-            partial[(size_t)blockIdx.x * kH * kH + (a + 16 * i) * kH + b + 16 * jj] = tot[i][jj];
-}
-
-// B0g + B1fg fused: one pass over the rows computes every advantage-weighted
+// Advantage-weighted halves of B0 and B1f in the split backward (dz0 =
+// onehot(choice) - p, du0 = dev_table[:D]^T dz0 from the rows pass):
+// one pass over the rows computes every advantage-weighted
 // output-side gradient,
 //   [w_att | w_out[:64]] += (adv o H)^T [DQ | DU]     (64 x (64 + dd), DMMA)
 //   dev_table          += (adv o DZ)^T U            (D x dd, SIMT)
@@ -1848,21 +1685,6 @@ int run_att_fin(dp_policy *p, const double *params, double *grad, cudaStream_t s
 int run_b0(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
            cudaStream_t st) {
     const PolicyDims &dm = p->dims;
-    if (mode == kGradsOnly) {
-        const int K = rows / dm.T, parts = K >= 2 * kNumSMs ? 1 : ceil_div(2 * kNumSMs, K);
-        const int n_units = K * parts, upc = ceil_div(n_units, 2 * kNumSMs), used = ceil_div(n_units, upc);
-        out_grads_kernel<<<used, kThreads, 0, st>>>(dm, parts, n_units, upc, adv, p->act_p, p->act_choice, p->act_u,
-                                                    p->act_h, p->row_du, p->partial);
-        DP_LAUNCH_CHECK();
-        const int na = dm.D + dm.D * dm.dd + 2 * kH * dm.dd;
-        launch_reduce(p->partial, used, na, dm.D, grad + dm.off.b_out, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(p->partial + dm.D, used, na, dm.D * dm.dd, grad + dm.off.dev_table, 0, st);
-        DP_LAUNCH_CHECK();
-        launch_reduce(p->partial + dm.D + dm.D * dm.dd, used, na, kH * dm.dd, grad + dm.off.w_out, 0, st);
-        DP_LAUNCH_CHECK();
-        return DP_OK;
-    }
     const Grid g = persist_grid(rows, kTile);
     const size_t smem = sizeof(PrepSmem);
     DP_CUDA_TRY(allow_big_smem((const void *)row_prep_kernel, smem));
@@ -1886,15 +1708,6 @@ int run_b0(dp_policy *p, const double *params, int rows, const double *adv, doub
 int run_b1f(dp_policy *p, const double *params, int rows, const double *adv, double *grad, int mode,
             cudaStream_t st) {
     const PolicyDims &dm = p->dims;
-    if (mode == kGradsOnly) {
-        const int K = rows / dm.T, parts = K >= 2 * kNumSMs ? 1 : ceil_div(2 * kNumSMs, K);
-        const int n_units = K * parts, upc = ceil_div(n_units, 2 * kNumSMs), used = ceil_div(n_units, upc);
-        watt_grad_kernel<<<used, kThreads, 0, st>>>(dm.T, parts, n_units, upc, adv, p->act_h, p->row_dq, p->partial);
-        DP_LAUNCH_CHECK();
-        launch_reduce(p->partial, used, kH * kH, kH * kH, grad + dm.off.w_att, 0, st);
-        DP_LAUNCH_CHECK();
-        return DP_OK;
-    }
     const Grid g = tiles_grid(rows, kFinTile);
     const size_t smem = sizeof(FinSmem);
     DP_CUDA_TRY(allow_big_smem((const void *)row_fin_kernel, smem));
