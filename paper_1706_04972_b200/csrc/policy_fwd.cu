@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
 #pragma unroll
-        for (int m = 0; m < MT; m++) lsm[m] = (skip & 8) ? lsm[m] : warp_sum(lsm[m]);
+        for (int m = 0; m < MT; m++) lsm[m] = ((skip & 8) || (FAST && MT == 2)) ? lsm[m] : warp_sum(lsm[m]);
         __syncwarp();
         // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
         // (lane = (m, j); full 32-row blocks read e and encW^T as 16-byte pairs)
@@ -742,7 +742,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             // with one shuffle (2/3 of the generic loop's shared-memory wavefronts)
             const int j = lane & 15, hh = lane >> 4, jj = j < dd ? j : dd - 1;
             const int i0 = warp * 32 + hh * 16, n = (skip & 1) ? 0 : max(0, min(16, T - i0));
-            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+            // the same pass also sums the e values (the warp's softmax partial sum,
+            // in place of a 5-level butterfly): every lane of a half holds it
+            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
             if (n == 16) {
                 const double2 *ap0 = reinterpret_cast<const double2 *>(alS + i0);
                 const double2 *ap1 = reinterpret_cast<const double2 *>(alS + a.Tpad + i0);
@@ -754,17 +756,27 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     c1 = fma(x.y, e.y, c1);
                     d0 = fma(y.x, e.x, d0);
                     d1 = fma(y.y, e.y, d1);
+                    s0 += x.x + x.y;
+                    s1 += y.x + y.y;
                 }
             } else {
                 for (int ii = 0; ii < n; ii++) {
                     const double e = encW[jj * a.ewld + i0 + ii];
                     c0 = fma(alS[i0 + ii], e, c0);
                     d0 = fma(alS[a.Tpad + i0 + ii], e, d0);
+                    s0 += alS[i0 + ii];
+                    s1 += alS[a.Tpad + i0 + ii];
                 }
             }
             double v0 = c0 + c1, v1 = d0 + d1;
             v0 += __shfl_xor_sync(0xffffffffu, v0, 16);
             v1 += __shfl_xor_sync(0xffffffffu, v1, 16);
+            s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+            s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+            if (!(skip & 8)) {
+                lsm[0] = s0;
+                lsm[1] = s1;
+            }
             if (j < dd) puc[(warp * M + hh) * dd + j] = hh ? v1 : v0;
         } else
         for (int pi = lane; pi < ((skip & 1) ? 0 : Mb * dd); pi += 32) {
