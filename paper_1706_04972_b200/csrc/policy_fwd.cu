@@ -330,7 +330,7 @@ struct DecArgs {
     int M, Tpad, ewld;
     // shared-memory offsets (doubles)
     int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_uh, o_alpha, o_pm, o_ps, o_puc, o_pz, o_gn, o_hc,
-        o_cc, o_ac, o_pcg, o_misc, o_v, o_wo, o_rn;
+        o_cc, o_ac, o_pcg, o_misc, o_v, o_wo, o_rn, o_fin;
 };
 
 // q = x / n for 0 <= x < MT * n without an integer division (MT <= 8)
@@ -371,6 +371,22 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the generic alternatives are compiled out, so the per-step loop's hot code
 // is compact (the draw chain measurably stalls on instruction fetch when it
 // jumps across the cold paths).
+// FAST: the draw warp leaves step s's (zsc, esum, gmx, gsum) in fin and its
+// choice in prev; a pcg warp writes the row's global cache entries a step later
+__device__ __forceinline__ void fin_store(const DecArgs &a, const double *fin, const int *prev, int k0, int m, int M,
+                                          int T, int s) {
+    if (k0 + m >= a.K) return;
+    const size_t row = (size_t)(k0 + m) * T + s;
+    const int ch = prev[(((s & 1) ^ 1) * M) + m];
+    const double *f = fin + ((s & 1) * M + m) * 4;
+    a.choice[row] = (uint8_t)ch;
+    if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
+    a.act_lz[row * 2] = f[0];
+    a.act_lz[row * 2 + 1] = f[1];
+    a.act_stat[row * 2] = f[2];  // softmax stats (max, sum) for the backward's recompute of alpha
+    a.act_stat[row * 2 + 1] = f[3];
+}
+
 template <int MT, bool PS, bool SPEC, bool FAST = false>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     extern __shared__ __align__(16) double sm[];
@@ -401,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);  // [2][M] previous choice, by step parity
     double *rnext = sm + a.o_rn;  // [2][M] the step's uniform, by step parity (pcg warps)
+    double *fin = sm + a.o_fin;   // FAST: [2][M][4] (zsc, esum, gmx, gsum) of the step, by parity
     // pcg warps: with 3 Mb <= 8 warps, warp 2 Mb + m steps sample m's PCG64 stream
     // during E and leaves the next step's uniform in rnext (off the draw chain)
     const bool pcgw = FAST || 3 * Mb <= kWarps;
@@ -1049,13 +1066,22 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     pcg[2 * m + 1] = rs.lo;
                 }
                 prev[(par ^ 1) * M + m] = ch;
-                a.choice[row] = (uint8_t)ch;
-                if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
-                a.act_lz[row * 2] = zsc;
-                a.act_lz[row * 2 + 1] = esum;
-                // softmax stats (max, sum) for the backward's recompute of alpha
-                a.act_stat[row * 2] = gmx;
-                a.act_stat[row * 2 + 1] = gsum;
+                if (FAST) {
+                    // the row's global stores are issued by the pcg warp one step on
+                    double *f = fin + (par * M + m) * 4;
+                    f[0] = zsc;
+                    f[1] = esum;
+                    f[2] = gmx;
+                    f[3] = gsum;
+                } else {
+                    a.choice[row] = (uint8_t)ch;
+                    if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
+                    a.act_lz[row * 2] = zsc;
+                    a.act_lz[row * 2 + 1] = esum;
+                    // softmax stats (max, sum) for the backward's recompute of alpha
+                    a.act_stat[row * 2] = gmx;
+                    a.act_stat[row * 2 + 1] = gsum;
+                }
             }
         }
         if (split && warp >= Mb && warp < 2 * Mb) {
@@ -1105,12 +1131,15 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 a.act_uc[row * dd + lane] = ucn;
             }
         }
-        if (pcgw && !a.forced && warp >= 2 * Mb && warp < 3 * Mb && lane == 0) {
+        if (pcgw && warp >= 2 * Mb && warp < 3 * Mb && lane == 0) {
             const int m = warp - 2 * Mb;
-            const u128 ns = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
-            pcg[2 * m] = ns.hi;
-            pcg[2 * m + 1] = ns.lo;
-            rnext[(par ^ 1) * M + m] = pcg_double(ns);
+            if (!a.forced) {
+                const u128 ns = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
+                pcg[2 * m] = ns.hi;
+                pcg[2 * m + 1] = ns.lo;
+                rnext[(par ^ 1) * M + m] = pcg_double(ns);
+            }
+            if (FAST && t > 0) fin_store(a, fin, prev, k0, m, M, T, t - 1);  // the previous step's row
         }
         if (SPEC && warp >= Mb && t + 1 < T) {
             // next step's LSTM cell for every possible choice d (the idle warps)
@@ -1144,6 +1173,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         DP_PHASE(2);
     }
 #undef DP_PHASE
+    if (FAST && tid < Mb && T > 0) fin_store(a, fin, prev, k0, tid, M, T, T - 1);  // the last step's row
     if (clk_on)
 #pragma unroll
         for (int i = 0; i < 3; i++) g_phase_clk[i] += clk_acc[i];
@@ -1459,6 +1489,7 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + 2 * M);
             a.o_rn = take(2 * M);
+            a.o_fin = take(8 * M);
             a.o_v = take(kH * D);
             a.o_wo = take(kH * dd);
             const size_t bytes = (size_t)o * sizeof(double);
