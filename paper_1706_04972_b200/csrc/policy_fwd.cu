@@ -371,14 +371,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the generic alternatives are compiled out, so the per-step loop's hot code
 // is compact (the draw chain measurably stalls on instruction fetch when it
 // jumps across the cold paths).
-// FAST: the draw warp leaves step s's (zsc, esum, gmx, gsum) in fin and its
+// FAST: the draw warp leaves step s's (zsc, esum, gmx, gsum, p) in fin and its
 // choice in prev; a pcg warp writes the row's global cache entries a step later
 __device__ __forceinline__ void fin_store(const DecArgs &a, const double *fin, const int *prev, int k0, int m, int M,
                                           int T, int s) {
     if (k0 + m >= a.K) return;
     const size_t row = (size_t)(k0 + m) * T + s;
     const int ch = prev[(((s & 1) ^ 1) * M) + m];
-    const double *f = fin + ((s & 1) * M + m) * 4;
+    const double *f = fin + ((s & 1) * M + m) * 8;
+    for (int d = 0; d < a.dm.D; d++) {
+        a.act_p[row * a.dm.D + d] = f[4 + d];
+        if (a.probs_out) a.probs_out[row * a.dm.D + d] = f[4 + d];
+    }
     a.choice[row] = (uint8_t)ch;
     if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
     a.act_lz[row * 2] = f[0];
@@ -417,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);  // [2][M] previous choice, by step parity
     double *rnext = sm + a.o_rn;  // [2][M] the step's uniform, by step parity (pcg warps)
-    double *fin = sm + a.o_fin;   // FAST: [2][M][4] (zsc, esum, gmx, gsum) of the step, by parity
+    double *fin = sm + a.o_fin;   // FAST: [2][M][8] (zsc, esum, gmx, gsum, p[4]) of the step, by parity
     // pcg warps: with 3 Mb <= 8 warps, warp 2 Mb + m steps sample m's PCG64 stream
     // during E and leaves the next step's uniform in rnext (off the draw chain)
     const bool pcgw = FAST || 3 * Mb <= kWarps;
@@ -1030,7 +1034,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 for (; i < D; i++) esum += __shfl_sync(0xffffffffu, ez, i);
             }
             const double pr = fm_div(ez, esum);
-            if (lane < D) {
+            if (FAST) {
+                if (lane < D) fin[(par * M + m) * 8 + 4 + lane] = pr;  // stored by the pcg warp
+            } else if (lane < D) {
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
             }
@@ -1068,7 +1074,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 prev[(par ^ 1) * M + m] = ch;
                 if (FAST) {
                     // the row's global stores are issued by the pcg warp one step on
-                    double *f = fin + (par * M + m) * 4;
+                    double *f = fin + (par * M + m) * 8;
                     f[0] = zsc;
                     f[1] = esum;
                     f[2] = gmx;
@@ -1174,6 +1180,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     }
 #undef DP_PHASE
     if (FAST && tid < Mb && T > 0) fin_store(a, fin, prev, k0, tid, M, T, T - 1);  // the last step's row
+    __syncthreads();  // the log-prob pass below reads those rows from other threads
     if (clk_on)
 #pragma unroll
         for (int i = 0; i < 3; i++) g_phase_clk[i] += clk_acc[i];
@@ -1489,7 +1496,7 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + 2 * M);
             a.o_rn = take(2 * M);
-            a.o_fin = take(8 * M);
+            a.o_fin = take(16 * M);
             a.o_v = take(kH * D);
             a.o_wo = take(kH * dd);
             const size_t bytes = (size_t)o * sizeof(double);
