@@ -1072,7 +1072,10 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
         clk_last = now_;                               \
     }
     __syncthreads();
-    for (int t = T - 1; t >= 0; t--) {
+    // this slot's da row in the gates array (in place), walked backwards
+    double *grow = gates + ((size_t)(q0 + (live ? xm : 0)) * T + (T - 1)) * kG + xu;
+    for (int t = T - 1; t >= 0; t--, grow -= kG) {
+        double da_i = 0.0, da_f = 0.0, da_o = 0.0, da_g = 0.0;
         if (live) {
             const double iv = cur.i, fv = cur.f, ov = cur.o, gv = cur.g, cp = cur.cp;
             const double dh = s_dh[x] + cur.dx;
@@ -1082,26 +1085,28 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
             const double dg = dcv * iv;
             const double df = dcv * cp;
             s_dc[x] = dcv * fv;
-            const double da_i = di * iv * (1.0 - iv);
-            const double da_f = df * fv * (1.0 - fv);
-            const double da_o = d_o * ov * (1.0 - ov);
-            const double da_g = dg * (1.0 - gv * gv);
+            da_i = di * iv * (1.0 - iv);
+            da_f = df * fv * (1.0 - fv);
+            da_o = d_o * ov * (1.0 - ov);
+            da_g = dg * (1.0 - gv * gv);
             double *sd = s_da + xm * kG + xu;
             sd[0] = da_i;
             sd[kH] = da_f;
             sd[2 * kH] = da_o;
             sd[3 * kH] = da_g;
-            double *g = gates + ((size_t)(q0 + xm) * T + t) * kG;
-            g[xu] = da_i;
-            g[kH + xu] = da_f;
-            g[2 * kH + xu] = da_o;
-            g[3 * kH + xu] = da_g;
         }
         cur = nxt;
         load(t - 2, nxt);  // lands during this and the next step's barrier + mat-vec
         DP_LPHASE(0);
         __syncthreads();
         DP_LPHASE(1);
+        if (live) {
+            // the global da row after the barrier: off the elementwise chain
+            grow[0] = da_i;
+            grow[kH] = da_f;
+            grow[2 * kH] = da_o;
+            grow[3 * kH] = da_g;
+        }
         if (live) tc = fm_gate_act(cur.c, true);  // tanh; independent of the mat-vec below: the chains interleave
         // per sample: partial row sums over this lane's 8 columns, then a
         // reduce-scatter butterfly: each xor level halves the rows a lane
