@@ -529,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             // ---- A: gates + LSTM cell (policy.py:292-294, 224-233) ----
             // every sample slot computes (no branches between the chains); stores check Mb
             double act[MT], cn[MT], hn[MT];
+            double hkeep = 0.0, ckeep = 0.0;  // (MT <= 4) this lane's sample: cached after the barrier
 #pragma unroll
             for (int m = 0; m < MT; m++) act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
 #pragma unroll
@@ -559,9 +560,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     if (gate == m && m < Mb) {
                         cst[m] = cq;
                         hS[m * kH + u] = hq;
-                        acth[m * sH] = hq;
-                        actc[m * sH] = cq;
                     }
+                hkeep = hq;
+                ckeep = cq;
             } else {
 #pragma unroll
                 for (int m = 0; m < MT; m++) hn[m] = act[m] * tanh_x(cn[m]);
@@ -575,6 +576,11 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     }
             }
             __syncthreads();
+            if (MT <= 4 && gate < Mb) {
+                // the step's h / c cache rows after the barrier (off A's tail)
+                acth[gate * sH] = hkeep;
+                actc[gate * sH] = ckeep;
+            }
         }
         DP_PHASE(0);
         // ---- C: scores s = proj @ h (policy.py:296), warp-local softmax stats + partials ----
