@@ -218,3 +218,27 @@ def test_attention_softmax_shift_paths_vs_oracle(scale):
         assert lp[k] == pytest.approx(olp, rel=1e-10)
     got = P.grad_log_prob(params, feats, [int(x) for x in pl[0]])
     assert _relnorm(got, pol.grad([int(x) for x in pl[0]])) < 1e-8
+
+
+@pytest.mark.parametrize("name,K,picks", [("C3", 256, (0, 1, 127, 255)), ("C5", 4096, (0, 2049, 4095))])
+def test_bench_size_decoder_vs_oracle(name, K, picks):
+    """The decoder instantiations bench.py times (C3 K=256: 2 samples per CTA,
+    FAST path; C5 K=4096: 8 samples per CTA, DM path) at their full sizes:
+    oracle spot checks via PCG64 jumps, and the size-independent property that
+    the teacher-forced pass over the whole sampled batch reproduces every
+    sampled log-probability."""
+    gg, topo, params, feats = _setup(name, seed=6)
+    T = len(feats)
+    pl, lp = P.sample_batch(params, feats, np.random.default_rng(91), K)
+    assert pl.shape == (K, T) and np.isfinite(lp).all() and (lp <= 0).all()
+    assert pl.min() >= 0 and pl.max() < topo.num_devices
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    for k in picks:
+        rng = np.random.default_rng(91)
+        rng.bit_generator.advance(k * T)
+        opl, olp, _ = pol.sample(rng)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
+    _, _, tlp, _ = P._teacher_forced(params, feats, [list(r) for r in pl])
+    np.testing.assert_allclose(tlp.cpu().numpy(), lp, rtol=LP_RTOL, atol=0)
