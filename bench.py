@@ -383,11 +383,15 @@ def main():
     dec_flops = sum(decoder_flops_per_placement(c.T, c.task.topo.num_devices) * c.K_local for c in ctls)
     pol_flops = sum(policy_flops_per_placement(c.T, c.task.topo.num_devices, c.K) * c.K_local for c in ctls)
     achieved = dec_flops / (dec_ms * 1e-3) / 1e12
-    tr = ncu_traffic("dec_kernel")  # DRAM bytes per launch from the committed ncu capture
+    # DRAM bytes per launch from the committed ncu capture, which is of the default
+    # workload (C3, K=256 on one GPU); other workloads report null rather than its number
+    same_wl = args.config == "C3" and all(c.K_local == 256 for c in ctls)
+    tr = ncu_traffic("dec_kernel") if same_wl else None
     roofline = {
         "kernel": "dec_kernel (dp_policy_decode)", "bound": "fp64", "achieved": achieved, "peak": peak64,
         "unit": "TFLOP/s", "frac": achieved / peak64 if peak64 else None,
-        "traffic": (tr or {}).get("bytes_per_launch"), "traffic_source": (tr or {}).get("source"),
+        "traffic": (tr or {}).get("bytes_per_launch"), "traffic_source": (tr or {}).get("source") if tr else
+        "none: the committed ncu capture is of C3 K=256 on one GPU, not this workload",
         "peak_source": "measured fp64 DFMA probe (dp_fp64_fma_probe) on this GPU; MEASURED_PEAKS.json "
                        "has no fp64 figure (bf16 tensor peak is not the denominator of an fp64 kernel)",
         "algorithmic_flops_per_launch": dec_flops, "avg_launch_ms": dec_ms,
