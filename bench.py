@@ -131,12 +131,13 @@ def decoder_flops_per_placement(T, D, dd=16, H=64):
     return T * (2 * (dd + H) * 4 * H + 4 * T * H + 2 * 2 * H * dd + 2 * dd * D)
 
 
-def ncu_traffic(kernel):
+def ncu_traffic(kernel, suffix=""):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of ``kernel`` from
-    the latest committed ncu --set full capture (profiles/rNN_ncu_summary.json)."""
+    the latest committed ncu --set full capture of the workload (C3 K=256:
+    profiles/rNN_ncu_summary.json; C5 K=4096: profiles/rNN_C5_ncu_summary.json)."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r[0-9][0-9]{suffix}_ncu_summary.json")))
     for f in reversed(files):
         try:
             d = json.load(open(f)).get(kernel)
@@ -383,15 +384,16 @@ def main():
     dec_flops = sum(decoder_flops_per_placement(c.T, c.task.topo.num_devices) * c.K_local for c in ctls)
     pol_flops = sum(policy_flops_per_placement(c.T, c.task.topo.num_devices, c.K) * c.K_local for c in ctls)
     achieved = dec_flops / (dec_ms * 1e-3) / 1e12
-    # DRAM bytes per launch from the committed ncu capture, which is of the default
-    # workload (C3, K=256 on one GPU); other workloads report null rather than its number
-    same_wl = args.config == "C3" and all(c.K_local == 256 for c in ctls)
-    tr = ncu_traffic("dec_kernel") if same_wl else None
+    # DRAM bytes per launch from the committed ncu capture of this workload (C3 K=256 or
+    # C5 K=4096 on one GPU); other workloads report null rather than another's number
+    k_loc = [c.K_local for c in ctls]
+    wl = {("C3", 256): "", ("C5", 4096): "_C5"}.get((args.config, k_loc[0] if len(k_loc) == 1 else -1))
+    tr = ncu_traffic("dec_kernel", wl) if wl is not None else None
     roofline = {
         "kernel": "dec_kernel (dp_policy_decode)", "bound": "fp64", "achieved": achieved, "peak": peak64,
         "unit": "TFLOP/s", "frac": achieved / peak64 if peak64 else None,
         "traffic": (tr or {}).get("bytes_per_launch"), "traffic_source": (tr or {}).get("source") if tr else
-        "none: the committed ncu capture is of C3 K=256 on one GPU, not this workload",
+        "none: no committed ncu capture of this workload (C3 K=256 and C5 K=4096 on one GPU have one)",
         "peak_source": "measured fp64 DFMA probe (dp_fp64_fma_probe) on this GPU; MEASURED_PEAKS.json "
                        "has no fp64 figure (bf16 tensor peak is not the denominator of an fp64 kernel)",
         "algorithmic_flops_per_launch": dec_flops, "avg_launch_ms": dec_ms,

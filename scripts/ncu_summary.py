@@ -77,7 +77,7 @@ def main(tag, reps):
     with open(f"profiles/{tag}_ncu_summary.json", "w") as fh:
         json.dump(res, fh, indent=1)
     with open(f"profiles/{tag}_ncu_summary.md", "w") as fh:
-        fh.write(f"# ncu --set full summaries ({tag}), one launch each, bench.py C3 K=256\n\n")
+        fh.write(f"# ncu --set full summaries ({tag}), one launch each, bench.py {os.environ.get('NCU_WORKLOAD', 'C3 K=256')}\n\n")
         fh.write("| kernel | ms | DRAM MB/launch | SM % | mem % | fp64 pipe % | DMMA pipe % | occ % | IPC/SM | top stalls |\n")
         fh.write("|---|---|---|---|---|---|---|---|---|---|\n")
         for n, d in res.items():
