@@ -135,6 +135,13 @@ int dp_debug_fastmath_error(int64_t n, uint64_t *h_max_ulps);
  * cell for every possible choice during the draw), 2 = forbid it. */
 int dp_debug_decoder_variant(int32_t mode);
 
+/* Debug (tests): free the optional backward stores of an engine so small
+ * batches run the code paths a C5-sized batch takes.  mask bit 0 = attention
+ * numerators (the attention backward recomputes the scores), bit 1 = per-tile
+ * attention partials (backward_rows is a no-op; backward_grads runs the fused
+ * backward). */
+int dp_debug_policy_drop_stores(dp_policy *p, int32_t mask);
+
 /* Copy the assembled encoder inputs of the last encode (embed_groups(),
  * pkg/policy.py:266-268) into out[T*input_dim] (device). */
 int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream);
@@ -151,11 +158,16 @@ int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream);
  *   choice_out[K*T] optional (device): sampled device per rank
  *   logp[K]       (device) log-probability of each placement
  *   probs_out[K*T*n_dev] optional (device): per-step distributions
+ *   margin[K]     optional (device, sampling only): per sample, the minimum over
+ *                 its T draws of min_{j < n_dev-1} |r - cdf_j| — how far each
+ *                 uniform was from flipping the searchsorted choice
+ *                 (pkg/policy.py:320-323).  +inf when n_dev == 1.
  * The activations of the last decode stay in the engine (the forward cache
  * used by dp_policy_backward). */
 int dp_policy_decode(dp_policy *p, const double *params, int32_t K, int64_t k_offset, const uint64_t *h_pcg,
                      uint64_t draw_base, const int64_t *draw_counter, int64_t draws_per_count,
-                     const uint8_t *forced, uint8_t *choice_out, double *logp, double *probs_out, void *stream);
+                     const uint8_t *forced, uint8_t *choice_out, double *logp, double *probs_out, double *margin,
+                     void *stream);
 
 /* grad[P] = sum_k adv[k] * d log p(placement_k) / d params over the samples of
  * the last decode call (K must match) — grad_log_prob() weighted and summed as

@@ -35,11 +35,12 @@ SIGNATURES = {
     "dp_policy_read_inputs": (I32, [P, P, P]),
     "dp_debug_phase_clocks": (I32, [I32, P]),
     "dp_debug_decoder_variant": (I32, [I32]),
+    "dp_debug_policy_drop_stores": (I32, [P, I32]),
     "dp_debug_fastmath_error": (I32, [I64, P]),
     "dp_debug_att_clocks": (I32, [I32, P]),
     "dp_debug_sim_variant": (I32, [I32]),
     "dp_debug_lstm_clocks": (I32, [I32, P]),
-    "dp_policy_decode": (I32, [P, P, I32, I64, P, U64, P, I64, P, P, P, P, P]),
+    "dp_policy_decode": (I32, [P, P, I32, I64, P, U64, P, I64, P, P, P, P, P, P]),
     "dp_policy_backward": (I32, [P, P, I32, P, P, P]),
     "dp_policy_backward_rows": (I32, [P, P, I32, P]),
     "dp_policy_backward_grads": (I32, [P, P, I32, P, P, P]),

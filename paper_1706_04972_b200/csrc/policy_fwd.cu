@@ -327,6 +327,7 @@ struct DecArgs {
     double *act_h, *act_c, *act_g, *act_uc, *act_u, *act_p, *act_stat, *act_lz, *act_e, *act_esc;
     uint8_t *choice, *choice_out;
     double *logp, *probs_out;
+    double *margin;  // [K] or NULL: min over steps of min_{j<D-1} |r - cdf_j| (sampling only)
     int M, Tpad, ewld;
     // shared-memory offsets (doubles)
     int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_uh, o_alpha, o_pm, o_ps, o_puc, o_pz, o_gn, o_hc,
@@ -510,6 +511,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
     long long clk_last = clk_on ? clock64() : 0;
     long long clk_acc[3] = {0, 0, 0};  // in registers; one global write at the end
+    // draw warp m (< Mb <= 8 warps) keeps sample m's running sampling margin
+    double mrun = INFINITY;
 #define DP_PHASE(i)                                       \
     if (clk_on) {                                         \
         const long long now_ = clock64();                 \
@@ -1050,8 +1053,11 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             if (a.forced) {
                 ch = a.forced[row];
             } else {
-                double cdf = 0.0;
+                double cdf = 0.0, mg = INFINITY;
                 int cnt = 0;
+                // margin: distance of the uniform to every cdf boundary that can
+                // change the choice (j < D-1; the last one is clamped away)
+                const bool wm = a.margin != nullptr;
                 if (FAST || D <= 8) {
                     constexpr int DG = FAST ? 4 : 8;  // lanes gathered
                     double pv[DG];
@@ -1062,13 +1068,16 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                         if (dv < D) {
                             cdf += pv[dv];
                             cnt += (cdf <= r) ? 1 : 0;
+                            if (wm && dv < D - 1) mg = fmin(mg, fabs(r - cdf));
                         }
                 } else {
                     for (int dv = 0; dv < D; dv++) {
                         cdf += __shfl_sync(0xffffffffu, pr, dv);
                         cnt += (cdf <= r) ? 1 : 0;
+                        if (wm && dv < D - 1) mg = fmin(mg, fabs(r - cdf));
                     }
                 }
+                mrun = fmin(mrun, mg);
                 ch = cnt < D - 1 ? cnt : D - 1;
             }
             const double zsc = __shfl_sync(0xffffffffu, zs, ch);
@@ -1186,6 +1195,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     }
 #undef DP_PHASE
     if (FAST && tid < Mb && T > 0) fin_store(a, fin, prev, k0, tid, M, T, T - 1);  // the last step's row
+    if (a.margin && !a.forced && warp < Mb && lane == 0) a.margin[k0 + warp] = mrun;
     __syncthreads();  // the log-prob pass below reads those rows from other threads
     if (clk_on)
 #pragma unroll
@@ -1410,6 +1420,30 @@ extern "C" int dp_debug_decoder_variant(int32_t mode) {
     return DP_OK;
 }
 
+// Debug: free the optional backward stores so a small engine takes the code
+// paths a C5-sized one does (mask bit 0: attention numerators act_e/act_esc ->
+// score-recompute att_bwd<false>; bit 1: per-tile partials tile_part/A -> the
+// rows pass is skipped and the grads call runs the fused backward).
+extern "C" int dp_debug_policy_drop_stores(dp_policy *p, int32_t mask) {
+    DP_ENTRY();
+    DP_REQUIRE(p, "dp_debug_policy_drop_stores: NULL policy");
+    DP_CUDA_TRY(cudaDeviceSynchronize());
+    auto drop = [](double *&q) {
+        if (q) cudaFree(q);
+        q = nullptr;
+    };
+    if (mask & 1) {
+        drop(p->act_e);
+        drop(p->act_esc);
+    }
+    if (mask & 2) {
+        drop(p->tile_part);
+        drop(p->tile_partA);
+    }
+    p->rows_ready = 0;
+    return DP_OK;
+}
+
 extern "C" int dp_debug_phase_clocks(int32_t enable, int64_t *h_out) {
     DP_ENTRY();
     const int on = enable ? 1 : 0;
@@ -1539,7 +1573,7 @@ const void *dec_fn(int MT, bool fast) {
 extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, int64_t k_offset,
                                 const uint64_t *h_pcg, uint64_t draw_base, const int64_t *draw_counter,
                                 int64_t draws_per_count, const uint8_t *forced, uint8_t *choice_out,
-                                double *logp, double *probs_out, void *stream) {
+                                double *logp, double *probs_out, double *margin, void *stream) {
     DP_ENTRY();
     DP_REQUIRE(p && params && logp, "dp_policy_decode: NULL argument");
     DP_REQUIRE(K >= 1 && K <= p->k_max, "dp_policy_decode: K out of range (1..k_max)");
@@ -1585,6 +1619,7 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.choice_out = choice_out;
     a.logp = logp;
     a.probs_out = probs_out;
+    a.margin = forced ? nullptr : margin;
     a.M = pl.M;
     a.Tpad = pl.Tpad;
     a.ewld = ((dm.T + 1) & ~1) + 2;

@@ -161,6 +161,19 @@ class _DeviceCache:
         self.engine_id, self.placement = engine_id, placement
 
 
+# Sampling certification (pkg/policy.py:320-323).  The device draw compares the
+# numpy uniform r with the fp64 cdf it computes; the reference compares r with
+# its own fp64 cdf.  The two cdfs differ only by rounding: the fp64 policy
+# agrees with the reference's log-probabilities to ~1e-13 relative and its
+# per-step distributions to ~1e-15 absolute (tests), with transcendentals
+# within 4 ulp of libm (csrc/fastmath.cuh).  A draw whose margin
+# min_j |r - cdf_j| exceeds SAMPLING_MARGIN_TOL (10^3 x the 1e-12 relative
+# tolerance the parity tests hold the per-step distributions to) therefore
+# picks the reference's index; smaller margins are counted as uncertified.
+SAMPLING_MARGIN_TOL = 1e-9
+FASTMATH_MAX_ULP = 4
+
+
 # ----------------------------------------------------------------------------- device engine
 def _hp(a):
     return a.ctypes.data if a.size else None
@@ -212,9 +225,11 @@ class DevicePolicy:
                   "dp_policy_encode")
 
     def decode(self, params_dev, K, pcg=None, draw_base=0, forced=None, k_offset=0, draw_counter=None,
-               draws_per_count=0, choice=None, logp=None, probs=None, stream=None):
+               draws_per_count=0, choice=None, logp=None, probs=None, margin=None, stream=None):
         """Sample (pcg=(state, inc) as Python ints) or teacher-force (forced: uint8
-        CUDA tensor [K, T] by rank) K placements.  Returns (choice [K,T] by rank, logp [K])."""
+        CUDA tensor [K, T] by rank) K placements.  Returns (choice [K,T] by rank, logp [K]).
+        margin: optional f64 CUDA tensor [K] <- per-sample sampling margin
+        (min over steps of |r - cdf_j|, j < D-1; see ``SAMPLING_MARGIN_TOL``)."""
         import torch
 
         from . import _native as nat
@@ -233,7 +248,7 @@ class DevicePolicy:
         rc = nat.lib().dp_policy_decode(
             self.handle, nat.ptr(params_dev), K, k_offset, hp, draw_base, nat.ptr(draw_counter),
             draws_per_count, nat.ptr(forced), nat.ptr(choice), nat.ptr(logp), nat.ptr(probs),
-            nat.stream_ptr(stream))
+            nat.ptr(margin), nat.stream_ptr(stream))
         nat.check(rc, "dp_policy_decode")
         return choice, logp
 
@@ -423,15 +438,20 @@ def weighted_grad(params: PolicyParams, feats: GroupFeatures, placements, weight
     return eng.backward(pdev, len(placements), adv)
 
 
-def sample_batch(params: PolicyParams, feats: GroupFeatures, rng, K: int):
+def sample_batch(params: PolicyParams, feats: GroupFeatures, rng, K: int, return_margin: bool = False):
     """K forward_sample calls in one launch: same placements/log-probs, same
-    draws consumed.  Returns (placements [K, T] by gid, log_probs [K]) numpy."""
+    draws consumed.  Returns (placements [K, T] by gid, log_probs [K]) numpy,
+    plus the per-sample sampling margins [K] when ``return_margin``."""
+    import torch
+
     eng = engine_for(params, feats, K)
     pdev = _params_dev(params, eng)
     eng.encode(pdev)
-    choice, logp = eng.decode(pdev, K, pcg=generator_state(rng))
+    margin = torch.empty(K, dtype=torch.float64, device=eng.device) if return_margin else None
+    choice, logp = eng.decode(pdev, K, pcg=generator_state(rng), margin=margin)
     rng.bit_generator.advance(K * len(feats))
-    return eng.by_gid(choice).cpu().numpy(), logp.cpu().numpy()
+    out = (eng.by_gid(choice).cpu().numpy(), logp.cpu().numpy())
+    return out + (margin.cpu().numpy(),) if return_margin else out
 
 
 def save_checkpoint(params: PolicyParams, path):

@@ -260,6 +260,8 @@ class TrainResult:
     final_params: np.ndarray
     store_versions: int
     rejected_updates: int
+    # sampling certificate (DeviceController.sampling_certificate; new field)
+    sampling: dict | None = None
 
     @property
     def found_feasible(self) -> bool:
@@ -285,6 +287,7 @@ class _ControllerResult:
     rows: list = field(default_factory=list)
     best_r: float = math.inf
     best_placement: list | None = None
+    sampling: dict | None = None
 
 
 def policy_template(gg, topo, config: TrainerConfig) -> PolicyParams:
@@ -346,6 +349,11 @@ class DeviceController:
         T = self.T
         self.choice = torch.zeros(self.K_local, T, dtype=torch.uint8, device=dev)
         self.logp = torch.zeros(self.K_local, dtype=torch.float64, device=dev)
+        # sampling certification: per-sample margin of the last update and the
+        # running minimum / count of samples below policy.SAMPLING_MARGIN_TOL
+        self.margin = torch.full((self.K_local,), math.inf, dtype=torch.float64, device=dev)
+        self.margin_min = torch.full((1,), math.inf, dtype=torch.float64, device=dev)
+        self.n_uncertified = torch.zeros(1, dtype=torch.int64, device=dev)
         self.sim_local = None
         self.adv = torch.zeros(self.K_local, dtype=torch.float64, device=dev)
         self.grad = torch.zeros(store.params.numel(), dtype=torch.float64, device=dev)
@@ -386,7 +394,10 @@ class DeviceController:
         mark("decode")
         self.eng.decode(p, self.K_local, pcg=self.pcg, draw_base=0, k_offset=self.k_offset,
                         draw_counter=state.view(torch.int64)[3:4], draws_per_count=self.K * self.T,
-                        choice=self.choice, logp=self.logp, stream=stream)
+                        choice=self.choice, logp=self.logp, margin=self.margin, stream=stream)
+        with torch.cuda.stream(main):
+            torch.minimum(self.margin_min, self.margin.amin(0, keepdim=True), out=self.margin_min)
+            self.n_uncertified += (self.margin < policy_mod.SAMPLING_MARGIN_TOL).sum()
         mark("simulate")
         # the advantage-independent half of the backward runs on a side stream
         # while the placements are scored
@@ -481,6 +492,14 @@ class DeviceController:
             out.append(LogRow(int(r[0]), int(r[1]), int(r[2]), float(r[3]), float(r[4]), float(r[5]),
                               int(r[6]), int(r[7]), float(walls[u]) if walls else 0.0))
         return out
+
+    def sampling_certificate(self) -> dict:
+        """Minimum sampling margin over every sample drawn so far and the number
+        of samples with a draw closer than policy.SAMPLING_MARGIN_TOL to a cdf
+        boundary (those indices are not certified equal to the reference's)."""
+        return {"min_margin": float(self.margin_min.item()), "tol": policy_mod.SAMPLING_MARGIN_TOL,
+                "uncertified_samples": int(self.n_uncertified.item()),
+                "fastmath_max_ulp": policy_mod.FASTMATH_MAX_ULP}
 
     def best(self):
         st = _state_read(self.state)
@@ -621,7 +640,7 @@ class ConcurrentRunner:
 def _result_of(task, store, ctls, walls) -> "TrainResult":
     res = []
     for c in ctls:
-        r = _ControllerResult(rows=c.rows(walls))
+        r = _ControllerResult(rows=c.rows(walls), sampling=c.sampling_certificate())
         r.best_r, r.best_placement = c.best()
         res.append(r)
     rows = sorted([row for r in res for row in r.rows], key=lambda r: (r.controller_id, r.update_index))
@@ -630,7 +649,18 @@ def _result_of(task, store, ctls, walls) -> "TrainResult":
     best_report = simulate(task.gg, task.topo, best_pl) if best_pl is not None else None
     final, _ = store.snapshot()
     return TrainResult(best_placement=best_pl, best_report=best_report, log=rows, final_params=final,
-                       store_versions=store.version, rejected_updates=store.rejected)
+                       store_versions=store.version, rejected_updates=store.rejected,
+                       sampling=_merge_certs([r.sampling for r in res]))
+
+
+def _merge_certs(certs):
+    certs = [c for c in certs if c]
+    if not certs:
+        return None
+    out = dict(certs[0])
+    out["min_margin"] = min(c["min_margin"] for c in certs)
+    out["uncertified_samples"] = sum(c["uncertified_samples"] for c in certs)
+    return out
 
 
 def train_many(jobs) -> list:
@@ -698,7 +728,7 @@ def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, 
         walls += ctl.run(cfg.total_updates - 1, use_graph=use_graph, wall=True)
     torch.cuda.current_stream().synchronize()
     ctl.check_errors()
-    res = _ControllerResult(rows=ctl.rows(walls))
+    res = _ControllerResult(rows=ctl.rows(walls), sampling=ctl.sampling_certificate())
     res.best_r, res.best_placement = ctl.best()
     return res
 
@@ -739,4 +769,4 @@ def train(graph, topo, config: TrainerConfig | None = None, *, group=None) -> Tr
     best_report = simulate(gg, topo, best_pl) if best_pl is not None else None
     final, _ = store.snapshot()
     return TrainResult(best_placement=best_pl, best_report=best_report, log=rows, final_params=final,
-                       store_versions=store.version, rejected_updates=store.rejected)
+                       store_versions=store.version, rejected_updates=store.rejected, sampling=res.sampling)
