@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=None, help="placements in the CPU baseline sample")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--profile-phases", type=int, default=3)
+    ap.add_argument("--mode", choices=["step", "sim"], default="step",
+                    help="step: full REINFORCE update (headline); sim: scorer only (placements scored/s)")
+    ap.add_argument("--sim-k", type=int, default=65536, help="placements per scorer-only step")
     return ap.parse_args()
 
 
@@ -170,51 +173,281 @@ def fp64_peak_tflops(nat, torch):
 
 
 # ----------------------------------------------------------------------------- CPU baseline
-def cpu_baseline(gg, topo, k_sample=None, workers=None, name="C3"):
+def cfg_path(name):
+    return os.path.join(ROOT, "tests", "golden", CFG_FILE[name])
+
+
+def cpu_k_for(name, K):
+    """Placements per timed CPU step: the config's own K where a reference update
+    takes seconds on the host cores (C1-C4), a bounded sample for C5 (one
+    reference placement there costs ~3 s of CPU)."""
+    return K if name != "C5" else 2 * len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(names, ks):
+    """The reference's own code (oracle/_ref, installed unmodified by
+    oracle/make_ref.sh) on all host cores: one warm-up + one timed REINFORCE
+    update per task (oracle/refarm.py).  Falls back to the oracle port when the
+    reference install is absent."""
     sys.path.insert(0, ROOT)
+    from oracle import refarm
+
+    workers = len(os.sched_getaffinity(0))
+    if not refarm.available():
+        return cpu_baseline_port(names, ks)
+    tot_p, tot_s, parts = 0, 0.0, []
+    for name, K in zip(names, ks):
+        k = cpu_k_for(name, K)
+        r = refarm.time_steps(cfg_path(name), k, steps=1, warmup=1, workers=workers)
+        tot_p += r["placements"]
+        tot_s += r["seconds"]
+        parts.append(f"{name}: one update of K={k} ({r['seconds']:.2f} s)")
+    return {"value": tot_p / tot_s, "unit": UNIT, "cores": workers, "kind": "reference",
+            "sample": "; ".join(parts) + " — the unmodified reference (oracle/_ref) forward_sample + measure + "
+                      "grad_log_prob per placement on a persistent fork pool (BLAS 1 thread/process), reference "
+                      "baseline/Adam in the parent, after one warm-up update"}
+
+
+def cpu_baseline_port(names, ks):
     from oracle.trainer import cpu_step_rate
 
-    workers = workers or len(os.sched_getaffinity(0))
-    k_sample = k_sample or 2 * workers
-    r = cpu_step_rate(gg, topo, k_sample, workers=workers)
-    return {"value": r["rate"], "unit": UNIT, "cores": r["workers"], "kind": "port",
-            "sample": f"{r['placements']} placements of config {name} (sample+score+grad per placement, "
-                      f"oracle/ numpy fp64 + C simulator restatement, {r['workers']} processes), "
-                      f"{r['seconds']:.2f} s; per-placement cost is K-independent"}
+    workers = len(os.sched_getaffinity(0))
+    tot_p, tot_s = 0, 0.0
+    for name in names:
+        gg, topo, _ = load_config(name)
+        r = cpu_step_rate(gg, topo, 2 * workers, workers=workers)
+        tot_p += r["placements"]
+        tot_s += r["seconds"]
+    return {"value": tot_p / tot_s, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": f"{tot_p} placements (oracle port: numpy fp64 + C simulator restatement)"}
+
+
+def reference_extras(name):
+    """R1 (reference train() as shipped, one process) and R2 (reference simulate
+    on all cores) for the reference line."""
+    from oracle import refarm
+
+    out = {}
+    try:
+        r1 = refarm.single_process_rate(cfg_path(name), k=16)
+        out["r1_single_process"] = {"value": r1["rate"], "unit": UNIT, "cores": 1,
+                                    "sample": f"reference train(k=16, 2 updates) in one process, "
+                                              f"update 1 wall {r1['update_ms']:.0f} ms"}
+    except Exception as ex:  # pragma: no cover
+        out["r1_single_process"] = {"error": repr(ex)}
+    try:
+        n = 4096 if name != "C5" else 512
+        r2 = refarm.scorer_rate(cfg_path(name), n=n)
+        out["r2_scorer_only"] = {"value": r2["rate"], "unit": "placements scored/s", "cores": r2["workers"],
+                                 "sample": f"reference simulate over {n} random placements, fork pool"}
+    except Exception as ex:  # pragma: no cover
+        out["r2_scorer_only"] = {"error": repr(ex)}
+    return out
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    names = ["C1", "C2"] if args.config == "C4" else [args.config]
-    workers = len(os.sched_getaffinity(0))
-    k_sample = args.cpu_sample or 2 * workers
-    from oracle.trainer import cpu_step_rate
+    sys.path.insert(0, ROOT)
+    from oracle import refarm
 
-    tot_p, tot_s, K = 0, 0.0, 0
+    workers = len(os.sched_getaffinity(0))
+    if args.mode == "sim":
+        name = args.config
+        vals = []
+        for _ in range(max(1, args.steps)):
+            vals.append(refarm.scorer_rate(cfg_path(name), n=4096 if name != "C5" else 512)["rate"])
+        value = statistics.median(vals)
+        line = {"impl": "reference", "metric": "placements scored/sec (simulator only)", "value": value,
+                "unit": "placements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": f"{name}: {CFG_DESC[name]}",
+                                                "parallelism": f"cpu fork pool x{workers}"},
+                "cpu_baseline": {"value": value, "unit": "placements/s", "cores": workers, "kind": "reference",
+                                 "sample": "reference simulate over 4096 random placements per step"},
+                "e2e": {"value": value, "unit": "placements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+    names = ["C1", "C2"] if args.config == "C4" else [args.config]
+    ks = []
     for name in names:
-        gg, topo, Kc = load_config(name)
-        K += 512 if args.config == "C4" else Kc
-        for _ in range(max(0, args.warmup)):
-            cpu_step_rate(gg, topo, max(1, workers), workers=workers)
-        for _ in range(args.steps):
-            r = cpu_step_rate(gg, topo, k_sample, workers=workers)
-            tot_p += r["placements"]
-            tot_s += r["seconds"]
+        _, _, Kc = load_config(name)
+        ks.append(512 if args.config == "C4" else Kc)
+    kind = "reference" if refarm.available() else "port"
+    tot_p, tot_s = 0, 0.0
+    if kind == "reference":
+        steppers = [refarm.RefStepper(cfg_path(n), cpu_k_for(n, k), workers=workers) for n, k in zip(names, ks)]
+        try:
+            for _ in range(max(0, args.warmup)):
+                for st in steppers:
+                    st.step()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                for st in steppers:
+                    tot_p += st.step()[0]
+            tot_s = time.perf_counter() - t0
+        finally:
+            for st in steppers:
+                st.close()
+        sample = (f"{args.steps} timed updates (+{args.warmup} warm-up) of " +
+                  " + ".join(f"{n} K={cpu_k_for(n, k)}" for n, k in zip(names, ks)) +
+                  ": the unmodified reference (oracle/_ref) per placement on a persistent fork pool "
+                  "(BLAS pinned to 1 thread), reference baseline + Adam in the parent")
+    else:
+        from oracle.trainer import cpu_step_rate
+
+        for name in names:
+            gg, topo, _ = load_config(name)
+            for _ in range(args.steps):
+                r = cpu_step_rate(gg, topo, 2 * workers, workers=workers)
+                tot_p += r["placements"]
+                tot_s += r["seconds"]
+        sample = f"{args.steps} steps x {2 * workers} placements, oracle port (reference not installed)"
     value = tot_p / tot_s
+    k_cpu = [cpu_k_for(n, k) for n, k in zip(names, ks)]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": f"{args.config}: {CFG_DESC[args.config]}, K={K}",
-                                    "parallelism": "cpu processes"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"{args.steps} steps x {k_sample} placements (sample+score+grad), "
-                                   f"oracle port of the reference (numpy fp64 + C simulator)"},
+        "data": "synthetic", "config": {"workload": f"{args.config}: {CFG_DESC[args.config]}",
+                                    "k_per_step": k_cpu, "same_k_as_gpu_arm": k_cpu == ks,
+                                    "parallelism": f"cpu fork pool x{workers}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if kind == "reference":
+        line.update(reference_extras(names[0]))
+        r1 = line.get("r1_single_process", {}).get("value")
+        if r1:
+            line["per_core_vs_single_process"] = value / workers / r1
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- scorer-only arm
+def sim_bytes_per_placement(n, e, d):
+    """B_sim: algorithmic bytes per scored
+    placement = 32N + 12E + 24D + 9."""
+    return 32 * n + 12 * e + 24 * d + 9
+
+
+def run_sim(args):
+    """Placements scored/s through dp_simulate_batch (the K-sim kernel alone):
+    ``--sim-k`` random placements (by group id) per GPU per step, resident in
+    HBM; e2e adds the placements' H2D copy and the makespan/feasible D2H."""
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1706_04972_b200 import _native as nat
+    from paper_1706_04972_b200 import simulator as S
+
+    name = args.config if args.config in CFG_FILE else "C3"
+    gg, topo, _ = load_config(name)
+    n, d, K = gg.num_groups, topo.num_devices, args.sim_k
+    dg = S.device_graph(gg, topo)
+    host = np.random.default_rng(1 + rank).integers(0, d, (K, n)).astype(np.uint8)
+    pl = torch.as_tensor(host, device="cuda")
+    out = dg.simulate(pl)
+    stream = torch.cuda.current_stream()
+    l0 = nat.lib().dp_launch_count()
+    for _ in range(max(1, args.warmup)):
+        dg.simulate(pl, out=out)
+    torch.cuda.synchronize()
+    launches = (nat.lib().dp_launch_count() - l0) // max(1, args.warmup)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            evs[i][0].record(stream)
+            dg.simulate(pl, out=out)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    tot = sum(ms)
+    # e2e: pinned host placements -> device, score, makespan + feasible -> host
+    hpl = torch.from_numpy(host).pin_memory()
+    hmk = torch.empty(K, dtype=torch.float64, pin_memory=True)
+    hfe = torch.empty(K, dtype=torch.uint8, pin_memory=True)
+    dpl = torch.empty_like(pl)
+    e2e = []
+    for i in range(args.steps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dpl.copy_(hpl, non_blocking=True)
+        o = dg.simulate(dpl, out=out)
+        hmk.copy_(o["makespan"], non_blocking=True)
+        hfe.copy_(o["feasible"], non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e.append(a.elapsed_time(b))
+    e2e_tot = sum(e2e)
+    if world > 1:
+        t = torch.tensor([tot, e2e_tot], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot, e2e_tot = t.tolist()
+    if rank != 0:
+        torch.distributed.destroy_process_group()
+        return
+    value = K * world * args.steps / (tot * 1e-3)
+    e = len(gg.group_edges)
+    bsim = sim_bytes_per_placement(n, e, d)
+    pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = pk.get("hbm_gbs") or 7672.0
+    per_launch_ms = tot / args.steps
+    achieved = bsim * K / (per_launch_ms * 1e-3) / 1e9
+    tr = ncu_traffic("sim_warp_kernel", "_sim") if (name, K) == ("C3", 65536) else None
+    cpu = None
+    if world == 1 and not args.skip_cpu:
+        sys.path.insert(0, ROOT)
+        from oracle import refarm
+
+        if refarm.available():
+            r2 = refarm.scorer_rate(cfg_path(name), n=4096 if name != "C5" else 512)
+            cpu = {"value": r2["rate"], "unit": "placements/s", "cores": r2["workers"], "kind": "reference",
+                   "sample": f"R2: reference simulate over {r2['placements']} random placements on a fork pool "
+                             f"({r2['seconds']:.2f} s)"}
+            # the kernel's makespans for the same placements equal the reference's
+            chk = torch.as_tensor(np.random.default_rng(1).integers(0, d, (r2["placements"], n)).astype(np.uint8),
+                                  device="cuda")
+            mine = dg.simulate(chk)["makespan"].cpu().numpy()
+            cpu["bit_exact_makespans"] = bool(np.array_equal(mine, r2["makespans"]))
+    line = {
+        "metric": "placements scored/sec (simulator only)", "value": value, "unit": "placements/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{name}: {CFG_DESC[name]}", "k_per_gpu": K, "global_k": K * world,
+                   "placements": "numpy default_rng(1 + rank) uniform device ids, by group id",
+                   "parallelism": f"dp{world} (placements sharded, no collective)",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "e2e": {"value": K * world * args.steps / (e2e_tot * 1e-3), "unit": "placements/s",
+                "h2d_bytes_per_step": K * n, "d2h_bytes_per_step": K * 9,
+                "note": "placements H2D from pinned host -> score -> makespan + feasible D2H"},
+        "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
+        "roofline": {"kernel": "sim_warp_kernel (dp_simulate_batch)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": (tr or {}).get("bytes_per_launch"),
+                     "traffic_source": (tr or {}).get("source"),
+                     "algorithmic_bytes_per_placement": bsim, "avg_launch_ms": per_launch_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk.get("hbm_gbs") else "B200_PROFILING fallback"},
+        "cpu_baseline": cpu, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -222,6 +455,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "sim":
+        return run_sim(args)
 
     import numpy as np
     import torch
@@ -403,14 +638,7 @@ def main():
     cpu = None
     if world == 1 and not args.skip_cpu:
         try:
-            if len(ctls) == 1:
-                cpu = cpu_baseline(ctl.task.gg, ctl.task.topo, args.cpu_sample, name=args.config)
-            else:
-                # mixed batch: per-task CPU rates combined over the same K mix
-                parts = [cpu_baseline(c.task.gg, c.task.topo, args.cpu_sample, name=n) for c, n in zip(ctls, names)]
-                ks = [c.K for c in ctls]
-                cpu = dict(parts[0], value=sum(ks) / sum(k / p["value"] for k, p in zip(ks, parts)),
-                           sample=" + ".join(p["sample"] for p in parts) + "; combined over the K mix")
+            cpu = cpu_baseline(names, [c.K for c in ctls])
         except Exception as ex:  # pragma: no cover
             cpu = {"error": repr(ex)}
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
