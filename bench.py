@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--mode", choices=["step", "sim"], default="step",
                     help="step: full REINFORCE update (headline); sim: scorer only (placements scored/s)")
     ap.add_argument("--sim-k", type=int, default=65536, help="placements per scorer-only step")
+    ap.add_argument("--single-process", action="store_true",
+                    help="one process drives --gpus N devices (MultiDeviceRunner, NCCL ncclCommInitAll); "
+                         "with fewer visible GPUs the ranks share cuda:0")
     return ap.parse_args()
 
 
@@ -450,6 +453,106 @@ def run_sim(args):
         torch.distributed.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- single-process multi-GPU
+def run_single_process(args):
+    """``--single-process --gpus N``: one process, N GPUs, the plain train()
+    path (trainer.MultiDeviceRunner): K = k_per_gpu * N sharded over the
+    devices, NCCL between them, one CUDA graph per device replayed per update.
+    Per-step time = max over devices of the CUDA-event interval on each
+    device's stream (all devices synchronised on both sides)."""
+    import numpy as np
+    import torch
+
+    import paper_1706_04972_b200 as dp
+    from paper_1706_04972_b200 import _native as nat
+
+    N = args.gpus
+    vis = torch.cuda.device_count()
+    devices = list(range(N)) if vis >= N else [0] * N
+    name = args.config if args.config in CFG_FILE else "C3"
+    gg, topo, K_cfg = load_config(name)
+    k_gpu = args.k_per_gpu or K_cfg
+    total_updates = args.warmup + 2 * args.steps + 4
+    cfg = dp.TrainerConfig(k=k_gpu * N, total_updates=total_updates, seed=0, devices=tuple(devices))
+    task = dp.trainer._make_task(gg, topo, cfg)
+    seq = np.random.SeedSequence(cfg.seed).spawn(1)[0]
+    runner = dp.trainer.MultiDeviceRunner(task, cfg, devices, seq)
+    l0 = nat.lib().dp_launch_count()
+    runner.step()
+    for d in sorted(set(devices)):
+        torch.cuda.synchronize(d)
+    launches = nat.lib().dp_launch_count() - l0
+    runner.capture()
+    for _ in range(max(0, args.warmup - 1)):
+        runner.replay()
+    uniq = sorted(set(devices))
+    flush = {d: torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{d}") for d in uniq}
+    streams = {d: s for d, s in zip(devices, runner.streams)}
+    evs = [{d: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for d in uniq}
+           for _ in range(args.steps)]
+    for d in uniq:
+        torch.cuda.synchronize(d)
+    with ClockSampler(uniq[0]) as clk:
+        for i in range(args.steps):
+            for d in uniq:
+                with torch.cuda.device(d):
+                    flush[d].fill_(float(i))
+                    streams[d].wait_stream(torch.cuda.current_stream(d))
+                    evs[i][d][0].record(streams[d])
+            for g, d, s in runner._graphs:
+                with torch.cuda.device(d), torch.cuda.stream(s):
+                    g.replay()
+            for d in uniq:
+                with torch.cuda.device(d):
+                    evs[i][d][1].record(streams[d])
+                    torch.cuda.current_stream(d).wait_stream(streams[d])
+        for d in uniq:
+            torch.cuda.synchronize(d)
+    step_ms = [max(evs[i][d][0].elapsed_time(evs[i][d][1]) for d in uniq) for i in range(args.steps)]
+    tot = sum(step_ms)
+    for c in runner.ctls:
+        c.check_errors()
+    K = cfg.k
+    value = K * args.steps / (tot * 1e-3)
+    # e2e: parameters from pinned host to every device's store, one update,
+    # parameters + log row of rank 0 back
+    hp = torch.empty(runner.stores[0].params.numel(), dtype=torch.float64, pin_memory=True)
+    hp.copy_(runner.stores[0].params.cpu())
+    ho = torch.empty_like(hp, pin_memory=True)
+    hl = torch.empty(8, dtype=torch.float64, pin_memory=True)
+    e2e = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        for st, d in zip(runner.stores, devices):
+            with torch.cuda.device(d):
+                st.params.copy_(hp, non_blocking=True)
+        runner.replay()
+        with torch.cuda.device(devices[0]):
+            ho.copy_(runner.stores[0].params, non_blocking=True)
+            hl.copy_(runner.ctls[0].log[:8], non_blocking=True)
+        for d in uniq:
+            torch.cuda.synchronize(d)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+        hp.copy_(ho)
+    cert = runner.result([0.0] * runner.ctls[0].updates_done).sampling
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{name}: {CFG_DESC[name]}", "k_per_gpu": k_gpu, "global_k": K,
+                   "parallelism": f"dp{N} single process (devices {devices}; "
+                                  f"{'shared GPU, LocalGroup' if runner.shared_gpu else 'NCCL ncclCommInitAll'})",
+                   "l2": "flushed between timed steps (256 MiB write)", "cuda_graph": True},
+        "steps_per_sec": 1e3 / (tot / args.steps),
+        "e2e": {"value": K * args.steps / (sum(e2e) * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": hp.numel() * 8 * len(devices), "d2h_bytes_per_step": hp.numel() * 8 + 64,
+                "note": "host wall clock around params H2D (every device) -> graph replay -> params + log D2H"},
+        "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
+        "sampling": cert, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse()
@@ -457,6 +560,8 @@ def main():
         return run_reference(args)
     if args.mode == "sim":
         return run_sim(args)
+    if args.single_process:
+        return run_single_process(args)
 
     import numpy as np
     import torch
@@ -519,7 +624,9 @@ def main():
     runner.step()
     torch.cuda.synchronize()
     launches_per_step = nat.lib().dp_launch_count() - l0
-    use_graph = (world == 1) and not args.no_graph
+    # N > 1 over NCCL: the library's own communicator enqueues the collectives on
+    # the step's stream, so the update is captured with them (gloo: eager)
+    use_graph = all(c.xchg is None or c.xchg.capturable for c in ctls) and not args.no_graph
     if use_graph:
         runner.capture()
 
@@ -606,6 +713,7 @@ def main():
         e2e_tot = max_over_ranks(e2e_tot)
     e2e_value = K * args.steps / (e2e_tot * 1e-3)
 
+    cert = ctls[0].sampling_certificate()  # collective when sharded: every rank calls it
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -660,6 +768,7 @@ def main():
         "gpu_launches_per_step": launches_per_step,
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "sampling": cert,
         "clocks": clk.summary(),
         "measured_peaks": {k: pk.get(k) for k in ("hbm_gbs", "bf16_tflops")},
     }

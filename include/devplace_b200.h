@@ -37,6 +37,7 @@ extern "C" {
 #define DP_OK 0
 #define DP_EINVAL 1
 #define DP_ECUDA 2
+#define DP_ECOMM 3
 
 typedef struct dp_graph dp_graph;
 typedef struct dp_policy dp_policy;
@@ -223,14 +224,19 @@ int dp_argmin_feasible(int32_t K, const double *makespan, const uint8_t *feasibl
 
 /* Rewards, best-so-far, success-only filter, baseline and advantages for one
  * update (pkg/trainer.py:66-72, 83-84, 138-154, 281-304), on device:
- *   makespan[K], feasible[K], choice[K*T]: all K samples of the update
+ *   makespan[K], feasible[K]: all K samples of the update
+ *   choice: placement rows by rank; the best sample k's row is
+ *           choice[(k / choice_div) * T ..] — choice_div = 1: all K rows;
+ *           choice_div = K_local: one candidate row per rank (the K-sharded
+ *           exchange gathers only each rank's local best, dp_exchange_pack)
  *   adv[K_local] (out): (R_k - B) for used samples k_offset.. else 0
  *   best_choice[T] (out): updated when the best reward improves
  *   log_rows[log_cap*8] (out): row `update` = (update, controller, version,
  *   mean_R, baseline, best_R, n_feasible, n_used); version is filled by
  *   dp_adam_apply. */
 int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespan, const uint8_t *feasible,
-                          const uint8_t *choice, double failing, double decay, int64_t success_only_after,
+                          const uint8_t *choice, int32_t choice_div, double failing, double decay,
+                          int64_t success_only_after,
                           int64_t k_offset, int32_t K_local, dp_train_state *state, double *adv,
                           uint8_t *best_choice, double *log_rows, int64_t log_cap, int32_t controller_id,
                           void *stream);
@@ -240,9 +246,44 @@ int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespan, const ui
  * factors[update][k][0..n_factors)) in numpy's pairwise order, update =
  * state->update.  factors = exp(sigma * default_rng(seed_k).standard_normal(
  * steps))[1:] per sample, seeds from the controller's noise stream (host).
+ * K-sharded: makespan/feasible hold samples k_offset..k_offset+K-1 of K_total
+ * (factor rows [update][k_offset + k]).
  * Sets state->error = 2 if update >= n_updates. */
-int dp_apply_measurement_noise(int32_t K, double *makespan, const uint8_t *feasible, const double *factors,
-                               int64_t n_updates, int32_t n_factors, dp_train_state *state, void *stream);
+int dp_apply_measurement_noise(int32_t K, int64_t k_offset, int32_t K_total, double *makespan,
+                               const uint8_t *feasible, const double *factors, int64_t n_updates,
+                               int32_t n_factors, dp_train_state *state, void *stream);
+
+/* K-sharded exchange buffers.  A rank's record is
+ * dp_exchange_record_bytes(K_local, T) bytes: makespan f64[K_local] |
+ * feasible u8[K_local] | its best candidate's placement row u8[T] (by rank;
+ * the first feasible sample with the smallest reward sqrt(makespan), the rule
+ * of pkg/trainer.py:284-287 restricted to the shard) — padded to 16 bytes.
+ * pack: local scores + choice[K_local*T] -> record.  unpack: the all-gathered
+ * records [nranks] -> makespan[K], feasible[K], rows[nranks*T] (the epilogue's
+ * choice with choice_div = K_local). */
+int64_t dp_exchange_record_bytes(int32_t K_local, int32_t T);
+int dp_exchange_pack(int32_t K_local, int32_t T, const double *makespan, const uint8_t *feasible,
+                     const uint8_t *choice, uint8_t *record, void *stream);
+int dp_exchange_unpack(int32_t nranks, int32_t K_local, int32_t T, const uint8_t *records, double *makespan,
+                       uint8_t *feasible, uint8_t *rows, void *stream);
+
+/* NCCL (dlopen'ed libnccl.so.2) for the K-sharded step; DP_ECOMM on failure.
+ * One process per GPU: dp_comm_unique_id on rank 0, broadcast the 128 bytes,
+ * dp_comm_init_rank on every rank (current CUDA device).  One process for all
+ * GPUs: dp_comm_init_all (one communicator per device).  With several
+ * communicators in one thread, wrap the per-device calls in
+ * dp_comm_group_start/end.  All collectives enqueue on `stream` and are CUDA
+ * graph capturable. */
+typedef struct dp_comm dp_comm;
+int dp_comm_version(int32_t *version);
+int dp_comm_unique_id(uint8_t *id_out /* [128] */);
+int dp_comm_init_rank(int32_t nranks, const uint8_t *id /* [128] */, int32_t rank, dp_comm **out);
+int dp_comm_init_all(int32_t ndev, const int32_t *devices, dp_comm **out /* [ndev] */);
+void dp_comm_destroy(dp_comm *c);
+int dp_comm_group_start(void);
+int dp_comm_group_end(void);
+int dp_comm_all_gather(dp_comm *c, const void *send, void *recv, int64_t bytes_per_rank, void *stream);
+int dp_comm_all_reduce_f64(dp_comm *c, double *buf, int64_t count, int32_t op_min, void *stream);
 
 /* ParameterStore.apply (pkg/trainer.py:113-131): grad is the advantage-weighted
  * SUM from dp_policy_backward; it is divided by n_used here.  Skips the step
@@ -252,7 +293,8 @@ int dp_apply_measurement_noise(int32_t K, double *makespan, const uint8_t *feasi
  * state->update.  flag: device int32 scratch, zero-initialised.
  * store_state: the shared ParameterStore's counters (adam_t, version,
  * rejected) when several controllers share one store (pkg/trainer.py:365-378);
- * NULL = state (single controller). */
+ * NULL = state (single controller).  A step beyond t_cap (the bias-correction
+ * table's length) sets state->error = 3 and leaves everything unchanged. */
 int dp_adam_apply(int64_t P, double *params, double *m, double *v, const double *grad, const double *bias_corr,
                   int64_t t_cap, double lr, double b1, double b2, double eps, dp_train_state *state,
                   dp_train_state *store_state, int32_t *flag, double *log_rows, int64_t log_cap, void *stream);

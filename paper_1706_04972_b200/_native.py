@@ -44,9 +44,21 @@ SIGNATURES = {
     "dp_policy_backward": (I32, [P, P, I32, P, P, P]),
     "dp_policy_backward_rows": (I32, [P, P, I32, P]),
     "dp_policy_backward_grads": (I32, [P, P, I32, P, P, P]),
-    "dp_reinforce_epilogue": (I32, [I32, I32, P, P, P, F64, F64, I64, I64, I32, P, P, P, P, I64, I32, P]),
+    "dp_reinforce_epilogue": (I32, [I32, I32, P, P, P, I32, F64, F64, I64, I64, I32, P, P, P, P, I64, I32, P]),
     "dp_adam_apply": (I32, [I64, P, P, P, P, P, I64, F64, F64, F64, F64, P, P, P, P, I64, P]),
-    "dp_apply_measurement_noise": (I32, [I32, P, P, P, I64, I32, P, P]),
+    "dp_apply_measurement_noise": (I32, [I32, I64, I32, P, P, P, I64, I32, P, P]),
+    "dp_exchange_record_bytes": (I64, [I32, I32]),
+    "dp_exchange_pack": (I32, [I32, I32, P, P, P, P, P]),
+    "dp_exchange_unpack": (I32, [I32, I32, I32, P, P, P, P, P]),
+    "dp_comm_version": (I32, [P]),
+    "dp_comm_unique_id": (I32, [P]),
+    "dp_comm_init_rank": (I32, [I32, P, I32, P]),
+    "dp_comm_init_all": (I32, [I32, P, P]),
+    "dp_comm_destroy": (None, [P]),
+    "dp_comm_group_start": (I32, []),
+    "dp_comm_group_end": (I32, []),
+    "dp_comm_all_gather": (I32, [P, P, P, I64, P]),
+    "dp_comm_all_reduce_f64": (I32, [P, P, I64, I32, P]),
     "dp_enumerate_placements": (I32, [I32, I32, ctypes.c_uint64, I32, P, P]),
     "dp_argmin_feasible": (I32, [I32, P, P, I64, P, P, P]),
 }

@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) sim_warp_kernel(
                         const int p = (i - 1) >> 1;
                         const int pr = heap[p];
                         if (!key_less(t, r, maxarr[pr], pr)) break;
+                        __syncwarp();  // every lane has read heap[p] before lane 0 moves entries
                         if (lane == 0) heap[i] = (uint16_t)pr;
                         i = p;
                     }
@@ -683,6 +684,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) sim_warp_kernel(
                         }
                     }
                     if (!key_less(ct, cr, xt, last)) break;
+                    __syncwarp();  // reads of heap[c], heap[c+1] precede lane 0's write
                     if (lane == 0) heap[i] = (uint16_t)cr;
                     i = c;
                 }
@@ -696,6 +698,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) sim_warp_kernel(
             while (pos > qhd) {
                 const int pr = devq[pos - 1];
                 if (!key_less(ht, hr, maxarr[pr], pr)) break;
+                __syncwarp();  // every lane has read devq[pos - 1] before lane 0 shifts it
                 if (lane == 0) devq[pos] = (uint16_t)pr;
                 pos--;
             }

@@ -79,7 +79,7 @@ __device__ double np_pairwise(const double *a, int n) {
 // then thread 0 runs the order-dependent scalar logic over shared memory
 __global__ void epilogue_kernel(int K, int T, const double *__restrict__ makespan,
                                 const uint8_t *__restrict__ feasible, const uint8_t *__restrict__ choice,
-                                double failing, double decay, long long success_only_after, long long k_offset,
+                                int choice_div, double failing, double decay, long long success_only_after, long long k_offset,
                                 int K_local, dp_train_state *st, double *__restrict__ adv,
                                 uint8_t *__restrict__ best_choice, double *__restrict__ log_rows, long long log_cap,
                                 int controller_id) {
@@ -151,16 +151,16 @@ __global__ void epilogue_kernel(int K, int T, const double *__restrict__ makespa
     }
     const int bk = s_best_k;
     if (bk >= 0)
-        for (int t = tid; t < T; t += blockDim.x) best_choice[t] = choice[(size_t)bk * T + t];
+        for (int t = tid; t < T; t += blockDim.x) best_choice[t] = choice[(size_t)(bk / choice_div) * T + t];
 }
 
 // measure() with lognormal noise (pkg/simulator.py:218-223): a feasible
 // sample's measurement is np.mean(base * factors[1:]) — the factors row of
 // (update, k) comes from the host (the reference's own numpy streams,
 // pkg/trainer.py:277), the product and numpy's pairwise mean run here.
-__global__ void noise_kernel(int K, double *__restrict__ makespan, const uint8_t *__restrict__ feasible,
-                             const double *__restrict__ factors, long long n_updates, int n_factors,
-                             dp_train_state *st) {
+__global__ void noise_kernel(int K, long long k_offset, int K_total, double *__restrict__ makespan,
+                             const uint8_t *__restrict__ feasible, const double *__restrict__ factors,
+                             long long n_updates, int n_factors, dp_train_state *st) {
     const long long u = st->update;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= K) return;
@@ -170,7 +170,7 @@ __global__ void noise_kernel(int K, double *__restrict__ makespan, const uint8_t
     }
     if (!feasible[k]) return;
     const double base = makespan[k];
-    const double *f = factors + ((size_t)u * K + k) * n_factors;
+    const double *f = factors + ((size_t)u * K_total + k_offset + k) * n_factors;
     double prod[64];
     for (int s = 0; s < n_factors; s++) prod[s] = base * f[s];
     makespan[k] = np_pairwise(prod, n_factors) / (double)n_factors;
@@ -193,7 +193,7 @@ __global__ void adam_kernel(long long P, double *__restrict__ p, double *__restr
     const long long nu = st->n_used;
     if (nu <= 0 || *flag) return;
     const long long t = store->adam_t + 1;
-    if (t > t_cap) return;
+    if (t > t_cap) return;  // step_finalize flags it (error 3) and skips the bump
     const double bc1 = bias_corr[2 * (t - 1)], bc2 = bias_corr[2 * (t - 1) + 1];
     const double c1 = 1.0 - b1, c2 = 1.0 - b2;
     const double n = (double)nu;
@@ -210,10 +210,12 @@ __global__ void adam_kernel(long long P, double *__restrict__ p, double *__restr
 }
 
 __global__ void step_finalize_kernel(dp_train_state *st, dp_train_state *store, int *flag, double *log_rows,
-                                     long long log_cap) {
+                                     long long log_cap, long long t_cap) {
     if (threadIdx.x != 0) return;
     if (st->n_used > 0) {
-        if (*flag) {
+        if (!*flag && store->adam_t + 1 > t_cap) {
+            st->error = 3;  // bias-correction table exhausted: no silent frozen update
+        } else if (*flag) {
             store->rejected += 1;
         } else {
             store->adam_t += 1;
@@ -225,13 +227,99 @@ __global__ void step_finalize_kernel(dp_train_state *st, dp_train_state *store, 
     st->update += 1;
 }
 
+// K-sharded exchange record (include/devplace_b200.h dp_exchange_*): one CTA
+// per rank record.  pack: warp-parallel first-minimum of the feasible rewards
+// (sqrt, the epilogue's own R), then the record's bytes.
+__host__ __device__ inline long long exch_fe_off(int K_local) { return 8LL * K_local; }
+__host__ __device__ inline long long exch_row_off(int K_local) { return 8LL * K_local + K_local; }
+__host__ __device__ inline long long exch_bytes(int K_local, int T) {
+    return (exch_row_off(K_local) + T + 15) / 16 * 16;
+}
+
+__global__ void exchange_pack_kernel(int K_local, int T, const double *__restrict__ makespan,
+                                     const uint8_t *__restrict__ feasible, const uint8_t *__restrict__ choice,
+                                     uint8_t *__restrict__ rec) {
+    __shared__ double sr[32];
+    __shared__ int sk[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    double best = INFINITY;
+    int bk = 0x7fffffff;
+    for (int k = tid; k < K_local; k += blockDim.x) {
+        const double m = makespan[k];
+        reinterpret_cast<double *>(rec)[k] = m;
+        const uint8_t ok = feasible[k];
+        rec[exch_fe_off(K_local) + k] = ok;
+        const double r = sqrt(m);
+        if (ok && (r < best || (r == best && k < bk))) {
+            best = r;
+            bk = k;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ok2 = __shfl_xor_sync(0xffffffffu, bk, o);
+        if (ob < best || (ob == best && ok2 < bk)) {
+            best = ob;
+            bk = ok2;
+        }
+    }
+    if (lane == 0) {
+        sr[warp] = best;
+        sk[warp] = bk;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < nw; w++)
+            if (sr[w] < sr[0] || (sr[w] == sr[0] && sk[w] < sk[0])) {
+                sr[0] = sr[w];
+                sk[0] = sk[w];
+            }
+    }
+    __syncthreads();
+    const int kb = sk[0] < K_local ? sk[0] : 0;  // no feasible sample: any row (never selected)
+    for (int t = tid; t < T; t += blockDim.x) rec[exch_row_off(K_local) + t] = choice[(size_t)kb * T + t];
+}
+
+__global__ void exchange_unpack_kernel(int K_local, int T, const uint8_t *__restrict__ recs,
+                                       double *__restrict__ makespan, uint8_t *__restrict__ feasible,
+                                       uint8_t *__restrict__ rows) {
+    const int r = blockIdx.x;
+    const uint8_t *rec = recs + (size_t)r * exch_bytes(K_local, T);
+    for (int k = threadIdx.x; k < K_local; k += blockDim.x) {
+        makespan[(size_t)r * K_local + k] = reinterpret_cast<const double *>(rec)[k];
+        feasible[(size_t)r * K_local + k] = rec[exch_fe_off(K_local) + k];
+    }
+    for (int t = threadIdx.x; t < T; t += blockDim.x) rows[(size_t)r * T + t] = rec[exch_row_off(K_local) + t];
+}
+
 }  // namespace
 }  // namespace dp
 
 using namespace dp;
 
+extern "C" int64_t dp_exchange_record_bytes(int32_t K_local, int32_t T) { return exch_bytes(K_local, T); }
+
+extern "C" int dp_exchange_pack(int32_t K_local, int32_t T, const double *makespan, const uint8_t *feasible,
+                                const uint8_t *choice, uint8_t *record, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(K_local >= 1 && T >= 1 && makespan && feasible && choice && record, "dp_exchange_pack: bad argument");
+    exchange_pack_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(K_local, T, makespan, feasible, choice, record);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
+extern "C" int dp_exchange_unpack(int32_t nranks, int32_t K_local, int32_t T, const uint8_t *records,
+                                  double *makespan, uint8_t *feasible, uint8_t *rows, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(nranks >= 1 && K_local >= 1 && T >= 1 && records && makespan && feasible && rows,
+               "dp_exchange_unpack: bad argument");
+    exchange_unpack_kernel<<<nranks, 256, 0, (cudaStream_t)stream>>>(K_local, T, records, makespan, feasible, rows);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
+
 extern "C" int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespan, const uint8_t *feasible,
-                                     const uint8_t *choice, double failing, double decay,
+                                     const uint8_t *choice, int32_t choice_div, double failing, double decay,
                                      int64_t success_only_after, int64_t k_offset, int32_t K_local,
                                      dp_train_state *state, double *adv, uint8_t *best_choice, double *log_rows,
                                      int64_t log_cap, int32_t controller_id, void *stream) {
@@ -240,23 +328,26 @@ extern "C" int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespa
     DP_REQUIRE(K_local >= 0 && k_offset >= 0 && k_offset + K_local <= K, "dp_reinforce_epilogue: bad shard");
     DP_REQUIRE(makespan && feasible && choice && state && best_choice && log_rows,
                "dp_reinforce_epilogue: NULL argument");
+    DP_REQUIRE(choice_div >= 1, "dp_reinforce_epilogue: choice_div must be >= 1");
     const size_t smem = sizeof(double) * 2 * (size_t)K + (size_t)K;
     DP_CUDA_TRY(allow_big_smem((const void *)epilogue_kernel, smem));
-    epilogue_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(K, T, makespan, feasible, choice, failing, decay,
+    epilogue_kernel<<<1, 256, smem, (cudaStream_t)stream>>>(K, T, makespan, feasible, choice, choice_div, failing,
+                                                            decay,
                                                             success_only_after, k_offset, K_local, state, adv,
                                                             best_choice, log_rows, log_cap, controller_id);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
 
-extern "C" int dp_apply_measurement_noise(int32_t K, double *makespan, const uint8_t *feasible,
-                                          const double *factors, int64_t n_updates, int32_t n_factors,
-                                          dp_train_state *state, void *stream) {
+extern "C" int dp_apply_measurement_noise(int32_t K, int64_t k_offset, int32_t K_total, double *makespan,
+                                          const uint8_t *feasible, const double *factors, int64_t n_updates,
+                                          int32_t n_factors, dp_train_state *state, void *stream) {
     DP_ENTRY();
     DP_REQUIRE(K >= 1 && makespan && feasible && factors && state, "dp_apply_measurement_noise: NULL argument");
+    DP_REQUIRE(k_offset >= 0 && k_offset + K <= K_total, "dp_apply_measurement_noise: bad shard");
     DP_REQUIRE(n_factors >= 1 && n_factors <= 64, "dp_apply_measurement_noise: need 1 <= steps-1 <= 64");
-    noise_kernel<<<ceil_div(K, 128), 128, 0, (cudaStream_t)stream>>>(K, makespan, feasible, factors, n_updates,
-                                                                       n_factors, state);
+    noise_kernel<<<ceil_div(K, 128), 128, 0, (cudaStream_t)stream>>>(K, k_offset, K_total, makespan, feasible,
+                                                                       factors, n_updates, n_factors, state);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }
@@ -276,7 +367,7 @@ extern "C" int dp_adam_apply(int64_t P, double *params, double *m, double *v, co
     adam_kernel<<<blocks, 256, 0, st>>>(P, params, m, v, grad, bias_corr, t_cap, lr, b1, b2, eps, state, store_state,
                                         flag);
     DP_LAUNCH_CHECK();
-    step_finalize_kernel<<<1, 32, 0, st>>>(state, store_state, flag, log_rows, log_cap);
+    step_finalize_kernel<<<1, 32, 0, st>>>(state, store_state, flag, log_rows, log_cap, t_cap);
     DP_LAUNCH_CHECK();
     return DP_OK;
 }

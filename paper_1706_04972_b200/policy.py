@@ -209,6 +209,11 @@ class DevicePolicy:
         self._destroy = nat.lib().dp_policy_destroy
         self.P = int(nat.lib().dp_policy_num_params(self.handle))
         self.order = torch.as_tensor(np.asarray(feats.order, np.int64), device=self.device)
+        # the engine's buffers (encoder state, forward cache) are mutable: the
+        # drop-in functions hold this lock across encode -> decode -> backward,
+        # so controller threads sharing a GroupFeatures object (pkg/trainer.py:
+        # 365-378) never interleave on one engine
+        self.lock = threading.RLock()
 
     def __del__(self):
         if getattr(self, "handle", None):
@@ -359,10 +364,11 @@ def embed_groups(params: PolicyParams, feats: GroupFeatures) -> np.ndarray:
     from . import _native as nat  # noqa: F401
 
     eng = engine_for(params, feats, 1)
-    pdev = _params_dev(params, eng)
-    eng.encode(pdev)
-    torch.cuda.current_stream().synchronize()
-    return _read_encoder_inputs(eng)
+    with eng.lock:
+        pdev = _params_dev(params, eng)
+        eng.encode(pdev)
+        torch.cuda.current_stream().synchronize()
+        return _read_encoder_inputs(eng)
 
 
 def _read_encoder_inputs(eng) -> np.ndarray:
@@ -382,18 +388,22 @@ def _read_encoder_inputs(eng) -> np.ndarray:
 def forward_sample(params: PolicyParams, feats: GroupFeatures, rng) -> SampledPlacement:
     """Sample one placement (``pkg/policy.py:317-326``); consumes exactly T draws of ``rng``."""
     eng = engine_for(params, feats, 1)
-    pdev = _params_dev(params, eng)
-    eng.encode(pdev)
-    choice, logp = eng.decode(pdev, 1, pcg=generator_state(rng))
-    rng.bit_generator.advance(len(feats))
-    placement = eng.by_gid(choice)[0].cpu().numpy().astype(int).tolist()
-    return SampledPlacement(placement, float(logp[0].item()), _DeviceCache(id(eng), placement))
+    with eng.lock:
+        pdev = _params_dev(params, eng)
+        eng.encode(pdev)
+        choice, logp = eng.decode(pdev, 1, pcg=generator_state(rng))
+        rng.bit_generator.advance(len(feats))
+        placement = eng.by_gid(choice)[0].cpu().numpy().astype(int).tolist()
+        return SampledPlacement(placement, float(logp[0].item()), _DeviceCache(id(eng), placement))
 
 
 def _teacher_forced(params, feats, placements, want_probs=False):
+    """Teacher-forced pass; the caller holds ``eng.lock`` (re-entrant) for as
+    long as it uses the engine's forward cache."""
     import torch
 
     eng = engine_for(params, feats, len(placements))
+    eng.lock.acquire()  # released by the caller (_locked_tf)
     pdev = _params_dev(params, eng)
     eng.encode(pdev)
     K = len(placements)
@@ -403,18 +413,33 @@ def _teacher_forced(params, feats, placements, want_probs=False):
     return eng, pdev, logp, probs
 
 
+class _locked_tf:
+    """``with _locked_tf(...) as (eng, pdev, logp, probs)``: teacher-forced pass
+    with the engine lock held until the block ends."""
+
+    def __init__(self, params, feats, placements, want_probs=False):
+        self.args = (params, feats, placements, want_probs)
+
+    def __enter__(self):
+        self.out = _teacher_forced(*self.args)
+        return self.out
+
+    def __exit__(self, *exc):
+        self.out[0].lock.release()
+
+
 def log_prob_of(params: PolicyParams, feats: GroupFeatures, placement) -> float:
     """Teacher-forced log-probability (``pkg/policy.py:329-333``)."""
     _check_placement_arg(params, feats, placement)
-    _, _, logp, _ = _teacher_forced(params, feats, [placement])
-    return float(logp[0].item())
+    with _locked_tf(params, feats, [placement]) as (_, _, logp, _):
+        return float(logp[0].item())
 
 
 def step_distributions(params: PolicyParams, feats: GroupFeatures, placement) -> np.ndarray:
     """Per-step device distributions (T, D) along a teacher-forced pass (``pkg/policy.py:336-340``)."""
     _check_placement_arg(params, feats, placement)
-    _, _, _, probs = _teacher_forced(params, feats, [placement], want_probs=True)
-    return probs[0].cpu().numpy()
+    with _locked_tf(params, feats, [placement], want_probs=True) as (_, _, _, probs):
+        return probs[0].cpu().numpy()
 
 
 def grad_log_prob(params: PolicyParams, feats: GroupFeatures, placement, cache=None) -> np.ndarray:
@@ -422,9 +447,9 @@ def grad_log_prob(params: PolicyParams, feats: GroupFeatures, placement, cache=N
     import torch
 
     _check_placement_arg(params, feats, placement)
-    eng, pdev, _, _ = _teacher_forced(params, feats, [placement])
-    adv = torch.ones(1, dtype=torch.float64, device=eng.device)
-    return eng.backward(pdev, 1, adv).cpu().numpy()
+    with _locked_tf(params, feats, [placement]) as (eng, pdev, _, _):
+        adv = torch.ones(1, dtype=torch.float64, device=eng.device)
+        return eng.backward(pdev, 1, adv).cpu().numpy()
 
 
 def weighted_grad(params: PolicyParams, feats: GroupFeatures, placements, weights):
@@ -433,9 +458,9 @@ def weighted_grad(params: PolicyParams, feats: GroupFeatures, placements, weight
 
     for pl in placements:
         _check_placement_arg(params, feats, pl)
-    eng, pdev, _, _ = _teacher_forced(params, feats, placements)
-    adv = torch.as_tensor(np.asarray(weights, np.float64), device=eng.device)
-    return eng.backward(pdev, len(placements), adv)
+    with _locked_tf(params, feats, placements) as (eng, pdev, _, _):
+        adv = torch.as_tensor(np.asarray(weights, np.float64), device=eng.device)
+        return eng.backward(pdev, len(placements), adv)
 
 
 def sample_batch(params: PolicyParams, feats: GroupFeatures, rng, K: int, return_margin: bool = False):
@@ -445,12 +470,13 @@ def sample_batch(params: PolicyParams, feats: GroupFeatures, rng, K: int, return
     import torch
 
     eng = engine_for(params, feats, K)
-    pdev = _params_dev(params, eng)
-    eng.encode(pdev)
-    margin = torch.empty(K, dtype=torch.float64, device=eng.device) if return_margin else None
-    choice, logp = eng.decode(pdev, K, pcg=generator_state(rng), margin=margin)
-    rng.bit_generator.advance(K * len(feats))
-    out = (eng.by_gid(choice).cpu().numpy(), logp.cpu().numpy())
+    with eng.lock:
+        pdev = _params_dev(params, eng)
+        eng.encode(pdev)
+        margin = torch.empty(K, dtype=torch.float64, device=eng.device) if return_margin else None
+        choice, logp = eng.decode(pdev, K, pcg=generator_state(rng), margin=margin)
+        rng.bit_generator.advance(K * len(feats))
+        out = (eng.by_gid(choice).cpu().numpy(), logp.cpu().numpy())
     return out + (margin.cpu().numpy(),) if return_margin else out
 
 

@@ -18,6 +18,7 @@ so the whole update can be captured once in a CUDA graph and replayed.
 
 from __future__ import annotations
 
+import copy
 import io
 import math
 import time
@@ -28,6 +29,21 @@ import numpy as np
 from . import policy as policy_mod
 from .policy import EmbeddingSpec, GroupFeatures, PolicyParams
 from .simulator import INFEASIBLE, SimReport, device_graph, simulate
+
+
+def make_exchange(group):
+    """The K-sharded exchange for a torch.distributed group: the library's own
+    NCCL communicator when the group runs NCCL (one per process, captured in the
+    update's CUDA graph), else torch.distributed host-staged (gloo)."""
+    import os
+
+    import torch.distributed as dist
+
+    from .parallel import NcclExchange, TorchExchange
+
+    if dist.get_backend(group) == "nccl" and os.environ.get("DP_EXCHANGE", "nccl") == "nccl":
+        return NcclExchange.from_group(group)
+    return TorchExchange(group)
 
 
 # ----------------------------------------------------------------------------- reference types
@@ -118,6 +134,7 @@ class ParameterStore:
         self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._bias_cap = 0
         self.bias = None
+        self._old_bias = []
         self._ensure_bias(max_steps)
         self._lock = threading.Lock()
         self._scratch_log = torch.zeros(8, dtype=torch.float64, device=self.device)
@@ -131,6 +148,10 @@ class ParameterStore:
         for t in range(1, steps + 1):  # Python float pow, as ParameterStore.apply computes it
             tab[2 * (t - 1)] = 1.0 - self.beta1 ** t
             tab[2 * (t - 1) + 1] = 1.0 - self.beta2 ** t
+        if self.bias is not None:
+            # a captured CUDA graph may still hold the old table's address (its
+            # launches carry their own t_cap and flag error 3 beyond it): keep it alive
+            self._old_bias.append(self.bias)
         self.bias = torch.as_tensor(tab, device=self.device)
         self._bias_cap = steps
 
@@ -213,6 +234,10 @@ class TrainerConfig:
     shape_slots: int = 8
     adjacency_slots: int = 64
     init_scale: float = 0.1
+    # new (not in the reference): GPUs the K samples are sharded over in this
+    # one process.  None = every visible GPU (the largest count dividing k);
+    # a tuple of CUDA device indices = exactly those (repeats share a GPU).
+    devices: tuple | None = None
 
     def __post_init__(self):
         if self.k < 1:
@@ -301,10 +326,15 @@ def policy_template(gg, topo, config: TrainerConfig) -> PolicyParams:
 class DeviceController:
     """One controller's REINFORCE loop on one GPU (or one rank's shard of K).
 
-    ``world=(rank, size, group)`` shards the K samples (rank r owns samples
-    [r*K/size, (r+1)*K/size)); per update the ranks all-gather the scores and
-    placements (so every rank replays the reference's sequential best /
-    baseline logic bit-identically) and all-reduce the gradient (NCCL)."""
+    ``world=(rank, size, comm)`` shards the K samples (rank r owns samples
+    [r*K/size, (r+1)*K/size)); per update the ranks all-gather one small
+    record each (scores + the shard's best candidate row, parallel.py) so every
+    rank replays the reference's sequential best / baseline logic
+    bit-identically, and all-reduce the gradient.  ``comm``: a
+    torch.distributed group (NCCL -> the library's own NCCL communicator,
+    captured in the update's CUDA graph; gloo -> host-staged), an exchange
+    object (parallel.NcclExchange / TorchExchange), or ``"external"`` (a
+    multi-device runner issues the collectives between the step's phases)."""
 
     def __init__(self, task: _TrainTask, store: ParameterStore, seed_seq, controller_id: int = 0,
                  world=None, log_cap: int | None = None, shared: bool = False):
@@ -317,13 +347,21 @@ class DeviceController:
         cfg = task.config
         self.task, self.store, self.cid = task, store, controller_id
         self.device = store.device
-        from .parallel import Exchange, shard
+        from .parallel import shard
 
-        self.rank, self.size, self.group = world if world is not None else (0, 1, None)
+        self.rank, self.size, comm = world if world is not None else (0, 1, None)
         K = cfg.k
         self.K = K
         self.k_offset, self.K_local = shard(K, self.rank, self.size)
-        self.xchg = Exchange(self.group) if self.size > 1 else None
+        self.xchg = None
+        if comm == "external":
+            self.exchanged = True
+        else:
+            if hasattr(comm, "all_gather"):
+                self.xchg = comm
+            elif comm is not None and self.size > 1:
+                self.xchg = make_exchange(comm)
+            self.exchanged = self.xchg is not None
         tmpl = task.template
         self.eng = policy_mod.DevicePolicy(task.feats, tmpl.spec, tmpl.num_devices, tmpl.hidden, tmpl.dev_dim,
                                            k_max=self.K_local)
@@ -335,13 +373,12 @@ class DeviceController:
         self.log_cap = log_cap if log_cap is not None else cfg.total_updates
         store._ensure_bias(cfg.total_updates * max(1, cfg.controllers) + 1)
         self.shared = shared
-        if shared:
-            self.state = _state_tensor(store.device)
-            self.params_src = torch.empty_like(store.params)
-        else:
-            self.state = store.state
-            self.state.zero_()
-            self.params_src = store.params
+        # every controller keeps its own state (baseline, best, update counter,
+        # n_used, error); the store's counters (adam_t, version, rejected) stay in
+        # store.state, so a store that already applied updates continues its
+        # version numbering and Adam step as the reference's does
+        self.state = _state_tensor(store.device)
+        self.params_src = torch.empty_like(store.params) if shared else store.params
         st = self.state
         st[0] = task.reward_spec.failing_signal
         st[2] = math.inf
@@ -359,10 +396,15 @@ class DeviceController:
         self.grad = torch.zeros(store.params.numel(), dtype=torch.float64, device=dev)
         self.best_choice = torch.zeros(T, dtype=torch.uint8, device=dev)
         self.log = torch.full((max(1, self.log_cap) * 8,), math.nan, dtype=torch.float64, device=dev)
-        if self.size > 1:
+        if self.exchanged:
+            from . import _native as nat
+
+            rb = int(nat.lib().dp_exchange_record_bytes(self.K_local, T))
+            self.rec = torch.zeros(rb, dtype=torch.uint8, device=dev)
+            self.recs = torch.zeros(self.size * rb, dtype=torch.uint8, device=dev)
             self.mk_all = torch.zeros(K, dtype=torch.float64, device=dev)
             self.fe_all = torch.zeros(K, dtype=torch.uint8, device=dev)
-            self.ch_all = torch.zeros(K, T, dtype=torch.uint8, device=dev)
+            self.rows_all = torch.zeros(self.size, T, dtype=torch.uint8, device=dev)
         self.measure_ok = cfg.measure_steps >= 2
         # measurement noise (f2): the factor rows of every update, drawn up front
         # from the controller's noise stream exactly as the reference does
@@ -380,12 +422,28 @@ class DeviceController:
         CUDA event at each phase boundary (bench.py phase timing).
         ``apply=False`` stops before the Adam step (the shared-store runner
         orders the controllers' applies itself)."""
+        self.phase_sample(stream, marks)
+        if self.xchg is not None:
+            (marks or (lambda _n: None))("exchange")
+            self.xchg.all_gather(self.recs, self.rec, stream=stream)
+        self.phase_score(stream, marks)
+        if self.xchg is not None:
+            (marks or (lambda _n: None))("allreduce")
+            self.xchg.all_reduce_sum(self.grad, stream=stream)
+        if apply:
+            (marks or (lambda _n: None))("adam")
+            self.apply(stream)
+        (marks or (lambda _n: None))("end")
+
+    def phase_sample(self, stream=None, marks=None):
+        """Encode, sample this shard, score it (the advantage-independent half of
+        the backward overlaps on a side stream); sharded: pack the exchange record."""
         import torch
 
         from . import _native as nat
 
         mark = marks or (lambda _name: None)
-        cfg, st = self.task.config, self.store
+        cfg = self.task.config
         p = self.params_src
         state = self.state
         main = stream if stream is not None else torch.cuda.current_stream()
@@ -404,38 +462,49 @@ class DeviceController:
         self.side.wait_stream(main)
         self.eng.backward_rows(p, self.K_local, stream=self.side)
         self.sim_local = self.dg.simulate(self.choice, by_rank=True, stream=stream, out=self.sim_local)
-        mk, fe, ch = self.sim_local["makespan"], self.sim_local["feasible"], self.choice
+        mk, fe = self.sim_local["makespan"], self.sim_local["feasible"]
         if not self.measure_ok:
             fe.zero_()  # measure() raises for steps < 2 -> every worker reports INFEASIBLE
-        if self.size > 1:
-            mark("exchange")
-            self.xchg.all_gather(self.mk_all, mk)
-            self.xchg.all_gather(self.fe_all, fe)
-            self.xchg.all_gather(self.ch_all, ch)
-            mk, fe, ch = self.mk_all, self.fe_all, self.ch_all
         if self.noise is not None:
             nat.check(nat.lib().dp_apply_measurement_noise(
-                self.K, nat.ptr(mk), nat.ptr(fe), nat.ptr(self.noise), self.noise.shape[0], self.noise.shape[2],
-                nat.ptr(state), nat.stream_ptr(stream)), "dp_apply_measurement_noise")
+                self.K_local, self.k_offset, self.K, nat.ptr(mk), nat.ptr(fe), nat.ptr(self.noise),
+                self.noise.shape[0], self.noise.shape[2], nat.ptr(state), nat.stream_ptr(stream)),
+                "dp_apply_measurement_noise")
+        if self.exchanged:
+            nat.check(nat.lib().dp_exchange_pack(self.K_local, self.T, nat.ptr(mk), nat.ptr(fe),
+                                                 nat.ptr(self.choice), nat.ptr(self.rec), nat.stream_ptr(stream)),
+                      "dp_exchange_pack")
+
+    def phase_score(self, stream=None, marks=None):
+        """Rewards / best / baseline / advantages over all K (after the exchange),
+        then the advantage-weighted backward."""
+        import torch
+
+        from . import _native as nat
+
+        mark = marks or (lambda _name: None)
+        cfg = self.task.config
+        main = stream if stream is not None else torch.cuda.current_stream()
+        if self.exchanged:
+            nat.check(nat.lib().dp_exchange_unpack(self.size, self.K_local, self.T, nat.ptr(self.recs),
+                                                   nat.ptr(self.mk_all), nat.ptr(self.fe_all),
+                                                   nat.ptr(self.rows_all), nat.stream_ptr(stream)),
+                      "dp_exchange_unpack")
+            mk, fe, ch, div = self.mk_all, self.fe_all, self.rows_all, self.K_local
+        else:
+            mk, fe, ch, div = self.sim_local["makespan"], self.sim_local["feasible"], self.choice, 1
         mark("epilogue")
         rc = nat.lib().dp_reinforce_epilogue(
-            self.K, self.T, nat.ptr(mk), nat.ptr(fe), nat.ptr(ch), self.task.reward_spec.failing_signal,
-            cfg.baseline_decay, cfg.success_only_after, self.k_offset, self.K_local, nat.ptr(state),
+            self.K, self.T, nat.ptr(mk), nat.ptr(fe), nat.ptr(ch), div, self.task.reward_spec.failing_signal,
+            cfg.baseline_decay, cfg.success_only_after, self.k_offset, self.K_local, nat.ptr(self.state),
             nat.ptr(self.adv), nat.ptr(self.best_choice), nat.ptr(self.log), self.log_cap, self.cid,
             nat.stream_ptr(stream))
         nat.check(rc, "dp_reinforce_epilogue")
         mark("backward")
         # backward_grads waits on the rows pass itself (its attention sums start
         # as soon as the attention backward is done, beside the LSTM backward)
-        self.eng.backward_grads(p, self.K_local, self.adv, grad=self.grad, stream=stream)
+        self.eng.backward_grads(self.params_src, self.K_local, self.adv, grad=self.grad, stream=stream)
         main.wait_stream(self.side)
-        if self.size > 1:
-            mark("allreduce")
-            self.xchg.all_reduce_sum(self.grad)
-        if apply:
-            mark("adam")
-            self.apply(stream)
-        mark("end")
 
     def apply(self, stream=None):
         """This controller's Adam step on the (possibly shared) store."""
@@ -480,6 +549,8 @@ class DeviceController:
         st = _state_read(self.state)
         if st["error"] == 2:
             raise RuntimeError("measurement-noise table exhausted (more updates than total_updates)")
+        if st["error"] == 3:
+            raise RuntimeError("Adam bias-correction table exhausted (more updates than the store's max_steps)")
         if st["error"]:
             raise ValueError("measurement must be positive and finite (a feasible placement has makespan <= 0)")
         return st
@@ -496,10 +567,18 @@ class DeviceController:
     def sampling_certificate(self) -> dict:
         """Minimum sampling margin over every sample drawn so far and the number
         of samples with a draw closer than policy.SAMPLING_MARGIN_TOL to a cdf
-        boundary (those indices are not certified equal to the reference's)."""
-        return {"min_margin": float(self.margin_min.item()), "tol": policy_mod.SAMPLING_MARGIN_TOL,
-                "uncertified_samples": int(self.n_uncertified.item()),
-                "fastmath_max_ulp": policy_mod.FASTMATH_MAX_ULP}
+        boundary (those indices are not certified equal to the reference's);
+        over all ranks when sharded."""
+        mm = self.margin_min.clone()
+        nu = self.n_uncertified.to(dtype=mm.dtype)
+        if self.xchg is not None:
+            self.xchg.all_reduce_min(mm)
+            self.xchg.all_reduce_sum(nu)
+            import torch
+
+            torch.cuda.current_stream().synchronize()
+        return {"min_margin": float(mm.item()), "tol": policy_mod.SAMPLING_MARGIN_TOL,
+                "uncertified_samples": int(nu.item()), "fastmath_max_ulp": policy_mod.FASTMATH_MAX_ULP}
 
     def best(self):
         st = _state_read(self.state)
@@ -711,14 +790,15 @@ def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, 
                    world=None, ctl=None) -> _ControllerResult:
     """``pkg/trainer.py:256-309`` on the device (CUDA-graph replay after update 0).
 
-    ``world=(rank, size, group)`` runs this rank's K-shard (parallel.py); the
-    multi-rank step stays eager (collectives are enqueued asynchronously)."""
+    ``world=(rank, size, group)`` runs this rank's K-shard (parallel.py); with
+    NCCL the collectives are captured in the update's graph, with a
+    host-staged (gloo) exchange the step runs eagerly."""
     import torch
 
     cfg = task.config
     if ctl is None:
         ctl = DeviceController(task, store, seed_seq, controller_id, world=world)
-    use_graph = ctl.size == 1
+    use_graph = ctl.xchg is None or ctl.xchg.capturable
     walls = []
     if cfg.total_updates > 0:
         walls += ctl.run(1, use_graph=False, wall=True)
@@ -733,24 +813,198 @@ def run_controller(controller_id: int, store: ParameterStore, task: _TrainTask, 
     return res
 
 
+class MultiDeviceRunner:
+    """One process drives G GPUs (a plain ``train()`` call
+    uses every visible device).  Rank r (device ``devices[r]``) owns samples
+    [r*K/G, (r+1)*K/G) with its own replicated parameter store; one update is
+    the controllers' phases interleaved across devices with the two
+    collectives in between (NCCL, one communicator per device from
+    ``ncclCommInitAll``, each call group-wrapped; or device copies when every
+    rank shares one GPU — parallel.LocalGroup).  The whole round — every
+    device's kernels and both collectives — is captured once (one CUDA graph
+    per device) and replayed."""
+
+    def __init__(self, task: _TrainTask, config: TrainerConfig, devices, seed_seq):
+        import torch
+
+        from .parallel import LocalGroup, NcclExchange, NcclGroup
+
+        self.devices = [int(d) for d in devices]
+        G = len(self.devices)
+        distinct = sorted(set(self.devices))
+        if len(distinct) not in (1, G):
+            raise ValueError(f"devices {self.devices}: either all distinct or all the same GPU")
+        self.shared_gpu = len(distinct) == 1 and G > 1
+        self.task, self.config = task, config
+        self.streams, self.stores, self.ctls = [], [], []
+        seed0 = copy.deepcopy(seed_seq)
+        for r, d in enumerate(self.devices):
+            with torch.cuda.device(d):
+                s = torch.cuda.Stream(device=d) if (r == 0 or not self.shared_gpu) else self.streams[0]
+                self.streams.append(s)
+                st = ParameterStore(task.template.to_flat(), learning_rate=config.learning_rate,
+                                    beta1=config.adam_beta1, beta2=config.adam_beta2, epsilon=config.adam_epsilon,
+                                    device=torch.device("cuda", d), max_steps=config.total_updates + 1)
+                self.stores.append(st)
+                # every rank replays the same controller streams: spawn from a copy
+                # (SeedSequence.spawn advances its child counter)
+                self.ctls.append(DeviceController(task, st, copy.deepcopy(seed0), 0, world=(r, G, "external")))
+        if self.shared_gpu:
+            self.comm = LocalGroup(G)
+        else:
+            self.comm = NcclGroup(NcclExchange.init_all(self.devices), self.streams)
+        self._graphs = None
+        torch.cuda.synchronize(self.devices[0])
+
+    def _each(self, fn):
+        import torch
+
+        for c, d, s in zip(self.ctls, self.devices, self.streams):
+            with torch.cuda.device(d), torch.cuda.stream(s):
+                fn(c, s)
+
+    def step(self):
+        import torch
+
+        for d, s in zip(self.devices, self.streams):  # order after prior default-stream work
+            with torch.cuda.device(d):
+                s.wait_stream(torch.cuda.current_stream(d))
+        self._each(lambda c, s: c.phase_sample(s))
+        with torch.cuda.device(self.devices[0]), torch.cuda.stream(self.streams[0]):
+            self.comm.all_gather([(c.recs, c.rec) for c in self.ctls])
+        self._each(lambda c, s: c.phase_score(s))
+        with torch.cuda.device(self.devices[0]), torch.cuda.stream(self.streams[0]):
+            self.comm.all_reduce_sum([c.grad for c in self.ctls])
+        self._each(lambda c, s: c.apply(s))
+        for d, s in zip(self.devices, self.streams):
+            with torch.cuda.device(d):
+                torch.cuda.current_stream(d).wait_stream(s)
+
+    def capture(self):
+        import gc
+
+        import torch
+
+        gc.collect()
+        gc.disable()
+        devs = self.devices[:1] if self.shared_gpu else self.devices
+        graphs = [torch.cuda.CUDAGraph() for _ in devs]
+        try:
+            for g, d, s in zip(graphs, devs, self.streams):
+                with torch.cuda.device(d), torch.cuda.stream(s):
+                    g.capture_begin(capture_error_mode="relaxed")
+            self._each(lambda c, s: c.phase_sample(s))
+            with torch.cuda.device(self.devices[0]), torch.cuda.stream(self.streams[0]):
+                self.comm.all_gather([(c.recs, c.rec) for c in self.ctls])
+            self._each(lambda c, s: c.phase_score(s))
+            with torch.cuda.device(self.devices[0]), torch.cuda.stream(self.streams[0]):
+                self.comm.all_reduce_sum([c.grad for c in self.ctls])
+            self._each(lambda c, s: c.apply(s))
+            for g, d, s in zip(graphs, devs, self.streams):
+                with torch.cuda.device(d), torch.cuda.stream(s):
+                    g.capture_end()
+        finally:
+            gc.enable()
+        self._graphs = list(zip(graphs, devs, self.streams))
+
+    def replay(self):
+        import torch
+
+        for g, d, s in self._graphs:
+            with torch.cuda.device(d):
+                s.wait_stream(torch.cuda.current_stream(d))
+                with torch.cuda.stream(s):
+                    g.replay()
+                torch.cuda.current_stream(d).wait_stream(s)
+
+    def run(self, updates, use_graph=True):
+        import torch
+
+        walls = []
+        for _ in range(updates):
+            t0 = time.perf_counter()
+            if use_graph and self._graphs is not None:
+                self.replay()
+            else:
+                self.step()
+            for d in sorted(set(self.devices)):
+                torch.cuda.synchronize(d)
+            walls.append((time.perf_counter() - t0) * 1e3)
+            for c in self.ctls:
+                c.updates_done += 1
+        return walls
+
+    def train(self, updates):
+        walls = []
+        if updates > 0:
+            walls += self.run(1, use_graph=False)
+        if updates > 1:
+            self.capture()
+            walls += self.run(updates - 1, use_graph=True)
+        for c in self.ctls:
+            c.check_errors()
+        return walls
+
+    def result(self, walls) -> "TrainResult":
+        import torch
+
+        c0 = self.ctls[0]
+        with torch.cuda.device(self.devices[0]):
+            rows = sorted(c0.rows(walls), key=lambda r: (r.controller_id, r.update_index))
+            best_r, best_pl = c0.best()
+            final, _ = self.stores[0].snapshot()
+            certs = []
+            for c, d in zip(self.ctls, self.devices):
+                with torch.cuda.device(d):
+                    certs.append(c.sampling_certificate())
+            best_report = simulate(self.task.gg, self.task.topo, best_pl) if best_pl is not None else None
+        return TrainResult(best_placement=best_pl, best_report=best_report, log=rows, final_params=final,
+                           store_versions=self.stores[0].version, rejected_updates=self.stores[0].rejected,
+                           sampling=_merge_certs(certs))
+
+
+def _auto_devices(config: TrainerConfig):
+    """Devices a plain train() shards over: the configured tuple, or every
+    visible GPU (the largest count that divides k)."""
+    import torch
+
+    if config.devices is not None:
+        return tuple(int(d) for d in config.devices)
+    n = torch.cuda.device_count()
+    G = max(g for g in range(1, max(1, n) + 1) if config.k % g == 0)
+    return tuple(range(G)) if G > 1 else (torch.cuda.current_device(),)
+
+
 def train(graph, topo, config: TrainerConfig | None = None, *, group=None) -> TrainResult:
     """Train the policy; return the best feasible placement ever measured
     (``pkg/trainer.py:341-393``).
 
-    ``group``: optional torch.distributed process group; every rank calls
-    train() with the same arguments and owns K/size of the samples (one GPU
-    per rank, NCCL).  Every rank returns the same result."""
+    Without ``group`` the K samples are sharded over ``config.devices`` (by
+    default every visible GPU, the largest count dividing k) inside this one
+    process (MultiDeviceRunner; NCCL).  ``group``: optional torch.distributed
+    process group; every rank calls train() with the same arguments and owns
+    K/size of the samples (one GPU per rank).  Every rank
+    returns the same result.  ``controllers > 1`` (f1) runs on one GPU."""
     from .graph import coalesce_sole_consumers
 
     config = config or TrainerConfig()
     gg = graph if hasattr(graph, "groups") else coalesce_sole_consumers(graph)
     task = _make_task(gg, topo, config)
     C = config.controllers
+    root = np.random.SeedSequence(config.seed)
+    seqs = root.spawn(C)
+    devices = _auto_devices(config) if group is None and C == 1 else None
+    if devices is not None and len(devices) > 1:
+        # one process, every GPU: K sharded over the devices (MultiDeviceRunner)
+        runner = MultiDeviceRunner(task, config, devices, seqs[0])
+        return runner.result(runner.train(config.total_updates))
+    if devices is not None:
+        import torch
+
+        torch.cuda.set_device(devices[0])
     store = ParameterStore(task.template.to_flat(), learning_rate=config.learning_rate, beta1=config.adam_beta1,
                            beta2=config.adam_beta2, epsilon=config.adam_epsilon,
                            max_steps=config.total_updates * C + 1)
-    root = np.random.SeedSequence(config.seed)
-    seqs = root.spawn(C)
     if C > 1:
         # f1: C controllers over one device-resident store (ConcurrentRunner)
         if group is not None:

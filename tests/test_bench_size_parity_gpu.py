@@ -167,8 +167,8 @@ def test_four_per_cta_decoder_vs_oracle(name, K, picks):
         opl, olp, _ = pol.sample(rng)
         assert np.array_equal(pl[k], opl), f"sample {k}"
         assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
-    _, _, tlp, _ = P._teacher_forced(params, feats, [list(r) for r in pl])
-    np.testing.assert_allclose(tlp.cpu().numpy(), lp, rtol=LP_RTOL, atol=0)
+    with P._locked_tf(params, feats, [list(r) for r in pl]) as (_, _, tlp, _):
+        np.testing.assert_allclose(tlp.cpu().numpy(), lp, rtol=LP_RTOL, atol=0)
 
 
 def _oracle_sample_with_margin(pol, rng):

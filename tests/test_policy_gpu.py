@@ -240,5 +240,37 @@ def test_bench_size_decoder_vs_oracle(name, K, picks):
         opl, olp, _ = pol.sample(rng)
         assert np.array_equal(pl[k], opl), f"sample {k}"
         assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
-    _, _, tlp, _ = P._teacher_forced(params, feats, [list(r) for r in pl])
-    np.testing.assert_allclose(tlp.cpu().numpy(), lp, rtol=LP_RTOL, atol=0)
+    with P._locked_tf(params, feats, [list(r) for r in pl]) as (_, _, tlp, _):
+        np.testing.assert_allclose(tlp.cpu().numpy(), lp, rtol=LP_RTOL, atol=0)
+
+
+def test_dropin_calls_from_threads_share_one_engine():
+    """Controller threads of the reference (pkg/trainer.py:365-378) call the
+    drop-in functions concurrently on one GroupFeatures object: the per-engine
+    lock keeps each encode -> decode -> backward sequence intact."""
+    import threading
+
+    gg, topo, params, feats = _setup("C1", seed=2)
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    errors = []
+
+    def worker(seed):
+        try:
+            rng, orng = np.random.default_rng(seed), np.random.default_rng(seed)
+            for _ in range(6):
+                s = P.forward_sample(params, feats, rng)
+                opl, olp, _ = pol.sample(orng)
+                assert s.placement == opl
+                g = P.grad_log_prob(params, feats, s.placement, cache=s.cache)
+                assert _relnorm(g, pol.grad(opl)) < GRAD_RTOL
+                assert P.log_prob_of(params, feats, s.placement) == pytest.approx(olp, rel=LP_RTOL)
+        except Exception as ex:  # surfaced below
+            errors.append(repr(ex))
+
+    ths = [threading.Thread(target=worker, args=(100 + i,)) for i in range(4)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
