@@ -77,8 +77,9 @@ void dp_graph_destroy(dp_graph *g);
 
 /* Score K placements — batched simulate() + check_memory()
  * (pkg/simulator.py:93-106, 122-194; measure() with noise off,
- * pkg/simulator.py:205-219).  One thread per placement, event-exact:
- * makespan/busy/transfer/peak/feasible and the dispatch order are bit-identical
+ * pkg/simulator.py:205-219).  One warp per placement (device state in the
+ * lanes; one thread per placement for many placements of small graphs — the
+ * planner picks), event-exact: makespan/busy/transfer/peak/feasible and the dispatch order are bit-identical
  * to the reference.
  *   placement[K*n]  device ids (u8); by_rank != 0: [k*n + r], else [k*n + gid]
  *   makespan[K], busy[K*d], transfer[K*d], peak[K*d] (int64), feasible[K]

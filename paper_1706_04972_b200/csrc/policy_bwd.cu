@@ -23,7 +23,9 @@
 //                  samples, so its backward runs once on the summed inputs
 //                  (the reference runs it per sample)
 //   B5 enc_wgrad   w_enc, b_enc, type_table (np.add.at order)
-// Deterministic: fixed partitions + ordered reductions, no float atomics.
+// Deterministic: fixed partitions + ordered reductions.  The only float atomics
+// (att_bwd's RED adds into per-sample partials) have a single writer per
+// address per launch, so their result does not depend on scheduling.
 // Measured B200 latencies that shaped the code (scripts/lat_probe.cu): DFMA
 // ~8 cycles, LDS ~47, shfl ~27, exp ~160, tanh ~290: inner products use
 // register micro-tiles (many independent FMAs per shared-memory load).

@@ -179,6 +179,21 @@ def _hp(a):
     return a.ctypes.data if a.size else None
 
 
+SUPPORTED_HIDDEN = 64
+MAX_DEV_DIM = 32
+MAX_DEVICES = 32
+
+
+def check_policy_dims(hidden: int, dev_dim: int, num_devices: int) -> None:
+    """ValueError for policy widths the sm_100a kernels do not implement."""
+    if hidden != SUPPORTED_HIDDEN:
+        raise ValueError(f"this build supports hidden={SUPPORTED_HIDDEN} (the reference default); got hidden={hidden}")
+    if not 1 <= dev_dim <= MAX_DEV_DIM:
+        raise ValueError(f"this build supports 1 <= dev_dim <= {MAX_DEV_DIM}; got dev_dim={dev_dim}")
+    if not 1 <= num_devices <= MAX_DEVICES:
+        raise ValueError(f"this build supports 1 <= num_devices <= {MAX_DEVICES}; got num_devices={num_devices}")
+
+
 class DevicePolicy:
     """One ``dp_policy`` engine: features of one graph + dims, capacity k_max."""
 
@@ -191,6 +206,10 @@ class DevicePolicy:
         self.T = len(feats)
         if self.T == 0:
             raise ValueError("cannot place an empty group sequence")
+        # the kernels keep the 4H = 256 gate columns in one CTA's lanes: the
+        # reference accepts any width (pkg/policy.py:127-146) but this build
+        # implements its default (pkg/trainer.py:173-174) and says so up front
+        check_policy_dims(hidden, dev_dim, num_devices)
         self.D, self.hidden, self.dev_dim, self.k_max = num_devices, hidden, dev_dim, k_max
         self.spec = spec
         self.device = torch.device("cuda", torch.cuda.current_device())

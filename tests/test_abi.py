@@ -49,3 +49,22 @@ def test_kernels_are_sm100a(lib_path):
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib_path],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_unsupported_policy_widths_raise_value_error(lib_path):
+    """The reference takes any hidden/dev_dim (pkg/policy.py:127-146); this build
+    implements hidden=64 and says so with a ValueError, on the host and at the C-ABI."""
+    import ctypes
+
+    from paper_1706_04972_b200 import _native
+    from paper_1706_04972_b200.policy import check_policy_dims
+
+    check_policy_dims(64, 16, 4)
+    for hidden, dd, d in ((8, 16, 2), (128, 16, 2), (64, 0, 2), (64, 33, 2), (64, 16, 0), (64, 16, 33)):
+        with pytest.raises(ValueError, match="this build supports"):
+            check_policy_dims(hidden, dd, d)
+    L = _native.load_only()
+    out = ctypes.c_void_p()
+    rc = L.dp_policy_create(4, 2, 8, 16, 16, 8, 64, 3, None, None, None, None, 1, ctypes.byref(out))
+    # status 1 is what _native.check() turns into ValueError(message)
+    assert rc == 1 and b"hidden=64" in L.dp_last_error()
