@@ -144,6 +144,12 @@ int dp_debug_decoder_variant(int32_t mode);
  * backward). */
 int dp_debug_policy_drop_stores(dp_policy *p, int32_t mask);
 
+/* Debug (tests, A/B timing): mode 1 runs the fp64 DMMA / SIMT kernels where a
+ * tcgen05 tensor-core path exists (the decoder weight gradient); 0 (default)
+ * uses the tensor cores wherever the shape allows; 2 = tensor cores with the
+ * accumulators drained every 3 steps (the long-batch path, at small sizes). */
+int dp_debug_tensor_core(int32_t mode);
+
 /* Copy the assembled encoder inputs of the last encode (embed_groups(),
  * pkg/policy.py:266-268) into out[T*input_dim] (device). */
 int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream);

@@ -36,6 +36,7 @@ SIGNATURES = {
     "dp_debug_phase_clocks": (I32, [I32, P]),
     "dp_debug_decoder_variant": (I32, [I32]),
     "dp_debug_policy_drop_stores": (I32, [P, I32]),
+    "dp_debug_tensor_core": (I32, [I32]),
     "dp_debug_fastmath_error": (I32, [I64, P]),
     "dp_debug_att_clocks": (I32, [I32, P]),
     "dp_debug_sim_variant": (I32, [I32]),

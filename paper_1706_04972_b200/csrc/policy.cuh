@@ -22,6 +22,14 @@ struct PolicyDims {
     ParamLayout off;
 };
 
+int dp_tensor_core_mode();  // dp_debug_tensor_core: 0 = tcgen05 paths where supported, 1 = DMMA/SIMT only
+
+// tcgen05 / TMA decoder weight gradient (wgrad_tc.cu)
+bool dec_wgrad_tc_ok(const PolicyDims &dm);
+int launch_dec_wgrad_tc(const PolicyDims &dm, int rows, const double *act_h, const double *enc_h,
+                        const uint8_t *choice, const double *da, const int *colexp, const double *adv, int K,
+                        double *partial, int *n_chunks, cudaStream_t st);
+
 }  // namespace dp
 
 struct dp_policy {
@@ -59,6 +67,7 @@ struct dp_policy {
     double *d_enc;                                       // [T*H]
     double *gsum;                                        // [T*H] GM: sum_k adv_k ds_k^T H_k
     double *da_enc;                                      // [T*G]
+    int *da_colexp;                                      // [G] max biased exponent of |da| per gate column (decoder LSTM backward)
     double *partial;                                     // per-CTA partial sums
     size_t partial_elems;
     double *gacc;                                        // [P] accumulator

@@ -37,6 +37,15 @@
 
 namespace dp {
 
+#define DP_TRY(x)                       \
+    do {                                \
+        const int rc_ = (x);            \
+        if (rc_ != DP_OK) return rc_;   \
+    } while (0)
+
+static int g_tc_mode = 0;  // dp_debug_tensor_core
+int dp_tensor_core_mode() { return g_tc_mode; }
+
 namespace {
 
 constexpr int kTile = 32;   // rows per tile (B0, B1, B3)
@@ -993,7 +1002,8 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     double *__restrict__ dh_out /* [seq][64] */, double *__restrict__ dc_out,
     const double *__restrict__ gates_in /* activations read (== gates: in place) */,
     const double *__restrict__ sum_dh /* M == 1, non-NULL: dh_in = sum_r sum_w[r] sum_dh[r], dc_in likewise */,
-    const double *__restrict__ sum_dc, const double *__restrict__ sum_w, int sum_rows) {
+    const double *__restrict__ sum_dc, const double *__restrict__ sum_w, int sum_rows,
+    int *__restrict__ colexp /* [256] or NULL: max biased exponent of |da| per gate column */) {
     extern __shared__ __align__(16) double sm[];
     double *s_dh = sm;                   // [M][64]
     double *s_dc = s_dh + M * kH;        // [M][64]
@@ -1076,6 +1086,11 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     __syncthreads();
     // this slot's da row in the gates array (in place), walked backwards
     double *grow = gates + ((size_t)(q0 + (live ? xm : 0)) * T + (T - 1)) * kG + xu;
+    // running max exponent of |da| per gate column (the tensor-core weight
+    // gradient's fixed-point scales, wgrad_tc.cu); integer max of the
+    // exponent fields, off the elementwise chain
+    int ex_i = 0, ex_f = 0, ex_o = 0, ex_g = 0;
+    auto expo = [](double v) { return (__double2hiint(v) >> 20) & 0x7FF; };
     for (int t = T - 1; t >= 0; t--, grow -= kG) {
         double da_i = 0.0, da_f = 0.0, da_o = 0.0, da_g = 0.0;
         if (live) {
@@ -1108,6 +1123,10 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
             grow[kH] = da_f;
             grow[2 * kH] = da_o;
             grow[3 * kH] = da_g;
+            ex_i = max(ex_i, expo(da_i));
+            ex_f = max(ex_f, expo(da_f));
+            ex_o = max(ex_o, expo(da_o));
+            ex_g = max(ex_g, expo(da_g));
         }
         if (live) tc = fm_gate_act(cur.c, true);  // tanh; independent of the mat-vec below: the chains interleave
         // per sample: partial row sums over this lane's 8 columns, then a
@@ -1161,6 +1180,12 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     if (clk_on)
 #pragma unroll
         for (int i = 0; i < 4; i++) g_lstm_clk[ci][i] += clk_acc[i];
+    if (colexp && live) {
+        atomicMax(colexp + xu, ex_i);
+        atomicMax(colexp + kH + xu, ex_f);
+        atomicMax(colexp + 2 * kH + xu, ex_o);
+        atomicMax(colexp + 3 * kH + xu, ex_g);
+    }
     for (int y = tid; y < Mb * kH; y += kLstmThreads) {
         const int m = y >> 6, u = y & 63;
         dh_out[(size_t)(q0 + m) * kH + u] = s_dh[y];
@@ -1742,8 +1767,9 @@ int run_b2(dp_policy *p, const double *params, int K, cudaStream_t st) {
         const double *null = nullptr;
         const double *gin = p->act_g;
         int zero = 0;
+        DP_CUDA_TRY(cudaMemsetAsync(p->da_colexp, 0, sizeof(int) * kG, st));
         void *args[] = {&T,       &n_seq,   &M,    &Wh,   &p->act_g, &p->act_c, &c_init, &p->row_dhx, &null,
-                        &null,    &p->dh0,  &p->dc0, &gin, &null,     &null,     &null,   &zero};
+                        &null,    &p->dh0,  &p->dc0, &gin, &null,     &null,     &null,   &zero, &p->da_colexp};
         DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(ceil_div(K, M)), dim3(kLstmThreads), args, smem, st));
     }
     DP_LAUNCH_CHECK();
@@ -1775,7 +1801,7 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         lstm_bwd_kernel<1><<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
                                                    p->enc_c, p->zeros, p->d_enc, nullptr, nullptr,
                                                    dhc_sum + 2 * kH, dhc_sum + 3 * kH, p->enc_g, p->dh0, p->dc0, adv,
-                                                   K);
+                                                   K, nullptr);
         DP_LAUNCH_CHECK();
         // the encoder weight grads and the type-table chain both only need
         // da_enc: fork the former onto a second side stream
@@ -1817,8 +1843,21 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         rb.launch(n_cta, 0, st);
         DP_LAUNCH_CHECK();
     }
-    // B3
-    {
+    // B3: tcgen05 / TMA int8-digit GEMM (wgrad_tc.cu) where the shape allows,
+    // else the DMMA kernel
+    if (dp_tensor_core_mode() != 1 && dec_wgrad_tc_ok(dm)) {
+        int n_chunks = 0;
+        DP_TRY(launch_dec_wgrad_tc(dm, rows, p->act_h, p->enc_h, p->act_choice, p->act_g, p->da_colexp, adv, K, part,
+                                   &n_chunks, st));
+        const size_t stride = (size_t)(kH + dm.D + 1) * kG;
+        RedBuilder rb;
+        rb.add(part, stride, kH * kG, grad + dm.off.w_dec + (size_t)dm.dd * kG);
+        rb.add(part + (size_t)kH * kG, stride, (dm.D + 1) * kG, p->gacc);
+        rb.launch(n_chunks, 0, st);
+        DP_LAUNCH_CHECK();
+        dec_finalize_kernel<<<1 + ceil_div((dm.D + 1) * dm.dd, kG / 32), kG, 0, st>>>(dm, params, p->gacc, grad);
+        DP_LAUNCH_CHECK();
+    } else {
         const Grid g = tiles_grid(rows, kTile);
         const size_t smem = sizeof(double) * ((size_t)2 * kTile * (kWgHLd + kWgDLd) + (size_t)(dm.D + 1) * kG);
         DP_CUDA_TRY(allow_big_smem((const void *)dec_wgrad_kernel, smem));
@@ -1838,11 +1877,6 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
     return DP_OK;
 }
 
-#define DP_TRY(x)                       \
-    do {                                \
-        const int rc_ = (x);            \
-        if (rc_ != DP_OK) return rc_;   \
-    } while (0)
 
 }  // namespace
 
@@ -1931,4 +1965,14 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
     DP_CUDA_TRY(cudaStreamWaitEvent(st, p->ev_rows, 0));
     // the encoder backward (sequential) forks first; B0 / B1f grads and B3 fill the other SMs
     return run_b345(p, params, K, adv, grad, st, true);
+}
+
+// Debug: 1 = run the DMMA / SIMT kernels where a tcgen05 path exists (A/B parity runs);
+// 2 = tcgen05 with a TMEM drain every 3 steps (exercises the multi-segment epilogue);
+// 3 / 4 / 5 = timing ablations of the tcgen05 weight gradient (no conversion / no TMA / neither; wrong results).
+extern "C" int dp_debug_tensor_core(int32_t mode) {
+    DP_ENTRY();
+    DP_REQUIRE(mode >= 0 && mode <= 5, "dp_debug_tensor_core: mode must be 0..5");
+    dp::g_tc_mode = mode;
+    return DP_OK;
 }

@@ -1,0 +1,149 @@
+// Blackwell (sm_100a) async-proxy primitives used by the tensor-core kernels:
+// mbarriers, TMA tensor loads (cp.async.bulk.tensor), tcgen05 TMEM allocation,
+// tcgen05.mma kind::i8 with TMEM accumulators, tcgen05.commit / tcgen05.ld.
+//
+// fp64-exact products on the int8 tensor cores (Ozaki-style splitting): an
+// fp64 operand x with a per-column scale 2^s (|x| 2^s < 2^46) becomes the
+// 48-bit integer v = round(x 2^s), written in balanced base 256,
+// v = sum_{b<6} d_b 256^b with d_b in [-128, 127].  Those digits are simply
+// the bytes of (v + B) ^ B with B = 0x808080808080 (v + B has the unsigned
+// digits d_b + 128, and XOR 0x80 turns each into the two's complement d_b).
+// A product sum_r x_r y_r is then sum_{b,c} 256^(b+c) sum_r dx_b dy_c: each
+// digit plane pair is one int8 MMA with exact int32 accumulation, summed per
+// diagonal b + c in TMEM.  Dropping the diagonals b + c < 5 leaves an error
+// below 2^-45 of max|x| max|y| per term with zero mean (balanced digits),
+// and rounding x 2^s to an integer below 2^-47 of max|x|.
+#pragma once
+#include <cuda.h>
+#include <stdint.h>
+
+namespace dp {
+namespace tc {
+
+constexpr int kDigits = 6;                          // 48-bit fixed point
+constexpr int kMinDiag = 5;                         // keep digit pairs b + c >= 5
+constexpr int kDiags = 2 * (kDigits - 1) - kMinDiag + 1;  // 6 accumulators
+constexpr unsigned long long kBias = 0x808080808080ull;
+constexpr int kFixBits = 46;                        // |x| 2^s < 2^46
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ---------------------------------------------------------------- mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "DP_MBAR_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra DP_MBAR_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// ---------------------------------------------------------------- TMA
+// 2-D tiled tensor load global -> shared, completion counted in bytes on bar.
+// Coordinates are signed (out-of-range rows/columns are zero-filled).
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async proxy (tensor core)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---------------------------------------------------------------- tcgen05
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {  // whole warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {  // whole warp
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// D[tmem] (+)= A[smem] B[smem], int8 x int8 -> int32, issued by one thread
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// arrive on bar once every previously issued tcgen05 op of this thread is done
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// 32 lanes x 8 consecutive 32-bit columns (warp w reads lanes 32 (w % 4) ..)
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Shared-memory matrix descriptor, no swizzle (canonical "interleaved"
+// layout): core matrices of 8 rows x 16 bytes; lbo / sbo = byte strides
+// between core matrices along the leading / strided dimension (sm_100 version 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+           (1ull << 46);
+}
+// Instruction descriptor kind::i8: signed x signed -> s32, both operands
+// MN-major (the fp64 sources are row-major over the contraction index).
+__host__ __device__ constexpr uint32_t idesc_i8_mn(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+
+// 2^e as a double for -1022 <= e <= 1023 (exponent-field construction)
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(e + 1023) << 52); }
+
+// Scale exponent s for a column whose max |x| has biased exponent eb:
+// |x| < 2^(eb - 1022) -> |x| 2^s < 2^46 with s = 1068 - eb (clamped so 2^s
+// stays a normal double; a column below 2^-954 contributes nothing).
+__device__ __forceinline__ int fix_shift(int eb) {
+    const int s = 1068 - eb;
+    return s > 1000 ? 1000 : s;
+}
+
+// fixed-point digits of x * 2^s: the 6 balanced int8 digits packed
+// little-endian in the low 48 bits.  fma(x, 2^s, 1.5 * 2^52) rounds x 2^s to
+// the nearest integer v in the low mantissa bits (|v| < 2^46 << 2^51), so
+// bits(t) - bits(1.5 * 2^52) = v and the digits are (v + B) ^ B.
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+constexpr unsigned long long kMagicBits = 0x4338000000000000ull;
+__device__ __forceinline__ unsigned long long digits6(double x, double scale) {
+    const double t = fma(x, scale, kMagic);
+    return ((unsigned long long)__double_as_longlong(t) + (kBias - kMagicBits)) ^ kBias;
+}
+
+}  // namespace tc
+}  // namespace dp

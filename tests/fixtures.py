@@ -71,3 +71,11 @@ def baseline_cases():
         rs = [int(x) for x in inst["rs_placement"]] if inst["rs_placement"].size else None
         out.append((gg, topo, bf, float(inst["bf_makespan"]), int(inst["rs_budget"]), rs))
     return out, [int(x) for x in a["c1_rs_placement"]]
+
+
+# Final parameters after Adam vs the reference / oracle: Adam's per-coordinate
+# m / sqrt(v) carries rounding-level gradient differences (the decoder weight
+# gradients are int8-digit tensor-core sums, ~1e-13 relative) into parameter
+# differences of the same relative size on every coordinate; training logs
+# stay byte-identical.  Gradients themselves are checked at 1e-9.
+PARAM_RTOL = 1e-10

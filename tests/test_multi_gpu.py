@@ -4,7 +4,7 @@ and C4 (several independent tasks advanced together on their own streams)."""
 import numpy as np
 import pytest
 
-from fixtures import cfg, train_golden
+from fixtures import cfg, train_golden, PARAM_RTOL
 from oracle import trainer as otr
 import paper_1706_04972_b200 as dp
 
@@ -22,7 +22,7 @@ def test_multi_controller_round_schedule_matches_oracle(name, C, K, U):
     assert dp.log_to_csv(res.log, include_wall=False) == otr.csv_of(want["rows"])
     assert res.store_versions == want["versions"]
     rel = np.linalg.norm(res.final_params - want["final"]) / np.linalg.norm(want["final"])
-    assert rel < 1e-12
+    assert rel < PARAM_RTOL
     # properties of any admissible interleaving: one row per (controller, update),
     # versions never decrease per controller, best_R monotone
     assert len(res.log) == C * U
@@ -44,7 +44,7 @@ def test_train_many_concurrent_equals_each_run_alone():
     for res, g in ((ra, a), (rb, b)):
         assert dp.log_to_csv(res.log, include_wall=False) == g["csv"]
         rel = np.linalg.norm(res.final_params - g["final_params"]) / np.linalg.norm(g["final_params"])
-        assert rel < 1e-12
+        assert rel < PARAM_RTOL
 
 
 def test_train_many_mixed_graphs_and_lengths():

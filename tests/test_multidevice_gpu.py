@@ -16,7 +16,7 @@ import numpy as np
 import pytest
 import torch
 
-from fixtures import cfg, train_golden
+from fixtures import cfg, train_golden, PARAM_RTOL
 import paper_1706_04972_b200 as dp
 from paper_1706_04972_b200 import parallel, trainer
 
@@ -31,7 +31,7 @@ def _check(res, g):
         assert res.best_placement is None
     assert res.store_versions == int(g["store_versions"])
     rel = np.linalg.norm(res.final_params - g["final_params"]) / np.linalg.norm(g["final_params"])
-    assert rel < 1e-12, rel
+    assert rel < PARAM_RTOL, rel
 
 
 def test_nccl_binding_loads():
@@ -55,7 +55,7 @@ def test_single_rank_nccl_exchange_captured_matches_reference(name):
     rows = sorted(r.rows, key=lambda q: (q.controller_id, q.update_index))
     assert dp.log_to_csv(rows, include_wall=False) == g["csv"]
     rel = np.linalg.norm(store.snapshot()[0] - g["final_params"]) / np.linalg.norm(g["final_params"])
-    assert rel < 1e-12
+    assert rel < PARAM_RTOL
 
 
 @pytest.mark.parametrize("name,G", [("C1", 2), ("C3tight", 2), ("C3tight", 4), ("C1noise", 2)])

@@ -59,7 +59,7 @@ def _worker(rank, size, port, name, q):
 
 @pytest.mark.parametrize("name,size", [("C1", 2), ("C3tight", 2), ("C3tight", 4)])
 def test_sharded_train_matches_single_process_reference(name, size):
-    from fixtures import train_golden
+    from fixtures import PARAM_RTOL, train_golden
 
     g = train_golden(name)
     ctx = mp.get_context("spawn")
@@ -77,7 +77,7 @@ def test_sharded_train_matches_single_process_reference(name, size):
             assert best == [int(x) for x in g["best_placement"]]
         assert versions == int(g["store_versions"])
         rel = np.linalg.norm(final - g["final_params"]) / np.linalg.norm(g["final_params"])
-        assert rel < 1e-12, (rank, rel)
+        assert rel < PARAM_RTOL, (rank, rel)
 
 
 def test_bench_multi_rank_line():

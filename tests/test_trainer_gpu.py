@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from fixtures import cfg, train_golden
+from fixtures import cfg, train_golden, PARAM_RTOL
 import paper_1706_04972_b200 as dp
 
 pytestmark = pytest.mark.gpu
@@ -30,7 +30,7 @@ def test_train_log_and_params_match_reference(name):
     assert res.store_versions == int(g["store_versions"])
     assert res.rejected_updates == int(g["rejected"])
     rel = np.linalg.norm(res.final_params - g["final_params"]) / np.linalg.norm(g["final_params"])
-    assert rel < 1e-12
+    assert rel < PARAM_RTOL
     np.testing.assert_allclose(res.final_params, g["final_params"], rtol=1e-6, atol=1e-12)
 
 
@@ -96,7 +96,7 @@ def test_train_with_measurement_noise_matches_reference(name, graph):
     assert dp.log_to_csv(res.log, include_wall=False) == g["csv"]
     assert res.store_versions == int(g["store_versions"])
     rel = np.linalg.norm(res.final_params - g["final_params"]) / np.linalg.norm(g["final_params"])
-    assert rel < 1e-12
+    assert rel < PARAM_RTOL
     if len(g["best_placement"]):
         assert res.best_placement == [int(x) for x in g["best_placement"]]
 
