@@ -144,6 +144,27 @@ int dp_debug_decoder_variant(int32_t mode);
  * backward). */
 int dp_debug_policy_drop_stores(dp_policy *p, int32_t mask);
 
+/* Graph ingestion on the device: per-group features and the
+ * deduplicated group-edge CSR of a grouped op graph (reference GroupedGraph,
+ * pkg/graph.py:183-238, and GroupFeatures.from_grouped, pkg/policy.py:97-114),
+ * all indexed by GROUP ID (the caller orders rows by its topological rank).
+ *   h_op_group[n_ops]     group id of each op
+ *   h_op_key[n_ops]       rank of the op's type name among the sorted names
+ *   h_key_to_index[n_keys] EmbeddingSpec row of each key (unknown -> last row)
+ *   h_op_elems[n_ops]     output element count (0 for a scalar output)
+ *   h_e_src/dst/bytes[n_edges]  op edges
+ * Outputs (host): type_off[G+1] / type_idx[n_ops] (multiset in key order),
+ * shape[G*shape_slots] (log1p of the largest counts, descending), adj[G*adj_slots]
+ * (multi-hot of in + out neighbour groups mod adj_slots), ge_off[G+1] /
+ * ge_dst[<= n_edges] / ge_bytes (out-edges to other groups, by destination,
+ * summed bytes), out_bytes[G] (all member out-edges incl. intra-group).
+ * Limits: <= 1024 type names, <= 2048 members / leaving edges per group. */
+int dp_group_features(int32_t n_ops, int32_t n_groups, const int32_t *h_op_group, const int32_t *h_op_key,
+                      int32_t n_keys, const int32_t *h_key_to_index, const int64_t *h_op_elems, int32_t n_edges,
+                      const int32_t *h_e_src, const int32_t *h_e_dst, const int64_t *h_e_bytes, int32_t shape_slots,
+                      int32_t adj_slots, int32_t *h_type_off, int32_t *h_type_idx, double *h_shape, double *h_adj,
+                      int32_t *h_ge_off, int32_t *h_ge_dst, int64_t *h_ge_bytes, int64_t *h_out_bytes);
+
 /* Debug (tests, A/B timing): mode 1 runs the fp64 DMMA / SIMT kernels where a
  * tcgen05 tensor-core path exists (the decoder weight gradient); 0 (default)
  * uses the tensor cores wherever the shape allows; 2 = tensor cores with the

@@ -213,7 +213,14 @@ def coalesce_sole_consumers(graph: ComputationGraph) -> GroupedGraph:
     """Manual seeds, then merge any group feeding exactly one other group until a
     fixed point; sweeps visit groups by ascending representative id and the
     smaller representative survives (reference ``pkg/graph.py:282-338``)."""
-    rep = list(range(graph.num_ops))
+    return GroupedGraph(graph, coalesce_partition(graph))
+
+
+def coalesce_partition(graph) -> list:
+    """The member tuples of :func:`coalesce_sole_consumers` (reference
+    ``_coalesce_partition``, ``pkg/graph.py:282-332``); duck typed over the
+    reference's ComputationGraph as well."""
+    rep = list(range(len(graph.ops)))
 
     def root(x):
         while rep[x] != x:
@@ -221,7 +228,7 @@ def coalesce_sole_consumers(graph: ComputationGraph) -> GroupedGraph:
             x = rep[x]
         return x
 
-    members = {i: [i] for i in range(graph.num_ops)}
+    members = {i: [i] for i in range(len(graph.ops))}
     for seed in graph.manual_groups:
         if len(seed) < 2:
             continue
@@ -245,4 +252,70 @@ def coalesce_sole_consumers(graph: ComputationGraph) -> GroupedGraph:
             rep[drop] = keep
             members[keep].extend(members.pop(drop))
             changed = True
-    return GroupedGraph(graph, [tuple(sorted(v)) for v in members.values()])
+    return [tuple(sorted(v)) for v in members.values()]
+
+
+def split_cyclic_groups(graph):
+    """Co-location seeds that keep the group graph acyclic.
+
+    The reference generators seed one manual group per model unit holding its
+    forward chain AND its backward mirror (``pkg/generators.py:132-143``);
+    units linked forward (src -> dst) and backward (dst -> src,
+    ``pkg/generators.py:146-150``) then form a cycle between groups, and
+    ``GroupedGraph`` rejects the grouping (``pkg/graph.py:266-272``).  This
+    splits every manual group into the runs its members form in a
+    group-greedy topological order of the ops (Kahn; the current group keeps
+    going while it has a ready op, else the smallest ready op id starts the
+    next run).  Runs are contiguous in one topological order, so every edge
+    between runs points forward: the quotient is acyclic.  A unit's forward
+    chain and backward mirror become two groups; an already-acyclic grouping
+    whose groups are convex keeps each group whole.
+
+    Accepts the reference's ``ComputationGraph`` or this package's (duck typed:
+    ``ops``, ``edges``, ``manual_groups``, ``out_ids``, ``in_ids``) and returns
+    the same class with the new ``manual_groups``."""
+    m = len(graph.ops)
+    grp = [-1] * m
+    for g, members in enumerate(graph.manual_groups):
+        for i in members:
+            grp[i] = g
+    indeg = [len(x) for x in graph.in_ids]
+    ready = [v for v in range(m) if indeg[v] == 0]
+    heapq.heapify(ready)
+    ready_of: dict[int, list[int]] = {}
+    for v in ready:
+        if grp[v] >= 0:
+            heapq.heappush(ready_of.setdefault(grp[v], []), v)
+    done = [False] * m
+    runs: list[list[int]] = []
+    cur, run = -1, None
+    placed = 0
+    while placed < m:
+        v = -1
+        if cur >= 0:
+            h = ready_of.get(cur)
+            while h and done[h[0]]:
+                heapq.heappop(h)
+            if h:
+                v = heapq.heappop(h)
+        if v < 0:
+            while done[ready[0]]:
+                heapq.heappop(ready)
+            v = heapq.heappop(ready)
+            if grp[v] != cur or grp[v] < 0:
+                cur = grp[v]
+                run = [] if cur >= 0 else None
+                if run is not None:
+                    runs.append(run)
+        done[v] = True
+        placed += 1
+        if run is not None:
+            run.append(v)
+        for w in graph.out_ids[v]:
+            indeg[w] -= 1
+            if indeg[w] == 0:
+                heapq.heappush(ready, w)
+                if grp[w] >= 0:
+                    heapq.heappush(ready_of.setdefault(grp[w], []), w)
+    new_groups = [sorted(r) for r in runs if len(r) > 1]
+    return type(graph)(graph.ops, graph.edges, new_groups)

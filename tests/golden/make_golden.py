@@ -45,6 +45,8 @@ import devplace as ref  # noqa: E402  (the reference)
 import devplace.simulator as ref_sim  # noqa: E402
 import devplace.trainer as ref_trainer  # noqa: E402
 import devplace.policy as ref_policy  # noqa: E402
+import devplace.generators as ref_gen  # noqa: E402
+import devplace.graph as ref_graph  # noqa: E402
 import util as ref_util  # noqa: E402  (reference tests/util.py)
 
 from paper_1706_04972_b200.instances import instance_arrays  # noqa: E402  (serializer only)
@@ -377,7 +379,70 @@ def main():
         fh.write("\n")
 
 
+INGEST_SPECS = {
+    "rnnlm_L2S20": dict(family="rnnlm_grid", layers=2, steps=20, seed=0),
+    "nmt_L4S40": dict(family="nmt_attention", layers=4, steps=40, seed=0),
+}
+
+
+def ingest_golden(spec):
+    """f4: a paper-scale generator graph (8.8k ops for nmt L4 S40) whose manual
+    groups are cyclic.  The acyclic split under test (graph.split_cyclic_groups)
+    provides the INPUT partition; every expected value below is the reference's
+    own GroupedGraph / coalescing / GroupFeatures on that input."""
+    from paper_1706_04972_b200.graph import split_cyclic_groups  # input only
+
+    g = ref_gen.generate(ref_gen.GeneratorSpec(**spec))
+    try:
+        ref.coalesce_sole_consumers(g)
+        raise AssertionError("expected the shipped manual groups to be cyclic")
+    except ref_graph.GraphError:
+        pass
+    fixed = split_cyclic_groups(g)
+    gg = ref.coalesce_sole_consumers(fixed)          # reference coalescing + validation
+    espec = ref_policy.EmbeddingSpec.build([gg])
+    feats = ref_policy.GroupFeatures.from_grouped(gg, espec)
+    types = sorted({op.op_type for op in g.ops})
+    tix = {t: i for i, t in enumerate(types)}
+    shape_ptr = np.zeros(len(g.ops) + 1, np.int64)
+    dims = []
+    for i, op in enumerate(g.ops):
+        dims.extend(op.output_shape)
+        shape_ptr[i + 1] = len(dims)
+    man_ptr = np.cumsum([0] + [len(x) for x in g.manual_groups])
+    split_ptr = np.cumsum([0] + [len(x) for x in fixed.manual_groups])
+    part_ptr = np.cumsum([0] + [len(grp.members) for grp in gg.groups])
+    tl = [np.asarray(x, np.int32) for x in feats.type_indices]
+    adj_t, adj_s = np.nonzero(feats.adj_blocks)
+    return dict(
+        types=np.array(types), op_type=np.array([tix[op.op_type] for op in g.ops], np.int32),
+        op_cost=np.array([op.compute_cost for op in g.ops], np.float64),
+        op_param=np.array([op.param_bytes for op in g.ops], np.int64),
+        shape_ptr=shape_ptr, shape_dims=np.array(dims, np.int64),
+        op_name_grad=np.array(["/grad_" in op.name for op in g.ops]),
+        edge_src=np.array([e.src for e in g.edges], np.int32), edge_dst=np.array([e.dst for e in g.edges], np.int32),
+        edge_bytes=np.array([e.tensor_bytes for e in g.edges], np.int64),
+        manual_ptr=man_ptr, manual_ops=np.concatenate([np.asarray(x, np.int32) for x in g.manual_groups]),
+        split_ptr=split_ptr, split_ops=np.concatenate([np.asarray(x, np.int32) for x in fixed.manual_groups]),
+        part_ptr=part_ptr, part_ops=np.concatenate([np.asarray(grp.members, np.int32) for grp in gg.groups]),
+        group_cost=np.array([grp.compute_cost for grp in gg.groups]),
+        group_param=np.array([grp.param_bytes for grp in gg.groups], np.int64),
+        group_out_bytes=np.array([grp.out_bytes for grp in gg.groups], np.int64),
+        ge_src=np.array([e.src for e in gg.group_edges], np.int32),
+        ge_dst=np.array([e.dst for e in gg.group_edges], np.int32),
+        ge_bytes=np.array([e.tensor_bytes for e in gg.group_edges], np.int64),
+        topo=np.array(gg.topo, np.int32), vocab=np.array(sorted(espec.type_vocab, key=espec.type_vocab.get)),
+        f_type_off=np.cumsum([0] + [len(x) for x in tl]), f_type_idx=np.concatenate(tl),
+        f_shape=np.asarray(feats.shape_blocks), f_adj_t=adj_t.astype(np.int32), f_adj_s=adj_s.astype(np.int16),
+    )
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "ingest":
+        for name, spec in INGEST_SPECS.items():
+            np.savez_compressed(os.path.join(HERE, f"ingest_{name}.npz"), **ingest_golden(spec))
+            print("ingest", name)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "noise":
         main_noise()
     elif len(sys.argv) > 1 and sys.argv[1] == "baselines":
