@@ -73,4 +73,8 @@ struct dp_graph {
     int64_t *mem;        // [d]
     int32_t max_indeg;
     size_t sim_smem_per_placement;
+    // shared-memory image of the graph (dur | out_bytes | bw | out_off | dst u16 |
+    // gid u16 | indeg u16, 16-byte padded) staged with one TMA bulk copy
+    unsigned char *image;
+    size_t image_bytes;
 };

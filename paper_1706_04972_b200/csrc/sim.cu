@@ -23,7 +23,11 @@
 // the reference's order, so every output is bit-identical, including the
 // dispatch order.  Compiled with --fmad=false (there are no mul-adds anyway).
 
+#include <cstring>
+#include <vector>
+
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace {
 
@@ -111,6 +115,24 @@ __host__ __device__ inline size_t graph_smem_bytes(int n, int d, int e) {
     return (b + 15) & ~(size_t)15;
 }
 
+// Stage the graph image into shared memory with the TMA bulk-copy engine (one
+// elected thread issues <= 32 KB chunks against one mbarrier; every thread
+// waits on its phase).  The image layout is the GS carve-up below.
+__device__ __forceinline__ void stage_graph(unsigned char *smem, const dp_graph &g, uint64_t *bar) {
+    if (threadIdx.x == 0) {
+        dp::tc::mbar_init(bar, 1);
+        dp::tc::fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t total = (uint32_t)g.image_bytes;
+        dp::tc::mbar_expect_tx(bar, total);
+        for (uint32_t o = 0; o < total; o += 32768u)
+            dp::tc::bulk_load(smem + o, g.image + o, total - o < 32768u ? total - o : 32768u, bar);
+    }
+    dp::tc::mbar_wait(bar, 0);
+}
+
 // Per-placement shared-memory bytes (DM > 0: device state in registers).
 __host__ __device__ inline size_t slot_bytes(int n, int d, bool reg_dev) {
     size_t b = (size_t)n * 8 + (size_t)d * d * 8;  // maxarr, link_free
@@ -127,6 +149,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
                                                   int64_t *__restrict__ peak_out, uint8_t *__restrict__ feasible,
                                                   int32_t *__restrict__ order, uint8_t *__restrict__ err, int S) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t s_stage_bar;
     const int s = threadIdx.x;
     const int k = blockIdx.x * S + s;
     const int n = g.n, D = g.d;
@@ -143,18 +166,7 @@ __global__ void __launch_bounds__(128) sim_kernel(dp_graph g, int K, const uint8
         uint16_t *sdst = reinterpret_cast<uint16_t *>(soff + n + 1);
         uint16_t *sgid = sdst + g.e;
         uint16_t *sind = sgid + n;
-        for (int i = s; i < n * D; i += blockDim.x) sdur[i] = g.dur[i];
-        for (int i = s; i < g.e; i += blockDim.x) {
-            sbytes[i] = g.out_bytes[i];
-            sdst[i] = (uint16_t)g.out_dst[i];
-        }
-        for (int i = s; i < D * D; i += blockDim.x) sbw[i] = g.bw[i];
-        for (int i = s; i <= n; i += blockDim.x) soff[i] = g.out_off[i];
-        for (int i = s; i < n; i += blockDim.x) {
-            sgid[i] = (uint16_t)g.gid[i];
-            sind[i] = (uint16_t)g.indeg[i];
-        }
-        __syncthreads();
+        stage_graph(smem, g, &s_stage_bar);
         g_dur = sdur;
         g_bytes = sbytes;
         g_bw = sbw;
@@ -430,6 +442,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) sim_warp_kernel(
     double *__restrict__ busy_out, double *__restrict__ transfer_out, int64_t *__restrict__ peak_out,
     uint8_t *__restrict__ feasible, int32_t *__restrict__ order, uint8_t *__restrict__ err) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint64_t s_stage_bar;
     constexpr unsigned kFull = 0xffffffffu;
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     const int n = g.n, D = g.d;
@@ -446,18 +459,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) sim_warp_kernel(
         uint16_t *sdst = reinterpret_cast<uint16_t *>(soff + n + 1);
         uint16_t *sgid = sdst + g.e;
         uint16_t *sind = sgid + n;
-        for (int i = tid; i < n * D; i += blockDim.x) sdur[i] = g.dur[i];
-        for (int i = tid; i < g.e; i += blockDim.x) {
-            sbytes[i] = g.out_bytes[i];
-            sdst[i] = (uint16_t)g.out_dst[i];
-        }
-        for (int i = tid; i < D * D; i += blockDim.x) sbw[i] = g.bw[i];
-        for (int i = tid; i <= n; i += blockDim.x) soff[i] = g.out_off[i];
-        for (int i = tid; i < n; i += blockDim.x) {
-            sgid[i] = (uint16_t)g.gid[i];
-            sind[i] = (uint16_t)g.indeg[i];
-        }
-        __syncthreads();
+        stage_graph(smem, g, &s_stage_bar);
         g_dur = sdur;
         g_bytes = sbytes;
         g_bw = sbw;
@@ -806,6 +808,27 @@ extern "C" int dp_graph_create(int32_t n, int32_t d, const double *h_cost, const
     for (int i = 0; i < e; i++) h_b[i] = (double)h_out_bytes[i];
     int32_t *h_rank = new int32_t[n > 0 ? n : 1];
     for (int r = 0; r < n; r++) h_rank[h_gid[r]] = r;
+    // shared-memory image for the TMA bulk staging (graph_smem_bytes layout)
+    g->image_bytes = graph_smem_bytes(n, d, e);
+    std::vector<unsigned char> img(g->image_bytes, 0);
+    {
+        double *idur = reinterpret_cast<double *>(img.data());
+        double *ibytes = idur + (size_t)n * d;
+        double *ibw = ibytes + e;
+        int32_t *ioff = reinterpret_cast<int32_t *>(ibw + (size_t)d * d);
+        uint16_t *idst = reinterpret_cast<uint16_t *>(ioff + n + 1);
+        uint16_t *igid = idst + e;
+        uint16_t *iind = igid + n;
+        std::memcpy(idur, h_dur, sizeof(double) * n * d);
+        std::memcpy(ibytes, h_b, sizeof(double) * e);
+        std::memcpy(ibw, h_bw, sizeof(double) * d * d);
+        std::memcpy(ioff, h_out_off, sizeof(int32_t) * (n + 1));
+        for (int i = 0; i < e; i++) idst[i] = (uint16_t)h_out_dst[i];
+        for (int r = 0; r < n; r++) {
+            igid[r] = (uint16_t)h_gid[r];
+            iind[r] = (uint16_t)h_indeg[r];
+        }
+    }
 
     auto up = [&](void **dst, const void *srcp, size_t bytes) -> bool {
         if (bytes == 0) bytes = 8;
@@ -824,7 +847,8 @@ extern "C" int dp_graph_create(int32_t n, int32_t d, const double *h_cost, const
               up((void **)&g->rank, n ? h_rank : nullptr, sizeof(int32_t) * n) &&
               up((void **)&g->rate, h_rate, sizeof(double) * d) &&
               up((void **)&g->bw, h_bw, sizeof(double) * d * d) &&
-              up((void **)&g->mem, h_mem, sizeof(int64_t) * d);
+              up((void **)&g->mem, h_mem, sizeof(int64_t) * d) &&
+              up((void **)&g->image, img.data(), g->image_bytes);
     delete[] h_dur;
     delete[] h_b;
     delete[] h_rank;
@@ -840,7 +864,7 @@ extern "C" int dp_graph_create(int32_t n, int32_t d, const double *h_cost, const
 extern "C" void dp_graph_destroy(dp_graph *g) {
     if (!g) return;
     void *ptrs[] = {g->cost, g->dur, g->indeg, g->out_off, g->out_dst, g->out_bytes,
-                    g->resident, g->gid, g->rank, g->rate, g->bw, g->mem};
+                    g->resident, g->gid, g->rank, g->rate, g->bw, g->mem, g->image};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     (void)cudaGetLastError();
