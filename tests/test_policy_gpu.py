@@ -274,3 +274,36 @@ def test_dropin_calls_from_threads_share_one_engine():
     for t in ths:
         t.join()
     assert not errors, errors
+
+
+def test_dropin_encoder_cache_follows_parameter_changes():
+    """forward_sample / grad_log_prob reuse the engine's encoder while the
+    caller's parameters are unchanged (content compare); a new snapshot, an
+    in-place edit of the same object, or a batched call that re-encodes
+    in between must all be honoured (oracle at every step)."""
+    gg, topo, params, feats = _setup("C2", seed=4)
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    vocab = opol.vocab_of(gg)
+
+    def oracle_for(p):
+        return opol.Policy(p.to_flat(), dims, opol.features(gg, vocab))
+
+    p2 = params.with_flat(params.to_flat() * 1.7)
+    for cur in (params, p2, params):
+        pol = oracle_for(cur)
+        rng, orng = np.random.default_rng(9), np.random.default_rng(9)
+        for _ in range(3):
+            s = P.forward_sample(cur, feats, rng)
+            opl, olp, _ = pol.sample(orng)
+            assert s.placement == opl and s.log_prob == pytest.approx(olp, rel=LP_RTOL)
+        assert _relnorm(P.grad_log_prob(cur, feats, s.placement, cache=s.cache), pol.grad(opl)) < GRAD_RTOL
+        # a batched call on the same engine re-encodes other parameters in between
+        P.sample_batch(p2 if cur is params else params, feats, np.random.default_rng(1), 3)
+        assert P.log_prob_of(cur, feats, s.placement) == pytest.approx(olp, rel=LP_RTOL)
+    # in-place edit of the same PolicyParams object
+    params.w_att *= 0.5
+    pol = oracle_for(params)
+    rng, orng = np.random.default_rng(5), np.random.default_rng(5)
+    s = P.forward_sample(params, feats, rng)
+    opl, olp, _ = pol.sample(orng)
+    assert s.placement == opl and s.log_prob == pytest.approx(olp, rel=LP_RTOL)
