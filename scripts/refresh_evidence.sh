@@ -8,7 +8,7 @@ TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT profiles
 reps=()
-for k in dec_kernel att_bwd_kernel lstm_bwd_kernel sim_warp_kernel row_prep_kernel enc_rec_kernel dec_wgrad_kernel adv_grads_kernel; do
+for k in dec_kernel att_bwd_kernel lstm_bwd_kernel sim_warp_kernel row_prep_kernel enc_rec_kernel dec_wgrad_tc_kernel adv_grads_kernel; do
     timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $OUT/prof_$k \
         python bench.py --steps 1 --warmup 3 --skip-cpu > $OUT/ncu_$k.log 2>&1
     reps+=($OUT/prof_$k.ncu-rep)
@@ -25,5 +25,11 @@ timeout 900 python bench.py > $OUT/${TAG}_bench_C3_1gpu.json 2> $OUT/bench_C3.er
 timeout 900 python bench.py --config C4 > $OUT/${TAG}_bench_C4_1gpu.json 2> $OUT/bench_C4.err
 timeout 900 python bench.py --config C5 > $OUT/${TAG}_bench_C5_1gpu.json 2> $OUT/bench_C5.err
 timeout 900 python bench.py --impl reference > $OUT/${TAG}_bench_reference_C3.json 2> $OUT/bench_ref.err
+timeout 900 python bench.py --mode sim > $OUT/${TAG}_bench_sim_C3.json 2> $OUT/bench_sim_C3.err
+timeout 900 python bench.py --mode sim --config C5 > $OUT/${TAG}_bench_sim_C5.json 2> $OUT/bench_sim_C5.err
+# tensor-core vs DMMA decoder weight gradient (per-launch device time)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:dec_wgrad --csv \
+    python scripts/wgrad_ab.py C3 256 0,1 > $OUT/${TAG}_wgrad_ab_ncu.csv 2>&1
+python scripts/sass_evidence.py > $OUT/${TAG}_sass_evidence.txt
 rm -f $OUT/prof_*.ncu-rep
 echo done
