@@ -167,8 +167,11 @@ int dp_group_features(int32_t n_ops, int32_t n_groups, const int32_t *h_op_group
 
 /* Debug (tests, A/B timing): mode 1 runs the fp64 DMMA / SIMT kernels where a
  * tcgen05 tensor-core path exists (the decoder weight gradient); 0 (default)
- * uses the tensor cores wherever the shape allows; 2 = tensor cores with the
- * accumulators drained every 3 steps (the long-batch path, at small sizes). */
+ * uses the tensor cores for the decoder weight gradient; 2 = the same with the
+ * accumulators drained every 3 steps (the long-batch path, at small sizes);
+ * 3-5 = timing ablations of that kernel (results invalid); 6 = additionally
+ * the attention backward's digit-plane tcgen05 kernel (att_tc.cu), which
+ * measures slower than the fp64 DMMA kernel at C3 and is not the default. */
 int dp_debug_tensor_core(int32_t mode);
 
 /* Copy the assembled encoder inputs of the last encode (embed_groups(),

@@ -30,6 +30,14 @@ int launch_dec_wgrad_tc(const PolicyDims &dm, int rows, const double *act_h, con
                         const uint8_t *choice, const double *da, const int *colexp, const double *adv, int K,
                         double *partial, int *n_chunks, cudaStream_t st);
 
+// tcgen05 / TMA attention backward, GM rows pass (att_tc.cu)
+bool att_bwd_tc_ok(const PolicyDims &dm);
+size_t att_bwd_tc_proj_bytes(int T);
+int launch_att_bwd_tc(const PolicyDims &dm, int K, const double *proj, uint8_t *proj_dig, double *proj_inv,
+                      const double *encW, const double *act_h, const double *row_w, const double *row_du,
+                      const double *act_e, const double *act_esc, double *tile_part, double *tile_partA,
+                      double *row_dhx, int n_cta, cudaStream_t st);
+
 }  // namespace dp
 
 struct dp_policy {
@@ -68,6 +76,8 @@ struct dp_policy {
     double *gsum;                                        // [T*H] GM: sum_k adv_k ds_k^T H_k
     double *da_enc;                                      // [T*G]
     int *da_colexp;                                      // [G] max biased exponent of |da| per gate column (decoder LSTM backward)
+    uint8_t *proj_dig;                                   // proj digit planes per 64-position chunk (tcgen05 attention backward)
+    double *proj_inv;                                    // [64] 2^-s per proj column
     double *partial;                                     // per-CTA partial sums
     size_t partial_elems;
     double *gacc;                                        // [P] accumulator

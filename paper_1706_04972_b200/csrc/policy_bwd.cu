@@ -1682,6 +1682,13 @@ int launch_att(dp_policy *p, const double *params, const Grid &g, size_t smem, i
     const int per_sample = tile_part && g.per % tps == 0 ? 1 : 0;
     p->att_per_sample = per_sample;
     p->att_gmode = p->act_e && tile_part ? 1 : 0;
+    if (p->att_gmode && dp_tensor_core_mode() == 6 && att_bwd_tc_ok(dm)) {
+        // tcgen05 / TMA digit-plane kernel (att_tc.cu): whole samples per CTA,
+        // per-tile partials
+        p->att_per_sample = 0;
+        return launch_att_bwd_tc(dm, rows / dm.T, p->proj, p->proj_dig, p->proj_inv, p->encW, p->act_h, p->row_w,
+                                 p->row_du, p->act_e, p->act_esc, tile_part, tile_partA, p->row_dhx, g.n_used, st);
+    }
     if (p->att_gmode) {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<true, true>, smem));
         att_bwd_kernel<true, true><<<g.n_used, kThreads, smem, st>>>(
@@ -1969,10 +1976,11 @@ extern "C" int dp_policy_backward_grads(dp_policy *p, const double *params, int3
 
 // Debug: 1 = run the DMMA / SIMT kernels where a tcgen05 path exists (A/B parity runs);
 // 2 = tcgen05 with a TMEM drain every 3 steps (exercises the multi-segment epilogue);
-// 3 / 4 / 5 = timing ablations of the tcgen05 weight gradient (no conversion / no TMA / neither; wrong results).
+// 3 / 4 / 5 = timing ablations of the tcgen05 weight gradient (no conversion / no TMA / neither; wrong results);
+// 6 = also the attention backward on tcgen05 (att_tc.cu; measured slower than the DMMA kernel at C3).
 extern "C" int dp_debug_tensor_core(int32_t mode) {
     DP_ENTRY();
-    DP_REQUIRE(mode >= 0 && mode <= 5, "dp_debug_tensor_core: mode must be 0..5");
+    DP_REQUIRE(mode >= 0 && mode <= 6, "dp_debug_tensor_core: mode must be 0..6");
     dp::g_tc_mode = mode;
     return DP_OK;
 }

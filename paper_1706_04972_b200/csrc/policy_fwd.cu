@@ -1252,7 +1252,7 @@ extern "C" void dp_policy_destroy(dp_policy *p) {
                     p->enc_g, p->edev, p->act_h, p->act_c, p->act_g, p->act_uc, p->row_du, p->proj, p->encW, p->proj_nmax, p->vdev, p->act_u, p->act_p,
                     p->act_stat, p->act_lz, p->act_choice, p->act_logp, p->row_q, p->row_w,
                     p->row_dq, p->row_dhx, p->dh0, p->dc0, p->d_enc, p->gsum, p->da_enc, p->partial, p->gacc,
-                    p->tile_part, p->tile_partA, p->partA, p->a_tot, p->act_e, p->act_esc, p->da_colexp};
+                    p->tile_part, p->tile_partA, p->partA, p->a_tot, p->act_e, p->act_esc, p->da_colexp, p->proj_dig, p->proj_inv};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p->side) cudaStreamDestroy(p->side);
@@ -1365,6 +1365,8 @@ extern "C" int dp_policy_create(int32_t T, int32_t n_dev, int32_t hidden, int32_
     alloc((void **)&p->gsum, sizeof(double) * T * kH);
     alloc((void **)&p->da_enc, sizeof(double) * T * kG);
     alloc((void **)&p->da_colexp, sizeof(int) * kG);
+    alloc((void **)&p->proj_dig, att_bwd_tc_proj_bytes(T));
+    alloc((void **)&p->proj_inv, sizeof(double) * kH);
     p->partial_elems = dp_backward_partial_elems(p);
     alloc((void **)&p->partial, sizeof(double) * p->partial_elems);
     alloc((void **)&p->gacc, sizeof(double) * dm.off.total);

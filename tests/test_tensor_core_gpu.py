@@ -95,3 +95,19 @@ def test_dec_wgrad_tc_bench_size_vs_oracle():
     g = _grad(params, feats, K, 21, w, 0)
     _, _, pl, _ = _sampled(params, feats, K, 21)
     assert _relnorm(g, _oracle_sum(pol, pl, w)) <= GRAD_RTOL
+
+
+@pytest.mark.parametrize("name,K,seed", [("C1", 8, 0), ("C2", 24, 1), ("C3", 256, 0), ("C3tight", 40, 2)])
+def test_att_bwd_tc_matches_dmma_and_oracle(name, K, seed):
+    """The attention backward on tcgen05 (att_tc.cu, debug mode 6): digit-plane
+    dq = ds proj, A = alpha^T du, G = ds^T H against the DMMA kernel (1e-12)
+    and the whole gradient against the oracle on weighted samples (1e-9)."""
+    gg, topo, params, feats, pol = _setup(name, seed)
+    w = np.random.default_rng(seed).normal(size=K) * 10.0 ** np.random.default_rng(seed + 1).uniform(-3, 3, K)
+    g_tc = _grad(params, feats, K, seed + 5, w, 6)
+    g_dm = _grad(params, feats, K, seed + 5, w, 1)
+    assert _relnorm(g_tc, g_dm) <= AB_RTOL
+    wo = _weights(K, _picks(K, 2), seed=5)
+    g = _grad(params, feats, K, seed + 5, wo, 6)
+    _, _, pl, _ = _sampled(params, feats, K, seed + 5)
+    assert _relnorm(g, _oracle_sum(pol, pl, wo)) <= GRAD_RTOL
