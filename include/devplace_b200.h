@@ -119,6 +119,11 @@ int dp_policy_encode(dp_policy *p, const double *params, void *stream);
  * (may be NULL). */
 int dp_debug_phase_clocks(int32_t enable, int64_t *h_out);
 
+/* Debug instrumentation: the decoder's per-warp phase-end arrival cycles
+ * (block 0, from each phase's start, summed over steps; phase clocks must be
+ * enabled) into h_out[8 * 3], warp-major; read and reset. */
+int dp_debug_warp_clocks(int64_t *h_out);
+
 /* Debug instrumentation: LSTM-backward phase clocks (block 0) into h_out[8]. */
 int dp_debug_lstm_clocks(int32_t enable, int64_t *h_out);
 
@@ -134,8 +139,15 @@ int dp_debug_fastmath_error(int64_t n, uint64_t *h_max_ulps);
 
 /* Decoder variant override (tests / measurement): 0 = automatic plan,
  * 1 = force the speculative next-step cell (idle warps evaluate the LSTM
- * cell for every possible choice during the draw), 2 = forbid it. */
+ * cell for every possible choice during the draw), 2 = forbid it, 4 = the
+ * FAST decoder with its gate mat-vec h W_h on tcgen05 (int8 digit planes of
+ * W_h resident in TMEM; measured slower at C3, so opt-in). */
 int dp_debug_decoder_variant(int32_t mode);
+
+/* Debug (tests): the decoder plan for a batch of K samples on this engine:
+ * out[6] = {samples per CTA, kernel sample slots, tensor-core gates (0/1),
+ * shared-memory bytes, speculative cell (0/1), operands in shared memory (0/1)}. */
+int dp_debug_decoder_plan(const dp_policy *p, int32_t K, int32_t *out);
 
 /* Debug (tests): free the optional backward stores of an engine so small
  * batches run the code paths a C5-sized batch takes.  mask bit 0 = attention

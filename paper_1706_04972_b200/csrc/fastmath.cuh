@@ -14,11 +14,11 @@
 
 namespace dp {
 
-// 2^k for integer-valued k, clamped: k <= -1023 -> 0, k >= 1024 -> +inf
-// (integer clamp: fp64 fmin/fmax cost ~6 instructions each here)
-__device__ __forceinline__ double fm_pow2(double k) {
-    const int ki = min(max(__double2int_rn(k), -1023), 1024);
-    return __hiloint2double((ki + 1023) << 20, 0);
+// 2^k for integer k, clamped: k <= -1023 -> 0, k >= 1024 -> +inf (integer
+// clamp: fp64 fmin/fmax cost ~25 cycles each here)
+__device__ __forceinline__ double fm_pow2i(int k) {
+    k = min(max(k, -1023), 1024);
+    return __hiloint2double((k + 1023) << 20, 0);
 }
 
 // expm1 on the reduced argument |r| <= ln2/2: r + r^2 (1/2! + r/3! + ... + r^11/13!)
@@ -40,15 +40,23 @@ __device__ __forceinline__ double fm_expm1_poly(double r) {
     return fma(r2, q, r);
 }
 
-__device__ __forceinline__ void fm_reduce(double y, double &k, double &r) {
+// y = k ln2 + r, |r| <= ln2/2 (+ rounding), k integer.  k comes from the
+// magic-number rounding t = fma(y, log2 e, 1.5 2^52): the integer sits in the
+// low mantissa bits of t (|y log2 e| << 2^51), so k = t - 1.5 2^52 and its
+// int32 value is t's low word — no FRND / F2I on the chain (~26 cycles each,
+// scripts/lat_probe2.cu).
+__device__ __forceinline__ void fm_reduce(double y, double &k, double &r, int &ki) {
     constexpr double kL2E = 1.4426950408889634;
     constexpr double kLn2Hi = 6.93147180559945286227e-01;  // ln2 rounded to double
     constexpr double kLn2Lo = 2.31904681384629955842e-17;  // ln2 - kLn2Hi
+    constexpr double kRnd = 6755399441055744.0;            // 1.5 * 2^52
     // clamp to [-1000, 1000] with fmin/fmax's NaN rule (NaN -> -1000) as two
     // compare-selects: saturates exp to 0 / inf, expm1 to -1 / inf; keeps r sane
     y = !(y >= -1000.0) ? -1000.0 : y;
     y = y > 1000.0 ? 1000.0 : y;
-    k = rint(y * kL2E);
+    const double t = fma(y, kL2E, kRnd);
+    k = t - kRnd;
+    ki = __double2loint(t);
     r = fma(-k, kLn2Hi, y);
     r = fma(-k, kLn2Lo, r);
 }
@@ -56,18 +64,20 @@ __device__ __forceinline__ void fm_reduce(double y, double &k, double &r) {
 // expm1(y) = 2^k (p + 1) - 1 = 2^k p + (2^k - 1)
 __device__ __forceinline__ double fm_expm1(double y) {
     double k, r;
-    fm_reduce(y, k, r);
+    int ki;
+    fm_reduce(y, k, r, ki);
     const double p = fm_expm1_poly(r);
-    const double s = fm_pow2(k);
+    const double s = fm_pow2i(ki);
     return fma(s, p, s - 1.0);
 }
 
 // exp(y) = 2^k (1 + p)
 __device__ __forceinline__ double fm_exp(double y) {
     double k, r;
-    fm_reduce(y, k, r);
+    int ki;
+    fm_reduce(y, k, r, ki);
     const double p = fm_expm1_poly(r);
-    const double s = fm_pow2(k);
+    const double s = fm_pow2i(ki);
     return fma(s, p, s);
 }
 

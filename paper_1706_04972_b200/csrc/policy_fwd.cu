@@ -32,6 +32,7 @@
 #include "fastmath.cuh"
 #include "pcg64.cuh"
 #include "policy.cuh"
+#include "tc.cuh"
 
 namespace dp {
 
@@ -53,6 +54,8 @@ __device__ __forceinline__ double tanh_x(double x) { return gate_act(x, true); }
 // Debug-only per-phase cycle counters of the decoder (block 0, thread 0).
 __device__ int g_dbg_clocks = 0;
 __device__ long long g_phase_clk[16];
+__device__ long long g_warp_clk[8 * 3];
+// debug: per-warp phase-end arrival (block 0), summed over steps (g_warp_clk above)
 __device__ int g_dbg_skip = 0;  // debug-only ablation bits (timing experiments; results invalid when set)
 
 // numpy pairwise_sum order for n <= 128 (np.add.reduce on a contiguous array):
@@ -300,6 +303,7 @@ __global__ void dec_prep_kernel(PolicyDims dm, const double *__restrict__ params
 constexpr int kProjLd = 66;
 constexpr int kWout1Ld = kH + 8;  // W_out[:64]^T row stride (== 8 mod 16 doubles: 8-lane groups in distinct banks)  // proj row stride in shared memory: 16-byte rows, conflict-free LDS.128
 constexpr int kWarps = kThreads / 32;
+static_assert(kWarps == 8, "g_warp_clk is sized for 8 warps");
 
 // sum_w fw[w] p[w * stride] over the 8 warp partials as a tree (depth 4)
 __device__ __forceinline__ double wsum8(const double *p, int stride, const double (&fw)[kWarps]) {
@@ -332,6 +336,7 @@ struct DecArgs {
     // shared-memory offsets (doubles)
     int o_proj, o_encw, o_wout, o_devt, o_bout, o_edev, o_h, o_uh, o_alpha, o_pm, o_ps, o_puc, o_pz, o_gn, o_hc,
         o_cc, o_ac, o_pcg, o_misc, o_v, o_wo, o_rn, o_fin;
+    int o_bdig, o_tmb;  // TCG: h digit-plane stacks (B operands), mbarrier + TMEM base
 };
 
 // q = x / n for 0 <= x < MT * n without an integer division (MT <= 8)
@@ -372,28 +377,43 @@ __device__ __forceinline__ double warp_sum(double v) {
 // the generic alternatives are compiled out, so the per-step loop's hot code
 // is compact (the draw chain measurably stalls on instruction fetch when it
 // jumps across the cold paths).
-// FAST: the draw warp leaves step s's (zsc, esum, gmx, gsum, p) in fin and its
-// choice in prev; a pcg warp writes the row's global cache entries a step later
-__device__ __forceinline__ void fin_store(const DecArgs &a, const double *fin, const int *prev, int k0, int m, int M,
-                                          int T, int s) {
+// FAST: the draw warp leaves step s's (esum, gmx, gsum, zs[D], ez[D]) in fin
+// and its choice in prev; a pcg warp finishes the row one step later, off the
+// draw chain: the probabilities p = ez / esum, the row's global cache entries,
+// and the sampling margin min_j<D-1 |r - cdf_j| with cdf = cumsum(p) (the
+// reference's searchsorted(cumsum(p), r), pkg/policy.py:320-323) against the
+// step's uniform r (still in rnext: the caller runs this before the pcg step
+// that overwrites it).
+__device__ __forceinline__ void fin_store(const DecArgs &a, double *fin, const int *prev, const double *rnext,
+                                          int k0, int m, int M, int T, int s) {
     if (k0 + m >= a.K) return;
+    const int D = a.dm.D;
     const size_t row = (size_t)(k0 + m) * T + s;
     const int ch = prev[(((s & 1) ^ 1) * M) + m];
-    const double *f = fin + ((s & 1) * M + m) * 8;
-    for (int d = 0; d < a.dm.D; d++) {
-        a.act_p[row * a.dm.D + d] = f[4 + d];
-        if (a.probs_out) a.probs_out[row * a.dm.D + d] = f[4 + d];
+    const double *f = fin + ((s & 1) * M + m) * 16;
+    const double esum = f[0];
+    const double y = fm_rcp(esum);
+    const double r = rnext[(s & 1) * M + m];
+    double cdf = 0.0, mg = INFINITY;
+    for (int d = 0; d < D; d++) {
+        const double p = fm_div_y(f[8 + d], esum, y);
+        a.act_p[row * D + d] = p;
+        if (a.probs_out) a.probs_out[row * D + d] = p;
+        cdf += p;
+        if (d < D - 1) mg = fmin(mg, fabs(r - cdf));
     }
     a.choice[row] = (uint8_t)ch;
     if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
-    a.act_lz[row * 2] = f[0];
-    a.act_lz[row * 2 + 1] = f[1];
-    a.act_stat[row * 2] = f[2];  // softmax stats (max, sum) for the backward's recompute of alpha
-    a.act_stat[row * 2 + 1] = f[3];
+    a.act_lz[row * 2] = f[4 + ch];
+    a.act_lz[row * 2 + 1] = esum;
+    a.act_stat[row * 2] = f[1];  // softmax stats (max, sum) for the backward's recompute of alpha
+    a.act_stat[row * 2 + 1] = f[2];
+    if (!a.forced) fin[32 * M + m] = fmin(fin[32 * M + m], mg);
 }
 
-template <int MT, bool PS, bool SPEC, bool FAST = false>
+template <int MT, bool PS, bool SPEC, bool FAST = false, bool TCG = false>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
+    static_assert(!TCG || (FAST && PS && !SPEC && MT <= 2), "TCG is a FAST-path variant");
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const PolicyDims &dm = a.dm;
@@ -422,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     unsigned long long *pcg = reinterpret_cast<unsigned long long *>(sm + a.o_pcg);  // [M][2]
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);  // [2][M] previous choice, by step parity
     double *rnext = sm + a.o_rn;  // [2][M] the step's uniform, by step parity (pcg warps)
-    double *fin = sm + a.o_fin;   // FAST: [2][M][8] (zsc, esum, gmx, gsum, p[4]) of the step, by parity
+    double *fin = sm + a.o_fin;   // FAST: [2][M][16] (esum, gmx, gsum, -, zs[4], ez[4]) of the step, by parity; [M] margins
     // pcg warps: with 3 Mb <= 8 warps, warp 2 Mb + m steps sample m's PCG64 stream
     // during E and leaves the next step's uniform in rnext (off the draw chain)
     const bool pcgw = FAST || 3 * Mb <= kWarps;
@@ -432,7 +452,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 
     // ---- stage the snapshot-constant operands ----
     if (PS) {
-        for (int i = tid; i < T * kH; i += kThreads) sm[a.o_proj + (i >> 6) * kProjLd + (i & 63)] = a.proj[i];
+        if (!TCG)  // TCG: each thread keeps its proj row in registers instead
+            for (int i = tid; i < T * kH; i += kThreads) sm[a.o_proj + (i >> 6) * kProjLd + (i & 63)] = a.proj[i];
         // transposed: encWT[j][i], row stride a.ewld (== 2 mod 32 words apart per j:
         // conflict-free LDS.128 for 8 consecutive j)
         for (int i = tid; i < T * dd; i += kThreads) sm[a.o_encw + (i % dd) * a.ewld + i / dd] = a.encW[i];
@@ -452,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // both parity halves, all M slots: the per-sample loops compute unguarded
     // (branch-free, so the samples' chains interleave) and only the stores check Mb
     if (tid < 2 * M) prev[tid] = SPEC ? 0 : D;  // SPEC: step 0's state lives in candidate slot 0
+    if (FAST && tid < M) fin[32 * M + tid] = INFINITY;  // running sampling margins
     if (tid < Mb) {
         if (!a.forced) {
             const long long kg = a.k_offset + k0 + tid;
@@ -467,11 +489,74 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
     }
     const int u = tid >> 2, gate = tid & 3, col = gate * kH + u;
+    // w: this thread's W_h gate column (the next step's g = h W_h on the fp64 pipe);
+    // TCG: this thread's proj row instead (row tid), and h W_h runs on the tensor
+    // cores with W_h's digit planes resident in TMEM (below)
     double w[kH];
-    {
+    if (TCG) {
+        const double *pr = a.proj + (size_t)(tid < T ? tid : T - 1) * kH;
+#pragma unroll
+        for (int k = 0; k < kH; k++) w[k] = pr[k];
+    } else {
         const double *Wh = P + dm.off.w_dec + (size_t)dd * kG;
 #pragma unroll
         for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
+    }
+    // TCG (tensor-core gates): g = h W_h as fp64-exact int8 digit-plane products
+    // (tc.cuh) on tcgen05.mma kind::i8.  A = W_h^T digit planes in TMEM, resident
+    // for the whole decode: thread tid writes ITS gate column col into TMEM lane
+    // tid % 128 of tile tid / 128 (per (tile, 32-deep k step, plane a): 8 columns
+    // of 4 bytes) — exactly the lane quarter its warp may access, so in phase A
+    // every thread reads its own column's accumulators back.  B = the step's h
+    // digit planes, one stack per k step of 8-row blocks (block b = plane b, row
+    // m = sample m, blocks 6.. zero): A plane a multiplies the window starting at
+    // block 5 - a, so accumulator block j collects diagonal 5 + j of every plane
+    // pair (24 MMAs, M=128, N=48, K=32 per step, issued by two idle warps in E;
+    // the dropped pairs a + b < 5 are below 2^-45 of max|W| per term, tc.cuh).
+    uint64_t *tmbar = reinterpret_cast<uint64_t *>(sm + a.o_tmb);
+    uint32_t *tmslot = reinterpret_cast<uint32_t *>(sm + a.o_tmb + 1);
+    uint8_t *bdig = reinterpret_cast<uint8_t *>(sm + a.o_bdig);
+    uint32_t tm = 0;
+    double gsc = 0.0;  // TCG: 2^(40 - s_col - 46), this column's digit scale
+    constexpr uint32_t kTmA = 0, kTmD = 192, kTmCols = 512;  // A planes [0, 192), accumulators [192, 288)
+    constexpr int kBStack = 11 * 256;                          // bytes per k step: 6 planes + 5 zero blocks
+    if (TCG) {
+        for (int i = tid; i < 2 * kBStack / 8; i += kThreads) sm[a.o_bdig + i] = 0.0;
+        if (warp == 0) tc::tmem_alloc(tmslot, kTmCols);
+        if (tid == 0) {
+            tc::mbar_init(tmbar, 2);
+            tc::fence_mbar_init();
+        }
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        tm = *tmslot;
+        const double *Wh = P + dm.off.w_dec + (size_t)dd * kG + col;
+        int eb = 0;
+        for (int k = 0; k < kH; k++) eb = max(eb, (__double2hiint(Wh[(size_t)k * kG]) >> 20) & 0x7FF);
+        const int sh = tc::fix_shift(eb);
+        const double scale = tc::pow2(sh);
+        gsc = tc::pow2(40 - sh - tc::kFixBits);
+        const uint32_t lane_base = tm + ((uint32_t)((warp & 3) * 32) << 16) + kTmA + (uint32_t)(tid >> 7) * 96;
+#pragma unroll 1
+        for (int ks = 0; ks < 2; ks++) {
+            uint32_t pw[6][8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+#pragma unroll
+                for (int b = 0; b < 6; b++) pw[b][c] = 0;
+#pragma unroll
+                for (int by = 0; by < 4; by++) {
+                    const unsigned long long d6 = tc::digits6(Wh[(size_t)(ks * 32 + 4 * c + by) * kG], scale);
+#pragma unroll
+                    for (int b = 0; b < 6; b++) pw[b][c] |= (uint32_t)((d6 >> (8 * b)) & 0xFF) << (8 * by);
+                }
+            }
+#pragma unroll
+            for (int b = 0; b < 6; b++) tc::tmem_st8(lane_base + (uint32_t)(ks * 6 + b) * 8, pw[b]);
+        }
+        tc::tmem_st_wait();
+        tc::fence_before();
     }
     const double c_init = a.enc_c[(size_t)(T - 1) * kH + u];
     double cst[MT];  // (non-SPEC) cell state of unit u, sample m: owned by lane m of the quad (MT <= 4), else gate 0
@@ -482,7 +567,19 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // g = h W_h for the first step (identical initial state for every sample)
     double gn[MT];
     {
-        const double g0 = dot64_sh_reg(h0, w);
+        double g0;
+        if (TCG) {
+            // step 0 on the fp64 pipe (identical for every sample)
+            const double *Wh = P + dm.off.w_dec + (size_t)dd * kG + col;
+            double q0 = 0.0, q1 = 0.0;
+            for (int k = 0; k < kH; k += 2) {
+                q0 = fma(h0[k], Wh[(size_t)k * kG], q0);
+                q1 = fma(h0[k + 1], Wh[(size_t)(k + 1) * kG], q1);
+            }
+            g0 = q0 + q1;
+        } else {
+            g0 = dot64_sh_reg(h0, w);
+        }
 #pragma unroll
         for (int m = 0; m < MT; m++) gn[m] = g0;
         if (SPEC) {
@@ -520,6 +617,13 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         clk_last = now_;                                  \
     }
     const int skip = g_dbg_skip;  // debug ablation bits (dp_debug_phase_clocks), read once
+    // debug: each warp's arrival at the phase-ending barrier, from the phase start
+    const bool wclk = g_dbg_clocks && blockIdx.x == 0 && lane == 0;
+    long long wst = wclk ? clock64() : 0, wacc[3] = {0, 0, 0};
+#define DP_WEND(i) \
+    if (wclk) wacc[i] += clock64() - wst;
+#define DP_WSTART() \
+    if (wclk) wst = clock64();
     // running row pointers of the step's cached activations (sample m at + m * T rows)
     const size_t sG = (size_t)T * kG, sH = (size_t)T * kH;
     double *actg = a.act_g + (size_t)k0 * sG + col;
@@ -533,8 +637,30 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             // every sample slot computes (no branches between the chains); stores check Mb
             double act[MT], cn[MT], hn[MT];
             double hkeep = 0.0, ckeep = 0.0;  // (MT <= 4) this lane's sample: cached after the barrier
+            if (TCG && t > 0 && !(skip & 32)) {
+                // this column's h_{t-1} W_h from the MMAs issued in the previous E: block j
+                // of the accumulator holds diagonal 5 + j for sample m at column 8 j + m;
+                // sum_j acc_j 256^(5 + j) in two exact int64 thirds (|acc| < 6 * 64 * 2^14)
+                tc::mbar_wait(tmbar, (uint32_t)((t - 1) & 1));
+                tc::fence_after();
+                const uint32_t lb = tm + ((uint32_t)((warp & 3) * 32) << 16) + kTmD + (uint32_t)(tid >> 7) * 48;
+                uint32_t acc[6][2];
 #pragma unroll
-            for (int m = 0; m < MT; m++) act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
+                for (int j = 0; j < 6; j++) tc::tmem_ld2(lb + 8 * j, acc[j]);
+                tc::tmem_ld_wait();
+                tc::fence_before();
+#pragma unroll
+                for (int m = 0; m < MT; m++) {
+                    const long long lo = (long long)(int)acc[0][m] + ((long long)(int)acc[1][m] << 8) +
+                                         ((long long)(int)acc[2][m] << 16);
+                    const long long hi = (long long)(int)acc[3][m] + ((long long)(int)acc[4][m] << 8) +
+                                         ((long long)(int)acc[5][m] << 16);
+                    gn[m] = fma((double)hi, 16777216.0, (double)lo) * gsc;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                act[m] = gate_act(edev[prv[m] * kG + col] + gn[m], gate == 3);
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) actg[m * sG] = act[m];
@@ -566,6 +692,16 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     }
                 hkeep = hq;
                 ckeep = cq;
+                if (TCG && gate < MT && t + 1 < T && !(skip & 64)) {
+                    // sample gate's h[u] -> its 6 digits (|h| < 1: fixed scale 2^46),
+                    // plane b into block b, row gate, k = u of the k step's stack
+                    const unsigned long long d6 = tc::digits6(hq, 70368744177664.0);  // 2^46
+                    const int k = u & 31;
+                    uint8_t *bq = bdig + (u >> 5) * kBStack + (k >> 4) * 128 + gate * 16 + (k & 15);
+#pragma unroll
+                    for (int b = 0; b < 6; b++) bq[b * 256] = (uint8_t)(d6 >> (8 * b));
+                    tc::fence_async_smem();
+                }
             } else {
 #pragma unroll
                 for (int m = 0; m < MT; m++) hn[m] = act[m] * tanh_x(cn[m]);
@@ -578,7 +714,25 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                         actc[m * sH] = cn[m];
                     }
             }
+            DP_WEND(0);
             __syncthreads();
+            DP_WSTART();
+            if (TCG && warp >= 6 && lane == 0 && t + 1 < T && !(skip & 32)) {
+                // the next step's h_t W_h: warp 6 + tl issues tile tl's 12 MMAs right after
+                // phase A (measured: issued in E they slow the draw warps' shared-memory loads)
+                tc::fence_after();
+                constexpr uint32_t idesc = tc::idesc_i8_k(128, 48);
+                const int tl = warp - 6;
+                const uint32_t b0 = tc::smem_u32(bdig);
+#pragma unroll
+                for (int ks = 0; ks < 2; ks++)
+#pragma unroll
+                    for (int aa = 0; aa < 6; aa++)
+                        tc::mma_i8_ta(tm + kTmD + 48 * tl, tm + kTmA + tl * 96 + (ks * 6 + aa) * 8,
+                                      tc::smem_desc(b0 + ks * kBStack + (5 - aa) * 256, 128, 256), idesc,
+                                      (ks | aa) ? 1u : 0u);
+                tc::mma_commit(tmbar);
+            }
             if (MT <= 4 && gate < Mb) {
                 // the step's h / c cache rows after the barrier (off A's tail)
                 acth[gate * sH] = hkeep;
@@ -654,6 +808,31 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 for (int i = tid; i < T; i += kThreads)
 #pragma unroll
                     for (int m = 0; m < MT; m++) lmx[m] = fmax(lmx[m], alS[m * a.Tpad + i]);
+        } else if (TCG) {
+            // scores only: this thread's proj row is in registers (w), h is broadcast
+            // from shared memory; the next step's h W_h is on the tensor cores
+            double s0[MT], s1[MT], s2[MT], s3[MT];
+#pragma unroll
+            for (int m = 0; m < MT; m++) s0[m] = s1[m] = s2[m] = s3[m] = 0.0;
+#pragma unroll
+            for (int j2 = 0; j2 < kH / 2; j2 += 2) {
+#pragma unroll
+                for (int m = 0; m < MT; m++) {
+                    const double2 h0 = reinterpret_cast<const double2 *>(hcur[m])[j2];
+                    const double2 h1 = reinterpret_cast<const double2 *>(hcur[m])[j2 + 1];
+                    s0[m] = fma(w[2 * j2], h0.x, s0[m]);
+                    s1[m] = fma(w[2 * j2 + 1], h0.y, s1[m]);
+                    s2[m] = fma(w[2 * j2 + 2], h1.x, s2[m]);
+                    s3[m] = fma(w[2 * j2 + 3], h1.y, s3[m]);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < MT; m++)
+                if (m < Mb && tid < T) {
+                    const double sv = (s0[m] + s1[m]) + (s2[m] + s3[m]);
+                    alS[m * a.Tpad + tid] = sv;
+                    lmx[m] = sv;
+                }
         } else {
             // fused pass: this thread's first score row and its gate column of the
             // next step's h W_h share every h load (W_h indices stay compile-time)
@@ -911,7 +1090,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 if (ok && (idx & 7) == 0) uhS[m * 32 + o] = part;
             }
         }
+        DP_WEND(1);
         __syncthreads();
+        DP_WSTART();
         DP_PHASE(1);
         // ---- E: combine, logits, softmax over devices, draw (policy.py:297-308, 320-323) ----
         // warp m < Mb runs sample m's draw chain; when there are spare warps, warp
@@ -1014,21 +1195,61 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             }
             double zmax = z;
 #pragma unroll
-            for (int o = FAST ? 2 : 16; o > 0; o >>= 1)  // FAST: D <= 4, lanes >= D hold -inf
-                if (FAST || o < d_pow2) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+            for (int o = FAST ? 2 : 16; o > 0; o >>= 1) {  // FAST: D <= 4, lanes >= D hold -inf
+                const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
+                // FAST: compare-select (~12 cycles) in place of fmax (~25); z is finite
+                if (FAST) zmax = oz > zmax ? oz : zmax;
+                else if (o < d_pow2) zmax = fmax(zmax, oz);
+            }
             const double zs = z - zmax;
             const double ezv = fm_exp(lane < D ? zs : -1000.0);
             const double ez = lane < D ? ezv : 0.0;
+            if (FAST) {
+                // the draw itself, nothing else on the chain: the cumulative sums of the
+                // 4 exponentials in numpy's order (cumsum / pairwise_sum with n < 8 are
+                // sequential; lanes >= D add exact zeros, so P[3] == esum) against r * esum
+                // — searchsorted(cumsum(ez / esum), r, 'right') without the division.
+                // p = ez / esum, the margin and the row's global stores are the pcg
+                // warp's, one step later (fin_store).  The decision agrees with the
+                // reference's whenever the margin recorded there exceeds
+                // SAMPLING_MARGIN_TOL (cumsum(p) and P / esum differ by a few ulp).
+                double P[4];
+                P[0] = __shfl_sync(0xffffffffu, ez, 0);
+#pragma unroll
+                for (int dv = 1; dv < 4; dv++) P[dv] = P[dv - 1] + __shfl_sync(0xffffffffu, ez, dv);
+                const double esum = P[3];
+                int ch;
+                if (a.forced) {
+                    ch = a.forced[row];
+                } else {
+                    const double rs = r * esum;
+                    int cnt = 0;
+#pragma unroll
+                    for (int dv = 0; dv < 3; dv++) cnt += (dv < D - 1 && P[dv] <= rs) ? 1 : 0;
+                    ch = cnt;
+                }
+                double *f = fin + (par * M + m) * 16;
+                if (lane == 0) prev[(par ^ 1) * M + m] = ch;
+                if (lane < D) {
+                    f[4 + lane] = zs;
+                    f[8 + lane] = ez;
+                }
+                if (lane == 0) {
+                    f[0] = esum;
+                    f[1] = gmx;
+                    f[2] = gsum;
+                }
+                continue;
+            }
             // numpy pairwise order over the D terms (np_sum_small), identical in every lane
             double esum;
-            if (FAST || D < 8) {
-                constexpr int DG = FAST ? 4 : 8;  // lanes gathered
-                double ev[DG];
+            if (D < 8) {
+                double ev[8];
 #pragma unroll
-                for (int dv = 0; dv < DG; dv++) ev[dv] = __shfl_sync(0xffffffffu, ez, dv);
+                for (int dv = 0; dv < 8; dv++) ev[dv] = __shfl_sync(0xffffffffu, ez, dv);
                 esum = 0.0;
 #pragma unroll
-                for (int dv = 0; dv < DG; dv++)
+                for (int dv = 0; dv < 8; dv++)
                     if (dv < D) esum += ev[dv];
             } else {
                 double rr[8];
@@ -1043,9 +1264,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 for (; i < D; i++) esum += __shfl_sync(0xffffffffu, ez, i);
             }
             const double pr = fm_div(ez, esum);
-            if (FAST) {
-                if (lane < D) fin[(par * M + m) * 8 + 4 + lane] = pr;  // stored by the pcg warp
-            } else if (lane < D) {
+            if (lane < D) {
                 a.act_p[row * D + lane] = pr;
                 if (a.probs_out) a.probs_out[row * D + lane] = pr;
             }
@@ -1058,13 +1277,12 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 // margin: distance of the uniform to every cdf boundary that can
                 // change the choice (j < D-1; the last one is clamped away)
                 const bool wm = a.margin != nullptr;
-                if (FAST || D <= 8) {
-                    constexpr int DG = FAST ? 4 : 8;  // lanes gathered
-                    double pv[DG];
+                if (D <= 8) {
+                    double pv[8];
 #pragma unroll
-                    for (int dv = 0; dv < DG; dv++) pv[dv] = __shfl_sync(0xffffffffu, pr, dv);
+                    for (int dv = 0; dv < 8; dv++) pv[dv] = __shfl_sync(0xffffffffu, pr, dv);
 #pragma unroll
-                    for (int dv = 0; dv < DG; dv++)
+                    for (int dv = 0; dv < 8; dv++)
                         if (dv < D) {
                             cdf += pv[dv];
                             cnt += (cdf <= r) ? 1 : 0;
@@ -1087,22 +1305,13 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     pcg[2 * m + 1] = rs.lo;
                 }
                 prev[(par ^ 1) * M + m] = ch;
-                if (FAST) {
-                    // the row's global stores are issued by the pcg warp one step on
-                    double *f = fin + (par * M + m) * 8;
-                    f[0] = zsc;
-                    f[1] = esum;
-                    f[2] = gmx;
-                    f[3] = gsum;
-                } else {
-                    a.choice[row] = (uint8_t)ch;
-                    if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
-                    a.act_lz[row * 2] = zsc;
-                    a.act_lz[row * 2 + 1] = esum;
-                    // softmax stats (max, sum) for the backward's recompute of alpha
-                    a.act_stat[row * 2] = gmx;
-                    a.act_stat[row * 2 + 1] = gsum;
-                }
+                a.choice[row] = (uint8_t)ch;
+                if (a.choice_out) a.choice_out[row] = (uint8_t)ch;
+                a.act_lz[row * 2] = zsc;
+                a.act_lz[row * 2 + 1] = esum;
+                // softmax stats (max, sum) for the backward's recompute of alpha
+                a.act_stat[row * 2] = gmx;
+                a.act_stat[row * 2 + 1] = gsum;
             }
         }
         if (split && warp >= Mb && warp < 2 * Mb) {
@@ -1154,13 +1363,14 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
         if (pcgw && warp >= 2 * Mb && warp < 3 * Mb && lane == 0) {
             const int m = warp - 2 * Mb;
+            // the previous step's row (reads that step's uniform before it is overwritten)
+            if (FAST && t > 0) fin_store(a, fin, prev, rnext, k0, m, M, T, t - 1);
             if (!a.forced) {
                 const u128 ns = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
                 pcg[2 * m] = ns.hi;
                 pcg[2 * m + 1] = ns.lo;
                 rnext[(par ^ 1) * M + m] = pcg_double(ns);
             }
-            if (FAST && t > 0) fin_store(a, fin, prev, k0, m, M, T, t - 1);  // the previous step's row
         }
         if (SPEC && warp >= Mb && t + 1 < T) {
             // next step's LSTM cell for every possible choice d (the idle warps)
@@ -1190,13 +1400,27 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         if (!SPEC) {
             // gn for the non-speculative A of the next step is already in registers
         }
+        DP_WEND(2);
         __syncthreads();
+        DP_WSTART();
         DP_PHASE(2);
     }
 #undef DP_PHASE
-    if (FAST && tid < Mb && T > 0) fin_store(a, fin, prev, k0, tid, M, T, T - 1);  // the last step's row
-    if (a.margin && !a.forced && warp < Mb && lane == 0) a.margin[k0 + warp] = mrun;
+#undef DP_WEND
+#undef DP_WSTART
+    if (wclk)
+#pragma unroll
+        for (int i = 0; i < 3; i++) g_warp_clk[warp * 3 + i] += wacc[i];
+    if (FAST && tid < Mb && T > 0) {
+        fin_store(a, fin, prev, rnext, k0, tid, M, T, T - 1);  // the last step's row
+        if (a.margin && !a.forced) a.margin[k0 + tid] = fin[32 * M + tid];
+    }
+    if (!FAST && a.margin && !a.forced && warp < Mb && lane == 0) a.margin[k0 + warp] = mrun;
     __syncthreads();  // the log-prob pass below reads those rows from other threads
+    if (TCG && warp == 0) {
+        tc::fence_after();
+        tc::tmem_dealloc(tm, kTmCols);
+    }
     if (clk_on)
 #pragma unroll
         for (int i = 0; i < 3; i++) g_phase_clk[i] += clk_acc[i];
@@ -1418,7 +1642,7 @@ extern "C" int64_t dp_policy_num_params(const dp_policy *p) { return p ? p->dims
 static int g_dec_variant = 0;  // dp_debug_decoder_variant
 extern "C" int dp_debug_decoder_variant(int32_t mode) {
     DP_ENTRY();
-    DP_REQUIRE(mode >= 0 && mode <= 2, "dp_debug_decoder_variant: mode must be 0, 1 or 2");
+    DP_REQUIRE(mode >= 0 && mode <= 4, "dp_debug_decoder_variant: mode must be 0..4");
     g_dec_variant = mode;
     return DP_OK;
 }
@@ -1461,6 +1685,17 @@ extern "C" int dp_debug_phase_clocks(int32_t enable, int64_t *h_out) {
     return DP_OK;
 }
 
+// Debug: read and reset the decoder's per-warp phase-end arrival sums (block 0,
+// cycles from the phase start summed over steps) into h_out[8 * 3] (warp-major).
+extern "C" int dp_debug_warp_clocks(int64_t *h_out) {
+    DP_ENTRY();
+    DP_REQUIRE(h_out, "dp_debug_warp_clocks: NULL argument");
+    DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_warp_clk, sizeof(long long) * kWarps * 3));
+    long long z[kWarps * 3] = {0};
+    DP_CUDA_TRY(cudaMemcpyToSymbol(g_warp_clk, z, sizeof(z)));
+    return DP_OK;
+}
+
 extern "C" int dp_policy_read_inputs(const dp_policy *p, double *out, void *stream) {
     DP_ENTRY();
     DP_REQUIRE(p && out, "dp_policy_read_inputs: NULL argument");
@@ -1488,7 +1723,7 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
 
 namespace {
 struct DecPlan {
-    int M, MT, enc_in_smem, spec, Tpad;
+    int M, MT, enc_in_smem, spec, tcg, Tpad;
     size_t smem;
     DecArgs proto;
 };
@@ -1509,6 +1744,12 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             const int enc_smem = variant < 2, spec = (variant % 2 == 0) && MT <= 4 && variant_mode == 1;
             if (variant % 2 == 0 && !spec) continue;
             DecArgs &a = pl.proto;
+            // tensor-core gates (TCG) on the FAST path: opt-in (mode 4).  Measured at C3
+            // (M=2, per-step phase clocks, same run): fp64 gates A 1321 / C 3989 / E 1914
+            // cycles; TCG A 1830 / C 3414 / E 2078 — the scores-only pass saves 1.1K cycles
+            // in C but the MMAs' operand traffic (+550 in C), the accumulator read-back
+            // (+250 in A) and the digit stores (+140 in A) give it back
+            const int tcg = enc_smem && !spec && MT <= 2 && D <= 4 && dd <= 16 && T <= kThreads && variant_mode == 4;
             // score rows [M][Tpad] with Tpad == 4 (mod 16) doubles: the DM path's
             // fragment loads (8 samples x 4 rows) hit distinct banks
             const int Tpad = ((T + 11) & ~15) + 4;
@@ -1518,7 +1759,7 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
                 o += (n + 1) & ~1;
                 return r;
             };
-            a.o_proj = enc_smem ? take(T * kProjLd) : 0;
+            a.o_proj = enc_smem && !tcg ? take(T * kProjLd) : 0;
             a.ewld = ((T + 1) & ~1) + 2;
             a.o_encw = enc_smem ? take(a.ewld * dd) : 0;
             a.o_wout = take(kWout1Ld * dd);
@@ -1539,15 +1780,23 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + 2 * M);
             a.o_rn = take(2 * M);
-            a.o_fin = take(16 * M);
+            a.o_fin = take(33 * M);  // FAST: [2][M][16] step records + [M] running sampling margins
             a.o_v = take(kH * D);
             a.o_wo = take(kH * dd);
+            if (tcg) {
+                o = (o + 15) & ~15;  // 128-byte aligned B operands
+                a.o_bdig = take(2 * 11 * 256 / 8);
+                a.o_tmb = take(2);
+            } else {
+                a.o_bdig = a.o_tmb = 0;
+            }
             const size_t bytes = (size_t)o * sizeof(double);
             if (bytes <= budget) {
                 pl.M = M;
                 pl.MT = MT;
                 pl.enc_in_smem = enc_smem;
                 pl.spec = spec;
+                pl.tcg = tcg;
                 pl.Tpad = Tpad;
                 pl.smem = bytes;
                 return true;
@@ -1559,7 +1808,12 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
 }
 
 template <bool PS, bool SPEC>
-const void *dec_fn(int MT, bool fast) {
+const void *dec_fn(int MT, bool fast, bool tcg) {
+    if constexpr (PS && !SPEC) {
+        if (fast && tcg)
+            return MT == 1 ? (const void *)dec_kernel<1, PS, false, true, true>
+                           : (const void *)dec_kernel<2, PS, false, true, true>;
+    }
     if (PS && !SPEC && fast) return MT == 1 ? (const void *)dec_kernel<1, PS, false, true>
                                             : (const void *)dec_kernel<2, PS, false, true>;
     if (SPEC)
@@ -1572,6 +1826,24 @@ const void *dec_fn(int MT, bool fast) {
                      : (const void *)dec_kernel<8, PS, false>;
 }
 }  // namespace
+
+// Debug / tests: the decoder plan for a batch of K on this engine:
+// out[6] = {samples per CTA, kernel MT, tensor-core gates, shared-memory bytes,
+// speculative cell, operands in shared memory}.
+extern "C" int dp_debug_decoder_plan(const dp_policy *p, int32_t K, int32_t *out) {
+    DP_ENTRY();
+    DP_REQUIRE(p && out && K >= 1, "dp_debug_decoder_plan: bad arguments");
+    DecPlan pl;
+    DP_REQUIRE(plan_decoder(p->dims, K, g_dec_variant, pl), "dp_debug_decoder_plan: shared-memory plan failed");
+    const bool fast = pl.MT <= 2 && p->dims.D <= 4 && p->dims.dd <= 16 && p->dims.T <= kThreads;
+    out[0] = pl.M;
+    out[1] = pl.MT;
+    out[2] = pl.tcg && fast && pl.enc_in_smem && !pl.spec;
+    out[3] = (int32_t)pl.smem;
+    out[4] = pl.spec;
+    out[5] = pl.enc_in_smem;
+    return DP_OK;
+}
 
 extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, int64_t k_offset,
                                 const uint64_t *h_pcg, uint64_t draw_base, const int64_t *draw_counter,
@@ -1629,8 +1901,9 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     const int grid = ceil_div(K, pl.M);
     cudaStream_t st = (cudaStream_t)stream;
     const bool fast = pl.MT <= 2 && dm.D <= 4 && dm.dd <= 16 && dm.T <= kThreads;
-    const void *fn = pl.enc_in_smem ? (pl.spec ? dec_fn<true, true>(pl.MT, false) : dec_fn<true, false>(pl.MT, fast))
-                                    : (pl.spec ? dec_fn<false, true>(pl.MT, false) : dec_fn<false, false>(pl.MT, false));
+    const void *fn = pl.enc_in_smem
+                         ? (pl.spec ? dec_fn<true, true>(pl.MT, false, false) : dec_fn<true, false>(pl.MT, fast, pl.tcg))
+                         : (pl.spec ? dec_fn<false, true>(pl.MT, false, false) : dec_fn<false, false>(pl.MT, false, false));
     DP_CUDA_TRY(allow_big_smem(fn, pl.smem));
     void *args[] = {&a};
     DP_CUDA_TRY(cudaLaunchKernel(fn, dim3(grid), dim3(kThreads), args, pl.smem, st));

@@ -307,3 +307,52 @@ def test_dropin_encoder_cache_follows_parameter_changes():
     s = P.forward_sample(params, feats, rng)
     opl, olp, _ = pol.sample(orng)
     assert s.placement == opl and s.log_prob == pytest.approx(olp, rel=LP_RTOL)
+
+
+def _decoder_plan(eng, K):
+    import ctypes
+
+    from paper_1706_04972_b200 import _native as nat
+
+    out = (ctypes.c_int32 * 6)()
+    nat.check(nat.lib().dp_debug_decoder_plan(eng.handle, K, out), "plan")
+    return dict(zip(["M", "MT", "tcg", "smem", "spec", "enc_in_smem"], list(out)))
+
+
+@pytest.mark.parametrize("name,K", [("C3", 256), ("C1", 100), ("C1", 290)])
+def test_tensor_core_gates_decoder(name, K):
+    """The opt-in FAST decoder with its gate mat-vec h W_h on tcgen05 (int8
+    digit planes of W_h resident in TMEM, csrc/policy_fwd.cu TCG,
+    dp_debug_decoder_variant(4)) against the default fp64-pipe mat-vec:
+    identical placements, log-probs within 1e-12, per-step probabilities within
+    1e-13, weighted gradients within 1e-10; and the oracle's placements /
+    log-probs for the first samples."""
+    from paper_1706_04972_b200 import _native as nat
+
+    gg, topo, params, feats = _setup(name, seed=4)
+    eng = P.engine_for(params, feats, K)
+    assert _decoder_plan(eng, K)["tcg"] == 0
+    pl3, lp3 = P.sample_batch(params, feats, np.random.default_rng(21), K)
+    w = np.linspace(-1.0, 1.0, 8)
+    g3 = P.weighted_grad(params, feats, [list(map(int, p)) for p in pl3[:8]], w).cpu().numpy()
+    pr3 = P.step_distributions(params, feats, list(map(int, pl3[0])))
+    nat.check(nat.lib().dp_debug_decoder_variant(4), "variant")
+    try:
+        plan = _decoder_plan(eng, K)
+        assert plan["tcg"] == 1 and plan["MT"] <= 2, plan
+        pl, lp = P.sample_batch(params, feats, np.random.default_rng(21), K)
+        g = P.weighted_grad(params, feats, [list(map(int, p)) for p in pl[:8]], w).cpu().numpy()
+        pr = P.step_distributions(params, feats, list(map(int, pl[0])))
+    finally:
+        nat.check(nat.lib().dp_debug_decoder_variant(0), "variant")
+    assert np.array_equal(pl, pl3)
+    np.testing.assert_allclose(lp, lp3, rtol=LP_RTOL, atol=0)
+    assert _relnorm(g, g3) <= 1e-10
+    assert np.max(np.abs(pr - pr3)) <= 1e-13
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    rng = np.random.default_rng(21)
+    for k in range(4):
+        opl, olp, _ = pol.sample(rng)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
