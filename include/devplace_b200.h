@@ -277,6 +277,12 @@ int dp_argmin_feasible(int32_t K, const double *makespan, const uint8_t *feasibl
  *   log_rows[log_cap*8] (out): row `update` = (update, controller, version,
  *   mean_R, baseline, best_R, n_feasible, n_used); version is filled by
  *   dp_adam_apply. */
+/* Sampling certificate (reference draw pkg/policy.py:320-323):
+ * margin_min[0] = min(margin_min[0], min_k margin[k]) and n_below[0] += #{k :
+ * margin[k] < tol} over the per-sample margins of one dp_policy_decode. */
+int dp_margin_accumulate(int32_t K, const double *margin, double tol, double *margin_min, int64_t *n_below,
+                         void *stream);
+
 int dp_reinforce_epilogue(int32_t K, int32_t T, const double *makespan, const uint8_t *feasible,
                           const uint8_t *choice, int32_t choice_div, double failing, double decay,
                           int64_t success_only_after,

@@ -37,6 +37,7 @@ SIGNATURES = {
     "dp_debug_warp_clocks": (I32, [P]),
     "dp_debug_decoder_variant": (I32, [I32]),
     "dp_debug_decoder_plan": (I32, [P, I32, P]),
+    "dp_margin_accumulate": (I32, [I32, P, ctypes.c_double, P, P, P]),
     "dp_debug_policy_drop_stores": (I32, [P, I32]),
     "dp_debug_tensor_core": (I32, [I32]),
     "dp_group_features": (I32, [I32, I32, P, P, I32, P, P, I32, P, P, P, I32, I32, P, P, P, P, P, P, P, P]),

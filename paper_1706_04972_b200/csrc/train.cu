@@ -292,10 +292,53 @@ __global__ void exchange_unpack_kernel(int K_local, int T, const uint8_t *__rest
     for (int t = threadIdx.x; t < T; t += blockDim.x) rows[(size_t)r * T + t] = rec[exch_row_off(K_local) + t];
 }
 
+// Sampling certificate of one decode: running minimum of the
+// per-sample margins and the count of samples below tol, in one launch.
+__global__ void margin_accumulate_kernel(int K, const double *__restrict__ margin, double tol,
+                                         double *__restrict__ margin_min, long long *__restrict__ n_below) {
+    __shared__ double smin[32];
+    __shared__ int scnt[32];
+    double mn = INFINITY;
+    int cnt = 0;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const double m = margin[k];
+        mn = fmin(mn, m);
+        cnt += m < tol ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        smin[w] = mn;
+        scnt[w] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < nw; i++) {
+            mn = fmin(mn, smin[i]);
+            cnt += scnt[i];
+        }
+        margin_min[0] = fmin(margin_min[0], mn);
+        n_below[0] += cnt;
+    }
+}
+
 }  // namespace
 }  // namespace dp
 
 using namespace dp;
+
+extern "C" int dp_margin_accumulate(int32_t K, const double *margin, double tol, double *margin_min,
+                                    int64_t *n_below, void *stream) {
+    DP_ENTRY();
+    DP_REQUIRE(K >= 1 && margin && margin_min && n_below, "dp_margin_accumulate: bad argument");
+    margin_accumulate_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(K, margin, tol, margin_min,
+                                                                  (long long *)n_below);
+    DP_LAUNCH_CHECK();
+    return DP_OK;
+}
 
 extern "C" int64_t dp_exchange_record_bytes(int32_t K_local, int32_t T) { return exch_bytes(K_local, T); }
 

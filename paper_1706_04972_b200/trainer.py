@@ -453,14 +453,15 @@ class DeviceController:
         self.eng.decode(p, self.K_local, pcg=self.pcg, draw_base=0, k_offset=self.k_offset,
                         draw_counter=state.view(torch.int64)[3:4], draws_per_count=self.K * self.T,
                         choice=self.choice, logp=self.logp, margin=self.margin, stream=stream)
-        with torch.cuda.stream(main):
-            torch.minimum(self.margin_min, self.margin.amin(0, keepdim=True), out=self.margin_min)
-            self.n_uncertified += (self.margin < policy_mod.SAMPLING_MARGIN_TOL).sum()
         mark("simulate")
         # the advantage-independent half of the backward runs on a side stream
         # while the placements are scored
         self.side.wait_stream(main)
         self.eng.backward_rows(p, self.K_local, stream=self.side)
+        # sampling certificate, off the rows pass's path
+        nat.check(nat.lib().dp_margin_accumulate(self.K_local, nat.ptr(self.margin), policy_mod.SAMPLING_MARGIN_TOL,
+                                                 nat.ptr(self.margin_min), nat.ptr(self.n_uncertified),
+                                                 nat.stream_ptr(stream)), "dp_margin_accumulate")
         self.sim_local = self.dg.simulate(self.choice, by_rank=True, stream=stream, out=self.sim_local)
         mk, fe = self.sim_local["makespan"], self.sim_local["feasible"]
         if not self.measure_ok:
