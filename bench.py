@@ -586,6 +586,10 @@ def main():
     import paper_1706_04972_b200 as dp
     from paper_1706_04972_b200 import _native as nat
 
+    # measurement A/B only: DP_DECODER_VARIANT=4 runs the opt-in tensor-core-gate decoder
+    if os.environ.get("DP_DECODER_VARIANT"):
+        nat.check(nat.lib().dp_debug_decoder_variant(int(os.environ["DP_DECODER_VARIANT"])), "variant")
+
     # C4 = the mixed batch: the C1 and C2 tasks (own parameters, stores, RNG
     # streams) advanced together, K=512 each
     names = ["C1", "C2"] if args.config == "C4" else [args.config]
