@@ -33,6 +33,7 @@
 #include <math.h>
 
 #include "fastmath.cuh"
+#include "cpasync.cuh"
 #include "policy.cuh"
 
 namespace dp {
@@ -57,22 +58,6 @@ constexpr int kFusedGrads = 3;  // B1f in the fused pass: grads only, rows alrea
 constexpr int kFinTile = 64;
 constexpr int kChunk = 64;  // B1: enc rows per chunk
 constexpr int kPad = 65;
-
-// 16-byte global -> shared async copy (LDGSTS); valid == false zero-fills.
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc, bool valid) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-    const int n = valid ? 16 : 0;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gsrc), "r"(n) : "memory");
-}
-// 8-byte variant (L1-allocating .ca; 8 is a legal .ca size, .cg takes only 16)
-__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gsrc, bool valid) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-    const int n = valid ? 8 : 0;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(n) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 __device__ int g_att_dbg = 0;             // debug-only phase clocks of att_bwd (block 0, thread 0)
 __device__ long long g_att_clk[8];

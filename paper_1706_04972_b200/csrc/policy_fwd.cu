@@ -29,6 +29,7 @@
 
 #include <vector>
 
+#include "cpasync.cuh"
 #include "fastmath.cuh"
 #include "pcg64.cuh"
 #include "policy.cuh"
@@ -304,6 +305,10 @@ constexpr int kProjLd = 66;
 constexpr int kWout1Ld = kH + 8;  // W_out[:64]^T row stride (== 8 mod 16 doubles: 8-lane groups in distinct banks)  // proj row stride in shared memory: 16-byte rows, conflict-free LDS.128
 constexpr int kWarps = kThreads / 32;
 static_assert(kWarps == 8, "g_warp_clk is sized for 8 warps");
+// DM streaming (C5-sized T, noshift): per-warp cp.async ring of 8-row blocks of
+// proj (row stride 68 doubles) and encW (row stride 18): conflict-free DMMA
+// fragment loads; 3 slots per warp, aliased onto the score rows alS
+constexpr int kDmsPR = 68, kDmsER = 18, kDmsSlot = 8 * kDmsPR + 8 * kDmsER, kDmsSlots = 3;
 
 // sum_w fw[w] p[w * stride] over the 8 warp partials as a tree (depth 4)
 __device__ __forceinline__ double wsum8(const double *p, int stride, const double (&fw)[kWarps]) {
@@ -474,6 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // (branch-free, so the samples' chains interleave) and only the stores check Mb
     if (tid < 2 * M) prev[tid] = SPEC ? 0 : D;  // SPEC: step 0's state lives in candidate slot 0
     if (FAST && tid < M) fin[32 * M + tid] = INFINITY;  // running sampling margins
+    if (MT == 8 && !PS && !SPEC && (dd & 1) == 0)  // DM streaming ring (aliases alS): zero pads
+        for (int i = tid; i < kWarps * kDmsSlots * kDmsSlot; i += kThreads) alS[i] = 0.0;
     if (tid < Mb) {
         if (!a.forced) {
             const long long kg = a.k_offset + k0 + tid;
@@ -768,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         // the scores are fp64 tensor-core tiles, S[i][m] = proj[i] . h[m] with
         // the 8 samples exactly the DMMA n extent; proj streams from L2
         constexpr bool DM = MT == 8 && !PS && !SPEC;
+        const bool dms = DM && noshift && (dd % 2 == 0);  // DM streaming (one pass over T, below)
         if (DM) {
             // next step's gate column g = h W_h (W_h column in registers)
             double g0[MT], g1[MT];
@@ -791,8 +799,87 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
             for (int ks = 0; ks < kH / 4; ks++) bf[ks] = hS[fg * kH + 4 * ks + ft];
             const int nblk = (T + 7) >> 3;
+            if (dms) {
+                // streaming (shift-free softmax): each warp owns row blocks warp + 8 k;
+                // their proj / encW rows arrive through a 3-slot cp.async ring (two
+                // blocks in flight), and per block one warp forms S^T = h proj^T (DMMA,
+                // M = the 8 samples, A = h from registers), e = exp(S) in place, the
+                // uc partial += e encW (DMMA, A = e straight from the score fragments:
+                // k step e' covers rows 2 t + e') and the softmax partial sum — no
+                // score rows in shared memory, no barrier, no second pass over T
+                double *ring = alS + warp * kDmsSlots * kDmsSlot;
+                const int nk = warp < nblk ? (nblk - 1 - warp) / kWarps + 1 : 0;
+                const int hd = dd >> 1;  // 16-byte chunks per encW row (<= 8)
+                // lane copies 16-byte chunk `lane` of the block's 8 proj rows and
+                // chunks (lane, lane + 32) of its 8 x hd encW chunks (row = idx / 8)
+                const int er0 = lane >> 3, ec = lane & 7;
+                auto stage = [&](int k, int slot) {
+                    if (k < nk) {
+                        const int b = warp + k * kWarps;
+                        double *sp = ring + slot * kDmsSlot, *se = sp + 8 * kDmsPR;
+                        const double *gp = proj + (size_t)(8 * b) * kH + 2 * lane;
+#pragma unroll
+                        for (int r = 0; r < 8; r++)
+                            cp_async16(sp + r * kDmsPR + 2 * lane, gp + (8 * b + r < T ? r * kH : 0), 8 * b + r < T);
+#pragma unroll
+                        for (int h2 = 0; h2 < 2; h2++) {
+                            const int r = er0 + 4 * h2, row = 8 * b + r;
+                            if (ec < hd)
+                                cp_async16(se + r * kDmsER + 2 * ec, encW + (size_t)(row < T ? row : 0) * dd + 2 * ec,
+                                           row < T);
+                        }
+                    }
+                    cp_async_commit();
+                };
+                stage(0, 0);
+                stage(1, 1);
+                double ua[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // uc[sample fg][8 n + 2 ft + e]
+                double es = 0.0;                             // sum of e[sample fg] over this lane's rows
+                for (int k = 0; k < nk; k++) {
+                    stage(k + 2, (k + 2) % kDmsSlots);
+                    cp_async_wait<2>();
+                    __syncwarp();
+                    const double *sp = ring + (k % kDmsSlots) * kDmsSlot, *se = sp + 8 * kDmsPR;
+                    const int b = warp + k * kWarps;
+                    // four independent accumulator chains (k steps q mod 4)
+                    double a4[4][2];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) a4[q][0] = a4[q][1] = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < kH / 4; ks++) dmma_f64(a4[ks & 3], bf[ks], sp[fg * kDmsPR + 4 * ks + ft]);
+                    double acc[2];
+#pragma unroll
+                    for (int e = 0; e < 2; e++) acc[e] = (a4[0][e] + a4[1][e]) + (a4[2][e] + a4[3][e]);
+                    double ev[2];
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const int i = 8 * b + 2 * ft + e;
+                        ev[e] = i < T ? fm_exp(acc[e]) : 0.0;
+                        es += ev[e];
+                        if (a.act_e && i < T && fg < Mb) a.act_e[((size_t)(k0 + fg) * T + t) * T + i] = ev[e];
+                    }
+#pragma unroll
+                    for (int e = 0; e < 2; e++)
+#pragma unroll
+                        for (int n = 0; n < 2; n++)
+                            if (n * 8 < dd) dmma_f64(ua[n], ev[e], se[(2 * ft + e) * kDmsER + 8 * n + fg]);
+                    __syncwarp();  // slot k % 3 is restaged at iteration k + 1
+                }
+                cp_async_wait<0>();
+                es += __shfl_xor_sync(0xffffffffu, es, 1);
+                es += __shfl_xor_sync(0xffffffffu, es, 2);
+#pragma unroll
+                for (int m = 0; m < MT; m++) lsm[m] = __shfl_sync(0xffffffffu, es, 4 * m);
+#pragma unroll
+                for (int n = 0; n < 2; n++)
+#pragma unroll
+                    for (int e = 0; e < 2; e++) {
+                        const int j = 8 * n + 2 * ft + e;
+                        if (j < dd && fg < Mb) puc[(warp * M + fg) * dd + j] = ua[n][e];
+                    }
+            }
 #pragma unroll 2
-            for (int blk = warp; blk < nblk; blk += kWarps) {
+            for (int blk = warp; blk < (dms ? 0 : nblk); blk += kWarps) {
                 const int i = blk * 8 + fg;
                 const double *pr = proj + (size_t)(i < T ? i : T - 1) * kH + ft;
                 double acc[2] = {0.0, 0.0};
@@ -803,7 +890,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     alS[(2 * ft + 1) * a.Tpad + i] = acc[1];  // sample 2t + 1
                 }
             }
-            __syncthreads();  // the exp loop reads rows other warps scored
+            if (!dms) __syncthreads();  // the exp loop reads rows other warps scored
             if (!noshift)
                 for (int i = tid; i < T; i += kThreads)
 #pragma unroll
@@ -896,7 +983,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         }
 #pragma unroll
         for (int m = 0; m < MT; m++) lmx[m] = noshift ? 0.0 : warp_max(lmx[m]);
-        for (int i = tid; i < ((skip & 16) ? 0 : T); i += kThreads) {
+        for (int i = tid; i < ((skip & 16) || dms ? 0 : T); i += kThreads) {
             double ev[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++) ev[m] = fm_exp(alS[m * a.Tpad + i] - lmx[m]);
@@ -909,7 +996,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
 #pragma unroll
-        for (int m = 0; m < MT; m++) lsm[m] = ((skip & 8) || (FAST && MT == 2)) ? lsm[m] : warp_sum(lsm[m]);
+        for (int m = 0; m < MT; m++) lsm[m] = ((skip & 8) || (FAST && MT == 2) || dms) ? lsm[m] : warp_sum(lsm[m]);
         __syncwarp();
         // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
         // (lane = (m, j); full 32-row blocks read e and encW^T as 16-byte pairs)
@@ -923,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             double acc[kNtMax][2];
 #pragma unroll
             for (int n = 0; n < kNtMax; n++) acc[n][0] = acc[n][1] = 0.0;
-            for (int ib = warp * 32; ib < ((skip & 1) ? 0 : T); ib += kThreads) {
+            for (int ib = warp * 32; ib < ((skip & 1) || dms ? 0 : T); ib += kThreads) {
 #pragma unroll
                 for (int ks = 0; ks < 8; ks++) {
                     const int i = ib + 4 * ks + ft;
@@ -943,7 +1030,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
                 for (int e = 0; e < 2; e++) {
                     const int j = 8 * n + 2 * ft + e;
-                    if (n < ntl && j < dd && fg < Mb) puc[(warp * M + fg) * dd + j] = acc[n][e];
+                    if (n < ntl && j < dd && fg < Mb && !dms) puc[(warp * M + fg) * dd + j] = acc[n][e];
                 }
         } else if (FAST && MT == 2) {
             // lane (j, half): 16 of the warp's 32 rows for both samples, so each
@@ -1768,7 +1855,8 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             a.o_edev = spec ? 0 : take((D + 1) * kG);
             a.o_h = spec ? 0 : take(M * kH);
             a.o_uh = take(M * 32);
-            a.o_alpha = take(M * (Tpad > kH ? Tpad : kH));
+            a.o_alpha = take(std::max(M * (Tpad > kH ? Tpad : kH),
+                                      MT == 8 && !enc_smem ? kWarps * kDmsSlots * kDmsSlot : 0));
             a.o_pm = take(kWarps * M);
             a.o_ps = take(kWarps * M);
             a.o_puc = take(kWarps * M * dd);
