@@ -601,6 +601,10 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                         for (int n = 0; n < 8; n++) dmma884(sv[n], aq, enc[(n * 8 + g) * kPadH + ks * 4 + t]);
                     }
                 const double m = S.mx[mr], l = S.sm[mr], wv = S.w[mr];
+                // score recompute: alpha = exp(s - max) / sum as branch-free fastmath
+                // exp times one reciprocal per row (libm exp and 16 divisions per lane
+                // serialised the chunk; both within a few ulp, far inside 1e-9)
+                const double rl = STORED ? 0.0 : fm_rcp(l);
 #pragma unroll
                 for (int n = 0; n < 8; n++)
 #pragma unroll
@@ -608,7 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                         const int i = n * 8 + 2 * t + e;
                         double al = 0.0, dsv = 0.0;
                         if (i0 + i < T && rok) {
-                            al = STORED ? ev[n][e] * (n < 4 ? esc0 : esc1) : exp(sv[n][e] - m) / l;
+                            al = STORED ? ev[n][e] * (n < 4 ? esc0 : esc1) : fm_exp(sv[n][e] - m) * rl;
                             dsv = al * (da[n][e] - wv);
                         }
                         S.al[mr * kPadH + i] = al;
