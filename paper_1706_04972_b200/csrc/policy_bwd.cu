@@ -973,6 +973,7 @@ constexpr int kLstmThreads = 256;
 constexpr int kMaxSeqPerCta = kLstmThreads / 64;   // one elementwise slot (sample, unit) per thread
 constexpr int kRpw = kH / (kLstmThreads / 32);     // W_h rows per warp in the mat-vec
 __device__ int g_lstm_dbg = 0;            // debug-only phase clocks of lstm_bwd (block 0, thread 0)
+static bool g_lstm_clocks_on = false;      // host side: launch the CLK instantiations
 __device__ long long g_lstm_clk[2][4];    // [M == 1 ? 0 : 1][phase]
 // Mat-vec mapping: lane j of warp w owns gate columns {j + 32q} (q < 8) of
 // W_h rows 4w..4w+3 (32 weights in registers).  Every lane reads a DIFFERENT
@@ -982,7 +983,9 @@ __device__ long long g_lstm_clk[2][4];    // [M == 1 ? 0 : 1][phase]
 // sums on lanes 0, 8, 16, 24.
 inline size_t lstm_bwd_smem(int M) { return sizeof(double) * (size_t)M * (2 * kH + kG); }
 
-template <int MT>
+// CLK: debug phase clocks compiled in (disabled instrumentation still costs
+// issue slots on this latency-bound chain), launched only while enabled
+template <int MT, bool CLK = false>
 __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     int T, int n_seq, int M, const double *__restrict__ Wh /* [64 x 256] row-major, ld 256 */,
     double *__restrict__ gates /* [seq][T][256] in: i,f,o,g  out: da */, const double *__restrict__ cst /* [seq][T][64] */,
@@ -1062,7 +1065,7 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
     load(T - 2, nxt);
     double tc = fm_gate_act(cur.c, true);  // tanh (branch-free, fastmath.cuh)
 
-    const bool clk_on = g_lstm_dbg && blockIdx.x == 0 && tid == 0;
+    const bool clk_on = CLK && blockIdx.x == 0 && tid == 0;
     const int ci = M == 1 ? 0 : 1;
     long long clk_last = clk_on ? clock64() : 0;
     long long clk_acc[4] = {0, 0, 0, 0};  // in registers; one global write at the end
@@ -1184,6 +1187,10 @@ __global__ void __launch_bounds__(kLstmThreads, 1) lstm_bwd_kernel(
 
 const void *lstm_bwd_fn(int M) {
     static_assert(kMaxSeqPerCta == 4, "lstm_bwd_fn instantiates MT <= 4");
+    if (g_lstm_clocks_on)
+        return M <= 1 ? (const void *)lstm_bwd_kernel<1, true>
+               : M <= 2 ? (const void *)lstm_bwd_kernel<2, true>
+                        : (const void *)lstm_bwd_kernel<4, true>;
     return M <= 1 ? (const void *)lstm_bwd_kernel<1>
            : M <= 2 ? (const void *)lstm_bwd_kernel<2>
                     : (const void *)lstm_bwd_kernel<4>;
@@ -1597,6 +1604,7 @@ extern "C" int dp_debug_lstm_clocks(int32_t enable, int64_t *h_out) {
     DP_ENTRY();
     const int on = enable ? 1 : 0;
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_lstm_dbg, &on, sizeof(int)));
+    g_lstm_clocks_on = on != 0;
     if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_lstm_clk, sizeof(long long) * 8));
     long long z[8] = {0};
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_lstm_clk, z, sizeof(z)));
@@ -1794,7 +1802,13 @@ int run_b345(dp_policy *p, const double *params, int K, const double *adv, doubl
         // encoder backward: reads the gate activations from enc_g, writes da to
         // da_enc, and sums the decoders' step-0 state gradients in its prologue
         const size_t smem = lstm_bwd_smem(1);
-        lstm_bwd_kernel<1><<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
+        if (g_lstm_clocks_on)
+            lstm_bwd_kernel<1, true><<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
+                                                   p->enc_c, p->zeros, p->d_enc, nullptr, nullptr,
+                                                   dhc_sum + 2 * kH, dhc_sum + 3 * kH, p->enc_g, p->dh0, p->dc0, adv,
+                                                   K, nullptr);
+        else
+            lstm_bwd_kernel<1><<<1, kLstmThreads, smem, ss>>>(T, 1, 1, params + dm.off.w_enc + (size_t)dm.F * kG, p->da_enc,
                                                    p->enc_c, p->zeros, p->d_enc, nullptr, nullptr,
                                                    dhc_sum + 2 * kH, dhc_sum + 3 * kH, p->enc_g, p->dh0, p->dc0, adv,
                                                    K, nullptr);

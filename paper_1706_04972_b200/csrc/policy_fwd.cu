@@ -167,6 +167,9 @@ __device__ __forceinline__ double dot64_sh_reg(const double *__restrict__ hs, co
 // 4-lane reduce-scatter that leaves gate q's full pre-activation in lane q
 // (= the gate column col = q*64 + u), activation, 4-lane shuffle to the
 // unit's owner, c/h update, one barrier.
+// CLK: debug phase clocks compiled in (a separate instantiation: disabled
+// instrumentation still costs issue slots on this latency-bound chain)
+template <bool CLK>
 __global__ void __launch_bounds__(kThreads, 1)
     enc_rec_kernel(PolicyDims dm, const double *__restrict__ params, const double *__restrict__ XP,
                    double *__restrict__ enc_h, double *__restrict__ enc_c, double *__restrict__ enc_g) {
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     const int base = lane & ~3;
     const bool hi = gate & 2, lo = gate & 1;
-    const bool clk_on = g_dbg_clocks && tid == 0;  // debug phase clocks -> g_phase_clk[4..7]
+    const bool clk_on = CLK && tid == 0;  // debug phase clocks -> g_phase_clk[4..7]
     long long ck[4] = {0, 0, 0, 0}, c_last = clk_on ? clock64() : 0;
 #define DP_ENC_PHASE(i)                      \
     if (clk_on) {                            \
@@ -416,7 +419,7 @@ __device__ __forceinline__ void fin_store(const DecArgs &a, double *fin, const i
     if (!a.forced) fin[32 * M + m] = fmin(fin[32 * M + m], mg);
 }
 
-template <int MT, bool PS, bool SPEC, bool FAST = false, bool TCG = false>
+template <int MT, bool PS, bool SPEC, bool FAST = false, bool TCG = false, bool CLK = false>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     static_assert(!TCG || (FAST && PS && !SPEC && MT <= 2), "TCG is a FAST-path variant");
     extern __shared__ __align__(16) double sm[];
@@ -612,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     int d_pow2 = 1;
     while (d_pow2 < D) d_pow2 <<= 1;
     // debug phase clocks (dp_debug_phase_clocks): block 0, thread 0, after each barrier
-    const bool clk_on = g_dbg_clocks && blockIdx.x == 0 && tid == 0;
+    const bool clk_on = CLK && blockIdx.x == 0 && tid == 0;
     long long clk_last = clk_on ? clock64() : 0;
     long long clk_acc[3] = {0, 0, 0};  // in registers; one global write at the end
     // draw warp m (< Mb <= 8 warps) keeps sample m's running sampling margin
@@ -625,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     }
     const int skip = g_dbg_skip;  // debug ablation bits (dp_debug_phase_clocks), read once
     // debug: each warp's arrival at the phase-ending barrier, from the phase start
-    const bool wclk = g_dbg_clocks && blockIdx.x == 0 && lane == 0;
+    const bool wclk = CLK && blockIdx.x == 0 && lane == 0;
     long long wst = wclk ? clock64() : 0, wacc[3] = {0, 0, 0};
 #define DP_WEND(i) \
     if (wclk) wacc[i] += clock64() - wst;
@@ -1727,6 +1730,7 @@ extern "C" int64_t dp_policy_num_params(const dp_policy *p) { return p ? p->dims
 // Debug: enable (1) / disable (0) decoder phase clocks, then read and reset
 // the 8 per-phase cycle sums (block 0) into h_out[8].  Synchronous.
 static int g_dec_variant = 0;  // dp_debug_decoder_variant
+static bool g_clocks_on = false;  // dp_debug_phase_clocks: launch the CLK instantiations
 extern "C" int dp_debug_decoder_variant(int32_t mode) {
     DP_ENTRY();
     DP_REQUIRE(mode >= 0 && mode <= 4, "dp_debug_decoder_variant: mode must be 0..4");
@@ -1766,6 +1770,7 @@ extern "C" int dp_debug_phase_clocks(int32_t enable, int64_t *h_out) {
         DP_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_skip, &skip, sizeof(int)));
     }
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_dbg_clocks, &on, sizeof(int)));
+    g_clocks_on = on != 0;
     if (h_out) DP_CUDA_TRY(cudaMemcpyFromSymbol(h_out, g_phase_clk, sizeof(long long) * 16));
     long long z[16] = {0};
     DP_CUDA_TRY(cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z)));
@@ -1800,7 +1805,10 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
     enc_prologue_kernel<<<dm.T + dm.D + 1, kG, 0, st>>>(dm, params, p->type_off, p->type_idx, p->shape, p->adj, p->X,
                                                        p->XP, p->edev);
     DP_LAUNCH_CHECK();
-    enc_rec_kernel<<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
+    if (g_clocks_on)
+        enc_rec_kernel<true><<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
+    else
+        enc_rec_kernel<false><<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
     DP_LAUNCH_CHECK();
     DP_CUDA_TRY(cudaMemsetAsync(p->proj_nmax, 0, sizeof(unsigned long long), st));
     dec_prep_kernel<<<dm.T, 128, 0, st>>>(dm, params, p->enc_h, p->proj, p->encW, p->proj_nmax, p->vdev);
@@ -1899,11 +1907,19 @@ template <bool PS, bool SPEC>
 const void *dec_fn(int MT, bool fast, bool tcg) {
     if constexpr (PS && !SPEC) {
         if (fast && tcg)
-            return MT == 1 ? (const void *)dec_kernel<1, PS, false, true, true>
-                           : (const void *)dec_kernel<2, PS, false, true, true>;
+            return g_clocks_on ? (MT == 1 ? (const void *)dec_kernel<1, PS, false, true, true, true>
+                                          : (const void *)dec_kernel<2, PS, false, true, true, true>)
+                               : (MT == 1 ? (const void *)dec_kernel<1, PS, false, true, true>
+                                          : (const void *)dec_kernel<2, PS, false, true, true>);
+        if (fast)
+            return g_clocks_on ? (MT == 1 ? (const void *)dec_kernel<1, PS, false, true, false, true>
+                                          : (const void *)dec_kernel<2, PS, false, true, false, true>)
+                               : (MT == 1 ? (const void *)dec_kernel<1, PS, false, true>
+                                          : (const void *)dec_kernel<2, PS, false, true>);
     }
-    if (PS && !SPEC && fast) return MT == 1 ? (const void *)dec_kernel<1, PS, false, true>
-                                            : (const void *)dec_kernel<2, PS, false, true>;
+    if constexpr (!PS && !SPEC) {
+        if (MT == 8 && g_clocks_on) return (const void *)dec_kernel<8, PS, false, false, false, true>;
+    }
     if (SPEC)
         return MT == 1 ? (const void *)dec_kernel<1, PS, SPEC>
                : MT == 2 ? (const void *)dec_kernel<2, PS, SPEC>
