@@ -15,13 +15,20 @@ for k in dec_kernel att_bwd_kernel lstm_bwd_kernel sim_warp_kernel row_prep_kern
 done
 python scripts/ncu_summary.py $TAG "${reps[@]}" > $OUT/ncu_summary.log 2>&1
 cp profiles/${TAG}_ncu_summary.json profiles/${TAG}_ncu_summary.md $OUT/
+# C5 decoder (DM streaming path) at its bench size, one launch
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:dec_kernel -c 1 -o $OUT/prof_c5_dec \
+    python bench.py --config C5 --steps 1 --warmup 3 --skip-cpu > $OUT/ncu_c5_dec.log 2>&1
+python scripts/ncu_summary.py ${TAG}_C5 $OUT/prof_c5_dec.ncu-rep > $OUT/ncu_summary_c5.log 2>&1
+cp profiles/${TAG}_C5_ncu_summary.json profiles/${TAG}_C5_ncu_summary.md $OUT/ 2>/dev/null
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/${TAG}_launches_C3.csv \
     python bench.py --steps 2 --warmup 3 --skip-cpu > /dev/null 2>&1
 python scripts/launch_summary.py $OUT/${TAG}_launches_C3.csv seq > $OUT/${TAG}_launch_summary.txt
 python scripts/dec_phases.py C3 256 > $OUT/${TAG}_decoder_phase_clocks.txt
+python scripts/dec_phases.py C5 4096 > $OUT/${TAG}_C5_decoder_phase_clocks.txt
 python scripts/lstm_phases.py C3 256 > $OUT/${TAG}_lstm_bwd_phase_clocks.txt
 python scripts/enc_phases.py C3 > $OUT/${TAG}_encoder_phase_clocks.txt
 timeout 900 python bench.py > $OUT/${TAG}_bench_C3_1gpu.json 2> $OUT/bench_C3.err
+bash scripts/launch_list.sh 60 "--config C5" > /dev/null 2>&1; python scripts/launch_summary.py $OUT/launches.csv seq > $OUT/${TAG}_launch_summary_C5.txt
 timeout 900 python bench.py --config C4 > $OUT/${TAG}_bench_C4_1gpu.json 2> $OUT/bench_C4.err
 timeout 900 python bench.py --config C5 > $OUT/${TAG}_bench_C5_1gpu.json 2> $OUT/bench_C5.err
 timeout 900 python bench.py --impl reference > $OUT/${TAG}_bench_reference_C3.json 2> $OUT/bench_ref.err
