@@ -309,9 +309,15 @@ constexpr int kWout1Ld = kH + 8;  // W_out[:64]^T row stride (== 8 mod 16 double
 constexpr int kWarps = kThreads / 32;
 static_assert(kWarps == 8, "g_warp_clk is sized for 8 warps");
 // DM streaming (C5-sized T, noshift): per-warp cp.async ring of 8-row blocks of
-// proj (row stride 68 doubles) and encW (row stride 18): conflict-free DMMA
-// fragment loads; 3 slots per warp, aliased onto the score rows alS
-constexpr int kDmsPR = 68, kDmsER = 18, kDmsSlot = 8 * kDmsPR + 8 * kDmsER, kDmsSlots = 3;
+// proj ([8][64]) and encW ([8][16]), XOR-swizzled by 16-byte chunk so the DMMA
+// fragment loads are conflict-free without padding; 4 slots per warp (two
+// blocks computed while the next two arrive), aliased onto the score rows alS
+constexpr int kDmsSlot = 8 * 64 + 8 * 16, kDmsSlots = 4;
+// word offset of proj element (r, k) / encW element (r, j) inside a slot
+__device__ __forceinline__ int dms_p(int r, int k) { return r * 64 + 2 * ((k >> 1) ^ r) + (k & 1); }
+__device__ __forceinline__ int dms_e(int r, int j) {
+    return 8 * 64 + r * 16 + 2 * ((j >> 1) ^ (((r >> 1) & 1) << 2)) + (j & 1);
+}
 
 // sum_w fw[w] p[w * stride] over the 8 warp partials as a tree (depth 4)
 __device__ __forceinline__ double wsum8(const double *p, int stride, const double (&fw)[kWarps]) {
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     int *prev = reinterpret_cast<int *>(sm + a.o_misc);  // [2][M] previous choice, by step parity
     double *rnext = sm + a.o_rn;  // [2][M] the step's uniform, by step parity (pcg warps)
     double *fin = sm + a.o_fin;   // FAST: [2][M][16] (esum, gmx, gsum, -, zs[4], ez[4]) of the step, by parity; [M] margins
-    // pcg warps: with 3 Mb <= 8 warps, warp 2 Mb + m steps sample m's PCG64 stream
+    // pcg warps: with 3 Mb <= 8 warps, warp 8 - Mb + m steps sample m's PCG64 stream
     // during E and leaves the next step's uniform in rnext (off the draw chain)
     const bool pcgw = FAST || 3 * Mb <= kWarps;
     const double *edev = SPEC ? a.edev : edevS;
@@ -502,12 +508,17 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // w: this thread's W_h gate column (the next step's g = h W_h on the fp64 pipe);
     // TCG: this thread's proj row instead (row tid), and h W_h runs on the tensor
     // cores with W_h's digit planes resident in TMEM (below)
+    // DMK (the large-T DM instantiation): W_h is read from L1/L2 when the gate
+    // column is formed each step (a few hundred cycles of latency on a ~100K-cycle
+    // step), which frees its 128 registers for the streaming score loop
+    constexpr bool DMK = MT == 8 && !PS && !SPEC;
+    const double *Whcol = P + dm.off.w_dec + (size_t)dd * kG + col;
     double w[kH];
     if (TCG) {
         const double *pr = a.proj + (size_t)(tid < T ? tid : T - 1) * kH;
 #pragma unroll
         for (int k = 0; k < kH; k++) w[k] = pr[k];
-    } else {
+    } else if (!DMK) {
         const double *Wh = P + dm.off.w_dec + (size_t)dd * kG;
 #pragma unroll
         for (int k = 0; k < kH; k++) w[k] = Wh[(size_t)k * kG + col];
@@ -578,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     double gn[MT];
     {
         double g0;
-        if (TCG) {
+        if (TCG || DMK) {
             // step 0 on the fp64 pipe (identical for every sample)
             const double *Wh = P + dm.off.w_dec + (size_t)dd * kG + col;
             double q0 = 0.0, q1 = 0.0;
@@ -780,17 +791,18 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         constexpr bool DM = MT == 8 && !PS && !SPEC;
         const bool dms = DM && noshift && (dd % 2 == 0);  // DM streaming (one pass over T, below)
         if (DM) {
-            // next step's gate column g = h W_h (W_h column in registers)
+            // next step's gate column g = h W_h (the W_h column from L1/L2, DMK)
             double g0[MT], g1[MT];
 #pragma unroll
             for (int m = 0; m < MT; m++) g0[m] = g1[m] = 0.0;
-#pragma unroll
+#pragma unroll 8
             for (int j2 = 0; j2 < kH / 2; j2++) {
+                const double w0 = __ldg(Whcol + (size_t)(2 * j2) * kG), w1 = __ldg(Whcol + (size_t)(2 * j2 + 1) * kG);
 #pragma unroll
                 for (int m = 0; m < MT; m++) {
                     const double2 hh = reinterpret_cast<const double2 *>(hcur[m])[j2];
-                    g0[m] = fma(hh.x, w[2 * j2], g0[m]);
-                    g1[m] = fma(hh.y, w[2 * j2 + 1], g1[m]);
+                    g0[m] = fma(hh.x, w0, g0[m]);
+                    g1[m] = fma(hh.y, w1, g1[m]);
                 }
             }
 #pragma unroll
@@ -804,69 +816,75 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             const int nblk = (T + 7) >> 3;
             if (dms) {
                 // streaming (shift-free softmax): each warp owns row blocks warp + 8 k;
-                // their proj / encW rows arrive through a 3-slot cp.async ring (two
-                // blocks in flight), and per block one warp forms S^T = h proj^T (DMMA,
-                // M = the 8 samples, A = h from registers), e = exp(S) in place, the
-                // uc partial += e encW (DMMA, A = e straight from the score fragments:
-                // k step e' covers rows 2 t + e') and the softmax partial sum — no
-                // score rows in shared memory, no barrier, no second pass over T
+                // their proj / encW rows arrive through a 4-slot cp.async ring, two
+                // blocks computed per iteration while the next two land.  Per block the
+                // warp forms S^T = h proj^T (DMMA, M = the 8 samples, A = h from
+                // registers), e = exp(S) in place, the uc partial += e encW (DMMA, A =
+                // e straight from the score fragments: k step e' covers rows 2 t + e')
+                // and the softmax partial sum — no score rows in shared memory, no
+                // barrier, no second pass over T
                 double *ring = alS + warp * kDmsSlots * kDmsSlot;
                 const int nk = warp < nblk ? (nblk - 1 - warp) / kWarps + 1 : 0;
                 const int hd = dd >> 1;  // 16-byte chunks per encW row (<= 8)
-                // lane copies 16-byte chunk `lane` of the block's 8 proj rows and
-                // chunks (lane, lane + 32) of its 8 x hd encW chunks (row = idx / 8)
                 const int er0 = lane >> 3, ec = lane & 7;
-                auto stage = [&](int k, int slot) {
+                auto stage = [&](int k) {
                     if (k < nk) {
                         const int b = warp + k * kWarps;
-                        double *sp = ring + slot * kDmsSlot, *se = sp + 8 * kDmsPR;
+                        double *sl = ring + (k & 3) * kDmsSlot;
                         const double *gp = proj + (size_t)(8 * b) * kH + 2 * lane;
 #pragma unroll
                         for (int r = 0; r < 8; r++)
-                            cp_async16(sp + r * kDmsPR + 2 * lane, gp + (8 * b + r < T ? r * kH : 0), 8 * b + r < T);
+                            cp_async16(sl + dms_p(r, 2 * lane), gp + (8 * b + r < T ? r * kH : 0), 8 * b + r < T);
 #pragma unroll
                         for (int h2 = 0; h2 < 2; h2++) {
                             const int r = er0 + 4 * h2, row = 8 * b + r;
                             if (ec < hd)
-                                cp_async16(se + r * kDmsER + 2 * ec, encW + (size_t)(row < T ? row : 0) * dd + 2 * ec,
+                                cp_async16(sl + dms_e(r, 2 * ec), encW + (size_t)(row < T ? row : 0) * dd + 2 * ec,
                                            row < T);
                         }
                     }
                     cp_async_commit();
                 };
-                stage(0, 0);
-                stage(1, 1);
-                double ua[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // uc[sample fg][8 n + 2 ft + e]
-                double es = 0.0;                             // sum of e[sample fg] over this lane's rows
-                for (int k = 0; k < nk; k++) {
-                    stage(k + 2, (k + 2) % kDmsSlots);
+                stage(0);
+                stage(1);
+                double ua[2][2][2] = {};  // [block parity][n][e]: uc[sample fg][8 n + 2 ft + e]
+                double es = 0.0;          // sum of e[sample fg] over this lane's rows
+                for (int k = 0; k < nk; k += 2) {
+                    stage(k + 2);
+                    stage(k + 3);
                     cp_async_wait<2>();
                     __syncwarp();
-                    const double *sp = ring + (k % kDmsSlots) * kDmsSlot, *se = sp + 8 * kDmsPR;
-                    const int b = warp + k * kWarps;
-                    // four independent accumulator chains (k steps q mod 4)
-                    double a4[4][2];
+                    double a4[2][4][2];
 #pragma unroll
-                    for (int q = 0; q < 4; q++) a4[q][0] = a4[q][1] = 0.0;
+                    for (int bb = 0; bb < 2; bb++)
 #pragma unroll
-                    for (int ks = 0; ks < kH / 4; ks++) dmma_f64(a4[ks & 3], bf[ks], sp[fg * kDmsPR + 4 * ks + ft]);
-                    double acc[2];
+                        for (int q = 0; q < 4; q++) a4[bb][q][0] = a4[bb][q][1] = 0.0;
 #pragma unroll
-                    for (int e = 0; e < 2; e++) acc[e] = (a4[0][e] + a4[1][e]) + (a4[2][e] + a4[3][e]);
-                    double ev[2];
+                    for (int ks = 0; ks < kH / 4; ks++)
 #pragma unroll
-                    for (int e = 0; e < 2; e++) {
-                        const int i = 8 * b + 2 * ft + e;
-                        ev[e] = i < T ? fm_exp(acc[e]) : 0.0;
-                        es += ev[e];
-                        if (a.act_e && i < T && fg < Mb) a.act_e[((size_t)(k0 + fg) * T + t) * T + i] = ev[e];
+                        for (int bb = 0; bb < 2; bb++)
+                            dmma_f64(a4[bb][ks & 3], bf[ks], ring[((k + bb) & 3) * kDmsSlot + dms_p(fg, 4 * ks + ft)]);
+#pragma unroll
+                    for (int bb = 0; bb < 2; bb++) {
+                        const int b = warp + (k + bb) * kWarps;
+                        const double *se = ring + ((k + bb) & 3) * kDmsSlot;
+                        double ev[2];
+#pragma unroll
+                        for (int e = 0; e < 2; e++) {
+                            const int i = 8 * b + 2 * ft + e;
+                            const double sv = (a4[bb][0][e] + a4[bb][1][e]) + (a4[bb][2][e] + a4[bb][3][e]);
+                            ev[e] = (k + bb < nk && i < T) ? fm_exp(sv) : 0.0;
+                            es += ev[e];
+                            if (a.act_e && k + bb < nk && i < T && fg < Mb)
+                                a.act_e[((size_t)(k0 + fg) * T + t) * T + i] = ev[e];
+                        }
+#pragma unroll
+                        for (int e = 0; e < 2; e++)
+#pragma unroll
+                            for (int n = 0; n < 2; n++)
+                                if (n * 8 < dd) dmma_f64(ua[bb][n], ev[e], se[dms_e(2 * ft + e, 8 * n + fg)]);
                     }
-#pragma unroll
-                    for (int e = 0; e < 2; e++)
-#pragma unroll
-                        for (int n = 0; n < 2; n++)
-                            if (n * 8 < dd) dmma_f64(ua[n], ev[e], se[(2 * ft + e) * kDmsER + 8 * n + fg]);
-                    __syncwarp();  // slot k % 3 is restaged at iteration k + 1
+                    __syncwarp();  // slots (k, k + 1) & 3 are restaged next iteration
                 }
                 cp_async_wait<0>();
                 es += __shfl_xor_sync(0xffffffffu, es, 1);
@@ -878,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
                     for (int e = 0; e < 2; e++) {
                         const int j = 8 * n + 2 * ft + e;
-                        if (j < dd && fg < Mb) puc[(warp * M + fg) * dd + j] = ua[n][e];
+                        if (j < dd && fg < Mb) puc[(warp * M + fg) * dd + j] = ua[0][n][e] + ua[1][n][e];
                     }
             }
 #pragma unroll 2
@@ -1451,8 +1469,10 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 a.act_uc[row * dd + lane] = ucn;
             }
         }
-        if (pcgw && warp >= 2 * Mb && warp < 3 * Mb && lane == 0) {
-            const int m = warp - 2 * Mb;
+        // pcg warps: the last Mb warps — on the sub-partitions of the split warps
+        // (warp w issues on SMSP w % 4), not sharing issue slots with the draw warps
+        if (pcgw && warp >= kWarps - Mb && lane == 0) {
+            const int m = warp - (kWarps - Mb);
             // the previous step's row (reads that step's uniform before it is overwritten)
             if (FAST && t > 0) fin_store(a, fin, prev, rnext, k0, m, M, T, t - 1);
             if (!a.forced) {
