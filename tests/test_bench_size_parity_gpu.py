@@ -228,3 +228,27 @@ def test_trainer_reports_sampling_certificate():
     res = dp.train(gg, topo, dp.TrainerConfig(k=64, total_updates=3, seed=2))
     cert = res.sampling
     assert cert["uncertified_samples"] == 0 and cert["min_margin"] > cert["tol"]
+
+
+def test_margin_accumulate_kernel():
+    """dp_margin_accumulate (the trainer's per-update sampling certificate):
+    running minimum of the per-sample margins and the count below tol, over
+    several launches and a K that spans several warps."""
+    import ctypes
+
+    from paper_1706_04972_b200 import _native as nat
+
+    rng = np.random.default_rng(5)
+    mm = torch.full((1,), np.inf, dtype=torch.float64, device="cuda")
+    nb = torch.zeros(1, dtype=torch.int64, device="cuda")
+    want_min, want_n = np.inf, 0
+    for K in (1, 37, 300, 4096):
+        m = rng.uniform(0.0, 1e-8, K) * (rng.random(K) < 0.5) + rng.uniform(1e-6, 1.0, K) * 0.5
+        m[rng.integers(0, K)] = np.inf
+        md = torch.as_tensor(m, device="cuda")
+        nat.check(nat.lib().dp_margin_accumulate(K, nat.ptr(md), ctypes.c_double(1e-7), nat.ptr(mm), nat.ptr(nb),
+                                                 nat.stream_ptr()), "dp_margin_accumulate")
+        want_min = min(want_min, float(np.min(m)))
+        want_n += int(np.sum(m < 1e-7))
+    torch.cuda.synchronize()
+    assert float(mm.item()) == want_min and int(nb.item()) == want_n
