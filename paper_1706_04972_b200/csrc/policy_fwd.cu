@@ -1407,9 +1407,10 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 ch = cnt < D - 1 ? cnt : D - 1;
             }
             const double zsc = __shfl_sync(0xffffffffu, zs, ch);
+            if (!a.forced && !pcgw) __syncwarp();  // every lane's read of pcg[] precedes lane 0's write
             if (lane == 0) {
                 if (!a.forced && !pcgw) {
-                    pcg[2 * m] = rs.hi;  // every lane has read the state by now (the cdf shuffles)
+                    pcg[2 * m] = rs.hi;
                     pcg[2 * m + 1] = rs.lo;
                 }
                 prev[(par ^ 1) * M + m] = ch;
