@@ -668,6 +668,7 @@ __global__ void __launch_bounds__(32 * kSimWarps) sim_warp_kernel(
         } else if (n_heap > 0) {
             // ---- READY (= the reference's final ARRIVAL, pkg/simulator.py:179-184) ----
             const int last = heap[--n_heap];
+            __syncwarp();  // every lane's reads of heap[0] / heap[last] precede lane 0's writes below
             if (n_heap > 0) {
                 const double xt = maxarr[last];
                 int i = 0;
