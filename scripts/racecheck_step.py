@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 from fixtures import cfg  # noqa: E402
 import paper_1706_04972_b200 as dp  # noqa: E402
 
-for name, K in (("C1", 6), ("C3", 4)):
+for name, K in [tuple(x.split(":")) for x in (sys.argv[1:] or ["C1:6", "C3:4"])]:
+    K = int(K)
     gg, topo, _, _ = cfg(name)
     res = dp.train(gg, topo, dp.TrainerConfig(k=K, total_updates=2, seed=3))
     print(name, K, res.log[-1])
