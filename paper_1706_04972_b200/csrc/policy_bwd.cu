@@ -427,6 +427,9 @@ __global__ void __launch_bounds__(kThreads, 1) adv_grads_kernel(PolicyDims dm, i
 
 // ------------------------------------------------------------------ B1
 constexpr int kAttTile = 64;  // rows per tile in att_bwd (2 rows per thread in the S/DA and dq passes)
+// GM prep scratch: uc rows [64][dd] at S.al[0], p rows [64][D] at S.al[kPrepP];
+// W_out[:64]^T [dd4][kPadH] at S.ds[0], dev_table [D][dd] at S.ds[kPrepDev]
+constexpr int kPrepP = kAttTile * kMaxDD, kPrepDev = kMaxDD * 68;
 
 struct AttSmem {
     double enc[2][kChunk * kPadH];  // cp.async double buffer over the T chunks
@@ -468,7 +471,13 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
     double *__restrict__ tile_partial /* [units][T][64] or NULL */,
     double *__restrict__ tile_partA /* [units][T][dd] */, const double *__restrict__ act_e,
     const double *__restrict__ act_esc, int do_denc, int per_sample /* partials per sample, not per tile */,
-    const double *__restrict__ w_att, double *__restrict__ row_dhx /* dh_ext += dq W_att^T (B1f rows part) */) {
+    const double *__restrict__ w_att, double *__restrict__ row_dhx /* dh_ext += dq W_att^T (B1f rows part) */,
+    // GM with prep: the rows pass's per-row half of B0 formed here per tile (no row_prep
+    // launch): dz = onehot(choice) - p, du = dev_table[:D]^T dz (-> row_du_out), w = uc . du,
+    // and dh_out = W_out[:64] du as the initial value of the tile's dh_ext accumulator
+    int prep = 0, const double *__restrict__ P = nullptr, const double *__restrict__ act_p = nullptr,
+    const uint8_t *__restrict__ choice = nullptr, const double *__restrict__ act_uc = nullptr,
+    double *__restrict__ row_du_out = nullptr) {
     extern __shared__ __align__(16) double smraw[];
     AttSmem &S = *reinterpret_cast<AttSmem *>(smraw);
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, g = lane >> 2, t = lane & 3;
@@ -507,17 +516,29 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
             const bool ok = r < nrow;
             cp_async16(&S.q[r * kPadH + j], row_q + (ok ? (size_t)(rb + r) * kH + j : 0), ok);
         }
-        for (int x = tid; x < kAttTile * dd; x += kThreads) {
-            const int r = x / dd;
-            const bool ok = r < nrow;
-            cp_async8(&S.du[r * kDuLd + (x - r * dd)], row_du + (ok ? (size_t)rb * dd + x : 0), ok);
+        if (GM && prep) {
+            // the tile's uc / p rows into scratch (S.al is free until the first chunk's ds)
+            for (int x = tid; x < kAttTile * dd; x += kThreads) {
+                const bool ok = x / dd < nrow;
+                cp_async8(&S.al[x], act_uc + (ok ? (size_t)rb * dd + x : 0), ok);
+            }
+            for (int x = tid; x < kAttTile * dm.D; x += kThreads) {
+                const bool ok = x / dm.D < nrow;
+                cp_async8(&S.al[kPrepP + x], act_p + (ok ? (size_t)rb * dm.D + x : 0), ok);
+            }
+        } else {
+            for (int x = tid; x < kAttTile * dd; x += kThreads) {
+                const int r = x / dd;
+                const bool ok = r < nrow;
+                cp_async8(&S.du[r * kDuLd + (x - r * dd)], row_du + (ok ? (size_t)rb * dd + x : 0), ok);
+            }
         }
         if (tid < kAttTile) {
             const bool ok = tid < nrow;
             const size_t row = ok ? (size_t)(rb + tid) : 0;
             cp_async8(&S.mx[tid], act_stat + row * 2, ok);
             cp_async8(&S.sm[tid], act_stat + row * 2 + 1, ok);
-            cp_async8(&S.w[tid], row_w + row, ok);
+            if (!(GM && prep)) cp_async8(&S.w[tid], row_w + row, ok);
         }
         cp_async_commit();
     };
@@ -580,6 +601,60 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 cp_async_wait<0>();
             }
             __syncthreads();
+            if (GM && prep && ch == 0) {
+                // B0's per-row half for this tile (row_prep_kernel's rows-only outputs)
+                const int D = dm.D;
+                const int dd4p = (dd + 3) & ~3;
+                double *wT = S.ds;               // W_out[:64]^T [o][j], o < dd4p (S.ds is free here)
+                double *dvt = S.ds + kPrepDev;   // dev_table[:D] [d][o]
+                for (int x = tid; x < dd4p * kH; x += kThreads) {
+                    const int o = x >> 6, j = x & 63;
+                    wT[o * kPadH + j] = o < dd ? __ldg(P + dm.off.w_out + (size_t)j * dd + o) : 0.0;
+                }
+                for (int x = tid; x < D * dd; x += kThreads) dvt[x] = __ldg(P + dm.off.dev_table + x);
+                const int rb0 = (tl / tps) * T + (tl % tps) * kAttTile;
+                const int nrow0 = min(kAttTile, T - (tl % tps) * kAttTile);
+                __syncthreads();
+                // du = dev_table[:D]^T dz, dz = onehot(choice) - p (row_prep's order)
+                for (int x = tid; x < kAttTile * dd4p; x += kThreads) {
+                    const int r = x / dd4p, o = x - r * dd4p;
+                    double v = 0.0;
+                    if (o < dd && r < nrow0) {
+                        const int chr = choice[rb0 + r];
+                        for (int d = 0; d < D; d++) {
+                            double dz = -S.al[kPrepP + r * D + d];
+                            if (d == chr) dz += 1.0;
+                            v = fma(dvt[d * dd + o], dz, v);
+                        }
+                        row_du_out[(size_t)(rb0 + r) * dd + o] = v;
+                    }
+                    S.du[r * kDuLd + o] = v;
+                }
+                __syncthreads();
+                // w = uc . du (8 lanes per row, two passes of 32 rows)
+                for (int pass = 0; pass < 2; pass++) {
+                    const int r = pass * 32 + (tid >> 3), jb = tid & 7;
+                    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                    for (int x = 0; x < kMaxDD / 8; x += 2) {
+                        const int o0 = jb + 8 * x, o1 = o0 + 8;
+                        if (o0 < dd) s0 = fma(S.al[r * dd + o0], S.du[r * kDuLd + o0], s0);
+                        if (o1 < dd) s1 = fma(S.al[r * dd + o1], S.du[r * kDuLd + o1], s1);
+                    }
+                    double sw = s0 + s1;
+                    sw += __shfl_xor_sync(0xffffffffu, sw, 1);
+                    sw += __shfl_xor_sync(0xffffffffu, sw, 2);
+                    sw += __shfl_xor_sync(0xffffffffu, sw, 4);
+                    if (jb == 0) S.w[r] = r < nrow0 ? sw : 0.0;
+                }
+                // dh_out = W_out[:64] du as the dh_ext accumulator's start (DMMA, k = dd4p)
+                for (int ks = 0; ks < dd4p / 4; ks++) {
+                    const double a = S.du[mr * kDuLd + ks * 4 + t];
+#pragma unroll
+                    for (int n = 0; n < 8; n++) dmma884(dq[n], a, wT[(ks * 4 + t) * kPadH + n * 8 + g]);
+                }
+                __syncthreads();  // S.w / S.du complete; the scratch in S.al / S.ds is free again
+            }
             DP_APHASE(0);
             const double *enc = S.enc[b];
             // DA (and S) for rows mr, columns i = n*8 + 2t + {0,1}
@@ -699,8 +774,12 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
 #pragma unroll
                 for (int n = 0; n < 8; n++) {
                     double2 *dst = reinterpret_cast<double2 *>(row_dhx + (size_t)(rb + mr) * kH + n * 8 + 2 * t);
-                    const double2 v = *dst;
-                    *dst = make_double2(v.x + dq[n][0], v.y + dq[n][1]);
+                    if (prep) {
+                        *dst = make_double2(dq[n][0], dq[n][1]);  // dh_out + ds proj, formed here
+                    } else {
+                        const double2 v = *dst;
+                        *dst = make_double2(v.x + dq[n][0], v.y + dq[n][1]);
+                    }
                 }
             first_cta_tile = false;
             DP_APHASE(7);
@@ -1672,8 +1751,14 @@ Grid att_grid(int K, int T) {
     return {ceil_div(n_tiles, per), per};
 }
 
+// Whether the rows pass's attention backward forms row_prep's per-row outputs itself
+// (GM DMMA kernel: act_e stored and per-tile partials allocated, not the tcgen05 variant).
+bool att_prep_merged(const dp_policy *p) {
+    return p->act_e && p->tile_part && !(dp_tensor_core_mode() == 6 && att_bwd_tc_ok(p->dims));
+}
+
 int launch_att(dp_policy *p, const double *params, const Grid &g, size_t smem, int rows, double *tile_part,
-               double *tile_partA, cudaStream_t st) {
+               double *tile_partA, cudaStream_t st, int prep = 0) {
     const PolicyDims &dm = p->dims;
     const int tps = (dm.T + kAttTile - 1) / kAttTile;
     const int per_sample = tile_part && g.per % tps == 0 ? 1 : 0;
@@ -1691,7 +1776,7 @@ int launch_att(dp_policy *p, const double *params, const Grid &g, size_t smem, i
         att_bwd_kernel<true, true><<<g.n_used, kThreads, smem, st>>>(
             dm, rows, g.per, p->proj, p->act_stat, p->act_h, p->encW, p->row_w, p->row_du, p->row_dq, p->partial,
             p->partA, tile_part, tile_partA, p->act_e, p->act_esc, 1, per_sample, params + p->dims.off.w_att,
-            p->row_dhx);
+            p->row_dhx, prep, params, p->act_p, p->act_choice, p->act_uc, p->row_du);
     } else if (p->act_e) {
         DP_CUDA_TRY(allow_big_smem((const void *)att_bwd_kernel<true>, smem));
         att_bwd_kernel<true><<<g.n_used, kThreads, smem, st>>>(dm, rows, g.per, p->enc_h, p->act_stat, p->row_q,
@@ -1929,11 +2014,13 @@ extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32
     const PolicyDims &dm = p->dims;
     cudaStream_t st = (cudaStream_t)stream;
     const int rows = K * dm.T;
-    DP_TRY(run_b0(p, params, rows, nullptr, nullptr, kRowsOnly, st));
+    // GM: the attention backward forms row_prep's per-row outputs per tile itself
+    const bool merged = att_prep_merged(p);
+    if (!merged) DP_TRY(run_b0(p, params, rows, nullptr, nullptr, kRowsOnly, st));
     {
         const Grid g = att_grid(K, dm.T);
         const size_t smem = sizeof(AttSmem);
-        DP_TRY(launch_att(p, params, g, smem, rows, p->tile_part, p->tile_partA, st));
+        DP_TRY(launch_att(p, params, g, smem, rows, p->tile_part, p->tile_partA, st, merged ? 1 : 0));
     }
     DP_CUDA_TRY(cudaEventRecord(p->ev_att, st));  // the grads pass's reductions may start here
     DP_TRY(run_b2(p, params, K, st));
