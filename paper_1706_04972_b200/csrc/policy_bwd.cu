@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1) att_bwd_kernel(
                 double *wT = S.ds;               // W_out[:64]^T [o][j], o < dd4p (S.ds is free here)
                 double *dvt = S.ds + kPrepDev;   // dev_table[:D] [d][o]
                 for (int x = tid; x < dd4p * kH; x += kThreads) {
-                    const int o = x >> 6, j = x & 63;
+                    const int j = x / dd4p, o = x - j * dd4p;  // o fastest: coalesced W_out rows
                     wT[o * kPadH + j] = o < dd ? __ldg(P + dm.off.w_out + (size_t)j * dd + o) : 0.0;
                 }
                 for (int x = tid; x < D * dd; x += kThreads) dvt[x] = __ldg(P + dm.off.dev_table + x);
