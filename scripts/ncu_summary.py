@@ -68,6 +68,9 @@ def main(tag, reps):
     os.makedirs("profiles", exist_ok=True)
     res = {}
     for rep in reps:
+        if not os.path.exists(rep):
+            print(f"skipping {rep}: no report (the kernel did not launch)")
+            continue
         name = os.path.basename(rep).replace("prof_", "").replace(".ncu-rep", "")
         d = raw(rep)
         d["stall_pct"] = stalls(rep)

@@ -8,7 +8,7 @@ TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT profiles
 reps=()
-for k in dec_kernel att_bwd_kernel lstm_bwd_kernel sim_warp_kernel row_prep_kernel enc_rec_kernel dec_wgrad_tc_kernel adv_grads_kernel; do
+for k in dec_kernel att_bwd_kernel lstm_bwd_kernel sim_warp_kernel enc_rec_kernel dec_wgrad_tc_kernel adv_grads_kernel; do
     timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $OUT/prof_$k \
         python bench.py --steps 1 --warmup 3 --skip-cpu > $OUT/ncu_$k.log 2>&1
     reps+=($OUT/prof_$k.ncu-rep)
