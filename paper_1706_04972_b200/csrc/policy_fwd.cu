@@ -1941,6 +1941,9 @@ const void *dec_fn(int MT, bool fast, bool tcg) {
     if constexpr (!PS && !SPEC) {
         if (MT == 8 && g_clocks_on) return (const void *)dec_kernel<8, PS, false, false, false, true>;
     }
+    if constexpr (PS && !SPEC) {
+        if (MT == 4 && g_clocks_on) return (const void *)dec_kernel<4, PS, false, false, false, true>;
+    }
     if (SPEC)
         return MT == 1 ? (const void *)dec_kernel<1, PS, SPEC>
                : MT == 2 ? (const void *)dec_kernel<2, PS, SPEC>
