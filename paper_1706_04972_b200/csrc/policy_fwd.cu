@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             unsigned long long n0 = a.draw_base + (unsigned long long)kg * (unsigned long long)T;
             if (a.draw_counter) n0 += (unsigned long long)(*a.draw_counter) * (unsigned long long)a.draws_per_count;
             u128 s = pcg_jump(u128{a.st_hi, a.st_lo}, u128{a.inc_hi, a.inc_lo}, n0);
-            if (3 * Mb <= kWarps) {  // pcgw: step 0's uniform up front
+            if (FAST || 3 * Mb <= kWarps) {  // pcgw: step 0's uniform up front
                 s = pcg_step(s, u128{a.inc_hi, a.inc_lo});
                 rnext[tid] = pcg_double(s);
             }
@@ -1754,7 +1754,7 @@ static int g_dec_variant = 0;  // dp_debug_decoder_variant
 static bool g_clocks_on = false;  // dp_debug_phase_clocks: launch the CLK instantiations
 extern "C" int dp_debug_decoder_variant(int32_t mode) {
     DP_ENTRY();
-    DP_REQUIRE(mode >= 0 && mode <= 4, "dp_debug_decoder_variant: mode must be 0..4");
+    DP_REQUIRE(mode >= 0 && mode <= 5, "dp_debug_decoder_variant: mode must be 0..5");
     g_dec_variant = mode;
     return DP_OK;
 }
@@ -1933,10 +1933,12 @@ const void *dec_fn(int MT, bool fast, bool tcg) {
                                : (MT == 1 ? (const void *)dec_kernel<1, PS, false, true, true>
                                           : (const void *)dec_kernel<2, PS, false, true, true>);
         if (fast)
-            return g_clocks_on ? (MT == 1 ? (const void *)dec_kernel<1, PS, false, true, false, true>
-                                          : (const void *)dec_kernel<2, PS, false, true, false, true>)
-                               : (MT == 1 ? (const void *)dec_kernel<1, PS, false, true>
-                                          : (const void *)dec_kernel<2, PS, false, true>);
+            return g_clocks_on ? (MT == 1   ? (const void *)dec_kernel<1, PS, false, true, false, true>
+                                  : MT == 2 ? (const void *)dec_kernel<2, PS, false, true, false, true>
+                                            : (const void *)dec_kernel<4, PS, false, true, false, true>)
+                               : (MT == 1   ? (const void *)dec_kernel<1, PS, false, true>
+                                  : MT == 2 ? (const void *)dec_kernel<2, PS, false, true>
+                                            : (const void *)dec_kernel<4, PS, false, true>);
     }
     if constexpr (!PS && !SPEC) {
         if (MT == 8 && g_clocks_on) return (const void *)dec_kernel<8, PS, false, false, false, true>;
@@ -2028,7 +2030,10 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     a.ewld = ((dm.T + 1) & ~1) + 2;
     const int grid = ceil_div(K, pl.M);
     cudaStream_t st = (cudaStream_t)stream;
-    const bool fast = pl.MT <= 2 && dm.D <= 4 && dm.dd <= 16 && dm.T <= kThreads;
+    // FAST: compact instantiation for <= 4 samples per CTA (debug mode 5: the generic kernel
+    // for 4 samples per CTA, A/B)
+    const bool fast = (pl.MT <= 2 || (pl.MT == 4 && g_dec_variant != 5)) && dm.D <= 4 && dm.dd <= 16 &&
+                      dm.T <= kThreads;
     const void *fn = pl.enc_in_smem
                          ? (pl.spec ? dec_fn<true, true>(pl.MT, false, false) : dec_fn<true, false>(pl.MT, fast, pl.tcg))
                          : (pl.spec ? dec_fn<false, true>(pl.MT, false, false) : dec_fn<false, false>(pl.MT, false, false));
