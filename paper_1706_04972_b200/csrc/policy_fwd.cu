@@ -398,19 +398,20 @@ __device__ __forceinline__ double warp_sum(double v) {
 // reference's searchsorted(cumsum(p), r), pkg/policy.py:320-323) against the
 // step's uniform r (still in rnext: the caller runs this before the pcg step
 // that overwrites it).
+template <int FS = 16, int EZO = 8>  // record stride and the ez offset (D <= 4: 16 / 8; D <= 8: 24 / 12)
 __device__ __forceinline__ void fin_store(const DecArgs &a, double *fin, const int *prev, const double *rnext,
                                           int k0, int m, int M, int T, int s) {
     if (k0 + m >= a.K) return;
     const int D = a.dm.D;
     const size_t row = (size_t)(k0 + m) * T + s;
     const int ch = prev[(((s & 1) ^ 1) * M) + m];
-    const double *f = fin + ((s & 1) * M + m) * 16;
+    const double *f = fin + ((s & 1) * M + m) * FS;
     const double esum = f[0];
     const double y = fm_rcp(esum);
     const double r = rnext[(s & 1) * M + m];
     double cdf = 0.0, mg = INFINITY;
     for (int d = 0; d < D; d++) {
-        const double p = fm_div_y(f[8 + d], esum, y);
+        const double p = fm_div_y(f[EZO + d], esum, y);
         a.act_p[row * D + d] = p;
         if (a.probs_out) a.probs_out[row * D + d] = p;
         cdf += p;
@@ -422,11 +423,15 @@ __device__ __forceinline__ void fin_store(const DecArgs &a, double *fin, const i
     a.act_lz[row * 2 + 1] = esum;
     a.act_stat[row * 2] = f[1];  // softmax stats (max, sum) for the backward's recompute of alpha
     a.act_stat[row * 2 + 1] = f[2];
-    if (!a.forced) fin[32 * M + m] = fmin(fin[32 * M + m], mg);
+    if (!a.forced) fin[2 * FS * M + m] = fmin(fin[2 * FS * M + m], mg);
 }
 
-template <int MT, bool PS, bool SPEC, bool FAST = false, bool TCG = false, bool CLK = false>
+template <int MT, bool PS, bool SPEC, bool FAST = false, bool TCG = false, bool CLK = false, int DX = 4>
 __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
+    static_assert(DX == 4 || (DX == 8 && FAST), "DX: the FAST path's device bound (4 or 8)");
+    // FAST draw layout: NP lanes per device in the logits, the step record stride FS and
+    // the ez offset EZO in it (D <= 4: 8 / 16 / 8; D <= 8: 4 / 24 / 12)
+    constexpr int NP = DX == 8 ? 4 : 8, FS = DX == 8 ? 24 : 16, EZO = 4 + DX;
     static_assert(!TCG || (FAST && PS && !SPEC && MT <= 2), "TCG is a FAST-path variant");
     extern __shared__ __align__(16) double sm[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -487,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
     // both parity halves, all M slots: the per-sample loops compute unguarded
     // (branch-free, so the samples' chains interleave) and only the stores check Mb
     if (tid < 2 * M) prev[tid] = SPEC ? 0 : D;  // SPEC: step 0's state lives in candidate slot 0
-    if (FAST && tid < M) fin[32 * M + tid] = INFINITY;  // running sampling margins
+    if (FAST && tid < M) fin[2 * FS * M + tid] = INFINITY;  // running sampling margins
     if (MT == 8 && !PS && !SPEC && (dd & 1) == 0)  // DM streaming ring (aliases alS): zero pads
         for (int i = tid; i < kWarps * kDmsSlots * kDmsSlot; i += kThreads) alS[i] = 0.0;
     if (tid < Mb) {
@@ -1017,7 +1022,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
 #pragma unroll
-        for (int m = 0; m < MT; m++) lsm[m] = ((skip & 8) || (FAST && MT == 2) || dms) ? lsm[m] : warp_sum(lsm[m]);
+        for (int m = 0; m < MT; m++)
+            lsm[m] = ((skip & 8) || (FAST && (MT == 2 || MT == 4)) || dms) ? lsm[m] : warp_sum(lsm[m]);
         __syncwarp();
         // uc_w[m][j] = sum over this warp's rows {32 warp + 256 r + l} of e_i encW[i][j]
         // (lane = (m, j); full 32-row blocks read e and encW^T as 16-byte pairs)
@@ -1095,6 +1101,47 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 lsm[1] = s1;
             }
             if (j < dd) puc[(warp * M + hh) * dd + j] = hh ? v1 : v0;
+        } else if (FAST && MT == 4) {
+            // lane (j, pair): all 32 of the warp's rows for samples 2 pair and 2 pair + 1, each
+            // encW^T pair loaded once for two samples; the same pass sums the e values (the
+            // warp's softmax partial sums, no butterflies)
+            const int j = lane & 15, pr = lane >> 4, jj = j < dd ? j : dd - 1;
+            const int i0 = warp * 32, n = (skip & 1) ? 0 : max(0, min(32, T - i0));
+            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+            const double *a0p = alS + (2 * pr) * a.Tpad + i0, *a1p = a0p + a.Tpad;
+            if (n == 32) {
+                const double2 *ap0 = reinterpret_cast<const double2 *>(a0p);
+                const double2 *ap1 = reinterpret_cast<const double2 *>(a1p);
+                const double2 *ep = reinterpret_cast<const double2 *>(encW + jj * a.ewld + i0);
+#pragma unroll
+                for (int q = 0; q < 16; q++) {
+                    const double2 e = ep[q], x = ap0[q], y = ap1[q];
+                    c0 = fma(x.x, e.x, c0);
+                    c1 = fma(x.y, e.y, c1);
+                    d0 = fma(y.x, e.x, d0);
+                    d1 = fma(y.y, e.y, d1);
+                    s0 += x.x + x.y;
+                    s1 += y.x + y.y;
+                }
+            } else {
+                for (int ii = 0; ii < n; ii++) {
+                    const double e = encW[jj * a.ewld + i0 + ii];
+                    c0 = fma(a0p[ii], e, c0);
+                    d0 = fma(a1p[ii], e, d0);
+                    s0 += a0p[ii];
+                    s1 += a1p[ii];
+                }
+            }
+            if (!(skip & 8)) {
+                lsm[0] = __shfl_sync(0xffffffffu, s0, 0);
+                lsm[1] = __shfl_sync(0xffffffffu, s1, 0);
+                lsm[2 % MT] = __shfl_sync(0xffffffffu, s0, 16);
+                lsm[3 % MT] = __shfl_sync(0xffffffffu, s1, 16);
+            }
+            if (j < dd) {
+                if (2 * pr < Mb) puc[(warp * M + 2 * pr) * dd + j] = c0 + c1;
+                if (2 * pr + 1 < Mb) puc[(warp * M + 2 * pr + 1) * dd + j] = d0 + d1;
+            }
         } else
         for (int pi = lane; pi < ((skip & 1) ? 0 : Mb * dd); pi += 32) {
             const int m = small_div<MT>(pi, dd), j = pi - m * dd;
@@ -1242,25 +1289,32 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             if (fastE) {
                 // lanes (d = lane / 8, part = lane % 8): h . vdev[:, d] (8 terms each)
                 // and dev_table[d] . sum_w uc_w (2 terms each), 3-level butterflies
-                const int dz = min(lane >> 3, D - 1), op = lane & 7;
+                // (D <= 8: lanes (d = lane / 4, part = lane % 4), 16 + 4 terms, 2 levels)
+                const int dz = min(lane / NP, D - 1), op = lane % NP;
                 const double *hv = SPEC ? hC + (m * D + prv[m]) * kH : hS + m * kH;
                 double v0 = 0.0, v1 = 0.0;
 #pragma unroll
-                for (int y = 0; y < 8; y += 2) {
-                    v0 = fma(hv[op + 8 * y], vS[(op + 8 * y) * D + dz], v0);
-                    v1 = fma(hv[op + 8 * y + 8], vS[(op + 8 * y + 8) * D + dz], v1);
+                for (int y = 0; y < kH / NP; y += 2) {
+                    v0 = fma(hv[op + NP * y], vS[(op + NP * y) * D + dz], v0);
+                    v1 = fma(hv[op + NP * y + NP], vS[(op + NP * y + NP) * D + dz], v1);
                 }
                 // 1 / gsum off the chain (the loads above are in flight); the context
                 // half joins the h half before one butterfly
                 const double rg = fm_div(1.0, gsum);
                 const double ucr = wsum8(puc + m * dd + lo, M * dd, fw);  // lane j < dd: sum_w fw[w] uc_w[j]
-                const double ua = __shfl_sync(0xffffffffu, ucr, op), ub = __shfl_sync(0xffffffffu, ucr, op + 8);
+                const double ua = __shfl_sync(0xffffffffu, ucr, op), ub = __shfl_sync(0xffffffffu, ucr, op + NP);
                 double c = op < dd ? devt[dz * dd + op] * ua : 0.0;
-                if (op + 8 < dd) c = fma(devt[dz * dd + op + 8], ub, c);
+                if (op + NP < dd) c = fma(devt[dz * dd + op + NP], ub, c);
+#pragma unroll
+                for (int q = 2; q < 16 / NP; q++) {
+                    const int j = op + NP * q;
+                    const double uq = __shfl_sync(0xffffffffu, ucr, j);
+                    if (j < dd) c = fma(devt[dz * dd + j], uq, c);
+                }
                 double v = fma(c, rg, v0 + v1);
 #pragma unroll
-                for (int o = 1; o < 8; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                zh = __shfl_sync(0xffffffffu, v, ld * 8);
+                for (int o = 1; o < NP; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                zh = __shfl_sync(0xffffffffu, v, ld * NP);
             } else if (D <= 4 && dd <= 16) {
                 // lanes (d = lane / 8, part = lane % 8): 2 terms each + a 3-level butterfly
                 const int dz = min(lane >> 3, D - 1), op = lane & 7;
@@ -1303,7 +1357,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             }
             double zmax = z;
 #pragma unroll
-            for (int o = FAST ? 2 : 16; o > 0; o >>= 1) {  // FAST: D <= 4, lanes >= D hold -inf
+            for (int o = FAST ? DX / 2 : 16; o > 0; o >>= 1) {  // FAST: D <= DX, lanes >= D hold -inf
                 const double oz = __shfl_xor_sync(0xffffffffu, zmax, o);
                 // FAST: compare-select (~12 cycles) in place of fmax (~25); z is finite
                 if (FAST) zmax = oz > zmax ? oz : zmax;
@@ -1321,11 +1375,11 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 // warp's, one step later (fin_store).  The decision agrees with the
                 // reference's whenever the margin recorded there exceeds
                 // SAMPLING_MARGIN_TOL (cumsum(p) and P / esum differ by a few ulp).
-                double P[4];
+                double P[DX];
                 P[0] = __shfl_sync(0xffffffffu, ez, 0);
 #pragma unroll
-                for (int dv = 1; dv < 4; dv++) P[dv] = P[dv - 1] + __shfl_sync(0xffffffffu, ez, dv);
-                const double esum = P[3];
+                for (int dv = 1; dv < DX; dv++) P[dv] = P[dv - 1] + __shfl_sync(0xffffffffu, ez, dv);
+                const double esum = P[DX - 1];
                 int ch;
                 if (a.forced) {
                     ch = a.forced[row];
@@ -1333,14 +1387,14 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     const double rs = r * esum;
                     int cnt = 0;
 #pragma unroll
-                    for (int dv = 0; dv < 3; dv++) cnt += (dv < D - 1 && P[dv] <= rs) ? 1 : 0;
+                    for (int dv = 0; dv < DX - 1; dv++) cnt += (dv < D - 1 && P[dv] <= rs) ? 1 : 0;
                     ch = cnt;
                 }
-                double *f = fin + (par * M + m) * 16;
+                double *f = fin + (par * M + m) * FS;
                 if (lane == 0) prev[(par ^ 1) * M + m] = ch;
                 if (lane < D) {
                     f[4 + lane] = zs;
-                    f[8 + lane] = ez;
+                    f[EZO + lane] = ez;
                 }
                 if (lane == 0) {
                     f[0] = esum;
@@ -1475,7 +1529,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         if (pcgw && warp >= kWarps - Mb && lane == 0) {
             const int m = warp - (kWarps - Mb);
             // the previous step's row (reads that step's uniform before it is overwritten)
-            if (FAST && t > 0) fin_store(a, fin, prev, rnext, k0, m, M, T, t - 1);
+            if (FAST && t > 0) fin_store<FS, EZO>(a, fin, prev, rnext, k0, m, M, T, t - 1);
             if (!a.forced) {
                 const u128 ns = pcg_step(u128{pcg[2 * m], pcg[2 * m + 1]}, u128{a.inc_hi, a.inc_lo});
                 pcg[2 * m] = ns.hi;
@@ -1523,8 +1577,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
 #pragma unroll
         for (int i = 0; i < 3; i++) g_warp_clk[warp * 3 + i] += wacc[i];
     if (FAST && tid < Mb && T > 0) {
-        fin_store(a, fin, prev, rnext, k0, tid, M, T, T - 1);  // the last step's row
-        if (a.margin && !a.forced) a.margin[k0 + tid] = fin[32 * M + tid];
+        fin_store<FS, EZO>(a, fin, prev, rnext, k0, tid, M, T, T - 1);  // the last step's row
+        if (a.margin && !a.forced) a.margin[k0 + tid] = fin[2 * FS * M + tid];
     }
     if (!FAST && a.margin && !a.forced && warp < Mb && lane == 0) a.margin[k0 + warp] = mrun;
     __syncthreads();  // the log-prob pass below reads those rows from other threads
@@ -1897,7 +1951,7 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
             a.o_pcg = take(2 * M);
             a.o_misc = take(16 + 2 * M);
             a.o_rn = take(2 * M);
-            a.o_fin = take(33 * M);  // FAST: [2][M][16] step records + [M] running sampling margins
+            a.o_fin = take(49 * M);  // FAST: [2][M][16 or 24] step records + [M] running sampling margins
             a.o_v = take(kH * D);
             a.o_wo = take(kH * dd);
             if (tcg) {
@@ -1925,8 +1979,15 @@ bool plan_decoder(const PolicyDims &dm, int K, int variant_mode, DecPlan &pl) {
 }
 
 template <bool PS, bool SPEC>
-const void *dec_fn(int MT, bool fast, bool tcg) {
+const void *dec_fn(int MT, bool fast, bool tcg, bool fast8 = false) {
     if constexpr (PS && !SPEC) {
+        if (fast8)  // FAST with 4 < D <= 8 devices
+            return g_clocks_on ? (MT == 1   ? (const void *)dec_kernel<1, PS, false, true, false, true, 8>
+                                  : MT == 2 ? (const void *)dec_kernel<2, PS, false, true, false, true, 8>
+                                            : (const void *)dec_kernel<4, PS, false, true, false, true, 8>)
+                               : (MT == 1   ? (const void *)dec_kernel<1, PS, false, true, false, false, 8>
+                                  : MT == 2 ? (const void *)dec_kernel<2, PS, false, true, false, false, 8>
+                                            : (const void *)dec_kernel<4, PS, false, true, false, false, 8>);
         if (fast && tcg)
             return g_clocks_on ? (MT == 1 ? (const void *)dec_kernel<1, PS, false, true, true, true>
                                           : (const void *)dec_kernel<2, PS, false, true, true, true>)
@@ -2034,8 +2095,12 @@ extern "C" int dp_policy_decode(dp_policy *p, const double *params, int32_t K, i
     // for 4 samples per CTA, A/B)
     const bool fast = (pl.MT <= 2 || (pl.MT == 4 && g_dec_variant != 5)) && dm.D <= 4 && dm.dd <= 16 &&
                       dm.T <= kThreads;
+    // ... and its instantiation for 4 < D <= 8 devices (C2's 4 GPUs + CPU)
+    const bool fast8 = pl.MT <= 4 && g_dec_variant != 5 && dm.D > 4 && dm.D <= 8 && dm.dd <= 16 &&
+                       dm.T <= kThreads && !pl.tcg;
     const void *fn = pl.enc_in_smem
-                         ? (pl.spec ? dec_fn<true, true>(pl.MT, false, false) : dec_fn<true, false>(pl.MT, fast, pl.tcg))
+                         ? (pl.spec ? dec_fn<true, true>(pl.MT, false, false)
+                                    : dec_fn<true, false>(pl.MT, fast, pl.tcg, fast8))
                          : (pl.spec ? dec_fn<false, true>(pl.MT, false, false) : dec_fn<false, false>(pl.MT, false, false));
     DP_CUDA_TRY(allow_big_smem(fn, pl.smem));
     void *args[] = {&a};
