@@ -14,7 +14,7 @@ import paper_1706_04972_b200 as dp  # noqa: E402
 from paper_1706_04972_b200 import _native as nat  # noqa: E402
 from paper_1706_04972_b200 import policy as P  # noqa: E402
 
-for name, K, variant in (("C1", 4, 0), ("C3", 3, 0), ("C3", 3, 4), ("C2", 600, 0)):
+for name, K, variant in (("C1", 4, 0), ("C3", 3, 0), ("C3", 3, 4), ("C2", 600, 0), ("C2", 8, 0), ("C2", 300, 0), ("C1", 300, 0)):
     gg, topo, _, _ = cfg(name)
     params = dp.trainer.policy_template(gg, topo, dp.TrainerConfig(seed=1))
     feats = P.GroupFeatures.from_grouped(gg, params.spec)
