@@ -252,3 +252,35 @@ def test_margin_accumulate_kernel():
         want_n += int(np.sum(m < 1e-7))
     torch.cuda.synchronize()
     assert float(mm.item()) == want_min and int(nb.item()) == want_n
+
+
+@pytest.mark.parametrize("ngpu,K,picks", [(5, 7, (0, 6)),            # D=6, 1 sample per CTA
+                                          (7, 200, (0, 1, 199)),     # D=8, 2 per CTA
+                                          (7, 297, (0, 3, 295, 296)),  # D=8, 4 per CTA, last CTA holds 1
+                                          (3, 297, (0, 296))])       # D=4, 4 per CTA, last CTA holds 1
+def test_fast_decoder_device_and_sample_bounds_vs_oracle(ngpu, K, picks):
+    """The FAST decoder instantiations at their bounds — up to 8 devices (4 logit
+    lanes per device, 24-double step records) and 4 samples per CTA including a
+    partial last CTA — against the oracle: placements bit-exact, log-probs and a
+    weighted gradient over the picked samples."""
+    from paper_1706_04972_b200 import _native as nat  # noqa: F401
+
+    gg, _, _, _ = cfg("C1")
+    topo = dp.simulator.default_topology(num_gpus=ngpu)
+    params = dp.trainer.policy_template(gg, topo, dp.TrainerConfig(seed=13))
+    feats = P.GroupFeatures.from_grouped(gg, params.spec)
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    T = len(feats)
+    pl, lp = P.sample_batch(params, feats, np.random.default_rng(31), K)
+    assert pl.max() < topo.num_devices
+    for k in picks:
+        rng = np.random.default_rng(31)
+        rng.bit_generator.advance(k * T)
+        opl, olp, _ = pol.sample(rng)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
+    w = np.zeros(K)
+    w[list(picks)] = np.linspace(0.5, -0.75, len(picks))
+    got = P.weighted_grad(params, feats, [list(map(int, p)) for p in pl], w).cpu().numpy()
+    assert _relnorm(got, _oracle_sum(pol, pl, w)) < GRAD_RTOL
