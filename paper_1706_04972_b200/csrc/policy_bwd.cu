@@ -1736,18 +1736,20 @@ Grid persist_grid(int rows, int tile) {
     return {ceil_div(n_tiles, per), per};
 }
 
-Grid att_grid(int K, int T) {
-    // one wave: att_bwd holds ~220 KB of shared memory (1 CTA per SM).  It
-    // leaves kSimSMs SMs free: in the split backward it runs concurrently with
-    // the placement simulator (small latency-bound CTAs that cannot co-reside
-    // with an att_bwd CTA).  When a CTA gets at least one whole sample, its
-    // tile range is rounded to whole samples (per-sample partials).
+Grid att_grid(int K, int T, bool split) {
+    // one wave: att_bwd holds ~220 KB of shared memory (1 CTA per SM).  The
+    // split backward's rows pass leaves kSimSMs SMs free (it runs concurrently
+    // with the placement simulator: small latency-bound CTAs that cannot
+    // co-reside with an att_bwd CTA) and, when a CTA gets at least one whole
+    // sample, rounds its tile range to whole samples (per-sample partials).
+    // The fused pass runs after scoring, takes every SM and accumulates per CTA.
     constexpr int kSimSMs = 20;
     const int tps = (T + kAttTile - 1) / kAttTile;
     const int n_tiles = K * tps;
-    const int n = n_tiles < kNumSMs - kSimSMs ? n_tiles : kNumSMs - kSimSMs;
+    const int n_sm = split ? kNumSMs - kSimSMs : kNumSMs;
+    const int n = n_tiles < n_sm ? n_tiles : n_sm;
     int per = ceil_div(n_tiles, n);
-    if (per >= tps) per = ceil_div(per, tps) * tps;
+    if (split && per >= tps) per = ceil_div(per, tps) * tps;
     return {ceil_div(n_tiles, per), per};
 }
 
@@ -1988,7 +1990,7 @@ extern "C" int dp_policy_backward(dp_policy *p, const double *params, int32_t K,
     p->rows_ready = 0;
     DP_TRY(run_b0(p, params, rows, adv, grad, kFused, st));
     {
-        const Grid g = att_grid(K, T);
+        const Grid g = att_grid(K, T, false);
         const size_t smem = sizeof(AttSmem);
         DP_TRY(launch_att(p, params, g, smem, rows, nullptr, nullptr, st));
         launch_reduce(p->partial, g.n_used, (size_t)T * kH, T * kH, p->d_enc, 0, st);
@@ -2018,7 +2020,7 @@ extern "C" int dp_policy_backward_rows(dp_policy *p, const double *params, int32
     const bool merged = att_prep_merged(p);
     if (!merged) DP_TRY(run_b0(p, params, rows, nullptr, nullptr, kRowsOnly, st));
     {
-        const Grid g = att_grid(K, dm.T);
+        const Grid g = att_grid(K, dm.T, true);
         const size_t smem = sizeof(AttSmem);
         DP_TRY(launch_att(p, params, g, smem, rows, p->tile_part, p->tile_partA, st, merged ? 1 : 0));
     }

@@ -15,10 +15,14 @@ for k in dec_kernel att_bwd_kernel lstm_bwd_kernel sim_warp_kernel enc_rec_kerne
 done
 python scripts/ncu_summary.py $TAG "${reps[@]}" > $OUT/ncu_summary.log 2>&1
 cp profiles/${TAG}_ncu_summary.json profiles/${TAG}_ncu_summary.md $OUT/
-# C5 decoder (DM streaming path) at its bench size, one launch
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:dec_kernel -c 1 -o $OUT/prof_c5_dec \
-    python bench.py --config C5 --steps 1 --warmup 3 --skip-cpu > $OUT/ncu_c5_dec.log 2>&1
-python scripts/ncu_summary.py ${TAG}_C5 $OUT/prof_c5_dec.ncu-rep > $OUT/ncu_summary_c5.log 2>&1
+# C5 decoder (DM streaming path) and score-recompute attention backward at their
+# bench size, one launch each (reports named by kernel: bench.py reads the decoder's traffic)
+mkdir -p $OUT/c5
+for k in dec_kernel att_bwd_kernel; do
+    timeout 900 ncu --set full --import-source on --clock-control none -k regex:$k -c 1 -o $OUT/c5/prof_$k \
+        python bench.py --config C5 --steps 1 --warmup 3 --skip-cpu > $OUT/ncu_c5_$k.log 2>&1
+done
+NCU_WORKLOAD="C5 K=4096" python scripts/ncu_summary.py ${TAG}_C5 $OUT/c5/prof_dec_kernel.ncu-rep $OUT/c5/prof_att_bwd_kernel.ncu-rep > $OUT/ncu_summary_c5.log 2>&1
 cp profiles/${TAG}_C5_ncu_summary.json profiles/${TAG}_C5_ncu_summary.md $OUT/ 2>/dev/null
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/${TAG}_launches_C3.csv \
     python bench.py --steps 2 --warmup 3 --skip-cpu > /dev/null 2>&1
@@ -38,5 +42,5 @@ timeout 900 python bench.py --mode sim --config C5 > $OUT/${TAG}_bench_sim_C5.js
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:dec_wgrad --csv \
     python scripts/wgrad_ab.py C3 256 0,1 > $OUT/${TAG}_wgrad_ab_ncu.csv 2>&1
 python scripts/sass_evidence.py > $OUT/${TAG}_sass_evidence.txt
-rm -f $OUT/prof_*.ncu-rep
+rm -f $OUT/prof_*.ncu-rep $OUT/c5/prof_*.ncu-rep
 echo done
