@@ -32,7 +32,7 @@ python scripts/dec_phases.py C5 4096 > $OUT/${TAG}_C5_decoder_phase_clocks.txt
 python scripts/lstm_phases.py C3 256 > $OUT/${TAG}_lstm_bwd_phase_clocks.txt
 python scripts/enc_phases.py C3 > $OUT/${TAG}_encoder_phase_clocks.txt
 timeout 900 python bench.py > $OUT/${TAG}_bench_C3_1gpu.json 2> $OUT/bench_C3.err
-bash scripts/launch_list.sh 60 "--config C5" > /dev/null 2>&1; python scripts/launch_summary.py $OUT/launches.csv seq > $OUT/${TAG}_launch_summary_C5.txt
+bash scripts/launch_list.sh 150 "--config C5" > /dev/null 2>&1; python scripts/launch_summary.py $OUT/launches.csv seq > $OUT/${TAG}_launch_summary_C5.txt
 timeout 900 python bench.py --config C4 > $OUT/${TAG}_bench_C4_1gpu.json 2> $OUT/bench_C4.err
 timeout 900 python bench.py --config C5 > $OUT/${TAG}_bench_C5_1gpu.json 2> $OUT/bench_C5.err
 timeout 900 python bench.py --impl reference > $OUT/${TAG}_bench_reference_C3.json 2> $OUT/bench_ref.err
