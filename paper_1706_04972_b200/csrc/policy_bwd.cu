@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(256) gsum_fin_kernel(PolicyDims dm, const doub
         gr[q][j] = i < T ? G[(size_t)i * kH + j] : 0.0;
         __syncthreads();
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-#pragma unroll 4  // fully unrolled, the hoisted shared loads spilled
+#pragma unroll
         for (int l = 0; l < kH; l += 4) {
             a0 = fma(gr[q][l], wa[l * kH + j], a0);
             a1 = fma(gr[q][l + 1], wa[(l + 1) * kH + j], a1);
