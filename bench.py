@@ -48,7 +48,9 @@ CFG_DESC = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: enough for a >= ~0.4 s timed region, so the 100 ms "
+                         "nvidia-smi clock sampler sees it; 20 for the reference arm and the long configs)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
@@ -63,7 +65,15 @@ def parse():
     ap.add_argument("--single-process", action="store_true",
                     help="one process drives --gpus N devices (MultiDeviceRunner, NCCL ncclCommInitAll); "
                          "with fewer visible GPUs the ranks share cuda:0")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:
+        if args.impl == "reference" or args.config == "C5":
+            args.steps = 20
+        elif args.mode == "sim":
+            args.steps = 60
+        else:
+            args.steps = 100 if args.config == "C4" else 200
+    return args
 
 
 def load_config(name):
@@ -86,7 +96,7 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.t_start, self.t_end = index, [], None, 0.0, None
 
     def __enter__(self):
         try:
@@ -95,15 +105,22 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a few hundred ms to start: wait for its first line
+            # (taken before the region, dropped) so the region is sampled throughout
+            t0 = time.monotonic()
+            while not self.rows and time.monotonic() - t0 < 3.0:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
+        self.t_start = time.monotonic()
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.monotonic(), [c.strip() for c in line.split(",")]))
 
     def __exit__(self, *exc):
+        self.t_end = time.monotonic()
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
@@ -113,18 +130,29 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        # only samples taken inside the timed region (a line is read a few ms after
+        # nvidia-smi takes it); if the region was shorter than the sampling period,
+        # the first sample after it, flagged
+        inside = [r for t, r in self.rows if t > self.t_start and (self.t_end is None or t <= self.t_end + 0.02)]
+        note = None
+        if not inside and self.rows:
+            after = [r for t, r in self.rows if t > self.t_start] or [self.rows[-1][1]]
+            inside, note = after[:1], "timed region shorter than the 100 ms sampling period: first sample after it"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in inside if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in inside if len(r) > 2 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in inside:
             for i, nm in enumerate(names):
                 if len(r) > 5 + i and r[5 + i].lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": sorted(reasons), "samples": len(inside)}
+        if note:
+            out["note"] = note
+        return out
 
 
 # ----------------------------------------------------------------------------- roofline terms
