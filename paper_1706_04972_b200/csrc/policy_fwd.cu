@@ -785,10 +785,14 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                 }
         }
         double lmx[MT], lsm[MT];
+        // FAST (one score row per thread): the row's scores stay in registers for
+        // the exponentials (no shared-memory round trip on the chain)
+        double sreg[MT];
 #pragma unroll
         for (int m = 0; m < MT; m++) {
             lmx[m] = -INFINITY;
             lsm[m] = 0.0;
+            sreg[m] = 0.0;
         }
         // DM (8 samples per CTA, proj too large for shared memory: C5-sized T):
         // the scores are fp64 tensor-core tiles, S[i][m] = proj[i] . h[m] with
@@ -943,7 +947,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
             for (int m = 0; m < MT; m++)
                 if (m < Mb && tid < T) {
                     const double sv = (s0[m] + s1[m]) + (s2[m] + s3[m]);
-                    alS[m * a.Tpad + tid] = sv;
+                    if (!FAST) alS[m * a.Tpad + tid] = sv;
+                    sreg[m] = sv;
                     lmx[m] = sv;
                 }
         } else {
@@ -979,7 +984,8 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
                     if (SPEC) gnS[m * kG + col] = gn[m];
                     if (tid < T) {
                         const double s = (s0[m] + s1[m]) + (s2[m] + s3[m]);
-                        alS[m * a.Tpad + tid] = s;
+                        if (!FAST) alS[m * a.Tpad + tid] = s;
+                        sreg[m] = s;
                         lmx[m] = s;
                     }
                 }
@@ -1012,7 +1018,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_kernel(DecArgs a) {
         for (int i = tid; i < ((skip & 16) || dms ? 0 : T); i += kThreads) {
             double ev[MT];
 #pragma unroll
-            for (int m = 0; m < MT; m++) ev[m] = fm_exp(alS[m * a.Tpad + i] - lmx[m]);
+            for (int m = 0; m < MT; m++) ev[m] = fm_exp((FAST ? sreg[m] : alS[m * a.Tpad + i]) - lmx[m]);
 #pragma unroll
             for (int m = 0; m < MT; m++)
                 if (m < Mb) {
