@@ -617,6 +617,8 @@ def main():
     # measurement A/B only: DP_DECODER_VARIANT=4 runs the opt-in tensor-core-gate decoder
     if os.environ.get("DP_DECODER_VARIANT"):
         nat.check(nat.lib().dp_debug_decoder_variant(int(os.environ["DP_DECODER_VARIANT"])), "variant")
+    if os.environ.get("DP_ENCODER_VARIANT"):
+        nat.check(nat.lib().dp_debug_encoder_variant(int(os.environ["DP_ENCODER_VARIANT"])), "variant")
 
     # C4 = the mixed batch: the C1 and C2 tasks (own parameters, stores, RNG
     # streams) advanced together, K=512 each

@@ -144,6 +144,12 @@ int dp_debug_fastmath_error(int64_t n, uint64_t *h_max_ulps);
  * W_h resident in TMEM; measured slower at C3, so opt-in). */
 int dp_debug_decoder_variant(int32_t mode);
 
+/* Encoder recurrence override (tests / measurement): 0 = one CTA (default),
+ * 1 = a 4-CTA cluster, each CTA a quarter of the gate columns, h exchanged
+ * every step through distributed shared memory (st.async completing an
+ * mbarrier transaction count; measured slower, so opt-in). */
+int dp_debug_encoder_variant(int32_t mode);
+
 /* Debug (tests): the decoder plan for a batch of K samples on this engine:
  * out[6] = {samples per CTA, kernel sample slots, tensor-core gates (0/1),
  * shared-memory bytes, speculative cell (0/1), operands in shared memory (0/1)}. */

@@ -36,6 +36,7 @@ SIGNATURES = {
     "dp_debug_phase_clocks": (I32, [I32, P]),
     "dp_debug_warp_clocks": (I32, [P]),
     "dp_debug_decoder_variant": (I32, [I32]),
+    "dp_debug_encoder_variant": (I32, [I32]),
     "dp_debug_decoder_plan": (I32, [P, I32, P]),
     "dp_margin_accumulate": (I32, [I32, P, ctypes.c_double, P, P, P]),
     "dp_debug_policy_drop_stores": (I32, [P, I32]),

@@ -246,6 +246,130 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 4; i++) g_phase_clk[4 + i] += ck[i];
 }
 
+// Encoder recurrence on a cluster of kEncCl CTAs (opt-in, dp_debug_encoder_variant(1);
+// measured slower: 2.2K vs 1.4K cycles per step).  CTA r owns units
+// [16 r, 16 r + 16), i.e. 64 of the 256 gate columns, so each SM issues a quarter
+// of the step's h W_h FMAs (the one-CTA kernel above is bound by the SM's fp64
+// pipe in that phase).  Thread lane = (u2, gate, kq): 4 lanes split a column's k
+// range (16 W_h values each in registers), two xor shuffles give every lane the
+// full pre-activation; the unit's 16 lanes gather i / f / o / g and update c
+// redundantly, and one lane per unit stores h_t into the step-parity h buffer of
+// every CTA of the cluster with st.async (DSMEM), which completes 8 bytes of that
+// CTA's buffer mbarrier transaction count (thread 0 of each CTA arms it with the
+// 64 values' bytes).  Every thread waits on its own CTA's barrier before the next
+// step's dot products: no CTA-wide barrier inside the loop.  Two buffers suffice:
+// a unit's h_t can only be formed after every warp of every CTA has finished the
+// step t-1 dot products that read the buffer h_t overwrites.
+constexpr int kEncCl = 4;
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_mapa(const void *p, uint32_t cta) {
+    uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__global__ void __cluster_dims__(kEncCl, 1, 1) __launch_bounds__(kThreads, 1)
+    enc_rec_cluster_kernel(PolicyDims dm, const double *__restrict__ params, const double *__restrict__ XP,
+                           double *__restrict__ enc_h, double *__restrict__ enc_c, double *__restrict__ enc_g) {
+    __shared__ __align__(16) double hbuf[2][kH];  // h of the previous step, by step parity
+    __shared__ __align__(8) unsigned long long hbar[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t rank = cl_rank();
+    const int u2 = lane >> 4, gate = (lane >> 2) & 3, kq = lane & 3;
+    const int u = (int)rank * 16 + warp * 2 + u2, col = gate * kH + u;
+    const double *Wh = params + dm.off.w_enc + (size_t)dm.F * kG;
+    double w[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) w[k] = Wh[(size_t)(16 * kq + k) * kG + col];
+    if (tid < kH) hbuf[0][tid] = 0.0;
+    // one local arrival per phase (thread 0's expect_tx of the 64 h values' bytes);
+    // the values themselves complete the transaction count (st.async)
+    const uint32_t hb0 = (uint32_t)__cvta_generic_to_shared(&hbar[0]);
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(hb0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(hb0 + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    double c = 0.0;
+    double xp = dm.T > 0 ? XP[col] : 0.0, xp2 = dm.T > 1 ? XP[kG + col] : 0.0;
+    const int base = lane & 16;
+    const bool writer = gate == 0 && kq == 0;
+    // cluster addresses of h[u] and of the barriers (buffer 0) in every CTA; buffer 1
+    // is at the same offset in each CTA's window
+    uint32_t rh[kEncCl], rb[kEncCl];
+#pragma unroll
+    for (int q = 0; q < kEncCl; q++) {
+        rh[q] = cl_mapa(&hbuf[0][u], q);
+        rb[q] = cl_mapa(&hbar[0], q);
+    }
+    constexpr uint32_t kHOff = kH * sizeof(double), kBOff = sizeof(unsigned long long);
+    cl_sync();  // barriers initialised and h_{-1} zeroed in every CTA before any remote access
+    for (int t = 0; t < dm.T; t++) {
+        const int b = t & 1;
+        if (t > 0) {
+            // h_{t-1} complete in this CTA (buffer b's phase (t-1)/2)
+            const uint32_t par = (uint32_t)((t - 1) >> 1) & 1u;
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "DP_ENC_WAIT_%=:\n"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                "@!p bra DP_ENC_WAIT_%=;\n"
+                "}\n" ::"r"(hb0 + 8u * (uint32_t)b),
+                "r"(par)
+                : "memory");
+        }
+        // arm the buffer h_t lands in (its previous phase, h_{t-2}, completed before
+        // this thread's wait at step t-1)
+        if (tid == 0 && t + 1 < dm.T)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(hb0 + 8u * (uint32_t)(b ^ 1)),
+                         "r"((uint32_t)(kH * sizeof(double)))
+                         : "memory");
+        const double2 *hq = reinterpret_cast<const double2 *>(hbuf[b] + 16 * kq);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            const double2 h0 = hq[k], h1 = hq[k + 1];
+            a0 = fma(h0.x, w[2 * k], a0);
+            a1 = fma(h0.y, w[2 * k + 1], a1);
+            a2 = fma(h1.x, w[2 * k + 2], a2);
+            a3 = fma(h1.y, w[2 * k + 3], a3);
+        }
+        double pre = (a0 + a1) + (a2 + a3);
+        pre += __shfl_xor_sync(0xffffffffu, pre, 1);
+        pre += __shfl_xor_sync(0xffffffffu, pre, 2);
+        const double act = fm_gate_act<true>(xp + pre, gate == 3);
+        xp = xp2;
+        if (t + 2 < dm.T) xp2 = XP[(size_t)(t + 2) * kG + col];
+        if (kq == 0) enc_g[(size_t)t * kG + col] = act;
+        const double iv = __shfl_sync(0xffffffffu, act, base + 0);
+        const double fv = __shfl_sync(0xffffffffu, act, base + 4);
+        const double ov = __shfl_sync(0xffffffffu, act, base + 8);
+        const double gv = __shfl_sync(0xffffffffu, act, base + 12);
+        c = fv * c + iv * gv;
+        if (writer) {
+            const double h = ov * fm_gate_act<true>(c, true);
+            const uint32_t nb = (uint32_t)(b ^ 1);
+            if (t + 1 < dm.T)
+#pragma unroll
+                for (int q = 0; q < kEncCl; q++)
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                                     rh[q] + nb * kHOff),
+                                 "d"(h), "r"(rb[q] + nb * kBOff)
+                                 : "memory");
+            enc_h[(size_t)t * kH + u] = h;
+            enc_c[(size_t)t * kH + u] = c;
+        }
+    }
+    cl_sync();  // no CTA leaves while a peer may still write into its shared memory
+}
+
 // ---------------------------------------------------------------- decoder
 // Per-snapshot decoder prologue, shared by all K samples (once per update):
 //   proj = enc_states @ W_att^T    [T x 64]  (policy.py:287 — the reference's own order)
@@ -1810,6 +1934,14 @@ extern "C" int64_t dp_policy_num_params(const dp_policy *p) { return p ? p->dims
 
 // Debug: enable (1) / disable (0) decoder phase clocks, then read and reset
 // the 8 per-phase cycle sums (block 0) into h_out[8].  Synchronous.
+static int g_enc_variant = 0;  // dp_debug_encoder_variant
+// Debug: encoder recurrence kernel (0 = one CTA, 1 = 4-CTA cluster with a DSMEM h exchange)
+extern "C" int dp_debug_encoder_variant(int32_t mode) {
+    DP_ENTRY();
+    DP_REQUIRE(mode == 0 || mode == 1, "dp_debug_encoder_variant: mode must be 0 or 1");
+    g_enc_variant = mode;
+    return DP_OK;
+}
 static int g_dec_variant = 0;  // dp_debug_decoder_variant
 static bool g_clocks_on = false;  // dp_debug_phase_clocks: launch the CLK instantiations
 extern "C" int dp_debug_decoder_variant(int32_t mode) {
@@ -1888,6 +2020,8 @@ extern "C" int dp_policy_encode(dp_policy *p, const double *params, void *stream
     DP_LAUNCH_CHECK();
     if (g_clocks_on)
         enc_rec_kernel<true><<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
+    else if (g_enc_variant == 1)
+        enc_rec_cluster_kernel<<<kEncCl, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
     else
         enc_rec_kernel<false><<<1, kThreads, 0, st>>>(dm, params, p->XP, p->enc_h, p->enc_c, p->enc_g);
     DP_LAUNCH_CHECK();

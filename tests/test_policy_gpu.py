@@ -201,6 +201,30 @@ def test_speculative_cell_decoder_vs_oracle(name, K):
         assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
 
 
+@pytest.mark.parametrize("name,K,n_check", [("C3", 16, 16), ("C1", 8, 8), ("C5", 4, 2)])
+def test_cluster_encoder_vs_oracle(name, K, n_check):
+    """The opt-in 4-CTA cluster encoder recurrence (dp_debug_encoder_variant(1):
+    DSMEM h exchange through st.async + mbarrier transaction counts) samples the
+    oracle's placements and matches its log-probs and gradient."""
+    from paper_1706_04972_b200 import _native as nat
+
+    gg, topo, params, feats = _setup(name, seed=23)  # a seed no other test encodes (engine cache)
+    nat.check(nat.lib().dp_debug_encoder_variant(1), "variant")
+    try:
+        pl, lp = P.sample_batch(params, feats, np.random.default_rng(17), K)
+        got = P.grad_log_prob(params, feats, [int(x) for x in pl[0]])
+    finally:
+        nat.check(nat.lib().dp_debug_encoder_variant(0), "variant")
+    dims = opol.Dims(params.spec.table_rows, topo.num_devices)
+    pol = opol.Policy(params.to_flat(), dims, opol.features(gg, opol.vocab_of(gg)))
+    rng = np.random.default_rng(17)
+    for k in range(n_check):
+        opl, olp, _ = pol.sample(rng)
+        assert np.array_equal(pl[k], opl), f"sample {k}"
+        assert lp[k] == pytest.approx(olp, rel=LP_RTOL)
+    assert _relnorm(got, pol.grad([int(x) for x in pl[0]])) < 1e-8
+
+
 @pytest.mark.parametrize("scale", [1.0, 400.0])
 def test_attention_softmax_shift_paths_vs_oracle(scale):
     """Large attention weights (8 max||proj_t|| > 600) take the max-shifted
