@@ -1,6 +1,7 @@
 """Blackwell instruction evidence in the built library, per kernel: tcgen05 MMA
 (UTC*MMA), TMEM loads (LDTM), TMA tensor loads (UTMALDG), TMA bulk copies
-(UBLKCP), mbarrier ops (SYNCS.*) and legacy fp64 tensor-core DMMA.
+(UBLKCP), mbarrier ops (SYNCS.*), distributed-shared-memory async stores (STAS) and
+cluster barriers (UCGABAR_*), and legacy fp64 tensor-core DMMA.
 usage: python scripts/sass_evidence.py [lib.so] > profiles/r02_sass_evidence.txt"""
 import collections
 import re
@@ -10,7 +11,7 @@ import sys
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_1706_04972_b200/_lib/libdevplace_b200.so"
 sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 pats = {"UTC*MMA": r"\bUTC[A-Z]*MMA\b", "LDTM": r"\bLDTM\b", "UTMALDG": r"\bUTMALDG\b", "UBLKCP": r"\bUBLKCP\b",
-        "SYNCS": r"\bSYNCS\.", "DMMA": r"\bDMMA\b"}
+        "SYNCS": r"\bSYNCS\.", "STAS": r"\bSTAS\b", "UCGABAR": r"\bUCGABAR_", "DMMA": r"\bDMMA\b"}
 counts = collections.defaultdict(collections.Counter)
 fn = None
 for line in sass.splitlines():
